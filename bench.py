@@ -1,0 +1,413 @@
+#!/usr/bin/env python3
+"""Benchmark: decode attention over the 2-bit rotated KV cache (BASELINE
+config 2, LLaMA-2-13B-shaped layer: 16 sequences x 40 heads x 128, 4096
+cached tokens, G=4) on N B200s, one process per GPU, batch-sharded with no
+collective on the data path (weak scaling: every rank holds 16 sequences).
+
+One step = quantize-append of 1 token for each of the rank's 16 sequences
+(rkv_quantize_kv, written at position 4096) + decode attention over the 4097
+cached tokens (rkv_decode_attention).  The cache (189.5 MB of packed K/V per
+step) is larger than the 126 MB L2, so no L2 flush is needed between steps.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0.  --impl reference times the reference's own
+CPU decode_step (oracle/_ref, compiled from /root/reference) on the host
+cores instead, on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decode-attn tokens/s and achieved HBM GB/s vs roofline (2-bit KV), 1/2/4/8 B200"
+CFG_ID = 2
+SEED = 44  # 42 + config index
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    a = ap.parse_args()
+    a.warmup = max(a.warmup, 3)
+    return a
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+def peak_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def decode_bytes(w, batch, tokens, sinks_per_seq):
+    """Algorithmic HBM bytes of one decode launch: per packed
+    token 2*(C/4 + 4*C/128), per sink token 2*C*2, plus q (fp16) and out (fp32)."""
+    c = w.channels
+    packed = (tokens - sinks_per_seq) * 2 * (c // 4 + 4 * c // 128)
+    sink = sinks_per_seq * 2 * c * 2
+    return batch * (packed + sink) + batch * w.num_q_heads * w.head_dim * (2 + 4)
+
+
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons during the timed region."""
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml as N
+
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            pass
+
+    def _names(self, mask):
+        N = self.N
+        table = {
+            "gpu_idle": getattr(N, "nvmlClocksEventReasonGpuIdle", 0x1),
+            "applications_clocks": getattr(N, "nvmlClocksEventReasonApplicationsClocksSetting", 0x2),
+            "sw_power_cap": getattr(N, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_slowdown": getattr(N, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "sync_boost": getattr(N, "nvmlClocksEventReasonSyncBoost", 0x10),
+            "sw_thermal_slowdown": getattr(N, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "hw_thermal_slowdown": getattr(N, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "hw_power_brake": getattr(N, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        return {k for k, v in table.items() if mask & v}
+
+    def _run(self):
+        N = self.N
+        while not self._stop.is_set():
+            try:
+                self.samples.append(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM))
+                try:
+                    m = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except Exception:
+                    m = N.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                self.reasons |= self._names(m)
+            except Exception:
+                break
+            time.sleep(0.001)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons - {"gpu_idle"}), "samples": len(self.samples)}
+
+
+def cpu_reference_decode(w, perm, nseq, nthreads, steps, warmup):
+    """The reference's own decode_step (oracle/_ref) on host threads; falls back
+    to the oracle port when the reference library was not built.  Returns
+    (seconds per step list, kind, sample description)."""
+    import numpy as np
+
+    import oracle
+
+    if oracle.have_ref():
+        R = oracle.ref()
+        perm32 = np.ascontiguousarray(perm, dtype=np.int32)
+        h = R.ref_bench_create(w.num_kv_heads, w.head_dim, w.heads_per_group, w.tokens, nseq,
+                               perm32.ctypes.data, w.rope_base, SEED, nthreads)
+        if not h:
+            raise RuntimeError("ref_bench_create failed")
+        try:
+            for _ in range(warmup):
+                R.ref_bench_step(h, nthreads)
+            times = [R.ref_bench_step(h, nthreads) for _ in range(steps)]
+        finally:
+            R.ref_bench_destroy(h)
+        sample = (f"{nseq} sequences x 1 decode step per step (T={w.tokens}, C={w.channels}, G={w.heads_per_group}) "
+                  f"through the reference's decode_step (incl. its identity projections), {nthreads} threads, "
+                  f"one sequence per thread")
+        return times, "reference", sample
+    # oracle port: one sequence per step, single thread
+    import numpy as np
+
+    rng = np.random.default_rng(SEED)
+    T, c = w.tokens, w.channels
+    k = rng.standard_normal((T, c)).astype(np.float16)
+    v = rng.standard_normal((T, c)).astype(np.float16)
+    kc, km, vc, vm = oracle.quantize_kv_rows(k, v, w.num_kv_heads, w.head_dim, w.heads_per_group, perm)
+    q = rng.standard_normal(w.num_q_heads * w.head_dim).astype(np.float16)
+    s = np.zeros(T, np.uint8)
+    s[0] = 1
+    times = []
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        oracle.decode_attention(kc, km, vc, vm, s, k, v, q, w.num_q_heads, w.num_kv_heads, w.head_dim,
+                                w.heads_per_group, perm, w.rope_base)
+        if i >= warmup:
+            times.append(time.perf_counter() - t0)
+    return times, "port", f"1 sequence x 1 decode step per step (T={T}, C={c}), oracle port, 1 thread"
+
+
+def run_reference(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    from paper_2501_16383_b200 import workload as WL
+
+    w = WL.CONFIGS[CFG_ID]
+    import numpy as np
+
+    perm = np.random.default_rng(SEED).permutation(w.channels).astype(np.int32)
+    nthreads = os.cpu_count() or 1
+    nseq = min(w.batch, nthreads)
+    times, kind, sample = cpu_reference_decode(w, perm, nseq, nthreads, args.steps, args.warmup)
+    total = sum(times)
+    value = nseq * len(times) / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": config_dict(w, world),
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": nthreads, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(w, world):
+    return {
+        "workload": w.name,
+        "batch_per_gpu": w.batch,
+        "global_batch": w.batch * world,
+        "cached_tokens": w.tokens,
+        "q_heads": w.num_q_heads,
+        "kv_heads": w.num_kv_heads,
+        "head_dim": w.head_dim,
+        "heads_per_group": w.heads_per_group,
+        "bits": 2,
+        "quant_group": 128,
+        "scale": "fp16 ceil",
+        "sinks": "token 0 (massive-activation detection)",
+        "step": "quantize-append 1 token x batch + decode attention over tokens+1",
+        "l2": "no flush: per-step cache bytes (189.5 MB) exceed the 126 MB L2",
+        "parallelism": f"batch-sharded x{world}, no collective on the data path",
+    }
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import paper_2501_16383_b200 as P
+    from paper_2501_16383_b200 import workload as WL
+
+    rank, local, world = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    w = WL.CONFIGS[CFG_ID]
+    B, T, Hq, D = w.batch, w.tokens, w.num_q_heads, w.head_dim
+    seed = SEED + 1000 * rank
+    perm = WL.calibration_perm(w, SEED, device=dev)  # one calibrated plan for every rank
+    cfg = P.LayerConfig(batch=B, num_q_heads=Hq, num_kv_heads=w.num_kv_heads, heads_per_group=w.heads_per_group,
+                        max_tokens=T + 1, max_sinks=4, rope_base=w.rope_base)
+    layer = P.RotateKVLayer(cfg, perm, device=dev)
+    sink_flags_row = P.detect_massive_activations(WL.hidden_with_sinks(w, seed, T))
+    nsinks = int(sink_flags_row.sum())
+    flags_all = torch.from_numpy(np.tile(sink_flags_row, (B, 1)))
+    chunk = 512
+    for t0 in range(0, T, chunk):
+        k, v = WL.make_kv(w, seed + t0, B, chunk, device=dev)
+        layer.append(k, v, flags_all[:, t0:t0 + chunk])
+        del k, v
+    torch.cuda.synchronize()
+
+    # step inputs (device resident): a few distinct token/query sets, cycled
+    nsets = 4
+    kn, vn = zip(*[WL.make_kv(w, seed + 9000 + i, B, 1, device=dev) for i in range(nsets)])
+    qs = [WL.make_q(w, seed, B, device=dev, step=i) for i in range(nsets)]
+    start_t = torch.full((B,), T, dtype=torch.int64, device=dev)
+    len_t = torch.full((B,), T + 1, dtype=torch.int64, device=dev)
+    out = torch.empty(B, Hq, D, dtype=torch.float32, device=dev)
+    ws, ws_bytes = layer.workspace(T + 1)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(i):
+        layer.append_device(kn[i % nsets], vn[i % nsets], start_t)
+        layer.decode_device(qs[i % nsets], len_t, T + 1, out, ws, ws_bytes)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+
+    # ---- timed region: device-resident inputs
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        start.record(stream)
+        for i in range(args.steps):
+            layer.append_device(kn[i % nsets], vn[i % nsets], start_t)
+            ev[i][0].record(stream)
+            layer.decode_device(qs[i % nsets], len_t, T + 1, out, ws, ws_bytes)
+            ev[i][1].record(stream)
+        end.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    elapsed_ms = start.elapsed_time(end)
+    decode_ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([elapsed_ms, decode_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms, decode_ms = t.tolist()
+    ms_per_step = elapsed_ms / args.steps
+    value = world * B * args.steps / (elapsed_ms / 1e3)
+
+    # ---- e2e: the same step through the C ABI with HOST buffers (pinned),
+    # H2D of the step's new K/V rows and queries, D2H of the outputs, inside
+    # the timed region
+    hk = [x.cpu().pin_memory() for x in kn]
+    hv = [x.cpu().pin_memory() for x in vn]
+    hq = [x.cpu().pin_memory() for x in qs]
+    hout = torch.empty(B, Hq, D, dtype=torch.float32).pin_memory()
+    dk = torch.empty_like(kn[0])
+    dv = torch.empty_like(vn[0])
+    dq = torch.empty_like(qs[0])
+
+    def e2e_step(i):
+        dk.copy_(hk[i % nsets], non_blocking=True)
+        dv.copy_(hv[i % nsets], non_blocking=True)
+        dq.copy_(hq[i % nsets], non_blocking=True)
+        layer.append_device(dk, dv, start_t)
+        layer.decode_device(dq, len_t, T + 1, out, ws, ws_bytes)
+        hout.copy_(out, non_blocking=True)
+
+    for i in range(args.warmup):
+        e2e_step(i)
+    torch.cuda.synchronize()
+    barrier()
+    s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s2.record(stream)
+    for i in range(args.steps):
+        e2e_step(i)
+    e2.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = s2.elapsed_time(e2)
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = t.item()
+    e2e_value = world * B * args.steps / (e2e_ms / 1e3)
+    h2d = (kn[0].numel() + vn[0].numel() + qs[0].numel()) * 2
+    d2h = out.numel() * 4
+
+    # ---- roofline of the dominant kernel (decode attention)
+    peak, peak_kind = peak_hbm()
+    dbytes = decode_bytes(w, B, T + 1, nsinks)
+    achieved = dbytes / (decode_ms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "decode_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    if rank != 0:
+        return
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            nthreads = os.cpu_count() or 1
+            nseq = min(B, nthreads)
+            times, kind, sample = cpu_reference_decode(w, perm, nseq, nthreads, steps=1, warmup=0)
+            cpu = {"value": nseq * len(times) / sum(times), "unit": "tokens/s", "cores": nthreads if kind == "reference" else 1,
+                   "kind": kind, "sample": sample}
+        except Exception as e:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": "tokens/s", "cores": 0, "kind": "unavailable", "sample": str(e)[:200]}
+
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "tokens/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_per_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic",
+        "config": config_dict(w, world),
+        "decode_ms": decode_ms,
+        "decode_hbm_gbs": achieved,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_kind": peak_kind, "kernel": "rkv_decode_attention",
+                     "bytes_per_launch": dbytes},
+        "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": 5 * args.steps,
+        "clocks": clocks.summary(),
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,161 @@
+/*
+ * rotatekv.h -- C ABI of the B200-native RotateKV KV-cache hot path.
+ *
+ * A drop-in for the reference's C++ hot-path API (namespace rotatekv in
+ * /root/reference/proj/include/rotatekv/*.hpp).  Each entry point names the
+ * reference interface it replaces.  Conventions:
+ *   - plain pointers and sizes only; fp16 tensors are passed as uint16_t bits;
+ *     `stream` is a cudaStream_t passed as void* (NULL = legacy default stream);
+ *   - device pointers unless stated otherwise; the ABI never allocates in
+ *     hot calls and is stream-ordered and re-entrant;
+ *   - errors: the reference throws std::invalid_argument / std::out_of_range /
+ *     std::runtime_error; here the same conditions return
+ *     RKV_ERR_INVALID_ARGUMENT / RKV_ERR_OUT_OF_RANGE / RKV_ERR_RUNTIME, and
+ *     rkv_last_error() holds the thread-local message.
+ *
+ * Layout of one layer's cache (all device memory, caller-owned, see
+ * rkv_cache_bytes / rkv_cache_carve), C = num_kv_heads * head_dim, W = C/16:
+ *   k_codes, v_codes  [B][max_tokens][W]        u32: 16 two-bit codes, code i of
+ *                     the (reordered, rotated) row at bits 2*(i%16) of word
+ *                     i/16 -- byte-identical to the reference's LSB-first
+ *                     pack_codes (proj/src/quant.cpp:25-35)
+ *   k_meta, v_meta    [B][max_tokens][C/128]    u32: fp16 scale | fp16 zero<<16
+ *   sink_k, sink_v    [B][max_sinks][C]         fp16 raw (pre-rotation) rows
+ *   sink_pos          [B][max_sinks]            i32 token position of each sink
+ *   sink_count        [B]                       i32
+ *   sink_mask         [B][ceil(max_tokens/32)]  u32 bit t%32 of word t/32 = sink
+ */
+#ifndef ROTATEKV_B200_H
+#define ROTATEKV_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    RKV_OK = 0,
+    RKV_ERR_INVALID_ARGUMENT = 1, /* reference: std::invalid_argument */
+    RKV_ERR_OUT_OF_RANGE = 2,     /* reference: std::out_of_range */
+    RKV_ERR_RUNTIME = 3,          /* reference: std::runtime_error */
+    RKV_ERR_CUDA = 4              /* CUDA launch / runtime failure */
+} rkv_status;
+
+typedef enum {
+    RKV_SCALE_FP16_CEIL = 0, /* north star: fp16 scale, rounded up */
+    RKV_SCALE_E4M3_CEIL = 1  /* reference storage (proj/src/quant.cpp:82): e4m3 ceil */
+} rkv_scale_format;
+
+typedef enum {
+    RKV_STAT_SUM = 0,     /* reference: signed channel sum (proj/src/reorder.cpp:98-100) */
+    RKV_STAT_MEAN_ABS = 1 /* north star: mean |K| */
+} rkv_calib_stat;
+
+/* One attention layer (replaces PipelineConfig + QuantConfig + RotationPlan,
+ * proj/include/rotatekv/pipeline.hpp:50-64, quant.hpp:11-18, hadamard.hpp:8-16). */
+typedef struct {
+    int32_t batch;           /* sequences held by this cache (this rank's shard) */
+    int32_t num_q_heads;     /* Hq */
+    int32_t num_kv_heads;    /* Hkv; Hq % Hkv == 0 (GQA extension) */
+    int32_t head_dim;        /* d: 128 */
+    int32_t heads_per_group; /* G: K FWHT spans G KV heads (n = G*d, power of 2) */
+    int32_t group_size;      /* quantization group: 128 */
+    int32_t bits;            /* 2 */
+    int32_t scale_format;    /* rkv_scale_format */
+    int64_t max_tokens;      /* cache capacity per sequence */
+    int32_t max_sinks;       /* sidecar capacity per sequence */
+    int32_t reserved;        /* must be 0 */
+    double rope_base;        /* RoPE theta (RopeConfig::base, rope.hpp:12) */
+} rkv_layer_desc;
+
+typedef struct {
+    uint32_t* k_codes;
+    uint32_t* v_codes;
+    uint32_t* k_meta;
+    uint32_t* v_meta;
+    uint16_t* sink_k;
+    uint16_t* sink_v;
+    int32_t* sink_pos;
+    int32_t* sink_count;
+    uint32_t* sink_mask;
+} rkv_cache;
+
+/* Thread-local message of the last failing call on this thread. */
+const char* rkv_last_error(void);
+const char* rkv_version(void);
+
+/* RotationPlan::make + QuantConfig::validate checks
+ * (proj/src/hadamard.cpp:18-33, proj/src/quant.cpp:15-23) plus the
+ * sm_100a kernels' shape limits.  Host only. */
+rkv_status rkv_layer_validate(const rkv_layer_desc* desc);
+
+/* Bytes of one layer's cache; carve a caller-allocated, 256-byte aligned
+ * device buffer into the arrays above.  Host only. */
+size_t rkv_cache_bytes(const rkv_layer_desc* desc);
+rkv_status rkv_cache_carve(const rkv_layer_desc* desc, void* base, size_t bytes, rkv_cache* out);
+
+/* Empty every sequence of the cache (LayerKVCache construction,
+ * proj/include/rotatekv/kv_cache.hpp:17): sink counts and masks to zero. */
+rkv_status rkv_cache_reset(const rkv_layer_desc* desc, const rkv_cache* cache, void* stream);
+
+/* RoPE cos/sin table [max_pos][head_dim/2] float2 (cos, sin of pos*theta_i,
+ * theta_i = base^(-2i/d) evaluated in double like proj/src/rope.cpp:17-24).
+ * Read by rkv_decode_attention; build once per (rope_base, max_pos). */
+size_t rkv_rope_table_bytes(const rkv_layer_desc* desc, int64_t max_pos);
+rkv_status rkv_rope_table_init(const rkv_layer_desc* desc, float* table, int64_t max_pos, void* stream);
+
+/* Fused quantize-append (replaces rotate_rows -> apply_reorder ->
+ * quantize_token -> LayerKVCache::append, proj/src/hadamard.cpp:75-84,
+ * proj/src/reorder.cpp:112-128, proj/src/quant.cpp:109-119,
+ * proj/src/kv_cache.cpp:8-22, as composed at proj/src/pipeline.cpp:171-176).
+ *   k_new, v_new : [B][num_new][C] fp16, pre-RoPE, unrotated
+ *   perm         : [C] int32, slot j <- channel perm[j] (ReorderPlan::perm[layer])
+ *   sink_flags   : [B][num_new] u8 (1 = keep the token in the fp16 sidecar), or NULL
+ *   start_pos    : [B] int64, cache index of each sequence's first new token
+ * Tokens are written at start_pos[b] .. start_pos[b]+num_new-1.  The device
+ * cannot throw: callers (the C++ layer) validate capacities first. */
+rkv_status rkv_quantize_kv(const rkv_layer_desc* desc, const uint16_t* k_new, const uint16_t* v_new,
+                           const int32_t* perm, const uint8_t* sink_flags, const int64_t* start_pos,
+                           int64_t num_new, const rkv_cache* cache, void* stream);
+
+/* Split-K decode attention over the 2-bit cache (replaces the attention half
+ * of decode_step: reconstruct_cache + prepare_queries + the per-head loop,
+ * proj/src/pipeline.cpp:133-152,211-261).
+ *   q        : [B][Hq][d] fp16, pre-RoPE; query position = seq_len[b]-1
+ *              (decode_step appends the token before attending, pipeline.cpp:197-211)
+ *   seq_len  : [B] int64 device, tokens 0..seq_len[b]-1 are attended (>= 1)
+ *   max_seq_len : host upper bound of seq_len (0 = desc->max_tokens)
+ *   perm     : [C] int32 layer permutation (the same array rkv_quantize_kv took);
+ *              un-reordering scatters slot j back to channel perm[j]
+ *   rope_table : from rkv_rope_table_init with max_pos >= max_seq_len
+ *   out      : [B][Hq][d] fp32, V's rotation undone (what W_o_f absorbs, pipeline.cpp:97)
+ *   workspace: >= rkv_decode_workspace_bytes(desc, max_seq_len) bytes of device memory */
+size_t rkv_decode_workspace_bytes(const rkv_layer_desc* desc, int64_t max_seq_len);
+rkv_status rkv_decode_attention(const rkv_layer_desc* desc, const uint16_t* q, const int64_t* seq_len,
+                                int64_t max_seq_len, const rkv_cache* cache, const int32_t* perm,
+                                const float* rope_table, float* out, void* workspace, size_t ws_bytes,
+                                void* stream);
+
+/* Grouped-head FWHT of raw fp16 K rows into fp32 (rotate_rows,
+ * proj/src/hadamard.cpp:75-84) -- the device half of calibration. */
+rkv_status rkv_rotate_keys(const rkv_layer_desc* desc, const uint16_t* k, int64_t rows, float* out,
+                           void* stream);
+
+/* calibrate_reorder (proj/src/reorder.cpp:91-110) on HOST memory:
+ * rotated_keys [rows][channels] fp32 -> perm/inverse [channels] int32. */
+rkv_status rkv_calibrate_reorder(const float* rotated_keys, int64_t rows, int64_t channels, int32_t stat,
+                                 int32_t* perm_out, int32_t* inverse_out);
+
+/* Massive-activation sink detection (proj/src/sink.cpp:14-45) on HOST memory:
+ * hidden [b][s][h] fp32 -> flags[s] (token 0 always flagged).  Returns the
+ * count through *num_sinks. */
+rkv_status rkv_detect_sinks(const float* hidden, int64_t b, int64_t s, int64_t h, double rel_threshold,
+                            double abs_floor, uint8_t* flags, int64_t* num_sinks);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ROTATEKV_B200_H */

@@ -1,0 +1,19 @@
+"""B200-native RotateKV KV-cache hot path (arxiv 2501.16383).
+
+The product is the sm_100a C-ABI library built from csrc/ into
+_lib/librotatekv_b200.so (include/rotatekv/rotatekv.h); rotatekv.py is the
+Python host layer mirroring the reference's C++ API.
+"""
+from .rotatekv import (  # noqa: F401
+    SCALE_E4M3_CEIL,
+    SCALE_FP16_CEIL,
+    STAT_MEAN_ABS,
+    STAT_SUM,
+    LayerConfig,
+    RotateKVLayer,
+    apply_reorder,
+    calibrate_reorder,
+    detect_massive_activations,
+    lib,
+    rotate_keys,
+)

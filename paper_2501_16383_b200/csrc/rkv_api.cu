@@ -1,0 +1,312 @@
+// rkv_api.cu -- the extern "C" boundary (include/rotatekv/rotatekv.h).
+//
+// Validation mirrors the reference's exceptions: RotationPlan::make
+// (proj/src/hadamard.cpp:18-33), QuantConfig::validate (proj/src/quant.cpp:
+// 15-23), rope check_cfg (proj/src/rope.cpp:8-12), calibrate_reorder
+// (proj/src/reorder.cpp:91-93), detect_massive_activations
+// (proj/src/sink.cpp:16-24).  Messages keep the reference's wording where
+// one exists.  Host-only entry points (validate, carve, calibrate, detect)
+// run without a GPU.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "rkv_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+rkv_status fail(rkv_status s, const std::string& msg) {
+    g_err = msg;
+    return s;
+}
+
+rkv_status cuda_fail(cudaError_t e, const char* where) {
+    return fail(RKV_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+bool is_pow2(int64_t n) { return n > 0 && (n & (n - 1)) == 0; }
+
+size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct CacheSizes {
+    size_t codes, meta, sink, sink_pos, sink_count, mask;
+};
+
+CacheSizes cache_sizes(const rkv_layer_desc& d) {
+    const size_t C = static_cast<size_t>(d.num_kv_heads) * d.head_dim;
+    const size_t B = static_cast<size_t>(d.batch), T = static_cast<size_t>(d.max_tokens);
+    CacheSizes s{};
+    s.codes = al256(B * T * (C / 16) * 4);
+    s.meta = al256(B * T * (C / 128) * 4);
+    s.sink = al256(B * static_cast<size_t>(d.max_sinks) * C * 2);
+    s.sink_pos = al256(B * static_cast<size_t>(d.max_sinks) * 4);
+    s.sink_count = al256(B * 4);
+    s.mask = al256(B * ((T + 31) / 32) * 4);
+    return s;
+}
+
+rkv_status validate(const rkv_layer_desc* d) {
+    if (!d) return fail(RKV_ERR_INVALID_ARGUMENT, "layer descriptor is null");
+    if (d->batch < 1 || d->num_q_heads < 1 || d->num_kv_heads < 1 || d->head_dim < 1 || d->heads_per_group < 1)
+        return fail(RKV_ERR_INVALID_ARGUMENT, "rotation plan dimensions must be positive");
+    if (d->num_kv_heads % d->heads_per_group != 0)
+        return fail(RKV_ERR_INVALID_ARGUMENT, "heads_per_group must divide num_heads");
+    const int64_t n = static_cast<int64_t>(d->heads_per_group) * d->head_dim;
+    if (!is_pow2(n)) return fail(RKV_ERR_INVALID_ARGUMENT, "rotation matrix dimension must be a power of two");
+    if (n > (int64_t{1} << 13)) return fail(RKV_ERR_INVALID_ARGUMENT, "rotation matrix dimension exceeds 2^13");
+    if (d->bits < 1 || d->bits > 8) return fail(RKV_ERR_INVALID_ARGUMENT, "quant bits must be in [1,8]");
+    if (d->group_size < 1) return fail(RKV_ERR_INVALID_ARGUMENT, "quant group_size must be >= 1");
+    if (!(d->rope_base > 1.0)) return fail(RKV_ERR_INVALID_ARGUMENT, "rope: base must be > 1");
+    if (d->head_dim % 2 != 0) return fail(RKV_ERR_INVALID_ARGUMENT, "rope: head_dim must be even and >= 2");
+    if (d->num_q_heads % d->num_kv_heads != 0)
+        return fail(RKV_ERR_INVALID_ARGUMENT, "num_q_heads must be a multiple of num_kv_heads");
+    if (d->max_tokens < 1 || d->max_tokens > (int64_t{1} << 30))
+        return fail(RKV_ERR_INVALID_ARGUMENT, "max_tokens must be in [1, 2^30]");
+    if (d->max_sinks < 0) return fail(RKV_ERR_INVALID_ARGUMENT, "max_sinks must be >= 0");
+    if (d->scale_format != RKV_SCALE_FP16_CEIL && d->scale_format != RKV_SCALE_E4M3_CEIL)
+        return fail(RKV_ERR_INVALID_ARGUMENT, "unknown scale_format");
+    if (d->reserved != 0) return fail(RKV_ERR_INVALID_ARGUMENT, "reserved field must be 0");
+    // sm_100a kernel specialisation limits (documented in DESIGN.md)
+    if (d->head_dim != 128) return fail(RKV_ERR_INVALID_ARGUMENT, "the sm_100a kernels need head_dim == 128");
+    if (d->bits != 2 || d->group_size != 128)
+        return fail(RKV_ERR_INVALID_ARGUMENT, "the sm_100a kernels implement bits == 2, group_size == 128");
+    if (n != 128 && n != 256 && n != 512)
+        return fail(RKV_ERR_INVALID_ARGUMENT, "the sm_100a kernels need heads_per_group*head_dim in {128,256,512}");
+    const int rep = d->num_q_heads / d->num_kv_heads;
+    if (rep != 1 && rep != 2 && rep != 4 && rep != 8)
+        return fail(RKV_ERR_INVALID_ARGUMENT, "q heads per kv head must be 1, 2, 4 or 8");
+    const int64_t C = static_cast<int64_t>(d->num_kv_heads) * d->head_dim;
+    if (C % 512 != 0) return fail(RKV_ERR_INVALID_ARGUMENT, "num_kv_heads*head_dim must be a multiple of 512");
+    if (C > 32768) return fail(RKV_ERR_INVALID_ARGUMENT, "num_kv_heads*head_dim must be <= 32768");
+    return RKV_OK;
+}
+
+rkv_status check_cache(const rkv_cache* c) {
+    if (!c || !c->k_codes || !c->v_codes || !c->k_meta || !c->v_meta || !c->sink_count || !c->sink_mask)
+        return fail(RKV_ERR_INVALID_ARGUMENT, "cache arrays must be non-null");
+    return RKV_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rkv_last_error(void) { return g_err.c_str(); }
+
+const char* rkv_version(void) { return "rotatekv-b200 0.1 (sm_100a)"; }
+
+rkv_status rkv_layer_validate(const rkv_layer_desc* desc) { return validate(desc); }
+
+size_t rkv_cache_bytes(const rkv_layer_desc* desc) {
+    if (validate(desc) != RKV_OK) return 0;
+    CacheSizes s = cache_sizes(*desc);
+    return 2 * s.codes + 2 * s.meta + 2 * s.sink + s.sink_pos + s.sink_count + s.mask;
+}
+
+rkv_status rkv_cache_carve(const rkv_layer_desc* desc, void* base, size_t bytes, rkv_cache* out) {
+    rkv_status st = validate(desc);
+    if (st != RKV_OK) return st;
+    if (!base || !out) return fail(RKV_ERR_INVALID_ARGUMENT, "cache_carve: null pointer");
+    if (reinterpret_cast<uintptr_t>(base) % 256 != 0)
+        return fail(RKV_ERR_INVALID_ARGUMENT, "cache_carve: base must be 256-byte aligned");
+    if (bytes < rkv_cache_bytes(desc)) return fail(RKV_ERR_INVALID_ARGUMENT, "cache_carve: buffer too small");
+    CacheSizes s = cache_sizes(*desc);
+    char* p = static_cast<char*>(base);
+    out->k_codes = reinterpret_cast<uint32_t*>(p), p += s.codes;
+    out->v_codes = reinterpret_cast<uint32_t*>(p), p += s.codes;
+    out->k_meta = reinterpret_cast<uint32_t*>(p), p += s.meta;
+    out->v_meta = reinterpret_cast<uint32_t*>(p), p += s.meta;
+    out->sink_k = reinterpret_cast<uint16_t*>(p), p += s.sink;
+    out->sink_v = reinterpret_cast<uint16_t*>(p), p += s.sink;
+    out->sink_pos = reinterpret_cast<int32_t*>(p), p += s.sink_pos;
+    out->sink_count = reinterpret_cast<int32_t*>(p), p += s.sink_count;
+    out->sink_mask = reinterpret_cast<uint32_t*>(p);
+    return RKV_OK;
+}
+
+rkv_status rkv_cache_reset(const rkv_layer_desc* desc, const rkv_cache* cache, void* stream) {
+    rkv_status st = validate(desc);
+    if (st != RKV_OK) return st;
+    if ((st = check_cache(cache)) != RKV_OK) return st;
+    CacheSizes s = cache_sizes(*desc);
+    cudaStream_t cs = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMemsetAsync(cache->sink_count, 0, static_cast<size_t>(desc->batch) * 4, cs);
+    if (e == cudaSuccess) e = cudaMemsetAsync(cache->sink_mask, 0, s.mask, cs);
+    if (e == cudaSuccess && cache->sink_pos) e = cudaMemsetAsync(cache->sink_pos, 0, s.sink_pos, cs);
+    if (e != cudaSuccess) return cuda_fail(e, "cache_reset");
+    return RKV_OK;
+}
+
+size_t rkv_rope_table_bytes(const rkv_layer_desc* desc, int64_t max_pos) {
+    if (validate(desc) != RKV_OK || max_pos < 1) return 0;
+    return static_cast<size_t>(max_pos) * (desc->head_dim / 2) * 2 * sizeof(float);
+}
+
+rkv_status rkv_rope_table_init(const rkv_layer_desc* desc, float* table, int64_t max_pos, void* stream) {
+    rkv_status st = validate(desc);
+    if (st != RKV_OK) return st;
+    if (!table || max_pos < 1) return fail(RKV_ERR_INVALID_ARGUMENT, "rope_table_init: null table or max_pos < 1");
+    cudaError_t e = rkv::launch_rope_table(*desc, reinterpret_cast<float2*>(table), max_pos,
+                                           static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "rope_table_init");
+    return RKV_OK;
+}
+
+rkv_status rkv_quantize_kv(const rkv_layer_desc* desc, const uint16_t* k_new, const uint16_t* v_new,
+                           const int32_t* perm, const uint8_t* sink_flags, const int64_t* start_pos,
+                           int64_t num_new, const rkv_cache* cache, void* stream) {
+    rkv_status st = validate(desc);
+    if (st != RKV_OK) return st;
+    if ((st = check_cache(cache)) != RKV_OK) return st;
+    if (num_new < 0) return fail(RKV_ERR_INVALID_ARGUMENT, "quantize_kv: num_new must be >= 0");
+    if (num_new == 0) return RKV_OK;
+    if (!k_new || !v_new || !perm || !start_pos)
+        return fail(RKV_ERR_INVALID_ARGUMENT, "quantize_kv: k_new, v_new, perm and start_pos must be non-null");
+    if (num_new > desc->max_tokens) return fail(RKV_ERR_OUT_OF_RANGE, "quantize_kv: num_new exceeds max_tokens");
+    if (sink_flags && (!cache->sink_k || !cache->sink_v || !cache->sink_pos))
+        return fail(RKV_ERR_INVALID_ARGUMENT, "quantize_kv: sink flags need the sidecar arrays");
+    rkv::QuantParams p{};
+    p.k_new = k_new;
+    p.v_new = v_new;
+    p.perm = perm;
+    p.sink_flags = sink_flags;
+    p.start_pos = start_pos;
+    p.num_new = num_new;
+    p.max_tokens = desc->max_tokens;
+    p.C = desc->num_kv_heads * desc->head_dim;
+    p.max_sinks = desc->max_sinks;
+    p.scale_format = desc->scale_format;
+    p.k_norm = 1.0f / std::sqrt(static_cast<float>(desc->heads_per_group * desc->head_dim));
+    p.v_norm = 1.0f / std::sqrt(static_cast<float>(desc->head_dim));
+    p.cache = *cache;
+    cudaError_t e = rkv::launch_quantize(*desc, p, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "quantize_kv");
+    return RKV_OK;
+}
+
+size_t rkv_decode_workspace_bytes(const rkv_layer_desc* desc, int64_t max_seq_len) {
+    if (validate(desc) != RKV_OK) return 0;
+    rkv::DecodePlan pl = rkv::plan_decode(*desc, max_seq_len);
+    const size_t rows = static_cast<size_t>(desc->batch) * (pl.S + 1) * desc->num_q_heads;
+    return al256(rows * 2 * sizeof(float)) + al256(rows * 128 * sizeof(float));
+}
+
+rkv_status rkv_decode_attention(const rkv_layer_desc* desc, const uint16_t* q, const int64_t* seq_len,
+                                int64_t max_seq_len, const rkv_cache* cache, const int32_t* perm,
+                                const float* rope_table, float* out, void* workspace, size_t ws_bytes,
+                                void* stream) {
+    rkv_status st = validate(desc);
+    if (st != RKV_OK) return st;
+    if ((st = check_cache(cache)) != RKV_OK) return st;
+    if (!q || !seq_len || !perm || !rope_table || !out || !workspace)
+        return fail(RKV_ERR_INVALID_ARGUMENT, "decode_attention: null argument");
+    if (max_seq_len < 0 || max_seq_len > desc->max_tokens)
+        return fail(RKV_ERR_OUT_OF_RANGE, "decode_attention: max_seq_len exceeds max_tokens");
+    if (max_seq_len == 0) max_seq_len = desc->max_tokens;
+    if (ws_bytes < rkv_decode_workspace_bytes(desc, max_seq_len))
+        return fail(RKV_ERR_INVALID_ARGUMENT, "decode_attention: workspace too small");
+    rkv::DecodePlan pl = rkv::plan_decode(*desc, max_seq_len);
+    if (pl.NT > 320 || pl.smem > 227 * 1024)
+        return fail(RKV_ERR_INVALID_ARGUMENT, "decode_attention: layer shape exceeds the sm_100a kernel's tile budget");
+    const size_t rows = static_cast<size_t>(desc->batch) * (pl.S + 1) * desc->num_q_heads;
+    rkv::DecodeParams p{};
+    p.q = q;
+    p.seq_len = seq_len;
+    p.perm = perm;
+    p.rope = reinterpret_cast<const float2*>(rope_table);
+    p.cache = *cache;
+    p.ws_ml = static_cast<float*>(workspace);
+    p.ws_o = reinterpret_cast<float*>(static_cast<char*>(workspace) + al256(rows * 2 * sizeof(float)));
+    p.out = out;
+    p.max_tokens = desc->max_tokens;
+    p.B = desc->batch;
+    p.Hq = desc->num_q_heads;
+    p.Hkv = desc->num_kv_heads;
+    p.C = desc->num_kv_heads * desc->head_dim;
+    p.S = pl.S;
+    p.chunk = pl.chunk;
+    p.P = pl.P;
+    p.k_norm = 1.0f / std::sqrt(static_cast<float>(desc->heads_per_group * desc->head_dim));
+    p.qscale = rkv::kLog2eHost / std::sqrt(static_cast<float>(desc->head_dim));
+    cudaError_t e = rkv::launch_decode(*desc, pl, p, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "decode_attention");
+    return RKV_OK;
+}
+
+rkv_status rkv_rotate_keys(const rkv_layer_desc* desc, const uint16_t* k, int64_t rows, float* out, void* stream) {
+    rkv_status st = validate(desc);
+    if (st != RKV_OK) return st;
+    if (!k || !out || rows < 0) return fail(RKV_ERR_INVALID_ARGUMENT, "rotate_keys: null argument");
+    if (rows == 0) return RKV_OK;
+    cudaError_t e = rkv::launch_rotate_keys(*desc, k, rows, out, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "rotate_keys");
+    return RKV_OK;
+}
+
+rkv_status rkv_calibrate_reorder(const float* rotated_keys, int64_t rows, int64_t channels, int32_t stat,
+                                 int32_t* perm_out, int32_t* inverse_out) {
+    if (!rotated_keys || !perm_out) return fail(RKV_ERR_INVALID_ARGUMENT, "calibrate_reorder: null argument");
+    if (rows < 1) return fail(RKV_ERR_INVALID_ARGUMENT, "calibrate_reorder: empty calibration set");
+    if (channels < 1) return fail(RKV_ERR_INVALID_ARGUMENT, "calibrate_reorder: channels must be >= 1");
+    if (stat != RKV_STAT_SUM && stat != RKV_STAT_MEAN_ABS)
+        return fail(RKV_ERR_INVALID_ARGUMENT, "calibrate_reorder: unknown statistic");
+    // per-channel statistic accumulated sequentially over rows in double
+    std::vector<double> key(static_cast<size_t>(channels), 0.0);
+    for (int64_t i = 0; i < rows; ++i) {
+        const float* r = rotated_keys + i * channels;
+        for (int64_t j = 0; j < channels; ++j) {
+            const double v = r[j];
+            key[static_cast<size_t>(j)] += stat == RKV_STAT_MEAN_ABS ? std::fabs(v) : v;
+        }
+    }
+    if (stat == RKV_STAT_MEAN_ABS)
+        for (double& k : key) k /= static_cast<double>(rows);
+    std::vector<int32_t> order(static_cast<size_t>(channels));
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int32_t a, int32_t b) { return key[static_cast<size_t>(a)] < key[static_cast<size_t>(b)]; });
+    std::memcpy(perm_out, order.data(), order.size() * sizeof(int32_t));
+    if (inverse_out)
+        for (int64_t j = 0; j < channels; ++j) inverse_out[order[static_cast<size_t>(j)]] = static_cast<int32_t>(j);
+    return RKV_OK;
+}
+
+rkv_status rkv_detect_sinks(const float* hidden, int64_t b, int64_t s, int64_t h, double rel_threshold,
+                            double abs_floor, uint8_t* flags, int64_t* num_sinks) {
+    if (!hidden || !flags) return fail(RKV_ERR_INVALID_ARGUMENT, "detect_massive_activations: null argument");
+    if (b < 1 || h < 1) return fail(RKV_ERR_INVALID_ARGUMENT, "detect_massive_activations: expected [b,s,hidden]");
+    if (!(rel_threshold > 1.0))
+        return fail(RKV_ERR_INVALID_ARGUMENT, "detect_massive_activations: rel_threshold must be > 1");
+    if (s < 1) return fail(RKV_ERR_INVALID_ARGUMENT, "detect_massive_activations: empty sequence");
+    const int64_t n = b * s * h;
+    std::vector<float> mags(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) mags[static_cast<size_t>(i)] = std::fabs(hidden[i]);
+    // the element a full ascending sort would put at index n/2
+    std::nth_element(mags.begin(), mags.begin() + n / 2, mags.end());
+    const double threshold = rel_threshold * static_cast<double>(mags[static_cast<size_t>(n / 2)]);
+    int64_t count = 0;
+    for (int64_t t = 0; t < s; ++t) {
+        bool hit = t == 0;
+        for (int64_t bi = 0; bi < b && !hit; ++bi) {
+            const float* row = hidden + (bi * s + t) * h;
+            for (int64_t c = 0; c < h; ++c) {
+                const double v = std::fabs(row[c]);
+                if (v > threshold && v > abs_floor) {
+                    hit = true;
+                    break;
+                }
+            }
+        }
+        flags[t] = hit ? 1 : 0;
+        count += hit ? 1 : 0;
+    }
+    if (num_sinks) *num_sinks = count;
+    return RKV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,125 @@
+// rkv_common.cuh -- shared device helpers for the sm_100a RotateKV kernels.
+//
+// FWHT layouts.  An N-point Walsh-Hadamard vector (N = G*128) is owned by a
+// group of L lanes, R = N/L values per lane:
+//   layout A: lane l holds indices l*R + j      (register bits = low index bits)
+//   layout B: lane l holds indices l + L*j      (register bits = high index bits)
+// Stages on index bits 0..log2(R)-1 run in registers in layout A, one
+// transpose through shared memory, then stages on the remaining high bits run
+// in registers in layout B.  Stage order is bit 0 first, exactly the
+// reference's half = 1, 2, ..., N/2 order (proj/src/hadamard.cpp:51-60), so
+// results are bit-identical to fwht_inplace.  Every register holds a float2:
+// the SAME index of two tokens, so every butterfly is one FADD2.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rkv {
+
+constexpr int kHeadDim = 128;
+constexpr int kQuantGroup = 128;
+constexpr float kLog2e = 1.4426950408889634f;
+
+__host__ __device__ constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x >> 1); }
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ float h2f(uint16_t h) { return __half2float(__ushort_as_half(h)); }
+
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+    return __fadd2_rn(a, make_float2(-b.x, -b.y));
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+
+// ------------------------------------------------------------ FWHT stages
+// Butterflies between registers j and j+H (H a power of two), packed.
+template <int R, int H>
+__device__ __forceinline__ void bfly(float2 (&x)[R]) {
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+        if ((j & H) == 0) {
+            float2 a = x[j], b = x[j + H];
+            x[j] = add2(a, b);
+            x[j + H] = sub2(a, b);
+        }
+    }
+}
+
+// Stages on register bits [lo, hi) in increasing order.
+template <int R, int LO, int HI>
+__device__ __forceinline__ void bfly_range(float2 (&x)[R]) {
+    if constexpr (LO < HI) {
+        bfly<R, (1 << LO)>(x);
+        bfly_range<R, LO + 1, HI>(x);
+    }
+}
+
+// ------------------------------------------------------ TMA bulk + mbarrier
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "RKV_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra RKV_WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// 1-D TMA bulk copy global -> shared (SASS: UBLKCP), completes on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ uint4 lds128(const void* p) {
+    return *reinterpret_cast<const uint4*>(p);
+}
+
+// ----------------------------------------------------- scale / code helpers
+// Smallest fp16 >= x (x > 0), saturating at 65504 (mirrors
+// e4m3_encode_ceil's saturation, proj/src/fp8.cpp:68-75).
+__device__ __forceinline__ uint16_t fp16_ceil(float x) {
+    if (!(x < 65504.0f)) return 0x7bffu;
+    __half h = __float2half_rn(x);
+    uint16_t b = __half_as_ushort(h);
+    if (__half2float(h) < x) b = static_cast<uint16_t>(b + 1u);
+    return b;
+}
+
+// Smallest OCP e4m3fn value >= x (x >= 0), == e4m3_decode(e4m3_encode_ceil(x))
+// (proj/src/fp8.cpp:68-75): RNE-then-bump equals "first table entry >= x".
+__device__ __forceinline__ float e4m3_ceil_value(float x) {
+    if (x >= 448.0f) return 448.0f;
+    // walk the monotone positive table: codes 0..0x7e
+    int lo = 0, hi = 0x7e;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        int e = (mid >> 3) & 0xf, m = mid & 7;
+        float v = e == 0 ? ldexpf(static_cast<float>(m), -9) : ldexpf(1.0f + m * 0.125f, e - 7);
+        if (v >= x) hi = mid; else lo = mid + 1;
+    }
+    int e = (lo >> 3) & 0xf, m = lo & 7;
+    return e == 0 ? ldexpf(static_cast<float>(m), -9) : ldexpf(1.0f + m * 0.125f, e - 7);
+}
+
+}  // namespace rkv

@@ -1,0 +1,63 @@
+// rkv_internal.h -- launch-side declarations shared by the .cu files.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "rotatekv/rotatekv.h"
+
+namespace rkv {
+
+constexpr float kLog2eHost = 1.4426950408889634f;
+
+struct QuantParams {
+    const uint16_t* k_new;
+    const uint16_t* v_new;
+    const int32_t* perm;
+    const uint8_t* sink_flags;
+    const int64_t* start_pos;
+    int64_t num_new;
+    int64_t max_tokens;
+    int C;
+    int max_sinks;
+    int scale_format;
+    float k_norm;  // 1.0f / sqrtf(float(G*d))   (proj/src/hadamard.cpp:62)
+    float v_norm;  // 1.0f / sqrtf(float(d))
+    rkv_cache cache;
+};
+
+struct DecodeParams {
+    const uint16_t* q;
+    const int64_t* seq_len;
+    const int32_t* perm;
+    const float2* rope;  // [max_pos][64]
+    rkv_cache cache;
+    float* ws_ml;  // [B][S+1][Hq][2]
+    float* ws_o;   // [B][S+1][Hq][128]
+    float* out;    // [B][Hq][128]
+    int64_t max_tokens;
+    int B, Hq, Hkv, C;
+    int S;      // packed splits (the sink partial is split index S)
+    int chunk;  // tokens per split, multiple of the tile
+    int P;      // token pairs per tile
+    float k_norm;
+    float qscale;  // log2(e) / sqrt(d)
+};
+
+// quantize_kv.cu
+cudaError_t launch_quantize(const rkv_layer_desc& d, const QuantParams& p, cudaStream_t s);
+// decode_attention.cu
+struct DecodePlan {
+    int N, REP, P, TT, NT, S, chunk;
+    size_t smem;
+};
+DecodePlan plan_decode(const rkv_layer_desc& d, int64_t max_seq_len);
+cudaError_t launch_decode(const rkv_layer_desc& d, const DecodePlan& plan, const DecodeParams& p,
+                          cudaStream_t s);
+cudaError_t launch_rope_table(const rkv_layer_desc& d, float2* table, int64_t max_pos, cudaStream_t s);
+cudaError_t launch_rotate_keys(const rkv_layer_desc& d, const uint16_t* k, int64_t rows, float* out,
+                               cudaStream_t s);
+int num_sms();
+
+}  // namespace rkv

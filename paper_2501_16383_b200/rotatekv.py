@@ -1,0 +1,350 @@
+"""Python host layer over the C ABI (include/rotatekv/rotatekv.h).
+
+Mirrors the reference's hot-path API (namespace rotatekv,
+/root/reference/proj/include/rotatekv/*.hpp) with the same names, argument
+meaning and error classes:
+
+    reference (C++)                           here
+    ----------------------------------------  -------------------------------------------
+    calibrate_reorder(rotated keys)           calibrate_reorder(rows, stat)
+    apply_reorder(x, plan, layer, inverse)    apply_reorder(x, perm, inverse)
+    rotate_rows(x, plan, inverse)             rotate_keys(layer, k)          (device FWHT)
+    detect_massive_activations(block, rel)    detect_massive_activations(hidden, rel, floor)
+    LayerKVCache(cfg, C) + append(k, v, sink) RotateKVLayer(...).append(k, v, sink_flags)
+    decode_step attention half                RotateKVLayer.decode(q)  /  .decode_step(k, v, q)
+
+std::invalid_argument -> ValueError, std::out_of_range -> IndexError,
+std::runtime_error -> RuntimeError.  Device tensors are torch CUDA tensors;
+torch is only the allocator/stream provider.  There is no CPU fallback: if
+the sm_100a library is missing the import of the device path fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "_lib", "librotatekv_b200.so")
+
+RKV_OK, RKV_ERR_INVALID_ARGUMENT, RKV_ERR_OUT_OF_RANGE, RKV_ERR_RUNTIME, RKV_ERR_CUDA = range(5)
+SCALE_FP16_CEIL, SCALE_E4M3_CEIL = 0, 1
+STAT_SUM, STAT_MEAN_ABS = 0, 1
+
+
+class LayerDesc(C.Structure):
+    _fields_ = [
+        ("batch", C.c_int32),
+        ("num_q_heads", C.c_int32),
+        ("num_kv_heads", C.c_int32),
+        ("head_dim", C.c_int32),
+        ("heads_per_group", C.c_int32),
+        ("group_size", C.c_int32),
+        ("bits", C.c_int32),
+        ("scale_format", C.c_int32),
+        ("max_tokens", C.c_int64),
+        ("max_sinks", C.c_int32),
+        ("reserved", C.c_int32),
+        ("rope_base", C.c_double),
+    ]
+
+
+class CacheView(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in (
+        "k_codes", "v_codes", "k_meta", "v_meta", "sink_k", "sink_v", "sink_pos", "sink_count", "sink_mask")]
+
+
+_lib = None
+
+
+def lib():
+    """Load the sm_100a C-ABI library; raises if it was never built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2501_16383_b200.build` "
+                              "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        P = C.c_void_p
+        D = C.POINTER(LayerDesc)
+        L.rkv_last_error.restype = C.c_char_p
+        L.rkv_version.restype = C.c_char_p
+        L.rkv_layer_validate.argtypes = [D]
+        L.rkv_cache_bytes.restype = C.c_size_t
+        L.rkv_cache_bytes.argtypes = [D]
+        L.rkv_cache_carve.argtypes = [D, P, C.c_size_t, C.POINTER(CacheView)]
+        L.rkv_cache_reset.argtypes = [D, C.POINTER(CacheView), P]
+        L.rkv_rope_table_bytes.restype = C.c_size_t
+        L.rkv_rope_table_bytes.argtypes = [D, C.c_int64]
+        L.rkv_rope_table_init.argtypes = [D, P, C.c_int64, P]
+        L.rkv_quantize_kv.argtypes = [D, P, P, P, P, P, C.c_int64, C.POINTER(CacheView), P]
+        L.rkv_decode_workspace_bytes.restype = C.c_size_t
+        L.rkv_decode_workspace_bytes.argtypes = [D, C.c_int64]
+        L.rkv_decode_attention.argtypes = [D, P, P, C.c_int64, C.POINTER(CacheView), P, P, P, P, C.c_size_t, P]
+        L.rkv_rotate_keys.argtypes = [D, P, C.c_int64, P, P]
+        L.rkv_calibrate_reorder.argtypes = [P, C.c_int64, C.c_int64, C.c_int32, P, P]
+        L.rkv_detect_sinks.argtypes = [P, C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_double, P,
+                                       C.POINTER(C.c_int64)]
+        for name in ("rkv_layer_validate", "rkv_cache_carve", "rkv_cache_reset", "rkv_rope_table_init",
+                     "rkv_quantize_kv", "rkv_decode_attention", "rkv_rotate_keys", "rkv_calibrate_reorder",
+                     "rkv_detect_sinks"):
+            getattr(L, name).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _check(status: int) -> None:
+    if status == RKV_OK:
+        return
+    msg = lib().rkv_last_error().decode()
+    if status == RKV_ERR_INVALID_ARGUMENT:
+        raise ValueError(msg)
+    if status == RKV_ERR_OUT_OF_RANGE:
+        raise IndexError(msg)
+    raise RuntimeError(msg)
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else int(t.data_ptr())
+
+
+def _np(a, dtype):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+@dataclass
+class LayerConfig:
+    """One attention layer (PipelineConfig + QuantConfig + RotationPlan)."""
+    batch: int
+    num_q_heads: int
+    num_kv_heads: int
+    head_dim: int = 128
+    heads_per_group: int = 4
+    max_tokens: int = 4096
+    max_sinks: int = 8
+    rope_base: float = 10000.0
+    scale_format: int = SCALE_FP16_CEIL
+    group_size: int = 128
+    bits: int = 2
+
+    def desc(self) -> LayerDesc:
+        return LayerDesc(self.batch, self.num_q_heads, self.num_kv_heads, self.head_dim, self.heads_per_group,
+                         self.group_size, self.bits, self.scale_format, self.max_tokens, self.max_sinks, 0,
+                         float(self.rope_base))
+
+    @property
+    def channels(self) -> int:
+        return self.num_kv_heads * self.head_dim
+
+    def validate(self) -> None:
+        d = self.desc()
+        _check(lib().rkv_layer_validate(C.byref(d)))
+
+
+# ------------------------------------------------------------ host helpers
+
+def calibrate_reorder(rotated_keys, stat: int = STAT_MEAN_ABS):
+    """calibrate_reorder (proj/src/reorder.cpp:91-110) -> (perm, inverse) int32.
+    rotated_keys: [rows, C] float (host).  stat: STAT_SUM (reference) or
+    STAT_MEAN_ABS (north star)."""
+    x = _np(rotated_keys, np.float32)
+    if x.ndim != 2:
+        raise ValueError("expected [b,h,s,d] or [tokens, channels]")
+    perm = np.empty(x.shape[1], np.int32)
+    inv = np.empty(x.shape[1], np.int32)
+    _check(lib().rkv_calibrate_reorder(x.ctypes.data, x.shape[0], x.shape[1], stat, perm.ctypes.data,
+                                       inv.ctypes.data))
+    return perm, inv
+
+
+def apply_reorder(x, perm, inverse: bool = False):
+    """apply_reorder (proj/src/reorder.cpp:112-128): dst[j] = src[p[j]]."""
+    perm = np.asarray(perm)
+    if x.shape[-1] != perm.size:
+        raise ValueError("apply_reorder: trailing dimension mismatch")
+    if inverse:
+        inv = np.empty_like(perm)
+        inv[perm] = np.arange(perm.size, dtype=perm.dtype)
+        perm = inv
+    return x[..., perm]
+
+
+def detect_massive_activations(hidden, rel_threshold: float = 50.0, abs_floor: float = 0.0):
+    """detect_massive_activations (proj/src/sink.cpp:14-45) -> uint8 flags [s]."""
+    h = _np(hidden, np.float32)
+    if h.ndim != 3:
+        raise ValueError("detect_massive_activations: expected [b,s,hidden]")
+    flags = np.empty(h.shape[1], np.uint8)
+    n = C.c_int64()
+    _check(lib().rkv_detect_sinks(h.ctypes.data, h.shape[0], h.shape[1], h.shape[2], float(rel_threshold),
+                                  float(abs_floor), flags.ctypes.data, C.byref(n)))
+    return flags
+
+
+# ------------------------------------------------------------ device layer
+
+class RotateKVLayer:
+    """One layer's 2-bit rotated KV cache on a CUDA device.
+
+    Host-side mirrors of every sequence's length and sink count give the
+    reference's argument checks (position == cache length, out-of-range
+    tokens, sidecar capacity) without a device round trip."""
+
+    def __init__(self, cfg: LayerConfig, perm, device="cuda", stream=None):
+        import torch
+
+        self.torch = torch
+        self.cfg = cfg
+        cfg.validate()
+        self.device = torch.device(device)
+        self._desc = cfg.desc()
+        c = cfg.channels
+        perm = _np(perm, np.int32)
+        if perm.shape != (c,) or not np.array_equal(np.sort(perm), np.arange(c)):
+            raise ValueError("reorder plan: perm must be a permutation of the channel count")
+        self.perm_host = perm
+        self.perm = torch.from_numpy(perm).to(self.device)
+        nbytes = lib().rkv_cache_bytes(C.byref(self._desc))
+        self._buf = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
+        base = (self._buf.data_ptr() + 255) // 256 * 256
+        self._view = CacheView()
+        _check(lib().rkv_cache_carve(C.byref(self._desc), base, nbytes, C.byref(self._view)))
+        self._base = base
+        rope_bytes = lib().rkv_rope_table_bytes(C.byref(self._desc), cfg.max_tokens)
+        self.rope = torch.empty(rope_bytes // 4, dtype=torch.float32, device=self.device)
+        self.lengths = np.zeros(cfg.batch, np.int64)
+        self.sink_counts = np.zeros(cfg.batch, np.int64)
+        self._ws = None
+        self._ws_for = None
+        self.stream = stream
+        _check(lib().rkv_rope_table_init(C.byref(self._desc), _ptr(self.rope), cfg.max_tokens, self._stream()))
+        self.reset()
+
+    # -- plumbing
+    def _stream(self):
+        s = self.stream if self.stream is not None else self.torch.cuda.current_stream(self.device)
+        return C.c_void_p(s.cuda_stream)
+
+    def reset(self):
+        _check(lib().rkv_cache_reset(C.byref(self._desc), C.byref(self._view), self._stream()))
+        self.lengths[:] = 0
+        self.sink_counts[:] = 0
+
+    def _arr(self, name, dtype, shape):
+        """A torch view of one carved cache array."""
+        torch = self.torch
+        off = getattr(self._view, name) - self._base
+        n = int(np.prod(shape))
+        esz = torch.empty((), dtype=dtype).element_size()
+        start = (self._base - self._buf.data_ptr()) + off
+        return self._buf[start:start + n * esz].view(dtype).view(*shape)
+
+    def arrays(self):
+        """Device views: k_codes/v_codes [B,T,C/16] int32 (u32 bits), k_meta/v_meta
+        [B,T,C/128] int32, sink_k/sink_v [B,S,C] fp16, sink_pos [B,S], sink_count [B],
+        sink_mask [B,ceil(T/32)]."""
+        t = self.torch
+        B, T, S, Cc = self.cfg.batch, self.cfg.max_tokens, self.cfg.max_sinks, self.cfg.channels
+        return {
+            "k_codes": self._arr("k_codes", t.int32, (B, T, Cc // 16)),
+            "v_codes": self._arr("v_codes", t.int32, (B, T, Cc // 16)),
+            "k_meta": self._arr("k_meta", t.int32, (B, T, Cc // 128)),
+            "v_meta": self._arr("v_meta", t.int32, (B, T, Cc // 128)),
+            "sink_k": self._arr("sink_k", t.float16, (B, max(S, 1), Cc)),
+            "sink_v": self._arr("sink_v", t.float16, (B, max(S, 1), Cc)),
+            "sink_pos": self._arr("sink_pos", t.int32, (B, max(S, 1))),
+            "sink_count": self._arr("sink_count", t.int32, (B,)),
+            "sink_mask": self._arr("sink_mask", t.int32, (B, (T + 31) // 32)),
+        }
+
+    # -- LayerKVCache::append (proj/src/kv_cache.cpp:8-22), batched
+    def append(self, k, v, sink_flags=None, start_pos=None):
+        """k, v: [B, n, C] fp16 CUDA tensors (pre-RoPE, unrotated).
+        sink_flags: optional [B, n] bool/uint8.  Appends at each sequence's
+        current length unless start_pos ([B] ints) is given."""
+        torch = self.torch
+        B, Cc = self.cfg.batch, self.cfg.channels
+        if k.dtype != torch.float16 or v.dtype != torch.float16:
+            raise ValueError("cache append: k and v must be fp16")
+        if k.dim() != 3 or k.shape[0] != B or k.shape[2] != Cc or v.shape != k.shape:
+            raise ValueError("cache append: row length must equal channel count")
+        n = k.shape[1]
+        start = self.lengths.copy() if start_pos is None else _np(start_pos, np.int64)
+        if np.any(start < 0) or np.any(start + n > self.cfg.max_tokens):
+            raise IndexError("cache: token index out of range")
+        flags_t = None
+        if sink_flags is not None:
+            f = torch.as_tensor(sink_flags).to(torch.uint8)
+            if tuple(f.shape) != (B, n):
+                raise ValueError("sink flags must be [batch, new tokens]")
+            add = f.cpu().numpy().sum(axis=1)
+            if np.any(self.sink_counts + add > self.cfg.max_sinks):
+                raise IndexError("cache: sink sidecar capacity exceeded")
+            self.sink_counts += add
+            flags_t = f.to(self.device).contiguous()
+        k = k.contiguous()
+        v = v.contiguous()
+        start_t = torch.from_numpy(start).to(self.device)
+        _check(lib().rkv_quantize_kv(C.byref(self._desc), _ptr(k), _ptr(v), _ptr(self.perm), _ptr(flags_t),
+                                     _ptr(start_t), n, C.byref(self._view), self._stream()))
+        self.lengths = np.maximum(self.lengths, start + n)
+        self._keep = (k, v, flags_t, start_t)  # keep inputs alive until the stream consumes them
+
+    def workspace(self, max_seq_len: int):
+        need = lib().rkv_decode_workspace_bytes(C.byref(self._desc), max_seq_len)
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = self.torch.empty(need, dtype=self.torch.uint8, device=self.device)
+        return self._ws, need
+
+    # -- the attention half of decode_step (proj/src/pipeline.cpp:211-261)
+    def decode(self, q, seq_len=None, out=None, max_seq_len=None):
+        """q: [B, Hq, 128] fp16 pre-RoPE at position seq_len-1.  Returns fp32
+        [B, Hq, 128] with V's rotation undone."""
+        torch = self.torch
+        B, Hq = self.cfg.batch, self.cfg.num_q_heads
+        if q.dtype != torch.float16 or tuple(q.shape) != (B, Hq, self.cfg.head_dim):
+            raise ValueError("decode_step: input must have d_model elements")
+        lens = self.lengths if seq_len is None else _np(seq_len, np.int64)
+        if np.any(lens < 1) or np.any(lens > self.lengths):
+            raise ValueError("decode_step: position must equal current cache length")
+        msl = int(lens.max()) if max_seq_len is None else int(max_seq_len)
+        if out is None:
+            out = torch.empty((B, Hq, self.cfg.head_dim), dtype=torch.float32, device=self.device)
+        ws, need = self.workspace(msl)
+        self._lens_t = torch.from_numpy(lens).to(self.device)
+        q = q.contiguous()
+        _check(lib().rkv_decode_attention(C.byref(self._desc), _ptr(q), _ptr(self._lens_t), msl,
+                                          C.byref(self._view), _ptr(self.perm), _ptr(self.rope), _ptr(out),
+                                          _ptr(ws), need, self._stream()))
+        return out
+
+    def decode_device(self, q, seq_len_t, max_seq_len, out, ws, ws_bytes):
+        """Allocation-free decode with device-resident lengths (CUDA-graph safe)."""
+        _check(lib().rkv_decode_attention(C.byref(self._desc), _ptr(q), _ptr(seq_len_t), int(max_seq_len),
+                                          C.byref(self._view), _ptr(self.perm), _ptr(self.rope), _ptr(out),
+                                          _ptr(ws), ws_bytes, self._stream()))
+        return out
+
+    def append_device(self, k, v, start_t, sink_flags_t=None):
+        """Allocation-free append with device-resident start positions."""
+        _check(lib().rkv_quantize_kv(C.byref(self._desc), _ptr(k), _ptr(v), _ptr(self.perm), _ptr(sink_flags_t),
+                                     _ptr(start_t), k.shape[1], C.byref(self._view), self._stream()))
+
+    def decode_step(self, k_new, v_new, q):
+        """decode_step without projections: append the new token (never a sink,
+        proj/src/pipeline.cpp:207-209), then attend over the whole cache."""
+        self.append(k_new, v_new)
+        return self.decode(q)
+
+
+def rotate_keys(cfg: LayerConfig, k):
+    """Grouped-head FWHT of raw fp16 K rows [rows, C] on the device -> fp32."""
+    torch = __import__("torch")
+    d = cfg.desc()
+    k = k.contiguous()
+    out = torch.empty(k.shape, dtype=torch.float32, device=k.device)
+    _check(lib().rkv_rotate_keys(C.byref(d), _ptr(k), k.numel() // cfg.channels, _ptr(out),
+                                 C.c_void_p(torch.cuda.current_stream(k.device).cuda_stream)))
+    return out

@@ -1,0 +1,326 @@
+"""GPU parity: the sm_100a kernels through the C ABI vs the CPU oracle
+(oracle/rkv_oracle.c) and, where oracle/_ref was built, the unmodified
+reference.  Bars (BASELINE.json north_star):
+  * packed 2-bit codes, scales and zeros: bit-exact;
+  * decode output: max|a-b|/max|b| <= 2e-3 (the reference's rel_diff,
+    proj/tests/test_pipeline.cpp:23-27) and cosine >= 0.9999.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2501_16383_b200 as P  # noqa: E402
+from paper_2501_16383_b200 import workload as WL  # noqa: E402
+
+REL_TOL = 2e-3
+COS_TOL = 0.9999
+
+
+def rel_err(a, b):
+    a = np.asarray(a, np.float64).reshape(-1)
+    b = np.asarray(b, np.float64).reshape(-1)
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-12))
+
+
+def cosine(a, b):
+    a = np.asarray(a, np.float64).reshape(-1)
+    b = np.asarray(b, np.float64).reshape(-1)
+    return float(a @ b / (np.linalg.norm(a) * np.linalg.norm(b)))
+
+
+def small_workload(hq, hkv, g, base=10000.0, outliers=4, gain=(10.0, 30.0)):
+    return WL.Workload("test", 1, hq, hkv, 0, g, base, outliers, gain)
+
+
+def build_layer(w, batch, max_tokens, seed, fmt=P.SCALE_FP16_CEIL, max_sinks=8, perm=None):
+    if perm is None:
+        perm = WL.calibration_perm(w, seed)
+    cfg = P.LayerConfig(batch=batch, num_q_heads=w.num_q_heads, num_kv_heads=w.num_kv_heads,
+                        heads_per_group=w.heads_per_group, max_tokens=max_tokens, max_sinks=max_sinks,
+                        rope_base=w.rope_base, scale_format=fmt)
+    return P.RotateKVLayer(cfg, perm), perm
+
+
+def cache_host(layer):
+    a = layer.arrays()
+    return {k: v.cpu().numpy() for k, v in a.items()}
+
+
+# ------------------------------------------------------------- quantize_kv
+
+@pytest.mark.parametrize("hq,hkv,g,fmt", [
+    (8, 8, 4, P.SCALE_FP16_CEIL), (8, 8, 2, P.SCALE_FP16_CEIL), (4, 4, 1, P.SCALE_FP16_CEIL),
+    (40, 40, 4, P.SCALE_FP16_CEIL), (32, 8, 2, P.SCALE_FP16_CEIL), (8, 8, 4, P.SCALE_E4M3_CEIL),
+    (40, 40, 4, P.SCALE_E4M3_CEIL),
+])
+def test_quantize_kv_bit_exact_vs_oracle(oracle, hq, hkv, g, fmt):
+    w = small_workload(hq, hkv, g)
+    B, T = 2, 37
+    layer, perm = build_layer(w, B, 64, seed=1, fmt=fmt)
+    k, v = WL.make_kv(w, 1, B, T)
+    sinks = torch.zeros(B, T, dtype=torch.uint8)
+    sinks[:, 0] = 1
+    sinks[1, 20] = 1
+    layer.append(k, v, sinks)
+    torch.cuda.synchronize()
+    got = cache_host(layer)
+    kh = k.cpu().numpy()
+    vh = v.cpu().numpy()
+    for b in range(B):
+        kc, km, vc, vm = oracle.quantize_kv_rows(kh[b], vh[b], hkv, 128, g, perm, fmt)
+        s = sinks[b].numpy().astype(bool)
+        kc[s] = 0
+        km[s] = 0
+        vc[s] = 0
+        vm[s] = 0
+        assert np.array_equal(got["k_codes"][b, :T].view(np.uint32), kc)
+        assert np.array_equal(got["k_meta"][b, :T].view(np.uint32), km)
+        assert np.array_equal(got["v_codes"][b, :T].view(np.uint32), vc)
+        assert np.array_equal(got["v_meta"][b, :T].view(np.uint32), vm)
+        pos = np.flatnonzero(s)
+        assert got["sink_count"][b] == len(pos)
+        assert list(got["sink_pos"][b, :len(pos)]) == list(pos)
+        for i, t in enumerate(pos):
+            assert np.array_equal(got["sink_k"][b, i].view(np.uint16), kh[b, t].view(np.uint16))
+            assert np.array_equal(got["sink_v"][b, i].view(np.uint16), vh[b, t].view(np.uint16))
+        mask = got["sink_mask"][b].view(np.uint32)
+        bits = [(mask[t // 32] >> (t % 32)) & 1 for t in range(T)]
+        assert bits == list(s.astype(int))
+
+
+def test_quantize_kv_e4m3_matches_unmodified_reference(ref):
+    """E4M3 mode vs the reference's own rotate_rows -> apply_reorder ->
+    quantize_token (compiled from /root/reference, oracle/_ref)."""
+    w = small_workload(8, 8, 4)
+    B, T = 1, 48
+    layer, perm = build_layer(w, B, 64, seed=3, fmt=P.SCALE_E4M3_CEIL)
+    k, v = WL.make_kv(w, 3, B, T)
+    layer.append(k, v)
+    torch.cuda.synchronize()
+    got = cache_host(layer)
+    kc, ks, kz, vc, vs, vz = ref.ref_quantize_kv_rows(k[0].float().cpu().numpy(), v[0].float().cpu().numpy(),
+                                                     8, 128, 4, perm)
+    assert np.array_equal(got["k_codes"][0, :T].view(np.uint32), kc)
+    assert np.array_equal(got["v_codes"][0, :T].view(np.uint32), vc)
+    dec = np.vectorize(lambda c: ref.e4m3_decode(int(c)))
+    km = got["k_meta"][0, :T].view(np.uint32)
+    assert np.array_equal((km & 0xFFFF).astype(np.uint16).view(np.float16).astype(np.float32), dec(ks))
+    assert np.array_equal((km >> 16).astype(np.uint16).view(np.float16).astype(np.float32), kz.astype(np.float32))
+
+
+def test_quantize_kv_boundary_values_bit_exact(oracle):
+    """Rows whose rotated values sit on rounding boundaries: inject rows made
+    of a few distinct values so FWHT outputs hit (m-0.5)*s ties."""
+    w = small_workload(8, 8, 4)
+    B, T = 1, 32
+    layer, perm = build_layer(w, B, 32, seed=5)
+    rng = np.random.default_rng(5)
+    k = rng.integers(-3, 4, size=(B, T, w.channels)).astype(np.float16)
+    v = (rng.integers(-2, 3, size=(B, T, w.channels)) * 0.5).astype(np.float16)
+    kt = torch.from_numpy(k).cuda()
+    vt = torch.from_numpy(v).cuda()
+    layer.append(kt, vt)
+    torch.cuda.synchronize()
+    got = cache_host(layer)
+    kc, km, vc, vm = oracle.quantize_kv_rows(k[0], v[0], 8, 128, 4, perm)
+    assert np.array_equal(got["k_codes"][0, :T].view(np.uint32), kc)
+    assert np.array_equal(got["v_codes"][0, :T].view(np.uint32), vc)
+    assert np.array_equal(got["k_meta"][0, :T].view(np.uint32), km)
+    assert np.array_equal(got["v_meta"][0, :T].view(np.uint32), vm)
+
+
+def test_quantize_odd_token_count_and_offsets(oracle):
+    """Appends of 1 token at a time and odd counts land at the right rows."""
+    w = small_workload(8, 8, 4)
+    B = 3
+    layer, perm = build_layer(w, B, 40, seed=6)
+    k, v = WL.make_kv(w, 6, B, 9)
+    layer.append(k[:, :5], v[:, :5])
+    for t in range(5, 9):
+        layer.append(k[:, t:t + 1], v[:, t:t + 1])
+    torch.cuda.synchronize()
+    got = cache_host(layer)
+    for b in range(B):
+        kc, km, vc, vm = oracle.quantize_kv_rows(k[b].cpu().numpy(), v[b].cpu().numpy(), 8, 128, 4, perm)
+        assert np.array_equal(got["k_codes"][b, :9].view(np.uint32), kc)
+        assert np.array_equal(got["v_meta"][b, :9].view(np.uint32), vm)
+
+
+# --------------------------------------------------------- decode_attention
+
+def oracle_decode(oracle, layer, got, b, T, q, w, perm, kraw, vraw):
+    s = np.zeros(T, np.uint8)
+    mask = got["sink_mask"][b].view(np.uint32)
+    for t in range(T):
+        s[t] = (mask[t // 32] >> (t % 32)) & 1
+    return oracle.decode_attention(got["k_codes"][b, :T].view(np.uint32), got["k_meta"][b, :T].view(np.uint32),
+                                   got["v_codes"][b, :T].view(np.uint32), got["v_meta"][b, :T].view(np.uint32),
+                                   s, kraw[:T], vraw[:T], q, w.num_q_heads, w.num_kv_heads, 128,
+                                   w.heads_per_group, perm, w.rope_base)
+
+
+@pytest.mark.parametrize("hq,hkv,g,base,T", [
+    (8, 8, 4, 10000.0, 37), (8, 8, 4, 10000.0, 1), (8, 8, 2, 10000.0, 300),
+    (32, 8, 2, 500000.0, 129), (4, 4, 1, 10000.0, 64), (40, 40, 4, 10000.0, 200),
+    (16, 8, 4, 10000.0, 77),
+])
+def test_decode_vs_oracle(oracle, hq, hkv, g, base, T):
+    w = small_workload(hq, hkv, g, base=base)
+    B = 2
+    layer, perm = build_layer(w, B, T + 8, seed=T)
+    k, v = WL.make_kv(w, T, B, T)
+    sinks = torch.zeros(B, T, dtype=torch.uint8)
+    sinks[:, 0] = 1
+    if T > 10:
+        sinks[0, T // 2] = 1
+    layer.append(k, v, sinks)
+    q = WL.make_q(w, T, B)
+    out = layer.decode(q).cpu().numpy()
+    got = cache_host(layer)
+    for b in range(B):
+        want = oracle_decode(oracle, layer, got, b, T, q[b].cpu().numpy(), w, perm, k[b].cpu().numpy(),
+                             v[b].cpu().numpy())
+        assert rel_err(out[b], want) < REL_TOL
+        assert cosine(out[b], want) > COS_TOL
+
+
+def test_decode_ragged_lengths(oracle):
+    """Sequences of different lengths in one call (split tails, short splits)."""
+    w = small_workload(8, 8, 4)
+    lens = [1, 17, 64, 251]
+    B = len(lens)
+    layer, perm = build_layer(w, B, 256, seed=9)
+    k, v = WL.make_kv(w, 9, B, 251)
+    sinks = torch.zeros(B, 251, dtype=torch.uint8)
+    sinks[:, 0] = 1
+    sinks[3, 100] = 1
+    layer.append(k, v, sinks)
+    q = WL.make_q(w, 9, B)
+    out = layer.decode(q, seq_len=lens).cpu().numpy()
+    got = cache_host(layer)
+    for b, T in enumerate(lens):
+        want = oracle_decode(oracle, layer, got, b, T, q[b].cpu().numpy(), w, perm, k[b].cpu().numpy(),
+                             v[b].cpu().numpy())
+        assert rel_err(out[b], want) < REL_TOL, (b, T)
+
+
+def test_decode_step_loop_vs_reference_semantics(oracle):
+    """decode_step semantics: append the token, then attend with q at its
+    position; several steps, each checked against the oracle."""
+    w = small_workload(8, 8, 4)
+    B, T0 = 2, 50
+    layer, perm = build_layer(w, B, 64, seed=12)
+    k, v = WL.make_kv(w, 12, B, T0 + 4)
+    sinks = torch.zeros(B, T0, dtype=torch.uint8)
+    sinks[:, 0] = 1
+    layer.append(k[:, :T0], v[:, :T0], sinks)
+    for step in range(4):
+        t = T0 + step
+        q = WL.make_q(w, 12, B, step=step)
+        out = layer.decode_step(k[:, t:t + 1], v[:, t:t + 1], q).cpu().numpy()
+        got = cache_host(layer)
+        for b in range(B):
+            want = oracle_decode(oracle, layer, got, b, t + 1, q[b].cpu().numpy(), w, perm, k[b].cpu().numpy(),
+                                 v[b].cpu().numpy())
+            assert rel_err(out[b], want) < REL_TOL
+
+
+def test_decode_matches_reference_decode_step(ref):
+    """End to end against the reference's own decode_step
+    (proj/src/pipeline.cpp:193-263) in e4m3 mode, identity projections."""
+    w = small_workload(8, 8, 4)
+    T = 40
+    layer, perm = build_layer(w, 1, T + 1, seed=21, fmt=P.SCALE_E4M3_CEIL)
+    k, v = WL.make_kv(w, 21, 1, T + 1)
+    x = k[:, T:T + 1]  # decode token: key = value = query (identity W)
+    sinks = torch.zeros(1, T, dtype=torch.uint8)
+    sinks[0, 0] = 1
+    sinks[0, 11] = 1
+    layer.append(k[:, :T], v[:, :T], sinks)
+    out = layer.decode_step(x, x, x.reshape(1, 8, 128)).cpu().numpy().reshape(-1)
+    want = ref.ref_decode_step(k[0, :T].float().cpu().numpy(), v[0, :T].float().cpu().numpy(), sinks[0].numpy(),
+                               perm, x[0, 0].float().cpu().numpy(), 8, 128, 4, 10000.0)
+    assert rel_err(out, want) < REL_TOL
+    assert cosine(out, want) > COS_TOL
+
+
+def test_decode_deterministic():
+    w = small_workload(40, 40, 4)
+    layer, perm = build_layer(w, 2, 600, seed=4)
+    k, v = WL.make_kv(w, 4, 2, 600)
+    layer.append(k, v)
+    q = WL.make_q(w, 4, 2)
+    a = layer.decode(q).clone()
+    b = layer.decode(q)
+    assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("cfg_id", [2, 3])
+def test_full_size_decode_sampled_vs_oracle(oracle, cfg_id):
+    """BASELINE config sizes: the whole batch runs on the GPU; two sampled
+    sequences are checked against the oracle."""
+    w = WL.CONFIGS[cfg_id]
+    B = w.batch if cfg_id == 2 else 8  # cfg3 batch-sharded: one 8-sequence shard
+    T = w.tokens
+    layer, perm = build_layer(w, B, T + 1, seed=cfg_id)
+    k, v = WL.make_kv(w, cfg_id, B, T)
+    flags = torch.zeros(B, T, dtype=torch.uint8)
+    for t in WL.sink_positions(w, cfg_id, T):
+        flags[:, t] = 1
+    layer.append(k, v, flags)
+    q = WL.make_q(w, cfg_id, B)
+    out = layer.decode(q).cpu().numpy()
+    got = cache_host(layer)
+    for b in (0, B - 1):
+        want = oracle_decode(oracle, layer, got, b, T, q[b].cpu().numpy(), w, perm, k[b].cpu().numpy(),
+                             v[b].cpu().numpy())
+        assert rel_err(out[b], want) < REL_TOL
+        assert cosine(out[b], want) > COS_TOL
+
+
+def test_full_size_quantize_sampled_rows_bit_exact(oracle):
+    """cfg2-sized append; sampled rows checked bit-exact."""
+    w = WL.CONFIGS[2]
+    B, T = 16, 1024
+    layer, perm = build_layer(w, B, T, seed=22)
+    k, v = WL.make_kv(w, 22, B, T)
+    layer.append(k, v)
+    got = cache_host(layer)
+    rng = np.random.default_rng(0)
+    for b in rng.choice(B, 3, replace=False):
+        rows = np.sort(rng.choice(T, 16, replace=False))
+        kc, km, vc, vm = oracle.quantize_kv_rows(k[b, rows].cpu().numpy(), v[b, rows].cpu().numpy(), 40, 128, 4,
+                                                 perm)
+        assert np.array_equal(got["k_codes"][b, rows].view(np.uint32), kc)
+        assert np.array_equal(got["k_meta"][b, rows].view(np.uint32), km)
+        assert np.array_equal(got["v_codes"][b, rows].view(np.uint32), vc)
+        assert np.array_equal(got["v_meta"][b, rows].view(np.uint32), vm)
+
+
+def test_rotate_keys_matches_oracle(oracle):
+    w = small_workload(8, 8, 4)
+    cfg = P.LayerConfig(batch=1, num_q_heads=8, num_kv_heads=8, heads_per_group=4)
+    k, _ = WL.make_kv(w, 30, 1, 16)
+    got = P.rotate_keys(cfg, k[0]).cpu().numpy()
+    want = oracle.rotate_rows(k[0].float().cpu().numpy(), 128, 4, 8)
+    assert np.array_equal(got, want)
+
+
+def test_errors_mirror_reference_exceptions():
+    w = small_workload(8, 8, 4)
+    layer, perm = build_layer(w, 1, 8, seed=1, max_sinks=1)
+    k, v = WL.make_kv(w, 1, 1, 9)
+    with pytest.raises(IndexError):  # std::out_of_range: past capacity
+        layer.append(k, v)
+    with pytest.raises(ValueError):  # std::invalid_argument: row length
+        layer.append(k[:, :, :512], v[:, :, :512])
+    two = torch.ones(1, 2, dtype=torch.uint8)
+    with pytest.raises(IndexError):  # sidecar full
+        layer.append(k[:, :2], v[:, :2], two)
+    with pytest.raises(ValueError):  # position must equal current cache length
+        layer.decode(WL.make_q(w, 1, 1))
