@@ -2,7 +2,7 @@
  * rotatekv.h -- C ABI of the B200-native RotateKV KV-cache hot path.
  *
  * A drop-in for the reference's C++ hot-path API (namespace rotatekv in
- * /root/reference/proj/include/rotatekv/*.hpp).  Each entry point names the
+ * /root/reference/proj/include/rotatekv/).  Each entry point names the
  * reference interface it replaces.  Conventions:
  *   - plain pointers and sizes only; fp16 tensors are passed as uint16_t bits;
  *     `stream` is a cudaStream_t passed as void* (NULL = legacy default stream);
@@ -100,9 +100,11 @@ rkv_status rkv_cache_carve(const rkv_layer_desc* desc, void* base, size_t bytes,
  * proj/include/rotatekv/kv_cache.hpp:17): sink counts and masks to zero. */
 rkv_status rkv_cache_reset(const rkv_layer_desc* desc, const rkv_cache* cache, void* stream);
 
-/* RoPE cos/sin table [max_pos][head_dim/2] float2 (cos, sin of pos*theta_i,
- * theta_i = base^(-2i/d) evaluated in double like proj/src/rope.cpp:17-24).
- * Read by rkv_decode_attention; build once per (rope_base, max_pos). */
+/* RoPE table [ceil(max_pos/2)][head_dim/2] float4: for the position pair
+ * (2k, 2k+1) and frequency i, (cos 2k*th_i, cos (2k+1)*th_i, sin 2k*th_i,
+ * sin (2k+1)*th_i) with th_i = base^(-2i/d) evaluated in double like
+ * proj/src/rope.cpp:17-24.  Read by rkv_decode_attention; build once per
+ * (rope_base, max_pos). */
 size_t rkv_rope_table_bytes(const rkv_layer_desc* desc, int64_t max_pos);
 rkv_status rkv_rope_table_init(const rkv_layer_desc* desc, float* table, int64_t max_pos, void* stream);
 

@@ -6,25 +6,31 @@
 //   query  = RoPE_{T-1}(q)                             (prepare_queries)
 //   logits = q.k / sqrt(d), softmax, o' = sum p v'     (v' in the rotated frame)
 //   out    = H_128 o'                                  (V's inverse rotation, W_o_f)
-// B200 mapping (one CTA per (split, sequence), grid = splits x B sized to the
-// 148 SMs):
-//   * TMA bulk copies (cp.async.bulk, UBLKCP) stream each tile of TT tokens --
-//     packed K/V words, K/V scale|zero words and the tile's RoPE rows -- into
-//     an NS-stage shared-memory ring guarded by mbarriers;
-//   * K1: every thread dequantizes whole packed words (one quant group per
-//     word, so one scale) and scatters the 16 values to their natural channel
-//     (slot j -> channel perm[j]) in a swizzled fp32 tile;
-//   * K2: a 16-lane group owns one FWHT group (G KV heads) of a token PAIR:
-//     float2 registers hold the same channel of both tokens, so the inverse
-//     FWHT (== the forward one, proj/src/hadamard.cpp:75), RoPE and the q.k
-//     dot are FADD2/FFMA2; lane partials reduce by shuffles;
-//   * online softmax in exp2 domain per head;
-//   * V: each thread owns one packed V word x one q head and accumulates
-//     sum p*s*code (zero point folded once per token), never materialising
-//     dequantized V;
-//   * sinks (raw fp16 sidecar rows) are one extra partial (decode_sinks_kernel)
-//     and a combine kernel merges the partials in a fixed order and applies
-//     H_128 to the rotated-frame accumulator.  Deterministic.
+//
+// B200 mapping.  Grid = splits x B (one CTA per SM, shared-memory bound);
+// inside a CTA a "lane group" of L = 16 lanes (8 for G = 1) owns one FWHT
+// group g (G KV heads = GH*REP q heads) and one token pair per tile.
+//   * TMA bulk copies (cp.async.bulk -> UBLKCP) stream each tile of TT tokens
+//     (packed K/V words, scale|zero words, the tile's RoPE rows) into an
+//     NS-stage shared-memory ring guarded by mbarriers.
+//   * K1 (all threads): each thread takes a whole packed word (one quant
+//     group, one scale) for a token pair, dequantizes the 16 codes exactly
+//     (s*(c-z), proj/src/quant.cpp:99-107) as FADD2/FMUL2 over the pair and
+//     scatters them (STS.64) to their natural channel (slot j -> perm[j]) in
+//     a pair-interleaved, XOR-swizzled fp32 tile.  __syncthreads.
+//   * K2 (per lane group, no CTA barrier): inverse grouped FWHT (== forward,
+//     proj/src/hadamard.cpp:75) on float2 = (token, token+1) registers:
+//     layout A (LDS.128) -> butterfly stages on the low index bits -> STS.128
+//     -> layout B (LDS.64) -> stages on the high bits; every butterfly is one
+//     FADD2/FFMA2.  RoPE, q.k with 1/sqrt(n) folded into q; reduce-scatter
+//     of the logits over the lane group.
+//   * online softmax (exp2 domain) and V accumulation for the group's heads,
+//     each lane owning VW packed V words: acc += 4ps*(1 + c/4) (codes turned
+//     into floats by a mantissa OR, zero point folded once per token), never
+//     materialising dequantized V.  __syncthreads closes the tile.
+//   * every lane group writes its own (m, l, o') partial; the combine kernel
+//     merges partials in a fixed order, adds the fp16 sink rows (computed
+//     inline, natural frame) and applies H_128.  Deterministic.
 #include <cfloat>
 #include <cmath>
 
@@ -38,21 +44,20 @@ namespace {
 constexpr int kStages = 3;
 
 __device__ __forceinline__ int64_t lmin(int64_t a, int64_t b) { return a < b ? a : b; }
-constexpr int kMaxThreads = 320;  // plan_decode keeps NT <= 320 (204 registers per thread)
 
-// knat swizzle (same construction as quantize_kv.cu): float4 chunks of a
-// lane's layout-A row XOR the lane, unit parity moves a lane group's scalar
-// layout-B traffic to the other 16 banks.
-template <int N, int L>
-__device__ __forceinline__ int kswz(int c) {
-    constexpr int R = N / L;
-    constexpr int LR = ilog2(R), LN = ilog2(N), LL = ilog2(L);
-    return c ^ (((c >> LR) & (R / 4 - 1)) << 2) ^ (((c >> LN) & (32 / L - 1)) << LL);
+__device__ __forceinline__ float2 lds64(const unsigned char* p) { return *reinterpret_cast<const float2*>(p); }
+__device__ __forceinline__ float4 lds128f(const unsigned char* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ float2 rope_at(const float4* t, int64_t pos, int f) {
+    const float4 r = __ldg(t + (pos >> 1) * 64 + f);
+    return (pos & 1) ? make_float2(r.y, r.w) : make_float2(r.x, r.z);
+}
+__device__ __forceinline__ void sts64(uint32_t addr, float2 v) {
+    asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(v.x), "f"(v.y) : "memory");
 }
 
 struct SmemLayout {
-    size_t stage_bytes, kc, km, vc, vm, rope;  // offsets inside a stage
-    size_t stages, mbar, knat, q, addr, logit, prob, alpha, mask, total;
+    size_t stage_bytes, kc, km, vc, vm, rope;  // offsets inside one stage
+    size_t stages, mbar, knat, q, addr, mask, total;
 };
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -69,52 +74,70 @@ __host__ __device__ inline SmemLayout smem_layout(int C, int Hq, int TT) {
     s.stages = 0;
     s.mbar = s.stages + kStages * s.stage_bytes;
     s.knat = align16(s.mbar + kStages * 8);
-    s.q = align16(s.knat + size_t(TT) * C * 4);
-    s.addr = align16(s.q + size_t(Hq) * 128 * 4);
-    s.logit = align16(s.addr + size_t(C) * 2);
-    s.prob = align16(s.logit + size_t(TT) * Hq * 4);
-    s.alpha = align16(s.prob + size_t(TT) * Hq * 4);
-    s.mask = align16(s.alpha + size_t(Hq) * 4);
+    s.q = align16(s.knat + size_t(TT / 2) * C * 8);  // TT/2 token pairs x C float2
+    s.addr = align16(s.q + size_t(Hq) * 128 * 4 * 3 / 2);  // padded q rows (<= 1.5x)
+    s.mask = align16(s.addr + size_t(C) * 4);
     s.total = align16(s.mask + 16);
     return s;
 }
 
+// Float2 index of natural channel c inside a pair row: unit g = c/N holds the
+// FWHT group; layout-A lane la = (c%N)/R owns a contiguous R-float2 row whose
+// 16-byte chunks are XOR-swizzled with la so layout-A LDS.128 (8 lanes per
+// phase) and layout-B LDS.64 (16 lanes per phase) are conflict-free.
+template <int N, int L>
+__host__ __device__ inline int pair_pos(int c) {
+    constexpr int R = N / L, LR = ilog2(R);
+    const int g = c / N, i = c % N, la = i >> LR, qp = i & (R - 1);
+    return g * N + la * R + 2 * ((qp >> 1) ^ (la & 7)) + (qp & 1);
+}
+
+template <int N>
+constexpr int max_threads() { return N == 512 ? 320 : 256; }
+
 template <int N, int REP>
-__global__ void __launch_bounds__(kMaxThreads, 1) decode_split_kernel(DecodeParams p) {
+__global__ void __launch_bounds__(max_threads<N>(), 1) decode_split_kernel(DecodeParams p) {
     constexpr int L = N >= 256 ? 16 : 8;  // lanes per FWHT group
-    constexpr int R = N / L;              // float2 registers per lane
+    constexpr int R = N / L;              // float2 registers per lane (one token pair)
     constexpr int LR = ilog2(R), LN = ilog2(N), LL = ilog2(L);
     constexpr int GH = N / 128;           // KV heads per FWHT group
-    constexpr int JJ = 128 / L;           // registers per head in layout B
-    constexpr int HALF = JJ / 2;          // RoPE partner distance (bit 6 of d)
+    constexpr int JJ = 128 / L;           // layout-B registers per head
+    constexpr int HALF = JJ / 2;          // RoPE partner distance (d vs d+64)
     constexpr int NV = GH * REP;          // q heads served by one group
-    static_assert(R >= L, "layout A/B must cover all index bits");
+    constexpr int V0 = 2 * NV;            // logits per token pair
+    constexpr int WPG = GH * 8;           // packed V words per token per group
+    constexpr int VW = WPG / L;           // V words per lane
+    constexpr int VH = VW * REP;          // q heads per lane in the V phase
+    constexpr int QS = JJ + 4;            // padded q_l row (conflict-free LDS.128)
+    static_assert(R >= L && R >= 16, "layouts A/B must cover all index bits");
+    static_assert(V0 <= L && WPG % L == 0 && VH <= 4, "unsupported (G, Hq/Hkv) combination");
 
     extern __shared__ __align__(128) unsigned char smem[];
     const int C = p.C, W = C / 16, MG = C / 128, Hq = p.Hq;
-    const int NG = C / N, P = p.P, TT = 2 * P;
+    const int NG = C / N, PP = p.P, TT = 2 * PP;
     const SmemLayout lay = smem_layout(C, Hq, TT);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + lay.mbar);
-    float* knat = reinterpret_cast<float*>(smem + lay.knat);
-    uint16_t* saddr = reinterpret_cast<uint16_t*>(smem + lay.addr);
-    float* logit_s = reinterpret_cast<float*>(smem + lay.logit);
-    float* prob_s = reinterpret_cast<float*>(smem + lay.prob);
-    float* alpha_s = reinterpret_cast<float*>(smem + lay.alpha);
+    unsigned char* knat = smem + lay.knat;
+    float* q_l = reinterpret_cast<float*>(smem + lay.q);
+    uint32_t* saddr = reinterpret_cast<uint32_t*>(smem + lay.addr);
     uint32_t* mask_s = reinterpret_cast<uint32_t*>(smem + lay.mask);
 
-    const int tid = threadIdx.x, lane = tid & 31, NT = blockDim.x;
+    const int tid = threadIdx.x, NT = blockDim.x;
+    const int lg = tid / L, lam = tid % L, lbase = (tid & 31) & ~(L - 1);
+    const int g = lg % NG, pp = lg / NG;
     const int b = blockIdx.y, split = blockIdx.x;
     const int64_t T = p.seq_len[b];
     const int64_t t_begin = static_cast<int64_t>(split) * p.chunk;
-    const int64_t t_end = min(T, t_begin + p.chunk);
-    const int64_t ws_row = (static_cast<int64_t>(b) * (p.S + 1) + split) * Hq;
+    const int64_t t_end = lmin(T, t_begin + p.chunk);
 
-    if (t_begin >= t_end) {  // empty split: neutral partial
-        for (int h = tid; h < Hq; h += NT) {
-            p.ws_ml[(ws_row + h) * 2] = -INFINITY;
-            p.ws_ml[(ws_row + h) * 2 + 1] = 0.0f;
+    if (t_begin >= t_end) {  // empty split: neutral partials for every lane group
+        for (int i = tid; i < PP * Hq; i += NT) {
+            const int64_t row = (static_cast<int64_t>(b) * p.NP + static_cast<int64_t>(split) * PP + i / Hq) * Hq + i % Hq;
+            p.ws_ml[row * 2] = -INFINITY;
+            p.ws_ml[row * 2 + 1] = 0.0f;
+            float4* o = reinterpret_cast<float4*>(p.ws_o + row * 128);
+            for (int k = 0; k < 32; ++k) o[k] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        for (int i = tid; i < Hq * 128; i += NT) p.ws_o[ws_row * 128 + i] = 0.0f;
         return;
     }
     const int ntiles = static_cast<int>((t_end - t_begin + TT - 1) / TT);
@@ -125,13 +148,13 @@ __global__ void __launch_bounds__(kMaxThreads, 1) decode_split_kernel(DecodePara
         const uint32_t n = static_cast<uint32_t>(lmin(TT, t_end - t0));
         unsigned char* st = smem + lay.stages + (it % kStages) * lay.stage_bytes;
         uint64_t* bar = mbar + (it % kStages);
-        const uint32_t bw = n * W * 4, bm = n * MG * 4, br = n * 64 * 8;
+        const uint32_t bw = n * W * 4, bm = n * MG * 4, br = ((n + 1) >> 1) * 64 * 16;
         mbar_arrive_expect_tx(bar, 2 * bw + 2 * bm + br);
         bulk_g2s(st + lay.kc, p.cache.k_codes + (row0 + t0) * W, bw, bar);
         bulk_g2s(st + lay.km, p.cache.k_meta + (row0 + t0) * MG, bm, bar);
         bulk_g2s(st + lay.vc, p.cache.v_codes + (row0 + t0) * W, bw, bar);
         bulk_g2s(st + lay.vm, p.cache.v_meta + (row0 + t0) * MG, bm, bar);
-        bulk_g2s(st + lay.rope, p.rope + t0 * 64, br, bar);
+        bulk_g2s(st + lay.rope, p.rope + (t0 >> 1) * 64, br, bar);
     };
 
     if (tid == 0) {
@@ -142,39 +165,50 @@ __global__ void __launch_bounds__(kMaxThreads, 1) decode_split_kernel(DecodePara
     if (tid == 0)
         for (int it = 0; it < kStages - 1 && it < ntiles; ++it) issue_tile(it);
 
-    // slot -> swizzled natural channel address inside a knat row
-    for (int j = tid; j < C; j += NT) saddr[j] = static_cast<uint16_t>(kswz<N, L>(__ldg(p.perm + j)));
+    // slot j -> byte offset of its natural channel inside a pair row, stored
+    // [j%16 / 4][word][j%4] so a warp's uint4 loads of consecutive words are
+    // conflict-free
+    for (int j = tid; j < C; j += NT) {
+        const int w = j >> 4, e = j & 15;
+        saddr[((e >> 2) * W + w) * 4 + (e & 3)] = static_cast<uint32_t>(pair_pos<N, L>(__ldg(p.perm + j))) * 8u;
+    }
 
-    // q: RoPE at position T-1 (prepare_queries), pre-scaled by log2(e)/sqrt(d),
-    // stored lane-major: q_l[(h*L + lam)*JJ + jj] = q[h][lam + L*jj]
-    float* q_l = reinterpret_cast<float*>(smem + lay.q);
+    // q: RoPE at position T-1 (prepare_queries), x log2(e)/sqrt(d) x 1/sqrt(n)
+    // (the FWHT normalisation), lane-major: q_l[(h*L + lam)*QS + jj] = q[h][lam + L*jj]
     {
-        const float2* cs = p.rope + (T - 1) * 64;
+        const float4* cs = p.rope + ((T - 1) >> 1) * 64;
+        const bool odd = (T - 1) & 1;
         const uint16_t* qb = p.q + static_cast<int64_t>(b) * Hq * 128;
-        auto qaddr = [&](int h, int d) { return (h * L + (d % L)) * JJ + d / L; };
+        const float qs = p.qscale * p.k_norm;
         for (int i = tid; i < Hq * 64; i += NT) {
             const int h = i >> 6, f = i & 63;
             const float a = h2f(qb[h * 128 + f]), bb = h2f(qb[h * 128 + f + 64]);
-            const float2 r = __ldg(cs + f);
-            q_l[qaddr(h, f)] = (a * r.x - bb * r.y) * p.qscale;
-            q_l[qaddr(h, f + 64)] = (a * r.y + bb * r.x) * p.qscale;
+            const float4 r4 = __ldg(cs + f);
+            const float2 r = odd ? make_float2(r4.y, r4.w) : make_float2(r4.x, r4.z);
+            q_l[(h * L + f % L) * QS + f / L] = (a * r.x - bb * r.y) * qs;
+            q_l[(h * L + (f + 64) % L) * QS + (f + 64) / L] = (a * r.y + bb * r.x) * qs;
         }
     }
 
-    // lane group = (FWHT group g, token pair pp)
-    const int lg = tid / L, lam = tid % L;
-    const int g = lg % NG, pp = lg / NG;
-
-    // V ownership: one packed word x one q head of its KV head
-    const int vw = tid % W, vr = tid / W;
-    const bool v_owner = tid < W * REP;
-    const int vh = (vw / 8) * REP + vr;
-    float2 acc[16];
+    // per-lane constants
+    const int pair_bytes = C * 8;
+    unsigned char* kpair = knat + pp * pair_bytes;  // this lane group's token pair
+    const int abase = (g * N + lam * R) * 8;        // layout-A row
+    uint32_t vb[L / 2];                              // layout-B bases (see pair_pos)
 #pragma unroll
-    for (int i = 0; i < 16; ++i) acc[i] = make_float2(0.f, 0.f);
-    float zsum = 0.f;
-    float m_run = -INFINITY, l_run = 0.f;  // head tid (tid < Hq)
-    __syncthreads();  // q_l and saddr complete
+    for (int k = 0; k < L / 2; ++k) vb[k] = static_cast<uint32_t>(g * N * 8 + 16 * ((lam >> 1) ^ k) + 8 * (lam & 1));
+
+    float m_run[VH], l_run[VH], zc[VH];
+    float2 acc[VH][8];
+#pragma unroll
+    for (int v = 0; v < VH; ++v) {
+        m_run[v] = -INFINITY;
+        l_run[v] = 0.f;
+        zc[v] = 0.f;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[v][e] = make_float2(0.f, 0.f);
+    }
+    __syncthreads();  // saddr and q_l complete
 
     const uint32_t* smask = p.cache.sink_mask + static_cast<int64_t>(b) * ((p.max_tokens + 31) / 32);
 
@@ -186,10 +220,10 @@ __global__ void __launch_bounds__(kMaxThreads, 1) decode_split_kernel(DecodePara
         const uint32_t* km = reinterpret_cast<const uint32_t*>(st + lay.km);
         const uint32_t* vc = reinterpret_cast<const uint32_t*>(st + lay.vc);
         const uint32_t* vm = reinterpret_cast<const uint32_t*>(st + lay.vm);
-        const float2* rope = reinterpret_cast<const float2*>(st + lay.rope);
+        const float4* rope4 = reinterpret_cast<const float4*>(st + lay.rope);
         mbar_wait(mbar + (it % kStages), (it / kStages) & 1);
 
-        // ---- K1: dequantize + un-reorder scatter
+        // ---- K1: exact dequantize of a word for a token pair + scatter (STS.64)
         if (tid == 0) {
             uint32_t m = 0;
             for (int tt = 0; tt < nv; ++tt) {
@@ -198,89 +232,107 @@ __global__ void __launch_bounds__(kMaxThreads, 1) decode_split_kernel(DecodePara
             }
             *mask_s = m;
         }
-        for (int item = tid; item < nv * W; item += NT) {
-            const int tt = item / W, w = item % W;
-            const uint32_t wd = kc[tt * W + w];
-            const uint32_t mt = km[tt * MG + (w >> 3)];
-            const float s = h2f(static_cast<uint16_t>(mt & 0xffffu));
-            const float zb = 8388608.0f + h2f(static_cast<uint16_t>(mt >> 16));
-            const uint4 a0 = lds128(saddr + 16 * w), a1 = lds128(saddr + 16 * w + 8);
-            const uint16_t* ad0 = reinterpret_cast<const uint16_t*>(&a0);
-            const uint16_t* ad1 = reinterpret_cast<const uint16_t*>(&a1);
-            float* dst = knat + tt * C;
+        // warp-granular items (W % 32 == 0): pq is warp-uniform, so the pair
+        // offset rides in a uniform register of the STS address
+        for (int wbase = (tid & ~31); wbase < PP * W; wbase += NT) {
+            const int pq = __shfl_sync(0xffffffffu, wbase / W, 0);
+            const int w = wbase - pq * W + (tid & 31);
+            const int tt0 = 2 * pq;
+            if (tt0 >= nv) continue;
+            const bool has1 = tt0 + 1 < nv;
+            const uint32_t w0 = kc[tt0 * W + w], w1 = has1 ? kc[(tt0 + 1) * W + w] : 0u;
+            const uint32_t m0 = km[tt0 * MG + (w >> 3)], m1 = has1 ? km[(tt0 + 1) * MG + (w >> 3)] : 0u;
+            const float2 s2 = make_float2(h2f(static_cast<uint16_t>(m0 & 0xffffu)), h2f(static_cast<uint16_t>(m1 & 0xffffu)));
+            const float2 nzb = make_float2(-(8388608.0f + h2f(static_cast<uint16_t>(m0 >> 16))),
+                                           -(8388608.0f + h2f(static_cast<uint16_t>(m1 >> 16))));
+            const uint4* ap = reinterpret_cast<const uint4*>(saddr) + w;
+            const uint32_t dst = smem_u32(knat) + pq * pair_bytes;
+            float2 val16[16];
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
-                // (2^23 + c) - (2^23 + z) = c - z exactly, times s exactly (proj/src/quant.cpp:99-107)
-                const float cz = __uint_as_float(0x4B000000u | ((wd >> (2 * e)) & 3u)) - zb;
-                dst[e < 8 ? ad0[e] : ad1[e - 8]] = s * cz;
+                // (2^23 + c) - (2^23 + z) = c - z exactly; times s exactly
+                const float2 xx = make_float2(__uint_as_float(and_or(w0 >> (2 * e), 3u, 0x4B000000u)),
+                                              __uint_as_float(and_or(w1 >> (2 * e), 3u, 0x4B000000u)));
+                val16[e] = mul2(add2(xx, nzb), s2);
+            }
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+                const uint4 a4 = ap[q4 * W];
+                sts64(dst + a4.x, val16[4 * q4]);
+                sts64(dst + a4.y, val16[4 * q4 + 1]);
+                sts64(dst + a4.z, val16[4 * q4 + 2]);
+                sts64(dst + a4.w, val16[4 * q4 + 3]);
             }
         }
         __syncthreads();
         if (tid == 0 && it + kStages - 1 < ntiles) issue_tile(it + kStages - 1);
 
-        // ---- K2: inverse grouped FWHT + RoPE + q.k for a token pair
-        for (int pq = pp; pq < P; pq += NT / (NG * L)) {
-            const int tt0 = 2 * pq;
-            float* r0 = knat + tt0 * C;
-            float* r1 = r0 + C;
-            float2 x[R];
+        // ---- K2: inverse grouped FWHT of the lane group's token pair
+        const int tt0 = 2 * pp;
+        float2 x[R];
 #pragma unroll
-            for (int q4 = 0; q4 < R / 4; ++q4) {
-                const int a = kswz<N, L>(g * N + lam * R + 4 * q4);
-                const float4 u = *reinterpret_cast<const float4*>(r0 + a);
-                const float4 v = *reinterpret_cast<const float4*>(r1 + a);
-                x[4 * q4] = make_float2(u.x, v.x);
-                x[4 * q4 + 1] = make_float2(u.y, v.y);
-                x[4 * q4 + 2] = make_float2(u.z, v.z);
-                x[4 * q4 + 3] = make_float2(u.w, v.w);
-            }
-            bfly_range<R, 0, LR>(x);
+        for (int q2 = 0; q2 < R / 2; ++q2) {
+            const float4 v = lds128f(kpair + abase + 16 * (q2 ^ (lam & 7)));
+            x[2 * q2] = make_float2(v.x, v.y);
+            x[2 * q2 + 1] = make_float2(v.z, v.w);
+        }
+        bfly_range<R, 0, LR>(x);
+        // two STS.64 per chunk: FADD2 results sit in arbitrary register pairs, an
+        // STS.128 would need 4 MOVs to build an aligned quad (same wavefronts)
+        const uint32_t kpair_s = smem_u32(kpair) + abase;
 #pragma unroll
-            for (int q4 = 0; q4 < R / 4; ++q4) {
-                const int a = kswz<N, L>(g * N + lam * R + 4 * q4);
-                *reinterpret_cast<float4*>(r0 + a) = make_float4(x[4 * q4].x, x[4 * q4 + 1].x, x[4 * q4 + 2].x, x[4 * q4 + 3].x);
-                *reinterpret_cast<float4*>(r1 + a) = make_float4(x[4 * q4].y, x[4 * q4 + 1].y, x[4 * q4 + 2].y, x[4 * q4 + 3].y);
-            }
-            __syncwarp();
+        for (int q2 = 0; q2 < R / 2; ++q2) {
+            const uint32_t a = kpair_s + 16 * (q2 ^ (lam & 7));
+            sts64(a, x[2 * q2]);
+            sts64(a + 8, x[2 * q2 + 1]);
+        }
+        __syncwarp();
 #pragma unroll
-            for (int j = 0; j < R; ++j) {
-                const int a = kswz<N, L>(g * N + lam + L * j);
-                x[j] = make_float2(r0[a], r1[a]);
-            }
-            bfly_range<R, LR - LL, LN - LL>(x);
-            // RoPE at each token's position, then the dot with every q head of the group
-            float2 part[NV];
+        for (int j = 0; j < R; ++j) {
+            // channel lam + L*j: layout-A owner la = (L*j) >> LR, in-row chunk
+            // ((lam >> 1) | c1) ^ (la & 7) with c1 = ((L*j) & (R-1)) >> 1
+            const int la = (L * j) >> LR;
+            const int c1 = ((L * j) & (R - 1)) >> 1;
+            const int k2 = la & 7;
+            const int lo = k2 & (L / 2 - 1);
+            const int hi = c1 ^ (k2 & ~(L / 2 - 1));
+            x[j] = lds64(kpair + vb[lo] + (la * R + 2 * hi) * 8);
+        }
+        bfly_range<R, LR - LL, LN - LL>(x);
+
+        // RoPE at each token's position, dot with the group's q heads
+        float2 part[NV];
 #pragma unroll
-            for (int v = 0; v < NV; ++v) part[v] = make_float2(0.f, 0.f);
-            const float2 nn = make_float2(p.k_norm, p.k_norm);
+        for (int v = 0; v < NV; ++v) part[v] = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int jj = 0; jj < HALF; ++jj) {
-                const int f = lam + L * jj;  // frequency index of (d, d+64)
-                const float2 c0 = rope[tt0 * 64 + f], c1 = rope[(tt0 + 1) * 64 + f];
-                const float2 cs = make_float2(c0.x, c1.x), sn = make_float2(c0.y, c1.y);
+        for (int jj = 0; jj < HALF; ++jj) {
+            const int f = lam + L * jj;  // frequency of (d, d+64)
+            // pair-interleaved table row: (cos t0, cos t1, sin t0, sin t1)
+            const float4 cq = rope4[pp * 64 + f];
+            const float2 cs = make_float2(cq.x, cq.y), sn = make_float2(cq.z, cq.w);
 #pragma unroll
-                for (int hh = 0; hh < GH; ++hh) {
-                    const float2 a = mul2(x[hh * JJ + jj], nn);
-                    const float2 bb = mul2(x[hh * JJ + jj + HALF], nn);
-                    const float2 ar = fma2(a, cs, mul2(make_float2(-bb.x, -bb.y), sn));  // a c - b s
-                    const float2 br = fma2(a, sn, mul2(bb, cs));                         // a s + b c
+            for (int hh = 0; hh < GH; ++hh) {
+                const float2 a = x[hh * JJ + jj], bb = x[hh * JJ + jj + HALF];
+                const float2 ar = fma2(a, cs, mul2(make_float2(-bb.x, -bb.y), sn));  // a c - b s
+                const float2 br = fma2(a, sn, mul2(bb, cs));                         // a s + b c
 #pragma unroll
-                    for (int r = 0; r < REP; ++r) {
-                        const float* qh = q_l + (((g * GH + hh) * REP + r) * L + lam) * JJ;
-                        const float qa = qh[jj], qb = qh[jj + HALF];
-                        part[hh * REP + r] = fma2(make_float2(qa, qa), ar, part[hh * REP + r]);
-                        part[hh * REP + r] = fma2(make_float2(qb, qb), br, part[hh * REP + r]);
-                    }
+                for (int r = 0; r < REP; ++r) {
+                    const float* qh = q_l + (((g * GH + hh) * REP + r) * L + lam) * QS;
+                    const float qa = qh[jj], qb = qh[jj + HALF];
+                    part[hh * REP + r] = fma2(make_float2(qa, qa), ar, part[hh * REP + r]);
+                    part[hh * REP + r] = fma2(make_float2(qb, qb), br, part[hh * REP + r]);
                 }
             }
-            // reduce the NV x 2 partials over the L lanes of the group
-            float val[2 * NV];
+        }
+        // reduce-scatter the V0 = 2*NV partials over the L lanes; afterwards lane
+        // lam holds value (lam >> SH) = 2*local_head + token
+        float val[V0];
 #pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                val[2 * v] = part[v].x;
-                val[2 * v + 1] = part[v].y;
-            }
-            constexpr int V0 = 2 * NV;
+        for (int v = 0; v < NV; ++v) {
+            val[2 * v] = part[v].x;
+            val[2 * v + 1] = part[v].y;
+        }
+        {
             int nvals = V0;
 #pragma unroll
             for (int stp = L / 2; stp >= 1; stp >>= 1) {
@@ -300,160 +352,144 @@ __global__ void __launch_bounds__(kMaxThreads, 1) decode_split_kernel(DecodePara
                     val[0] += __shfl_xor_sync(0xffffffffu, val[0], stp);
                 }
             }
-            // after the halvings lane lam holds value index lam >> (LL - log2(V0)) (V0 <= L)
-            // or values lam*(V0/L) + k (V0 > L)
-            if constexpr (V0 <= L) {
-                constexpr int sh = LL - ilog2(V0);
-                if ((lam & ((1 << sh) - 1)) == 0) {
-                    const int vidx = lam >> sh;
-                    const int v = vidx >> 1, tok = vidx & 1;
-                    const int h = (g * GH + v / REP) * REP + (v % REP);
-                    logit_s[(tt0 + tok) * Hq + h] = val[0];
-                }
-            } else {
-#pragma unroll
-                for (int k = 0; k < V0 / L; ++k) {
-                    const int vidx = lam * (V0 / L) + k;
-                    const int v = vidx >> 1, tok = vidx & 1;
-                    const int h = (g * GH + v / REP) * REP + (v % REP);
-                    logit_s[(tt0 + tok) * Hq + h] = val[k];
-                }
-            }
-            __syncwarp();
         }
-        __syncthreads();
+        constexpr int SH = LL - ilog2(V0);
 
-        // ---- online softmax (exp2 domain), one thread per q head
+        // ---- online softmax for the lane's V heads (replicated per lane)
         const uint32_t tmask = *mask_s;
-        for (int h = tid; h < Hq; h += NT) {
-            float mx = -INFINITY;
-            for (int tt = 0; tt < TT; ++tt)
-                if ((tmask >> tt) & 1u) mx = fmaxf(mx, logit_s[tt * Hq + h]);
-            const float m_new = fmaxf(m_run, mx);
-            const float alpha = (m_new == -INFINITY) ? 1.0f : exp2f(m_run - m_new);
-            float lsum = 0.f;
-            for (int tt = 0; tt < TT; ++tt) {
-                const float pr = ((tmask >> tt) & 1u) ? exp2f(logit_s[tt * Hq + h] - m_new) : 0.0f;
-                prob_s[tt * Hq + h] = pr;
-                lsum += pr;
-            }
-            l_run = l_run * alpha + lsum;
-            m_run = m_new;
-            alpha_s[h] = alpha;
+        const bool ok0 = (tmask >> tt0) & 1u, ok1 = (tmask >> (tt0 + 1)) & 1u;
+        float pr0[VH], pr1[VH];
+#pragma unroll
+        for (int v = 0; v < VH; ++v) {
+            const int i = v / REP, r = v % REP;
+            const int kvl = (lam + L * i) >> 3;
+            const int hv = kvl * REP + r;
+            const float l0 = __shfl_sync(0xffffffffu, val[0], lbase + ((2 * hv) << SH));
+            const float l1 = __shfl_sync(0xffffffffu, val[0], lbase + ((2 * hv + 1) << SH));
+            const float mx = fmaxf(ok0 ? l0 : -INFINITY, ok1 ? l1 : -INFINITY);
+            const float m_new = fmaxf(m_run[v], mx);
+            const float alpha = (m_new == -INFINITY) ? 1.0f : exp2f(m_run[v] - m_new);
+            pr0[v] = ok0 ? exp2f(l0 - m_new) : 0.0f;
+            pr1[v] = ok1 ? exp2f(l1 - m_new) : 0.0f;
+            l_run[v] = l_run[v] * alpha + pr0[v] + pr1[v];
+            m_run[v] = m_new;
+            zc[v] *= alpha;
+            const float2 a2 = make_float2(alpha, alpha);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[v][e] = mul2(acc[v][e], a2);
         }
-        __syncthreads();
 
-        // ---- V: acc += p * s * code, zero folded per token; rotated frame kept
-        if (v_owner) {
-            const float al = alpha_s[vh];
-            const float2 a2 = make_float2(al, al);
+        // ---- V: acc += 4 p s (1 + c/4); zero point and the +1 folded into zc
 #pragma unroll
-            for (int i = 0; i < 16; ++i) acc[i] = mul2(acc[i], a2);
-            zsum *= al;
-            for (int tt = 0; tt < nv; tt += 2) {
-                const float p0 = prob_s[tt * Hq + vh];
-                const float p1 = (tt + 1 < nv) ? prob_s[(tt + 1) * Hq + vh] : 0.0f;
-                if (p0 == 0.0f && p1 == 0.0f) continue;
-                const uint32_t w0 = vc[tt * W + vw];
-                const uint32_t w1 = (tt + 1 < nv) ? vc[(tt + 1) * W + vw] : 0u;
-                const uint32_t m0 = vm[tt * MG + (vw >> 3)];
-                const uint32_t m1 = (tt + 1 < nv) ? vm[(tt + 1) * MG + (vw >> 3)] : 0u;
-                const float ps0 = p0 > 0.0f ? p0 * h2f(static_cast<uint16_t>(m0 & 0xffffu)) : 0.0f;
-                const float ps1 = p1 > 0.0f ? p1 * h2f(static_cast<uint16_t>(m1 & 0xffffu)) : 0.0f;
-                if (p0 > 0.0f) zsum += ps0 * h2f(static_cast<uint16_t>(m0 >> 16));
-                if (p1 > 0.0f) zsum += ps1 * h2f(static_cast<uint16_t>(m1 >> 16));
-                const float2 ps = make_float2(ps0, ps1);
-                const float2 off = make_float2(-8388608.0f, -8388608.0f);
+        for (int i = 0; i < VW; ++i) {
+            const int gw = g * WPG + lam + L * i;
+            const uint32_t w0 = vc[tt0 * W + gw], w1 = vc[(tt0 + 1) * W + gw];
+            const uint32_t m0 = vm[tt0 * MG + (gw >> 3)], m1 = vm[(tt0 + 1) * MG + (gw >> 3)];
+            float2 xa[8], xb[8];
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const float2 c = add2(make_float2(__uint_as_float(0x4B000000u | ((w0 >> (2 * i)) & 3u)),
-                                                      __uint_as_float(0x4B000000u | ((w1 >> (2 * i)) & 3u))),
-                                          off);
-                    acc[i] = fma2(ps, c, acc[i]);
+            for (int e = 0; e < 8; ++e) {
+                const int s0 = 21 - 2 * e, s1 = 21 - 2 * (e + 8);
+                const uint32_t ca = s0 >= 0 ? (w0 << s0) : (w0 >> -s0);
+                const uint32_t cb = s1 >= 0 ? (w0 << s1) : (w0 >> -s1);
+                const uint32_t cc = s0 >= 0 ? (w1 << s0) : (w1 >> -s0);
+                const uint32_t cd = s1 >= 0 ? (w1 << s1) : (w1 >> -s1);
+                xa[e] = make_float2(__uint_as_float(and_or(ca, 0x600000u, 0x3F800000u)),
+                                    __uint_as_float(and_or(cb, 0x600000u, 0x3F800000u)));
+                xb[e] = make_float2(__uint_as_float(and_or(cc, 0x600000u, 0x3F800000u)),
+                                    __uint_as_float(and_or(cd, 0x600000u, 0x3F800000u)));
+            }
+            const float s0 = h2f(static_cast<uint16_t>(m0 & 0xffffu)), z0 = h2f(static_cast<uint16_t>(m0 >> 16));
+            const float s1 = h2f(static_cast<uint16_t>(m1 & 0xffffu)), z1 = h2f(static_cast<uint16_t>(m1 >> 16));
+#pragma unroll
+            for (int r = 0; r < REP; ++r) {
+                const int v = i * REP + r;
+                const float ps0 = pr0[v] > 0.0f ? pr0[v] * s0 : 0.0f;
+                const float ps1 = pr1[v] > 0.0f ? pr1[v] * s1 : 0.0f;
+                // garbage metadata of masked tokens never reaches the sums
+                zc[v] += (ps0 != 0.0f ? ps0 * (z0 + 4.0f) : 0.0f) + (ps1 != 0.0f ? ps1 * (z1 + 4.0f) : 0.0f);
+                const float2 f0 = make_float2(4.0f * ps0, 4.0f * ps0), f1 = make_float2(4.0f * ps1, 4.0f * ps1);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    acc[v][e] = fma2(f0, xa[e], acc[v][e]);
+                    acc[v][e] = fma2(f1, xb[e], acc[v][e]);
                 }
             }
         }
-        // next iteration's first barrier orders these reads before prob_s is rewritten
+        __syncthreads();  // knat and this stage are free for the next tile
     }
 
-    // ---- partial (m, l, o') of this split
-    for (int h = tid; h < Hq; h += NT) {
-        p.ws_ml[(ws_row + h) * 2] = m_run;
-        p.ws_ml[(ws_row + h) * 2 + 1] = l_run;
-    }
-    if (v_owner) {
-        float4* o = reinterpret_cast<float4*>(p.ws_o + (ws_row + vh) * 128 + (vw & 7) * 16);
+    // ---- this lane group's partial (m, l, o')
+    const int64_t prow = static_cast<int64_t>(b) * p.NP + static_cast<int64_t>(split) * PP + pp;
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-            o[i] = make_float4(acc[4 * i].x + acc[4 * i].y - zsum, acc[4 * i + 1].x + acc[4 * i + 1].y - zsum,
-                               acc[4 * i + 2].x + acc[4 * i + 2].y - zsum, acc[4 * i + 3].x + acc[4 * i + 3].y - zsum);
+    for (int v = 0; v < VH; ++v) {
+        const int i = v / REP, r = v % REP;
+        const int wl = lam + L * i;
+        const int h = (g * GH + (wl >> 3)) * REP + r;
+        const int64_t row = prow * Hq + h;
+        if ((wl & 7) == 0) {
+            p.ws_ml[row * 2] = m_run[v];
+            p.ws_ml[row * 2 + 1] = l_run[v];
+        }
+        float4* o = reinterpret_cast<float4*>(p.ws_o + row * 128 + (wl & 7) * 16);
+        const float z = zc[v];
+        o[0] = make_float4(acc[v][0].x - z, acc[v][1].x - z, acc[v][2].x - z, acc[v][3].x - z);
+        o[1] = make_float4(acc[v][4].x - z, acc[v][5].x - z, acc[v][6].x - z, acc[v][7].x - z);
+        o[2] = make_float4(acc[v][0].y - z, acc[v][1].y - z, acc[v][2].y - z, acc[v][3].y - z);
+        o[3] = make_float4(acc[v][4].y - z, acc[v][5].y - z, acc[v][6].y - z, acc[v][7].y - z);
     }
 }
 
-// Sink partial (split index S): raw fp16 K/V rows of the sidecar, natural
-// frame, RoPE at each sink's own position.  One CTA per sequence, thread = d.
-__global__ void __launch_bounds__(128) decode_sinks_kernel(DecodeParams p, int max_sinks) {
-    const int b = blockIdx.x, d = threadIdx.x, Hq = p.Hq, C = p.C;
-    const int rep = p.Hq / p.Hkv;
+// Merge the NP packed partials of (b, h) (rotated V frame) in a fixed order,
+// add the sink tokens' raw fp16 rows (natural frame, RoPE at their own
+// position, kept exact like the reference's sidecar), then
+// out = (H_128 o'_rot + o_sink) / l.  One CTA per (h, b), thread = channel d.
+__global__ void __launch_bounds__(128) decode_combine_kernel(DecodeParams p) {
+    const int h = blockIdx.x, b = blockIdx.y, d = threadIdx.x, Hq = p.Hq, C = p.C;
+    const int64_t base = static_cast<int64_t>(b) * p.NP * Hq;
     const int64_t T = p.seq_len[b];
-    const int64_t ws_row = (static_cast<int64_t>(b) * (p.S + 1) + p.S) * Hq;
+    __shared__ float buf[128];
     __shared__ float red[4];
-    const int nsink = min(p.cache.sink_count[b], max_sinks);
-    const float2* cq = p.rope + (T - 1) * 64;
+    __shared__ float slog[16];
+    const int nsink = min(min(p.cache.sink_count[b], p.max_sinks), 16);
     const int f = d & 63;
-    for (int h = 0; h < Hq; ++h) {
+    const int kvh = h / (p.Hq / p.Hkv);
+    float qd;
+    {
         const uint16_t* qh = p.q + (static_cast<int64_t>(b) * Hq + h) * 128;
         const float a = h2f(qh[f]), bb = h2f(qh[f + 64]);
-        const float2 r = __ldg(cq + f);
-        const float qd = (d < 64 ? (a * r.x - bb * r.y) : (a * r.y + bb * r.x)) * p.qscale;
-        const int kvh = h / rep;
-        float m = -INFINITY, l = 0.f, o = 0.f;
-        for (int s = 0; s < nsink; ++s) {
-            const int pos = p.cache.sink_pos[b * max_sinks + s];
-            if (pos >= T) continue;
-            const uint16_t* kr = p.cache.sink_k + (static_cast<int64_t>(b) * max_sinks + s) * C + kvh * 128;
-            const uint16_t* vr = p.cache.sink_v + (static_cast<int64_t>(b) * max_sinks + s) * C + kvh * 128;
-            const float ka = h2f(kr[f]), kb = h2f(kr[f + 64]);
-            const float2 rk = __ldg(p.rope + static_cast<int64_t>(pos) * 64 + f);
-            const float kd = d < 64 ? (ka * rk.x - kb * rk.y) : (ka * rk.y + kb * rk.x);
-            float prod = qd * kd;
-#pragma unroll
-            for (int o2 = 16; o2 >= 1; o2 >>= 1) prod += __shfl_xor_sync(0xffffffffu, prod, o2);
-            __syncthreads();
-            if ((d & 31) == 0) red[d >> 5] = prod;
-            __syncthreads();
-            const float lg = red[0] + red[1] + red[2] + red[3];
-            const float m_new = fmaxf(m, lg);
-            const float al = exp2f(m - m_new), pr = exp2f(lg - m_new);
-            l = l * al + pr;
-            o = o * al + pr * h2f(vr[d]);
-            m = m_new;
-        }
-        if (d == 0) {
-            p.ws_ml[(ws_row + h) * 2] = m;
-            p.ws_ml[(ws_row + h) * 2 + 1] = l;
-        }
-        p.ws_o[(ws_row + h) * 128 + d] = o;
+        const float2 r = rope_at(p.rope, T - 1, f);
+        qd = (d < 64 ? (a * r.x - bb * r.y) : (a * r.y + bb * r.x)) * p.qscale;
     }
-}
-
-// Merge S packed partials (rotated V frame) and the sink partial (natural
-// frame) in a fixed order; out = (H_128 o'_rot + o_sink) / l.
-__global__ void __launch_bounds__(128) decode_combine_kernel(DecodeParams p) {
-    const int h = blockIdx.x, b = blockIdx.y, d = threadIdx.x, Hq = p.Hq;
-    const int64_t base = static_cast<int64_t>(b) * (p.S + 1) * Hq;
-    __shared__ float buf[128];
+    for (int s = 0; s < nsink; ++s) {  // sink logits (log2 domain)
+        const int pos = p.cache.sink_pos[b * p.max_sinks + s];
+        const uint16_t* kr = p.cache.sink_k + (static_cast<int64_t>(b) * p.max_sinks + s) * C + kvh * 128;
+        const float ka = h2f(kr[f]), kb = h2f(kr[f + 64]);
+        const float2 rk = rope_at(p.rope, pos, f);
+        float prod = qd * (d < 64 ? (ka * rk.x - kb * rk.y) : (ka * rk.y + kb * rk.x));
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) prod += __shfl_xor_sync(0xffffffffu, prod, o);
+        if ((d & 31) == 0) red[d >> 5] = prod;
+        __syncthreads();
+        if (d == 0) slog[s] = (pos < T) ? (red[0] + red[1] + red[2] + red[3]) : -INFINITY;
+        __syncthreads();
+    }
     float M = -INFINITY;
-    for (int s = 0; s <= p.S; ++s) M = fmaxf(M, p.ws_ml[((base + static_cast<int64_t>(s) * Hq) + h) * 2]);
-    float L = 0.f, rot = 0.f, raw = 0.f;
-    for (int s = 0; s <= p.S; ++s) {
+    for (int s = 0; s < p.NP; ++s) M = fmaxf(M, p.ws_ml[(base + static_cast<int64_t>(s) * Hq + h) * 2]);
+    for (int s = 0; s < nsink; ++s) M = fmaxf(M, slog[s]);
+    float Lsum = 0.f, rot = 0.f, raw = 0.f;
+    for (int s = 0; s < p.NP; ++s) {
         const int64_t r = base + static_cast<int64_t>(s) * Hq + h;
         const float ms = p.ws_ml[r * 2];
         if (ms == -INFINITY) continue;
         const float e = exp2f(ms - M);
-        L += e * p.ws_ml[r * 2 + 1];
-        const float ov = p.ws_o[r * 128 + d];
-        if (s < p.S) rot += e * ov; else raw += e * ov;
+        Lsum += e * p.ws_ml[r * 2 + 1];
+        rot += e * p.ws_o[r * 128 + d];
+    }
+    for (int s = 0; s < nsink; ++s) {
+        if (slog[s] == -INFINITY) continue;
+        const float e = exp2f(slog[s] - M);
+        Lsum += e;
+        raw += e * h2f(p.cache.sink_v[(static_cast<int64_t>(b) * p.max_sinks + s) * C + kvh * 128 + d]);
     }
     // H_128 on the rotated-frame accumulator (value_rotation inverse)
     buf[d] = rot;
@@ -467,17 +503,21 @@ __global__ void __launch_bounds__(128) decode_combine_kernel(DecodeParams p) {
         __syncthreads();
     }
     const float hv = buf[d] * (1.0f / sqrtf(128.0f));
-    p.out[(static_cast<int64_t>(b) * Hq + h) * 128 + d] = (hv + raw) / L;
+    p.out[(static_cast<int64_t>(b) * Hq + h) * 128 + d] = (hv + raw) / Lsum;
 }
 
-__global__ void rope_table_kernel(float2* table, int64_t max_pos, double base) {
+// table[pos/2][f] = (cos(p0 th_f), cos(p1 th_f), sin(p0 th_f), sin(p1 th_f)),
+// p0 = pos & ~1, p1 = p0 + 1: a token pair's rotation is one LDS.128.
+__global__ void rope_table_kernel(float4* table, int64_t npairs, double base) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= max_pos * 64) return;
-    const int64_t pos = i / 64;
+    if (i >= npairs * 64) return;
+    const int64_t pr = i / 64;
     const int f = static_cast<int>(i % 64);
     const double theta = pow(base, -2.0 * static_cast<double>(f) / 128.0);  // proj/src/rope.cpp:17-24
-    const double ang = 1.0 * static_cast<double>(pos) * theta;              // dir * pos * theta
-    table[i] = make_float2(static_cast<float>(cos(ang)), static_cast<float>(sin(ang)));
+    const double a0 = 1.0 * static_cast<double>(2 * pr) * theta;            // dir * pos * theta
+    const double a1 = 1.0 * static_cast<double>(2 * pr + 1) * theta;
+    table[i] = make_float4(static_cast<float>(cos(a0)), static_cast<float>(cos(a1)), static_cast<float>(sin(a0)),
+                           static_cast<float>(sin(a1)));
 }
 
 template <int N, int L>
@@ -502,28 +542,14 @@ __global__ void rotate_keys_kernel(const uint16_t* __restrict__ k, int64_t rows,
 }
 
 template <int N, int REP>
-cudaError_t launch_decode_nr(const DecodePlan& plan, const DecodeParams& p, int B, int max_sinks,
-                             cudaStream_t s) {
+cudaError_t launch_decode_nr(const DecodePlan& plan, const DecodeParams& p, int B, cudaStream_t s) {
     auto kern = decode_split_kernel<N, REP>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(plan.smem));
     if (e != cudaSuccess) return e;
     kern<<<dim3(plan.S, B), plan.NT, plan.smem, s>>>(p);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    decode_sinks_kernel<<<B, 128, 0, s>>>(p, max_sinks);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
     decode_combine_kernel<<<dim3(p.Hq, B), 128, 0, s>>>(p);
     return cudaGetLastError();
-}
-
-template <int N>
-cudaError_t launch_decode_n(const DecodePlan& plan, const DecodeParams& p, int B, int max_sinks, cudaStream_t s) {
-    switch (plan.REP) {
-        case 1: return launch_decode_nr<N, 1>(plan, p, B, max_sinks, s);
-        case 2: return launch_decode_nr<N, 2>(plan, p, B, max_sinks, s);
-        case 4: return launch_decode_nr<N, 4>(plan, p, B, max_sinks, s);
-        case 8: return launch_decode_nr<N, 8>(plan, p, B, max_sinks, s);
-        default: return cudaErrorInvalidValue;
-    }
 }
 
 }  // namespace
@@ -538,6 +564,15 @@ int num_sms() {
     return n;
 }
 
+bool decode_supported(int N, int REP) {
+    switch (N) {
+        case 512: return REP == 1 || REP == 2;
+        case 256: return REP == 1 || REP == 2 || REP == 4;
+        case 128: return REP == 1 || REP == 2 || REP == 4;
+        default: return false;
+    }
+}
+
 DecodePlan plan_decode(const rkv_layer_desc& d, int64_t max_seq_len) {
     DecodePlan pl{};
     const int C = d.num_kv_heads * d.head_dim;
@@ -545,39 +580,47 @@ DecodePlan plan_decode(const rkv_layer_desc& d, int64_t max_seq_len) {
     pl.REP = d.num_q_heads / d.num_kv_heads;
     const int L = pl.N >= 256 ? 16 : 8;
     const int NG = C / pl.N;
-    // enough lane groups for >= 256 threads and >= one V owner per (word, q head)
-    int P = 1;
-    while (NG * P * L < 256 || NG * P * L < d.num_q_heads * 8) ++P;
+    const int max_nt = pl.N == 512 ? 320 : 256;
+    int P = max_nt / (NG * L);
+    if (P > 4) P = 4;
+    if (P < 1) P = 1;
     pl.P = P;
     pl.TT = 2 * P;
     pl.NT = NG * P * L;
     pl.smem = smem_layout(C, d.num_q_heads, pl.TT).total;
     if (max_seq_len <= 0 || max_seq_len > d.max_tokens) max_seq_len = d.max_tokens;
-    const int ctas = num_sms();  // one CTA per SM (shared memory bound)
+    const int ctas = num_sms();  // one CTA per SM (shared-memory bound)
     int S = ctas / d.batch;
     if (S < 1) S = 1;
-    // keep >= 4 tiles per split
-    const int64_t max_split = (max_seq_len + 4 * pl.TT - 1) / (4 * pl.TT);
+    const int64_t max_split = (max_seq_len + 4 * pl.TT - 1) / (4 * pl.TT);  // >= 4 tiles per split
     if (S > max_split) S = static_cast<int>(max_split > 0 ? max_split : 1);
     int64_t chunk = (max_seq_len + S - 1) / S;
     chunk = (chunk + pl.TT - 1) / pl.TT * pl.TT;
     pl.chunk = static_cast<int>(chunk);
     pl.S = static_cast<int>((max_seq_len + chunk - 1) / chunk);
+    pl.NP = pl.S * P;
     return pl;
 }
 
 cudaError_t launch_decode(const rkv_layer_desc& d, const DecodePlan& plan, const DecodeParams& p, cudaStream_t s) {
-    switch (plan.N) {
-        case 128: return launch_decode_n<128>(plan, p, d.batch, d.max_sinks, s);
-        case 256: return launch_decode_n<256>(plan, p, d.batch, d.max_sinks, s);
-        case 512: return launch_decode_n<512>(plan, p, d.batch, d.max_sinks, s);
+    const int B = d.batch;
+    switch (plan.N * 16 + plan.REP) {
+        case 512 * 16 + 1: return launch_decode_nr<512, 1>(plan, p, B, s);
+        case 512 * 16 + 2: return launch_decode_nr<512, 2>(plan, p, B, s);
+        case 256 * 16 + 1: return launch_decode_nr<256, 1>(plan, p, B, s);
+        case 256 * 16 + 2: return launch_decode_nr<256, 2>(plan, p, B, s);
+        case 256 * 16 + 4: return launch_decode_nr<256, 4>(plan, p, B, s);
+        case 128 * 16 + 1: return launch_decode_nr<128, 1>(plan, p, B, s);
+        case 128 * 16 + 2: return launch_decode_nr<128, 2>(plan, p, B, s);
+        case 128 * 16 + 4: return launch_decode_nr<128, 4>(plan, p, B, s);
         default: return cudaErrorInvalidValue;
     }
 }
 
-cudaError_t launch_rope_table(const rkv_layer_desc& d, float2* table, int64_t max_pos, cudaStream_t s) {
-    const int64_t n = max_pos * 64;
-    rope_table_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(table, max_pos, d.rope_base);
+cudaError_t launch_rope_table(const rkv_layer_desc& d, float4* table, int64_t max_pos, cudaStream_t s) {
+    const int64_t npairs = (max_pos + 1) / 2;
+    const int64_t n = npairs * 64;
+    rope_table_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(table, npairs, d.rope_base);
     return cudaGetLastError();
 }
 

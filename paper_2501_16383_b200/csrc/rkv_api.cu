@@ -78,8 +78,10 @@ rkv_status validate(const rkv_layer_desc* d) {
     if (n != 128 && n != 256 && n != 512)
         return fail(RKV_ERR_INVALID_ARGUMENT, "the sm_100a kernels need heads_per_group*head_dim in {128,256,512}");
     const int rep = d->num_q_heads / d->num_kv_heads;
-    if (rep != 1 && rep != 2 && rep != 4 && rep != 8)
-        return fail(RKV_ERR_INVALID_ARGUMENT, "q heads per kv head must be 1, 2, 4 or 8");
+    if (!rkv::decode_supported(static_cast<int>(n), rep))
+        return fail(RKV_ERR_INVALID_ARGUMENT,
+                    "unsupported (heads_per_group, q heads per kv head): the sm_100a decode kernel takes "
+                    "G=4 with Hq/Hkv in {1,2}, G in {1,2} with Hq/Hkv in {1,2,4}");
     const int64_t C = static_cast<int64_t>(d->num_kv_heads) * d->head_dim;
     if (C % 512 != 0) return fail(RKV_ERR_INVALID_ARGUMENT, "num_kv_heads*head_dim must be a multiple of 512");
     if (C > 32768) return fail(RKV_ERR_INVALID_ARGUMENT, "num_kv_heads*head_dim must be <= 32768");
@@ -144,14 +146,14 @@ rkv_status rkv_cache_reset(const rkv_layer_desc* desc, const rkv_cache* cache, v
 
 size_t rkv_rope_table_bytes(const rkv_layer_desc* desc, int64_t max_pos) {
     if (validate(desc) != RKV_OK || max_pos < 1) return 0;
-    return static_cast<size_t>(max_pos) * (desc->head_dim / 2) * 2 * sizeof(float);
+    return static_cast<size_t>((max_pos + 1) / 2) * (desc->head_dim / 2) * 4 * sizeof(float);
 }
 
 rkv_status rkv_rope_table_init(const rkv_layer_desc* desc, float* table, int64_t max_pos, void* stream) {
     rkv_status st = validate(desc);
     if (st != RKV_OK) return st;
     if (!table || max_pos < 1) return fail(RKV_ERR_INVALID_ARGUMENT, "rope_table_init: null table or max_pos < 1");
-    cudaError_t e = rkv::launch_rope_table(*desc, reinterpret_cast<float2*>(table), max_pos,
+    cudaError_t e = rkv::launch_rope_table(*desc, reinterpret_cast<float4*>(table), max_pos,
                                            static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "rope_table_init");
     return RKV_OK;
@@ -192,7 +194,7 @@ rkv_status rkv_quantize_kv(const rkv_layer_desc* desc, const uint16_t* k_new, co
 size_t rkv_decode_workspace_bytes(const rkv_layer_desc* desc, int64_t max_seq_len) {
     if (validate(desc) != RKV_OK) return 0;
     rkv::DecodePlan pl = rkv::plan_decode(*desc, max_seq_len);
-    const size_t rows = static_cast<size_t>(desc->batch) * (pl.S + 1) * desc->num_q_heads;
+    const size_t rows = static_cast<size_t>(desc->batch) * pl.NP * desc->num_q_heads;
     return al256(rows * 2 * sizeof(float)) + al256(rows * 128 * sizeof(float));
 }
 
@@ -211,14 +213,14 @@ rkv_status rkv_decode_attention(const rkv_layer_desc* desc, const uint16_t* q, c
     if (ws_bytes < rkv_decode_workspace_bytes(desc, max_seq_len))
         return fail(RKV_ERR_INVALID_ARGUMENT, "decode_attention: workspace too small");
     rkv::DecodePlan pl = rkv::plan_decode(*desc, max_seq_len);
-    if (pl.NT > 320 || pl.smem > 227 * 1024)
+    if (pl.NT > (pl.N == 512 ? 320 : 256) || pl.smem > 227 * 1024)
         return fail(RKV_ERR_INVALID_ARGUMENT, "decode_attention: layer shape exceeds the sm_100a kernel's tile budget");
-    const size_t rows = static_cast<size_t>(desc->batch) * (pl.S + 1) * desc->num_q_heads;
+    const size_t rows = static_cast<size_t>(desc->batch) * pl.NP * desc->num_q_heads;
     rkv::DecodeParams p{};
     p.q = q;
     p.seq_len = seq_len;
     p.perm = perm;
-    p.rope = reinterpret_cast<const float2*>(rope_table);
+    p.rope = reinterpret_cast<const float4*>(rope_table);
     p.cache = *cache;
     p.ws_ml = static_cast<float*>(workspace);
     p.ws_o = reinterpret_cast<float*>(static_cast<char*>(workspace) + al256(rows * 2 * sizeof(float)));
@@ -229,6 +231,8 @@ rkv_status rkv_decode_attention(const rkv_layer_desc* desc, const uint16_t* q, c
     p.Hkv = desc->num_kv_heads;
     p.C = desc->num_kv_heads * desc->head_dim;
     p.S = pl.S;
+    p.NP = pl.NP;
+    p.max_sinks = desc->max_sinks;
     p.chunk = pl.chunk;
     p.P = pl.P;
     p.k_norm = 1.0f / std::sqrt(static_cast<float>(desc->heads_per_group * desc->head_dim));

@@ -31,17 +31,19 @@ struct DecodeParams {
     const uint16_t* q;
     const int64_t* seq_len;
     const int32_t* perm;
-    const float2* rope;  // [max_pos][64]
+    const float4* rope;  // [max_pos/2][64] (cos p0, cos p1, sin p0, sin p1)
     rkv_cache cache;
-    float* ws_ml;  // [B][S+1][Hq][2]
-    float* ws_o;   // [B][S+1][Hq][128]
+    float* ws_ml;  // [B][NP][Hq][2]   partial (m, l) per lane-group partition
+    float* ws_o;   // [B][NP][Hq][128] partial o' (rotated V frame)
     float* out;    // [B][Hq][128]
     int64_t max_tokens;
     int B, Hq, Hkv, C;
-    int S;      // packed splits (the sink partial is split index S)
+    int S;      // splits (CTAs per sequence)
+    int NP;     // partial rows per sequence = S * P
     int chunk;  // tokens per split, multiple of the tile
-    int P;      // token pairs per tile
-    float k_norm;
+    int P;      // token pairs per tile (= lane-group partitions per FWHT group)
+    int max_sinks;
+    float k_norm;  // 1/sqrt(G*d), folded into q
     float qscale;  // log2(e) / sqrt(d)
 };
 
@@ -49,13 +51,14 @@ struct DecodeParams {
 cudaError_t launch_quantize(const rkv_layer_desc& d, const QuantParams& p, cudaStream_t s);
 // decode_attention.cu
 struct DecodePlan {
-    int N, REP, P, TT, NT, S, chunk;
+    int N, REP, P, TT, NT, S, NP, chunk;
     size_t smem;
 };
+bool decode_supported(int N, int REP);
 DecodePlan plan_decode(const rkv_layer_desc& d, int64_t max_seq_len);
 cudaError_t launch_decode(const rkv_layer_desc& d, const DecodePlan& plan, const DecodeParams& p,
                           cudaStream_t s);
-cudaError_t launch_rope_table(const rkv_layer_desc& d, float2* table, int64_t max_pos, cudaStream_t s);
+cudaError_t launch_rope_table(const rkv_layer_desc& d, float4* table, int64_t max_pos, cudaStream_t s);
 cudaError_t launch_rotate_keys(const rkv_layer_desc& d, const uint16_t* k, int64_t rows, float* out,
                                cudaStream_t s);
 int num_sms();

@@ -279,7 +279,7 @@ class RotateKVLayer:
             f = torch.as_tensor(sink_flags).to(torch.uint8)
             if tuple(f.shape) != (B, n):
                 raise ValueError("sink flags must be [batch, new tokens]")
-            add = f.cpu().numpy().sum(axis=1)
+            add = f.cpu().numpy().astype(np.int64).sum(axis=1)
             if np.any(self.sink_counts + add > self.cfg.max_sinks):
                 raise IndexError("cache: sink sidecar capacity exceeded")
             self.sink_counts += add
