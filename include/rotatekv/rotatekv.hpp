@@ -1,0 +1,188 @@
+// rotatekv.hpp -- C++ host API over the C ABI (rotatekv.h), mirroring the
+// reference's hot-path API (namespace rotatekv, /root/reference/proj/include/
+// rotatekv/{reorder,kv_cache,pipeline}.hpp) so a reference caller switches by
+// changing the namespace and handing device pointers.  Header-only; link
+// against paper_2501_16383_b200/_lib/librotatekv_b200.so and cudart.
+//
+//   reference                                   rotatekv_b200
+//   ------------------------------------------  -----------------------------------------
+//   ReorderPlan calibrate_reorder(layers)        ReorderPlan calibrate_reorder(layers, C, stat)
+//   LayerKVCache(cfg, C); append(k, v, sink)     DeviceLayerCache(desc, perm); append(...)
+//   LayerKVCache::size()/is_sink()               DeviceLayerCache::size(b)/sink_count(b)
+//   decode_step(...) attention half              DeviceLayerCache::decode_attention(q, out)
+//
+// Exceptions are the reference's: std::invalid_argument, std::out_of_range,
+// std::runtime_error (CUDA failures included).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "rotatekv/rotatekv.h"
+
+namespace rotatekv_b200 {
+
+inline void check(rkv_status s) {
+    switch (s) {
+        case RKV_OK: return;
+        case RKV_ERR_INVALID_ARGUMENT: throw std::invalid_argument(rkv_last_error());
+        case RKV_ERR_OUT_OF_RANGE: throw std::out_of_range(rkv_last_error());
+        default: throw std::runtime_error(rkv_last_error());
+    }
+}
+
+inline void check_cuda(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// proj/include/rotatekv/reorder.hpp:14-28
+struct ReorderPlan {
+    std::vector<std::vector<int32_t>> perm;     // perm[l][j] = source channel of slot j
+    std::vector<std::vector<int32_t>> inverse;  // inverse[l][perm[l][j]] == j
+    int64_t layers() const { return static_cast<int64_t>(perm.size()); }
+    int64_t channels() const { return perm.empty() ? 0 : static_cast<int64_t>(perm[0].size()); }
+};
+
+// calibrate_reorder (proj/src/reorder.cpp:91-110): one [rows x channels]
+// row-major fp32 tensor of ROTATED keys per layer.
+inline ReorderPlan calibrate_reorder(const std::vector<std::vector<float>>& rotated_keys_per_layer,
+                                     int64_t channels, rkv_calib_stat stat = RKV_STAT_SUM) {
+    if (rotated_keys_per_layer.empty()) throw std::invalid_argument("calibrate_reorder: empty calibration set");
+    ReorderPlan plan;
+    for (const auto& layer : rotated_keys_per_layer) {
+        if (channels < 1 || layer.size() % static_cast<size_t>(channels) != 0)
+            throw std::invalid_argument("calibrate_reorder: rows must be [tokens, channels]");
+        std::vector<int32_t> p(static_cast<size_t>(channels)), inv(static_cast<size_t>(channels));
+        check(rkv_calibrate_reorder(layer.data(), static_cast<int64_t>(layer.size()) / channels, channels, stat,
+                                    p.data(), inv.data()));
+        plan.perm.push_back(std::move(p));
+        plan.inverse.push_back(std::move(inv));
+    }
+    return plan;
+}
+
+// apply_reorder (proj/src/reorder.cpp:112-128) on host rows.
+inline std::vector<float> apply_reorder(const std::vector<float>& x, const ReorderPlan& plan, int64_t layer,
+                                        bool inverse) {
+    if (layer < 0 || layer >= plan.layers()) throw std::invalid_argument("apply_reorder: layer out of range");
+    const auto& p = inverse ? plan.inverse[static_cast<size_t>(layer)] : plan.perm[static_cast<size_t>(layer)];
+    const size_t c = p.size();
+    if (c == 0 || x.size() % c != 0) throw std::invalid_argument("apply_reorder: trailing dimension mismatch");
+    std::vector<float> out(x.size());
+    for (size_t r = 0; r < x.size() / c; ++r)
+        for (size_t j = 0; j < c; ++j) out[r * c + j] = x[r * c + static_cast<size_t>(p[j])];
+    return out;
+}
+
+// One layer's 2-bit rotated KV cache on the device (LayerKVCache,
+// proj/include/rotatekv/kv_cache.hpp:13-50, for a batch of sequences).
+class DeviceLayerCache {
+public:
+    DeviceLayerCache(const rkv_layer_desc& desc, const std::vector<int32_t>& perm, cudaStream_t stream = nullptr)
+        : desc_(desc), stream_(stream), len_(static_cast<size_t>(desc.batch), 0),
+          sinks_(static_cast<size_t>(desc.batch), 0) {
+        check(rkv_layer_validate(&desc_));
+        const size_t c = static_cast<size_t>(desc.num_kv_heads) * desc.head_dim;
+        if (perm.size() != c) throw std::invalid_argument("reorder plan: wrong channel count in layer line");
+        bytes_ = rkv_cache_bytes(&desc_);
+        check_cuda(cudaMalloc(&base_, bytes_), "cudaMalloc cache");
+        check(rkv_cache_carve(&desc_, base_, bytes_, &cache_));
+        check_cuda(cudaMalloc(&perm_, c * sizeof(int32_t)), "cudaMalloc perm");
+        check_cuda(cudaMemcpyAsync(perm_, perm.data(), c * sizeof(int32_t), cudaMemcpyHostToDevice, stream_), "perm");
+        rope_bytes_ = rkv_rope_table_bytes(&desc_, desc.max_tokens);
+        check_cuda(cudaMalloc(&rope_, rope_bytes_), "cudaMalloc rope");
+        check(rkv_rope_table_init(&desc_, static_cast<float*>(rope_), desc.max_tokens, stream_));
+        ws_bytes_ = rkv_decode_workspace_bytes(&desc_, desc.max_tokens);
+        check_cuda(cudaMalloc(&ws_, ws_bytes_), "cudaMalloc workspace");
+        check_cuda(cudaMalloc(&dev_pos_, static_cast<size_t>(desc.batch) * sizeof(int64_t)), "cudaMalloc pos");
+        check(rkv_cache_reset(&desc_, &cache_, stream_));
+    }
+    DeviceLayerCache(const DeviceLayerCache&) = delete;
+    DeviceLayerCache& operator=(const DeviceLayerCache&) = delete;
+    ~DeviceLayerCache() {
+        cudaFree(base_);
+        cudaFree(perm_);
+        cudaFree(rope_);
+        cudaFree(ws_);
+        cudaFree(dev_pos_);
+    }
+
+    int64_t size(int b) const { return len_.at(static_cast<size_t>(b)); }
+    int64_t sink_count(int b) const { return sinks_.at(static_cast<size_t>(b)); }
+    const rkv_cache& view() const { return cache_; }
+    const rkv_layer_desc& desc() const { return desc_; }
+
+    // LayerKVCache::append for num_new tokens of every sequence.
+    // k_new/v_new: device [B][num_new][C] fp16; sink_flags_host: [B][num_new] or empty.
+    void append(const uint16_t* k_new, const uint16_t* v_new, int64_t num_new,
+                const std::vector<uint8_t>& sink_flags_host = {}) {
+        const int B = desc_.batch;
+        for (int b = 0; b < B; ++b)
+            if (len_[static_cast<size_t>(b)] + num_new > desc_.max_tokens)
+                throw std::out_of_range("cache: token index out of range");
+        uint8_t* dflags = nullptr;
+        if (!sink_flags_host.empty()) {
+            if (sink_flags_host.size() != static_cast<size_t>(B) * static_cast<size_t>(num_new))
+                throw std::invalid_argument("sink flags must be [batch, new tokens]");
+            for (int b = 0; b < B; ++b) {
+                int64_t add = 0;
+                for (int64_t i = 0; i < num_new; ++i) add += sink_flags_host[static_cast<size_t>(b * num_new + i)] != 0;
+                if (sinks_[static_cast<size_t>(b)] + add > desc_.max_sinks)
+                    throw std::out_of_range("cache: sink sidecar capacity exceeded");
+            }
+            check_cuda(cudaMalloc(&dflags, sink_flags_host.size()), "cudaMalloc flags");
+            check_cuda(cudaMemcpyAsync(dflags, sink_flags_host.data(), sink_flags_host.size(), cudaMemcpyHostToDevice,
+                                       stream_), "flags");
+        }
+        check_cuda(cudaMemcpyAsync(dev_pos_, len_.data(), static_cast<size_t>(B) * sizeof(int64_t),
+                                   cudaMemcpyHostToDevice, stream_), "positions");
+        rkv_status st = rkv_quantize_kv(&desc_, k_new, v_new, perm_, dflags, dev_pos_, num_new, &cache_, stream_);
+        if (dflags) {
+            cudaStreamSynchronize(stream_);
+            cudaFree(dflags);
+        }
+        check(st);
+        for (int b = 0; b < B; ++b) {
+            len_[static_cast<size_t>(b)] += num_new;
+            if (!sink_flags_host.empty())
+                for (int64_t i = 0; i < num_new; ++i)
+                    sinks_[static_cast<size_t>(b)] += sink_flags_host[static_cast<size_t>(b * num_new + i)] != 0;
+        }
+        check_cuda(cudaStreamSynchronize(stream_), "append");  // dev_pos_ is reused by the next call
+    }
+
+    // The attention half of decode_step (proj/src/pipeline.cpp:211-261): q
+    // [B][Hq][d] fp16 device (pre-RoPE, position = size-1), out [B][Hq][d] fp32.
+    void decode_attention(const uint16_t* q, float* out) {
+        int64_t mx = 0;
+        for (int64_t l : len_) {
+            if (l < 1) throw std::invalid_argument("decode_step: position must equal current cache length");
+            mx = l > mx ? l : mx;
+        }
+        check_cuda(cudaMemcpyAsync(dev_pos_, len_.data(), len_.size() * sizeof(int64_t), cudaMemcpyHostToDevice,
+                                   stream_), "seq_len");
+        check(rkv_decode_attention(&desc_, q, dev_pos_, mx, &cache_, perm_, static_cast<const float*>(rope_), out, ws_,
+                                   ws_bytes_, stream_));
+        check_cuda(cudaStreamSynchronize(stream_), "decode");
+    }
+
+private:
+    rkv_layer_desc desc_;
+    cudaStream_t stream_;
+    std::vector<int64_t> len_, sinks_;
+    void* base_ = nullptr;
+    size_t bytes_ = 0;
+    rkv_cache cache_{};
+    int32_t* perm_ = nullptr;
+    void* rope_ = nullptr;
+    size_t rope_bytes_ = 0;
+    void* ws_ = nullptr;
+    size_t ws_bytes_ = 0;
+    int64_t* dev_pos_ = nullptr;
+};
+
+}  // namespace rotatekv_b200

@@ -146,3 +146,10 @@ def test_null_and_size_errors(lib):
     assert lib.rkv_decode_attention(C.byref(d), None, None, 0, C.byref(view), None, None, None, None, 0, None) \
         == R.RKV_ERR_INVALID_ARGUMENT
     assert b"null" in lib.rkv_last_error()
+
+
+def test_cpp_api_program_compiles(tmp_path, lib):
+    """include/rotatekv/rotatekv.hpp + the C ABI link into a C++ program."""
+    from tests._cpp import build_cpp_test
+
+    assert os.path.exists(build_cpp_test(str(tmp_path)))

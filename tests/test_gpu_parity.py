@@ -324,3 +324,15 @@ def test_errors_mirror_reference_exceptions():
         layer.append(k[:, :2], v[:, :2], two)
     with pytest.raises(ValueError):  # position must equal current cache length
         layer.decode(WL.make_q(w, 1, 1))
+
+
+def test_cpp_api_program(tmp_path):
+    """The C++ API (rotatekv.hpp) end to end: parity + exception classes."""
+    import subprocess
+
+    from tests._cpp import build_cpp_test
+
+    exe = build_cpp_test(str(tmp_path))
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
