@@ -122,6 +122,19 @@ rkv_status rkv_quantize_kv(const rkv_layer_desc* desc, const uint16_t* k_new, co
                            const int32_t* perm, const uint8_t* sink_flags, const int64_t* start_pos,
                            int64_t num_new, const rkv_cache* cache, void* stream);
 
+/* Per-layer decode plan (once per layer, after calibration): from the HOST
+ * permutation perm [C] (slot j <- channel perm[j]) choose which packed word
+ * each decode thread un-reorders so the shared-memory scatter's bank
+ * conflicts are minimal, and upload word indices + scatter offsets to
+ * `plan_dev` (>= rkv_layer_plan_bytes).  rkv_layer_plan_build writes the same
+ * words to host memory and reports the schedule cost (sum over half-warps and
+ * rounds of the worst bank-slot multiplicity; 16 per half-warp is ideal). */
+size_t rkv_layer_plan_bytes(const rkv_layer_desc* desc);
+rkv_status rkv_layer_plan_build(const rkv_layer_desc* desc, const int32_t* perm, uint32_t* plan_host,
+                                size_t bytes, int32_t* cost_out);
+rkv_status rkv_layer_plan_init(const rkv_layer_desc* desc, const int32_t* perm, void* plan_dev, size_t bytes,
+                               void* stream);
+
 /* Split-K decode attention over the 2-bit cache (replaces the attention half
  * of decode_step: reconstruct_cache + prepare_queries + the per-head loop,
  * proj/src/pipeline.cpp:133-152,211-261).
@@ -129,14 +142,14 @@ rkv_status rkv_quantize_kv(const rkv_layer_desc* desc, const uint16_t* k_new, co
  *              (decode_step appends the token before attending, pipeline.cpp:197-211)
  *   seq_len  : [B] int64 device, tokens 0..seq_len[b]-1 are attended (>= 1)
  *   max_seq_len : host upper bound of seq_len (0 = desc->max_tokens)
- *   perm     : [C] int32 layer permutation (the same array rkv_quantize_kv took);
- *              un-reordering scatters slot j back to channel perm[j]
+ *   layer_plan : from rkv_layer_plan_init for the layer's permutation
+ *              (un-reordering scatters slot j back to channel perm[j])
  *   rope_table : from rkv_rope_table_init with max_pos >= max_seq_len
  *   out      : [B][Hq][d] fp32, V's rotation undone (what W_o_f absorbs, pipeline.cpp:97)
  *   workspace: >= rkv_decode_workspace_bytes(desc, max_seq_len) bytes of device memory */
 size_t rkv_decode_workspace_bytes(const rkv_layer_desc* desc, int64_t max_seq_len);
 rkv_status rkv_decode_attention(const rkv_layer_desc* desc, const uint16_t* q, const int64_t* seq_len,
-                                int64_t max_seq_len, const rkv_cache* cache, const int32_t* perm,
+                                int64_t max_seq_len, const rkv_cache* cache, const void* layer_plan,
                                 const float* rope_table, float* out, void* workspace, size_t ws_bytes,
                                 void* stream);
 

@@ -96,6 +96,9 @@ public:
         rope_bytes_ = rkv_rope_table_bytes(&desc_, desc.max_tokens);
         check_cuda(cudaMalloc(&rope_, rope_bytes_), "cudaMalloc rope");
         check(rkv_rope_table_init(&desc_, static_cast<float*>(rope_), desc.max_tokens, stream_));
+        plan_bytes_ = rkv_layer_plan_bytes(&desc_);
+        check_cuda(cudaMalloc(&plan_, plan_bytes_), "cudaMalloc plan");
+        check(rkv_layer_plan_init(&desc_, perm.data(), plan_, plan_bytes_, stream_));
         ws_bytes_ = rkv_decode_workspace_bytes(&desc_, desc.max_tokens);
         check_cuda(cudaMalloc(&ws_, ws_bytes_), "cudaMalloc workspace");
         check_cuda(cudaMalloc(&dev_pos_, static_cast<size_t>(desc.batch) * sizeof(int64_t)), "cudaMalloc pos");
@@ -108,6 +111,7 @@ public:
         cudaFree(perm_);
         cudaFree(rope_);
         cudaFree(ws_);
+        cudaFree(plan_);
         cudaFree(dev_pos_);
     }
 
@@ -165,7 +169,7 @@ public:
         }
         check_cuda(cudaMemcpyAsync(dev_pos_, len_.data(), len_.size() * sizeof(int64_t), cudaMemcpyHostToDevice,
                                    stream_), "seq_len");
-        check(rkv_decode_attention(&desc_, q, dev_pos_, mx, &cache_, perm_, static_cast<const float*>(rope_), out, ws_,
+        check(rkv_decode_attention(&desc_, q, dev_pos_, mx, &cache_, plan_, static_cast<const float*>(rope_), out, ws_,
                                    ws_bytes_, stream_));
         check_cuda(cudaStreamSynchronize(stream_), "decode");
     }
@@ -182,6 +186,8 @@ private:
     size_t rope_bytes_ = 0;
     void* ws_ = nullptr;
     size_t ws_bytes_ = 0;
+    void* plan_ = nullptr;
+    size_t plan_bytes_ = 0;
     int64_t* dev_pos_ = nullptr;
 };
 

@@ -14,6 +14,7 @@ from .rotatekv import (  # noqa: F401
     apply_reorder,
     calibrate_reorder,
     detect_massive_activations,
+    layer_plan_build,
     lib,
     rotate_keys,
 )

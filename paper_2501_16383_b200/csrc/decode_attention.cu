@@ -36,6 +36,7 @@
 
 #include "rkv_common.cuh"
 #include "rkv_internal.h"
+#include "rkv_layout.h"
 
 namespace rkv {
 
@@ -62,7 +63,7 @@ struct SmemLayout {
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-__host__ __device__ inline SmemLayout smem_layout(int C, int Hq, int TT) {
+__host__ __device__ inline SmemLayout smem_layout(int C, int Hq, int TT, int chunk, int N, int plan_smem_words) {
     SmemLayout s{};
     const int W = C / 16, MG = C / 128;
     s.kc = 0;
@@ -74,22 +75,11 @@ __host__ __device__ inline SmemLayout smem_layout(int C, int Hq, int TT) {
     s.stages = 0;
     s.mbar = s.stages + kStages * s.stage_bytes;
     s.knat = align16(s.mbar + kStages * 8);
-    s.q = align16(s.knat + size_t(TT / 2) * C * 8);  // TT/2 token pairs x C float2
-    s.addr = align16(s.q + size_t(Hq) * 128 * 4 * 3 / 2);  // padded q rows (<= 1.5x)
-    s.mask = align16(s.addr + size_t(C) * 4);
-    s.total = align16(s.mask + 16);
+    s.q = align16(s.knat + size_t(TT / 2) * knat_pair_f2(N, C) * 8);  // TT/2 token pairs
+    s.addr = align16(s.q + size_t(Hq) * 128 * 4 * 3 / 2);              // padded q rows (<= 1.5x)
+    s.mask = align16(s.addr + size_t(plan_smem_words) * 4);            // omega + scatter schedule
+    s.total = align16(s.mask + size_t(chunk / 32 + 2) * 4);  // the split's sink-mask words
     return s;
-}
-
-// Float2 index of natural channel c inside a pair row: unit g = c/N holds the
-// FWHT group; layout-A lane la = (c%N)/R owns a contiguous R-float2 row whose
-// 16-byte chunks are XOR-swizzled with la so layout-A LDS.128 (8 lanes per
-// phase) and layout-B LDS.64 (16 lanes per phase) are conflict-free.
-template <int N, int L>
-__host__ __device__ inline int pair_pos(int c) {
-    constexpr int R = N / L, LR = ilog2(R);
-    const int g = c / N, i = c % N, la = i >> LR, qp = i & (R - 1);
-    return g * N + la * R + 2 * ((qp >> 1) ^ (la & 7)) + (qp & 1);
 }
 
 template <int N>
@@ -115,11 +105,12 @@ __global__ void __launch_bounds__(max_threads<N>(), 1) decode_split_kernel(Decod
     extern __shared__ __align__(128) unsigned char smem[];
     const int C = p.C, W = C / 16, MG = C / 128, Hq = p.Hq;
     const int NG = C / N, PP = p.P, TT = 2 * PP;
-    const SmemLayout lay = smem_layout(C, Hq, TT);
+    const SmemLayout lay = smem_layout(C, Hq, TT, p.chunk, N, 17 * W);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + lay.mbar);
     unsigned char* knat = smem + lay.knat;
     float* q_l = reinterpret_cast<float*>(smem + lay.q);
-    uint32_t* saddr = reinterpret_cast<uint32_t*>(smem + lay.addr);
+    uint32_t* omega_s = reinterpret_cast<uint32_t*>(smem + lay.addr);   // [W]
+    const uint4* saddr4 = reinterpret_cast<const uint4*>(omega_s + W);  // [4][W] x 4 scatter offsets
     uint32_t* mask_s = reinterpret_cast<uint32_t*>(smem + lay.mask);
 
     const int tid = threadIdx.x, NT = blockDim.x;
@@ -165,12 +156,12 @@ __global__ void __launch_bounds__(max_threads<N>(), 1) decode_split_kernel(Decod
     if (tid == 0)
         for (int it = 0; it < kStages - 1 && it < ntiles; ++it) issue_tile(it);
 
-    // slot j -> byte offset of its natural channel inside a pair row, stored
-    // [j%16 / 4][word][j%4] so a warp's uint4 loads of consecutive words are
-    // conflict-free
-    for (int j = tid; j < C; j += NT) {
-        const int w = j >> 4, e = j & 15;
-        saddr[((e >> 2) * W + w) * 4 + (e & 3)] = static_cast<uint32_t>(pair_pos<N, L>(__ldg(p.perm + j))) * 8u;
+    // the layer's scatter plan (rkv_plan.cu): word assignment + scatter offsets
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(p.plan + kPlanHeader);
+        uint4* dst = reinterpret_cast<uint4*>(omega_s);
+        const int n4 = 17 * W / 4;
+        for (int i = tid; i < n4; i += NT) dst[i] = __ldg(src + i);
     }
 
     // q: RoPE at position T-1 (prepare_queries), x log2(e)/sqrt(d) x 1/sqrt(n)
@@ -190,13 +181,21 @@ __global__ void __launch_bounds__(max_threads<N>(), 1) decode_split_kernel(Decod
         }
     }
 
-    // per-lane constants
-    const int pair_bytes = C * 8;
-    unsigned char* kpair = knat + pp * pair_bytes;  // this lane group's token pair
-    const int abase = (g * N + lam * R) * 8;        // layout-A row
-    uint32_t vb[L / 2];                              // layout-B bases (see pair_pos)
-#pragma unroll
-    for (int k = 0; k < L / 2; ++k) vb[k] = static_cast<uint32_t>(g * N * 8 + 16 * ((lam >> 1) ^ k) + 8 * (lam & 1));
+    // the split's sink-mask words (bit t%32 of word t/32 = sink), so no thread
+    // touches global memory for token validity inside the tile loop
+    const int64_t mw0 = t_begin >> 5;
+    {
+        const uint32_t* smask = p.cache.sink_mask + static_cast<int64_t>(b) * ((p.max_tokens + 31) / 32);
+        const int nw = static_cast<int>(((t_end - 1) >> 5) - mw0 + 1);
+        for (int i = tid; i < nw; i += NT) mask_s[i] = smask[mw0 + i];
+    }
+
+    // per-lane constants (padded rows: see rkv_layout.h)
+    constexpr int RS = R + 1;                                 // row stride in float2
+    const int pair_bytes = knat_pair_f2(N, C) * 8;
+    unsigned char* kpair = knat + pp * pair_bytes;           // this lane group's token pair
+    unsigned char* kunit = kpair + g * L * RS * 8;           // its FWHT group
+    unsigned char* arow = kunit + lam * RS * 8;              // its layout-A row
 
     float m_run[VH], l_run[VH], zc[VH];
     float2 acc[VH][8];
@@ -208,9 +207,14 @@ __global__ void __launch_bounds__(max_threads<N>(), 1) decode_split_kernel(Decod
 #pragma unroll
         for (int e = 0; e < 8; ++e) acc[v][e] = make_float2(0.f, 0.f);
     }
-    __syncthreads();  // saddr and q_l complete
+    __syncthreads();  // plan and q_l complete
 
-    const uint32_t* smask = p.cache.sink_mask + static_cast<int64_t>(b) * ((p.max_tokens + 31) / 32);
+    // K1 item mapping (loop invariant; plan_decode guarantees NT % W == 0 or
+    // W % NT == 0): thread -> word position k1w (+NT...), token pairs k1p0,
+    // k1p0+k1ps, ...; a half-warp = 16 consecutive word positions
+    const int k1w = NT >= W ? tid % W : tid;
+    const int k1p0 = __shfl_sync(0xffffffffu, NT >= W ? tid / W : 0, 0);  // warp-uniform (W % 32 == 0)
+    const int k1ps = NT >= W ? NT / W : 1;
 
     for (int it = 0; it < ntiles; ++it) {
         const int64_t t0 = t_begin + static_cast<int64_t>(it) * TT;
@@ -223,45 +227,36 @@ __global__ void __launch_bounds__(max_threads<N>(), 1) decode_split_kernel(Decod
         const float4* rope4 = reinterpret_cast<const float4*>(st + lay.rope);
         mbar_wait(mbar + (it % kStages), (it / kStages) & 1);
 
-        // ---- K1: exact dequantize of a word for a token pair + scatter (STS.64)
-        if (tid == 0) {
-            uint32_t m = 0;
-            for (int tt = 0; tt < nv; ++tt) {
-                const int64_t t = t0 + tt;
-                if (!((smask[t >> 5] >> (t & 31)) & 1u)) m |= 1u << tt;
-            }
-            *mask_s = m;
-        }
-        // warp-granular items (W % 32 == 0): pq is warp-uniform, so the pair
-        // offset rides in a uniform register of the STS address
-        for (int wbase = (tid & ~31); wbase < PP * W; wbase += NT) {
-            const int pq = __shfl_sync(0xffffffffu, wbase / W, 0);
-            const int w = wbase - pq * W + (tid & 31);
+        // ---- K1: dequantize a word for a token pair + scatter (STS.64); pq is
+        // warp-uniform, so the pair offset rides in a uniform register
+        for (int wp = k1w; wp < W; wp += NT)
+        for (int pq = k1p0; pq < PP; pq += k1ps) {
             const int tt0 = 2 * pq;
-            if (tt0 >= nv) continue;
+            if (tt0 >= nv) break;
             const bool has1 = tt0 + 1 < nv;
+            const int w = omega_s[wp];
             const uint32_t w0 = kc[tt0 * W + w], w1 = has1 ? kc[(tt0 + 1) * W + w] : 0u;
             const uint32_t m0 = km[tt0 * MG + (w >> 3)], m1 = has1 ? km[(tt0 + 1) * MG + (w >> 3)] : 0u;
-            const float2 s2 = make_float2(h2f(static_cast<uint16_t>(m0 & 0xffffu)), h2f(static_cast<uint16_t>(m1 & 0xffffu)));
-            const float2 nzb = make_float2(-(8388608.0f + h2f(static_cast<uint16_t>(m0 >> 16))),
-                                           -(8388608.0f + h2f(static_cast<uint16_t>(m1 >> 16))));
-            const uint4* ap = reinterpret_cast<const uint4*>(saddr) + w;
+            // x = 1 + c/4 (code OR'd into the mantissa): s*(c - z) = x*(4s) - (4 + z)*s,
+            // every term exact, so one FFMA2 per token pair
+            const float s0 = h2f(static_cast<uint16_t>(m0 & 0xffffu)), s1 = h2f(static_cast<uint16_t>(m1 & 0xffffu));
+            const float2 s4 = make_float2(4.0f * s0, 4.0f * s1);
+            const float2 nzb = make_float2(-(4.0f + h2f(static_cast<uint16_t>(m0 >> 16))) * s0,
+                                           -(4.0f + h2f(static_cast<uint16_t>(m1 >> 16))) * s1);
             const uint32_t dst = smem_u32(knat) + pq * pair_bytes;
-            float2 val16[16];
-#pragma unroll
-            for (int e = 0; e < 16; ++e) {
-                // (2^23 + c) - (2^23 + z) = c - z exactly; times s exactly
-                const float2 xx = make_float2(__uint_as_float(and_or(w0 >> (2 * e), 3u, 0x4B000000u)),
-                                              __uint_as_float(and_or(w1 >> (2 * e), 3u, 0x4B000000u)));
-                val16[e] = mul2(add2(xx, nzb), s2);
-            }
 #pragma unroll
             for (int q4 = 0; q4 < 4; ++q4) {
-                const uint4 a4 = ap[q4 * W];
-                sts64(dst + a4.x, val16[4 * q4]);
-                sts64(dst + a4.y, val16[4 * q4 + 1]);
-                sts64(dst + a4.z, val16[4 * q4 + 2]);
-                sts64(dst + a4.w, val16[4 * q4 + 3]);
+                const uint4 a4 = saddr4[q4 * W + wp];
+                const uint32_t ad[4] = {a4.x, a4.y, a4.z, a4.w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int e = 4 * q4 + k, sh = 21 - 2 * e;
+                    const uint32_t a0 = sh >= 0 ? (w0 << sh) : (w0 >> -sh);
+                    const uint32_t a1 = sh >= 0 ? (w1 << sh) : (w1 >> -sh);
+                    const float2 xx = make_float2(__uint_as_float(and_or(a0, 0x600000u, 0x3F800000u)),
+                                                  __uint_as_float(and_or(a1, 0x600000u, 0x3F800000u)));
+                    sts64(dst + ad[k], fma2(xx, s4, nzb));
+                }
             }
         }
         __syncthreads();
@@ -271,32 +266,18 @@ __global__ void __launch_bounds__(max_threads<N>(), 1) decode_split_kernel(Decod
         const int tt0 = 2 * pp;
         float2 x[R];
 #pragma unroll
-        for (int q2 = 0; q2 < R / 2; ++q2) {
-            const float4 v = lds128f(kpair + abase + 16 * (q2 ^ (lam & 7)));
-            x[2 * q2] = make_float2(v.x, v.y);
-            x[2 * q2 + 1] = make_float2(v.z, v.w);
-        }
+        for (int j = 0; j < R; ++j) x[j] = lds64(arow + 8 * j);
         bfly_range<R, 0, LR>(x);
-        // two STS.64 per chunk: FADD2 results sit in arbitrary register pairs, an
-        // STS.128 would need 4 MOVs to build an aligned quad (same wavefronts)
-        const uint32_t kpair_s = smem_u32(kpair) + abase;
+        {
+            const uint32_t a = smem_u32(arow);
 #pragma unroll
-        for (int q2 = 0; q2 < R / 2; ++q2) {
-            const uint32_t a = kpair_s + 16 * (q2 ^ (lam & 7));
-            sts64(a, x[2 * q2]);
-            sts64(a + 8, x[2 * q2 + 1]);
+            for (int j = 0; j < R; ++j) sts64(a + 8 * j, x[j]);
         }
         __syncwarp();
 #pragma unroll
         for (int j = 0; j < R; ++j) {
-            // channel lam + L*j: layout-A owner la = (L*j) >> LR, in-row chunk
-            // ((lam >> 1) | c1) ^ (la & 7) with c1 = ((L*j) & (R-1)) >> 1
-            const int la = (L * j) >> LR;
-            const int c1 = ((L * j) & (R - 1)) >> 1;
-            const int k2 = la & 7;
-            const int lo = k2 & (L / 2 - 1);
-            const int hi = c1 ^ (k2 & ~(L / 2 - 1));
-            x[j] = lds64(kpair + vb[lo] + (la * R + 2 * hi) * 8);
+            // channel lam + L*j of the group: row (L*j)/R, column lam + (L*j)%R
+            x[j] = lds64(kunit + (((L * j) >> LR) * RS + ((L * j) & (R - 1)) + lam) * 8);
         }
         bfly_range<R, LR - LL, LN - LL>(x);
 
@@ -356,8 +337,12 @@ __global__ void __launch_bounds__(max_threads<N>(), 1) decode_split_kernel(Decod
         constexpr int SH = LL - ilog2(V0);
 
         // ---- online softmax for the lane's V heads (replicated per lane)
-        const uint32_t tmask = *mask_s;
-        const bool ok0 = (tmask >> tt0) & 1u, ok1 = (tmask >> (tt0 + 1)) & 1u;
+        bool ok0, ok1;
+        {
+            const int64_t ta = t0 + tt0, tb = ta + 1;
+            ok0 = tt0 < nv && !((mask_s[(ta >> 5) - mw0] >> (ta & 31)) & 1u);
+            ok1 = tt0 + 1 < nv && !((mask_s[(tb >> 5) - mw0] >> (tb & 31)) & 1u);
+        }
         float pr0[VH], pr1[VH];
 #pragma unroll
         for (int v = 0; v < VH; ++v) {
@@ -587,7 +572,6 @@ DecodePlan plan_decode(const rkv_layer_desc& d, int64_t max_seq_len) {
     pl.P = P;
     pl.TT = 2 * P;
     pl.NT = NG * P * L;
-    pl.smem = smem_layout(C, d.num_q_heads, pl.TT).total;
     if (max_seq_len <= 0 || max_seq_len > d.max_tokens) max_seq_len = d.max_tokens;
     const int ctas = num_sms();  // one CTA per SM (shared-memory bound)
     int S = ctas / d.batch;
@@ -599,6 +583,7 @@ DecodePlan plan_decode(const rkv_layer_desc& d, int64_t max_seq_len) {
     pl.chunk = static_cast<int>(chunk);
     pl.S = static_cast<int>((max_seq_len + chunk - 1) / chunk);
     pl.NP = pl.S * P;
+    pl.smem = smem_layout(C, d.num_q_heads, pl.TT, pl.chunk, pl.N, 17 * (C / 16)).total;
     return pl;
 }
 

@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "rkv_internal.h"
+#include "rkv_layout.h"
 
 namespace {
 
@@ -191,6 +192,47 @@ rkv_status rkv_quantize_kv(const rkv_layer_desc* desc, const uint16_t* k_new, co
     return RKV_OK;
 }
 
+size_t rkv_layer_plan_bytes(const rkv_layer_desc* desc) {
+    if (validate(desc) != RKV_OK) return 0;
+    const int W = desc->num_kv_heads * desc->head_dim / 16;
+    return static_cast<size_t>(rkv::plan_words(W)) * 4;
+}
+
+rkv_status rkv_layer_plan_build(const rkv_layer_desc* desc, const int32_t* perm, uint32_t* plan_host,
+                                size_t bytes, int32_t* cost_out) {
+    rkv_status st = validate(desc);
+    if (st != RKV_OK) return st;
+    if (!perm || !plan_host) return fail(RKV_ERR_INVALID_ARGUMENT, "layer_plan: null argument");
+    const int C = desc->num_kv_heads * desc->head_dim;
+    std::vector<int32_t> inv(static_cast<size_t>(C), -1);
+    for (int j = 0; j < C; ++j) {
+        if (perm[j] < 0 || perm[j] >= C || inv[static_cast<size_t>(perm[j])] != -1)
+            return fail(RKV_ERR_INVALID_ARGUMENT, "reorder plan: perm must be a permutation of the channel count");
+        inv[static_cast<size_t>(perm[j])] = j;
+    }
+    std::vector<uint32_t> words;
+    int cost = 0;
+    if (!rkv::build_decode_plan(*desc, perm, words, cost)) return fail(RKV_ERR_RUNTIME, "layer_plan: build failed");
+    if (bytes < words.size() * 4) return fail(RKV_ERR_INVALID_ARGUMENT, "layer_plan: buffer too small");
+    std::memcpy(plan_host, words.data(), words.size() * 4);
+    if (cost_out) *cost_out = cost;
+    return RKV_OK;
+}
+
+rkv_status rkv_layer_plan_init(const rkv_layer_desc* desc, const int32_t* perm, void* plan_dev, size_t bytes,
+                               void* stream) {
+    std::vector<uint32_t> host(bytes / 4);
+    rkv_status st = rkv_layer_plan_build(desc, perm, host.data(), bytes, nullptr);
+    if (st != RKV_OK) return st;
+    if (!plan_dev) return fail(RKV_ERR_INVALID_ARGUMENT, "layer_plan: null device buffer");
+    const size_t used = rkv_layer_plan_bytes(desc);
+    cudaStream_t cs = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMemcpyAsync(plan_dev, host.data(), used, cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(cs);  // host staging buffer dies on return
+    if (e != cudaSuccess) return cuda_fail(e, "layer_plan_init");
+    return RKV_OK;
+}
+
 size_t rkv_decode_workspace_bytes(const rkv_layer_desc* desc, int64_t max_seq_len) {
     if (validate(desc) != RKV_OK) return 0;
     rkv::DecodePlan pl = rkv::plan_decode(*desc, max_seq_len);
@@ -199,13 +241,13 @@ size_t rkv_decode_workspace_bytes(const rkv_layer_desc* desc, int64_t max_seq_le
 }
 
 rkv_status rkv_decode_attention(const rkv_layer_desc* desc, const uint16_t* q, const int64_t* seq_len,
-                                int64_t max_seq_len, const rkv_cache* cache, const int32_t* perm,
+                                int64_t max_seq_len, const rkv_cache* cache, const void* layer_plan,
                                 const float* rope_table, float* out, void* workspace, size_t ws_bytes,
                                 void* stream) {
     rkv_status st = validate(desc);
     if (st != RKV_OK) return st;
     if ((st = check_cache(cache)) != RKV_OK) return st;
-    if (!q || !seq_len || !perm || !rope_table || !out || !workspace)
+    if (!q || !seq_len || !layer_plan || !rope_table || !out || !workspace)
         return fail(RKV_ERR_INVALID_ARGUMENT, "decode_attention: null argument");
     if (max_seq_len < 0 || max_seq_len > desc->max_tokens)
         return fail(RKV_ERR_OUT_OF_RANGE, "decode_attention: max_seq_len exceeds max_tokens");
@@ -213,13 +255,14 @@ rkv_status rkv_decode_attention(const rkv_layer_desc* desc, const uint16_t* q, c
     if (ws_bytes < rkv_decode_workspace_bytes(desc, max_seq_len))
         return fail(RKV_ERR_INVALID_ARGUMENT, "decode_attention: workspace too small");
     rkv::DecodePlan pl = rkv::plan_decode(*desc, max_seq_len);
-    if (pl.NT > (pl.N == 512 ? 320 : 256) || pl.smem > 227 * 1024)
+    const int W = desc->num_kv_heads * desc->head_dim / 16;
+    if (pl.NT > (pl.N == 512 ? 320 : 256) || pl.smem > 227 * 1024 || (pl.NT % W != 0 && W % pl.NT != 0))
         return fail(RKV_ERR_INVALID_ARGUMENT, "decode_attention: layer shape exceeds the sm_100a kernel's tile budget");
     const size_t rows = static_cast<size_t>(desc->batch) * pl.NP * desc->num_q_heads;
     rkv::DecodeParams p{};
     p.q = q;
     p.seq_len = seq_len;
-    p.perm = perm;
+    p.plan = static_cast<const uint32_t*>(layer_plan);
     p.rope = reinterpret_cast<const float4*>(rope_table);
     p.cache = *cache;
     p.ws_ml = static_cast<float*>(workspace);

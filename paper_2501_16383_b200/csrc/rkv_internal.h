@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 #include "rotatekv/rotatekv.h"
 
@@ -30,7 +31,7 @@ struct QuantParams {
 struct DecodeParams {
     const uint16_t* q;
     const int64_t* seq_len;
-    const int32_t* perm;
+    const uint32_t* plan;  // rkv_layer_plan_init (rkv_layout.h)
     const float4* rope;  // [max_pos/2][64] (cos p0, cos p1, sin p0, sin p1)
     rkv_cache cache;
     float* ws_ml;  // [B][NP][Hq][2]   partial (m, l) per lane-group partition
@@ -62,5 +63,7 @@ cudaError_t launch_rope_table(const rkv_layer_desc& d, float4* table, int64_t ma
 cudaError_t launch_rotate_keys(const rkv_layer_desc& d, const uint16_t* k, int64_t rows, float* out,
                                cudaStream_t s);
 int num_sms();
+// rkv_plan.cu
+bool build_decode_plan(const rkv_layer_desc& d, const int32_t* perm, std::vector<uint32_t>& out, int& cost);
 
 }  // namespace rkv

@@ -83,13 +83,17 @@ def lib():
         L.rkv_decode_workspace_bytes.restype = C.c_size_t
         L.rkv_decode_workspace_bytes.argtypes = [D, C.c_int64]
         L.rkv_decode_attention.argtypes = [D, P, P, C.c_int64, C.POINTER(CacheView), P, P, P, P, C.c_size_t, P]
+        L.rkv_layer_plan_bytes.restype = C.c_size_t
+        L.rkv_layer_plan_bytes.argtypes = [D]
+        L.rkv_layer_plan_build.argtypes = [D, P, P, C.c_size_t, C.POINTER(C.c_int32)]
+        L.rkv_layer_plan_init.argtypes = [D, P, P, C.c_size_t, P]
         L.rkv_rotate_keys.argtypes = [D, P, C.c_int64, P, P]
         L.rkv_calibrate_reorder.argtypes = [P, C.c_int64, C.c_int64, C.c_int32, P, P]
         L.rkv_detect_sinks.argtypes = [P, C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_double, P,
                                        C.POINTER(C.c_int64)]
         for name in ("rkv_layer_validate", "rkv_cache_carve", "rkv_cache_reset", "rkv_rope_table_init",
                      "rkv_quantize_kv", "rkv_decode_attention", "rkv_rotate_keys", "rkv_calibrate_reorder",
-                     "rkv_detect_sinks"):
+                     "rkv_detect_sinks", "rkv_layer_plan_build", "rkv_layer_plan_init"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -183,6 +187,18 @@ def detect_massive_activations(hidden, rel_threshold: float = 50.0, abs_floor: f
     return flags
 
 
+def layer_plan_build(cfg: LayerConfig, perm):
+    """Host build of the decode plan (scatter word assignment) -> (uint32
+    words, cost = summed worst bank-slot multiplicity, 16 per half-warp ideal)."""
+    d = cfg.desc()
+    perm = _np(perm, np.int32)
+    n = lib().rkv_layer_plan_bytes(C.byref(d))
+    out = np.zeros(n // 4, np.uint32)
+    cost = C.c_int32()
+    _check(lib().rkv_layer_plan_build(C.byref(d), perm.ctypes.data, out.ctypes.data, n, C.byref(cost)))
+    return out, cost.value
+
+
 # ------------------------------------------------------------ device layer
 
 class RotateKVLayer:
@@ -214,6 +230,10 @@ class RotateKVLayer:
         self._base = base
         rope_bytes = lib().rkv_rope_table_bytes(C.byref(self._desc), cfg.max_tokens)
         self.rope = torch.empty(rope_bytes // 4, dtype=torch.float32, device=self.device)
+        plan_bytes = lib().rkv_layer_plan_bytes(C.byref(self._desc))
+        self.plan = torch.empty(plan_bytes, dtype=torch.uint8, device=self.device)
+        _check(lib().rkv_layer_plan_init(C.byref(self._desc), perm.ctypes.data, _ptr(self.plan), plan_bytes,
+                                         self._stream_or_none(stream)))
         self.lengths = np.zeros(cfg.batch, np.int64)
         self.sink_counts = np.zeros(cfg.batch, np.int64)
         self._ws = None
@@ -223,6 +243,10 @@ class RotateKVLayer:
         self.reset()
 
     # -- plumbing
+    def _stream_or_none(self, stream):
+        s = stream if stream is not None else self.torch.cuda.current_stream(self.device)
+        return C.c_void_p(s.cuda_stream)
+
     def _stream(self):
         s = self.stream if self.stream is not None else self.torch.cuda.current_stream(self.device)
         return C.c_void_p(s.cuda_stream)
@@ -316,14 +340,14 @@ class RotateKVLayer:
         self._lens_t = torch.from_numpy(lens).to(self.device)
         q = q.contiguous()
         _check(lib().rkv_decode_attention(C.byref(self._desc), _ptr(q), _ptr(self._lens_t), msl,
-                                          C.byref(self._view), _ptr(self.perm), _ptr(self.rope), _ptr(out),
+                                          C.byref(self._view), _ptr(self.plan), _ptr(self.rope), _ptr(out),
                                           _ptr(ws), need, self._stream()))
         return out
 
     def decode_device(self, q, seq_len_t, max_seq_len, out, ws, ws_bytes):
         """Allocation-free decode with device-resident lengths (CUDA-graph safe)."""
         _check(lib().rkv_decode_attention(C.byref(self._desc), _ptr(q), _ptr(seq_len_t), int(max_seq_len),
-                                          C.byref(self._view), _ptr(self.perm), _ptr(self.rope), _ptr(out),
+                                          C.byref(self._view), _ptr(self.plan), _ptr(self.rope), _ptr(out),
                                           _ptr(ws), ws_bytes, self._stream()))
         return out
 
