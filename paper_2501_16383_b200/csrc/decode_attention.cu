@@ -31,8 +31,10 @@
 //   * every lane group writes its own (m, l, o') partial; the combine kernel
 //     merges partials in a fixed order, adds the fp16 sink rows (computed
 //     inline, natural frame) and applies H_128.  Deterministic.
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
 
 #include "rkv_common.cuh"
 #include "rkv_internal.h"
@@ -42,7 +44,7 @@ namespace rkv {
 
 namespace {
 
-constexpr int kStages = 3;
+constexpr int kMaxStages = 4;
 
 __device__ __forceinline__ int64_t lmin(int64_t a, int64_t b) { return a < b ? a : b; }
 
@@ -63,7 +65,8 @@ struct SmemLayout {
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-__host__ __device__ inline SmemLayout smem_layout(int C, int Hq, int TT, int chunk, int N, int plan_smem_words) {
+__host__ __device__ inline SmemLayout smem_layout(int C, int Hq, int TT, int chunk, int N, int plan_smem_words,
+                                                 int kStages) {
     SmemLayout s{};
     const int W = C / 16, MG = C / 128;
     s.kc = 0;
@@ -105,7 +108,8 @@ __global__ void __launch_bounds__(max_threads<N>(), 1) decode_split_kernel(Decod
     extern __shared__ __align__(128) unsigned char smem[];
     const int C = p.C, W = C / 16, MG = C / 128, Hq = p.Hq;
     const int NG = C / N, PP = p.P, TT = 2 * PP;
-    const SmemLayout lay = smem_layout(C, Hq, TT, p.chunk, N, 17 * W);
+    const int kStages = p.stages;
+    const SmemLayout lay = smem_layout(C, Hq, TT, p.chunk, N, 17 * W, kStages);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + lay.mbar);
     unsigned char* knat = smem + lay.knat;
     float* q_l = reinterpret_cast<float*>(smem + lay.q);
@@ -229,33 +233,38 @@ __global__ void __launch_bounds__(max_threads<N>(), 1) decode_split_kernel(Decod
 
         // ---- K1: dequantize a word for a token pair + scatter (STS.64); pq is
         // warp-uniform, so the pair offset rides in a uniform register
-        for (int wp = k1w; wp < W; wp += NT)
-        for (int pq = k1p0; pq < PP; pq += k1ps) {
-            const int tt0 = 2 * pq;
-            if (tt0 >= nv) break;
-            const bool has1 = tt0 + 1 < nv;
+        for (int wp = k1w; wp < W; wp += NT) {
             const int w = omega_s[wp];
-            const uint32_t w0 = kc[tt0 * W + w], w1 = has1 ? kc[(tt0 + 1) * W + w] : 0u;
-            const uint32_t m0 = km[tt0 * MG + (w >> 3)], m1 = has1 ? km[(tt0 + 1) * MG + (w >> 3)] : 0u;
-            // x = 1 + c/4 (code OR'd into the mantissa): s*(c - z) = x*(4s) - (4 + z)*s,
-            // every term exact, so one FFMA2 per token pair
-            const float s0 = h2f(static_cast<uint16_t>(m0 & 0xffffu)), s1 = h2f(static_cast<uint16_t>(m1 & 0xffffu));
-            const float2 s4 = make_float2(4.0f * s0, 4.0f * s1);
-            const float2 nzb = make_float2(-(4.0f + h2f(static_cast<uint16_t>(m0 >> 16))) * s0,
-                                           -(4.0f + h2f(static_cast<uint16_t>(m1 >> 16))) * s1);
-            const uint32_t dst = smem_u32(knat) + pq * pair_bytes;
+            uint32_t ad[16];  // scatter offsets of the word's 16 codes, reused for every pair
 #pragma unroll
             for (int q4 = 0; q4 < 4; ++q4) {
                 const uint4 a4 = saddr4[q4 * W + wp];
-                const uint32_t ad[4] = {a4.x, a4.y, a4.z, a4.w};
+                ad[4 * q4] = a4.x;
+                ad[4 * q4 + 1] = a4.y;
+                ad[4 * q4 + 2] = a4.z;
+                ad[4 * q4 + 3] = a4.w;
+            }
+            for (int pq = k1p0; pq < PP; pq += k1ps) {
+                const int tt0 = 2 * pq;
+                if (tt0 >= nv) break;
+                const bool has1 = tt0 + 1 < nv;
+                const uint32_t w0 = kc[tt0 * W + w], w1 = has1 ? kc[(tt0 + 1) * W + w] : 0u;
+                const uint32_t m0 = km[tt0 * MG + (w >> 3)], m1 = has1 ? km[(tt0 + 1) * MG + (w >> 3)] : 0u;
+                // x = 1 + c/4 (code OR'd into the mantissa): s*(c - z) = x*(4s) - (4 + z)*s,
+                // every term exact, so one FFMA2 per token pair
+                const float s0 = h2f(static_cast<uint16_t>(m0 & 0xffffu)), s1 = h2f(static_cast<uint16_t>(m1 & 0xffffu));
+                const float2 s4 = make_float2(4.0f * s0, 4.0f * s1);
+                const float2 nzb = make_float2(-(4.0f + h2f(static_cast<uint16_t>(m0 >> 16))) * s0,
+                                               -(4.0f + h2f(static_cast<uint16_t>(m1 >> 16))) * s1);
+                const uint32_t dst = smem_u32(knat) + pq * pair_bytes;
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int e = 4 * q4 + k, sh = 21 - 2 * e;
+                for (int e = 0; e < 16; ++e) {
+                    const int sh = 21 - 2 * e;
                     const uint32_t a0 = sh >= 0 ? (w0 << sh) : (w0 >> -sh);
                     const uint32_t a1 = sh >= 0 ? (w1 << sh) : (w1 >> -sh);
                     const float2 xx = make_float2(__uint_as_float(and_or(a0, 0x600000u, 0x3F800000u)),
                                                   __uint_as_float(and_or(a1, 0x600000u, 0x3F800000u)));
-                    sts64(dst + ad[k], fma2(xx, s4, nzb));
+                    sts64(dst + ad[e], fma2(xx, s4, nzb));
                 }
             }
         }
@@ -549,6 +558,33 @@ int num_sms() {
     return n;
 }
 
+template <int N, int REP>
+int occupancy_nr(const DecodePlan& pl) {
+    int n = 0;
+    if (cudaFuncSetAttribute(decode_split_kernel<N, REP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(pl.smem)) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, decode_split_kernel<N, REP>, pl.NT, pl.smem) != cudaSuccess) {
+        cudaGetLastError();
+        const int by_smem = static_cast<int>((227u * 1024u) / (pl.smem + 1024));
+        return std::max(1, by_smem);
+    }
+    return std::max(1, n);
+}
+
+int occupancy(const DecodePlan& pl) {
+    switch (pl.N * 16 + pl.REP) {
+        case 512 * 16 + 1: return occupancy_nr<512, 1>(pl);
+        case 512 * 16 + 2: return occupancy_nr<512, 2>(pl);
+        case 256 * 16 + 1: return occupancy_nr<256, 1>(pl);
+        case 256 * 16 + 2: return occupancy_nr<256, 2>(pl);
+        case 256 * 16 + 4: return occupancy_nr<256, 4>(pl);
+        case 128 * 16 + 1: return occupancy_nr<128, 1>(pl);
+        case 128 * 16 + 2: return occupancy_nr<128, 2>(pl);
+        case 128 * 16 + 4: return occupancy_nr<128, 4>(pl);
+        default: return 1;
+    }
+}
+
 bool decode_supported(int N, int REP) {
     switch (N) {
         case 512: return REP == 1 || REP == 2;
@@ -569,11 +605,18 @@ DecodePlan plan_decode(const rkv_layer_desc& d, int64_t max_seq_len) {
     int P = max_nt / (NG * L);
     if (P > 4) P = 4;
     if (P < 1) P = 1;
+    pl.stages = 3;
+    if (const char* e = std::getenv("RKV_DECODE_P")) P = std::max(1, std::min(P, std::atoi(e)));  // tuning knobs
+    if (const char* e = std::getenv("RKV_DECODE_STAGES")) pl.stages = std::max(2, std::min(kMaxStages, std::atoi(e)));
     pl.P = P;
     pl.TT = 2 * P;
     pl.NT = NG * P * L;
     if (max_seq_len <= 0 || max_seq_len > d.max_tokens) max_seq_len = d.max_tokens;
-    const int ctas = num_sms();  // one CTA per SM (shared-memory bound)
+    // CTAs resident per SM (shared memory and registers decide)
+    pl.smem = smem_layout(C, d.num_q_heads, pl.TT, static_cast<int>(max_seq_len) + pl.TT, pl.N, 17 * (C / 16),
+                          pl.stages).total;  // upper bound (chunk <= max_seq_len)
+    pl.per_sm = occupancy(pl);
+    const int ctas = num_sms() * pl.per_sm;
     int S = ctas / d.batch;
     if (S < 1) S = 1;
     const int64_t max_split = (max_seq_len + 4 * pl.TT - 1) / (4 * pl.TT);  // >= 4 tiles per split
@@ -583,7 +626,7 @@ DecodePlan plan_decode(const rkv_layer_desc& d, int64_t max_seq_len) {
     pl.chunk = static_cast<int>(chunk);
     pl.S = static_cast<int>((max_seq_len + chunk - 1) / chunk);
     pl.NP = pl.S * P;
-    pl.smem = smem_layout(C, d.num_q_heads, pl.TT, pl.chunk, pl.N, 17 * (C / 16)).total;
+    pl.smem = smem_layout(C, d.num_q_heads, pl.TT, pl.chunk, pl.N, 17 * (C / 16), pl.stages).total;
     return pl;
 }
 

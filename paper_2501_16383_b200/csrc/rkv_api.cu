@@ -278,6 +278,7 @@ rkv_status rkv_decode_attention(const rkv_layer_desc* desc, const uint16_t* q, c
     p.max_sinks = desc->max_sinks;
     p.chunk = pl.chunk;
     p.P = pl.P;
+    p.stages = pl.stages;
     p.k_norm = 1.0f / std::sqrt(static_cast<float>(desc->heads_per_group * desc->head_dim));
     p.qscale = rkv::kLog2eHost / std::sqrt(static_cast<float>(desc->head_dim));
     cudaError_t e = rkv::launch_decode(*desc, pl, p, static_cast<cudaStream_t>(stream));

@@ -43,6 +43,7 @@ struct DecodeParams {
     int NP;     // partial rows per sequence = S * P
     int chunk;  // tokens per split, multiple of the tile
     int P;      // token pairs per tile (= lane-group partitions per FWHT group)
+    int stages; // TMA ring depth
     int max_sinks;
     float k_norm;  // 1/sqrt(G*d), folded into q
     float qscale;  // log2(e) / sqrt(d)
@@ -52,7 +53,7 @@ struct DecodeParams {
 cudaError_t launch_quantize(const rkv_layer_desc& d, const QuantParams& p, cudaStream_t s);
 // decode_attention.cu
 struct DecodePlan {
-    int N, REP, P, TT, NT, S, NP, chunk;
+    int N, REP, P, TT, NT, S, NP, chunk, stages, per_sm;
     size_t smem;
 };
 bool decode_supported(int N, int REP);
