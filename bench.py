@@ -40,6 +40,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-quantize", action="store_true", help="skip the config-5 quantize measurement")
     a = ap.parse_args()
     a.warmup = max(a.warmup, 3)
     return a
@@ -222,6 +223,58 @@ def config_dict(w, world):
     }
 
 
+def bench_quantize_cfg5(dev, world, rank):
+    """BASELINE config 5: bulk prefill quantization of a 40-layer
+    LLaMA-2-13B-shaped KV cache (128 sequences x 2048 tokens, 40 heads x 128,
+    per-layer seeded outlier channels and reorder permutations, sink at token
+    0), batch-sharded.  Inputs are generated per layer on the device (214.7 GB
+    of fp16 K/V does not fit one GPU); only the quantize-append kernels are
+    timed (CUDA events on the stream)."""
+    import numpy as np
+    import torch
+
+    import paper_2501_16383_b200 as P
+    from paper_2501_16383_b200 import sharding
+    from paper_2501_16383_b200 import workload as WL
+
+    w = WL.CONFIGS[5]
+    _, B = sharding.batch_shard(w.batch, world, rank)
+    T, Cc = w.tokens, w.channels
+    stream = torch.cuda.current_stream(dev)
+    k = torch.empty(B, T, Cc, dtype=torch.float16, device=dev)
+    v = torch.empty_like(k)
+    flags = torch.zeros(B, T, dtype=torch.uint8)
+    flags[:, 0] = 1
+    total_ms = 0.0
+    layers = []
+    for layer in range(w.layers):
+        perm = WL.calibration_perm(w, SEED + 5, device=dev, layer=layer)
+        cfg = P.LayerConfig(batch=B, num_q_heads=w.num_q_heads, num_kv_heads=w.num_kv_heads,
+                            heads_per_group=w.heads_per_group, max_tokens=T, max_sinks=2, rope_base=w.rope_base)
+        lay = P.RotateKVLayer(cfg, perm, device=dev)
+        for b0 in range(0, B, 16):  # seeded per-layer inputs, generated in slices
+            kk, vv = WL.make_kv(w, SEED + 5 + 1000 * b0, min(16, B - b0), T, device=dev, layer=layer)
+            k[b0:b0 + kk.shape[0]].copy_(kk)
+            v[b0:b0 + vv.shape[0]].copy_(vv)
+            del kk, vv
+        if layer == 0:  # warm-up launch (same shapes)
+            lay.append(k, v, flags)
+            lay.reset()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        lay.append(k, v, flags)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        total_ms += e0.elapsed_time(e1)
+        layers.append(lay)  # keep the 40-layer cache resident (755 MB / layer at B=128)
+    rows = B * T * w.layers
+    bytes_ = rows * (2 * Cc * 2 + 2 * (Cc // 4 + Cc // 32))
+    return {"workload": w.name, "sequences_per_gpu": B, "layers": w.layers, "tokens": rows,
+            "ms": total_ms, "tokens_per_s_per_gpu": rows / (total_ms / 1e3),
+            "hbm_gbs": bytes_ / (total_ms / 1e3) / 1e9, "bytes": bytes_}
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -356,6 +409,22 @@ def run_ours(args):
         except Exception:
             traffic = None
 
+    quant5 = None
+    if not args.no_quantize:
+        del layer, ws
+        torch.cuda.empty_cache()
+        quant5 = bench_quantize_cfg5(dev, world, rank)
+        quant5["hbm_frac"] = quant5["hbm_gbs"] / peak_hbm()[0]
+        if world > 1:
+            import torch.distributed as dist
+
+            t = torch.tensor([quant5["ms"]], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            quant5["ms_max_over_ranks"] = t.item()
+            quant5["tokens_per_s"] = quant5["tokens"] * world / (t.item() / 1e3)
+        else:
+            quant5["tokens_per_s"] = quant5["tokens_per_s_per_gpu"]
+
     if world > 1:
         import torch.distributed as dist
 
@@ -397,6 +466,7 @@ def run_ours(args):
         "gpu_launches": 5 * args.steps,
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,
+        "quantize_cfg5": quant5,
     }
     print(json.dumps(line), flush=True)
 

@@ -1,7 +1,8 @@
 // quantize_kv.cu -- fused quantize-append for sm_100a.
 //
-// One CTA takes two new tokens of one sequence (a token pair shares every
-// register as a float2, so each FWHT butterfly is one FADD2):
+// Grid (X, B, 2): z selects K or V; a CTA loops over token pairs of one
+// sequence (every register holds a float2 = the same channel of the pair's
+// two tokens, so each FWHT butterfly is one FADD2):
 //   1. K rows: grouped-head FWHT over G KV heads (n = G*128) in registers
 //      (layout A -> smem transpose -> layout B, rkv_common.cuh), x 1/sqrt(n).
 //      V rows: per-head FWHT (n = 128).  Results land in shared memory.
@@ -125,131 +126,126 @@ __device__ __forceinline__ GroupQuant group_params(float mn, float mx, int scale
     return g;
 }
 
+// Grid (X, B, 2): z = 0 quantizes K rows, z = 1 V rows; each CTA loops over
+// token pairs blockIdx.x, blockIdx.x + X, ... of sequence b, so the slot ->
+// channel address table is built once per CTA.
 template <int N>
 __global__ void __launch_bounds__(256) quantize_kv_kernel(QuantParams p) {
     constexpr int LK = N >= 256 ? 16 : 8;
     extern __shared__ float4 smem4[];
     const int C = p.C, W = C / 16, MG = C / kQuantGroup;
-    float* rowK = reinterpret_cast<float*>(smem4);  // [2][C]
-    float* rowV = rowK + 2 * C;                     // [2][C]
-    uint16_t* kaddr = reinterpret_cast<uint16_t*>(rowV + 2 * C);  // [C]
-    uint16_t* vaddr = kaddr + C;                                  // [C]
+    float* row = reinterpret_cast<float*>(smem4);                // [2][C]
+    uint16_t* addr = reinterpret_cast<uint16_t*>(row + 2 * C);   // [C]
     __shared__ int s_slot[2];
 
     const int b = blockIdx.y;
-    const int64_t i0 = static_cast<int64_t>(blockIdx.x) * 2;
-    const bool has1 = i0 + 1 < p.num_new;
+    const bool isv = blockIdx.z == 1;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    const int64_t npairs = (p.num_new + 1) / 2;
 
-    for (int j = tid; j < C; j += blockDim.x) {
-        kaddr[j] = static_cast<uint16_t>(swz<N, LK>(__ldg(p.perm + j)));
-        vaddr[j] = static_cast<uint16_t>(swz<128, 8>(j));
-    }
-    // sink bookkeeping: slot = sink_count + #sinks among earlier new tokens of b
-    if (tid < 2) {
-        int slot = -1;
-        int64_t i = i0 + tid;
-        if (p.sink_flags && i < p.num_new && p.sink_flags[b * p.num_new + i]) {
-            int before = 0;
-            for (int64_t k = 0; k < i; ++k) before += p.sink_flags[b * p.num_new + k] ? 1 : 0;
-            slot = p.cache.sink_count[b] + before;
+    for (int j = tid; j < C; j += blockDim.x)
+        addr[j] = static_cast<uint16_t>(isv ? swz<128, 8>(j) : swz<N, LK>(__ldg(p.perm + j)));
+
+    for (int64_t pi = blockIdx.x; pi < npairs; pi += gridDim.x) {
+        const int64_t i0 = pi * 2;
+        const bool has1 = i0 + 1 < p.num_new;
+        // sink bookkeeping: slot = sink_count + #sinks among earlier new tokens of b
+        if (tid < 2) {
+            int slot = -1;
+            const int64_t i = i0 + tid;
+            if (p.sink_flags && i < p.num_new && p.sink_flags[b * p.num_new + i]) {
+                int before = 0;
+                for (int64_t k = 0; k < i; ++k) before += p.sink_flags[b * p.num_new + k] ? 1 : 0;
+                slot = p.cache.sink_count[b] + before;
+            }
+            s_slot[tid] = slot;
         }
-        s_slot[tid] = slot;
-    }
+        const uint16_t* src0 = (isv ? p.v_new : p.k_new) + (static_cast<int64_t>(b) * p.num_new + i0) * C;
+        const uint16_t* src1 = has1 ? src0 + C : src0;
+        __syncthreads();  // addr / s_slot ready; previous pair's reads of row done
 
-    const uint16_t* k0 = p.k_new + (static_cast<int64_t>(b) * p.num_new + i0) * C;
-    const uint16_t* v0 = p.v_new + (static_cast<int64_t>(b) * p.num_new + i0) * C;
-    const uint16_t* k1 = has1 ? k0 + C : k0;
-    const uint16_t* v1 = has1 ? v0 + C : v0;
-
-    // --- K: C/N grouped-head units, LK lanes each
-    {
-        constexpr int UPW = 32 / LK;
-        const int NG = C / N;
-        for (int ub = warp * UPW; ub < NG; ub += nwarps * UPW) {
-            int u = ub + lane / LK;
-            fwht_unit<N, LK>(k0, k1, rowK, rowK + C, u, lane % LK, u < NG, p.k_norm);
-        }
-    }
-    // --- V: per-head units (n = 128), 8 lanes each (proj/src/pipeline.cpp:120)
-    {
-        const int NU = C / 128;
-        for (int ub = warp * 4; ub < NU; ub += nwarps * 4) {
-            int u = ub + lane / 8;
-            fwht_unit<128, 8>(v0, v1, rowV, rowV + C, u, lane % 8, u < NU, p.v_norm);
-        }
-    }
-    __syncthreads();
-
-    // --- quantize: item = (token, K|V, word); 8 lanes = one 128-slot group
-    const int items = 4 * W;  // multiple of 32 (C % 128 == 0)
-    for (int base = warp * 32; base < items; base += nwarps * 32) {
-        const int it = base + lane;
-        const int tok = it / (2 * W);
-        const int kind = (it / W) & 1;  // 0 = K, 1 = V
-        const int w = it % W;
-        const float* row = (kind ? rowV : rowK) + tok * C;
-        const uint16_t* ad = (kind ? vaddr : kaddr) + 16 * w;
-        float x[16];
-        {
-            uint4 a0 = lds128(ad), a1 = lds128(ad + 8);
-            const uint16_t* h0 = reinterpret_cast<const uint16_t*>(&a0);
-            const uint16_t* h1 = reinterpret_cast<const uint16_t*>(&a1);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                x[e] = row[h0[e]];
-                x[8 + e] = row[h1[e]];
+        if (!isv) {  // K: C/N grouped-head units, LK lanes each
+            constexpr int UPW = 32 / LK;
+            const int NG = C / N;
+            for (int ub = warp * UPW; ub < NG; ub += nwarps * UPW) {
+                const int u = ub + lane / LK;
+                fwht_unit<N, LK>(src0, src1, row, row + C, u, lane % LK, u < NG, p.k_norm);
+            }
+        } else {  // V: per-head units (n = 128), 8 lanes each (proj/src/pipeline.cpp:120)
+            const int NU = C / 128;
+            for (int ub = warp * 4; ub < NU; ub += nwarps * 4) {
+                const int u = ub + lane / 8;
+                fwht_unit<128, 8>(src0, src1, row, row + C, u, lane % 8, u < NU, p.v_norm);
             }
         }
-        float mn = x[0], mx = x[0];
-#pragma unroll
-        for (int e = 1; e < 16; ++e) {
-            mn = fminf(mn, x[e]);
-            mx = fmaxf(mx, x[e]);
-        }
-#pragma unroll
-        for (int o = 1; o < 8; o <<= 1) {
-            mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        }
-        GroupQuant gq{};
-        if ((lane & 7) == 0) gq = group_params(mn, mx, p.scale_format);
-        const int leader = lane & ~7;
-        gq.t1 = __shfl_sync(0xffffffffu, gq.t1, leader);
-        gq.t2 = __shfl_sync(0xffffffffu, gq.t2, leader);
-        gq.t3 = __shfl_sync(0xffffffffu, gq.t3, leader);
-        uint32_t word = 0;
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-            uint32_t c = (x[e] >= gq.t1) + (x[e] >= gq.t2) + (x[e] >= gq.t3);
-            word |= c << (2 * e);
-        }
-        const bool valid = tok == 0 || has1;
-        if (valid) {
-            const int64_t pos = p.start_pos[b] + i0 + tok;
-            const bool sink = s_slot[tok] >= 0;
-            const int64_t rowi = static_cast<int64_t>(b) * p.max_tokens + pos;
-            uint32_t* codes = kind ? p.cache.v_codes : p.cache.k_codes;
-            uint32_t* meta = kind ? p.cache.v_meta : p.cache.k_meta;
-            codes[rowi * W + w] = sink ? 0u : word;
-            if ((lane & 7) == 0) meta[rowi * MG + w / 8] = sink ? 0u : gq.meta;
-        }
-    }
+        __syncthreads();
 
-    // --- sink rows: raw fp16 K/V into the sidecar (exact, proj/tests/test_kv_cache.cpp:22-45)
+        // quantize: item = (token, word); 8 lanes = one 128-slot group
+        const int items = 2 * W;  // multiple of 32 (C % 256 == 0)
+        for (int base = warp * 32; base < items; base += nwarps * 32) {
+            const int it = base + lane;
+            const int tok = it / W;
+            const int w = it - tok * W;
+            const float* rw = row + tok * C;
+            const uint16_t* ad = addr + 16 * w;
+            float x[16];
+            {
+                const uint4 a0 = lds128(ad), a1 = lds128(ad + 8);
+                const uint16_t* h0 = reinterpret_cast<const uint16_t*>(&a0);
+                const uint16_t* h1 = reinterpret_cast<const uint16_t*>(&a1);
 #pragma unroll
-    for (int tok = 0; tok < 2; ++tok) {
-        const int slot = s_slot[tok];
-        if (slot < 0 || slot >= p.max_sinks) continue;
-        const uint4* ks = reinterpret_cast<const uint4*>(tok ? k1 : k0);
-        const uint4* vs = reinterpret_cast<const uint4*>(tok ? v1 : v0);
-        uint4* kd = reinterpret_cast<uint4*>(p.cache.sink_k + (static_cast<int64_t>(b) * p.max_sinks + slot) * C);
-        uint4* vd = reinterpret_cast<uint4*>(p.cache.sink_v + (static_cast<int64_t>(b) * p.max_sinks + slot) * C);
-        for (int j = tid; j < C / 8; j += blockDim.x) {
-            kd[j] = __ldg(ks + j);
-            vd[j] = __ldg(vs + j);
+                for (int e = 0; e < 8; ++e) {
+                    x[e] = rw[h0[e]];
+                    x[8 + e] = rw[h1[e]];
+                }
+            }
+            float mn = x[0], mx = x[0];
+#pragma unroll
+            for (int e = 1; e < 16; ++e) {
+                mn = fminf(mn, x[e]);
+                mx = fmaxf(mx, x[e]);
+            }
+#pragma unroll
+            for (int o = 1; o < 8; o <<= 1) {
+                mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+                mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            }
+            GroupQuant gq{};
+            if ((lane & 7) == 0) gq = group_params(mn, mx, p.scale_format);
+            const int leader = lane & ~7;
+            gq.t1 = __shfl_sync(0xffffffffu, gq.t1, leader);
+            gq.t2 = __shfl_sync(0xffffffffu, gq.t2, leader);
+            gq.t3 = __shfl_sync(0xffffffffu, gq.t3, leader);
+            uint32_t word = 0;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                const uint32_t c = (x[e] >= gq.t1) + (x[e] >= gq.t2) + (x[e] >= gq.t3);
+                word |= c << (2 * e);
+            }
+            if (tok == 0 || has1) {
+                const int64_t pos = p.start_pos[b] + i0 + tok;
+                const bool sink = s_slot[tok] >= 0;
+                const int64_t rowi = static_cast<int64_t>(b) * p.max_tokens + pos;
+                uint32_t* codes = isv ? p.cache.v_codes : p.cache.k_codes;
+                uint32_t* meta = isv ? p.cache.v_meta : p.cache.k_meta;
+                codes[rowi * W + w] = sink ? 0u : word;
+                if ((lane & 7) == 0) meta[rowi * MG + w / 8] = sink ? 0u : gq.meta;
+            }
         }
-        if (tid == 0) p.cache.sink_pos[b * p.max_sinks + slot] = static_cast<int32_t>(p.start_pos[b] + i0 + tok);
+
+        // sink rows: raw fp16 rows into the sidecar (exact, proj/tests/test_kv_cache.cpp:22-45)
+#pragma unroll
+        for (int tok = 0; tok < 2; ++tok) {
+            const int slot = s_slot[tok];
+            if (slot < 0 || slot >= p.max_sinks) continue;
+            const uint4* srcr = reinterpret_cast<const uint4*>(tok ? src1 : src0);
+            uint16_t* side = isv ? p.cache.sink_v : p.cache.sink_k;
+            uint4* dst = reinterpret_cast<uint4*>(side + (static_cast<int64_t>(b) * p.max_sinks + slot) * C);
+            for (int j = tid; j < C / 8; j += blockDim.x) dst[j] = __ldg(srcr + j);
+            if (tid == 0 && !isv)
+                p.cache.sink_pos[b * p.max_sinks + slot] = static_cast<int32_t>(p.start_pos[b] + i0 + tok);
+        }
+        __syncthreads();  // s_slot and row are rewritten by the next pair
     }
 }
 
@@ -281,11 +277,21 @@ __global__ void quantize_finalize_kernel(QuantParams p) {
 
 template <int N>
 cudaError_t launch_quantize_n(const QuantParams& p, int B, cudaStream_t s) {
-    const size_t smem = static_cast<size_t>(p.C) * (4 * sizeof(float) + 2 * sizeof(uint16_t));
+    const size_t smem = static_cast<size_t>(p.C) * (2 * sizeof(float) + sizeof(uint16_t));
     cudaError_t e = cudaFuncSetAttribute(quantize_kv_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    dim3 grid(static_cast<unsigned>((p.num_new + 1) / 2), static_cast<unsigned>(B));
+    int per_sm = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, quantize_kv_kernel<N>, 256, smem) != cudaSuccess) {
+        cudaGetLastError();
+        per_sm = 1;
+    }
+    const int64_t npairs = (p.num_new + 1) / 2;
+    // enough CTAs for ~4 waves; each loops over token pairs (amortises the address table)
+    int64_t x = (static_cast<int64_t>(num_sms()) * (per_sm > 0 ? per_sm : 1) * 4 + 2 * B - 1) / (2 * B);
+    if (x > npairs) x = npairs;
+    if (x < 1) x = 1;
+    dim3 grid(static_cast<unsigned>(x), static_cast<unsigned>(B), 2);
     quantize_kv_kernel<N><<<grid, 256, smem, s>>>(p);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
