@@ -116,6 +116,7 @@ rkv_status rkv_rope_table_init(const rkv_layer_desc* desc, float* table, int64_t
  *   perm         : [C] int32, slot j <- channel perm[j] (ReorderPlan::perm[layer])
  *   sink_flags   : [B][num_new] u8 (1 = keep the token in the fp16 sidecar), or NULL
  *   start_pos    : [B] int64, cache index of each sequence's first new token
+ * k_new, v_new and perm must be 16-byte aligned (TMA / vector loads).
  * Tokens are written at start_pos[b] .. start_pos[b]+num_new-1.  The device
  * cannot throw: callers (the C++ layer) validate capacities first. */
 rkv_status rkv_quantize_kv(const rkv_layer_desc* desc, const uint16_t* k_new, const uint16_t* v_new,

@@ -1,18 +1,33 @@
 // quantize_kv.cu -- fused quantize-append for sm_100a.
 //
-// Grid (X, B, 2): z selects K or V; a CTA loops over token pairs of one
-// sequence (every register holds a float2 = the same channel of the pair's
-// two tokens, so each FWHT butterfly is one FADD2):
-//   1. K rows: grouped-head FWHT over G KV heads (n = G*128) in registers
-//      (layout A -> smem transpose -> layout B, rkv_common.cuh), x 1/sqrt(n).
-//      V rows: per-head FWHT (n = 128).  Results land in shared memory.
-//   2. Each thread owns one packed word (16 slots).  K slots gather their
-//      channel through the calibrated permutation (slot j <- channel perm[j],
-//      proj/src/reorder.cpp:112-128); 8 consecutive lanes form one 128-slot
-//      quant group: min/max by shuffles, the group leader derives the stored
-//      scale / zero in double exactly as proj/src/quant.cpp:53-97 does and
-//      turns the reference's round-half-away division into three float
-//      thresholds, so code = (x>=T1)+(x>=T2)+(x>=T3) is bit-identical.
+// One work item = (K or V, sequence b, token pair).  A persistent CTA walks
+// items blockIdx.x, blockIdx.x + gridDim.x, ...; the pair's two fp16 rows
+// (contiguous in [B][num_new][C]) arrive by one TMA bulk copy into a
+// double-buffered stage, so the next item's rows stream in while this one is
+// computed.  Every register holds a float2 = one channel of both tokens, so
+// each FWHT butterfly, normalisation and threshold subtraction is one
+// packed FP32x2 instruction.
+//
+//   1. FWHT (thread g owns channels [32g, 32g+32) = its "region"):
+//      layout A: registers = channel bits 0..4 (5 stages), result to the
+//      token-pair row in shared memory (float4 = 2 channels x 2 tokens,
+//      16-byte chunks XOR-swizzled by region);  layout B': lane lam of a
+//      unit holds chunk pairs lam + L*j, registers = channel bit 0 and the
+//      high bits (stages 5 .. log2(n)-1), x 1/sqrt(n), back to the row.
+//      K units: n = G*128 channels (grouped-head rotation), V: n = 128.
+//      The fp16 rows are read in a per-lane XOR-relabelled chunk order so the
+//      LDS.128 stream is bank-conflict free; the relabelling turns into a
+//      +-1 per 8-channel block after the A stages (H P_s = D_s H), applied
+//      exactly before the row is stored.
+//   2. Quantize (thread g owns slots [32g, 32g+32) = two packed words per
+//      token; 4 lanes = one 128-slot group).  K slots gather their channel
+//      through the calibrated permutation (slot j <- channel perm[j],
+//      proj/src/reorder.cpp:112-128) via a per-CTA byte-offset table; V slots
+//      are the natural channels.  Group min/max by shuffles; one lane per
+//      (group, token) derives scale / zero as proj/src/quant.cpp:53-97 does and
+//      turns round-half-away(x/s) + zero into three exact fp32 thresholds, so
+//      code = #{k : x >= T_k} -- taken from the sign bits of x - T_k (one
+//      FADD2 covers both tokens) and packed with funnel shifts.
 //   3. Sink tokens (proj/src/kv_cache.cpp:8-22 `sink`) keep their raw fp16
 //      rows in the sidecar; their packed words/meta are zero.
 // Reference chain restated: rotate_rows -> apply_reorder -> quantize_token ->
@@ -26,62 +41,17 @@ namespace rkv {
 
 namespace {
 
-// Shared-memory swizzle of an N-point unit region (see rkv_common.cuh):
-// XOR the float4-chunk index with the owning lane (conflict-free layout-A
-// float4 traffic) and the unit index with the lane-group slot inside a warp
-// (conflict-free layout-B scalar traffic).
-template <int N, int L>
-__device__ __forceinline__ int swz(int c) {
-    constexpr int R = N / L;
-    constexpr int LR = ilog2(R), LN = ilog2(N), LL = ilog2(L);
-    return c ^ (((c >> LR) & (R / 4 - 1)) << 2) ^ (((c >> LN) & (32 / L - 1)) << LL);
-}
+// float2 index (one channel of both tokens) of channel c in the token-pair
+// row: 32-channel regions padded to 33 slots, so layout-A stores (one region
+// per lane), layout-B reads (consecutive channels of one region per unit) and
+// the V quantize reads are bank-conflict free per half-warp with plain
+// [reg + immediate] addressing.
+__device__ __forceinline__ int pos2(int c) { return (c >> 5) * 33 + (c & 31); }
 
-// FWHT of unit u (N contiguous channels) of two fp16 rows into smem rows
-// dst0/dst1 (natural order, swizzled).  Lanes of the unit: lam = 0..L-1.
-template <int N, int L>
-__device__ __forceinline__ void fwht_unit(const uint16_t* __restrict__ src0, const uint16_t* __restrict__ src1,
-                                          float* dst0, float* dst1, int u, int lam, bool active, float norm) {
-    constexpr int R = N / L;
-    constexpr int LR = ilog2(R), LN = ilog2(N), LL = ilog2(L);
-    float2 x[R];
-    if (active) {
-        const uint4* a = reinterpret_cast<const uint4*>(src0 + u * N + lam * R);
-        const uint4* b = reinterpret_cast<const uint4*>(src1 + u * N + lam * R);
-#pragma unroll
-        for (int q = 0; q < R / 8; ++q) {
-            uint4 va = __ldg(a + q), vb = __ldg(b + q);
-            const uint16_t* ha = reinterpret_cast<const uint16_t*>(&va);
-            const uint16_t* hb = reinterpret_cast<const uint16_t*>(&vb);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) x[8 * q + e] = make_float2(h2f(ha[e]), h2f(hb[e]));
-        }
-        bfly_range<R, 0, LR>(x);  // index bits 0 .. LR-1
-#pragma unroll
-        for (int q = 0; q < R / 4; ++q) {
-            int p = swz<N, L>(u * N + lam * R + 4 * q);
-            *reinterpret_cast<float4*>(dst0 + p) = make_float4(x[4 * q].x, x[4 * q + 1].x, x[4 * q + 2].x, x[4 * q + 3].x);
-            *reinterpret_cast<float4*>(dst1 + p) = make_float4(x[4 * q].y, x[4 * q + 1].y, x[4 * q + 2].y, x[4 * q + 3].y);
-        }
-    }
-    __syncwarp();
-    if (active) {
-#pragma unroll
-        for (int j = 0; j < R; ++j) {
-            int p = swz<N, L>(u * N + lam + L * j);
-            x[j] = make_float2(dst0[p], dst1[p]);
-        }
-        bfly_range<R, LR - LL, LN - LL>(x);  // index bits LR .. LN-1
-        const float2 nn = make_float2(norm, norm);
-#pragma unroll
-        for (int j = 0; j < R; ++j) {
-            int p = swz<N, L>(u * N + lam + L * j);
-            float2 y = mul2(x[j], nn);
-            dst0[p] = y.x;
-            dst1[p] = y.y;
-        }
-    }
-    __syncwarp();
+// STS.64 straight from an FP32x2 result pair (a plain float2 store makes the
+// compiler copy the pair first).
+__device__ __forceinline__ void sts64(uint32_t addr, float2 v) {
+    asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(v.x), "f"(v.y) : "memory");
 }
 
 struct GroupQuant {
@@ -89,147 +59,274 @@ struct GroupQuant {
     uint32_t meta;
 };
 
-// proj/src/quant.cpp:74-94 for bits = 2, evaluated once per group.
-__device__ __forceinline__ GroupQuant group_params(float mn, float mx, int scale_format) {
-    double range = __dsub_rn(static_cast<double>(mx), static_cast<double>(mn));
+// proj/src/quant.cpp:74-94 for bits = 2 (scale rounded up to fp16
+// or e4m3 as in the reference).
+//   zero = clamp(rhaz(-mn / s), 0, 3): RN64(-mn/s) >= k + 0.5 exactly when
+//   -mn >= (k + 0.5) s (mn is fp32, s has <= 11 significant bits, so the
+//   quotient's rounding can never reach k + 0.5 from below), and (k + 0.5) s
+//   is exact in fp32.
+//   code >= k  <=>  rhaz(x/s) >= m := k - zero  <=>  x >= (m - 0.5) s (m >= 1),
+//   x > (m - 0.5) s (m <= 0); (m - 0.5) s is exact in fp32 and the strict
+//   case becomes >= on the next float up.
+template <int FMT>
+__device__ __forceinline__ GroupQuant group_params(float mn, float mx) {
+    const double range = __dsub_rn(static_cast<double>(mx), static_cast<double>(mn));
     float raw = __double2float_rn(__ddiv_rn(range, 3.0));
     if (raw < 1e-8f) raw = 1e-8f;
     uint16_t sbits;
     float sf;
-    if (scale_format == RKV_SCALE_E4M3_CEIL) {
+    if constexpr (FMT == RKV_SCALE_E4M3_CEIL) {
         sf = e4m3_ceil_value(raw);
         sbits = __half_as_ushort(__float2half_rn(sf));  // exact: e4m3 values are fp16 values
     } else {
         sbits = fp16_ceil(raw);
         sf = __half2float(__ushort_as_half(sbits));
     }
-    const double s = static_cast<double>(sf);
-    double zero = round(__ddiv_rn(-static_cast<double>(mn), s));
-    zero = fmin(fmax(zero, 0.0), 3.0);
-    GroupQuant g;
+    const float nm = -mn;
+    const int z = (nm >= 0.5f * sf) + (nm >= 1.5f * sf) + (nm >= 2.5f * sf);
     float t[3];
 #pragma unroll
     for (int k = 1; k <= 3; ++k) {
-        // code >= k  <=>  round_half_away(x/s) >= k - zero  (m = k - zero)
-        //            <=>  x >= (m - 0.5) s  for m >= 1,  x > (m - 0.5) s  for m <= 0
-        double m = static_cast<double>(k) - zero;
-        double tt = __dmul_rn(m - 0.5, s);  // exact: (m-0.5) has 3 bits, s has 11
-        float f = __double2float_ru(tt);
-        if (m <= 0.0 && static_cast<double>(f) == tt) f = nextafterf(f, INFINITY);
-        t[k - 1] = f;
+        const int m = k - z;
+        float tt = __fmul_rn(static_cast<float>(m) - 0.5f, sf);
+        if (m <= 0) tt = __uint_as_float(__float_as_uint(tt) - 1u);  // tt < 0: next float toward +inf
+        t[k - 1] = tt;
     }
+    GroupQuant g;
     g.t1 = t[0];
     g.t2 = t[1];
     g.t3 = t[2];
-    g.meta = static_cast<uint32_t>(sbits) |
-             (static_cast<uint32_t>(__half_as_ushort(__float2half_rn(static_cast<float>(zero)))) << 16);
+    g.meta = static_cast<uint32_t>(sbits) | (static_cast<uint32_t>(__half_as_ushort(__int2half_rn(z))) << 16);
     return g;
 }
 
-// Grid (X, B, 2): z = 0 quantizes K rows, z = 1 V rows; each CTA loops over
-// token pairs blockIdx.x, blockIdx.x + X, ... of sequence b, so the slot ->
-// channel address table is built once per CTA.
+// Layout-A half of the FWHT for region g: channels [32g, 32g+32) of both
+// tokens from the fp16 stage rows, stages on channel bits 0..4, stored to the
+// token-pair row.
+__device__ __forceinline__ void fwht_region_a(const uint16_t* st0, const uint16_t* st1, float2* row, int g) {
+    float2 x[32];
+    const int s = (g >> 1) & 3;  // chunk relabel: conflict-free 64-byte-strided LDS.128
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const uint4 va = lds128(st0 + 32 * g + 8 * (q ^ s));
+        const uint4 vb = lds128(st1 + 32 * g + 8 * (q ^ s));
+        const uint16_t* ha = reinterpret_cast<const uint16_t*>(&va);
+        const uint16_t* hb = reinterpret_cast<const uint16_t*>(&vb);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) x[8 * q + e] = make_float2(h2f(ha[e]), h2f(hb[e]));
+    }
+    bfly_range<32, 0, 5>(x);
+    // block q now holds true block q times (-1)^popcount(q & s)
+    const float f1 = (s & 1) ? -1.0f : 1.0f, f2 = (s & 2) ? -1.0f : 1.0f;
+    const float2 sg1 = make_float2(f1, f1), sg2 = make_float2(f2, f2), sg3 = make_float2(f1 * f2, f1 * f2);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        x[8 + e] = mul2(x[8 + e], sg1);
+        x[16 + e] = mul2(x[16 + e], sg2);
+        x[24 + e] = mul2(x[24 + e], sg3);
+    }
+    const uint32_t dst = smem_u32(row + 33 * g);
+#pragma unroll
+    for (int c = 0; c < 32; ++c) sts64(dst + 8 * c, x[c]);
+}
+
+// Layout-B half: lane lam of an n-channel unit u (L = n/32 lanes) holds the
+// channels u*n + lam + L*j, j = 0..31; stages on channel bits 5..log2(n)-1,
+// then x norm, back in place.
 template <int N>
-__global__ void __launch_bounds__(256) quantize_kv_kernel(QuantParams p) {
-    constexpr int LK = N >= 256 ? 16 : 8;
-    extern __shared__ float4 smem4[];
-    const int C = p.C, W = C / 16, MG = C / kQuantGroup;
-    float* row = reinterpret_cast<float*>(smem4);                // [2][C]
-    uint16_t* addr = reinterpret_cast<uint16_t*>(row + 2 * C);   // [C]
+__device__ __forceinline__ void fwht_unit_b(float2* row, int u, int lam, float norm) {
+    constexpr int L = N / 32, LL = ilog2(L), LN = ilog2(N);
+    float2 x[32];
+    float2* base = row + 33 * (u * L) + lam;  // channel u*N + lam + L*j -> base + pos2(L*j)
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = base[pos2(L * j)];
+    bfly_range<32, 5 - LL, LN - LL>(x);
+    const float2 nn = make_float2(norm, norm);
+    const uint32_t b32 = smem_u32(base);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) sts64(b32 + 8 * pos2(L * j), mul2(x[j], nn));
+}
+
+// Slots [32g, 32g+32) of both tokens -> two packed words per token + group meta.
+struct QuantOut {
+    uint32_t w[2][2];  // [token][word]
+    uint32_t meta;     // this lane's (group, token) meta: lane&3 == 0 -> token 0, == 1 -> token 1
+};
+
+// sign bits of x - T_k for 8 consecutive slots of one token -> 16 code bits
+// (inverted: bit set = below threshold).  bit1 = sign(d2),
+// bit0 = sign(d1) ^ sign(d2) ^ sign(d3)  (T1 <= T2 <= T3).
+template <int TOK>
+__device__ __forceinline__ uint32_t code_bits8(const float2* x, float2 n1, float2 n2, float2 n3) {
+    uint32_t a = 0;
+#pragma unroll
+    for (int e = 7; e >= 0; --e) {
+        const float2 d1 = add2(x[e], n1), d2 = add2(x[e], n2), d3 = add2(x[e], n3);
+        const float s1 = TOK ? d1.y : d1.x, s2 = TOK ? d2.y : d2.x, s3 = TOK ? d3.y : d3.x;
+        a = __funnelshift_l(__float_as_uint(s2), a, 1);
+        a = __funnelshift_l(__float_as_uint(s1) ^ __float_as_uint(s2) ^ __float_as_uint(s3), a, 1);
+    }
+    return a;
+}
+
+template <int FMT>
+__device__ __forceinline__ QuantOut quantize_run(const float2 (&x)[32], int lane) {
+    float mn0 = x[0].x, mx0 = x[0].x, mn1 = x[0].y, mx1 = x[0].y;
+#pragma unroll
+    for (int e = 1; e < 31; e += 2) {
+        mn0 = fminf(mn0, fminf(x[e].x, x[e + 1].x));
+        mx0 = fmaxf(mx0, fmaxf(x[e].x, x[e + 1].x));
+        mn1 = fminf(mn1, fminf(x[e].y, x[e + 1].y));
+        mx1 = fmaxf(mx1, fmaxf(x[e].y, x[e + 1].y));
+    }
+    mn0 = fminf(mn0, x[31].x);
+    mx0 = fmaxf(mx0, x[31].x);
+    mn1 = fminf(mn1, x[31].y);
+    mx1 = fmaxf(mx1, x[31].y);
+#pragma unroll
+    for (int o = 1; o < 4; o <<= 1) {
+        mn0 = fminf(mn0, __shfl_xor_sync(0xffffffffu, mn0, o));
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
+        mn1 = fminf(mn1, __shfl_xor_sync(0xffffffffu, mn1, o));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+    }
+    const bool odd = lane & 1;
+    const GroupQuant gq = group_params<FMT>(odd ? mn1 : mn0, odd ? mx1 : mx0);
+    const int l0 = lane & ~3;
+    const float2 n1 = make_float2(-__shfl_sync(0xffffffffu, gq.t1, l0), -__shfl_sync(0xffffffffu, gq.t1, l0 + 1));
+    const float2 n2 = make_float2(-__shfl_sync(0xffffffffu, gq.t2, l0), -__shfl_sync(0xffffffffu, gq.t2, l0 + 1));
+    const float2 n3 = make_float2(-__shfl_sync(0xffffffffu, gq.t3, l0), -__shfl_sync(0xffffffffu, gq.t3, l0 + 1));
+    QuantOut o;
+    o.meta = gq.meta;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        o.w[0][h] = ~__byte_perm(code_bits8<0>(x + 16 * h, n1, n2, n3), code_bits8<0>(x + 16 * h + 8, n1, n2, n3),
+                                 0x5410);
+        o.w[1][h] = ~__byte_perm(code_bits8<1>(x + 16 * h, n1, n2, n3), code_bits8<1>(x + 16 * h + 8, n1, n2, n3),
+                                 0x5410);
+    }
+    return o;
+}
+
+struct Item {
+    bool isv, has1;
+    int b;
+    int i0;
+};
+
+__device__ __forceinline__ Item decode_item(uint32_t it, uint32_t npairs, int num_new) {
+    Item r;
+    r.isv = it & 1u;
+    const uint32_t rest = it >> 1;
+    const uint32_t b = rest / npairs;
+    r.b = static_cast<int>(b);
+    r.i0 = static_cast<int>(rest - b * npairs) * 2;
+    r.has1 = r.i0 + 1 < num_new;
+    return r;
+}
+
+__device__ __forceinline__ void issue_item(const QuantParams& p, uint32_t it, uint32_t npairs, uint16_t* dst,
+                                           uint64_t* bar) {
+    const Item r = decode_item(it, npairs, static_cast<int>(p.num_new));
+    const uint16_t* src = (r.isv ? p.v_new : p.k_new) + (static_cast<int64_t>(r.b) * p.num_new + r.i0) * p.C;
+    const uint32_t bytes = static_cast<uint32_t>((r.has1 ? 2 : 1) * p.C * 2);
+    mbar_arrive_expect_tx(bar, bytes);
+    bulk_g2s(dst, src, bytes, bar);
+}
+
+// Shared memory: row [C/32][33] float2 (8.25 C B) | gather table [8][C/32] of
+// 4 x u16 float2 indices (2C B) | stage [2][C] fp16 (4C B).  One stage buffer:
+// the next item's TMA is issued as soon as every warp has finished layout A.
+template <int N, int FMT>
+__global__ void __launch_bounds__(256, 2) quantize_kv_kernel(QuantParams p, uint32_t items, uint32_t npairs) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ uint64_t bar;
     __shared__ int s_slot[2];
+    const int C = p.C, G32 = C / 32, W = C / 16, MG = C / kQuantGroup;
+    const int num_new = static_cast<int>(p.num_new);
+    float2* row = reinterpret_cast<float2*>(smem);
+    uint16_t* tbl = reinterpret_cast<uint16_t*>(smem + G32 * 33 * 8);
+    uint16_t* stage = reinterpret_cast<uint16_t*>(smem + G32 * 33 * 8 + 2 * C);
 
-    const int b = blockIdx.y;
-    const bool isv = blockIdx.z == 1;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-    const int64_t npairs = (p.num_new + 1) / 2;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const bool act = tid < G32;
+    const int g = act ? tid : tid - 16;  // C/32 is a multiple of 16: idle half-warps mirror the previous one
 
-    for (int j = tid; j < C; j += blockDim.x)
-        addr[j] = static_cast<uint16_t>(isv ? swz<128, 8>(j) : swz<N, LK>(__ldg(p.perm + j)));
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        mbar_fence_init();
+        if (blockIdx.x < items) issue_item(p, blockIdx.x, npairs, stage, &bar);
+    }
+    // K gather table, only if this CTA sees a K item (even item index):
+    // slot j = 32t + 4q + e  ->  tbl[(q * G32 + t) * 4 + e] = float2 index of channel perm[j]
+    if (act && ((gridDim.x & 1u) || !(blockIdx.x & 1u))) {
+        const int4* pv = reinterpret_cast<const int4*>(p.perm) + 8 * g;
+        int4 v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = __ldg(pv + q);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const uint32_t lo = static_cast<uint32_t>(pos2(v[q].x)) | (static_cast<uint32_t>(pos2(v[q].y)) << 16);
+            const uint32_t hi = static_cast<uint32_t>(pos2(v[q].z)) | (static_cast<uint32_t>(pos2(v[q].w)) << 16);
+            *reinterpret_cast<uint2*>(tbl + (q * G32 + g) * 4) = make_uint2(lo, hi);
+        }
+    }
+    __syncthreads();
 
-    for (int64_t pi = blockIdx.x; pi < npairs; pi += gridDim.x) {
-        const int64_t i0 = pi * 2;
-        const bool has1 = i0 + 1 < p.num_new;
+    uint32_t k = 0;
+    for (uint32_t it = blockIdx.x; it < items; it += gridDim.x, ++k) {
+        const Item r = decode_item(it, npairs, num_new);
         // sink bookkeeping: slot = sink_count + #sinks among earlier new tokens of b
         if (tid < 2) {
             int slot = -1;
-            const int64_t i = i0 + tid;
-            if (p.sink_flags && i < p.num_new && p.sink_flags[b * p.num_new + i]) {
+            const int i = r.i0 + tid;
+            if (p.sink_flags && i < num_new && p.sink_flags[static_cast<int64_t>(r.b) * num_new + i]) {
                 int before = 0;
-                for (int64_t k = 0; k < i; ++k) before += p.sink_flags[b * p.num_new + k] ? 1 : 0;
-                slot = p.cache.sink_count[b] + before;
+                for (int q = 0; q < i; ++q) before += p.sink_flags[static_cast<int64_t>(r.b) * num_new + q] ? 1 : 0;
+                slot = p.cache.sink_count[r.b] + before;
             }
             s_slot[tid] = slot;
         }
-        const uint16_t* src0 = (isv ? p.v_new : p.k_new) + (static_cast<int64_t>(b) * p.num_new + i0) * C;
-        const uint16_t* src1 = has1 ? src0 + C : src0;
-        __syncthreads();  // addr / s_slot ready; previous pair's reads of row done
+        mbar_wait(&bar, k & 1u);
 
-        if (!isv) {  // K: C/N grouped-head units, LK lanes each
-            constexpr int UPW = 32 / LK;
-            const int NG = C / N;
-            for (int ub = warp * UPW; ub < NG; ub += nwarps * UPW) {
-                const int u = ub + lane / LK;
-                fwht_unit<N, LK>(src0, src1, row, row + C, u, lane % LK, u < NG, p.k_norm);
-            }
-        } else {  // V: per-head units (n = 128), 8 lanes each (proj/src/pipeline.cpp:120)
-            const int NU = C / 128;
-            for (int ub = warp * 4; ub < NU; ub += nwarps * 4) {
-                const int u = ub + lane / 8;
-                fwht_unit<128, 8>(src0, src1, row, row + C, u, lane % 8, u < NU, p.v_norm);
-            }
+        fwht_region_a(stage, r.has1 ? stage + C : stage, row, g);
+        __syncwarp();
+        if (!r.isv) {
+            fwht_unit_b<N>(row, g / (N / 32), g % (N / 32), p.k_norm);
+        } else {
+            fwht_unit_b<128>(row, g / 4, g % 4, p.v_norm);
         }
-        __syncthreads();
+        __syncthreads();  // stage consumed, row complete, s_slot visible
+        if (tid == 0 && it + gridDim.x < items) issue_item(p, it + gridDim.x, npairs, stage, &bar);
 
-        // quantize: item = (token, word); 8 lanes = one 128-slot group
-        const int items = 2 * W;  // multiple of 32 (C % 256 == 0)
-        for (int base = warp * 32; base < items; base += nwarps * 32) {
-            const int it = base + lane;
-            const int tok = it / W;
-            const int w = it - tok * W;
-            const float* rw = row + tok * C;
-            const uint16_t* ad = addr + 16 * w;
-            float x[16];
-            {
-                const uint4 a0 = lds128(ad), a1 = lds128(ad + 8);
-                const uint16_t* h0 = reinterpret_cast<const uint16_t*>(&a0);
-                const uint16_t* h1 = reinterpret_cast<const uint16_t*>(&a1);
+        float2 x[32];
+        if (!r.isv) {
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    x[e] = rw[h0[e]];
-                    x[8 + e] = rw[h1[e]];
-                }
+            for (int q = 0; q < 8; ++q) {
+                const uint2 a = *reinterpret_cast<const uint2*>(tbl + (q * G32 + g) * 4);
+                x[4 * q + 0] = row[a.x & 0xffffu];
+                x[4 * q + 1] = row[a.x >> 16];
+                x[4 * q + 2] = row[a.y & 0xffffu];
+                x[4 * q + 3] = row[a.y >> 16];
             }
-            float mn = x[0], mx = x[0];
+        } else {
+            const float2* src = row + 33 * g;
 #pragma unroll
-            for (int e = 1; e < 16; ++e) {
-                mn = fminf(mn, x[e]);
-                mx = fmaxf(mx, x[e]);
-            }
+            for (int c = 0; c < 32; ++c) x[c] = src[c];
+        }
+        const QuantOut qo = quantize_run<FMT>(x, lane);
+        if (act) {
+            uint32_t* codes = r.isv ? p.cache.v_codes : p.cache.k_codes;
+            uint32_t* meta = r.isv ? p.cache.v_meta : p.cache.k_meta;
+            const int64_t row0 = static_cast<int64_t>(r.b) * p.max_tokens + p.start_pos[r.b] + r.i0;
 #pragma unroll
-            for (int o = 1; o < 8; o <<= 1) {
-                mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-                mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-            }
-            GroupQuant gq{};
-            if ((lane & 7) == 0) gq = group_params(mn, mx, p.scale_format);
-            const int leader = lane & ~7;
-            gq.t1 = __shfl_sync(0xffffffffu, gq.t1, leader);
-            gq.t2 = __shfl_sync(0xffffffffu, gq.t2, leader);
-            gq.t3 = __shfl_sync(0xffffffffu, gq.t3, leader);
-            uint32_t word = 0;
-#pragma unroll
-            for (int e = 0; e < 16; ++e) {
-                const uint32_t c = (x[e] >= gq.t1) + (x[e] >= gq.t2) + (x[e] >= gq.t3);
-                word |= c << (2 * e);
-            }
-            if (tok == 0 || has1) {
-                const int64_t pos = p.start_pos[b] + i0 + tok;
+            for (int tok = 0; tok < 2; ++tok) {
+                if (tok == 1 && !r.has1) break;
                 const bool sink = s_slot[tok] >= 0;
-                const int64_t rowi = static_cast<int64_t>(b) * p.max_tokens + pos;
-                uint32_t* codes = isv ? p.cache.v_codes : p.cache.k_codes;
-                uint32_t* meta = isv ? p.cache.v_meta : p.cache.k_meta;
-                codes[rowi * W + w] = sink ? 0u : word;
-                if ((lane & 7) == 0) meta[rowi * MG + w / 8] = sink ? 0u : gq.meta;
+                const int64_t rowi = row0 + tok;
+                *reinterpret_cast<uint2*>(codes + rowi * W + 2 * g) =
+                    sink ? make_uint2(0u, 0u) : make_uint2(qo.w[tok][0], qo.w[tok][1]);
+                if ((lane & 3) == tok) meta[rowi * MG + g / 4] = sink ? 0u : qo.meta;
             }
         }
 
@@ -238,14 +335,15 @@ __global__ void __launch_bounds__(256) quantize_kv_kernel(QuantParams p) {
         for (int tok = 0; tok < 2; ++tok) {
             const int slot = s_slot[tok];
             if (slot < 0 || slot >= p.max_sinks) continue;
-            const uint4* srcr = reinterpret_cast<const uint4*>(tok ? src1 : src0);
-            uint16_t* side = isv ? p.cache.sink_v : p.cache.sink_k;
-            uint4* dst = reinterpret_cast<uint4*>(side + (static_cast<int64_t>(b) * p.max_sinks + slot) * C);
+            const uint4* srcr = reinterpret_cast<const uint4*>(
+                (r.isv ? p.v_new : p.k_new) + (static_cast<int64_t>(r.b) * p.num_new + r.i0 + tok) * C);
+            uint16_t* side = r.isv ? p.cache.sink_v : p.cache.sink_k;
+            uint4* dst = reinterpret_cast<uint4*>(side + (static_cast<int64_t>(r.b) * p.max_sinks + slot) * C);
             for (int j = tid; j < C / 8; j += blockDim.x) dst[j] = __ldg(srcr + j);
-            if (tid == 0 && !isv)
-                p.cache.sink_pos[b * p.max_sinks + slot] = static_cast<int32_t>(p.start_pos[b] + i0 + tok);
+            if (tid == 0 && !r.isv)
+                p.cache.sink_pos[r.b * p.max_sinks + slot] = static_cast<int32_t>(p.start_pos[r.b] + r.i0 + tok);
         }
-        __syncthreads();  // s_slot and row are rewritten by the next pair
+        __syncthreads();  // row and s_slot are rewritten next
     }
 }
 
@@ -275,28 +373,39 @@ __global__ void quantize_finalize_kernel(QuantParams p) {
     if (threadIdx.x == 0 && s_count) p.cache.sink_count[b] += s_count;
 }
 
-template <int N>
+template <int N, int FMT>
 cudaError_t launch_quantize_n(const QuantParams& p, int B, cudaStream_t s) {
-    const size_t smem = static_cast<size_t>(p.C) * (2 * sizeof(float) + sizeof(uint16_t));
-    cudaError_t e = cudaFuncSetAttribute(quantize_kv_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    int per_sm = 1;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, quantize_kv_kernel<N>, 256, smem) != cudaSuccess) {
-        cudaGetLastError();
-        per_sm = 1;
+    const size_t smem = static_cast<size_t>(p.C / 32) * 33 * 8 + static_cast<size_t>(p.C) * 6;
+    static int per_sm_cache[9] = {0};  // keyed by C / 1024 (C <= 8192)
+    int& per_sm = per_sm_cache[p.C / 1024];
+    const int threads = (p.C / 32 + 31) / 32 * 32;
+    if (per_sm == 0) {
+        cudaError_t e = cudaFuncSetAttribute(quantize_kv_kernel<N, FMT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        int n = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, quantize_kv_kernel<N, FMT>, threads, smem);
+        if (e != cudaSuccess) return e;
+        if (n < 1) return cudaErrorInvalidConfiguration;
+        per_sm = n;
     }
     const int64_t npairs = (p.num_new + 1) / 2;
-    // enough CTAs for ~4 waves; each loops over token pairs (amortises the address table)
-    int64_t x = (static_cast<int64_t>(num_sms()) * (per_sm > 0 ? per_sm : 1) * 4 + 2 * B - 1) / (2 * B);
-    if (x > npairs) x = npairs;
-    if (x < 1) x = 1;
-    dim3 grid(static_cast<unsigned>(x), static_cast<unsigned>(B), 2);
-    quantize_kv_kernel<N><<<grid, 256, smem, s>>>(p);
-    e = cudaGetLastError();
+    const int64_t items = 2 * static_cast<int64_t>(B) * npairs;
+    if (items >= (int64_t{1} << 31)) return cudaErrorInvalidValue;
+    int64_t grid = static_cast<int64_t>(num_sms()) * per_sm;
+    if (grid > items) grid = items;
+    quantize_kv_kernel<N, FMT><<<static_cast<unsigned>(grid), threads, smem, s>>>(
+        p, static_cast<uint32_t>(items), static_cast<uint32_t>(npairs));
+    cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     quantize_finalize_kernel<<<B, 256, 0, s>>>(p);
     return cudaGetLastError();
+}
+
+template <int N>
+cudaError_t launch_quantize_fmt(const QuantParams& p, int B, cudaStream_t s) {
+    return p.scale_format == RKV_SCALE_E4M3_CEIL ? launch_quantize_n<N, RKV_SCALE_E4M3_CEIL>(p, B, s)
+                                                 : launch_quantize_n<N, RKV_SCALE_FP16_CEIL>(p, B, s);
 }
 
 }  // namespace
@@ -304,9 +413,9 @@ cudaError_t launch_quantize_n(const QuantParams& p, int B, cudaStream_t s) {
 cudaError_t launch_quantize(const rkv_layer_desc& d, const QuantParams& p, cudaStream_t s) {
     const int n = d.heads_per_group * d.head_dim;
     switch (n) {
-        case 128: return launch_quantize_n<128>(p, d.batch, s);
-        case 256: return launch_quantize_n<256>(p, d.batch, s);
-        case 512: return launch_quantize_n<512>(p, d.batch, s);
+        case 128: return launch_quantize_fmt<128>(p, d.batch, s);
+        case 256: return launch_quantize_fmt<256>(p, d.batch, s);
+        case 512: return launch_quantize_fmt<512>(p, d.batch, s);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -85,7 +85,7 @@ rkv_status validate(const rkv_layer_desc* d) {
                     "G=4 with Hq/Hkv in {1,2}, G in {1,2} with Hq/Hkv in {1,2,4}");
     const int64_t C = static_cast<int64_t>(d->num_kv_heads) * d->head_dim;
     if (C % 512 != 0) return fail(RKV_ERR_INVALID_ARGUMENT, "num_kv_heads*head_dim must be a multiple of 512");
-    if (C > 32768) return fail(RKV_ERR_INVALID_ARGUMENT, "num_kv_heads*head_dim must be <= 32768");
+    if (C > 8192) return fail(RKV_ERR_INVALID_ARGUMENT, "num_kv_heads*head_dim must be <= 8192");
     return RKV_OK;
 }
 
@@ -171,6 +171,9 @@ rkv_status rkv_quantize_kv(const rkv_layer_desc* desc, const uint16_t* k_new, co
     if (!k_new || !v_new || !perm || !start_pos)
         return fail(RKV_ERR_INVALID_ARGUMENT, "quantize_kv: k_new, v_new, perm and start_pos must be non-null");
     if (num_new > desc->max_tokens) return fail(RKV_ERR_OUT_OF_RANGE, "quantize_kv: num_new exceeds max_tokens");
+    if ((reinterpret_cast<uintptr_t>(k_new) | reinterpret_cast<uintptr_t>(v_new) | reinterpret_cast<uintptr_t>(perm)) &
+        15u)
+        return fail(RKV_ERR_INVALID_ARGUMENT, "quantize_kv: k_new, v_new and perm must be 16-byte aligned");
     if (sink_flags && (!cache->sink_k || !cache->sink_v || !cache->sink_pos))
         return fail(RKV_ERR_INVALID_ARGUMENT, "quantize_kv: sink flags need the sidecar arrays");
     rkv::QuantParams p{};
