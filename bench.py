@@ -229,7 +229,8 @@ def bench_quantize_cfg5(dev, world, rank):
     per-layer seeded outlier channels and reorder permutations, sink at token
     0), batch-sharded.  Inputs are generated per layer on the device (214.7 GB
     of fp16 K/V does not fit one GPU); only the quantize-append kernels are
-    timed (CUDA events on the stream)."""
+    timed (CUDA events on the stream, positions and sink flags device-resident
+    through the allocation-free rkv_quantize_kv entry)."""
     import numpy as np
     import torch
 
@@ -243,8 +244,9 @@ def bench_quantize_cfg5(dev, world, rank):
     stream = torch.cuda.current_stream(dev)
     k = torch.empty(B, T, Cc, dtype=torch.float16, device=dev)
     v = torch.empty_like(k)
-    flags = torch.zeros(B, T, dtype=torch.uint8)
+    flags = torch.zeros(B, T, dtype=torch.uint8, device=dev)
     flags[:, 0] = 1
+    start = torch.zeros(B, dtype=torch.int64, device=dev)
     total_ms = 0.0
     layers = []
     for layer in range(w.layers):
@@ -258,12 +260,12 @@ def bench_quantize_cfg5(dev, world, rank):
             v[b0:b0 + vv.shape[0]].copy_(vv)
             del kk, vv
         if layer == 0:  # warm-up launch (same shapes)
-            lay.append(k, v, flags)
+            lay.append_device(k, v, start, flags)
             lay.reset()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        lay.append(k, v, flags)
+        lay.append_device(k, v, start, flags)  # device-resident positions / flags: kernels only
         e1.record(stream)
         torch.cuda.synchronize()
         total_ms += e0.elapsed_time(e1)

@@ -343,30 +343,31 @@ __global__ void __launch_bounds__(256, 2) quantize_kv_kernel(QuantParams p, uint
             if (tid == 0 && !r.isv)
                 p.cache.sink_pos[r.b * p.max_sinks + slot] = static_cast<int32_t>(p.start_pos[r.b] + r.i0 + tok);
         }
+        // per-token sink bits (the K item owns them)
+        if (tid < 2 && !r.isv && (tid == 0 || r.has1)) {
+            const int64_t pos = p.start_pos[r.b] + r.i0 + tid;
+            if (pos >= 0 && pos < p.max_tokens) {
+                uint32_t* mw = p.cache.sink_mask + static_cast<int64_t>(r.b) * ((p.max_tokens + 31) / 32) + (pos >> 5);
+                const uint32_t bit = 1u << (pos & 31);
+                if (s_slot[tid] >= 0) atomicOr(mw, bit);
+                else atomicAnd(mw, ~bit);
+            }
+        }
         __syncthreads();  // row and s_slot are rewritten next
     }
 }
 
-// Sink counts and per-token sink bits for the appended tokens.
-__global__ void quantize_finalize_kernel(QuantParams p) {
+// Sink counts for the appended tokens (only launched with sink flags; it runs
+// after every item has read the old count).
+__global__ void quantize_sink_count_kernel(QuantParams p) {
     const int b = blockIdx.x;
     __shared__ int s_count;
     if (threadIdx.x == 0) s_count = 0;
     __syncthreads();
     int local = 0;
     for (int64_t i = threadIdx.x; i < p.num_new; i += blockDim.x) {
-        const bool sink = p.sink_flags && p.sink_flags[b * p.num_new + i];
         const int64_t pos = p.start_pos[b] + i;
-        if (pos < 0 || pos >= p.max_tokens) continue;
-        const int64_t words = (p.max_tokens + 31) / 32;
-        uint32_t* mw = p.cache.sink_mask + b * words + (pos >> 5);
-        const uint32_t bit = 1u << (pos & 31);
-        if (sink) {
-            atomicOr(mw, bit);
-            ++local;
-        } else {
-            atomicAnd(mw, ~bit);
-        }
+        if (pos >= 0 && pos < p.max_tokens && p.sink_flags[b * p.num_new + i]) ++local;
     }
     if (local) atomicAdd(&s_count, local);
     __syncthreads();
@@ -398,7 +399,8 @@ cudaError_t launch_quantize_n(const QuantParams& p, int B, cudaStream_t s) {
         p, static_cast<uint32_t>(items), static_cast<uint32_t>(npairs));
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    quantize_finalize_kernel<<<B, 256, 0, s>>>(p);
+    if (!p.sink_flags) return cudaSuccess;
+    quantize_sink_count_kernel<<<B, 256, 0, s>>>(p);
     return cudaGetLastError();
 }
 
