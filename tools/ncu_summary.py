@@ -28,7 +28,11 @@ for i, n in enumerate(h):
     if n.startswith("smsp__pcsamp_warps_issue_stalled_") and not n.endswith("not_issued") and v[i] not in ("", "0"):
         stalls.append((int(v[i].replace(",", "")), n.replace("smsp__pcsamp_warps_issue_stalled_", "")))
     if n in ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
-             "dram__bytes_read.sum", "dram__bytes_write.sum", "smsp__inst_executed.sum"):
+             "dram__bytes_read.sum", "dram__bytes_write.sum", "smsp__inst_executed.sum",
+             "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+             "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+             "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+             "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"):
         print(f"{n:<60} {v[i]}")
 tot = sum(s for s, _ in stalls)
 print("stalls:", ", ".join(f"{n} {s / tot * 100:.0f}%" for s, n in sorted(stalls, reverse=True)[:9]))
