@@ -41,6 +41,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-quantize", action="store_true", help="skip the config-5 quantize measurement")
+    ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of CUDA-graph replays")
     a = ap.parse_args()
     a.warmup = max(a.warmup, 3)
     return a
@@ -332,22 +333,48 @@ def run_ours(args):
 
             dist.barrier()
 
-    # ---- timed region: device-resident inputs
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    # the step as a CUDA-graph-captured pair: one graph per input set
+    graphs = None
+    if not args.no_graph:
+        try:
+            graphs = []
+            for j in range(nsets):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    step(j)
+                graphs.append(g)
+            for j in range(nsets):
+                graphs[j].replay()
+            torch.cuda.synchronize()
+        except Exception as e:  # fall back to eager launches, and say so
+            print(f"[bench] CUDA graph capture failed ({e}); timing eager launches", file=sys.stderr)
+            graphs = None
+
+    # ---- timed region: device-resident inputs, whole steps
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clocks:
         start.record(stream)
         for i in range(args.steps):
-            layer.append_device(kn[i % nsets], vn[i % nsets], start_t)
-            ev[i][0].record(stream)
-            layer.decode_device(qs[i % nsets], len_t, T + 1, out, ws, ws_bytes)
-            ev[i][1].record(stream)
+            if graphs is not None:
+                graphs[i % nsets].replay()
+            else:
+                step(i)
         end.record(stream)
         torch.cuda.synchronize()
     barrier()
     elapsed_ms = start.elapsed_time(end)
+
+    # ---- the decode-attention launch alone (roofline of the dominant kernel)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        layer.append_device(kn[i % nsets], vn[i % nsets], start_t)
+        ev[i][0].record(stream)
+        layer.decode_device(qs[i % nsets], len_t, T + 1, out, ws, ws_bytes)
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
     decode_ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
     if world > 1:
         import torch.distributed as dist
@@ -465,7 +492,8 @@ def run_ours(args):
                      "traffic": traffic, "peak_kind": peak_kind, "kernel": "rkv_decode_attention",
                      "bytes_per_launch": dbytes},
         "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-        "gpu_launches": 5 * args.steps,
+        "gpu_launches": 3 * args.steps,  # quantize_kv, decode split, decode combine per step
+        "cuda_graph": graphs is not None,
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,
         "quantize_cfg5": quant5,
