@@ -170,6 +170,20 @@ rkv_status rkv_calibrate_reorder(const float* rotated_keys, int64_t rows, int64_
 rkv_status rkv_detect_sinks(const float* hidden, int64_t b, int64_t s, int64_t h, double rel_threshold,
                             double abs_floor, uint8_t* flags, int64_t* num_sinks);
 
+/* The same detection on DEVICE memory (no host round trip):
+ *   hidden     : [b][s][h] fp32, device
+ *   flags      : [s] u8, device (1 = sink; token 0 always), ready for
+ *                rkv_quantize_kv's sink_flags once broadcast over the batch
+ *   median_out : device float (the median of |hidden|), or NULL
+ *   workspace  : rkv_detect_sinks_workspace_bytes() bytes of device memory
+ * Exact: the median is a radix select on the magnitude bits, the threshold
+ * compare is done in fp32 against RD(rel * median) (== the reference's
+ * double compare for float inputs).  Stream-ordered, graph-capturable. */
+size_t rkv_detect_sinks_workspace_bytes(void);
+rkv_status rkv_detect_sinks_device(const float* hidden, int64_t b, int64_t s, int64_t h, double rel_threshold,
+                                   double abs_floor, uint8_t* flags, float* median_out, void* workspace,
+                                   size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

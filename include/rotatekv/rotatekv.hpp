@@ -78,6 +78,23 @@ inline std::vector<float> apply_reorder(const std::vector<float>& x, const Reord
     return out;
 }
 
+// detect_massive_activations (proj/src/sink.cpp:14-45) on device memory:
+// hidden [b][s][h] fp32 -> flags [s] u8 (device), optional device median.
+// Allocates its small workspace per call; use rkv_detect_sinks_device with a
+// persistent workspace inside CUDA graphs.
+inline void detect_massive_activations_device(const float* hidden, int64_t b, int64_t s, int64_t h, uint8_t* flags,
+                                              double rel_threshold = 50.0, double abs_floor = 0.0,
+                                              float* median_out = nullptr, cudaStream_t stream = nullptr) {
+    const size_t nws = rkv_detect_sinks_workspace_bytes();
+    void* ws = nullptr;
+    check_cuda(cudaMalloc(&ws, nws), "cudaMalloc sink workspace");
+    const rkv_status st =
+        rkv_detect_sinks_device(hidden, b, s, h, rel_threshold, abs_floor, flags, median_out, ws, nws, stream);
+    cudaStreamSynchronize(stream);
+    cudaFree(ws);
+    check(st);
+}
+
 // One layer's 2-bit rotated KV cache on the device (LayerKVCache,
 // proj/include/rotatekv/kv_cache.hpp:13-50, for a batch of sequences).
 class DeviceLayerCache {

@@ -14,6 +14,7 @@ from .rotatekv import (  # noqa: F401
     apply_reorder,
     calibrate_reorder,
     detect_massive_activations,
+    detect_massive_activations_device,
     layer_plan_build,
     lib,
     rotate_keys,

@@ -360,4 +360,25 @@ rkv_status rkv_detect_sinks(const float* hidden, int64_t b, int64_t s, int64_t h
     return RKV_OK;
 }
 
+size_t rkv_detect_sinks_workspace_bytes(void) { return rkv::detect_sinks_workspace_bytes(); }
+
+rkv_status rkv_detect_sinks_device(const float* hidden, int64_t b, int64_t s, int64_t h, double rel_threshold,
+                                   double abs_floor, uint8_t* flags, float* median_out, void* workspace,
+                                   size_t workspace_bytes, void* stream) {
+    if (!hidden || !flags || !workspace)
+        return fail(RKV_ERR_INVALID_ARGUMENT, "detect_massive_activations: null argument");
+    if (b < 1 || h < 1) return fail(RKV_ERR_INVALID_ARGUMENT, "detect_massive_activations: expected [b,s,hidden]");
+    if (!(rel_threshold > 1.0))
+        return fail(RKV_ERR_INVALID_ARGUMENT, "detect_massive_activations: rel_threshold must be > 1");
+    if (s < 1) return fail(RKV_ERR_INVALID_ARGUMENT, "detect_massive_activations: empty sequence");
+    if (workspace_bytes < rkv::detect_sinks_workspace_bytes())
+        return fail(RKV_ERR_INVALID_ARGUMENT, "detect_massive_activations: workspace too small");
+    if (reinterpret_cast<uintptr_t>(hidden) & 15u)
+        return fail(RKV_ERR_INVALID_ARGUMENT, "detect_massive_activations: hidden must be 16-byte aligned");
+    cudaError_t e = rkv::launch_detect_sinks(hidden, b, s, h, rel_threshold, abs_floor, flags, median_out, workspace,
+                                             static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "detect_massive_activations");
+    return RKV_OK;
+}
+
 }  // extern "C"

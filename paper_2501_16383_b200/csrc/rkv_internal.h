@@ -64,6 +64,10 @@ cudaError_t launch_rope_table(const rkv_layer_desc& d, float4* table, int64_t ma
 cudaError_t launch_rotate_keys(const rkv_layer_desc& d, const uint16_t* k, int64_t rows, float* out,
                                cudaStream_t s);
 int num_sms();
+// sink_detect.cu
+size_t detect_sinks_workspace_bytes();
+cudaError_t launch_detect_sinks(const float* x, int64_t b, int64_t s, int64_t hidden, double rel, double abs_floor,
+                                uint8_t* flags, float* median_out, void* ws, cudaStream_t stream);
 // rkv_plan.cu
 bool build_decode_plan(const rkv_layer_desc& d, const int32_t* perm, std::vector<uint32_t>& out, int& cost);
 

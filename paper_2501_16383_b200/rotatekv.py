@@ -91,9 +91,13 @@ def lib():
         L.rkv_calibrate_reorder.argtypes = [P, C.c_int64, C.c_int64, C.c_int32, P, P]
         L.rkv_detect_sinks.argtypes = [P, C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_double, P,
                                        C.POINTER(C.c_int64)]
+        L.rkv_detect_sinks_workspace_bytes.restype = C.c_size_t
+        L.rkv_detect_sinks_workspace_bytes.argtypes = []
+        L.rkv_detect_sinks_device.argtypes = [P, C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_double, P, P, P,
+                                              C.c_size_t, P]
         for name in ("rkv_layer_validate", "rkv_cache_carve", "rkv_cache_reset", "rkv_rope_table_init",
                      "rkv_quantize_kv", "rkv_decode_attention", "rkv_rotate_keys", "rkv_calibrate_reorder",
-                     "rkv_detect_sinks", "rkv_layer_plan_build", "rkv_layer_plan_init"):
+                     "rkv_detect_sinks", "rkv_detect_sinks_device", "rkv_layer_plan_build", "rkv_layer_plan_init"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -185,6 +189,29 @@ def detect_massive_activations(hidden, rel_threshold: float = 50.0, abs_floor: f
     _check(lib().rkv_detect_sinks(h.ctypes.data, h.shape[0], h.shape[1], h.shape[2], float(rel_threshold),
                                   float(abs_floor), flags.ctypes.data, C.byref(n)))
     return flags
+
+
+def detect_massive_activations_device(hidden, rel_threshold: float = 50.0, abs_floor: float = 0.0,
+                                     return_median: bool = False):
+    """detect_massive_activations on the GPU: hidden = CUDA fp32 [b, s, h]
+    tensor -> CUDA uint8 flags [s] (and the median of |hidden|), no host
+    round trip; the flags feed RotateKVLayer.append_device after a broadcast
+    over the batch."""
+    torch = __import__("torch")
+    if hidden.ndim != 3:
+        raise ValueError("detect_massive_activations: expected [b,s,hidden]")
+    if hidden.dtype != torch.float32 or not hidden.is_cuda:
+        raise ValueError("detect_massive_activations: hidden must be a CUDA float32 tensor")
+    hidden = hidden.contiguous()
+    b, s_, h = hidden.shape
+    flags = torch.empty(s_, dtype=torch.uint8, device=hidden.device)
+    median = torch.empty(1, dtype=torch.float32, device=hidden.device)
+    nws = lib().rkv_detect_sinks_workspace_bytes()
+    ws = torch.empty(nws, dtype=torch.uint8, device=hidden.device)
+    stream = C.c_void_p(torch.cuda.current_stream(hidden.device).cuda_stream)
+    _check(lib().rkv_detect_sinks_device(_ptr(hidden), b, s_, h, float(rel_threshold), float(abs_floor), _ptr(flags),
+                                         _ptr(median), _ptr(ws), nws, stream))
+    return (flags, median) if return_median else flags
 
 
 def layer_plan_build(cfg: LayerConfig, perm):
