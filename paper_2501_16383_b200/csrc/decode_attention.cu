@@ -50,8 +50,12 @@ __device__ __forceinline__ int64_t lmin(int64_t a, int64_t b) { return a < b ? a
 
 __device__ __forceinline__ float2 lds64(const unsigned char* p) { return *reinterpret_cast<const float2*>(p); }
 __device__ __forceinline__ float4 lds128f(const unsigned char* p) { return *reinterpret_cast<const float4*>(p); }
+// RoPE table rows are per position pair, 128 float4 (2 KB): [0, 64) section 1
+// (cos p0, cos p1, sin p0, sin p1) per frequency; [64, 128) section 2 (one
+// 32-float4 frequency-pair row per position, tensor-core decode).
+constexpr int kRopeRow = 128;
 __device__ __forceinline__ float2 rope_at(const float4* t, int64_t pos, int f) {
-    const float4 r = __ldg(t + (pos >> 1) * 64 + f);
+    const float4 r = __ldg(t + (pos >> 1) * kRopeRow + f);
     return (pos & 1) ? make_float2(r.y, r.w) : make_float2(r.x, r.z);
 }
 __device__ __forceinline__ void sts64(uint32_t addr, float2 v) {
@@ -143,13 +147,14 @@ __global__ void __launch_bounds__(max_threads<N>(), 1) decode_split_kernel(Decod
         const uint32_t n = static_cast<uint32_t>(lmin(TT, t_end - t0));
         unsigned char* st = smem + lay.stages + (it % kStages) * lay.stage_bytes;
         uint64_t* bar = mbar + (it % kStages);
-        const uint32_t bw = n * W * 4, bm = n * MG * 4, br = ((n + 1) >> 1) * 64 * 16;
-        mbar_arrive_expect_tx(bar, 2 * bw + 2 * bm + br);
+        const uint32_t bw = n * W * 4, bm = n * MG * 4, npr = (n + 1) >> 1;
+        mbar_arrive_expect_tx(bar, 2 * bw + 2 * bm + npr * 1024);
         bulk_g2s(st + lay.kc, p.cache.k_codes + (row0 + t0) * W, bw, bar);
         bulk_g2s(st + lay.km, p.cache.k_meta + (row0 + t0) * MG, bm, bar);
         bulk_g2s(st + lay.vc, p.cache.v_codes + (row0 + t0) * W, bw, bar);
         bulk_g2s(st + lay.vm, p.cache.v_meta + (row0 + t0) * MG, bm, bar);
-        bulk_g2s(st + lay.rope, p.rope + (t0 >> 1) * 64, br, bar);
+        for (uint32_t r = 0; r < npr; ++r)  // section 1 of each position-pair row
+            bulk_g2s(st + lay.rope + r * 1024, p.rope + ((t0 >> 1) + r) * kRopeRow, 1024, bar);
     };
 
     if (tid == 0) {
@@ -171,7 +176,7 @@ __global__ void __launch_bounds__(max_threads<N>(), 1) decode_split_kernel(Decod
     // q: RoPE at position T-1 (prepare_queries), x log2(e)/sqrt(d) x 1/sqrt(n)
     // (the FWHT normalisation), lane-major: q_l[(h*L + lam)*QS + jj] = q[h][lam + L*jj]
     {
-        const float4* cs = p.rope + ((T - 1) >> 1) * 64;
+        const float4* cs = p.rope + ((T - 1) >> 1) * kRopeRow;
         const bool odd = (T - 1) & 1;
         const uint16_t* qb = p.q + static_cast<int64_t>(b) * Hq * 128;
         const float qs = p.qscale * p.k_norm;
@@ -501,7 +506,8 @@ __global__ void __launch_bounds__(128) decode_combine_kernel(DecodeParams p) {
 }
 
 // table[pos/2][f] = (cos(p0 th_f), cos(p1 th_f), sin(p0 th_f), sin(p1 th_f)),
-// p0 = pos & ~1, p1 = p0 + 1: a token pair's rotation is one LDS.128.
+// p0 = pos & ~1, p1 = p0 + 1: a token pair's rotation is one LDS.128
+// (section 1 of the kRopeRow-float4 position-pair row).
 __global__ void rope_table_kernel(float4* table, int64_t npairs, double base) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= npairs * 64) return;
@@ -510,8 +516,29 @@ __global__ void rope_table_kernel(float4* table, int64_t npairs, double base) {
     const double theta = pow(base, -2.0 * static_cast<double>(f) / 128.0);  // proj/src/rope.cpp:17-24
     const double a0 = 1.0 * static_cast<double>(2 * pr) * theta;            // dir * pos * theta
     const double a1 = 1.0 * static_cast<double>(2 * pr + 1) * theta;
-    table[i] = make_float4(static_cast<float>(cos(a0)), static_cast<float>(cos(a1)), static_cast<float>(sin(a0)),
-                           static_cast<float>(sin(a1)));
+    table[pr * kRopeRow + f] = make_float4(static_cast<float>(cos(a0)), static_cast<float>(cos(a1)),
+                                           static_cast<float>(sin(a0)), static_cast<float>(sin(a1)));
+}
+
+// Second section (tensor-core decode): token-major, one float4 per frequency
+// pair (f, f+1) = 2j, 2j+1:  G = 4: (u_f, u_f+1, w_f, w_f+1), u = cos - sin,
+// w = cos + sin (the bit-6 butterfly folded into RoPE, decode_mma.cu);
+// otherwise (cos_f, cos_f+1, sin_f, sin_f+1).  Evaluated in double.
+__global__ void rope_table2_kernel(float4* table, int64_t npos, double base, int fold) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= npos * 32) return;
+    const int64_t pos = i / 32;
+    const int j = static_cast<int>(i % 32);
+    double c[2], sn[2];
+    for (int k = 0; k < 2; ++k) {
+        const double theta = pow(base, -2.0 * static_cast<double>(2 * j + k) / 128.0);
+        c[k] = cos(static_cast<double>(pos) * theta);
+        sn[k] = sin(static_cast<double>(pos) * theta);
+    }
+    table[(pos >> 1) * kRopeRow + 64 + (pos & 1) * 32 + j] = fold ? make_float4(static_cast<float>(c[0] - sn[0]), static_cast<float>(c[1] - sn[1]),
+                                  static_cast<float>(c[0] + sn[0]), static_cast<float>(c[1] + sn[1]))
+                    : make_float4(static_cast<float>(c[0]), static_cast<float>(c[1]), static_cast<float>(sn[0]),
+                                  static_cast<float>(sn[1]));
 }
 
 template <int N, int L>
@@ -542,11 +569,15 @@ cudaError_t launch_decode_nr(const DecodePlan& plan, const DecodeParams& p, int 
     if (e != cudaSuccess) return e;
     kern<<<dim3(plan.S, B), plan.NT, plan.smem, s>>>(p);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    decode_combine_kernel<<<dim3(p.Hq, B), 128, 0, s>>>(p);
-    return cudaGetLastError();
+    return launch_decode_combine(p, B, s);
 }
 
 }  // namespace
+
+cudaError_t launch_decode_combine(const DecodeParams& p, int B, cudaStream_t s) {
+    decode_combine_kernel<<<dim3(p.Hq, B), 128, 0, s>>>(p);
+    return cudaGetLastError();
+}
 
 int num_sms() {
     static int n = 0;
@@ -595,7 +626,9 @@ bool decode_supported(int N, int REP) {
 }
 
 DecodePlan plan_decode(const rkv_layer_desc& d, int64_t max_seq_len) {
+    if (decode_kind(d) == kDecodeMma) return plan_decode_mma(d, max_seq_len);
     DecodePlan pl{};
+    pl.kind = kDecodeSimt;
     const int C = d.num_kv_heads * d.head_dim;
     pl.N = d.heads_per_group * d.head_dim;
     pl.REP = d.num_q_heads / d.num_kv_heads;
@@ -627,10 +660,14 @@ DecodePlan plan_decode(const rkv_layer_desc& d, int64_t max_seq_len) {
     pl.S = static_cast<int>((max_seq_len + chunk - 1) / chunk);
     pl.NP = pl.S * P;
     pl.smem = smem_layout(C, d.num_q_heads, pl.TT, pl.chunk, pl.N, 17 * (C / 16), pl.stages).total;
+    pl.PP = P;
+    const int W = C / 16;
+    pl.ok = pl.NT <= max_nt && pl.smem <= 227 * 1024 && (pl.NT % W == 0 || W % pl.NT == 0);
     return pl;
 }
 
 cudaError_t launch_decode(const rkv_layer_desc& d, const DecodePlan& plan, const DecodeParams& p, cudaStream_t s) {
+    if (plan.kind == kDecodeMma) return launch_decode_mma(d, plan, p, s);
     const int B = d.batch;
     switch (plan.N * 16 + plan.REP) {
         case 512 * 16 + 1: return launch_decode_nr<512, 1>(plan, p, B, s);
@@ -649,6 +686,11 @@ cudaError_t launch_rope_table(const rkv_layer_desc& d, float4* table, int64_t ma
     const int64_t npairs = (max_pos + 1) / 2;
     const int64_t n = npairs * 64;
     rope_table_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(table, npairs, d.rope_base);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const int64_t npos = 2 * npairs;
+    rope_table2_kernel<<<static_cast<unsigned>((npos * 32 + 255) / 256), 256, 0, s>>>(
+        table, npos, d.rope_base, d.heads_per_group == 4 ? 1 : 0);
     return cudaGetLastError();
 }
 

@@ -1,0 +1,600 @@
+// decode_mma.cu -- split-K decode attention over the 2-bit rotated cache with
+// the inverse FWHT on the tensor cores (mma.sync m16n8k16, fp16 in, fp32 acc).
+//
+// Same contract as decode_attention.cu (the attention half of decode_step,
+// proj/src/pipeline.cpp:133-152,211-261): keys = RoPE_t(H_G . P^-1 . deq(k')),
+// logits = q.k/sqrt(d), online softmax, o' = sum p v' (rotated V frame); the
+// combine kernel (decode_attention.cu) merges the split partials, adds the
+// fp16 sink rows and applies H_128 (V's inverse rotation).
+//
+// Why tensor cores here.  The CUDA-core kernel spends ~4.5 FADD2 per cached
+// K element on the 9-stage FWHT and FADD2/FFMA2 run at half rate on sm_100
+// (measured: 60 instr/clk/SM), so the FWHT alone costs more FMA-pipe time
+// than streaming the 2-bit cache from HBM.  The Sylvester Hadamard matrix
+// factors over index bits: H_512 = H_2(bit 6) (x) H_16(F2 bits) (x)
+// H_16(F1 bits).  Per token and FWHT group the two H_16 factors are two
+// chained mma.sync: the fp32 accumulator fragment of the first MMA is, element
+// for element, the B fragment of the second (D[m][n] -> B[k=n][n'=m]), so the
+// rotation never leaves registers.  The remaining H_2 acts on bit 6 -- the
+// RoPE partner bit -- and folds into the RoPE coefficients for free:
+//   q.(R_t (a'+b', a'-b')) = a'(q_a u + q_b w) + b'(q_a w - q_b u),
+//   u = cos - sin, w = cos + sin.
+// Precision: the MMA inputs are fp16.  The dequantised K (s*(c-z)) is rounded
+// to fp16 once, and the half-way result of the first MMA is split into an
+// fp16 hi part and an fp16 residual (two MMAs), so the rotation is accurate to
+// ~2^-22 (tools/hmma_precision.py: 2e-5 normalised max error vs 7.6e-4 with a
+// single fp16 rounding; the north star allows 2e-3).
+//
+// Pipeline per CTA (one split of one sequence; NG = C/N FWHT groups, one warp
+// per group, PW warps per group splitting the token pairs):
+//   * TMA bulk copies stream each tile (packed K/V words, scale|zero words,
+//     the tile's RoPE rows) into an NS-stage ring (mbarrier complete_tx).
+//   * scatter: every thread takes one packed K word for each token pair of
+//     the NEXT tile, dequantises its 16 codes for both tokens as half2 ops
+//     (code -> 2^(10-2e)+c by one LOP3 on the interleaved pair, HSUB2 of the
+//     zero point, HMUL2 of the scale) and stores them (STS.32) to their
+//     natural channel (slot j -> perm[j]) in B-fragment order, double
+//     buffered, so one __syncthreads per tile separates scatter and compute.
+//   * compute (per warp = FWHT group, per token pair): 4 LDS.128 + PRMT give
+//     the B fragments of both tokens, 4 + 8 mma.sync per token, RoPE+q.k on
+//     the fp32 fragments (FFMA2 over the token pair), a 5-shuffle
+//     reduce-scatter, online softmax, and the V accumulation on CUDA cores:
+//     one LOP3 turns two codes into fp16 subnormals c*2^(2e-24) and a mixed
+//     FHFMA (fp16 x fp16 + fp32) adds p*s*c; the zero point is folded once
+//     per token.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <type_traits>
+
+#include "rkv_common.cuh"
+#include "rkv_internal.h"
+#include "rkv_layout.h"
+
+namespace rkv {
+
+namespace {
+
+constexpr int kMmaMaxThreads = 384;  // one warp per FWHT group: C <= 6144 at G = 4
+
+__device__ __forceinline__ int64_t lmin64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+    return r;
+}
+__device__ __forceinline__ uint32_t h2sub(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+__device__ __forceinline__ uint32_t h2mul(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+__device__ __forceinline__ uint32_t h2add(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("add.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+// half2(lo, hi) from two floats, round to nearest (F2FP.F16.F32.PACK_AB)
+__device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+// d - float(half) in one FHADD (mixed f16 + f32 add, sm_100)
+__device__ __forceinline__ float sub_lo(float d, uint32_t h) {
+    float r;
+    asm("{.reg .b16 l, u, n; mov.b32 {l, u}, %1; neg.f16 n, l; add.rn.f32.f16 %0, n, %2;}" : "=f"(r) : "r"(h), "f"(d));
+    return r;
+}
+__device__ __forceinline__ float sub_hi(float d, uint32_t h) {
+    float r;
+    asm("{.reg .b16 l, u, n; mov.b32 {l, u}, %1; neg.f16 n, u; add.rn.f32.f16 %0, n, %2;}" : "=f"(r) : "r"(h), "f"(d));
+    return r;
+}
+// c + a.half(SA) * b.half(SB) in fp32 (FHFMA)
+template <int SA, int SB>
+__device__ __forceinline__ float fhfma(uint32_t a, uint32_t b, float c) {
+    float r;
+    if constexpr (SA == 0 && SB == 0)
+        asm("{.reg .b16 al, ah, bl, bh; mov.b32 {al, ah}, %1; mov.b32 {bl, bh}, %2; fma.rn.f32.f16 %0, al, bl, %3;}"
+            : "=f"(r) : "r"(a), "r"(b), "f"(c));
+    else if constexpr (SA == 1 && SB == 0)
+        asm("{.reg .b16 al, ah, bl, bh; mov.b32 {al, ah}, %1; mov.b32 {bl, bh}, %2; fma.rn.f32.f16 %0, ah, bl, %3;}"
+            : "=f"(r) : "r"(a), "r"(b), "f"(c));
+    else if constexpr (SA == 0 && SB == 1)
+        asm("{.reg .b16 al, ah, bl, bh; mov.b32 {al, ah}, %1; mov.b32 {bl, bh}, %2; fma.rn.f32.f16 %0, al, bh, %3;}"
+            : "=f"(r) : "r"(a), "r"(b), "f"(c));
+    else
+        asm("{.reg .b16 al, ah, bl, bh; mov.b32 {al, ah}, %1; mov.b32 {bl, bh}, %2; fma.rn.f32.f16 %0, ah, bh, %3;}"
+            : "=f"(r) : "r"(a), "r"(b), "f"(c));
+    return r;
+}
+__device__ __forceinline__ float ex2(float x) {  // 2^x, MUFU.EX2 (2^-inf = 0)
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+// D = A(16x16, fp16) * B(16x8, fp16) + C, fp32 accumulate
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1,
+                                         const float (&c)[4]) {
+    asm("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%10,%11,%12,%13};"
+        : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "f"(c[0]), "f"(c[1]), "f"(c[2]),
+          "f"(c[3]));
+}
+
+struct MmaSmem {
+    size_t stage_bytes, kc, km, vc, vm, rope;  // offsets inside one stage
+    size_t stages, mbar, knat, plan, mask, total;
+};
+
+__host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
+
+__host__ __device__ inline MmaSmem mma_smem(int C, int TT, int chunk, int stages) {
+    MmaSmem s{};
+    const int W = C / 16, MG = C / 128, PP = TT / 2;
+    s.kc = 0;
+    s.km = al16(s.kc + size_t(TT) * W * 4);
+    s.vc = al16(s.km + size_t(TT) * MG * 4);
+    s.vm = al16(s.vc + size_t(TT) * W * 4);
+    s.rope = al16(s.vm + size_t(TT) * MG * 4);
+    s.stage_bytes = al16(s.rope + size_t(PP) * 64 * 16);
+    s.stages = 0;
+    s.mbar = s.stages + stages * s.stage_bytes;
+    s.knat = al16(s.mbar + stages * 8);
+    s.plan = al16(s.knat + size_t(PP) * C * 4);         // token-pair rows of one tile
+    s.mask = al16(s.plan + size_t(17) * (C / 16) * 4);  // scatter plan: omega + 16 offsets per word
+    s.total = al16(s.mask + size_t(chunk / 32 + 2) * 4);
+    return s;
+}
+
+// H_16 as an m16n8k16 A fragment (row-major, +-1 in fp16): a[0] = (g, 2t..),
+// a[1] = (g+8, 2t..), a[2] = (g, 2t+8..), a[3] = (g+8, 2t+8..)
+__device__ __forceinline__ void hadamard16_frag(uint32_t (&a)[4], int lane) {
+    const int g = lane >> 2, t = lane & 3;
+    auto h = [](int m, int k) -> uint32_t { return (__popc(m & k) & 1) ? 0xBC00u : 0x3C00u; };
+    const int rows[4] = {g, g + 8, g, g + 8}, cols[4] = {2 * t, 2 * t, 2 * t + 8, 2 * t + 8};
+#pragma unroll
+    for (int r = 0; r < 4; ++r) a[r] = h(rows[r], cols[r]) | (h(rows[r], cols[r] + 1) << 16);
+}
+
+// D = A(16x16, fp16) * B(16x8, fp16), fp16 accumulate from zero: the result
+// (pairs along n) is already a B fragment of the next MMA.  Measured on B200
+// (tools/microbench4.cu): equal to the round-to-nearest fp16 of the exact
+// H_16 . X for all but 3e-5 of outputs (ties), never off by more than half an ulp.
+__device__ __forceinline__ void mma16816_h(uint32_t (&d)[2], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm("mma.sync.aligned.m16n8k16.row.col.f16.f16.f16.f16 {%0,%1}, {%2,%3,%4,%5}, {%6,%7}, {%8,%8};"
+        : "=r"(d[0]), "=r"(d[1])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "r"(0u));
+}
+
+// Tile geometry (compile time): TT = 4 tokens = 2 token pairs per tile, one
+// warp per FWHT group, 3-deep TMA ring; ~102 KB of shared memory and <= 96
+// registers so that two CTAs (20 warps) share an SM and cover each other's
+// barrier and MMA-latency stalls.
+constexpr int kPP = 2, kTT = 2 * kPP, kNS = 3, kCtasPerSm = 2;
+
+// G = 4 (N = 512), one q head per KV head.
+template <int G, int REP>
+__global__ void __launch_bounds__(320, kCtasPerSm) decode_mma_kernel(DecodeParams p) {
+    static_assert(G == 4 && REP == 1, "decode_mma_kernel: G = 4, MHA");
+    constexpr int N = 128 * G;
+    constexpr int NJ = N / 128;  // MMA-1 instances per token (F2 bit 3, outer bit 6)
+
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int C = p.C, W = C / 16, MG = C / 128, Hq = p.Hq;
+    const int NG = C / N;
+    const MmaSmem lay = mma_smem(C, kTT, p.chunk, kNS);
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + lay.mbar);
+    uint32_t* mask_s = reinterpret_cast<uint32_t*>(smem + lay.mask);
+
+    const int tid = threadIdx.x, NT = blockDim.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int gam = warp % NG;
+    const int b = blockIdx.y, split = blockIdx.x;
+    const int64_t T = p.seq_len[b];
+    const int64_t t_begin = static_cast<int64_t>(split) * p.chunk;
+    const int64_t t_end = lmin64(T, t_begin + p.chunk);
+
+    if (t_begin >= t_end) {  // empty split: neutral partials
+        for (int i = tid; i < Hq; i += NT) {
+            const int64_t row = (static_cast<int64_t>(b) * p.NP + split) * Hq + i;
+            p.ws_ml[row * 2] = -INFINITY;
+            p.ws_ml[row * 2 + 1] = 0.0f;
+            float4* o = reinterpret_cast<float4*>(p.ws_o + row * 128);
+            for (int k = 0; k < 32; ++k) o[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        return;
+    }
+    const int ntiles = static_cast<int>((t_end - t_begin + kTT - 1) / kTT);
+    const int64_t row0 = static_cast<int64_t>(b) * p.max_tokens;
+
+    auto issue_tile = [&](int it) {
+        const int64_t t0 = t_begin + static_cast<int64_t>(it) * kTT;
+        const uint32_t n = static_cast<uint32_t>(lmin64(kTT, t_end - t0));
+        unsigned char* st = smem + lay.stages + (it % kNS) * lay.stage_bytes;
+        uint64_t* bar = mbar + (it % kNS);
+        const uint32_t bw = n * W * 4, bm = n * MG * 4, npr = (n + 1) >> 1;
+        mbar_arrive_expect_tx(bar, 2 * bw + 2 * bm + npr * 1024);
+        bulk_g2s(st + lay.kc, p.cache.k_codes + (row0 + t0) * W, bw, bar);
+        bulk_g2s(st + lay.km, p.cache.k_meta + (row0 + t0) * MG, bm, bar);
+        bulk_g2s(st + lay.vc, p.cache.v_codes + (row0 + t0) * W, bw, bar);
+        bulk_g2s(st + lay.vm, p.cache.v_meta + (row0 + t0) * MG, bm, bar);
+        for (uint32_t r = 0; r < npr; ++r)  // section 2 (frequency-pair rows) of each position-pair row
+            bulk_g2s(st + lay.rope + r * 1024, p.rope + ((t0 >> 1) + r) * 128 + 64, 1024, bar);
+    };
+
+    if (tid == 0) {
+        for (int s = 0; s < kNS; ++s) mbar_init(mbar + s, 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    if (tid == 0)
+        for (int it = 0; it < kNS && it < ntiles; ++it) issue_tile(it);
+
+    const int64_t mw0 = t_begin >> 5;
+    {
+        const uint32_t* smask = p.cache.sink_mask + static_cast<int64_t>(b) * ((p.max_tokens + 31) / 32);
+        const int nw = static_cast<int>(((t_end - 1) >> 5) - mw0 + 1);
+        for (int i = tid; i < nw; i += NT) mask_s[i] = smask[mw0 + i];
+    }
+
+    // ---- scatter role: word position wp = tid (NT == W for G = 4); the plan
+    // (omega + the 16 store offsets of each word position) lives in shared memory
+    const uint32_t* plan_s = reinterpret_cast<const uint32_t*>(smem + lay.plan);
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(p.plan + kPlanHeader);
+        uint4* dst = reinterpret_cast<uint4*>(smem + lay.plan);
+        for (int i = tid; i < 17 * W / 4; i += NT) dst[i] = __ldg(src + i);
+    }
+    const uint32_t pair_bytes = static_cast<uint32_t>(C) * 4u;
+
+    // B_e = 2^(10 - 2e') as fp16 exponent bits, e' = 0..4: code e' of a 16-bit lane ORed into the mantissa
+    auto bexp = [](int sh) -> uint32_t { const uint32_t be = static_cast<uint32_t>(25 - 2 * sh) << 10; return be | (be << 16); };
+
+    // Branch-free tile bodies: tokens past the end of the split (last tile only)
+    // are processed on whatever the stage holds and masked out of the softmax
+    // (their probability is 0 and their V weight is exactly 0).
+    auto scatter_tile = [&](int slot) {
+        const unsigned char* st = smem + lay.stages + slot * lay.stage_bytes;
+        const uint32_t* kc = reinterpret_cast<const uint32_t*>(st + lay.kc);
+        const uint32_t* km = reinterpret_cast<const uint32_t*>(st + lay.km);
+        const uint32_t buf = static_cast<uint32_t>(lay.knat) + smem_u32(smem);
+        const int wsrc = static_cast<int>(plan_s[tid]);
+        uint32_t ad[16];
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+            const uint4 a4 = reinterpret_cast<const uint4*>(plan_s + W)[q4 * W + tid];
+            ad[4 * q4] = a4.x;
+            ad[4 * q4 + 1] = a4.y;
+            ad[4 * q4 + 2] = a4.z;
+            ad[4 * q4 + 3] = a4.w;
+        }
+#pragma unroll
+        for (int pq = 0; pq < kPP; ++pq) {
+            const int tt0 = 2 * pq;
+            const uint32_t w0 = kc[tt0 * W + wsrc], w1 = kc[(tt0 + 1) * W + wsrc];
+            const uint32_t m0 = km[tt0 * MG + (wsrc >> 3)], m1 = km[(tt0 + 1) * MG + (wsrc >> 3)];
+            const uint32_t ss = prmt(m0, m1, 0x5410u);  // (s0, s1)
+            const uint32_t zz = prmt(m0, m1, 0x7632u);  // (z0, z1)
+            uint32_t bz[5];
+#pragma unroll
+            for (int e = 0; e < 5; ++e) bz[e] = h2add(bexp(e), zz);  // B_e + z, exact
+            const uint32_t xl = prmt(w0, w1, 0x5410u), xh = prmt(w0, w1, 0x7632u);  // codes 0-7 | 8-15 of (t0, t1)
+            const uint32_t xls = xl >> 10, xhs = xh >> 10;
+            const uint32_t dst = buf + static_cast<uint32_t>(pq) * pair_bytes;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                const int ee = e & 7;
+                const uint32_t src = ee < 5 ? (e < 8 ? xl : xh) : (e < 8 ? xls : xhs);
+                const int sh = ee < 5 ? ee : ee - 5;
+                const uint32_t h = and_or(src, 0x00030003u << (2 * sh), bexp(sh));  // (B + c0, B + c1)
+                const uint32_t x = h2mul(h2sub(h, bz[sh]), ss);                      // s * (c - z), fp16
+                asm volatile("st.shared.b32 [%0], %1;" ::"r"(dst + ad[e]), "r"(x) : "memory");
+            }
+        }
+    };
+
+    // ---- compute role constants
+    const int g = lane >> 2, tl = lane & 3;
+    uint32_t AH[4];
+    hadamard16_frag(AH, lane);
+    // q: RoPE at T-1, x log2(e)/sqrt(d) x 1/sqrt(N).  Frequency pair (f, f+1),
+    // f = 2tl + 8 f1 + 16 (g&3); head hq = 4 gam + (g>>2) + 2 rh.
+    float2 P2[2][2], Q2[2][2];
+    {
+        const float4* cs = p.rope + ((T - 1) >> 1) * 128;
+        const bool odd = (T - 1) & 1;
+        const uint16_t* qb = p.q + static_cast<int64_t>(b) * Hq * 128;
+        const float qs = p.qscale * p.k_norm;
+#pragma unroll
+        for (int f1 = 0; f1 < 2; ++f1) {
+#pragma unroll
+            for (int rh = 0; rh < 2; ++rh) {
+                const int hq = gam * G + (g >> 2) + 2 * rh;
+                float pv[2], qv[2];
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const int f = 2 * tl + i + 8 * f1 + 16 * (g & 3);
+                    const float4 r4 = __ldg(cs + f);
+                    const float cT = odd ? r4.y : r4.x, sT = odd ? r4.w : r4.z;
+                    const float a = h2f(qb[hq * 128 + f]), bb = h2f(qb[hq * 128 + f + 64]);
+                    pv[i] = (a * cT - bb * sT) * qs;
+                    qv[i] = (a * sT + bb * cT) * qs;
+                }
+                P2[f1][rh] = make_float2(pv[0], pv[1]);
+                Q2[f1][rh] = make_float2(qv[0], qv[1]);
+            }
+        }
+    }
+    const int bit1 = (lane >> 1) & 1, bit2 = (lane >> 2) & 1, bit3 = (lane >> 3) & 1;
+    const int hv = (lane >> 4) + 2 * bit3;                 // V head (= head of the reduced logits)
+    const int gw = gam * (N / 16) + hv * 8 + (lane & 7);  // V word of the group
+    const int gm = gam * G + hv;                           // V meta word (= kv head = q head)
+    float m_run = -INFINITY, l_run = 0.f, zc = 0.f;
+    float acc[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) acc[e] = 0.f;
+
+    const uint32_t lane_off = static_cast<uint32_t>(gam * N * 4 + lane * NJ * 16);
+    const int swz = (lane >> 1) & 3;
+    const int fpi = tl + 8 * (g & 3);  // frequency-pair row index of f1 = 0 (f = 2 fpi)
+
+    // K phase of a tile: logits lg[tk] of head hv (log2 domain)
+    auto k_tile = [&](int slot, float (&lg)[kTT]) {
+        const unsigned char* st = smem + lay.stages + slot * lay.stage_bytes;
+        const float4* rope4 = reinterpret_cast<const float4*>(st + lay.rope);  // [token][32] frequency pairs
+        const unsigned char* bufp = smem + lay.knat;
+        float pv[kTT][2];  // partial logits [token][rh]
+#pragma unroll
+        for (int pq = 0; pq < kPP; ++pq) {
+            uint32_t bf[2][NJ][2];
+            const unsigned char* lb = bufp + static_cast<size_t>(pq) * pair_bytes + lane_off;
+#pragma unroll
+            for (int jc = 0; jc < NJ; ++jc) {
+                const uint4 u = lds128(lb + ((jc ^ swz) << 4));
+                bf[0][jc][0] = prmt(u.x, u.y, 0x5410u);
+                bf[0][jc][1] = prmt(u.z, u.w, 0x5410u);
+                bf[1][jc][0] = prmt(u.x, u.y, 0x7632u);
+                bf[1][jc][1] = prmt(u.z, u.w, 0x7632u);
+            }
+#pragma unroll
+            for (int tk = 0; tk < 2; ++tk) {
+                // Y = H_16(F1) X in fp32; B fragments of the second MMA: hi = fp16(Y)
+                // and the residual lo = fp16(Y - hi) (one FHADD per element)
+                float yf[NJ][4];
+                const float zero[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int jc = 0; jc < NJ; ++jc) mma16816(yf[jc], AH, bf[tk][jc][0], bf[tk][jc][1], zero);
+                float2 part[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+                for (int f1 = 0; f1 < 2; ++f1) {
+                    float z[2][4];  // [outer]: Z = H_16(F2) Y, fragments of channels with bit 6 = outer
+#pragma unroll
+                    for (int o = 0; o < 2; ++o) {
+                        const float* ya = yf[2 * o];      // F2 bit 3 = 0
+                        const float* yb = yf[2 * o + 1];  // F2 bit 3 = 1
+                        const uint32_t h0 = pack_h2(ya[2 * f1], ya[2 * f1 + 1]);
+                        const uint32_t h1 = pack_h2(yb[2 * f1], yb[2 * f1 + 1]);
+                        const uint32_t l0 = pack_h2(sub_lo(ya[2 * f1], h0), sub_hi(ya[2 * f1 + 1], h0));
+                        const uint32_t l1 = pack_h2(sub_lo(yb[2 * f1], h1), sub_hi(yb[2 * f1 + 1], h1));
+                        float t4[4];
+                        mma16816(t4, AH, h0, h1, zero);
+                        mma16816(z[o], AH, l0, l1, t4);
+                    }
+                    // RoPE (bit-6 butterfly folded into u, w) and q.k over the frequency pair
+                    const float4 r4 = rope4[(2 * pq + tk) * 32 + fpi + 4 * f1];  // (u f, u f+1, w f, w f+1)
+                    const float2 u = make_float2(r4.x, r4.y), w = make_float2(r4.z, r4.w);
+#pragma unroll
+                    for (int rh = 0; rh < 2; ++rh) {
+                        const float2 al = fma2(Q2[f1][rh], w, mul2(P2[f1][rh], u));   // q_a u + q_b w
+                        const float2 be = fma2(make_float2(-Q2[f1][rh].x, -Q2[f1][rh].y), u, mul2(P2[f1][rh], w));  // q_a w - q_b u
+                        part[rh] = fma2(make_float2(z[0][2 * rh], z[0][2 * rh + 1]), al, part[rh]);
+                        part[rh] = fma2(make_float2(z[1][2 * rh], z[1][2 * rh + 1]), be, part[rh]);
+                    }
+                }
+                pv[2 * pq + tk][0] = part[0].x + part[0].y;
+                pv[2 * pq + tk][1] = part[1].x + part[1].y;
+            }
+        }
+        // reduce-scatter the 8 partials over the 16 lanes of the half-warp:
+        // lane keeps (rh = bit3, token = 2*bit2 + bit1)
+        float r4v[4], r2v[2];
+#pragma unroll
+        for (int tk = 0; tk < 4; ++tk) {
+            const float keep = bit3 ? pv[tk][1] : pv[tk][0], send = bit3 ? pv[tk][0] : pv[tk][1];
+            r4v[tk] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+        }
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {  // token pair bit2
+            const float keep = bit2 ? r4v[2 + j] : r4v[j], send = bit2 ? r4v[j] : r4v[2 + j];
+            r2v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+        }
+        float v;
+        {
+            const float keep = bit1 ? r2v[1] : r2v[0], send = bit1 ? r2v[0] : r2v[1];
+            v = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+        }
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        // the 4 logits of head hv: token 2*bit2' + bit1' sits in lane ^ (2*bit1 ^ ...) -> gather
+        const int mytk = 2 * bit2 + bit1;
+        {
+            const float x2 = __shfl_xor_sync(0xffffffffu, v, 2);  // token mytk ^ 1
+            const float x4 = __shfl_xor_sync(0xffffffffu, v, 4);  // token mytk ^ 2
+            const float x6 = __shfl_xor_sync(0xffffffffu, v, 6);  // token mytk ^ 3
+#pragma unroll
+            for (int tk = 0; tk < kTT; ++tk) {
+                const int dlt = tk ^ mytk;
+                lg[tk] = dlt == 0 ? v : dlt == 1 ? x2 : dlt == 2 ? x4 : x6;
+            }
+        }
+    };
+
+    // online softmax for head hv over a tile's tokens (valid: in range and not a
+    // sink); rescales the running state, returns the tile's probabilities
+    auto softmax_tile = [&](int it, const float (&lg)[kTT], float (&pr)[kTT]) {
+        const int64_t t0 = t_begin + static_cast<int64_t>(it) * kTT;
+        const int nv = static_cast<int>(lmin64(kTT, t_end - t0));
+        // valid tokens: in range and not a sink (t0 % 4 == 0: one mask word)
+        const uint32_t ok = ~(mask_s[(t0 >> 5) - mw0] >> (t0 & 31)) & ((1u << nv) - 1u);
+        float mx = m_run;
+#pragma unroll
+        for (int tk = 0; tk < kTT; ++tk) mx = fmaxf(mx, ((ok >> tk) & 1u) ? lg[tk] : -INFINITY);
+        if (mx > m_run) {  // rescale only when the running max moves (rare after the first tiles)
+            const float alpha = ex2(m_run - mx);
+            l_run *= alpha;
+            zc *= alpha;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) acc[e] *= alpha;
+            m_run = mx;
+        }
+#pragma unroll
+        for (int tk = 0; tk < kTT; ++tk) {
+            pr[tk] = ((ok >> tk) & 1u) ? ex2(lg[tk] - m_run) : 0.0f;
+            l_run += pr[tk];
+        }
+    };
+
+    // V phase of a tile: acc[e] += fp16(p s) * c_e * 2^(2e'-24) (codes as fp16
+    // subnormals), the zero point folded into zc with the same rounded weights
+    auto v_tile = [&](int slot, const float (&pr)[kTT]) {
+        const unsigned char* st = smem + lay.stages + slot * lay.stage_bytes;
+        const uint32_t* vc = reinterpret_cast<const uint32_t*>(st + lay.vc);
+        const uint32_t* vm = reinterpret_cast<const uint32_t*>(st + lay.vm);
+#pragma unroll
+        for (int pq = 0; pq < kPP; ++pq) {
+            const int tt0 = 2 * pq;
+            const uint32_t vw0 = vc[tt0 * W + gw], vw1 = vc[(tt0 + 1) * W + gw];
+            // weight-0 tokens may carry garbage metadata (NaN z would poison zc)
+            const uint32_t vm0 = pr[tt0] > 0.f ? vm[tt0 * MG + gm] : 0u;
+            const uint32_t vm1 = pr[tt0 + 1] > 0.f ? vm[(tt0 + 1) * MG + gm] : 0u;
+            const float ps0 = pr[tt0] * h2f(static_cast<uint16_t>(vm0 & 0xffffu));
+            const float ps1 = pr[tt0 + 1] * h2f(static_cast<uint16_t>(vm1 & 0xffffu));
+            const uint32_t wt = pack_h2(ps0, ps1);
+            const uint32_t zz = prmt(vm0, vm1, 0x7632u);  // (z0, z1)
+            zc = fhfma<0, 0>(wt, zz, zc);
+            zc = fhfma<1, 1>(wt, zz, zc);
+            const uint32_t v0s = vw0 >> 10, v1s = vw1 >> 10;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const int sh = e < 5 ? e : e - 5;
+                const uint32_t m = 0x00030003u << (2 * sh);
+                const uint32_t c0 = (e < 5 ? vw0 : v0s) & m, c1 = (e < 5 ? vw1 : v1s) & m;
+                acc[e] = fhfma<0, 0>(c0, wt, acc[e]);
+                acc[e + 8] = fhfma<1, 0>(c0, wt, acc[e + 8]);
+                acc[e] = fhfma<0, 1>(c1, wt, acc[e]);
+                acc[e + 8] = fhfma<1, 1>(c1, wt, acc[e + 8]);
+            }
+        }
+    };
+
+    // Per tile: scatter into the (single) token-pair buffer, barrier, logits +
+    // softmax + V, barrier, re-arm the stage with tile it + kNS.  The second
+    // resident CTA fills the barrier bubbles.
+    __syncthreads();  // mask words and plan
+    int slot = 0;
+    uint32_t phase = 0;
+    for (int it = 0; it < ntiles; ++it) {
+        mbar_wait(mbar + slot, phase);
+        scatter_tile(slot);
+        __syncthreads();
+        float lg[kTT], pr[kTT];
+        k_tile(slot, lg);
+        softmax_tile(it, lg, pr);
+        v_tile(slot, pr);
+        __syncthreads();
+        if (tid == 0 && it + kNS < ntiles) issue_tile(it + kNS);
+        if (++slot == kNS) {
+            slot = 0;
+            phase ^= 1u;
+        }
+    }
+
+    // ---- this warp's partial (m, l, o') for head gm
+    const int64_t row = (static_cast<int64_t>(b) * p.NP + split) * Hq + gm;
+    if ((lane & 7) == 0) {
+        p.ws_ml[row * 2] = m_run;
+        p.ws_ml[row * 2 + 1] = l_run;
+    }
+    float o[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+        const int sh = (e & 7) < 5 ? (e & 7) : (e & 7) - 5;
+        o[e] = acc[e] * __int_as_float((127 + 24 - 2 * sh) << 23) - zc;
+    }
+    float4* dst = reinterpret_cast<float4*>(p.ws_o + row * 128 + (lane & 7) * 16);
+    dst[0] = make_float4(o[0], o[1], o[2], o[3]);
+    dst[1] = make_float4(o[4], o[5], o[6], o[7]);
+    dst[2] = make_float4(o[8], o[9], o[10], o[11]);
+    dst[3] = make_float4(o[12], o[13], o[14], o[15]);
+}
+
+}  // namespace
+
+bool decode_mma_supported(int N, int REP, int C) { return N == 512 && REP == 1 && C / N * 32 <= kMmaMaxThreads; }
+
+int decode_kind(const rkv_layer_desc& d) {
+    const int N = d.heads_per_group * d.head_dim, REP = d.num_q_heads / d.num_kv_heads;
+    if (const char* e = std::getenv("RKV_DECODE_KERNEL"))
+        if (std::strcmp(e, "simt") == 0) return kDecodeSimt;
+    return decode_mma_supported(N, REP, d.num_kv_heads * d.head_dim) ? kDecodeMma : kDecodeSimt;
+}
+
+DecodePlan plan_decode_mma(const rkv_layer_desc& d, int64_t max_seq_len) {
+    DecodePlan pl{};
+    const int C = d.num_kv_heads * d.head_dim;
+    pl.kind = kDecodeMma;
+    pl.N = d.heads_per_group * d.head_dim;
+    pl.REP = d.num_q_heads / d.num_kv_heads;
+    const int NG = C / pl.N;
+    const int PW = 1, PP = kPP;
+    pl.stages = kNS;
+    pl.P = PW;
+    pl.PP = PP;
+    pl.TT = 2 * PP;
+    pl.NT = NG * 32 * PW;
+    if (max_seq_len <= 0 || max_seq_len > d.max_tokens) max_seq_len = d.max_tokens;
+    pl.smem = mma_smem(C, pl.TT, static_cast<int>(max_seq_len) + pl.TT, pl.stages).total;
+    pl.per_sm = std::max(1, std::min(kCtasPerSm, static_cast<int>((227u * 1024u) / (pl.smem + 1024))));
+    {
+        int n = 0;
+        auto kern = decode_mma_kernel<4, 1>;
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pl.smem)) ==
+                cudaSuccess &&
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, pl.NT, pl.smem) == cudaSuccess && n > 0)
+            pl.per_sm = n;
+        else
+            cudaGetLastError();
+    }
+    const int ctas = num_sms() * pl.per_sm;
+    int S = ctas / d.batch;
+    if (S < 1) S = 1;
+    const int64_t max_split = (max_seq_len + 4 * pl.TT - 1) / (4 * pl.TT);
+    if (S > max_split) S = static_cast<int>(max_split > 0 ? max_split : 1);
+    int64_t chunk = (max_seq_len + S - 1) / S;
+    chunk = (chunk + pl.TT - 1) / pl.TT * pl.TT;
+    pl.chunk = static_cast<int>(chunk);
+    pl.S = static_cast<int>((max_seq_len + chunk - 1) / chunk);
+    pl.NP = pl.S * PW;
+    pl.smem = mma_smem(C, pl.TT, pl.chunk, pl.stages).total;
+    pl.ok = pl.NT <= kMmaMaxThreads && pl.smem <= 227 * 1024 && pl.NT % (C / 16) == 0;
+    return pl;
+}
+
+cudaError_t launch_decode_mma(const rkv_layer_desc& d, const DecodePlan& plan, const DecodeParams& p, cudaStream_t s) {
+    auto kern = decode_mma_kernel<4, 1>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(plan.smem));
+    if (e != cudaSuccess) return e;
+    kern<<<dim3(plan.S, d.batch), plan.NT, plan.smem, s>>>(p);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    return launch_decode_combine(p, d.batch, s);
+}
+
+}  // namespace rkv

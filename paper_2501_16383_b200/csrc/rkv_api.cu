@@ -147,7 +147,10 @@ rkv_status rkv_cache_reset(const rkv_layer_desc* desc, const rkv_cache* cache, v
 
 size_t rkv_rope_table_bytes(const rkv_layer_desc* desc, int64_t max_pos) {
     if (validate(desc) != RKV_OK || max_pos < 1) return 0;
-    return static_cast<size_t>((max_pos + 1) / 2) * (desc->head_dim / 2) * 4 * sizeof(float);
+    // per position pair 128 float4: section 1 (cos p0, cos p1, sin p0, sin p1) x 64
+    // frequencies, section 2 two [32] frequency-pair rows (decode_attention.cu)
+    const size_t npairs = static_cast<size_t>((max_pos + 1) / 2);
+    return 2 * npairs * (desc->head_dim / 2) * 4 * sizeof(float);
 }
 
 rkv_status rkv_rope_table_init(const rkv_layer_desc* desc, float* table, int64_t max_pos, void* stream) {
@@ -258,8 +261,7 @@ rkv_status rkv_decode_attention(const rkv_layer_desc* desc, const uint16_t* q, c
     if (ws_bytes < rkv_decode_workspace_bytes(desc, max_seq_len))
         return fail(RKV_ERR_INVALID_ARGUMENT, "decode_attention: workspace too small");
     rkv::DecodePlan pl = rkv::plan_decode(*desc, max_seq_len);
-    const int W = desc->num_kv_heads * desc->head_dim / 16;
-    if (pl.NT > (pl.N == 512 ? 320 : 256) || pl.smem > 227 * 1024 || (pl.NT % W != 0 && W % pl.NT != 0))
+    if (!pl.ok)
         return fail(RKV_ERR_INVALID_ARGUMENT, "decode_attention: layer shape exceeds the sm_100a kernel's tile budget");
     const size_t rows = static_cast<size_t>(desc->batch) * pl.NP * desc->num_q_heads;
     rkv::DecodeParams p{};
@@ -281,6 +283,7 @@ rkv_status rkv_decode_attention(const rkv_layer_desc* desc, const uint16_t* q, c
     p.max_sinks = desc->max_sinks;
     p.chunk = pl.chunk;
     p.P = pl.P;
+    p.P_pairs = pl.PP;
     p.stages = pl.stages;
     p.k_norm = 1.0f / std::sqrt(static_cast<float>(desc->heads_per_group * desc->head_dim));
     p.qscale = rkv::kLog2eHost / std::sqrt(static_cast<float>(desc->head_dim));

@@ -32,7 +32,8 @@ struct DecodeParams {
     const uint16_t* q;
     const int64_t* seq_len;
     const uint32_t* plan;  // rkv_layer_plan_init (rkv_layout.h)
-    const float4* rope;  // [max_pos/2][64] (cos p0, cos p1, sin p0, sin p1)
+    const float4* rope;  // [max_pos/2][128]: section 1 (cos p0, cos p1, sin p0, sin p1) x 64, section 2
+                         // two [32] frequency-pair rows (decode_attention.cu, kRopeRow)
     rkv_cache cache;
     float* ws_ml;  // [B][NP][Hq][2]   partial (m, l) per lane-group partition
     float* ws_o;   // [B][NP][Hq][128] partial o' (rotated V frame)
@@ -42,7 +43,8 @@ struct DecodeParams {
     int S;      // splits (CTAs per sequence)
     int NP;     // partial rows per sequence = S * P
     int chunk;  // tokens per split, multiple of the tile
-    int P;      // token pairs per tile (= lane-group partitions per FWHT group)
+    int P;      // partial partitions per split (simt: token pairs per tile; mma: warps per FWHT group)
+    int P_pairs;  // mma kernel: token pairs per tile
     int stages; // TMA ring depth
     int max_sinks;
     float k_norm;  // 1/sqrt(G*d), folded into q
@@ -53,13 +55,21 @@ struct DecodeParams {
 cudaError_t launch_quantize(const rkv_layer_desc& d, const QuantParams& p, cudaStream_t s);
 // decode_attention.cu
 struct DecodePlan {
-    int N, REP, P, TT, NT, S, NP, chunk, stages, per_sm;
+    int kind, N, REP, P, PP, TT, NT, S, NP, chunk, stages, per_sm;
+    bool ok;
     size_t smem;
 };
 bool decode_supported(int N, int REP);
 DecodePlan plan_decode(const rkv_layer_desc& d, int64_t max_seq_len);
 cudaError_t launch_decode(const rkv_layer_desc& d, const DecodePlan& plan, const DecodeParams& p,
                           cudaStream_t s);
+cudaError_t launch_decode_combine(const DecodeParams& p, int B, cudaStream_t s);
+// decode_mma.cu (tensor-core FWHT kernel)
+int decode_kind(const rkv_layer_desc& d);  // kDecodeSimt / kDecodeMma (rkv_layout.h)
+bool decode_mma_supported(int N, int REP, int C);
+DecodePlan plan_decode_mma(const rkv_layer_desc& d, int64_t max_seq_len);
+cudaError_t launch_decode_mma(const rkv_layer_desc& d, const DecodePlan& plan, const DecodeParams& p,
+                              cudaStream_t s);
 cudaError_t launch_rope_table(const rkv_layer_desc& d, float4* table, int64_t max_pos, cudaStream_t s);
 cudaError_t launch_rotate_keys(const rkv_layer_desc& d, const uint16_t* k, int64_t rows, float* out,
                                cudaStream_t s);

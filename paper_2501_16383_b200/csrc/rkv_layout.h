@@ -30,6 +30,32 @@ RKV_HD inline int knat_pos(int N, int c) {
 }
 RKV_HD inline int knat_pair_f2(int N, int C) { return (C / N) * knat_unit(N); }  // float2 per pair row
 
+// ---------------------------------------------------------------------------
+// Tensor-core decode (decode_mma.cu) K tile: per token pair one u32 =
+// half2(token, token+1) per channel, laid out in mma.sync B-fragment order.
+// A group's N = 128*G channel index i is split into bit fields:
+//   F1 = bits 0-3                   contraction of the first  H_16 MMA
+//   F2 = bits {4,5,7,8} (G = 4)     contraction of the second H_16 MMA
+//        bits {4,5,7,6} (G = 2)
+//   outer = bit 6 (G = 4 only)      the last H_2, fused into RoPE
+// B fragment of m16n8k16 (k = F1, n = F2 bits 0-2): lane = 4*n + (k>>1 & 3)
+// holds k = 2t,2t+1 (kreg 0) and 2t+8,2t+9 (kreg 1); instance jc = F2 bit 3
+// (+ 2*outer).  Each lane's EPL = N/32 elements (4 per 16-byte chunk, one
+// chunk per instance) are contiguous; chunks are XOR-swizzled by lane so the
+// per-lane LDS.128 fragment loads are bank-conflict free.
+RKV_HD inline int mma_nj(int N) { return N / 128; }  // MMA-1 instances = 16-byte chunks per lane
+RKV_HD inline int mma_swz(int N, int lane) { return N == 512 ? (lane >> 1) & 3 : (lane >> 2) & 1; }
+RKV_HD inline int mma_pos(int N, int c) {  // byte offset of channel c in a token-pair row
+    const int g = c / N, i = c % N;
+    const int k = i & 15;
+    const int n = ((i >> 4) & 1) | (((i >> 5) & 1) << 1) | (((i >> 7) & 1) << 2);
+    const int jc = N == 512 ? (((i >> 8) & 1) | (((i >> 6) & 1) << 1)) : ((i >> 6) & 1);
+    const int lane = 4 * n + ((k >> 1) & 3);
+    const int nj = mma_nj(N);
+    const int chunk = jc ^ mma_swz(N, lane);
+    return g * N * 4 + lane * nj * 16 + chunk * 16 + ((k >> 3) * 2 + (k & 1)) * 4;
+}
+
 // Decode plan (rkv_layer_plan_init, rkv_plan.cu): the un-reorder scatter's
 // word assignment.
 //   words[0 .. kPlanHeader)   header (magic, version, N, L, C, W, cost)
@@ -41,9 +67,13 @@ RKV_HD inline int knat_pair_f2(int N, int C) { return (C / N) * knat_unit(N); } 
 // A half-warp = 16 consecutive word positions; in round e every lane stores
 // code e of its word.  omega is chosen per layer to spread each round's 16
 // stores over distinct 8-byte bank slots.
+// For the tensor-core kernel (PH_KIND = 1) the offsets are mma_pos() bytes,
+// a warp = 32 consecutive word positions stores half2 words (STS.32) and
+// omega spreads each round's 32 stores over distinct 4-byte banks.
 constexpr uint32_t kPlanMagic = 0x504B5652u;  // "RVKP"
 constexpr int kPlanHeader = 16;
-enum { PH_MAGIC = 0, PH_VERSION, PH_N, PH_L, PH_C, PH_W, PH_COST };
+enum { PH_MAGIC = 0, PH_VERSION, PH_N, PH_L, PH_C, PH_W, PH_COST, PH_KIND };
+enum { kDecodeSimt = 0, kDecodeMma = 1 };
 
 RKV_HD inline int plan_words(int W) { return kPlanHeader + W + 16 * W; }
 

@@ -36,13 +36,14 @@ struct SplitMix {
     double uniform() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
 };
 
-// sum over rounds e of the largest bank-slot multiplicity among 16 words
-int group_cost(const int* cls, const int* words) {
+// sum over rounds e of the largest bank-slot multiplicity among the GS words
+// of one store group (16 lanes x 8-byte slots, or 32 lanes x 4-byte banks)
+int group_cost(const int* cls, const int* words, int GS) {
     int cost = 0;
     for (int e = 0; e < 16; ++e) {
-        int cnt[16] = {0};
+        int cnt[32] = {0};
         int mx = 0;
-        for (int i = 0; i < 16; ++i) mx = std::max(mx, ++cnt[cls[words[i] * 16 + e]]);
+        for (int i = 0; i < GS; ++i) mx = std::max(mx, ++cnt[cls[words[i] * 16 + e]]);
         cost += mx;
     }
     return cost;
@@ -52,14 +53,18 @@ int group_cost(const int* cls, const int* words) {
 
 bool build_decode_plan(const rkv_layer_desc& d, const int32_t* perm, std::vector<uint32_t>& out, int& cost_out) {
     const int C = d.num_kv_heads * d.head_dim, N = d.heads_per_group * d.head_dim;
-    const int W = C / 16, G = W / 16;
+    const int kind = decode_kind(d);
+    const int GS = kind == kDecodeMma ? 32 : 16;  // lanes whose stores share a wavefront
+    const int W = C / 16, G = W / GS;
+    auto pos = [&](int c) { return kind == kDecodeMma ? mma_pos(N, c) : knat_pos(N, c) * 8; };
     std::vector<int> cls(static_cast<size_t>(C));
-    for (int j = 0; j < C; ++j) cls[static_cast<size_t>(j)] = knat_pos(N, perm[j]) & 15;
+    for (int j = 0; j < C; ++j)
+        cls[static_cast<size_t>(j)] = kind == kDecodeMma ? (pos(perm[j]) >> 2) & 31 : (pos(perm[j]) >> 3) & 15;
 
     std::vector<int> omega(static_cast<size_t>(W));
     for (int w = 0; w < W; ++w) omega[static_cast<size_t>(w)] = w;
     std::vector<int> cost(static_cast<size_t>(G));
-    for (int k = 0; k < G; ++k) cost[static_cast<size_t>(k)] = group_cost(cls.data(), &omega[static_cast<size_t>(k) * 16]);
+    for (int k = 0; k < G; ++k) cost[static_cast<size_t>(k)] = group_cost(cls.data(), &omega[static_cast<size_t>(k) * GS], GS);
     if (G > 1) {
         SplitMix rng{0x5EEDULL ^ static_cast<uint64_t>(C) * 0x9E3779B97F4A7C15ULL};
         const long iters = 120000L * std::min(G, 8);
@@ -67,11 +72,11 @@ bool build_decode_plan(const rkv_layer_desc& d, const int32_t* perm, std::vector
             const double T = 1.5 * (1.0 - static_cast<double>(it) / static_cast<double>(iters)) + 1e-3;
             const int p1 = static_cast<int>(rng.next() % static_cast<uint64_t>(W));
             const int p2 = static_cast<int>(rng.next() % static_cast<uint64_t>(W));
-            const int g1 = p1 / 16, g2 = p2 / 16;
+            const int g1 = p1 / GS, g2 = p2 / GS;
             if (g1 == g2) continue;
             std::swap(omega[static_cast<size_t>(p1)], omega[static_cast<size_t>(p2)]);
-            const int c1 = group_cost(cls.data(), &omega[static_cast<size_t>(g1) * 16]);
-            const int c2 = group_cost(cls.data(), &omega[static_cast<size_t>(g2) * 16]);
+            const int c1 = group_cost(cls.data(), &omega[static_cast<size_t>(g1) * GS], GS);
+            const int c2 = group_cost(cls.data(), &omega[static_cast<size_t>(g2) * GS], GS);
             const int dl = c1 + c2 - cost[static_cast<size_t>(g1)] - cost[static_cast<size_t>(g2)];
             if (dl <= 0 || rng.uniform() < std::exp(-dl / T)) {
                 cost[static_cast<size_t>(g1)] = c1;
@@ -87,19 +92,20 @@ bool build_decode_plan(const rkv_layer_desc& d, const int32_t* perm, std::vector
 
     out.assign(static_cast<size_t>(plan_words(W)), 0u);
     out[PH_MAGIC] = kPlanMagic;
-    out[PH_VERSION] = 2;
+    out[PH_VERSION] = 3;
     out[PH_N] = static_cast<uint32_t>(N);
     out[PH_L] = static_cast<uint32_t>(fwht_lanes(N));
     out[PH_C] = static_cast<uint32_t>(C);
     out[PH_W] = static_cast<uint32_t>(W);
     out[PH_COST] = static_cast<uint32_t>(total);
+    out[PH_KIND] = static_cast<uint32_t>(kind);
     uint32_t* om = out.data() + kPlanHeader;
     uint32_t* addr = om + W;
     for (int wp = 0; wp < W; ++wp) {
         const int w = omega[static_cast<size_t>(wp)];
         om[wp] = static_cast<uint32_t>(w);
         for (int e = 0; e < 16; ++e)
-            addr[(static_cast<size_t>(e / 4) * W + wp) * 4 + e % 4] = static_cast<uint32_t>(knat_pos(N, perm[w * 16 + e])) * 8u;
+            addr[(static_cast<size_t>(e / 4) * W + wp) * 4 + e % 4] = static_cast<uint32_t>(pos(perm[w * 16 + e]));
     }
     return true;
 }

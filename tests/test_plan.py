@@ -21,13 +21,31 @@ def knat_pos(N, c):
     return g * L * (R + 1) + (i // R) * (R + 1) + (i % R)
 
 
-def cost_of(cls, omega):
+def mma_pos(N, c):
+    """Byte offset of channel c in the tensor-core kernel's token-pair row (rkv_layout.h mma_pos)."""
+    g, i = c // N, c % N
+    k = i & 15
+    n = ((i >> 4) & 1) | (((i >> 5) & 1) << 1) | (((i >> 7) & 1) << 2)
+    jc = (((i >> 8) & 1) | (((i >> 6) & 1) << 1)) if N == 512 else ((i >> 6) & 1)
+    lane = 4 * n + ((k >> 1) & 3)
+    nj = N // 128
+    swz = ((lane >> 1) & 3) if N == 512 else ((lane >> 2) & 1)
+    return g * N * 4 + lane * nj * 16 + (jc ^ swz) * 16 + ((k >> 3) * 2 + (k & 1)) * 4
+
+
+def cost_of(cls, omega, gs=16):
     tot = 0
-    for k in range(len(omega) // 16):
-        words = omega[16 * k:16 * k + 16]
+    for k in range(len(omega) // gs):
+        words = omega[gs * k:gs * k + gs]
         for e in range(16):
-            tot += np.bincount(cls[words, e], minlength=16).max()
+            tot += np.bincount(cls[words, e], minlength=gs).max()
     return tot
+
+
+def test_mma_positions_are_a_bijection():
+    for N, C in [(512, 5120), (512, 4096), (256, 1024)]:
+        pos = sorted(mma_pos(N, c) for c in range(C))
+        assert pos == list(range(0, 4 * C, 4))
 
 
 @pytest.mark.parametrize("hq,hkv,g,seed", [(40, 40, 4, 0), (32, 32, 4, 1), (32, 8, 2, 2), (8, 8, 4, 3), (4, 4, 1, 4)])
@@ -42,14 +60,17 @@ def test_plan_is_a_valid_scatter(hq, hkv, g, seed):
     omega = words[HEADER:HEADER + W].astype(np.int64)
     addr = words[HEADER + W:HEADER + W + 16 * W].reshape(4, W, 4)
     assert sorted(omega.tolist()) == list(range(W))
+    mma = int(words[7]) == 1  # PH_KIND: tensor-core decode layout
+    pos = (lambda c: mma_pos(N, c)) if mma else (lambda c: knat_pos(N, c) * 8)
     for wp in range(W):
         w = omega[wp]
         for e in range(16):
-            assert addr[e // 4, wp, e % 4] == knat_pos(N, int(perm[16 * w + e])) * 8
-    cls = np.array([knat_pos(N, int(c)) % 16 for c in perm]).reshape(W, 16)
-    assert cost == cost_of(cls, omega)
-    if W >= 32:  # more than one half-warp group: the assignment must beat the identity
-        assert cost < 0.85 * cost_of(cls, np.arange(W))
+            assert addr[e // 4, wp, e % 4] == pos(int(perm[16 * w + e]))
+    gs = 32 if mma else 16
+    cls = np.array([(pos(int(c)) >> 2) % 32 if mma else (pos(int(c)) >> 3) % 16 for c in perm]).reshape(W, 16)
+    assert cost == cost_of(cls, omega, gs)
+    if W >= 2 * gs:  # more than one store group: the assignment must beat the identity
+        assert cost < 0.85 * cost_of(cls, np.arange(W), gs)
 
 
 def test_plan_rejects_non_permutation():
