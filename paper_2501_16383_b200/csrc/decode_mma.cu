@@ -181,16 +181,18 @@ __device__ __forceinline__ void mma16816_h(uint32_t (&d)[2], const uint32_t (&a)
 // barrier and MMA-latency stalls.
 constexpr int kPP = 2, kTT = 2 * kPP, kNS = 3, kCtasPerSm = 2;
 
-// G = 4 (N = 512), one q head per KV head.
-template <int G, int REP>
+// G = 4 (N = 512), one q head per KV head.  NGC = number of FWHT groups
+// (C / 512) when known at compile time (8: LLaMA-2-7B, 10: 13B), so every
+// shared-memory offset folds into an immediate; 0 = taken from the launch.
+template <int G, int REP, int NGC>
 __global__ void __launch_bounds__(320, kCtasPerSm) decode_mma_kernel(DecodeParams p) {
     static_assert(G == 4 && REP == 1, "decode_mma_kernel: G = 4, MHA");
     constexpr int N = 128 * G;
     constexpr int NJ = N / 128;  // MMA-1 instances per token (F2 bit 3, outer bit 6)
 
     extern __shared__ __align__(128) unsigned char smem[];
-    const int C = p.C, W = C / 16, MG = C / 128, Hq = p.Hq;
-    const int NG = C / N;
+    const int NG = NGC ? NGC : p.C / N;
+    const int C = NG * N, W = C / 16, MG = C / 128, Hq = NGC ? NGC * G * REP : p.Hq;
     const MmaSmem lay = mma_smem(C, kTT, p.chunk, kNS);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + lay.mbar);
     uint32_t* mask_s = reinterpret_cast<uint32_t*>(smem + lay.mask);
@@ -423,18 +425,9 @@ __global__ void __launch_bounds__(320, kCtasPerSm) decode_mma_kernel(DecodeParam
             v = keep + __shfl_xor_sync(0xffffffffu, send, 2);
         }
         v += __shfl_xor_sync(0xffffffffu, v, 1);
-        // the 4 logits of head hv: token 2*bit2' + bit1' sits in lane ^ (2*bit1 ^ ...) -> gather
-        const int mytk = 2 * bit2 + bit1;
-        {
-            const float x2 = __shfl_xor_sync(0xffffffffu, v, 2);  // token mytk ^ 1
-            const float x4 = __shfl_xor_sync(0xffffffffu, v, 4);  // token mytk ^ 2
-            const float x6 = __shfl_xor_sync(0xffffffffu, v, 6);  // token mytk ^ 3
+        // the 4 logits of head hv: token tk sits in the lanes with bits (2,1) = tk
 #pragma unroll
-            for (int tk = 0; tk < kTT; ++tk) {
-                const int dlt = tk ^ mytk;
-                lg[tk] = dlt == 0 ? v : dlt == 1 ? x2 : dlt == 2 ? x4 : x6;
-            }
-        }
+        for (int tk = 0; tk < kTT; ++tk) lg[tk] = __shfl_sync(0xffffffffu, v, (lane & 0x19) | (tk << 1));
     };
 
     // online softmax for head hv over a tile's tokens (valid: in range and not a
@@ -565,7 +558,7 @@ DecodePlan plan_decode_mma(const rkv_layer_desc& d, int64_t max_seq_len) {
     pl.per_sm = std::max(1, std::min(kCtasPerSm, static_cast<int>((227u * 1024u) / (pl.smem + 1024))));
     {
         int n = 0;
-        auto kern = decode_mma_kernel<4, 1>;
+        auto kern = decode_mma_kernel<4, 1, 0>;
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pl.smem)) ==
                 cudaSuccess &&
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, pl.NT, pl.smem) == cudaSuccess && n > 0)
@@ -589,7 +582,8 @@ DecodePlan plan_decode_mma(const rkv_layer_desc& d, int64_t max_seq_len) {
 }
 
 cudaError_t launch_decode_mma(const rkv_layer_desc& d, const DecodePlan& plan, const DecodeParams& p, cudaStream_t s) {
-    auto kern = decode_mma_kernel<4, 1>;
+    const int NG = p.C / 512;
+    auto kern = NG == 10 ? decode_mma_kernel<4, 1, 10> : NG == 8 ? decode_mma_kernel<4, 1, 8> : decode_mma_kernel<4, 1, 0>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(plan.smem));
     if (e != cudaSuccess) return e;
     kern<<<dim3(plan.S, d.batch), plan.NT, plan.smem, s>>>(p);

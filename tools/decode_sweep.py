@@ -1,0 +1,66 @@
+"""Decode-kernel timing over the BASELINE decode configs on one GPU (a
+development tool next to bench.py): fills a seeded 2-bit cache per config and
+times rkv_decode_attention alone with CUDA events.
+
+    python tools/decode_sweep.py [cfg ...]      (default: 2 3 4)
+    RKV_DECODE_KERNEL=simt python tools/decode_sweep.py   # the CUDA-core kernel
+
+cfg 4 (8 x 32768 tokens) is timed at full size; cfg 3 at batch 64 x 8192.
+"""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2501_16383_b200 as P  # noqa: E402
+from paper_2501_16383_b200 import workload as WL  # noqa: E402
+
+
+def decode_bytes(w, B, T, nsinks):
+    c = w.channels
+    return B * ((T - nsinks) * 2 * (c // 4 + 4 * c // 128) + nsinks * 4 * c) + B * w.num_q_heads * 128 * 6
+
+
+def run(cfg_id, iters=20):
+    w = WL.CONFIGS[cfg_id]
+    dev = torch.device("cuda", 0)
+    B, T = w.batch, w.tokens
+    perm = WL.calibration_perm(w, 42 + cfg_id, device=dev)
+    cfg = P.LayerConfig(batch=B, num_q_heads=w.num_q_heads, num_kv_heads=w.num_kv_heads,
+                        heads_per_group=w.heads_per_group, max_tokens=T, max_sinks=4, rope_base=w.rope_base)
+    layer = P.RotateKVLayer(cfg, perm, device=dev)
+    flags_row = np.zeros(T, np.uint8)
+    for t in WL.sink_positions(w, 42 + cfg_id, T):
+        flags_row[t] = 1
+    flags = torch.from_numpy(np.tile(flags_row, (B, 1)))
+    chunk = max(1, min(T, (1 << 26) // (B * w.channels)))
+    for t0 in range(0, T, chunk):
+        k, v = WL.make_kv(w, 42 + cfg_id + t0, B, min(chunk, T - t0), device=dev)
+        layer.append(k, v, flags[:, t0:t0 + k.shape[1]])
+        del k, v
+    q = WL.make_q(w, 42 + cfg_id, B, device=dev)
+    lens = torch.full((B,), T, dtype=torch.int64, device=dev)
+    out = torch.empty(B, w.num_q_heads, 128, dtype=torch.float32, device=dev)
+    ws, wsb = layer.workspace(T)
+    for _ in range(3):
+        layer.decode_device(q, lens, T, out, ws, wsb)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        layer.decode_device(q, lens, T, out, ws, wsb)
+    e1.record()
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / iters
+    nb = decode_bytes(w, B, T, int(flags_row.sum()))
+    return {"cfg": cfg_id, "workload": w.name, "kernel": os.environ.get("RKV_DECODE_KERNEL", "default"),
+            "us": round(us, 1), "GB/s": round(nb / us / 1e3, 1), "bytes": nb}
+
+
+if __name__ == "__main__":
+    ids = [int(a) for a in sys.argv[1:]] or [2, 3, 4]
+    for i in ids:
+        print(json.dumps(run(i)), flush=True)
