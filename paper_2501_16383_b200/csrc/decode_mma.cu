@@ -529,9 +529,408 @@ __global__ void __launch_bounds__(320, kCtasPerSm) decode_mma_kernel(DecodeParam
     dst[3] = make_float4(o[12], o[13], o[14], o[15]);
 }
 
+// ---------------------------------------------------------------------------
+// GQA variant: G = 2 (N = 256, two KV heads per FWHT group), REP q heads per
+// KV head (BASELINE config 3: LLaMA-3-8B, 32 q / 8 KV heads).  The K side is
+// the same H_16 (x) H_16 chain (no outer bit: channel bit 6, the RoPE
+// partner, is F2 bit 3, i.e. the row half of the second MMA's output).  With
+// REP = 4 the P.V product is a real matrix product and runs on the tensor
+// cores too: per 8 tokens and code position e, one m16n8k8 with A = the
+// codes of 16 channels (8 words x {e, e+8}) as fp16 subnormals (one LOP3 per
+// register) and B = the 4 heads' weights p*s split into fp16 hi and lo
+// columns.  A warp owns one group and 8 consecutive tokens of a tile (PW warps
+// per group split the tile), keeps 64 fp32 P.V accumulators and its own
+// softmax state, and emits one partial per (warp, head).
+constexpr int kGqaNS = 3;
+
+__device__ __forceinline__ void mma1688(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t b) {
+    asm("mma.sync.aligned.m16n8k8.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(b));
+}
+
+__host__ __device__ inline MmaSmem gqa_smem(int C, int TT, int chunk) {
+    MmaSmem s{};
+    const int W = C / 16, MG = C / 128, PP = TT / 2;
+    s.kc = 0;
+    s.km = al16(s.kc + size_t(TT) * W * 4);
+    s.vc = al16(s.km + size_t(TT) * MG * 4);
+    s.vm = al16(s.vc + size_t(TT) * W * 4);
+    s.rope = al16(s.vm + size_t(TT) * MG * 4);
+    s.stage_bytes = al16(s.rope + size_t(PP) * 64 * 16);
+    s.stages = 0;
+    s.mbar = s.stages + kGqaNS * s.stage_bytes;
+    s.knat = al16(s.mbar + kGqaNS * 8);
+    s.plan = al16(s.knat + size_t(PP) * C * 4);
+    s.mask = al16(s.plan + size_t(17) * W * 4);
+    s.total = al16(s.mask + size_t(chunk / 32 + 2) * 4);
+    return s;
+}
+
+template <int REP, int PW>
+__global__ void __launch_bounds__(32 * 4 * PW, 1) decode_gqa_kernel(DecodeParams p) {
+    static_assert(REP == 4, "decode_gqa_kernel: 4 q heads per KV head");
+    constexpr int G = 2, N = 256, NJ = 2, TT = 8 * PW, PPT = TT / 2;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int C = p.C, W = C / 16, MG = C / 128, Hq = p.Hq, NG = C / N;
+    const MmaSmem lay = gqa_smem(C, TT, p.chunk);
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + lay.mbar);
+    uint32_t* mask_s = reinterpret_cast<uint32_t*>(smem + lay.mask);
+
+    const int tid = threadIdx.x, NT = blockDim.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int gam = warp % NG, pw = warp / NG;
+    const int b = blockIdx.y, split = blockIdx.x;
+    const int64_t T = p.seq_len[b];
+    const int64_t t_begin = static_cast<int64_t>(split) * p.chunk;
+    const int64_t t_end = lmin64(T, t_begin + p.chunk);
+
+    if (t_begin >= t_end) {  // empty split: neutral partials
+        for (int i = tid; i < PW * Hq; i += NT) {
+            const int64_t row = (static_cast<int64_t>(b) * p.NP + static_cast<int64_t>(split) * PW + i / Hq) * Hq + i % Hq;
+            p.ws_ml[row * 2] = -INFINITY;
+            p.ws_ml[row * 2 + 1] = 0.0f;
+            float4* o = reinterpret_cast<float4*>(p.ws_o + row * 128);
+            for (int k = 0; k < 32; ++k) o[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        return;
+    }
+    const int ntiles = static_cast<int>((t_end - t_begin + TT - 1) / TT);
+    const int64_t row0 = static_cast<int64_t>(b) * p.max_tokens;
+
+    auto issue_tile = [&](int it) {
+        const int64_t t0 = t_begin + static_cast<int64_t>(it) * TT;
+        const uint32_t n = static_cast<uint32_t>(lmin64(TT, t_end - t0));
+        unsigned char* st = smem + lay.stages + (it % kGqaNS) * lay.stage_bytes;
+        uint64_t* bar = mbar + (it % kGqaNS);
+        const uint32_t bw = n * W * 4, bm = n * MG * 4, npr = (n + 1) >> 1;
+        mbar_arrive_expect_tx(bar, 2 * bw + 2 * bm + npr * 1024);
+        bulk_g2s(st + lay.kc, p.cache.k_codes + (row0 + t0) * W, bw, bar);
+        bulk_g2s(st + lay.km, p.cache.k_meta + (row0 + t0) * MG, bm, bar);
+        bulk_g2s(st + lay.vc, p.cache.v_codes + (row0 + t0) * W, bw, bar);
+        bulk_g2s(st + lay.vm, p.cache.v_meta + (row0 + t0) * MG, bm, bar);
+        for (uint32_t r = 0; r < npr; ++r)
+            bulk_g2s(st + lay.rope + r * 1024, p.rope + ((t0 >> 1) + r) * 128 + 64, 1024, bar);
+    };
+
+    if (tid == 0) {
+        for (int s = 0; s < kGqaNS; ++s) mbar_init(mbar + s, 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    if (tid == 0)
+        for (int it = 0; it < kGqaNS && it < ntiles; ++it) issue_tile(it);
+
+    const int64_t mw0 = t_begin >> 5;
+    {
+        const uint32_t* smask = p.cache.sink_mask + static_cast<int64_t>(b) * ((p.max_tokens + 31) / 32);
+        const int nw = static_cast<int>(((t_end - 1) >> 5) - mw0 + 1);
+        for (int i = tid; i < nw; i += NT) mask_s[i] = smask[mw0 + i];
+    }
+    const uint32_t* plan_s = reinterpret_cast<const uint32_t*>(smem + lay.plan);
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(p.plan + kPlanHeader);
+        uint4* dst = reinterpret_cast<uint4*>(smem + lay.plan);
+        for (int i = tid; i < 17 * W / 4; i += NT) dst[i] = __ldg(src + i);
+    }
+    const uint32_t pair_bytes = static_cast<uint32_t>(C) * 4u;
+    auto bexp = [](int sh) -> uint32_t { const uint32_t be = static_cast<uint32_t>(25 - 2 * sh) << 10; return be | (be << 16); };
+
+    // scatter: thread -> word position wp, token pairs pq0 and pq0 + NT/W (two per thread)
+    const int wp = tid % W, pq0 = tid / W, pqs = NT / W;
+    auto scatter_tile = [&](int slot) {
+        const unsigned char* st = smem + lay.stages + slot * lay.stage_bytes;
+        const uint32_t* kc = reinterpret_cast<const uint32_t*>(st + lay.kc);
+        const uint32_t* km = reinterpret_cast<const uint32_t*>(st + lay.km);
+        const uint32_t buf = static_cast<uint32_t>(lay.knat) + smem_u32(smem);
+        const int wsrc = static_cast<int>(plan_s[wp]);
+        uint32_t ad[16];
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+            const uint4 a4 = reinterpret_cast<const uint4*>(plan_s + W)[q4 * W + wp];
+            ad[4 * q4] = a4.x;
+            ad[4 * q4 + 1] = a4.y;
+            ad[4 * q4 + 2] = a4.z;
+            ad[4 * q4 + 3] = a4.w;
+        }
+        for (int pq = pq0; pq < PPT; pq += pqs) {
+            const int tt0 = 2 * pq;
+            const uint32_t w0 = kc[tt0 * W + wsrc], w1 = kc[(tt0 + 1) * W + wsrc];
+            const uint32_t m0 = km[tt0 * MG + (wsrc >> 3)], m1 = km[(tt0 + 1) * MG + (wsrc >> 3)];
+            const uint32_t ss = prmt(m0, m1, 0x5410u), zz = prmt(m0, m1, 0x7632u);
+            uint32_t bz[5];
+#pragma unroll
+            for (int e = 0; e < 5; ++e) bz[e] = h2add(bexp(e), zz);
+            const uint32_t xl = prmt(w0, w1, 0x5410u), xh = prmt(w0, w1, 0x7632u);
+            const uint32_t xls = xl >> 10, xhs = xh >> 10;
+            const uint32_t dst = buf + static_cast<uint32_t>(pq) * pair_bytes;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                const int ee = e & 7;
+                const uint32_t src = ee < 5 ? (e < 8 ? xl : xh) : (e < 8 ? xls : xhs);
+                const int sh = ee < 5 ? ee : ee - 5;
+                const uint32_t h = and_or(src, 0x00030003u << (2 * sh), bexp(sh));
+                const uint32_t x = h2mul(h2sub(h, bz[sh]), ss);
+                asm volatile("st.shared.b32 [%0], %1;" ::"r"(dst + ad[e]), "r"(x) : "memory");
+            }
+        }
+    };
+
+    // ---- compute role: lane (g, tl); KV head kvh = lane >> 4 of the group
+    const int g = lane >> 2, tl = lane & 3, kvh = lane >> 4;
+    const int bit0 = lane & 1, bit1 = (lane >> 1) & 1, bit2 = (lane >> 2) & 1, bit3 = (lane >> 3) & 1;
+    uint32_t AH[4];
+    hadamard16_frag(AH, lane);
+    // RoPE(T-1) q of the frequency pairs (f, f+1), (f+64, f+65).  Slot sl holds
+    // head r = sl ^ (g & 3): the first two reduce-scatter steps then keep / send
+    // fixed slots on every lane (no selects) and leave head g & 3 in slot 0.
+    float2 QA[2][REP], QB[2][REP];
+    {
+        const float4* cs = p.rope + ((T - 1) >> 1) * 128;
+        const bool odd = (T - 1) & 1;
+        const uint16_t* qb = p.q + static_cast<int64_t>(b) * Hq * 128;
+        const float qs = p.qscale * p.k_norm;
+#pragma unroll
+        for (int f1 = 0; f1 < 2; ++f1) {
+#pragma unroll
+            for (int sl = 0; sl < REP; ++sl) {
+                const int r = sl ^ (g & 3);
+                const int hq = (gam * G + kvh) * REP + r;
+                float a2[2], b2[2];
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const int f = 2 * tl + i + 8 * f1 + 16 * (g & 3);
+                    const float4 r4 = __ldg(cs + f);
+                    const float cT = odd ? r4.y : r4.x, sT = odd ? r4.w : r4.z;
+                    const float a = h2f(qb[hq * 128 + f]), bb = h2f(qb[hq * 128 + f + 64]);
+                    a2[i] = (a * cT - bb * sT) * qs;
+                    b2[i] = (a * sT + bb * cT) * qs;
+                }
+                QA[f1][sl] = make_float2(a2[0], a2[1]);
+                QB[f1][sl] = make_float2(b2[0], b2[1]);
+            }
+        }
+    }
+    const uint32_t lane_off = static_cast<uint32_t>(gam * N * 4 + lane * NJ * 16);
+    const int swz = (lane >> 2) & 1;
+    const int fpi = tl + 8 * (g & 3);
+    // softmax state of head (kvh, r = g & 3) over this lane's tokens (replicated over tl lanes)
+    float m_run = -INFINITY, l_part = 0.f, zc_part = 0.f;
+    float acc[2][8][4];  // P.V accumulators [kvh][code position][fragment]
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[h][e][c] = 0.f;
+
+    auto compute_tile = [&](int it, int slot) {
+        const int64_t t0 = t_begin + static_cast<int64_t>(it) * TT;
+        const int nv = static_cast<int>(lmin64(TT, t_end - t0));
+        const unsigned char* st = smem + lay.stages + slot * lay.stage_bytes;
+        const uint32_t* vc = reinterpret_cast<const uint32_t*>(st + lay.vc);
+        const uint32_t* vm = reinterpret_cast<const uint32_t*>(st + lay.vm);
+        const float4* rope4 = reinterpret_cast<const float4*>(st + lay.rope);
+        const unsigned char* bufp = smem + lay.knat;
+        float pv[8][REP];
+#pragma unroll
+        for (int pq = 0; pq < 4; ++pq) {
+            const int tp = 4 * pw + pq;  // token pair in the tile
+            uint32_t bf[2][NJ][2];
+            const unsigned char* lb = bufp + static_cast<size_t>(tp) * pair_bytes + lane_off;
+#pragma unroll
+            for (int jc = 0; jc < NJ; ++jc) {
+                const uint4 u = lds128(lb + ((jc ^ swz) << 4));
+                bf[0][jc][0] = prmt(u.x, u.y, 0x5410u);
+                bf[0][jc][1] = prmt(u.z, u.w, 0x5410u);
+                bf[1][jc][0] = prmt(u.x, u.y, 0x7632u);
+                bf[1][jc][1] = prmt(u.z, u.w, 0x7632u);
+            }
+#pragma unroll
+            for (int tk = 0; tk < 2; ++tk) {
+                float yf[NJ][4];
+                const float zero[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int jc = 0; jc < NJ; ++jc) mma16816(yf[jc], AH, bf[tk][jc][0], bf[tk][jc][1], zero);
+                float2 part[REP];
+#pragma unroll
+                for (int r = 0; r < REP; ++r) part[r] = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int f1 = 0; f1 < 2; ++f1) {
+                    const uint32_t h0 = pack_h2(yf[0][2 * f1], yf[0][2 * f1 + 1]);
+                    const uint32_t h1 = pack_h2(yf[1][2 * f1], yf[1][2 * f1 + 1]);
+                    const uint32_t l0 = pack_h2(sub_lo(yf[0][2 * f1], h0), sub_hi(yf[0][2 * f1 + 1], h0));
+                    const uint32_t l1 = pack_h2(sub_lo(yf[1][2 * f1], h1), sub_hi(yf[1][2 * f1 + 1], h1));
+                    float t4[4], z[4];
+                    mma16816(t4, AH, h0, h1, zero);
+                    mma16816(z, AH, l0, l1, t4);
+                    // z: (c0, c1) channels f, f+1 (bit 6 = 0), (c2, c3) channels f+64, f+65
+                    const float4 r4 = rope4[(2 * tp + tk) * 32 + fpi + 4 * f1];  // (cos f, cos f+1, sin f, sin f+1)
+                    const float2 cs2 = make_float2(r4.x, r4.y), sn2 = make_float2(r4.z, r4.w);
+                    const float2 a2 = make_float2(z[0], z[1]), b2 = make_float2(z[2], z[3]);
+                    const float2 kra = fma2(cs2, a2, mul2(make_float2(-sn2.x, -sn2.y), b2));
+                    const float2 krb = fma2(sn2, a2, mul2(cs2, b2));
+#pragma unroll
+                    for (int r = 0; r < REP; ++r) {
+                        part[r] = fma2(QA[f1][r], kra, part[r]);
+                        part[r] = fma2(QB[f1][r], krb, part[r]);
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < REP; ++r) pv[2 * pq + tk][r] = part[r].x + part[r].y;
+            }
+        }
+        // reduce-scatter over the 16 lanes of the KV head: lane keeps tokens (2tl, 2tl+1), head r = g & 3
+        // (partner lanes of steps 1-2 differ in g & 3, so slot s+2 / 1 of one is slot s / 0 of the other)
+        float a[8][2], bq[8], cq[4], d[2];
+#pragma unroll
+        for (int tk = 0; tk < 8; ++tk)
+#pragma unroll
+            for (int r0 = 0; r0 < 2; ++r0) a[tk][r0] = pv[tk][r0] + __shfl_xor_sync(0xffffffffu, pv[tk][2 + r0], 8);
+#pragma unroll
+        for (int tk = 0; tk < 8; ++tk) bq[tk] = a[tk][0] + __shfl_xor_sync(0xffffffffu, a[tk][1], 4);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float keep = bit1 ? bq[j + 4] : bq[j], send = bit1 ? bq[j] : bq[j + 4];
+            cq[j] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const float keep = bit0 ? cq[u + 2] : cq[u], send = bit0 ? cq[u] : cq[u + 2];
+            d[u] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+        }
+        // online softmax (log2 domain) for head (kvh, g & 3) over the warp's 8 tokens
+        const int64_t tw = t0 + 8 * pw;  // multiple of 8
+        const int nvw = nv - 8 * pw;
+        const uint32_t okm = ~(mask_s[(tw >> 5) - mw0] >> (tw & 31)) & (nvw >= 8 ? 0xffu : nvw > 0 ? (1u << nvw) - 1u : 0u);
+        const bool ok0 = (okm >> (2 * tl)) & 1u, ok1 = (okm >> (2 * tl + 1)) & 1u;
+        float mx = fmaxf(ok0 ? d[0] : -INFINITY, ok1 ? d[1] : -INFINITY);
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        const float m_new = fmaxf(m_run, mx);
+        if (__any_sync(0xffffffffu, m_new > m_run)) {
+            const float alpha = m_new > m_run ? ex2(m_run - m_new) : 1.0f;
+            l_part *= alpha;
+            zc_part *= alpha;
+            // accumulator columns 2tl, 2tl+1 = heads ((2tl)&3, (2tl+1)&3) of both KV heads
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const int r = (2 * tl + c) & 3;
+                    const float al = __shfl_sync(0xffffffffu, alpha, ((h * 4 + r) << 2));
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        acc[h][e][c] *= al;
+                        acc[h][e][c + 2] *= al;
+                    }
+                }
+        }
+        m_run = m_new;
+        const float p0 = ok0 ? ex2(d[0] - m_run) : 0.f, p1 = ok1 ? ex2(d[1] - m_run) : 0.f;
+        l_part += p0 + p1;
+        // weights p * s (V scale of the KV head), zero point folded into zc
+        const int tt = 8 * pw + 2 * tl;  // token of d[0] within the tile
+        const uint32_t vm0 = p0 > 0.f ? vm[tt * MG + gam * G + kvh] : 0u;
+        const uint32_t vm1 = p1 > 0.f ? vm[(tt + 1) * MG + gam * G + kvh] : 0u;
+        const float ps0 = p0 * h2f(static_cast<uint16_t>(vm0 & 0xffffu)), ps1 = p1 * h2f(static_cast<uint16_t>(vm1 & 0xffffu));
+        zc_part += ps0 * h2f(static_cast<uint16_t>(vm0 >> 16)) + ps1 * h2f(static_cast<uint16_t>(vm1 >> 16));
+        const uint32_t whi = pack_h2(ps0, ps1);
+        const uint32_t wlo = pack_h2(sub_lo(ps0, whi), sub_hi(ps1, whi));
+        const uint32_t recv = __shfl_xor_sync(0xffffffffu, kvh ? whi : wlo, 16);
+        const uint32_t bv[2] = {kvh ? recv : whi, kvh ? wlo : recv};  // B columns (r = g&3, hi | lo) per KV head
+        // P.V: per KV head and code position, m16n8k8 over the warp's 8 tokens
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int word = gam * (N / 16) + h * 8 + g;
+            const int ta = 8 * pw + 2 * tl;
+            const uint32_t w0 = vc[ta * W + word], w1 = vc[(ta + 1) * W + word];
+            const uint32_t xl = prmt(w0, w1, 0x5410u), xh = prmt(w0, w1, 0x7632u);
+            const uint32_t xls = xl >> 10, xhs = xh >> 10;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const int sh = e < 5 ? e : e - 5;
+                const uint32_t m = 0x00030003u << (2 * sh);
+                mma1688(acc[h][e], (e < 5 ? xl : xls) & m, (e < 5 ? xh : xhs) & m, bv[h]);
+            }
+        }
+    };
+
+    __syncthreads();  // mask words and plan
+    int slot = 0;
+    uint32_t phase = 0;
+    for (int it = 0; it < ntiles; ++it) {
+        mbar_wait(mbar + slot, phase);
+        scatter_tile(slot);
+        __syncthreads();
+        compute_tile(it, slot);
+        __syncthreads();
+        if (tid == 0 && it + kGqaNS < ntiles) issue_tile(it + kGqaNS);
+        if (++slot == kGqaNS) {
+            slot = 0;
+            phase ^= 1u;
+        }
+    }
+
+    // ---- partials: lane (g, tl) holds columns 2tl, 2tl+1 (heads r = (2tl)&3 + c, hi for tl < 2,
+    // lo for tl >= 2) of channels g*16 + e and g*16 + e + 8, for both KV heads
+    float lsum = l_part, zsum = zc_part;
+    lsum += __shfl_xor_sync(0xffffffffu, lsum, 1);
+    lsum += __shfl_xor_sync(0xffffffffu, lsum, 2);
+    zsum += __shfl_xor_sync(0xffffffffu, zsum, 1);
+    zsum += __shfl_xor_sync(0xffffffffu, zsum, 2);
+    const int64_t rbase = (static_cast<int64_t>(b) * p.NP + static_cast<int64_t>(split) * PW + pw) * Hq;
+    if (tl == 0) {
+        const int hq = (gam * G + kvh) * REP + (g & 3);
+        p.ws_ml[(rbase + hq) * 2] = m_run;
+        p.ws_ml[(rbase + hq) * 2 + 1] = lsum;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const int r = (2 * tl + c) & 3;
+            const float z = __shfl_sync(0xffffffffu, zsum, ((h * 4 + r) << 2));
+            const int hq = (gam * G + h) * REP + r;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const int sh = e < 5 ? e : e - 5;
+                const float sc = __int_as_float((127 + 24 - 2 * sh) << 23);
+                const float o0 = acc[h][e][c] + __shfl_xor_sync(0xffffffffu, acc[h][e][c], 2);          // hi + lo
+                const float o1 = acc[h][e][c + 2] + __shfl_xor_sync(0xffffffffu, acc[h][e][c + 2], 2);
+                if (tl < 2) {
+                    float* orow = p.ws_o + (rbase + hq) * 128 + g * 16;
+                    orow[e] = o0 * sc - z;
+                    orow[e + 8] = o1 * sc - z;
+                }
+            }
+        }
+}
+
 }  // namespace
 
-bool decode_mma_supported(int N, int REP, int C) { return N == 512 && REP == 1 && C / N * 32 <= kMmaMaxThreads; }
+bool decode_mma_supported(int N, int REP, int C) {
+    if (N == 512) return REP == 1 && C / N * 32 <= kMmaMaxThreads;
+    if (N == 256) return REP == 4 && C / N <= 4;  // GQA kernel: 4 groups x 32 x PW threads
+    return false;
+}
+
+namespace {
+int gqa_pw() {
+    int pw = 2;
+    if (const char* e = std::getenv("RKV_GQA_PW")) pw = std::max(2, std::min(4, std::atoi(e)));
+    return pw;
+}
+template <int PW>
+void* gqa_kernel_ptr() { return reinterpret_cast<void*>(decode_gqa_kernel<4, PW>); }
+void* gqa_kernel(int pw) {
+    switch (pw) {
+        case 4: return gqa_kernel_ptr<4>();
+        case 3: return gqa_kernel_ptr<3>();
+        default: return gqa_kernel_ptr<2>();
+    }
+}
+}  // namespace
 
 int decode_kind(const rkv_layer_desc& d) {
     const int N = d.heads_per_group * d.head_dim, REP = d.num_q_heads / d.num_kv_heads;
@@ -547,18 +946,22 @@ DecodePlan plan_decode_mma(const rkv_layer_desc& d, int64_t max_seq_len) {
     pl.N = d.heads_per_group * d.head_dim;
     pl.REP = d.num_q_heads / d.num_kv_heads;
     const int NG = C / pl.N;
-    const int PW = 1, PP = kPP;
-    pl.stages = kNS;
+    const bool gqa = pl.N == 256;
+    const int PW = gqa ? gqa_pw() : 1, PP = gqa ? 4 * PW : kPP;
+    pl.stages = gqa ? kGqaNS : kNS;
     pl.P = PW;
     pl.PP = PP;
     pl.TT = 2 * PP;
     pl.NT = NG * 32 * PW;
     if (max_seq_len <= 0 || max_seq_len > d.max_tokens) max_seq_len = d.max_tokens;
-    pl.smem = mma_smem(C, pl.TT, static_cast<int>(max_seq_len) + pl.TT, pl.stages).total;
+    auto smem_of = [&](int chunk) {
+        return gqa ? gqa_smem(C, pl.TT, chunk).total : mma_smem(C, pl.TT, chunk, pl.stages).total;
+    };
+    pl.smem = smem_of(static_cast<int>(max_seq_len) + pl.TT);
     pl.per_sm = std::max(1, std::min(kCtasPerSm, static_cast<int>((227u * 1024u) / (pl.smem + 1024))));
     {
         int n = 0;
-        auto kern = decode_mma_kernel<4, 1, 0>;
+        const void* kern = gqa ? gqa_kernel(PW) : reinterpret_cast<const void*>(decode_mma_kernel<4, 1, 0>);
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pl.smem)) ==
                 cudaSuccess &&
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, pl.NT, pl.smem) == cudaSuccess && n > 0)
@@ -566,22 +969,43 @@ DecodePlan plan_decode_mma(const rkv_layer_desc& d, int64_t max_seq_len) {
         else
             cudaGetLastError();
     }
-    const int ctas = num_sms() * pl.per_sm;
-    int S = ctas / d.batch;
-    if (S < 1) S = 1;
-    const int64_t max_split = (max_seq_len + 4 * pl.TT - 1) / (4 * pl.TT);
-    if (S > max_split) S = static_cast<int>(max_split > 0 ? max_split : 1);
+    // splits per sequence: fill every resident CTA slot, and prefer a split count
+    // whose CTA total is close to a whole number of waves (within 4x the minimum)
+    const int slots = num_sms() * pl.per_sm;
+    const int64_t max_split = std::max<int64_t>(1, (max_seq_len + 4 * pl.TT - 1) / (4 * pl.TT));
+    const int S0 = static_cast<int>(std::min<int64_t>(max_split, std::max(1, slots / d.batch)));
+    int S = S0;
+    double best = 0.0;
+    for (int cand = S0; cand <= std::min<int64_t>(max_split, 4 * S0 + 4); ++cand) {
+        const int64_t n = static_cast<int64_t>(cand) * d.batch;
+        const double eff = static_cast<double>(n) / (static_cast<double>((n + slots - 1) / slots) * slots);
+        if (eff > best + 0.02) {
+            best = eff;
+            S = cand;
+        }
+        if (best >= 0.95) break;
+    }
     int64_t chunk = (max_seq_len + S - 1) / S;
     chunk = (chunk + pl.TT - 1) / pl.TT * pl.TT;
     pl.chunk = static_cast<int>(chunk);
     pl.S = static_cast<int>((max_seq_len + chunk - 1) / chunk);
     pl.NP = pl.S * PW;
-    pl.smem = mma_smem(C, pl.TT, pl.chunk, pl.stages).total;
-    pl.ok = pl.NT <= kMmaMaxThreads && pl.smem <= 227 * 1024 && pl.NT % (C / 16) == 0;
+    pl.smem = smem_of(pl.chunk);
+    pl.ok = pl.smem <= 227 * 1024 && (gqa ? pl.NT <= 512 : pl.NT <= kMmaMaxThreads && pl.NT % (C / 16) == 0);
     return pl;
 }
 
 cudaError_t launch_decode_mma(const rkv_layer_desc& d, const DecodePlan& plan, const DecodeParams& p, cudaStream_t s) {
+    if (plan.N == 256) {
+        const void* kern = gqa_kernel(plan.P);
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(plan.smem));
+        if (e != cudaSuccess) return e;
+        DecodeParams pp = p;
+        void* args[] = {&pp};
+        e = cudaLaunchKernel(kern, dim3(plan.S, d.batch), dim3(plan.NT), args, plan.smem, s);
+        if (e != cudaSuccess) return e;
+        return launch_decode_combine(p, d.batch, s);
+    }
     const int NG = p.C / 512;
     auto kern = NG == 10 ? decode_mma_kernel<4, 1, 10> : NG == 8 ? decode_mma_kernel<4, 1, 8> : decode_mma_kernel<4, 1, 0>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(plan.smem));
