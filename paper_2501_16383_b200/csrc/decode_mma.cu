@@ -732,7 +732,7 @@ __global__ void __launch_bounds__(32 * 4 * PW, 1) decode_gqa_kernel(DecodeParams
         const uint32_t* vm = reinterpret_cast<const uint32_t*>(st + lay.vm);
         const float4* rope4 = reinterpret_cast<const float4*>(st + lay.rope);
         const unsigned char* bufp = smem + lay.knat;
-        float pv[8][REP];
+        float bq[8];  // per token: the partial logit after the first two reduce-scatter steps
 #pragma unroll
         for (int pq = 0; pq < 4; ++pq) {
             const int tp = 4 * pw + pq;  // token pair in the tile
@@ -776,19 +776,19 @@ __global__ void __launch_bounds__(32 * 4 * PW, 1) decode_gqa_kernel(DecodeParams
                         part[r] = fma2(QB[f1][r], krb, part[r]);
                     }
                 }
+                // reduce-scatter steps 1-2 over lanes ^8 and ^4 (partners differ in g & 3,
+                // so slot s+2 / 1 of one lane is slot s / 0 of the other; see QA)
+                float pv[REP];
 #pragma unroll
-                for (int r = 0; r < REP; ++r) pv[2 * pq + tk][r] = part[r].x + part[r].y;
+                for (int r = 0; r < REP; ++r) pv[r] = part[r].x + part[r].y;
+                const float a0 = pv[0] + __shfl_xor_sync(0xffffffffu, pv[2], 8);
+                const float a1 = pv[1] + __shfl_xor_sync(0xffffffffu, pv[3], 8);
+                bq[2 * pq + tk] = a0 + __shfl_xor_sync(0xffffffffu, a1, 4);
             }
         }
-        // reduce-scatter over the 16 lanes of the KV head: lane keeps tokens (2tl, 2tl+1), head r = g & 3
-        // (partner lanes of steps 1-2 differ in g & 3, so slot s+2 / 1 of one is slot s / 0 of the other)
-        float a[8][2], bq[8], cq[4], d[2];
-#pragma unroll
-        for (int tk = 0; tk < 8; ++tk)
-#pragma unroll
-            for (int r0 = 0; r0 < 2; ++r0) a[tk][r0] = pv[tk][r0] + __shfl_xor_sync(0xffffffffu, pv[tk][2 + r0], 8);
-#pragma unroll
-        for (int tk = 0; tk < 8; ++tk) bq[tk] = a[tk][0] + __shfl_xor_sync(0xffffffffu, a[tk][1], 4);
+        // reduce-scatter steps 3-4 over the 16 lanes of the KV head: lane keeps tokens
+        // (2tl, 2tl+1) of head r = g & 3
+        float cq[4], d[2];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const float keep = bit1 ? bq[j + 4] : bq[j], send = bit1 ? bq[j] : bq[j + 4];
