@@ -164,6 +164,15 @@ __device__ __forceinline__ void hadamard16_frag(uint32_t (&a)[4], int lane) {
 #pragma unroll
     for (int r = 0; r < 4; ++r) a[r] = h(rows[r], cols[r]) | (h(rows[r], cols[r] + 1) << 16);
 }
+// a[2] == a[0] and a[3] == a[1] on every lane (H_16 rows never see column bit
+// 3 for g < 8).  XOR-ing an opaque zero keeps the four registers distinct;
+// otherwise the compiler shares them and rebuilds the aligned register quad
+// the mma.sync A operand needs (4 MOVs) in front of every MMA.
+__device__ __forceinline__ void hadamard16_frag(uint32_t (&a)[4], int lane, uint32_t opaque_zero) {
+    hadamard16_frag(a, lane);
+    a[2] ^= opaque_zero;
+    a[3] ^= opaque_zero;
+}
 
 // D = A(16x16, fp16) * B(16x8, fp16), fp16 accumulate from zero: the result
 // (pairs along n) is already a B fragment of the next MMA.  Measured on B200
@@ -307,7 +316,7 @@ __global__ void __launch_bounds__(320, kCtasPerSm) decode_mma_kernel(DecodeParam
     // ---- compute role constants
     const int g = lane >> 2, tl = lane & 3;
     uint32_t AH[4];
-    hadamard16_frag(AH, lane);
+    hadamard16_frag(AH, lane, static_cast<uint32_t>(p.max_tokens >> 40));  // max_tokens <= 2^30
     // q: RoPE at T-1, x log2(e)/sqrt(d) x 1/sqrt(N).  Frequency pair (f, f+1),
     // f = 2tl + 8 f1 + 16 (g&3); head hq = 4 gam + (g>>2) + 2 rh.
     float2 P2[2][2], Q2[2][2];
@@ -680,7 +689,7 @@ __global__ void __launch_bounds__(32 * 4 * PW, 1) decode_gqa_kernel(DecodeParams
     const int g = lane >> 2, tl = lane & 3, kvh = lane >> 4;
     const int bit0 = lane & 1, bit1 = (lane >> 1) & 1, bit2 = (lane >> 2) & 1, bit3 = (lane >> 3) & 1;
     uint32_t AH[4];
-    hadamard16_frag(AH, lane);
+    hadamard16_frag(AH, lane, static_cast<uint32_t>(p.max_tokens >> 40));  // max_tokens <= 2^30
     // RoPE(T-1) q of the frequency pairs (f, f+1), (f+64, f+65).  Slot sl holds
     // head r = sl ^ (g & 3): the first two reduce-scatter steps then keep / send
     // fixed slots on every lane (no selects) and leave head g & 3 in slot 0.
