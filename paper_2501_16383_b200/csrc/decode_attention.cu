@@ -49,7 +49,6 @@ constexpr int kMaxStages = 4;
 __device__ __forceinline__ int64_t lmin(int64_t a, int64_t b) { return a < b ? a : b; }
 
 __device__ __forceinline__ float2 lds64(const unsigned char* p) { return *reinterpret_cast<const float2*>(p); }
-__device__ __forceinline__ float4 lds128f(const unsigned char* p) { return *reinterpret_cast<const float4*>(p); }
 // RoPE table rows are per position pair, 128 float4 (2 KB): [0, 64) section 1
 // (cos p0, cos p1, sin p0, sin p1) per frequency; [64, 128) section 2 (one
 // 32-float4 frequency-pair row per position, tensor-core decode).
@@ -438,71 +437,115 @@ __global__ void __launch_bounds__(max_threads<N>(), 1) decode_split_kernel(Decod
     }
 }
 
-// Merge the NP packed partials of (b, h) (rotated V frame) in a fixed order,
-// add the sink tokens' raw fp16 rows (natural frame, RoPE at their own
-// position, kept exact like the reference's sidecar), then
-// out = (H_128 o'_rot + o_sink) / l.  One CTA per (h, b), thread = channel d.
+// Merge the NP partials of (b, h) (rotated V frame) in a fixed order (online,
+// deterministic), add the sink tokens' raw fp16 rows (natural frame, RoPE at
+// their own position, kept exact like the reference's sidecar), then
+// out = (H_128 o'_rot / sqrt(128) + o_sink) / l.  One warp per (b, h); lane
+// owns channels 4*lane .. 4*lane+3, so H_128 is 2 register stages + 5 shuffle
+// stages and the sink dot products are warp reductions.
 __global__ void __launch_bounds__(128) decode_combine_kernel(DecodeParams p) {
-    const int h = blockIdx.x, b = blockIdx.y, d = threadIdx.x, Hq = p.Hq, C = p.C;
-    const int64_t base = static_cast<int64_t>(b) * p.NP * Hq;
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = static_cast<int64_t>(blockIdx.x) * 4 + (threadIdx.x >> 5);
+    if (wid >= static_cast<int64_t>(p.B) * p.Hq) return;
+    const int b = static_cast<int>(wid / p.Hq), h = static_cast<int>(wid % p.Hq), C = p.C;
+    const int64_t base = static_cast<int64_t>(b) * p.NP * p.Hq;
     const int64_t T = p.seq_len[b];
-    __shared__ float buf[128];
-    __shared__ float red[4];
-    __shared__ float slog[16];
-    const int nsink = min(min(p.cache.sink_count[b], p.max_sinks), 16);
-    const int f = d & 63;
     const int kvh = h / (p.Hq / p.Hkv);
-    float qd;
+    // merge the packed partials: lanes fetch (m, l) of 32 partials at a time,
+    // the warp max fixes the weights, then the o' rows are summed with loads
+    // that do not depend on each other (unrolled), in a fixed order
+    float M = -INFINITY, L = 0.f;
+    float4 rot = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s0 = 0; s0 < p.NP; s0 += 32) {
+        const int s = s0 + lane;
+        const int64_t r = base + static_cast<int64_t>(s) * p.Hq + h;
+        const float ms = s < p.NP ? p.ws_ml[r * 2] : -INFINITY;
+        const float ls = s < p.NP ? p.ws_ml[r * 2 + 1] : 0.f;
+        float mx = ms;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (mx == -INFINITY) continue;
+        const float mn = fmaxf(M, mx);
+        const float a = exp2f(M - mn);
+        const float w = ms == -INFINITY ? 0.f : exp2f(ms - mn);
+        float lw = w * ls;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) lw += __shfl_xor_sync(0xffffffffu, lw, o);
+        L = L * a + lw;
+        rot = make_float4(rot.x * a, rot.y * a, rot.z * a, rot.w * a);
+        M = mn;
+        const int n = min(32, p.NP - s0);
+        const float4* src = reinterpret_cast<const float4*>(p.ws_o + (base + static_cast<int64_t>(s0) * p.Hq + h) * 128) + lane;
+        const int64_t stride = static_cast<int64_t>(p.Hq) * 32;  // float4 per partial row step
+#pragma unroll 4
+        for (int k = 0; k < n; ++k) {
+            const float wk = __shfl_sync(0xffffffffu, w, k);
+            const float4 o = src[k * stride];
+            rot = make_float4(rot.x + wk * o.x, rot.y + wk * o.y, rot.z + wk * o.z, rot.w + wk * o.w);
+        }
+    }
+    // sinks: logits from q and the raw fp16 key rows, both RoPE'd (log2 domain)
+    const int nsink = min(min(p.cache.sink_count[b], p.max_sinks), 16);
+    float4 raw = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (nsink > 0) {
+        float qd[4];
+        const uint16_t* qh = p.q + (static_cast<int64_t>(b) * p.Hq + h) * 128;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int d = 4 * lane + j, f = d & 63;
+            const float a = h2f(qh[f]), bb = h2f(qh[f + 64]);
+            const float2 r = rope_at(p.rope, T - 1, f);
+            qd[j] = (d < 64 ? (a * r.x - bb * r.y) : (a * r.y + bb * r.x)) * p.qscale;
+        }
+        for (int s = 0; s < nsink; ++s) {
+            const int pos = p.cache.sink_pos[b * p.max_sinks + s];
+            if (pos >= T) continue;
+            const int64_t srow = (static_cast<int64_t>(b) * p.max_sinks + s) * C + kvh * 128;
+            float prod = 0.f;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int d = 4 * lane + j, f = d & 63;
+                const float ka = h2f(p.cache.sink_k[srow + f]), kb = h2f(p.cache.sink_k[srow + f + 64]);
+                const float2 rk = rope_at(p.rope, pos, f);
+                prod += qd[j] * (d < 64 ? (ka * rk.x - kb * rk.y) : (ka * rk.y + kb * rk.x));
+            }
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) prod += __shfl_xor_sync(0xffffffffu, prod, o);
+            const float mn = fmaxf(M, prod);
+            const float a = exp2f(M - mn), e = exp2f(prod - mn);
+            L = L * a + e;
+            rot = make_float4(rot.x * a, rot.y * a, rot.z * a, rot.w * a);
+            const uint2 vv = *reinterpret_cast<const uint2*>(p.cache.sink_v + srow + 4 * lane);
+            raw = make_float4(raw.x * a + e * h2f(static_cast<uint16_t>(vv.x & 0xffffu)),
+                              raw.y * a + e * h2f(static_cast<uint16_t>(vv.x >> 16)),
+                              raw.z * a + e * h2f(static_cast<uint16_t>(vv.y & 0xffffu)),
+                              raw.w * a + e * h2f(static_cast<uint16_t>(vv.y >> 16)));
+            M = mn;
+        }
+    }
+    // H_128 on the rotated-frame accumulator (value_rotation inverse): index
+    // bits 0-1 in registers, bits 2-6 across lanes (xor 1..16)
+    float x[4] = {rot.x, rot.y, rot.z, rot.w};
     {
-        const uint16_t* qh = p.q + (static_cast<int64_t>(b) * Hq + h) * 128;
-        const float a = h2f(qh[f]), bb = h2f(qh[f + 64]);
-        const float2 r = rope_at(p.rope, T - 1, f);
-        qd = (d < 64 ? (a * r.x - bb * r.y) : (a * r.y + bb * r.x)) * p.qscale;
+        const float a0 = x[0] + x[1], a1 = x[0] - x[1], a2 = x[2] + x[3], a3 = x[2] - x[3];
+        x[0] = a0 + a2;
+        x[1] = a1 + a3;
+        x[2] = a0 - a2;
+        x[3] = a1 - a3;
     }
-    for (int s = 0; s < nsink; ++s) {  // sink logits (log2 domain)
-        const int pos = p.cache.sink_pos[b * p.max_sinks + s];
-        const uint16_t* kr = p.cache.sink_k + (static_cast<int64_t>(b) * p.max_sinks + s) * C + kvh * 128;
-        const float ka = h2f(kr[f]), kb = h2f(kr[f + 64]);
-        const float2 rk = rope_at(p.rope, pos, f);
-        float prod = qd * (d < 64 ? (ka * rk.x - kb * rk.y) : (ka * rk.y + kb * rk.x));
 #pragma unroll
-        for (int o = 16; o >= 1; o >>= 1) prod += __shfl_xor_sync(0xffffffffu, prod, o);
-        if ((d & 31) == 0) red[d >> 5] = prod;
-        __syncthreads();
-        if (d == 0) slog[s] = (pos < T) ? (red[0] + red[1] + red[2] + red[3]) : -INFINITY;
-        __syncthreads();
-    }
-    float M = -INFINITY;
-    for (int s = 0; s < p.NP; ++s) M = fmaxf(M, p.ws_ml[(base + static_cast<int64_t>(s) * Hq + h) * 2]);
-    for (int s = 0; s < nsink; ++s) M = fmaxf(M, slog[s]);
-    float Lsum = 0.f, rot = 0.f, raw = 0.f;
-    for (int s = 0; s < p.NP; ++s) {
-        const int64_t r = base + static_cast<int64_t>(s) * Hq + h;
-        const float ms = p.ws_ml[r * 2];
-        if (ms == -INFINITY) continue;
-        const float e = exp2f(ms - M);
-        Lsum += e * p.ws_ml[r * 2 + 1];
-        rot += e * p.ws_o[r * 128 + d];
-    }
-    for (int s = 0; s < nsink; ++s) {
-        if (slog[s] == -INFINITY) continue;
-        const float e = exp2f(slog[s] - M);
-        Lsum += e;
-        raw += e * h2f(p.cache.sink_v[(static_cast<int64_t>(b) * p.max_sinks + s) * C + kvh * 128 + d]);
-    }
-    // H_128 on the rotated-frame accumulator (value_rotation inverse)
-    buf[d] = rot;
-    __syncthreads();
+    for (int o = 1; o < 32; o <<= 1) {
+        const bool upper = lane & o;
 #pragma unroll
-    for (int half = 1; half < 128; half <<= 1) {
-        const float a = buf[d & ~half], bb = buf[d | half];
-        const float y = (d & half) ? a - bb : a + bb;
-        __syncthreads();
-        buf[d] = y;
-        __syncthreads();
+        for (int j = 0; j < 4; ++j) {
+            const float y = __shfl_xor_sync(0xffffffffu, x[j], o);
+            x[j] = upper ? y - x[j] : x[j] + y;
+        }
     }
-    const float hv = buf[d] * (1.0f / sqrtf(128.0f));
-    p.out[(static_cast<int64_t>(b) * Hq + h) * 128 + d] = (hv + raw) / Lsum;
+    const float inv = 1.0f / L, nrm = 1.0f / sqrtf(128.0f);
+    reinterpret_cast<float4*>(p.out + (static_cast<int64_t>(b) * p.Hq + h) * 128)[lane] =
+        make_float4((x[0] * nrm + raw.x) * inv, (x[1] * nrm + raw.y) * inv, (x[2] * nrm + raw.z) * inv,
+                    (x[3] * nrm + raw.w) * inv);
 }
 
 // table[pos/2][f] = (cos(p0 th_f), cos(p1 th_f), sin(p0 th_f), sin(p1 th_f)),
@@ -575,7 +618,8 @@ cudaError_t launch_decode_nr(const DecodePlan& plan, const DecodeParams& p, int 
 }  // namespace
 
 cudaError_t launch_decode_combine(const DecodeParams& p, int B, cudaStream_t s) {
-    decode_combine_kernel<<<dim3(p.Hq, B), 128, 0, s>>>(p);
+    const int64_t warps = static_cast<int64_t>(B) * p.Hq;
+    decode_combine_kernel<<<static_cast<unsigned>((warps + 3) / 4), 128, 0, s>>>(p);
     return cudaGetLastError();
 }
 

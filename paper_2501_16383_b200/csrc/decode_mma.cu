@@ -174,16 +174,6 @@ __device__ __forceinline__ void hadamard16_frag(uint32_t (&a)[4], int lane, uint
     a[3] ^= opaque_zero;
 }
 
-// D = A(16x16, fp16) * B(16x8, fp16), fp16 accumulate from zero: the result
-// (pairs along n) is already a B fragment of the next MMA.  Measured on B200
-// (tools/microbench4.cu): equal to the round-to-nearest fp16 of the exact
-// H_16 . X for all but 3e-5 of outputs (ties), never off by more than half an ulp.
-__device__ __forceinline__ void mma16816_h(uint32_t (&d)[2], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-    asm("mma.sync.aligned.m16n8k16.row.col.f16.f16.f16.f16 {%0,%1}, {%2,%3,%4,%5}, {%6,%7}, {%8,%8};"
-        : "=r"(d[0]), "=r"(d[1])
-        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "r"(0u));
-}
-
 // Tile geometry (compile time): TT = 4 tokens = 2 token pairs per tile, one
 // warp per FWHT group, 3-deep TMA ring; ~102 KB of shared memory and <= 96
 // registers so that two CTAs (20 warps) share an SM and cover each other's
@@ -687,7 +677,7 @@ __global__ void __launch_bounds__(32 * 4 * PW, 1) decode_gqa_kernel(DecodeParams
 
     // ---- compute role: lane (g, tl); KV head kvh = lane >> 4 of the group
     const int g = lane >> 2, tl = lane & 3, kvh = lane >> 4;
-    const int bit0 = lane & 1, bit1 = (lane >> 1) & 1, bit2 = (lane >> 2) & 1, bit3 = (lane >> 3) & 1;
+    const int bit0 = lane & 1, bit1 = (lane >> 1) & 1;
     uint32_t AH[4];
     hadamard16_frag(AH, lane, static_cast<uint32_t>(p.max_tokens >> 40));  // max_tokens <= 2^30
     // RoPE(T-1) q of the frequency pairs (f, f+1), (f+64, f+65).  Slot sl holds
