@@ -164,6 +164,23 @@ rkv_status rkv_rotate_keys(const rkv_layer_desc* desc, const uint16_t* k, int64_
 rkv_status rkv_calibrate_reorder(const float* rotated_keys, int64_t rows, int64_t channels, int32_t stat,
                                  int32_t* perm_out, int32_t* inverse_out);
 
+/* calibrate_reorder from raw fp16 pre-RoPE keys on DEVICE memory (SURVEY
+ * 8(f) 2; proj/src/pipeline.cpp:101-109 rotate_rows -> proj/src/reorder.cpp:
+ * 91-110 calibrate_reorder):
+ *   k_rows     : [rows][C] fp16, device (pre-RoPE K of the calibration set)
+ *   stat       : RKV_STAT_SUM (reference) or RKV_STAT_MEAN_ABS (north star)
+ *   workspace  : rkv_calibrate_workspace_bytes(desc, rows) bytes of device memory
+ *   perm_out   : [C] int32, HOST (slot j <- channel perm[j]); inverse_out: [C] or NULL
+ * The rows are rotated on the device (bit-identical to rotate_rows) and each
+ * channel's statistic is accumulated in double over the rows IN ORDER, the
+ * reference's summation order, so the statistics and the stable argsort (host)
+ * are bit-identical to rkv_calibrate_reorder on the rotated rows.  Synchronizes
+ * the stream (the permutation is returned on the host). */
+size_t rkv_calibrate_workspace_bytes(const rkv_layer_desc* desc, int64_t rows);
+rkv_status rkv_calibrate_reorder_device(const rkv_layer_desc* desc, const uint16_t* k_rows, int64_t rows,
+                                        int32_t stat, void* workspace, size_t workspace_bytes, int32_t* perm_out,
+                                        int32_t* inverse_out, void* stream);
+
 /* Massive-activation sink detection (proj/src/sink.cpp:14-45) on HOST memory:
  * hidden [b][s][h] fp32 -> flags[s] (token 0 always flagged).  Returns the
  * count through *num_sinks. */

@@ -13,6 +13,7 @@ from .rotatekv import (  # noqa: F401
     RotateKVLayer,
     apply_reorder,
     calibrate_reorder,
+    calibrate_reorder_device,
     detect_massive_activations,
     detect_massive_activations_device,
     layer_plan_build,

@@ -605,6 +605,22 @@ __global__ void rotate_keys_kernel(const uint16_t* __restrict__ k, int64_t rows,
     for (int j = 0; j < R; ++j) out[r * C + u * N + lam + L * j] = __fmul_rn(x[j].x, norm);
 }
 
+// Per-channel calibration statistic (proj/src/reorder.cpp:98-105): thread c
+// accumulates sum_r x[r][c] (or |x|) in double over r = 0, 1, ... in order --
+// the reference's summation order, so the result is bit-identical.  Reads are
+// coalesced across threads (consecutive channels).
+__global__ void channel_stats_kernel(const float* __restrict__ x, int64_t rows, int64_t C, int mean_abs,
+                                     double* __restrict__ out) {
+    const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (c >= C) return;
+    double acc = 0.0;
+    for (int64_t r = 0; r < rows; ++r) {
+        const double v = x[r * C + c];
+        acc += mean_abs ? fabs(v) : v;
+    }
+    out[c] = mean_abs ? acc / static_cast<double>(rows) : acc;
+}
+
 template <int N, int REP>
 cudaError_t launch_decode_nr(const DecodePlan& plan, const DecodeParams& p, int B, cudaStream_t s) {
     auto kern = decode_split_kernel<N, REP>;
@@ -724,6 +740,13 @@ cudaError_t launch_decode(const rkv_layer_desc& d, const DecodePlan& plan, const
         case 128 * 16 + 4: return launch_decode_nr<128, 4>(plan, p, B, s);
         default: return cudaErrorInvalidValue;
     }
+}
+
+cudaError_t launch_channel_stats(const float* rows_f32, int64_t rows, int64_t C, bool mean_abs, double* stats,
+                                 cudaStream_t s) {
+    channel_stats_kernel<<<static_cast<unsigned>((C + 127) / 128), 128, 0, s>>>(rows_f32, rows, C, mean_abs ? 1 : 0,
+                                                                                stats);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_rope_table(const rkv_layer_desc& d, float4* table, int64_t max_pos, cudaStream_t s) {

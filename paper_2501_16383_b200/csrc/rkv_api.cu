@@ -89,6 +89,17 @@ rkv_status validate(const rkv_layer_desc* d) {
     return RKV_OK;
 }
 
+// stable ascending argsort of the per-channel statistic (proj/src/reorder.cpp:105-109)
+void sort_channels(const std::vector<double>& key, int32_t* perm_out, int32_t* inverse_out) {
+    std::vector<int32_t> order(key.size());
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int32_t a, int32_t b) { return key[static_cast<size_t>(a)] < key[static_cast<size_t>(b)]; });
+    std::memcpy(perm_out, order.data(), order.size() * sizeof(int32_t));
+    if (inverse_out)
+        for (size_t j = 0; j < order.size(); ++j) inverse_out[order[j]] = static_cast<int32_t>(j);
+}
+
 rkv_status check_cache(const rkv_cache* c) {
     if (!c || !c->k_codes || !c->v_codes || !c->k_meta || !c->v_meta || !c->sink_count || !c->sink_mask)
         return fail(RKV_ERR_INVALID_ARGUMENT, "cache arrays must be non-null");
@@ -320,13 +331,39 @@ rkv_status rkv_calibrate_reorder(const float* rotated_keys, int64_t rows, int64_
     }
     if (stat == RKV_STAT_MEAN_ABS)
         for (double& k : key) k /= static_cast<double>(rows);
-    std::vector<int32_t> order(static_cast<size_t>(channels));
-    std::iota(order.begin(), order.end(), 0);
-    std::stable_sort(order.begin(), order.end(),
-                     [&](int32_t a, int32_t b) { return key[static_cast<size_t>(a)] < key[static_cast<size_t>(b)]; });
-    std::memcpy(perm_out, order.data(), order.size() * sizeof(int32_t));
-    if (inverse_out)
-        for (int64_t j = 0; j < channels; ++j) inverse_out[order[static_cast<size_t>(j)]] = static_cast<int32_t>(j);
+    sort_channels(key, perm_out, inverse_out);
+    return RKV_OK;
+}
+
+size_t rkv_calibrate_workspace_bytes(const rkv_layer_desc* desc, int64_t rows) {
+    if (validate(desc) != RKV_OK || rows < 1) return 0;
+    const size_t C = static_cast<size_t>(desc->num_kv_heads) * desc->head_dim;
+    return al256(static_cast<size_t>(rows) * C * sizeof(float)) + al256(C * sizeof(double));
+}
+
+rkv_status rkv_calibrate_reorder_device(const rkv_layer_desc* desc, const uint16_t* k_rows, int64_t rows,
+                                        int32_t stat, void* workspace, size_t workspace_bytes, int32_t* perm_out,
+                                        int32_t* inverse_out, void* stream) {
+    rkv_status st = validate(desc);
+    if (st != RKV_OK) return st;
+    if (rows < 1) return fail(RKV_ERR_INVALID_ARGUMENT, "calibrate_reorder: empty calibration set");
+    if (!k_rows || !workspace || !perm_out) return fail(RKV_ERR_INVALID_ARGUMENT, "calibrate_reorder: null argument");
+    if (stat != RKV_STAT_SUM && stat != RKV_STAT_MEAN_ABS)
+        return fail(RKV_ERR_INVALID_ARGUMENT, "calibrate_reorder: unknown statistic");
+    if (workspace_bytes < rkv_calibrate_workspace_bytes(desc, rows))
+        return fail(RKV_ERR_INVALID_ARGUMENT, "calibrate_reorder: workspace too small");
+    const int64_t C = static_cast<int64_t>(desc->num_kv_heads) * desc->head_dim;
+    float* rotated = static_cast<float*>(workspace);
+    double* stats = reinterpret_cast<double*>(static_cast<char*>(workspace) +
+                                              al256(static_cast<size_t>(rows) * C * sizeof(float)));
+    cudaStream_t cs = static_cast<cudaStream_t>(stream);
+    cudaError_t e = rkv::launch_rotate_keys(*desc, k_rows, rows, rotated, cs);
+    if (e == cudaSuccess) e = rkv::launch_channel_stats(rotated, rows, C, stat == RKV_STAT_MEAN_ABS, stats, cs);
+    std::vector<double> key(static_cast<size_t>(C));
+    if (e == cudaSuccess) e = cudaMemcpyAsync(key.data(), stats, key.size() * sizeof(double), cudaMemcpyDeviceToHost, cs);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+    if (e != cudaSuccess) return cuda_fail(e, "calibrate_reorder_device");
+    sort_channels(key, perm_out, inverse_out);
     return RKV_OK;
 }
 

@@ -74,6 +74,8 @@ cudaError_t launch_rope_table(const rkv_layer_desc& d, float4* table, int64_t ma
 cudaError_t launch_rotate_keys(const rkv_layer_desc& d, const uint16_t* k, int64_t rows, float* out,
                                cudaStream_t s);
 int num_sms();
+cudaError_t launch_channel_stats(const float* rows_f32, int64_t rows, int64_t C, bool mean_abs, double* stats,
+                                 cudaStream_t s);
 // sink_detect.cu
 size_t detect_sinks_workspace_bytes();
 cudaError_t launch_detect_sinks(const float* x, int64_t b, int64_t s, int64_t hidden, double rel, double abs_floor,

@@ -95,9 +95,13 @@ def lib():
         L.rkv_detect_sinks_workspace_bytes.argtypes = []
         L.rkv_detect_sinks_device.argtypes = [P, C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_double, P, P, P,
                                               C.c_size_t, P]
+        L.rkv_calibrate_workspace_bytes.restype = C.c_size_t
+        L.rkv_calibrate_workspace_bytes.argtypes = [D, C.c_int64]
+        L.rkv_calibrate_reorder_device.argtypes = [D, P, C.c_int64, C.c_int32, P, C.c_size_t, P, P, P]
         for name in ("rkv_layer_validate", "rkv_cache_carve", "rkv_cache_reset", "rkv_rope_table_init",
                      "rkv_quantize_kv", "rkv_decode_attention", "rkv_rotate_keys", "rkv_calibrate_reorder",
-                     "rkv_detect_sinks", "rkv_detect_sinks_device", "rkv_layer_plan_build", "rkv_layer_plan_init"):
+                     "rkv_detect_sinks", "rkv_detect_sinks_device", "rkv_layer_plan_build", "rkv_layer_plan_init",
+                     "rkv_calibrate_reorder_device"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -388,6 +392,24 @@ class RotateKVLayer:
         proj/src/pipeline.cpp:207-209), then attend over the whole cache."""
         self.append(k_new, v_new)
         return self.decode(q)
+
+
+def calibrate_reorder_device(cfg: LayerConfig, k, stat: int = STAT_MEAN_ABS):
+    """calibrate_reorder from raw fp16 pre-RoPE K rows [rows, C] on the device
+    (rotation + per-channel double statistic on the GPU, argsort on the host)
+    -> (perm, inverse) int32 numpy, bit-identical to calibrate_reorder(rotate_keys(k))."""
+    torch = __import__("torch")
+    d = cfg.desc()
+    k = k.contiguous().reshape(-1, cfg.channels)
+    rows = k.shape[0]
+    nws = lib().rkv_calibrate_workspace_bytes(C.byref(d), rows)
+    ws = torch.empty(max(nws, 1), dtype=torch.uint8, device=k.device)
+    perm = np.empty(cfg.channels, np.int32)
+    inv = np.empty(cfg.channels, np.int32)
+    _check(lib().rkv_calibrate_reorder_device(C.byref(d), _ptr(k), rows, stat, _ptr(ws), nws, perm.ctypes.data,
+                                              inv.ctypes.data,
+                                              C.c_void_p(torch.cuda.current_stream(k.device).cuda_stream)))
+    return perm, inv
 
 
 def rotate_keys(cfg: LayerConfig, k):

@@ -94,12 +94,12 @@ def make_q(w: Workload, seed: int, batch: int, device="cuda", step: int = 0):
 
 
 def calibration_perm(w: Workload, seed: int, device="cuda", layer: int = 0, rows: int = 256):
-    """Permutation from mean |rotated K| over 256 seeded calibration tokens."""
-    from .rotatekv import LayerConfig, STAT_MEAN_ABS, calibrate_reorder, rotate_keys
+    """Permutation from mean |rotated K| over 256 seeded calibration tokens
+    (rotation and channel statistics on the device, rkv_calibrate_reorder_device)."""
+    from .rotatekv import LayerConfig, STAT_MEAN_ABS, calibrate_reorder_device
 
     k, _ = make_kv(w, seed + 100, 1, rows, device=device, layer=layer)
     cfg = LayerConfig(batch=1, num_q_heads=w.num_q_heads, num_kv_heads=w.num_kv_heads,
                       heads_per_group=w.heads_per_group, max_tokens=rows, rope_base=w.rope_base)
-    rk = rotate_keys(cfg, k.reshape(rows, w.channels)).cpu().numpy()
-    perm, _ = calibrate_reorder(rk, STAT_MEAN_ABS)
+    perm, _ = calibrate_reorder_device(cfg, k.reshape(rows, w.channels), STAT_MEAN_ABS)
     return perm
