@@ -181,6 +181,30 @@ rkv_status rkv_calibrate_reorder_device(const rkv_layer_desc* desc, const uint16
                                         int32_t stat, void* workspace, size_t workspace_bytes, int32_t* perm_out,
                                         int32_t* inverse_out, void* stream);
 
+/* Cache wire format: LayerKVCache::serialize /
+ * deserialize (proj/src/kv_cache.cpp:119-173, blocks proj/src/quant.cpp:
+ * 139-158): u8 bits, u64 group, u64 channels, u64 tokens (little endian), then
+ * per token a sink byte and either two fp32 rows (K then V, the fused frame:
+ * K' = reorder(rotate_G(k)), V' = rotate_1(v), what the reference's sidecar
+ * holds) or the K blocks then the V blocks, each [e4m3 scale][u8 zero][codes
+ * LSB-first].  RKV_WIRE_REFERENCE is that format byte for byte (needs
+ * scale_format == RKV_SCALE_E4M3_CEIL, or fp16 scales that are e4m3 values);
+ * RKV_WIRE_FP16_SCALE is the same layout with a 2-byte fp16 scale per block,
+ * the sink rows as the raw fp16 rows the sidecar holds (2 x C x 2 bytes) and
+ * bits | 0x80 in the header: lossless for every cache.  Importing the
+ * reference format turns the fused-frame fp32 sink rows back into the raw
+ * frame (inverse reorder + FWHT) and rounds them to fp16.
+ * Both calls move ONE sequence (index seq) between device cache and host
+ * bytes and synchronize the stream.  perm: [C] int32 host (the layer's
+ * reorder, for the sink rows' frame).  Import replaces the sequence. */
+typedef enum { RKV_WIRE_REFERENCE = 0, RKV_WIRE_FP16_SCALE = 1 } rkv_wire_format;
+size_t rkv_cache_wire_bytes(const rkv_layer_desc* desc, int64_t tokens, int64_t num_sinks, int32_t format);
+rkv_status rkv_cache_export(const rkv_layer_desc* desc, const rkv_cache* cache, int64_t seq, int64_t tokens,
+                            const int32_t* perm, int32_t format, uint8_t* out, size_t out_bytes, size_t* written,
+                            void* stream);
+rkv_status rkv_cache_import(const rkv_layer_desc* desc, const uint8_t* bytes, size_t num_bytes, const int32_t* perm,
+                            int64_t seq, const rkv_cache* cache, int64_t* tokens_out, void* stream);
+
 /* Massive-activation sink detection (proj/src/sink.cpp:14-45) on HOST memory:
  * hidden [b][s][h] fp32 -> flags[s] (token 0 always flagged).  Returns the
  * count through *num_sinks. */

@@ -104,6 +104,10 @@ def ref():
         R.ref_apply_rope_rows.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_void_p, C.c_int]
         R.ref_detect_sinks.restype = C.c_int64
         R.ref_detect_sinks.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_void_p]
+        R.ref_cache_serialize.restype = C.c_int64
+        R.ref_cache_serialize.argtypes = [C.c_void_p] * 3 + [C.c_int64] * 4 + [C.c_void_p] * 2 + [C.c_int64]
+        R.ref_cache_reserialize.restype = C.c_int64
+        R.ref_cache_reserialize.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64]
         R.ref_quantize_kv_rows.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_void_p] + [C.c_void_p] * 6
         R.ref_decode_step.argtypes = [C.c_int64] * 3 + [C.c_void_p] * 3 + [C.c_int64, C.c_void_p, C.c_double, C.c_void_p, C.c_void_p]
         R.ref_bench_create.restype = C.c_void_p
@@ -264,6 +268,33 @@ def decode_attention(k_codes, k_meta, v_codes, v_meta, is_sink, sink_k, sink_v, 
     if rc != 0:
         raise ValueError("decode_attention failed")
     return out
+
+
+def ref_cache_serialize(k_raw, v_raw, sink, perm, num_heads, head_dim, heads_per_group):
+    """The reference's LayerKVCache::serialize of raw rows appended as prefill does."""
+    k, v = f32(k_raw), f32(v_raw)
+    sink = np.ascontiguousarray(sink, np.uint8)
+    perm = np.ascontiguousarray(perm, np.int32)
+    rows = k.shape[0]
+    n = ref().ref_cache_serialize(_p(k), _p(v), _p(sink), rows, num_heads, head_dim, heads_per_group, _p(perm),
+                                  None, 0)
+    if n < 0:
+        raise ValueError("ref_cache_serialize failed")
+    out = np.empty(n, np.uint8)
+    ref().ref_cache_serialize(_p(k), _p(v), _p(sink), rows, num_heads, head_dim, heads_per_group, _p(perm),
+                              _p(out), n)
+    return out.tobytes()
+
+
+def ref_cache_reserialize(data):
+    """LayerKVCache::deserialize + serialize in the reference (None if it throws)."""
+    buf = np.frombuffer(data, np.uint8).copy()
+    n = ref().ref_cache_reserialize(_p(buf), buf.size, None, 0)
+    if n < 0:
+        return None
+    out = np.empty(n, np.uint8)
+    ref().ref_cache_reserialize(_p(buf), buf.size, _p(out), n)
+    return out.tobytes()
 
 
 def ref_decode_step(k_raw, v_raw, sink, perm, x, num_heads, head_dim, heads_per_group, rope_base):

@@ -204,6 +204,46 @@ int ref_quantize_kv_rows(const float* k_raw, const float* v_raw, int64_t rows, i
     } catch (const std::exception&) { return -1; }
 }
 
+// LayerKVCache::serialize (proj/src/kv_cache.cpp:119-139) of a cache the
+// reference fills from raw rows as prefill does: fused-frame rows (rotate +
+// reorder for K, per-head rotate for V), sinks in the fp32 sidecar.  Returns
+// the byte count (copies at most cap bytes), -1 on error.
+int64_t ref_cache_serialize(const float* k_raw, const float* v_raw, const uint8_t* sink, int64_t rows,
+                            int64_t num_heads, int64_t head_dim, int64_t hpg, const int32_t* perm, uint8_t* out,
+                            int64_t cap) {
+    try {
+        int64_t c = num_heads * head_dim;
+        RotationPlan kr = RotationPlan::make(head_dim, hpg, num_heads);
+        RotationPlan vr = RotationPlan::make(head_dim, 1, num_heads);
+        ReorderPlan plan = plan_from_perm(perm, c);
+        QuantConfig q;
+        q.bits = 2;
+        q.group_size = 128;
+        Tensor k({rows, c}, std::vector<float>(k_raw, k_raw + rows * c));
+        Tensor v({rows, c}, std::vector<float>(v_raw, v_raw + rows * c));
+        Tensor kt = apply_reorder(rotate_rows(k, kr, false), plan, 0, false);
+        Tensor vt = rotate_rows(v, vr, false);
+        LayerKVCache cache(q, c);
+        for (int64_t r = 0; r < rows; ++r)
+            cache.append(std::span<const float>(kt.data() + r * c, static_cast<size_t>(c)),
+                         std::span<const float>(vt.data() + r * c, static_cast<size_t>(c)), sink[r] != 0);
+        std::vector<uint8_t> bytes = cache.serialize();
+        std::memcpy(out, bytes.data(), std::min<size_t>(bytes.size(), static_cast<size_t>(cap)));
+        return static_cast<int64_t>(bytes.size());
+    } catch (const std::exception&) { return -1; }
+}
+
+// LayerKVCache::deserialize then serialize again (the reference accepts the
+// bytes and reproduces them); returns the byte count or -1 if it throws.
+int64_t ref_cache_reserialize(const uint8_t* in, int64_t n, uint8_t* out, int64_t cap) {
+    try {
+        LayerKVCache cache = LayerKVCache::deserialize(std::span<const uint8_t>(in, static_cast<size_t>(n)));
+        std::vector<uint8_t> bytes = cache.serialize();
+        std::memcpy(out, bytes.data(), std::min<size_t>(bytes.size(), static_cast<size_t>(cap)));
+        return static_cast<int64_t>(bytes.size());
+    } catch (const std::exception&) { return -1; }
+}
+
 // One decode step through the reference's own decode_step
 // (proj/src/pipeline.cpp:193-263) with identity projections, so the decode
 // token's raw row x is simultaneously its key, value and query.  The prefix

@@ -9,6 +9,8 @@ from .rotatekv import (  # noqa: F401
     SCALE_FP16_CEIL,
     STAT_MEAN_ABS,
     STAT_SUM,
+    WIRE_FP16_SCALE,
+    WIRE_REFERENCE,
     LayerConfig,
     RotateKVLayer,
     apply_reorder,

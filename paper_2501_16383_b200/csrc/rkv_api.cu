@@ -100,6 +100,105 @@ void sort_channels(const std::vector<double>& key, int32_t* perm_out, int32_t* i
         for (size_t j = 0; j < order.size(); ++j) inverse_out[order[j]] = static_cast<int32_t>(j);
 }
 
+
+// ---------------------------------------------------------------- wire format
+// Host helpers for rkv_cache_export / rkv_cache_import.
+
+float half_bits_to_float(uint16_t h) {
+    const uint32_t sgn = static_cast<uint32_t>(h & 0x8000u) << 16;
+    uint32_t e = (h >> 10) & 0x1fu, m = h & 0x3ffu;
+    uint32_t bits;
+    if (e == 0) {
+        if (m == 0) {
+            bits = sgn;
+        } else {  // subnormal: normalise
+            int sh = 0;
+            while (!(m & 0x400u)) {
+                m <<= 1;
+                ++sh;
+            }
+            bits = sgn | ((113u - static_cast<uint32_t>(sh)) << 23) | ((m & 0x3ffu) << 13);
+        }
+    } else if (e == 31) {
+        bits = sgn | 0x7f800000u | (m << 13);
+    } else {
+        bits = sgn | ((e + 112u) << 23) | (m << 13);
+    }
+    float f;
+    std::memcpy(&f, &bits, 4);
+    return f;
+}
+
+uint16_t float_to_half_bits(float f) {  // round to nearest even
+    uint32_t x;
+    std::memcpy(&x, &f, 4);
+    const uint32_t sgn = (x >> 16) & 0x8000u;
+    const int32_t e = static_cast<int32_t>((x >> 23) & 0xffu) - 127 + 15;
+    uint32_t m = x & 0x7fffffu;
+    if (((x >> 23) & 0xffu) == 0xffu) return static_cast<uint16_t>(sgn | 0x7c00u | (m ? 0x200u : 0u));
+    if (e >= 31) return static_cast<uint16_t>(sgn | 0x7c00u);
+    if (e <= 0) {
+        if (e < -10) return static_cast<uint16_t>(sgn);
+        m |= 0x800000u;
+        const int sh = 14 - e;
+        uint32_t hm = m >> sh;
+        const uint32_t rem = m & ((1u << sh) - 1), half = 1u << (sh - 1);
+        if (rem > half || (rem == half && (hm & 1u))) ++hm;
+        return static_cast<uint16_t>(sgn | hm);
+    }
+    uint32_t hm = m >> 13;
+    const uint32_t rem = m & 0x1fffu;
+    uint32_t he = static_cast<uint32_t>(e);
+    if (rem > 0x1000u || (rem == 0x1000u && (hm & 1u))) {
+        if (++hm == 0x400u) {
+            hm = 0;
+            ++he;
+        }
+    }
+    if (he >= 31) return static_cast<uint16_t>(sgn | 0x7c00u);
+    return static_cast<uint16_t>(sgn | (he << 10) | hm);
+}
+
+float e4m3_value(uint8_t c) {  // OCP e4m3fn, positive codes
+    const int e = (c >> 3) & 0xf, m = c & 7;
+    return e == 0 ? std::ldexp(static_cast<float>(m), -9) : std::ldexp(1.0f + m * 0.125f, e - 7);
+}
+
+bool e4m3_code_of(float v, uint8_t* code) {  // exact inverse on e4m3 values
+    for (int c = 0; c <= 0x7e; ++c)
+        if (e4m3_value(static_cast<uint8_t>(c)) == v) {
+            *code = static_cast<uint8_t>(c);
+            return true;
+        }
+    return false;
+}
+
+// In-place grouped FWHT of one row (rotate_rows, proj/src/hadamard.cpp:47-84):
+// stages half = 1, 2, ..., n/2 in fp32, then x 1/sqrtf(n).
+void fwht_row(float* x, int64_t C, int64_t n) {
+    const float norm = 1.0f / std::sqrt(static_cast<float>(n));
+    for (int64_t base = 0; base < C; base += n) {
+        float* v = x + base;
+        for (int64_t h = 1; h < n; h <<= 1)
+            for (int64_t i = 0; i < n; i += 2 * h)
+                for (int64_t j = i; j < i + h; ++j) {
+                    const float a = v[j], b = v[j + h];
+                    v[j] = a + b;
+                    v[j + h] = a - b;
+                }
+        for (int64_t j = 0; j < n; ++j) v[j] *= norm;
+    }
+}
+
+void put_u64(std::vector<uint8_t>& o, uint64_t v) {
+    for (int i = 0; i < 8; ++i) o.push_back(static_cast<uint8_t>(v >> (8 * i)));
+}
+void put_f32(std::vector<uint8_t>& o, float f) {
+    uint32_t b;
+    std::memcpy(&b, &f, 4);
+    for (int i = 0; i < 4; ++i) o.push_back(static_cast<uint8_t>(b >> (8 * i)));
+}
+
 rkv_status check_cache(const rkv_cache* c) {
     if (!c || !c->k_codes || !c->v_codes || !c->k_meta || !c->v_meta || !c->sink_count || !c->sink_mask)
         return fail(RKV_ERR_INVALID_ARGUMENT, "cache arrays must be non-null");
@@ -364,6 +463,237 @@ rkv_status rkv_calibrate_reorder_device(const rkv_layer_desc* desc, const uint16
     if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
     if (e != cudaSuccess) return cuda_fail(e, "calibrate_reorder_device");
     sort_channels(key, perm_out, inverse_out);
+    return RKV_OK;
+}
+
+size_t rkv_cache_wire_bytes(const rkv_layer_desc* desc, int64_t tokens, int64_t num_sinks, int32_t format) {
+    if (validate(desc) != RKV_OK || tokens < 0 || num_sinks < 0 || num_sinks > tokens) return 0;
+    const size_t C = static_cast<size_t>(desc->num_kv_heads) * desc->head_dim, G = C / 128;
+    const size_t block = (format == RKV_WIRE_FP16_SCALE ? 2 : 1) + 1 + 32;
+    const size_t sink_row = format == RKV_WIRE_FP16_SCALE ? 2 : 4;  // raw fp16 rows vs fused-frame fp32 rows
+    return 25 + static_cast<size_t>(tokens) + static_cast<size_t>(num_sinks) * 2 * C * sink_row +
+           static_cast<size_t>(tokens - num_sinks) * 2 * G * block;
+}
+
+rkv_status rkv_cache_export(const rkv_layer_desc* desc, const rkv_cache* cache, int64_t seq, int64_t tokens,
+                            const int32_t* perm, int32_t format, uint8_t* out, size_t out_bytes, size_t* written,
+                            void* stream) {
+    rkv_status st = validate(desc);
+    if (st != RKV_OK) return st;
+    if ((st = check_cache(cache)) != RKV_OK) return st;
+    if (!perm || !out) return fail(RKV_ERR_INVALID_ARGUMENT, "cache serialize: null argument");
+    if (format != RKV_WIRE_REFERENCE && format != RKV_WIRE_FP16_SCALE)
+        return fail(RKV_ERR_INVALID_ARGUMENT, "cache serialize: unknown wire format");
+    if (seq < 0 || seq >= desc->batch) return fail(RKV_ERR_OUT_OF_RANGE, "cache serialize: sequence index");
+    if (tokens < 0 || tokens > desc->max_tokens) return fail(RKV_ERR_OUT_OF_RANGE, "cache serialize: token count");
+    const int64_t C = static_cast<int64_t>(desc->num_kv_heads) * desc->head_dim, W = C / 16, MG = C / 128;
+    const int64_t N = static_cast<int64_t>(desc->heads_per_group) * desc->head_dim, T = desc->max_tokens;
+    const int64_t MW = (T + 31) / 32, S = desc->max_sinks;
+    cudaStream_t cs = static_cast<cudaStream_t>(stream);
+    std::vector<uint32_t> kc(static_cast<size_t>(tokens * W)), vc(kc.size()), km(static_cast<size_t>(tokens * MG)),
+        vm(km.size()), mask(static_cast<size_t>(MW));
+    std::vector<uint16_t> sk(static_cast<size_t>(S * C)), sv(sk.size());
+    std::vector<int32_t> spos(static_cast<size_t>(S));
+    int32_t scount = 0;
+    const int64_t r0 = seq * T;
+    cudaError_t e = cudaSuccess;
+    auto d2h = [&](void* dst, const void* src, size_t n) {
+        if (e == cudaSuccess && n) e = cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, cs);
+    };
+    d2h(kc.data(), cache->k_codes + r0 * W, kc.size() * 4);
+    d2h(vc.data(), cache->v_codes + r0 * W, vc.size() * 4);
+    d2h(km.data(), cache->k_meta + r0 * MG, km.size() * 4);
+    d2h(vm.data(), cache->v_meta + r0 * MG, vm.size() * 4);
+    d2h(mask.data(), cache->sink_mask + seq * MW, mask.size() * 4);
+    d2h(&scount, cache->sink_count + seq, 4);
+    if (S > 0 && cache->sink_k && cache->sink_v && cache->sink_pos) {
+        d2h(sk.data(), cache->sink_k + seq * S * C, sk.size() * 2);
+        d2h(sv.data(), cache->sink_v + seq * S * C, sv.size() * 2);
+        d2h(spos.data(), cache->sink_pos + seq * S, spos.size() * 4);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+    if (e != cudaSuccess) return cuda_fail(e, "cache serialize");
+    scount = std::min<int32_t>(scount, static_cast<int32_t>(S));
+
+    std::vector<uint8_t> o;
+    o.reserve(rkv_cache_wire_bytes(desc, tokens, 0, format));
+    o.push_back(static_cast<uint8_t>(desc->bits | (format == RKV_WIRE_FP16_SCALE ? 0x80 : 0)));
+    put_u64(o, static_cast<uint64_t>(desc->group_size));
+    put_u64(o, static_cast<uint64_t>(C));
+    put_u64(o, static_cast<uint64_t>(tokens));
+    std::vector<float> row(static_cast<size_t>(C)), tmp(static_cast<size_t>(C));
+    for (int64_t t = 0; t < tokens; ++t) {
+        const bool sink = (mask[static_cast<size_t>(t >> 5)] >> (t & 31)) & 1u;
+        o.push_back(sink ? 1 : 0);
+        if (sink) {
+            int s = -1;
+            for (int i = 0; i < scount; ++i)
+                if (spos[static_cast<size_t>(i)] == t) s = i;
+            if (s < 0) return fail(RKV_ERR_RUNTIME, "cache serialize: sink row missing from the sidecar");
+            if (format == RKV_WIRE_FP16_SCALE) {  // lossless: the raw fp16 rows as stored
+                for (int64_t j = 0; j < C; ++j) {
+                    o.push_back(static_cast<uint8_t>(sk[static_cast<size_t>(s * C + j)] & 0xffu));
+                    o.push_back(static_cast<uint8_t>(sk[static_cast<size_t>(s * C + j)] >> 8));
+                }
+                for (int64_t j = 0; j < C; ++j) {
+                    o.push_back(static_cast<uint8_t>(sv[static_cast<size_t>(s * C + j)] & 0xffu));
+                    o.push_back(static_cast<uint8_t>(sv[static_cast<size_t>(s * C + j)] >> 8));
+                }
+                continue;
+            }
+            // K' = apply_reorder(rotate_rows(k, G)) (slot j <- channel perm[j]); V' = rotate_rows(v, 1)
+            for (int64_t j = 0; j < C; ++j) tmp[static_cast<size_t>(j)] = half_bits_to_float(sk[static_cast<size_t>(s * C + j)]);
+            fwht_row(tmp.data(), C, N);
+            for (int64_t j = 0; j < C; ++j) row[static_cast<size_t>(j)] = tmp[static_cast<size_t>(perm[j])];
+            for (float f : row) put_f32(o, f);
+            for (int64_t j = 0; j < C; ++j) row[static_cast<size_t>(j)] = half_bits_to_float(sv[static_cast<size_t>(s * C + j)]);
+            fwht_row(row.data(), C, desc->head_dim);
+            for (float f : row) put_f32(o, f);
+            continue;
+        }
+        for (int kv = 0; kv < 2; ++kv) {
+            const uint32_t* codes = (kv ? vc : kc).data() + t * W;
+            const uint32_t* meta = (kv ? vm : km).data() + t * MG;
+            for (int64_t g = 0; g < MG; ++g) {
+                const uint16_t sbits = static_cast<uint16_t>(meta[g] & 0xffffu);
+                const float zero = half_bits_to_float(static_cast<uint16_t>(meta[g] >> 16));
+                if (format == RKV_WIRE_REFERENCE) {
+                    uint8_t code;
+                    if (!e4m3_code_of(half_bits_to_float(sbits), &code))
+                        return fail(RKV_ERR_INVALID_ARGUMENT,
+                                    "cache serialize: scale is not an e4m3 value (use RKV_WIRE_FP16_SCALE or "
+                                    "scale_format = RKV_SCALE_E4M3_CEIL)");
+                    o.push_back(code);
+                } else {
+                    o.push_back(static_cast<uint8_t>(sbits & 0xffu));
+                    o.push_back(static_cast<uint8_t>(sbits >> 8));
+                }
+                o.push_back(static_cast<uint8_t>(zero));
+                for (int w = 0; w < 8; ++w)
+                    for (int i = 0; i < 4; ++i) o.push_back(static_cast<uint8_t>(codes[g * 8 + w] >> (8 * i)));
+            }
+        }
+    }
+    if (written) *written = o.size();
+    if (out_bytes < o.size()) return fail(RKV_ERR_INVALID_ARGUMENT, "cache serialize: output buffer too small");
+    std::memcpy(out, o.data(), o.size());
+    return RKV_OK;
+}
+
+rkv_status rkv_cache_import(const rkv_layer_desc* desc, const uint8_t* bytes, size_t num_bytes, const int32_t* perm,
+                            int64_t seq, const rkv_cache* cache, int64_t* tokens_out, void* stream) {
+    rkv_status st = validate(desc);
+    if (st != RKV_OK) return st;
+    if ((st = check_cache(cache)) != RKV_OK) return st;
+    if (!perm) return fail(RKV_ERR_INVALID_ARGUMENT, "cache deserialize: null argument");
+    if (seq < 0 || seq >= desc->batch) return fail(RKV_ERR_OUT_OF_RANGE, "cache deserialize: sequence index");
+    if (!bytes || num_bytes == 0) return fail(RKV_ERR_RUNTIME, "cache deserialize: empty input");
+    size_t off = 0;
+    auto need = [&](size_t n) { return off + n <= num_bytes; };
+    auto u64 = [&]() {
+        uint64_t v = 0;
+        for (int i = 0; i < 8; ++i) v |= static_cast<uint64_t>(bytes[off + i]) << (8 * i);
+        off += 8;
+        return v;
+    };
+    if (!need(25)) return fail(RKV_ERR_RUNTIME, "cache deserialize: truncated");
+    const uint8_t hdr = bytes[off++];
+    const bool fp16 = (hdr & 0x80) != 0;
+    const int bits = hdr & 0x7f;
+    const uint64_t group = u64(), channels = u64(), tokens = u64();
+    const int64_t C = static_cast<int64_t>(desc->num_kv_heads) * desc->head_dim, W = C / 16, MG = C / 128;
+    const int64_t N = static_cast<int64_t>(desc->heads_per_group) * desc->head_dim, T = desc->max_tokens;
+    const int64_t MW = (T + 31) / 32, S = desc->max_sinks;
+    if (bits != desc->bits || group != static_cast<uint64_t>(desc->group_size) || channels != static_cast<uint64_t>(C))
+        return fail(RKV_ERR_INVALID_ARGUMENT, "cache deserialize: bits / group / channels differ from the layer");
+    if (tokens > static_cast<uint64_t>(T)) return fail(RKV_ERR_OUT_OF_RANGE, "cache deserialize: more tokens than max_tokens");
+    const int64_t n = static_cast<int64_t>(tokens);
+    std::vector<uint32_t> kc(static_cast<size_t>(n * W), 0u), vc(kc.size(), 0u), km(static_cast<size_t>(n * MG), 0u),
+        vm(km.size(), 0u), mask(static_cast<size_t>(MW), 0u);
+    std::vector<uint16_t> sk(static_cast<size_t>(S * C), 0), sv(sk.size(), 0);
+    std::vector<int32_t> spos(static_cast<size_t>(S), 0);
+    int32_t scount = 0;
+    std::vector<float> row(static_cast<size_t>(C)), tmp(static_cast<size_t>(C));
+    auto f32 = [&]() {
+        uint32_t b = 0;
+        for (int i = 0; i < 4; ++i) b |= static_cast<uint32_t>(bytes[off + i]) << (8 * i);
+        off += 4;
+        float f;
+        std::memcpy(&f, &b, 4);
+        return f;
+    };
+    const size_t block = (fp16 ? 2 : 1) + 1 + 32;
+    for (int64_t t = 0; t < n; ++t) {
+        if (!need(1)) return fail(RKV_ERR_RUNTIME, "cache deserialize: truncated");
+        const bool sink = bytes[off++] != 0;
+        if (sink) {
+            if (!need(static_cast<size_t>(2 * C * (fp16 ? 2 : 4)))) return fail(RKV_ERR_RUNTIME, "cache deserialize: truncated");
+            if (scount >= S) return fail(RKV_ERR_OUT_OF_RANGE, "cache deserialize: more sinks than max_sinks");
+            spos[static_cast<size_t>(scount)] = static_cast<int32_t>(t);
+            mask[static_cast<size_t>(t >> 5)] |= 1u << (t & 31);
+            if (fp16) {  // raw fp16 rows (RKV_WIRE_FP16_SCALE)
+                for (int64_t j = 0; j < 2 * C; ++j) {
+                    const uint16_t h = static_cast<uint16_t>(bytes[off] | (bytes[off + 1] << 8));
+                    off += 2;
+                    (j < C ? sk : sv)[static_cast<size_t>(scount * C + (j % C))] = h;
+                }
+                ++scount;
+                continue;
+            }
+            // back to the raw frame: k = rotate_G(unreorder(K')), v = rotate_1(V') (the FWHT is an involution)
+            for (int64_t j = 0; j < C; ++j) row[static_cast<size_t>(j)] = f32();
+            for (int64_t j = 0; j < C; ++j) tmp[static_cast<size_t>(perm[j])] = row[static_cast<size_t>(j)];
+            fwht_row(tmp.data(), C, N);
+            for (int64_t j = 0; j < C; ++j) sk[static_cast<size_t>(scount * C + j)] = float_to_half_bits(tmp[static_cast<size_t>(j)]);
+            for (int64_t j = 0; j < C; ++j) row[static_cast<size_t>(j)] = f32();
+            fwht_row(row.data(), C, desc->head_dim);
+            for (int64_t j = 0; j < C; ++j) sv[static_cast<size_t>(scount * C + j)] = float_to_half_bits(row[static_cast<size_t>(j)]);
+            ++scount;
+            continue;
+        }
+        if (!need(static_cast<size_t>(2 * MG) * block)) return fail(RKV_ERR_RUNTIME, "cache deserialize: truncated");
+        for (int kv = 0; kv < 2; ++kv) {
+            uint32_t* codes = (kv ? vc : kc).data() + t * W;
+            uint32_t* meta = (kv ? vm : km).data() + t * MG;
+            for (int64_t g = 0; g < MG; ++g) {
+                uint16_t sbits;
+                if (fp16) {
+                    sbits = static_cast<uint16_t>(bytes[off] | (bytes[off + 1] << 8));
+                    off += 2;
+                } else {
+                    sbits = float_to_half_bits(e4m3_value(bytes[off++]));  // exact: e4m3 values are fp16 values
+                }
+                const uint16_t zbits = float_to_half_bits(static_cast<float>(bytes[off++]));
+                meta[g] = static_cast<uint32_t>(sbits) | (static_cast<uint32_t>(zbits) << 16);
+                for (int w = 0; w < 8; ++w) {
+                    uint32_t v = 0;
+                    for (int i = 0; i < 4; ++i) v |= static_cast<uint32_t>(bytes[off + i]) << (8 * i);
+                    off += 4;
+                    codes[g * 8 + w] = v;
+                }
+            }
+        }
+    }
+    cudaStream_t cs = static_cast<cudaStream_t>(stream);
+    const int64_t r0 = seq * T;
+    cudaError_t e = cudaSuccess;
+    auto h2d = [&](void* dst, const void* src, size_t nb) {
+        if (e == cudaSuccess && nb) e = cudaMemcpyAsync(dst, src, nb, cudaMemcpyHostToDevice, cs);
+    };
+    h2d(cache->k_codes + r0 * W, kc.data(), kc.size() * 4);
+    h2d(cache->v_codes + r0 * W, vc.data(), vc.size() * 4);
+    h2d(cache->k_meta + r0 * MG, km.data(), km.size() * 4);
+    h2d(cache->v_meta + r0 * MG, vm.data(), vm.size() * 4);
+    h2d(cache->sink_mask + seq * MW, mask.data(), mask.size() * 4);
+    h2d(cache->sink_count + seq, &scount, 4);
+    if (S > 0 && cache->sink_k && cache->sink_v && cache->sink_pos) {
+        h2d(cache->sink_k + seq * S * C, sk.data(), sk.size() * 2);
+        h2d(cache->sink_v + seq * S * C, sv.data(), sv.size() * 2);
+        h2d(cache->sink_pos + seq * S, spos.data(), spos.size() * 4);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(cs);  // host staging buffers die on return
+    if (e != cudaSuccess) return cuda_fail(e, "cache deserialize");
+    if (tokens_out) *tokens_out = n;
     return RKV_OK;
 }
 

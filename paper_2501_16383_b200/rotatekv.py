@@ -95,13 +95,17 @@ def lib():
         L.rkv_detect_sinks_workspace_bytes.argtypes = []
         L.rkv_detect_sinks_device.argtypes = [P, C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_double, P, P, P,
                                               C.c_size_t, P]
+        L.rkv_cache_wire_bytes.restype = C.c_size_t
+        L.rkv_cache_wire_bytes.argtypes = [D, C.c_int64, C.c_int64, C.c_int32]
+        L.rkv_cache_export.argtypes = [D, P, C.c_int64, C.c_int64, P, C.c_int32, P, C.c_size_t, P, P]
+        L.rkv_cache_import.argtypes = [D, P, C.c_size_t, P, C.c_int64, P, P, P]
         L.rkv_calibrate_workspace_bytes.restype = C.c_size_t
         L.rkv_calibrate_workspace_bytes.argtypes = [D, C.c_int64]
         L.rkv_calibrate_reorder_device.argtypes = [D, P, C.c_int64, C.c_int32, P, C.c_size_t, P, P, P]
         for name in ("rkv_layer_validate", "rkv_cache_carve", "rkv_cache_reset", "rkv_rope_table_init",
                      "rkv_quantize_kv", "rkv_decode_attention", "rkv_rotate_keys", "rkv_calibrate_reorder",
                      "rkv_detect_sinks", "rkv_detect_sinks_device", "rkv_layer_plan_build", "rkv_layer_plan_init",
-                     "rkv_calibrate_reorder_device"):
+                     "rkv_calibrate_reorder_device", "rkv_cache_export", "rkv_cache_import"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -156,6 +160,9 @@ class LayerConfig:
 
 
 # ------------------------------------------------------------ host helpers
+
+WIRE_REFERENCE, WIRE_FP16_SCALE = 0, 1
+
 
 def calibrate_reorder(rotated_keys, stat: int = STAT_MEAN_ABS):
     """calibrate_reorder (proj/src/reorder.cpp:91-110) -> (perm, inverse) int32.
@@ -313,6 +320,32 @@ class RotateKVLayer:
             "sink_count": self._arr("sink_count", t.int32, (B,)),
             "sink_mask": self._arr("sink_mask", t.int32, (B, (T + 31) // 32)),
         }
+
+    # -- LayerKVCache::serialize / deserialize (proj/src/kv_cache.cpp:119-173), one sequence
+    def serialize(self, seq: int, fmt: int = None) -> bytes:
+        """Wire bytes of sequence `seq` (its current length).  fmt:
+        WIRE_REFERENCE (the reference's byte format, e4m3 scales) or
+        WIRE_FP16_SCALE; default: the one matching the layer's scale_format."""
+        if fmt is None:
+            fmt = WIRE_REFERENCE if self.cfg.scale_format == SCALE_E4M3_CEIL else WIRE_FP16_SCALE
+        n = int(self.lengths[seq]) if 0 <= seq < self.cfg.batch else 0  # the C ABI reports a bad index
+        cap = lib().rkv_cache_wire_bytes(C.byref(self._desc), n, min(n, self.cfg.max_sinks), fmt)  # upper bound
+        out = np.empty(max(cap, 1), np.uint8)
+        written = C.c_size_t()
+        _check(lib().rkv_cache_export(C.byref(self._desc), C.byref(self._view), seq, n, self.perm_host.ctypes.data,
+                                      fmt, out.ctypes.data, out.size, C.byref(written), self._stream()))
+        return out[:written.value].tobytes()
+
+    def deserialize(self, data: bytes, seq: int) -> int:
+        """Replace sequence `seq` with the serialized cache; returns its token count."""
+        buf = np.frombuffer(data, np.uint8)
+        n = C.c_int64()
+        _check(lib().rkv_cache_import(C.byref(self._desc), buf.ctypes.data if buf.size else None, buf.size,
+                                      self.perm_host.ctypes.data, seq, C.byref(self._view), C.byref(n),
+                                      self._stream()))
+        self.lengths[seq] = n.value
+        self.sink_counts[seq] = int(self.arrays()["sink_count"][seq].item())
+        return n.value
 
     # -- LayerKVCache::append (proj/src/kv_cache.cpp:8-22), batched
     def append(self, k, v, sink_flags=None, start_pos=None):
