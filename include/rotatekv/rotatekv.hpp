@@ -17,6 +17,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -66,6 +67,23 @@ inline ReorderPlan calibrate_reorder(const std::vector<std::vector<float>>& rota
 }
 
 // apply_reorder (proj/src/reorder.cpp:112-128) on host rows.
+// rotate_rows + calibrate_reorder on device keys (proj/src/pipeline.cpp:101-109):
+// k_rows [rows][C] fp16 device -> perm / inverse of one layer (bit-identical to the host path).
+inline void calibrate_reorder_device(const rkv_layer_desc& desc, const uint16_t* k_rows, int64_t rows, int32_t stat,
+                                     std::vector<int32_t>& perm, std::vector<int32_t>& inverse,
+                                     cudaStream_t stream = nullptr) {
+    const size_t c = static_cast<size_t>(desc.num_kv_heads) * desc.head_dim;
+    const size_t ws_bytes = rkv_calibrate_workspace_bytes(&desc, rows);
+    void* ws = nullptr;
+    if (ws_bytes) check_cuda(cudaMalloc(&ws, ws_bytes), "cudaMalloc calibration workspace");
+    perm.resize(c);
+    inverse.resize(c);
+    const rkv_status st =
+        rkv_calibrate_reorder_device(&desc, k_rows, rows, stat, ws, ws_bytes, perm.data(), inverse.data(), stream);
+    cudaFree(ws);
+    check(st);
+}
+
 inline std::vector<float> apply_reorder(const std::vector<float>& x, const ReorderPlan& plan, int64_t layer,
                                         bool inverse) {
     if (layer < 0 || layer >= plan.layers()) throw std::invalid_argument("apply_reorder: layer out of range");
@@ -101,7 +119,7 @@ class DeviceLayerCache {
 public:
     DeviceLayerCache(const rkv_layer_desc& desc, const std::vector<int32_t>& perm, cudaStream_t stream = nullptr)
         : desc_(desc), stream_(stream), len_(static_cast<size_t>(desc.batch), 0),
-          sinks_(static_cast<size_t>(desc.batch), 0) {
+          sinks_(static_cast<size_t>(desc.batch), 0), perm_host_(perm) {
         check(rkv_layer_validate(&desc_));
         const size_t c = static_cast<size_t>(desc.num_kv_heads) * desc.head_dim;
         if (perm.size() != c) throw std::invalid_argument("reorder plan: wrong channel count in layer line");
@@ -191,6 +209,28 @@ public:
         check_cuda(cudaStreamSynchronize(stream_), "decode");
     }
 
+    // LayerKVCache::serialize (proj/src/kv_cache.cpp:119-139) of sequence b;
+    // format RKV_WIRE_REFERENCE (the reference's bytes, e4m3 scales) or
+    // RKV_WIRE_FP16_SCALE (lossless for fp16 scales).
+    std::vector<uint8_t> serialize(int b, int32_t format) const {
+        const int64_t n = size(b);
+        std::vector<uint8_t> out(rkv_cache_wire_bytes(&desc_, n, std::min<int64_t>(n, desc_.max_sinks), format));
+        size_t written = 0;
+        check(rkv_cache_export(&desc_, &cache_, b, n, perm_host_.data(), format, out.data(), out.size(), &written,
+                               stream_));
+        out.resize(written);
+        return out;
+    }
+    // LayerKVCache::deserialize (proj/src/kv_cache.cpp:141-173) into sequence b.
+    void deserialize(const std::vector<uint8_t>& bytes, int b) {
+        int64_t n = 0;
+        check(rkv_cache_import(&desc_, bytes.data(), bytes.size(), perm_host_.data(), b, &cache_, &n, stream_));
+        len_.at(static_cast<size_t>(b)) = n;
+        int32_t count = 0;
+        check_cuda(cudaMemcpy(&count, cache_.sink_count + b, sizeof(int32_t), cudaMemcpyDeviceToHost), "sink count");
+        sinks_[static_cast<size_t>(b)] = count;
+    }
+
 private:
     rkv_layer_desc desc_;
     cudaStream_t stream_;
@@ -206,6 +246,7 @@ private:
     void* plan_ = nullptr;
     size_t plan_bytes_ = 0;
     int64_t* dev_pos_ = nullptr;
+    std::vector<int32_t> perm_host_;
 };
 
 }  // namespace rotatekv_b200

@@ -155,6 +155,27 @@ int main() {
             std::printf("sequence %d: decode rel err %.3g\n", b, err / mx);
             CHECK(err / mx < 2e-3);
         }
+
+        // LayerKVCache::serialize / deserialize round trip (fp16-scale wire format)
+        const std::vector<uint8_t> blob = cache.serialize(1, RKV_WIRE_FP16_SCALE);
+        rotatekv_b200::DeviceLayerCache other(desc, perm);
+        other.deserialize(blob, 0);
+        CHECK(other.size(0) == T && other.sink_count(0) == 1);
+        CHECK(other.serialize(0, RKV_WIRE_FP16_SCALE) == blob);
+        std::vector<uint8_t> truncated(blob.begin(), blob.end() - 5);
+        CHECK_THROWS_AS(other.deserialize(truncated, 1), std::runtime_error);
+    }
+
+    // rotate_rows + calibrate_reorder on the device == the oracle's on the host
+    {
+        const int R = 64;
+        std::vector<int32_t> dperm, dinv, operm(C), oinv(C);
+        rotatekv_b200::calibrate_reorder_device(desc, dk, R, RKV_STAT_MEAN_ABS, dperm, dinv);
+        std::vector<float> rows(static_cast<size_t>(R) * C);
+        for (size_t i = 0; i < rows.size(); ++i) rows[i] = rkvo_half_to_float(k[i]);
+        rkvo_rotate_rows(rows.data(), R, D, G, H);
+        rkvo_calibrate_reorder(rows.data(), R, C, RKVO_STAT_MEAN_ABS, operm.data(), oinv.data());
+        CHECK(dperm == operm);
     }
     // RotationPlan::make validation (proj/tests/test_hadamard.cpp:57-61)
     rkv_layer_desc bad = desc;
