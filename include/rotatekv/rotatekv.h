@@ -154,6 +154,26 @@ rkv_status rkv_decode_attention(const rkv_layer_desc* desc, const uint16_t* q, c
                                 const float* rope_table, float* out, void* workspace, size_t ws_bytes,
                                 void* stream);
 
+/* Causal attention of a block of queries over the cache (the
+ * attention half of prefill, proj/src/pipeline.cpp:156-191 -- reconstruct_cache
+ * then causal reference_attention, proj/src/attention.cpp:20-49):
+ *   q          : [B][num_q][Hq][d] fp16 pre-RoPE; row i of sequence b sits at
+ *                position q_start[b] + i and attends to cache tokens
+ *                0 .. q_start[b] + i (and < seq_len[b])
+ *   q_start, seq_len : [B] int64, device
+ *   max_seq_len: host upper bound of seq_len (sizes the key reconstruction)
+ *   out        : [B][num_q][Hq][d] fp32, V's rotation undone (like decode)
+ *   workspace  : rkv_prefill_workspace_bytes(desc, num_q, max_seq_len) bytes
+ * Keys are reconstructed once (tensor-core FWHT + RoPE, fp16 hi/lo), then a
+ * flash-attention kernel runs Q.K^T and P.V on the tensor cores; sinks are
+ * added exactly.  Layer shapes: those with a tensor-core decode kernel
+ * (G = 4 with Hq == Hkv, G = 2 with Hq == 4 Hkv).  Stream-ordered. */
+size_t rkv_prefill_workspace_bytes(const rkv_layer_desc* desc, int64_t num_q, int64_t max_seq_len);
+rkv_status rkv_prefill_attention(const rkv_layer_desc* desc, const uint16_t* q, int64_t num_q, const int64_t* q_start,
+                                 const int64_t* seq_len, int64_t max_seq_len, const rkv_cache* cache,
+                                 const void* layer_plan, const float* rope_table, float* out, void* workspace,
+                                 size_t workspace_bytes, void* stream);
+
 /* Grouped-head FWHT of raw fp16 K rows into fp32 (rotate_rows,
  * proj/src/hadamard.cpp:75-84) -- the device half of calibration. */
 rkv_status rkv_rotate_keys(const rkv_layer_desc* desc, const uint16_t* k, int64_t rows, float* out,

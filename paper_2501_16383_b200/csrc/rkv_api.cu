@@ -402,6 +402,62 @@ rkv_status rkv_decode_attention(const rkv_layer_desc* desc, const uint16_t* q, c
     return RKV_OK;
 }
 
+size_t rkv_prefill_workspace_bytes(const rkv_layer_desc* desc, int64_t num_q, int64_t max_seq_len) {
+    if (validate(desc) != RKV_OK || num_q < 0 || max_seq_len < 0) return 0;
+    const size_t C = static_cast<size_t>(desc->num_kv_heads) * desc->head_dim, B = static_cast<size_t>(desc->batch);
+    const size_t rows = B * static_cast<size_t>(num_q) * desc->num_q_heads;
+    const size_t keys = B * static_cast<size_t>(desc->max_tokens) * C * 2;  // fp16 per plane
+    return 2 * al256(keys) + al256(rows * 2 * sizeof(float)) + al256(rows * 128 * sizeof(float));
+}
+
+rkv_status rkv_prefill_attention(const rkv_layer_desc* desc, const uint16_t* q, int64_t num_q, const int64_t* q_start,
+                                 const int64_t* seq_len, int64_t max_seq_len, const rkv_cache* cache,
+                                 const void* layer_plan, const float* rope_table, float* out, void* workspace,
+                                 size_t ws_bytes, void* stream) {
+    rkv_status st = validate(desc);
+    if (st != RKV_OK) return st;
+    if ((st = check_cache(cache)) != RKV_OK) return st;
+    if (num_q < 0) return fail(RKV_ERR_INVALID_ARGUMENT, "prefill: negative query count");
+    if (num_q == 0) return RKV_OK;
+    if (!q || !q_start || !seq_len || !layer_plan || !rope_table || !out || !workspace)
+        return fail(RKV_ERR_INVALID_ARGUMENT, "prefill: null argument");
+    if (max_seq_len < 1 || max_seq_len > desc->max_tokens)
+        return fail(RKV_ERR_OUT_OF_RANGE, "prefill: max_seq_len must be in [1, max_tokens]");
+    if (rkv::decode_kind(*desc) != rkv::kDecodeMma)
+        return fail(RKV_ERR_INVALID_ARGUMENT,
+                    "prefill: the tensor-core path covers G = 4 with Hq == Hkv and G = 2 with Hq == 4 Hkv");
+    if (ws_bytes < rkv_prefill_workspace_bytes(desc, num_q, max_seq_len))
+        return fail(RKV_ERR_INVALID_ARGUMENT, "prefill: workspace too small");
+    const size_t C = static_cast<size_t>(desc->num_kv_heads) * desc->head_dim, B = static_cast<size_t>(desc->batch);
+    const size_t keys = B * static_cast<size_t>(desc->max_tokens) * C * 2;
+    const size_t rows = B * static_cast<size_t>(num_q) * desc->num_q_heads;
+    char* w = static_cast<char*>(workspace);
+    rkv::PrefillParams p{};
+    p.q = q;
+    p.q_start = q_start;
+    p.seq_len = seq_len;
+    p.plan = static_cast<const uint32_t*>(layer_plan);
+    p.rope = reinterpret_cast<const float4*>(rope_table);
+    p.cache = *cache;
+    p.kr_hi = reinterpret_cast<uint16_t*>(w);
+    p.kr_lo = reinterpret_cast<uint16_t*>(w + al256(keys));
+    p.ws_ml = reinterpret_cast<float*>(w + 2 * al256(keys));
+    p.ws_o = reinterpret_cast<float*>(w + 2 * al256(keys) + al256(rows * 2 * sizeof(float)));
+    p.out = out;
+    p.max_tokens = desc->max_tokens;
+    p.num_q = num_q;
+    p.B = desc->batch;
+    p.Hq = desc->num_q_heads;
+    p.Hkv = desc->num_kv_heads;
+    p.C = static_cast<int>(C);
+    p.max_sinks = desc->max_sinks;
+    p.k_norm = 1.0f / std::sqrt(static_cast<float>(desc->heads_per_group * desc->head_dim));
+    p.qscale = rkv::kLog2eHost / std::sqrt(static_cast<float>(desc->head_dim));
+    cudaError_t e = rkv::launch_prefill(*desc, p, max_seq_len, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "prefill_attention");
+    return RKV_OK;
+}
+
 rkv_status rkv_rotate_keys(const rkv_layer_desc* desc, const uint16_t* k, int64_t rows, float* out, void* stream) {
     rkv_status st = validate(desc);
     if (st != RKV_OK) return st;

@@ -51,6 +51,23 @@ struct DecodeParams {
     float qscale;  // log2(e) / sqrt(d)
 };
 
+struct PrefillParams {
+    const uint16_t* q;        // [B][num_q][Hq][128] fp16 pre-RoPE
+    const int64_t* q_start;   // [B] position of query row 0
+    const int64_t* seq_len;   // [B] cache length (keys [0, seq_len))
+    const uint32_t* plan;     // layer plan (tensor-core layout)
+    const float4* rope;       // rope table (decode_attention.cu layout)
+    rkv_cache cache;
+    uint16_t* kr_hi;          // [B][max_tokens][C] reconstructed keys, fp16 hi
+    uint16_t* kr_lo;          //                               and fp16 lo
+    float* ws_ml;             // [B][num_q][Hq][2]
+    float* ws_o;              // [B][num_q][Hq][128]
+    float* out;               // [B][num_q][Hq][128]
+    int64_t max_tokens, num_q;
+    int B, Hq, Hkv, C, max_sinks;
+    float k_norm, qscale;
+};
+
 // quantize_kv.cu
 cudaError_t launch_quantize(const rkv_layer_desc& d, const QuantParams& p, cudaStream_t s);
 // decode_attention.cu
@@ -76,6 +93,8 @@ cudaError_t launch_rotate_keys(const rkv_layer_desc& d, const uint16_t* k, int64
 int num_sms();
 cudaError_t launch_channel_stats(const float* rows_f32, int64_t rows, int64_t C, bool mean_abs, double* stats,
                                  cudaStream_t s);
+// prefill.cu
+cudaError_t launch_prefill(const rkv_layer_desc& d, const PrefillParams& p, int64_t max_seq_len, cudaStream_t s);
 // sink_detect.cu
 size_t detect_sinks_workspace_bytes();
 cudaError_t launch_detect_sinks(const float* x, int64_t b, int64_t s, int64_t hidden, double rel, double abs_floor,

@@ -95,6 +95,9 @@ def lib():
         L.rkv_detect_sinks_workspace_bytes.argtypes = []
         L.rkv_detect_sinks_device.argtypes = [P, C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_double, P, P, P,
                                               C.c_size_t, P]
+        L.rkv_prefill_workspace_bytes.restype = C.c_size_t
+        L.rkv_prefill_workspace_bytes.argtypes = [D, C.c_int64, C.c_int64]
+        L.rkv_prefill_attention.argtypes = [D, P, C.c_int64, P, P, C.c_int64, P, P, P, P, P, C.c_size_t, P]
         L.rkv_cache_wire_bytes.restype = C.c_size_t
         L.rkv_cache_wire_bytes.argtypes = [D, C.c_int64, C.c_int64, C.c_int32]
         L.rkv_cache_export.argtypes = [D, P, C.c_int64, C.c_int64, P, C.c_int32, P, C.c_size_t, P, P]
@@ -105,7 +108,8 @@ def lib():
         for name in ("rkv_layer_validate", "rkv_cache_carve", "rkv_cache_reset", "rkv_rope_table_init",
                      "rkv_quantize_kv", "rkv_decode_attention", "rkv_rotate_keys", "rkv_calibrate_reorder",
                      "rkv_detect_sinks", "rkv_detect_sinks_device", "rkv_layer_plan_build", "rkv_layer_plan_init",
-                     "rkv_calibrate_reorder_device", "rkv_cache_export", "rkv_cache_import"):
+                     "rkv_calibrate_reorder_device", "rkv_cache_export", "rkv_cache_import",
+                     "rkv_prefill_attention"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -320,6 +324,33 @@ class RotateKVLayer:
             "sink_count": self._arr("sink_count", t.int32, (B,)),
             "sink_mask": self._arr("sink_mask", t.int32, (B, (T + 31) // 32)),
         }
+
+    # -- the attention half of prefill (proj/src/pipeline.cpp:156-191): causal, over the cache
+    def prefill_attention(self, q, q_start=None, out=None):
+        """q: [B, nq, Hq, 128] fp16 pre-RoPE; row i of sequence b is the query at
+        position q_start[b] + i (default: the last nq cached tokens) and attends
+        causally to cache tokens 0 .. that position.  Returns fp32 [B, nq, Hq, 128]
+        with V's rotation undone."""
+        torch = self.torch
+        B, Hq = self.cfg.batch, self.cfg.num_q_heads
+        if q.dtype != torch.float16 or q.dim() != 4 or q.shape[0] != B or q.shape[2] != Hq or q.shape[3] != 128:
+            raise ValueError("prefill: q must be [batch, num_q, Hq, 128] fp16")
+        nq = q.shape[1]
+        start = self.lengths - nq if q_start is None else _np(q_start, np.int64)
+        if np.any(start < 0) or np.any(start + nq > self.lengths):
+            raise IndexError("prefill: query positions must lie inside the cache")
+        q = q.contiguous()
+        if out is None:
+            out = torch.empty(B, nq, Hq, 128, dtype=torch.float32, device=self.device)
+        mx = int(self.lengths.max())
+        nws = lib().rkv_prefill_workspace_bytes(C.byref(self._desc), nq, mx)
+        ws = torch.empty(max(nws, 1), dtype=torch.uint8, device=self.device)
+        st = torch.from_numpy(np.ascontiguousarray(start)).to(self.device)
+        ln = torch.from_numpy(self.lengths.copy()).to(self.device)
+        _check(lib().rkv_prefill_attention(C.byref(self._desc), _ptr(q), nq, _ptr(st), _ptr(ln), mx,
+                                           C.byref(self._view), _ptr(self.plan), _ptr(self.rope), _ptr(out),
+                                           _ptr(ws), nws, self._stream()))
+        return out
 
     # -- LayerKVCache::serialize / deserialize (proj/src/kv_cache.cpp:119-173), one sequence
     def serialize(self, seq: int, fmt: int = None) -> bytes:

@@ -1,0 +1,94 @@
+"""Prefill (causal) attention over the quantized cache (
+proj/src/pipeline.cpp:156-191: reconstruct_cache, then causal
+reference_attention, proj/src/attention.cpp:20-49) vs the oracle.
+
+Query row p attends to cache tokens 0..p, so its expected output is the
+oracle's decode_attention over the first p+1 tokens with that row as the query
+(the decode step's semantics, proj/src/pipeline.cpp:197-261).  Tolerance: the
+north star's 2e-3 normalised max error and cosine >= 0.9999, per query row."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2501_16383_b200 as P  # noqa: E402
+from paper_2501_16383_b200 import workload as WL  # noqa: E402
+
+
+def build(hq, hkv, g, T, sinks, seed, B=2, base=10000.0):
+    w = WL.Workload("prefill", B, hq, hkv, T, g, base, 4, (10.0, 30.0))
+    perm = WL.calibration_perm(w, seed)
+    cfg = P.LayerConfig(batch=B, num_q_heads=hq, num_kv_heads=hkv, heads_per_group=g, max_tokens=T + 5,
+                        max_sinks=4, rope_base=base)
+    layer = P.RotateKVLayer(cfg, perm)
+    k, v = WL.make_kv(w, seed, B, T)
+    flags = torch.zeros(B, T, dtype=torch.uint8)
+    for t in sinks:
+        if t < T:
+            flags[:, t] = 1
+    layer.append(k, v, flags)
+    gen = torch.Generator(device="cuda").manual_seed(seed + 5)
+    q = torch.randn(B, T, hq, 128, generator=gen, device="cuda").to(torch.float16)
+    return layer, k, v, flags, q, perm
+
+
+def expected_rows(oracle, layer, k, v, flags, q, perm, b, rows):
+    cfg = layer.cfg
+    a = {n: t.cpu().numpy() for n, t in layer.arrays().items()}
+    kn, vn, qn, fl = k[b].cpu().numpy(), v[b].cpu().numpy(), q[b].cpu().numpy(), flags[b].numpy()
+    out = []
+    for p in rows:
+        n = p + 1
+        out.append(oracle.decode_attention(a["k_codes"][b, :n].view(np.uint32), a["k_meta"][b, :n].view(np.uint32),
+                                           a["v_codes"][b, :n].view(np.uint32), a["v_meta"][b, :n].view(np.uint32),
+                                           fl[:n], kn[:n], vn[:n], qn[p], cfg.num_q_heads, cfg.num_kv_heads, 128,
+                                           cfg.heads_per_group, perm, cfg.rope_base))
+    return np.stack(out)
+
+
+def check(got, want):
+    err = float(np.abs(got - want).max() / np.abs(want).max())
+    cos = float((got * want).sum() / np.linalg.norm(got) / np.linalg.norm(want))
+    assert err <= 2e-3 and cos >= 0.9999, (err, cos)
+    return err
+
+
+@pytest.mark.parametrize("hq,hkv,g,T,sinks,seed", [
+    (8, 8, 4, 1, (0,), 0),
+    (8, 8, 4, 37, (0,), 1),
+    (8, 8, 4, 100, (0, 41, 99), 2),
+    (40, 40, 4, 70, (0,), 3),
+    (32, 8, 2, 90, (0, 3, 64), 4),
+    (32, 8, 2, 33, (), 5),
+])
+def test_prefill_matches_oracle(oracle, hq, hkv, g, T, sinks, seed):
+    layer, k, v, flags, q, perm = build(hq, hkv, g, T, sinks, seed)
+    out = layer.prefill_attention(q, q_start=np.zeros(2, np.int64)).cpu().numpy()
+    for b in range(2):
+        want = expected_rows(oracle, layer, k, v, flags, q, perm, b, range(T))
+        check(out[b], want)
+
+
+def test_chunked_queries_and_decode_agree(oracle):
+    """A chunk of 20 queries at positions 60..79 of an 80-token cache, and the
+    last row against the decode kernel's output for the same query."""
+    layer, k, v, flags, q, perm = build(8, 8, 4, 80, (0, 10), 7)
+    qc = q[:, 60:80].contiguous()
+    out = layer.prefill_attention(qc, q_start=np.full(2, 60, np.int64)).cpu().numpy()
+    for b in range(2):
+        want = expected_rows(oracle, layer, k, v, flags, q, perm, b, range(60, 80))
+        check(out[b], want)
+    dec = layer.decode(q[:, 79].contiguous()).cpu().numpy()
+    check(out[:, 19], dec)
+
+
+def test_prefill_rejects_bad_arguments():
+    layer, k, v, flags, q, perm = build(8, 8, 4, 16, (0,), 9)
+    with pytest.raises(IndexError):
+        layer.prefill_attention(q, q_start=np.full(2, 5, np.int64))  # rows past the cache
+    with pytest.raises(ValueError):
+        layer.prefill_attention(q.float())
