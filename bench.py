@@ -278,6 +278,52 @@ def bench_quantize_cfg5(dev, world, rank):
             "hbm_gbs": bytes_ / (total_ms / 1e3) / 1e9, "bytes": bytes_}
 
 
+def bench_prefill_cfg1(dev):
+    """the attention half of prefill over the quantized cache,
+    BASELINE config 1's layer shape (32 heads x 128, G = 4, theta 10000) with a
+    4096-token prompt: all 4096 query positions attend causally over the 2-bit
+    cache (key reconstruction + flash attention + sink combine), CUDA events.
+    Roofline: tensor bound, standard causal-attention flop count (QK^T + PV)
+    against the measured dense bf16 peak (the kernel issues 2x that for the
+    hi/lo split of Q.K^T)."""
+    import torch
+
+    import paper_2501_16383_b200 as P
+    from paper_2501_16383_b200 import workload as WL
+
+    w, T, B = WL.CONFIGS[1], 4096, 1
+    perm = WL.calibration_perm(w, SEED - 1, device=dev)
+    cfg = P.LayerConfig(batch=B, num_q_heads=w.num_q_heads, num_kv_heads=w.num_kv_heads,
+                        heads_per_group=w.heads_per_group, max_tokens=T, max_sinks=4, rope_base=w.rope_base)
+    layer = P.RotateKVLayer(cfg, perm, device=dev)
+    flags = torch.zeros(B, T, dtype=torch.uint8)
+    flags[:, 0] = 1
+    k, v = WL.make_kv(w, SEED - 1, B, T, device=dev)
+    layer.append(k, v, flags)
+    gen = torch.Generator(device=dev).manual_seed(SEED)
+    q = torch.randn(B, T, w.num_q_heads, 128, generator=gen, device=dev).to(torch.float16)
+    out = layer.prefill_attention(q)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters = 10
+    e0.record(torch.cuda.current_stream(dev))
+    for _ in range(iters):
+        layer.prefill_attention(q, out=out)
+    e1.record(torch.cuda.current_stream(dev))
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / iters
+    flops = 4.0 * B * w.num_q_heads * 128 * T * (T + 1) / 2
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peak = float(json.load(f)["bf16_tflops"])
+    except Exception:
+        peak = 2250.0
+    tf = flops / (ms / 1e3) / 1e12
+    return {"workload": "cfg1-llama2-7b-prefill-b1-t4096 (causal attention over the 2-bit cache)", "ms": ms,
+            "prompt_tokens_per_s": B * T / (ms / 1e3),
+            "roofline": {"bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak}}
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -438,6 +484,12 @@ def run_ours(args):
         except Exception:
             traffic = None
 
+    prefill1 = None
+    if rank == 0 and world == 1 and not args.no_quantize:
+        try:
+            prefill1 = bench_prefill_cfg1(dev)
+        except Exception as exc:  # report, never fail the headline line
+            prefill1 = {"error": str(exc)}
     quant5 = None
     if not args.no_quantize:
         del layer, ws
@@ -497,6 +549,7 @@ def run_ours(args):
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,
         "quantize_cfg5": quant5,
+        "prefill_cfg1": prefill1,
     }
     print(json.dumps(line), flush=True)
 

@@ -380,12 +380,16 @@ cudaError_t launch_quantize_n(const QuantParams& p, int B, cudaStream_t s) {
     static int per_sm_cache[9] = {0};  // keyed by C / 1024 (C <= 8192)
     int& per_sm = per_sm_cache[p.C / 1024];
     const int threads = (p.C / 32 + 31) / 32 * 32;
-    if (per_sm == 0) {
-        cudaError_t e = cudaFuncSetAttribute(quantize_kv_kernel<N, FMT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem));
+    // the shared-memory limit is a per-kernel attribute: set it for THIS launch's
+    // size every time (a layer of another width may have lowered it)
+    {
+        const cudaError_t e = cudaFuncSetAttribute(quantize_kv_kernel<N, FMT>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         if (e != cudaSuccess) return e;
+    }
+    if (per_sm == 0) {
         int n = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, quantize_kv_kernel<N, FMT>, threads, smem);
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, quantize_kv_kernel<N, FMT>, threads, smem);
         if (e != cudaSuccess) return e;
         if (n < 1) return cudaErrorInvalidConfiguration;
         per_sm = n;
