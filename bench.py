@@ -273,9 +273,25 @@ def bench_quantize_cfg5(dev, world, rank):
         layers.append(lay)  # keep the 40-layer cache resident (755 MB / layer at B=128)
     rows = B * T * w.layers
     bytes_ = rows * (2 * Cc * 2 + 2 * (Cc // 4 + Cc // 32))
+    cpu = None
+    try:  # the reference's quantize chain (rotate_rows -> apply_reorder -> quantize_token) on the host
+        import oracle
+
+        if rank == 0 and oracle.have_ref():
+            ns = 256
+            kk, vv = WL.make_kv(w, SEED + 5, 1, ns, device=dev)
+            kf, vf = kk[0].float().cpu().numpy(), vv[0].float().cpu().numpy()
+            t0 = time.perf_counter()
+            oracle.ref_quantize_kv_rows(kf, vf, w.num_kv_heads, 128, w.heads_per_group, perm)
+            cpu_s = time.perf_counter() - t0
+            cpu = {"value": ns / cpu_s, "unit": "token rows/s (K+V)", "cores": 1, "kind": "reference",
+                   "sample": f"{ns} token rows of one layer (C={Cc}, G={w.heads_per_group}) through the reference's "
+                             "rotate_rows -> apply_reorder -> quantize_token, 1 thread"}
+    except Exception as exc:
+        cpu = {"error": str(exc)}
     return {"workload": w.name, "sequences_per_gpu": B, "layers": w.layers, "tokens": rows,
             "ms": total_ms, "tokens_per_s_per_gpu": rows / (total_ms / 1e3),
-            "hbm_gbs": bytes_ / (total_ms / 1e3) / 1e9, "bytes": bytes_}
+            "hbm_gbs": bytes_ / (total_ms / 1e3) / 1e9, "bytes": bytes_, "cpu_baseline": cpu}
 
 
 def bench_prefill_cfg1(dev):
@@ -319,9 +335,45 @@ def bench_prefill_cfg1(dev):
     except Exception:
         peak = 2250.0
     tf = flops / (ms / 1e3) / 1e12
-    return {"workload": "cfg1-llama2-7b-prefill-b1-t4096 (causal attention over the 2-bit cache)", "ms": ms,
-            "prompt_tokens_per_s": B * T / (ms / 1e3),
-            "roofline": {"bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak}}
+    res = {"workload": "cfg1-llama2-7b-prefill-b1-t4096 (causal attention over the 2-bit cache)", "ms": ms,
+           "prompt_tokens_per_s": B * T / (ms / 1e3),
+           "roofline": {"bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak}}
+    # the reference's own prefill (identity projections) on the host, bounded sample: a 512-token prompt
+    try:
+        import numpy as np
+
+        import oracle
+
+        if oracle.have_ref():
+            Ts = 512
+            rng = np.random.default_rng(SEED)
+            x = rng.standard_normal((Ts, w.channels)).astype(np.float16)
+            fl = np.zeros(Ts, np.uint8)
+            fl[0] = 1
+            t0 = time.perf_counter()
+            oracle.ref_prefill(x.astype(np.float32), fl, perm, w.num_kv_heads, 128, w.heads_per_group, w.rope_base)
+            cpu_s = time.perf_counter() - t0
+            cfg_s = P.LayerConfig(batch=1, num_q_heads=w.num_q_heads, num_kv_heads=w.num_kv_heads,
+                                  heads_per_group=w.heads_per_group, max_tokens=Ts, max_sinks=4, rope_base=w.rope_base)
+            lay_s = P.RotateKVLayer(cfg_s, perm, device=dev)
+            xt = torch.from_numpy(x).to(dev)[None]
+            lay_s.append(xt, xt, torch.from_numpy(fl)[None])
+            qs = xt.reshape(1, Ts, w.num_q_heads, 128)
+            lay_s.prefill_attention(qs)
+            torch.cuda.synchronize()
+            e0.record(torch.cuda.current_stream(dev))
+            for _ in range(iters):
+                lay_s.prefill_attention(qs)
+            e1.record(torch.cuda.current_stream(dev))
+            torch.cuda.synchronize()
+            res["cpu_baseline"] = {"value": Ts / cpu_s, "unit": "prompt tokens/s", "cores": 1, "kind": "reference",
+                                   "sample": f"1 x {Ts}-token prompt through the reference's prefill (its quantized "
+                                             "cache, reconstruct_cache, causal reference_attention; identity "
+                                             "projections), 1 thread",
+                                   "gpu_same_sample_tokens_per_s": Ts / (e0.elapsed_time(e1) / iters / 1e3)}
+    except Exception as exc:
+        res["cpu_baseline"] = {"error": str(exc)}
+    return res
 
 
 def run_ours(args):

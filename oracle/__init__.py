@@ -104,6 +104,8 @@ def ref():
         R.ref_apply_rope_rows.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_void_p, C.c_int]
         R.ref_detect_sinks.restype = C.c_int64
         R.ref_detect_sinks.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_void_p]
+        R.ref_prefill.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                                  C.c_double, C.c_void_p]
         R.ref_cache_serialize.restype = C.c_int64
         R.ref_cache_serialize.argtypes = [C.c_void_p] * 3 + [C.c_int64] * 4 + [C.c_void_p] * 2 + [C.c_int64]
         R.ref_cache_reserialize.restype = C.c_int64
@@ -267,6 +269,19 @@ def decode_attention(k_codes, k_meta, v_codes, v_meta, is_sink, sink_k, sink_v, 
                                      float(rope_base), _p(out))
     if rc != 0:
         raise ValueError("decode_attention failed")
+    return out
+
+
+def ref_prefill(x, sink, perm, num_heads, head_dim, heads_per_group, rope_base):
+    """The reference's prefill attention output [T, C] (identity projections:
+    x rows are keys, values and queries; token 0 + flagged tokens are sinks)."""
+    x = f32(x)
+    sink = np.ascontiguousarray(sink, np.uint8)
+    perm = np.ascontiguousarray(perm, np.int32)
+    out = np.empty_like(x)
+    if ref().ref_prefill(num_heads, head_dim, heads_per_group, _p(x), _p(sink), x.shape[0], _p(perm),
+                         float(rope_base), _p(out)) != 0:
+        raise ValueError("ref_prefill failed")
     return out
 
 

@@ -286,6 +286,37 @@ int ref_decode_step(int64_t num_heads, int64_t head_dim, int64_t hpg, const floa
     } catch (const std::exception&) { return -1; }
 }
 
+// The reference's own prefill (proj/src/pipeline.cpp:156-191) with identity
+// projections: x [T][C] is each token's key, value and query; token 0 and the
+// flagged tokens are sinks; out = prefill's attention output [T][C] (after the
+// fused W_o, i.e. V's rotation undone).  MHA only (the reference has no GQA).
+int ref_prefill(int64_t num_heads, int64_t head_dim, int64_t hpg, const float* x, const uint8_t* sink, int64_t T,
+                const int32_t* perm, double rope_base, float* out) {
+    try {
+        int64_t c = num_heads * head_dim;
+        QuantConfig q;
+        q.bits = 2;
+        q.group_size = 128;
+        PipelineConfig cfg = PipelineConfig::make(PipelineMode::RotateKV, num_heads, head_dim, hpg, q, true);
+        cfg.reorder = plan_from_perm(perm, c);
+        cfg.rope.base = rope_base;
+        AttentionWeights w;
+        w.wq = eye(c);
+        w.wk = eye(c);
+        w.wv = eye(c);
+        w.wo = eye(c);
+        fuse_weights(w, cfg.key_rotation, cfg.reorder, cfg.value_rotation);
+        SinkSet extra;
+        extra.tokens.push_back(0);  // token 0 is always a member (proj/include/rotatekv/sink.hpp:18-19)
+        for (int64_t t = 1; t < T; ++t)
+            if (sink[t]) extra.tokens.push_back(t);
+        Tensor xt({1, T, c}, std::vector<float>(x, x + T * c));
+        PrefillResult r = prefill(xt, w, cfg, &extra);
+        std::memcpy(out, r.output.data(), sizeof(float) * static_cast<size_t>(T * c));
+        return 0;
+    } catch (const std::exception&) { return -1; }
+}
+
 void* ref_bench_create(int64_t num_heads, int64_t head_dim, int64_t hpg, int64_t T, int64_t nseq,
                        const int32_t* perm, double rope_base, uint64_t seed, int nthreads) {
     try {

@@ -92,3 +92,27 @@ def test_prefill_rejects_bad_arguments():
         layer.prefill_attention(q, q_start=np.full(2, 5, np.int64))  # rows past the cache
     with pytest.raises(ValueError):
         layer.prefill_attention(q.float())
+
+
+@pytest.mark.parametrize("heads,g,T,sinks,seed", [(8, 4, 48, (0, 20), 11), (4, 4, 9, (0,), 12), (16, 4, 64, (0, 1, 63), 13)])
+def test_prefill_matches_reference_prefill(oracle, heads, g, T, sinks, seed):
+    """Against the UNMODIFIED reference's prefill (identity projections: each
+    token's raw row is its key, value and query; e4m3 scales so the cache is
+    the reference's bit for bit)."""
+    if not oracle.have_ref():
+        pytest.skip("oracle/_ref not built")
+    C = heads * 128
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((T, C)).astype(np.float16)
+    perm = rng.permutation(C).astype(np.int32)
+    flags = np.zeros(T, np.uint8)
+    for t in sinks:
+        flags[t] = 1
+    cfg = P.LayerConfig(batch=1, num_q_heads=heads, num_kv_heads=heads, heads_per_group=g, max_tokens=T,
+                        max_sinks=4, scale_format=P.SCALE_E4M3_CEIL)
+    layer = P.RotateKVLayer(cfg, perm)
+    xt = torch.from_numpy(x).cuda()[None]
+    layer.append(xt, xt, torch.from_numpy(flags)[None])
+    out = layer.prefill_attention(xt.reshape(1, T, heads, 128), q_start=np.zeros(1, np.int64)).cpu().numpy()
+    want = oracle.ref_prefill(x.astype(np.float32), flags, perm, heads, 128, g, 10000.0)
+    check(out[0].reshape(T, C), want)
