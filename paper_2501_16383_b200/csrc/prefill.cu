@@ -186,16 +186,29 @@ __global__ void __launch_bounds__(512) reconstruct_keys_kernel(PrefillParams p) 
 
 // -------------------------------------------------------------- 2. attention
 constexpr int kQB = 64, kKT = 32, kRowH = 136;  // queries per CTA, keys per tile, padded smem row (halves)
+// one K/V tile buffer: K hi + lo rows, V words of the KV head, V meta words, sink-mask word
+constexpr int kTileBytes = 2 * kKT * kRowH * 2 + kKT * 8 * 4 + kKT * 4 + 16;
+
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], uint32_t addr) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr));
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src, uint32_t src_bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 __global__ void __launch_bounds__(128) prefill_attn_kernel(PrefillParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     uint16_t* qhi = reinterpret_cast<uint16_t*>(smem);  // [64][136]
     uint16_t* qlo = qhi + kQB * kRowH;
-    uint16_t* khi = qlo + kQB * kRowH;                   // [32][136]
-    uint16_t* klo = khi + kKT * kRowH;
-    uint32_t* vws = reinterpret_cast<uint32_t*>(klo + kKT * kRowH);  // [32][8] V words of the KV head
-    uint32_t* vms = vws + kKT * 8;                                    // [32] V meta word
-    uint32_t* msk = vms + kKT;                                        // [1] sink bits of the tile
+    unsigned char* tiles = reinterpret_cast<unsigned char*>(qlo + kQB * kRowH);  // 2 x kTileBytes
 
     const int qb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, tl = lane & 3;
@@ -206,6 +219,35 @@ __global__ void __launch_bounds__(128) prefill_attn_kernel(PrefillParams p) {
     const int64_t qpos0 = p.q_start[b] + i0;
     const int64_t T = p.seq_len[b];
     const int64_t row0 = static_cast<int64_t>(b) * p.max_tokens;
+    const uint32_t* smask = p.cache.sink_mask + static_cast<int64_t>(b) * ((p.max_tokens + 31) / 32);
+    const int64_t kend = lmin64(T, qpos0 + nrows);  // keys [0, kend)
+
+    // K/V tile k0 -> buffer bi, cp.async (rows past the end are zero-filled)
+    auto issue = [&](int bi, int64_t k0) {
+        unsigned char* tb = tiles + bi * kTileBytes;
+        const uint32_t khs = smem_u32(tb), kls = khs + kKT * kRowH * 2;
+        const uint32_t vws = kls + kKT * kRowH * 2, vms = vws + kKT * 8 * 4, mks = vms + kKT * 4;
+        const int nk = static_cast<int>(lmin64(kKT, kend - k0));
+        for (int idx = tid; idx < kKT * 16; idx += 128) {
+            const int kk = idx >> 4, ch = (idx & 15) * 8;
+            const int64_t src = (row0 + k0 + (kk < nk ? kk : 0)) * C + kvh * 128 + ch;
+            const uint32_t nb = kk < nk ? 16u : 0u;
+            cp_async16(khs + (kk * kRowH + ch) * 2, p.kr_hi + src, nb);
+            cp_async16(kls + (kk * kRowH + ch) * 2, p.kr_lo + src, nb);
+        }
+        if (tid < kKT * 2) {  // V words: 8 per key = two 16-byte chunks
+            const int kk = tid >> 1;
+            const int64_t src = (row0 + k0 + (kk < nk ? kk : 0)) * W + kvh * 8 + (tid & 1) * 4;
+            cp_async16(vws + tid * 16, p.cache.v_codes + src, kk < nk ? 16u : 0u);
+        } else if (tid < kKT * 3) {  // V meta word of the KV head
+            const int kk = tid - kKT * 2;
+            cp_async4(vms + kk * 4, p.cache.v_meta + (row0 + k0 + (kk < nk ? kk : 0)) * MG + kvh, kk < nk ? 4u : 0u);
+        } else if (tid == kKT * 3) {
+            cp_async4(mks, smask + (k0 >> 5), 4u);  // k0 % 32 == 0
+        }
+        cp_async_commit();
+    };
+    if (kend > 0) issue(0, 0);
 
     // q: RoPE at each row's position, x log2(e)/sqrt(d), split into fp16 hi + lo
     for (int idx = tid; idx < kQB * 64; idx += blockDim.x) {
@@ -228,145 +270,138 @@ __global__ void __launch_bounds__(128) prefill_attn_kernel(PrefillParams p) {
     const int wr = warp * 16;  // this warp's first row
     const int64_t qp_a = qpos0 + wr + g, qp_b = qp_a + 8;
     const int64_t warp_last = qpos0 + std::min(wr + 15, nrows - 1);
-    const int64_t kend = lmin64(T, qpos0 + nrows);  // keys [0, kend)
     float m_r[2] = {-INFINITY, -INFINITY}, l_r[2] = {0.f, 0.f}, zc_r[2] = {0.f, 0.f};
     float o[16][4];
 #pragma unroll
     for (int e = 0; e < 16; ++e)
 #pragma unroll
         for (int c = 0; c < 4; ++c) o[e][c] = 0.f;
+    // ldmatrix lane addresses: A (Q rows wr.., matrices (r0-7,c0-7),(r8-15,c0-7),(r0-7,c8-15),(r8-15,c8-15));
+    // B (K rows = keys: (k0-7,c0-7),(k0-7,c8-15),(k8-15,c0-7),(k8-15,c8-15) -> two n-tiles)
+    const int mi = lane >> 3, mr = lane & 7;
+    const uint32_t qa_hi = smem_u32(qhi + (wr + mr + 8 * (mi & 1)) * kRowH + 8 * (mi >> 1));
+    const uint32_t qa_lo = qa_hi + kQB * kRowH * 2;
+    const uint32_t kb_off = ((mr + 8 * (mi >> 1)) * kRowH + 8 * (mi & 1)) * 2;
 
-    const uint32_t* smask = p.cache.sink_mask + static_cast<int64_t>(b) * ((p.max_tokens + 31) / 32);
-    for (int64_t k0 = 0; k0 < kend; k0 += kKT) {
-        __syncthreads();  // previous tile consumed (and q tile written)
+    int bi = 0;
+    for (int64_t k0 = 0; k0 < kend; k0 += kKT, bi ^= 1) {
+        if (k0 + kKT < kend) {
+            issue(bi ^ 1, k0 + kKT);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();  // tile k0 (and the q tile) visible
+        const unsigned char* tb = tiles + bi * kTileBytes;
+        const uint32_t khs = smem_u32(tb), kls = khs + kKT * kRowH * 2;
+        const uint32_t* vws = reinterpret_cast<const uint32_t*>(tb + 2 * kKT * kRowH * 2);
+        const uint32_t* vms = vws + kKT * 8;
+        const uint32_t mbits = vms[kKT];
         const int nk = static_cast<int>(lmin64(kKT, kend - k0));
-        for (int idx = tid; idx < kKT * 16; idx += blockDim.x) {  // K hi/lo rows: 16 x 16-byte chunks each
-            const int kk = idx >> 4, ch = (idx & 15) * 8;
-            uint4 vh = make_uint4(0, 0, 0, 0), vl = vh;
-            if (kk < nk) {
-                const int64_t src = (row0 + k0 + kk) * C + kvh * 128 + ch;
-                vh = *reinterpret_cast<const uint4*>(p.kr_hi + src);
-                vl = *reinterpret_cast<const uint4*>(p.kr_lo + src);
+        if (!(k0 > warp_last || wr >= nrows)) {
+            // S = Q K^T (16 rows x 32 keys), fp16 hi/lo split on both operands
+            float s[4][4];
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) s[nt][c] = 0.f;
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+                uint32_t ah[4], al[4];
+                ldsm_x4(ah, qa_hi + ks * 32);
+                ldsm_x4(al, qa_lo + ks * 32);
+#pragma unroll
+                for (int np = 0; np < 2; ++np) {  // n-tile pairs (2np, 2np+1)
+                    uint32_t bh[4], bl[4];
+                    const uint32_t off = kb_off + (np * 16 * kRowH + ks * 16) * 2;
+                    ldsm_x4(bh, khs + off);
+                    ldsm_x4(bl, kls + off);
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        float (&acc)[4] = s[2 * np + j];
+                        mma16816(acc, ah, bh[2 * j], bh[2 * j + 1], acc);
+                        mma16816(acc, ah, bl[2 * j], bl[2 * j + 1], acc);
+                        mma16816(acc, al, bh[2 * j], bh[2 * j + 1], acc);
+                    }
+                }
             }
-            *reinterpret_cast<uint4*>(khi + kk * kRowH + ch) = vh;
-            *reinterpret_cast<uint4*>(klo + kk * kRowH + ch) = vl;
-        }
-        for (int idx = tid; idx < kKT * 8; idx += blockDim.x) {
-            const int kk = idx >> 3;
-            vws[idx] = kk < nk ? p.cache.v_codes[(row0 + k0 + kk) * W + kvh * 8 + (idx & 7)] : 0u;
-        }
-        if (tid < kKT) vms[tid] = tid < nk ? p.cache.v_meta[(row0 + k0 + tid) * MG + kvh] : 0u;
-        if (tid == 0) {  // k0 % 32 == 0
-            uint32_t mbits = smask[k0 >> 5];
-            msk[0] = mbits;
-        }
-        __syncthreads();
-        if (k0 > warp_last || wr >= nrows) continue;  // every row of this warp is masked for this tile
-
-        // S = Q K^T (16 rows x 32 keys), fp16 hi/lo split on both operands
-        float s[4][4];
+            // mask (causal, length, sinks) and online softmax for rows g, g+8
+            float mx[2] = {-INFINITY, -INFINITY};
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt)
+            for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
-            for (int c = 0; c < 4; ++c) s[nt][c] = 0.f;
+                for (int c = 0; c < 4; ++c) {
+                    const int kk = nt * 8 + 2 * tl + (c & 1);
+                    const int64_t kp = k0 + kk;
+                    const int64_t qp = (c >> 1) ? qp_b : qp_a;
+                    const bool ok = kk < nk && kp <= qp && !((mbits >> kk) & 1u);
+                    s[nt][c] = ok ? s[nt][c] : -INFINITY;
+                    mx[c >> 1] = fmaxf(mx[c >> 1], s[nt][c]);
+                }
+            float alpha[2];
 #pragma unroll
-        for (int ks = 0; ks < 8; ++ks) {
-            const int c0 = 16 * ks + 2 * tl;
-            uint32_t ah[4], al[4];
-            ah[0] = *reinterpret_cast<const uint32_t*>(qhi + (wr + g) * kRowH + c0);
-            ah[1] = *reinterpret_cast<const uint32_t*>(qhi + (wr + g + 8) * kRowH + c0);
-            ah[2] = *reinterpret_cast<const uint32_t*>(qhi + (wr + g) * kRowH + c0 + 8);
-            ah[3] = *reinterpret_cast<const uint32_t*>(qhi + (wr + g + 8) * kRowH + c0 + 8);
-            al[0] = *reinterpret_cast<const uint32_t*>(qlo + (wr + g) * kRowH + c0);
-            al[1] = *reinterpret_cast<const uint32_t*>(qlo + (wr + g + 8) * kRowH + c0);
-            al[2] = *reinterpret_cast<const uint32_t*>(qlo + (wr + g) * kRowH + c0 + 8);
-            al[3] = *reinterpret_cast<const uint32_t*>(qlo + (wr + g + 8) * kRowH + c0 + 8);
+            for (int r = 0; r < 2; ++r) {
+                mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
+                mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
+                const float mn = fmaxf(m_r[r], mx[r]);
+                alpha[r] = mn == -INFINITY ? 1.0f : ex2(m_r[r] - mn);
+                m_r[r] = mn;
+                l_r[r] *= alpha[r];
+                zc_r[r] *= alpha[r];
+            }
+            if (alpha[0] != 1.0f || alpha[1] != 1.0f) {
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                    o[e][0] *= alpha[0];
+                    o[e][1] *= alpha[0];
+                    o[e][2] *= alpha[1];
+                    o[e][3] *= alpha[1];
+                }
+            }
+            // P (x the key's V scale, fp16) as the A operand of P.V; zero point folded per row
+            uint32_t pa[2][4];
 #pragma unroll
             for (int nt = 0; nt < 4; ++nt) {
-                const int kr = nt * 8 + g;
-                const uint32_t bh0 = *reinterpret_cast<const uint32_t*>(khi + kr * kRowH + c0);
-                const uint32_t bh1 = *reinterpret_cast<const uint32_t*>(khi + kr * kRowH + c0 + 8);
-                const uint32_t bl0 = *reinterpret_cast<const uint32_t*>(klo + kr * kRowH + c0);
-                const uint32_t bl1 = *reinterpret_cast<const uint32_t*>(klo + kr * kRowH + c0 + 8);
-                mma16816(s[nt], ah, bh0, bh1, s[nt]);
-                mma16816(s[nt], ah, bl0, bl1, s[nt]);
-                mma16816(s[nt], al, bh0, bh1, s[nt]);
+                float w[4], zr[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int kk = nt * 8 + 2 * tl + (c & 1);
+                    const float pr = s[nt][c] == -INFINITY ? 0.f : ex2(s[nt][c] - m_r[c >> 1]);
+                    l_r[c >> 1] += pr;
+                    const uint32_t vm = pr > 0.f ? vms[kk] : 0u;
+                    w[c] = pr * h2f(static_cast<uint16_t>(vm & 0xffffu));
+                    zr[c] = h2f(static_cast<uint16_t>(vm >> 16));
+                }
+                const uint32_t p01 = pack_h2(w[0], w[1]), p23 = pack_h2(w[2], w[3]);
+                const uint32_t z01 = pack_h2(zr[0], zr[1]), z23 = pack_h2(zr[2], zr[3]);
+                zc_r[0] = fhfma<0, 0>(p01, z01, zc_r[0]);
+                zc_r[0] = fhfma<1, 1>(p01, z01, zc_r[0]);
+                zc_r[1] = fhfma<0, 0>(p23, z23, zc_r[1]);
+                zc_r[1] = fhfma<1, 1>(p23, z23, zc_r[1]);
+                pa[nt >> 1][(nt & 1) * 2 + 0] = p01;  // rows g: keys 2tl..(+8)
+                pa[nt >> 1][(nt & 1) * 2 + 1] = p23;  // rows g+8
+            }
+#pragma unroll
+            for (int kb = 0; kb < 2; ++kb) {
+                const uint32_t a[4] = {pa[kb][0], pa[kb][1], pa[kb][2], pa[kb][3]};
+                const int ka = 16 * kb + 2 * tl;
+                const uint32_t w0 = vws[ka * 8 + g], w1 = vws[(ka + 1) * 8 + g];
+                const uint32_t w8 = vws[(ka + 8) * 8 + g], w9 = vws[(ka + 9) * 8 + g];
+                const uint32_t xl0 = prmt(w0, w1, 0x5410u), xh0 = prmt(w0, w1, 0x7632u);
+                const uint32_t xl8 = prmt(w8, w9, 0x5410u), xh8 = prmt(w8, w9, 0x7632u);
+                const uint32_t xl0s = xl0 >> 10, xh0s = xh0 >> 10, xl8s = xl8 >> 10, xh8s = xh8 >> 10;
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                    const int ee = e & 7;
+                    const int sh = ee < 5 ? ee : ee - 5;
+                    const uint32_t m = 0x00030003u << (2 * sh);
+                    const uint32_t b0 = (e < 8 ? (ee < 5 ? xl0 : xl0s) : (ee < 5 ? xh0 : xh0s)) & m;
+                    const uint32_t b1 = (e < 8 ? (ee < 5 ? xl8 : xl8s) : (ee < 5 ? xh8 : xh8s)) & m;
+                    mma16816(o[e], a, b0, b1, o[e]);
+                }
             }
         }
-        // mask (causal, length, sinks) and online softmax for rows g, g+8
-        const uint32_t mbits = msk[0];
-        float mx[2] = {-INFINITY, -INFINITY};
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const int kk = nt * 8 + 2 * tl + (c & 1);
-                const int64_t kp = k0 + kk;
-                const int64_t qp = (c >> 1) ? qp_b : qp_a;
-                const bool ok = kk < nk && kp <= qp && !((mbits >> kk) & 1u);
-                s[nt][c] = ok ? s[nt][c] : -INFINITY;
-                mx[c >> 1] = fmaxf(mx[c >> 1], s[nt][c]);
-            }
-        float alpha[2];
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
-            mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
-            const float mn = fmaxf(m_r[r], mx[r]);
-            alpha[r] = mn == -INFINITY ? 1.0f : ex2(m_r[r] - mn);
-            m_r[r] = mn;
-            l_r[r] *= alpha[r];
-            zc_r[r] *= alpha[r];
-        }
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-            o[e][0] *= alpha[0];
-            o[e][1] *= alpha[0];
-            o[e][2] *= alpha[1];
-            o[e][3] *= alpha[1];
-        }
-        // P (x the key's V scale, fp16) as the A operand of P.V; zero point folded per row
-        uint32_t pa[2][4];
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt) {
-            float w[4];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const int kk = nt * 8 + 2 * tl + (c & 1);
-                const float pr = s[nt][c] == -INFINITY ? 0.f : ex2(s[nt][c] - m_r[c >> 1]);
-                l_r[c >> 1] += pr;
-                const uint32_t vm = pr > 0.f ? vms[kk] : 0u;
-                w[c] = pr * h2f(static_cast<uint16_t>(vm & 0xffffu));
-                s[nt][c] = h2f(static_cast<uint16_t>(vm >> 16));  // reuse: zero point of the key
-            }
-            const uint32_t p01 = pack_h2(w[0], w[1]), p23 = pack_h2(w[2], w[3]);
-            zc_r[0] = fhfma<0, 0>(p01, pack_h2(s[nt][0], s[nt][1]), zc_r[0]);
-            zc_r[0] = fhfma<1, 1>(p01, pack_h2(s[nt][0], s[nt][1]), zc_r[0]);
-            zc_r[1] = fhfma<0, 0>(p23, pack_h2(s[nt][2], s[nt][3]), zc_r[1]);
-            zc_r[1] = fhfma<1, 1>(p23, pack_h2(s[nt][2], s[nt][3]), zc_r[1]);
-            pa[nt >> 1][(nt & 1) * 2 + 0] = p01;  // rows g: keys 2tl..(+8)
-            pa[nt >> 1][(nt & 1) * 2 + 1] = p23;  // rows g+8
-        }
-#pragma unroll
-        for (int kb = 0; kb < 2; ++kb) {
-            // A fragment: (g, k 2tl..), (g+8, k 2tl..), (g, k 2tl+8..), (g+8, k 2tl+8..)
-            const uint32_t a[4] = {pa[kb][0], pa[kb][1], pa[kb][2], pa[kb][3]};
-            const int ka = 16 * kb + 2 * tl;
-            const uint32_t w0 = vws[ka * 8 + g], w1 = vws[(ka + 1) * 8 + g];
-            const uint32_t w8 = vws[(ka + 8) * 8 + g], w9 = vws[(ka + 9) * 8 + g];
-            const uint32_t xl0 = prmt(w0, w1, 0x5410u), xh0 = prmt(w0, w1, 0x7632u);
-            const uint32_t xl8 = prmt(w8, w9, 0x5410u), xh8 = prmt(w8, w9, 0x7632u);
-            const uint32_t xl0s = xl0 >> 10, xh0s = xh0 >> 10, xl8s = xl8 >> 10, xh8s = xh8 >> 10;
-#pragma unroll
-            for (int e = 0; e < 16; ++e) {
-                const int ee = e & 7;
-                const int sh = ee < 5 ? ee : ee - 5;
-                const uint32_t m = 0x00030003u << (2 * sh);
-                const uint32_t b0 = (e < 8 ? (ee < 5 ? xl0 : xl0s) : (ee < 5 ? xh0 : xh0s)) & m;
-                const uint32_t b1 = (e < 8 ? (ee < 5 ? xl8 : xl8s) : (ee < 5 ? xh8 : xh8s)) & m;
-                mma16816(o[e], a, b0, b1, o[e]);
-            }
-        }
+        __syncthreads();  // buffer bi free for the tile after next
     }
     // per-row partials: l, zc summed over the quad; o' = o * 2^(24-2e') - zc
 #pragma unroll
@@ -474,9 +509,7 @@ __global__ void __launch_bounds__(128) prefill_combine_kernel(PrefillParams p) {
 
 }  // namespace
 
-size_t prefill_attn_smem() {
-    return (2 * kQB * kRowH + 2 * kKT * kRowH) * 2 + (kKT * 8 + kKT + 4) * 4;
-}
+size_t prefill_attn_smem() { return static_cast<size_t>(2 * kQB * kRowH) * 2 + 2 * static_cast<size_t>(kTileBytes); }
 
 cudaError_t launch_prefill(const rkv_layer_desc& d, const PrefillParams& p, int64_t max_seq_len, cudaStream_t s) {
     const int C = p.C, W = C / 16, MG = C / 128;
