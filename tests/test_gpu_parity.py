@@ -167,7 +167,7 @@ def oracle_decode(oracle, layer, got, b, T, q, w, perm, kraw, vraw):
 @pytest.mark.parametrize("hq,hkv,g,base,T", [
     (8, 8, 4, 10000.0, 37), (8, 8, 4, 10000.0, 1), (8, 8, 2, 10000.0, 300),
     (32, 8, 2, 500000.0, 129), (4, 4, 1, 10000.0, 64), (40, 40, 4, 10000.0, 200),
-    (16, 8, 4, 10000.0, 77),
+    (16, 8, 4, 10000.0, 77), (32, 32, 4, 10000.0, 1500),
 ])
 def test_decode_vs_oracle(oracle, hq, hkv, g, base, T):
     w = small_workload(hq, hkv, g, base=base)
@@ -260,12 +260,14 @@ def test_decode_deterministic():
     assert torch.equal(a, b)
 
 
-@pytest.mark.parametrize("cfg_id", [2, 3])
+@pytest.mark.parametrize("cfg_id", [2, 3, 4])
 def test_full_size_decode_sampled_vs_oracle(oracle, cfg_id):
     """BASELINE config sizes: the whole batch runs on the GPU; two sampled
-    sequences are checked against the oracle."""
+    sequences are checked against the oracle (cfg3: one 8-sequence shard of
+    the 64; cfg4: the 32768-token context of one GPU's 1-sequence shard,
+    plus a second sequence)."""
     w = WL.CONFIGS[cfg_id]
-    B = w.batch if cfg_id == 2 else 8  # cfg3 batch-sharded: one 8-sequence shard
+    B = {2: w.batch, 3: 8, 4: 2}[cfg_id]
     T = w.tokens
     layer, perm = build_layer(w, B, T + 1, seed=cfg_id)
     k, v = WL.make_kv(w, cfg_id, B, T)
