@@ -228,12 +228,20 @@ __global__ void __launch_bounds__(128) prefill_attn_kernel(PrefillParams p) {
         const uint32_t khs = smem_u32(tb), kls = khs + kKT * kRowH * 2;
         const uint32_t vws = kls + kKT * kRowH * 2, vms = vws + kKT * 8 * 4, mks = vms + kKT * 4;
         const int nk = static_cast<int>(lmin64(kKT, kend - k0));
-        for (int idx = tid; idx < kKT * 16; idx += 128) {
-            const int kk = idx >> 4, ch = (idx & 15) * 8;
-            const int64_t src = (row0 + k0 + (kk < nk ? kk : 0)) * C + kvh * 128 + ch;
-            const uint32_t nb = kk < nk ? 16u : 0u;
-            cp_async16(khs + (kk * kRowH + ch) * 2, p.kr_hi + src, nb);
-            cp_async16(kls + (kk * kRowH + ch) * 2, p.kr_lo + src, nb);
+        {
+            // thread -> chunk column (tid & 15) of key rows (tid >> 4) + 8 i
+            const int ch = (tid & 15) * 8, kr0 = tid >> 4;
+            const uint16_t* sh = p.kr_hi + (row0 + k0) * C + kvh * 128 + ch;
+            const uint16_t* sl = p.kr_lo + (row0 + k0) * C + kvh * 128 + ch;
+            const uint32_t dofs = (kr0 * kRowH + ch) * 2;
+#pragma unroll
+            for (int i = 0; i < kKT / 8; ++i) {
+                const int kk = kr0 + 8 * i;
+                const int64_t so = static_cast<int64_t>(kk < nk ? kk : 0) * C;
+                const uint32_t nb = kk < nk ? 16u : 0u;
+                cp_async16(khs + dofs + i * 8 * kRowH * 2, sh + so, nb);
+                cp_async16(kls + dofs + i * 8 * kRowH * 2, sl + so, nb);
+            }
         }
         if (tid < kKT * 2) {  // V words: 8 per key = two 16-byte chunks
             const int kk = tid >> 1;
@@ -325,19 +333,26 @@ __global__ void __launch_bounds__(128) prefill_attn_kernel(PrefillParams p) {
                     }
                 }
             }
-            // mask (causal, length, sinks) and online softmax for rows g, g+8
+            // mask (causal, length, sinks) -- only tiles that need it: the warp's
+            // first row sees the whole tile, no sink in it, tile full
             float mx[2] = {-INFINITY, -INFINITY};
+            const bool full = nk == kKT && mbits == 0u && k0 + kKT - 1 <= qpos0 + wr;
+            if (!full) {
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const int kk = nt * 8 + 2 * tl + (c & 1);
+                        const int64_t kp = k0 + kk;
+                        const int64_t qp = (c >> 1) ? qp_b : qp_a;
+                        const bool ok = kk < nk && kp <= qp && !((mbits >> kk) & 1u);
+                        s[nt][c] = ok ? s[nt][c] : -INFINITY;
+                    }
+            }
 #pragma unroll
             for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    const int kk = nt * 8 + 2 * tl + (c & 1);
-                    const int64_t kp = k0 + kk;
-                    const int64_t qp = (c >> 1) ? qp_b : qp_a;
-                    const bool ok = kk < nk && kp <= qp && !((mbits >> kk) & 1u);
-                    s[nt][c] = ok ? s[nt][c] : -INFINITY;
-                    mx[c >> 1] = fmaxf(mx[c >> 1], s[nt][c]);
-                }
+                for (int c = 0; c < 4; ++c) mx[c >> 1] = fmaxf(mx[c >> 1], s[nt][c]);
             float alpha[2];
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
