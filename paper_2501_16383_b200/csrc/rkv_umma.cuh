@@ -1,0 +1,107 @@
+// rkv_umma.cuh -- thin sm_100a wrappers for the 5th-generation tensor cores
+// (tcgen05.mma with operands in shared memory, accumulators in tensor memory)
+// used by the prefill attention kernel.
+//
+// Shared-memory operands use the canonical K-major SWIZZLE_128B layout: an
+// operand row (M or N index) holds 64 fp16 K elements = 128 bytes, rows are
+// consecutive, and the 16-byte chunk c of row r sits at chunk c ^ (r & 7)
+// (1024-byte atoms of 8 rows, 1024-byte aligned).  K beyond 64 lives in a
+// second "slab" of the same shape.  One MMA consumes K = 16 (32 bytes): the
+// k-th step inside a slab advances the descriptor's start address by 32 k
+// bytes and the hardware applies the XOR on the final address.
+#pragma once
+
+#include <cstdint>
+
+#include "rkv_common.cuh"
+
+namespace rkv {
+namespace umma {
+
+// byte offset of (row r, 16-byte chunk c) in a K-major SWIZZLE_128B slab
+__host__ __device__ __forceinline__ uint32_t sw128(uint32_t r, uint32_t c) { return (r << 7) + (((c ^ r) & 7u) << 4); }
+
+// shared-memory matrix descriptor: start address, LBO (unused for swizzled
+// K-major: 1), SBO = 1024 (next 8-row group), version 1, SWIZZLE_128B (2)
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
+    uint64_t d = static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4);
+    d |= static_cast<uint64_t>(1u) << 16;              // LBO (16-byte units)
+    d |= static_cast<uint64_t>(1024u >> 4) << 32;      // SBO
+    d |= static_cast<uint64_t>(1u) << 46;              // descriptor version (sm_100)
+    d |= static_cast<uint64_t>(2u) << 61;              // SWIZZLE_128B
+    return d;
+}
+
+// instruction descriptor, kind::f16: A = B = fp16, D = fp32, both K-major
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+    return (1u << 4)                                   // D format F32
+           | (0u << 7) | (0u << 10)                    // A, B = F16
+           | (static_cast<uint32_t>(N >> 3) << 17)     // N / 8
+           | (static_cast<uint32_t>(M >> 4) << 24);    // M / 16
+}
+
+// D[tmem] (+)= A[smem] . B[smem]^T   (issued by one thread)
+__device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n.reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+// arrive on `bar` once every tcgen05 operation this thread issued so far completed
+__device__ __forceinline__ void commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// generic-proxy shared-memory writes -> visible to the tensor core (async proxy)
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// warp-wide TMEM allocation; the base address lands in *slot (shared memory)
+template <int kCols>
+__device__ __forceinline__ void alloc(uint32_t* slot) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)), "n"(kCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+template <int kCols>
+__device__ __forceinline__ void dealloc(uint32_t taddr) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols) : "memory");
+}
+
+// 32 lanes x 32 bit x 16 columns: thread i of the warp gets TMEM lane
+// (32 (warp % 4) + i), columns [col, col + 16)
+__device__ __forceinline__ void ld16(uint32_t taddr, uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+          "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void st16(uint32_t taddr, const uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+        "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
+}
+__device__ __forceinline__ void wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred;
+    asm volatile(
+        "{\n.reg .pred p;\n.reg .b32 r;\n"
+        "elect.sync r|p, 0xffffffff;\n"
+        "selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(pred));
+    return pred != 0;
+}
+
+}  // namespace umma
+}  // namespace rkv
