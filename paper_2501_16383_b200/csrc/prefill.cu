@@ -28,6 +28,7 @@
 #include "rkv_internal.h"
 #include "rkv_layout.h"
 #include "rkv_mma.cuh"
+#include "rkv_umma.cuh"
 
 namespace rkv {
 
@@ -40,6 +41,24 @@ constexpr int kRopeRowF4 = 128;  // float4 per position-pair row of the RoPE tab
 __device__ __forceinline__ float2 rope_cs(const float4* t, int64_t pos, int f) {
     const float4 r = __ldg(t + (pos >> 1) * kRopeRowF4 + f);
     return (pos & 1) ? make_float2(r.y, r.w) : make_float2(r.x, r.z);
+}
+
+// operand tile of (sequence b, KV head, 64-key tile): K hi slabs [0, 16K),
+// K lo slabs [16K, 32K), V^T [32K, 48K)
+__device__ __forceinline__ unsigned char* kv_tile(const PrefillParams& p, int b, int kvh, int64_t j) {
+    return p.kv_tiles + ((static_cast<int64_t>(b) * p.Hkv + kvh) * p.kv_tiles_per_seq + j) * kPrefillTileBytes;
+}
+
+// channels d, d + 1 (d even) of key `pos`, split into fp16 hi + lo, at their
+// K-major SWIZZLE_128B position (slab d / 64, row pos % 64)
+__device__ __forceinline__ void store_key_pair(const PrefillParams& p, int b, int64_t pos, int kvh, int d, float x0,
+                                               float x1) {
+    unsigned char* t = kv_tile(p, b, kvh, pos >> 6);
+    const uint32_t off = static_cast<uint32_t>(d >> 6) * 8192u + umma::sw128(static_cast<uint32_t>(pos & 63), (d & 63) >> 3) +
+                         static_cast<uint32_t>(d & 7) * 2u;
+    const uint32_t h = pack_h2(x0, x1);
+    *reinterpret_cast<uint32_t*>(t + off) = h;
+    *reinterpret_cast<uint32_t*>(t + 16384 + off) = pack_h2(sub_lo(x0, h), sub_hi(x1, h));
 }
 
 // ------------------------------------------------------------------ 1. keys
@@ -96,8 +115,6 @@ __global__ void __launch_bounds__(512) reconstruct_keys_kernel(PrefillParams p) 
     const float kn = p.k_norm;
     const int swz = mma_swz(N, lane);
     const unsigned char* lbase = knat + gam * N * 4 + lane * NJ * 16;
-    uint16_t* khi = p.kr_hi + row0 * C;
-    uint16_t* klo = p.kr_lo + row0 * C;
     for (int pq = 0; pq < 2; ++pq) {
         uint32_t bf[2][NJ][2];
 #pragma unroll
@@ -148,12 +165,8 @@ __global__ void __launch_bounds__(512) reconstruct_keys_kernel(PrefillParams p) 
                             ka[i] = (a * u + bb * w) * kn;  // RoPE(H_2 (a', b')) channel f
                             kb[i] = (a * w - bb * u) * kn;  // channel f + 64
                         }
-                        const int64_t o0 = tt * static_cast<int64_t>(C) + kvh * 128 + f;
-                        const uint32_t ha = pack_h2(ka[0], ka[1]), hb = pack_h2(kb[0], kb[1]);
-                        *reinterpret_cast<uint32_t*>(khi + o0) = ha;
-                        *reinterpret_cast<uint32_t*>(khi + o0 + 64) = hb;
-                        *reinterpret_cast<uint32_t*>(klo + o0) = pack_h2(sub_lo(ka[0], ha), sub_hi(ka[1], ha));
-                        *reinterpret_cast<uint32_t*>(klo + o0 + 64) = pack_h2(sub_lo(kb[0], hb), sub_hi(kb[1], hb));
+                        store_key_pair(p, b, pos, kvh, f, ka[0], ka[1]);
+                        store_key_pair(p, b, pos, kvh, f + 64, kb[0], kb[1]);
                     }
                 } else {
                     const uint32_t h0 = pack_h2(yf[0][2 * f1], yf[0][2 * f1 + 1]);
@@ -172,281 +185,352 @@ __global__ void __launch_bounds__(512) reconstruct_keys_kernel(PrefillParams p) 
                         ka[i] = (a * c - bb * s) * kn;
                         kb[i] = (a * s + bb * c) * kn;
                     }
-                    const int64_t o0 = tt * static_cast<int64_t>(C) + kvh * 128 + f;
-                    const uint32_t ha = pack_h2(ka[0], ka[1]), hb = pack_h2(kb[0], kb[1]);
-                    *reinterpret_cast<uint32_t*>(khi + o0) = ha;
-                    *reinterpret_cast<uint32_t*>(khi + o0 + 64) = hb;
-                    *reinterpret_cast<uint32_t*>(klo + o0) = pack_h2(sub_lo(ka[0], ha), sub_hi(ka[1], ha));
-                    *reinterpret_cast<uint32_t*>(klo + o0 + 64) = pack_h2(sub_lo(kb[0], hb), sub_hi(kb[1], hb));
+                    store_key_pair(p, b, pos, kvh, f, ka[0], ka[1]);
+                    store_key_pair(p, b, pos, kvh, f + 64, kb[0], kb[1]);
                 }
             }
         }
     }
 }
 
-// -------------------------------------------------------------- 2. attention
-constexpr int kQB = 64, kKT = 32, kRowH = 136;  // queries per CTA, keys per tile, padded smem row (halves)
-// one K/V tile buffer: K hi + lo rows, V words of the KV head, V meta words, sink-mask word
-constexpr int kTileBytes = 2 * kKT * kRowH * 2 + kKT * 8 * 4 + kKT * 4 + 16;
-
-__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], uint32_t addr) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-                 : "r"(addr));
-}
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
-}
-__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src, uint32_t src_bytes) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-__global__ void __launch_bounds__(128) prefill_attn_kernel(PrefillParams p) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    uint16_t* qhi = reinterpret_cast<uint16_t*>(smem);  // [64][136]
-    uint16_t* qlo = qhi + kQB * kRowH;
-    unsigned char* tiles = reinterpret_cast<unsigned char*>(qlo + kQB * kRowH);  // 2 x kTileBytes
-
-    const int qb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, tl = lane & 3;
-    const int C = p.C, W = C / 16, MG = C / 128, Hq = p.Hq, REP = p.Hq / p.Hkv;
-    const int kvh = h / REP;
-    const int64_t nq = p.num_q, i0 = static_cast<int64_t>(qb) * kQB;
-    const int nrows = static_cast<int>(lmin64(kQB, nq - i0));
-    const int64_t qpos0 = p.q_start[b] + i0;
-    const int64_t T = p.seq_len[b];
-    const int64_t row0 = static_cast<int64_t>(b) * p.max_tokens;
-    const uint32_t* smask = p.cache.sink_mask + static_cast<int64_t>(b) * ((p.max_tokens + 31) / 32);
-    const int64_t kend = lmin64(T, qpos0 + nrows);  // keys [0, kend)
-
-    // K/V tile k0 -> buffer bi, cp.async (rows past the end are zero-filled)
-    auto issue = [&](int bi, int64_t k0) {
-        unsigned char* tb = tiles + bi * kTileBytes;
-        const uint32_t khs = smem_u32(tb), kls = khs + kKT * kRowH * 2;
-        const uint32_t vws = kls + kKT * kRowH * 2, vms = vws + kKT * 8 * 4, mks = vms + kKT * 4;
-        const int nk = static_cast<int>(lmin64(kKT, kend - k0));
-        {
-            // thread -> chunk column (tid & 15) of key rows (tid >> 4) + 8 i
-            const int ch = (tid & 15) * 8, kr0 = tid >> 4;
-            const uint16_t* sh = p.kr_hi + (row0 + k0) * C + kvh * 128 + ch;
-            const uint16_t* sl = p.kr_lo + (row0 + k0) * C + kvh * 128 + ch;
-            const uint32_t dofs = (kr0 * kRowH + ch) * 2;
+// ---------------------------------------------------------------- 2. values
+// V^T tile of (sequence, KV head, 64 keys): the dequantized rotated values
+// s (c - z), rounded once to fp16 (the decode kernels' operand rounding),
+// [128 channels][64 keys] K-major SWIZZLE_128B; keys >= seq_len are zero.
+// Thread t: code word w = t >> 4 (channels 16w..16w+15), keys 8kc..8kc+7
+// (kc = (t >> 1) & 7), codes 8 (t & 1) .. + 7 of the word.
+__global__ void __launch_bounds__(128) reconstruct_values_kernel(PrefillParams p) {
+    const int64_t j = blockIdx.x;
+    const int kvh = blockIdx.y, b = blockIdx.z, t = threadIdx.x;
+    const int W = p.C / 16, MG = p.C / 128;
+    const int w = t >> 4, kc = (t >> 1) & 7, e0 = 8 * (t & 1);
+    const int64_t T = p.seq_len[b], row0 = static_cast<int64_t>(b) * p.max_tokens;
+    uint32_t cw[8];
+    float sc[8], zr[8];
 #pragma unroll
-            for (int i = 0; i < kKT / 8; ++i) {
-                const int kk = kr0 + 8 * i;
-                const int64_t so = static_cast<int64_t>(kk < nk ? kk : 0) * C;
-                const uint32_t nb = kk < nk ? 16u : 0u;
-                cp_async16(khs + dofs + i * 8 * kRowH * 2, sh + so, nb);
-                cp_async16(kls + dofs + i * 8 * kRowH * 2, sl + so, nb);
+    for (int i = 0; i < 8; ++i) {
+        const int64_t key = j * kPrefillKT + 8 * kc + i;
+        const bool ok = key < T;
+        cw[i] = ok ? __ldg(p.cache.v_codes + (row0 + key) * W + kvh * 8 + w) : 0u;
+        const uint32_t m = ok ? __ldg(p.cache.v_meta + (row0 + key) * MG + kvh) : 0u;
+        sc[i] = h2f(static_cast<uint16_t>(m & 0xffffu));
+        zr[i] = h2f(static_cast<uint16_t>(m >> 16));
+    }
+    unsigned char* vt = kv_tile(p, b, kvh, j) + 32768;
+#pragma unroll
+    for (int e = e0; e < e0 + 8; ++e) {
+        uint32_t h[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float c0 = static_cast<float>((cw[2 * i] >> (2 * e)) & 3u), c1 = static_cast<float>((cw[2 * i + 1] >> (2 * e)) & 3u);
+            h[i] = pack_h2(sc[2 * i] * (c0 - zr[2 * i]), sc[2 * i + 1] * (c1 - zr[2 * i + 1]));
+        }
+        *reinterpret_cast<uint4*>(vt + umma::sw128(static_cast<uint32_t>(16 * w + e), static_cast<uint32_t>(kc))) =
+            make_uint4(h[0], h[1], h[2], h[3]);
+    }
+}
+
+// ------------------------------------------------------------- 3. attention
+// Flash attention on the 5th-generation tensor cores.  CTA = (sequence, q
+// head, 128 query rows); 8 warps: warp 0 streams the operand tiles
+// (cp.async.bulk; keys 3 tiles deep, values 2), warp 1 (one elected lane)
+// issues tcgen05.mma, warps 2-7 stage the query block, then warps 4-7 run
+// the softmax with one query row per thread (TMEM lane = row).  Per 64-key
+// tile j:
+//   S_j (TMEM, double-buffered) = Qhi Khi^T + Qhi Klo^T + Qlo Khi^T
+//     (M = 128, N = 64, 3 x 8 K-steps; ~2^-22 relative, as the mma.sync path),
+//   softmax: causal / length / sink mask, running max with lazy rescale (O in
+//     TMEM is rescaled only when a row's max grows by more than 2^14), P = 2^(S - m)
+//     as fp16 into shared memory (K-major SWIZZLE_128B, double-buffered),
+//   O (TMEM, 128 x 128 fp32) += P V_j (M = 128, N = 128, 4 K-steps).
+// The MMA lane issues QK(j + 1) before PV(j), so S_{j+1} is ready when the
+// softmax of tile j ends and the tensor core runs PV(j) + QK(j + 2) under the
+// softmax of tile j + 1.  Every hand-off is an mbarrier (TMA transaction
+// bytes, tcgen05.commit, or the 128 / 192 arrivals of the softmax / staging
+// threads).
+constexpr int kQR = 128, kAttnThreads = 256, kKSlots = 3, kVSlots = 2;
+constexpr uint32_t kQSlab = 16384, kKSlab = 8192, kKTile = 32768, kVTile = 16384, kPBuf = 16384;
+constexpr uint32_t kOffQlo = 2 * kQSlab, kOffK = 4 * kQSlab, kOffV = kOffK + kKSlots * kKTile,
+                   kOffP = kOffV + kVSlots * kVTile, kOffBar = kOffP + 2 * kPBuf;
+constexpr size_t kAttnSmem = kOffBar + 192 + 1024;  // + barriers, + alignment slack
+constexpr float kLazy = 14.0f;                       // rescale O only when the max grows by > 2^14 (P <= 2^14 in fp16)
+constexpr int kStageThreads = kAttnThreads - 64;     // warps 2-7 stage the query block
+
+__global__ void __launch_bounds__(kAttnThreads, 1) prefill_attn_kernel(PrefillParams p) {
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // 1024-byte aligned
+    const uint32_t sbase = smem_u32(smem);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kOffBar);
+    uint64_t *kfull = bar, *kempty = bar + 3, *vfull = bar + 6, *vempty = bar + 8, *s_full = bar + 10,
+             *s_free = bar + 12, *p_full = bar + 14, *pv_done = bar + 16, *q_full = bar + 18;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 19);
+
+    const int qb = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, b = blockIdx.z;  // heaviest query blocks first
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int REP = p.Hq / p.Hkv, kvh = h / REP;
+    const int64_t nq = p.num_q, i0 = static_cast<int64_t>(qb) * kQR;
+    const int nrows = static_cast<int>(lmin64(kQR, nq - i0));
+    const int64_t q0 = p.q_start[b] + i0, T = p.seq_len[b];
+    const int64_t kend = lmin64(T, q0 + nrows);
+    const int nt = kend > 0 ? static_cast<int>((kend + kPrefillKT - 1) / kPrefillKT) : 0;
+
+    if (tid == 0) {
+        for (int i = 0; i < kKSlots; ++i) {
+            mbar_init(kfull + i, 1);
+            mbar_init(kempty + i, 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(vfull + i, 1);
+            mbar_init(vempty + i, 1);
+            mbar_init(s_full + i, 1);
+            mbar_init(s_free + i, 128);
+            mbar_init(p_full + i, 128);
+            mbar_init(pv_done + i, 1);
+        }
+        mbar_init(q_full, kStageThreads);
+        mbar_fence_init();
+    }
+    if (warp == 1) umma::alloc<256>(tslot);
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+    const uint32_t tmem = *tslot;  // S_0: columns [0, 64), S_1: [64, 128), O: [128, 256)
+
+    if (warp == 0) {
+        // ---- producer: K(j + 2) runs ahead of V(j)
+        if (umma::elect_one()) {
+            auto load_k = [&](int j) {
+                const int sl = j % kKSlots;
+                if (j >= kKSlots) mbar_wait_sleep(kempty + sl, ((j / kKSlots) - 1) & 1);
+                const unsigned char* src = kv_tile(p, b, kvh, j);
+                unsigned char* dst = smem + kOffK + sl * kKTile;
+                mbar_arrive_expect_tx(kfull + sl, kKTile);
+                bulk_g2s(dst, src, kKTile / 2, kfull + sl);
+                bulk_g2s(dst + kKTile / 2, src + kKTile / 2, kKTile / 2, kfull + sl);
+            };
+            auto load_v = [&](int j) {
+                const int sl = j & 1;
+                if (j >= kVSlots) mbar_wait_sleep(vempty + sl, ((j >> 1) - 1) & 1);
+                mbar_arrive_expect_tx(vfull + sl, kVTile);
+                bulk_g2s(smem + kOffV + sl * kVTile, kv_tile(p, b, kvh, j) + kKTile, kVTile, vfull + sl);
+            };
+            if (nt > 0) load_k(0);
+            if (nt > 1) load_k(1);
+            for (int j = 0; j < nt; ++j) {
+                if (j + 2 < nt) load_k(j + 2);
+                load_v(j);
             }
         }
-        if (tid < kKT * 2) {  // V words: 8 per key = two 16-byte chunks
-            const int kk = tid >> 1;
-            const int64_t src = (row0 + k0 + (kk < nk ? kk : 0)) * W + kvh * 8 + (tid & 1) * 4;
-            cp_async16(vws + tid * 16, p.cache.v_codes + src, kk < nk ? 16u : 0u);
-        } else if (tid < kKT * 3) {  // V meta word of the KV head
-            const int kk = tid - kKT * 2;
-            cp_async4(vms + kk * 4, p.cache.v_meta + (row0 + k0 + (kk < nk ? kk : 0)) * MG + kvh, kk < nk ? 4u : 0u);
-        } else if (tid == kKT * 3) {
-            cp_async4(mks, smask + (k0 >> 5), 4u);  // k0 % 32 == 0
+        __syncwarp();
+    } else if (warp == 1) {
+        // ---- MMA issuer
+        if (umma::elect_one()) {
+            constexpr uint32_t idS = umma::idesc_f16(128, 64), idO = umma::idesc_f16(128, 128);
+            mbar_wait_sleep(q_full, 0);
+            auto qk = [&](int j) {
+                const int sl = j % kKSlots, sb = j & 1;
+                mbar_wait_sleep(kfull + sl, (j / kKSlots) & 1);
+                if (j >= 2) mbar_wait_sleep(s_free + sb, ((j >> 1) - 1) & 1);
+                umma::fence_after();
+                const uint32_t d = tmem + 64u * sb, kb = sbase + kOffK + sl * kKTile;
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks) {
+                    const uint32_t qo = (ks >> 2) * kQSlab + (ks & 3) * 32, ko = (ks >> 2) * kKSlab + (ks & 3) * 32;
+                    const uint64_t ah = umma::sdesc(sbase + qo), al = umma::sdesc(sbase + kOffQlo + qo);
+                    const uint64_t bh = umma::sdesc(kb + ko), bl = umma::sdesc(kb + 2 * kKSlab + ko);
+                    umma::mma_f16(d, ah, bh, idS, ks > 0);
+                    umma::mma_f16(d, ah, bl, idS, 1);
+                    umma::mma_f16(d, al, bh, idS, 1);
+                }
+                umma::commit(s_full + sb);
+                umma::commit(kempty + sl);
+            };
+            auto pv = [&](int j) {
+                const int sb = j & 1;
+                mbar_wait_sleep(vfull + sb, (j >> 1) & 1);
+                mbar_wait_sleep(p_full + sb, (j >> 1) & 1);
+                umma::fence_after();
+                const uint32_t pa = sbase + kOffP + sb * kPBuf, vb = sbase + kOffV + sb * kVTile;
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)
+                    umma::mma_f16(tmem + 128, umma::sdesc(pa + kk * 32), umma::sdesc(vb + kk * 32), idO, (j > 0 || kk > 0));
+                umma::commit(vempty + sb);
+                umma::commit(pv_done + sb);
+            };
+            if (nt > 0) qk(0);
+            for (int j = 0; j < nt; ++j) {
+                if (j + 1 < nt) qk(j + 1);
+                pv(j);
+            }
         }
-        cp_async_commit();
-    };
-    if (kend > 0) issue(0, 0);
-
-    // q: RoPE at each row's position, x log2(e)/sqrt(d), split into fp16 hi + lo
-    for (int idx = tid; idx < kQB * 64; idx += blockDim.x) {
-        const int r = idx >> 6, f = idx & 63;
-        float qa = 0.f, qb2 = 0.f;
-        if (r < nrows) {
-            const uint16_t* qr = p.q + ((static_cast<int64_t>(b) * nq + i0 + r) * Hq + h) * 128;
-            const float a = h2f(qr[f]), bb = h2f(qr[f + 64]);
-            const float2 cs = rope_cs(p.rope, qpos0 + r, f);
-            qa = (a * cs.x - bb * cs.y) * p.qscale;
-            qb2 = (a * cs.y + bb * cs.x) * p.qscale;
+        __syncwarp();
+    } else {
+        // ---- warps 2-7: the query block, RoPE at each row's position,
+        // x log2(e)/sqrt(d), fp16 hi + lo; item = (row, 8 frequencies)
+        for (int idx = tid - 64; idx < kQR * 8; idx += kStageThreads) {
+            const int r = idx >> 3, c = idx & 7, f = 8 * c;
+            float qa[8], qv[8];
+            if (r < nrows) {
+                const uint16_t* qr = p.q + ((static_cast<int64_t>(b) * nq + i0 + r) * p.Hq + h) * 128;
+                const uint4 ua = *reinterpret_cast<const uint4*>(qr + f), ub = *reinterpret_cast<const uint4*>(qr + f + 64);
+                const uint16_t* ha = reinterpret_cast<const uint16_t*>(&ua);
+                const uint16_t* hb = reinterpret_cast<const uint16_t*>(&ub);
+                const int64_t pos = q0 + r;
+                const float4* rr = p.rope + (pos >> 1) * kRopeRowF4 + f;
+                const bool odd = pos & 1;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const float4 r4 = __ldg(rr + i);
+                    const float cs = odd ? r4.y : r4.x, sn = odd ? r4.w : r4.z;
+                    const float a = h2f(ha[i]), bb = h2f(hb[i]);
+                    qa[i] = (a * cs - bb * sn) * p.qscale;
+                    qv[i] = (a * sn + bb * cs) * p.qscale;
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) qa[i] = qv[i] = 0.f;
+            }
+            uint32_t hia[4], loa[4], hib[4], lob[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                hia[i] = pack_h2(qa[2 * i], qa[2 * i + 1]);
+                loa[i] = pack_h2(sub_lo(qa[2 * i], hia[i]), sub_hi(qa[2 * i + 1], hia[i]));
+                hib[i] = pack_h2(qv[2 * i], qv[2 * i + 1]);
+                lob[i] = pack_h2(sub_lo(qv[2 * i], hib[i]), sub_hi(qv[2 * i + 1], hib[i]));
+            }
+            const uint32_t off = umma::sw128(static_cast<uint32_t>(r), static_cast<uint32_t>(c));
+            *reinterpret_cast<uint4*>(smem + off) = make_uint4(hia[0], hia[1], hia[2], hia[3]);
+            *reinterpret_cast<uint4*>(smem + kQSlab + off) = make_uint4(hib[0], hib[1], hib[2], hib[3]);
+            *reinterpret_cast<uint4*>(smem + kOffQlo + off) = make_uint4(loa[0], loa[1], loa[2], loa[3]);
+            *reinterpret_cast<uint4*>(smem + kOffQlo + kQSlab + off) = make_uint4(lob[0], lob[1], lob[2], lob[3]);
         }
-        const __half ha = __float2half_rn(qa), hb = __float2half_rn(qb2);
-        qhi[r * kRowH + f] = __half_as_ushort(ha);
-        qhi[r * kRowH + f + 64] = __half_as_ushort(hb);
-        qlo[r * kRowH + f] = __half_as_ushort(__float2half_rn(qa - __half2float(ha)));
-        qlo[r * kRowH + f + 64] = __half_as_ushort(__float2half_rn(qb2 - __half2float(hb)));
-    }
+        umma::fence_proxy_async();
+        mbar_arrive(q_full);
 
-    const int wr = warp * 16;  // this warp's first row
-    const int64_t qp_a = qpos0 + wr + g, qp_b = qp_a + 8;
-    const int64_t warp_last = qpos0 + std::min(wr + 15, nrows - 1);
-    float m_r[2] = {-INFINITY, -INFINITY}, l_r[2] = {0.f, 0.f}, zc_r[2] = {0.f, 0.f};
-    float o[16][4];
+        if (warp >= 4) {
+            // ---- softmax: one query row per thread
+            const int row = 32 * (warp - 4) + lane;
+            const int64_t qpos = q0 + row;
+            const uint32_t lrow = static_cast<uint32_t>(32 * (warp - 4)) << 16;
+            const uint32_t* smask = p.cache.sink_mask + static_cast<int64_t>(b) * ((p.max_tokens + 31) / 32);
+            float m = -INFINITY, l = 0.f;
+            for (int j = 0; j < nt; ++j) {
+                const int sb = j & 1;
+                mbar_wait(s_full + sb, (j >> 1) & 1);
+                umma::fence_after();
+                uint32_t v[4][16];
 #pragma unroll
-    for (int e = 0; e < 16; ++e)
+                for (int c = 0; c < 4; ++c) umma::ld16(tmem + lrow + 64u * sb + 16u * c, v[c]);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) o[e][c] = 0.f;
-    // ldmatrix lane addresses: A (Q rows wr.., matrices (r0-7,c0-7),(r8-15,c0-7),(r0-7,c8-15),(r8-15,c8-15));
-    // B (K rows = keys: (k0-7,c0-7),(k0-7,c8-15),(k8-15,c0-7),(k8-15,c8-15) -> two n-tiles)
-    const int mi = lane >> 3, mr = lane & 7;
-    const uint32_t qa_hi = smem_u32(qhi + (wr + mr + 8 * (mi & 1)) * kRowH + 8 * (mi >> 1));
-    const uint32_t qa_lo = qa_hi + kQB * kRowH * 2;
-    const uint32_t kb_off = ((mr + 8 * (mi >> 1)) * kRowH + 8 * (mi & 1)) * 2;
-
-    int bi = 0;
-    for (int64_t k0 = 0; k0 < kend; k0 += kKT, bi ^= 1) {
-        if (k0 + kKT < kend) {
-            issue(bi ^ 1, k0 + kKT);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncthreads();  // tile k0 (and the q tile) visible
-        const unsigned char* tb = tiles + bi * kTileBytes;
-        const uint32_t khs = smem_u32(tb), kls = khs + kKT * kRowH * 2;
-        const uint32_t* vws = reinterpret_cast<const uint32_t*>(tb + 2 * kKT * kRowH * 2);
-        const uint32_t* vms = vws + kKT * 8;
-        const uint32_t mbits = vms[kKT];
-        const int nk = static_cast<int>(lmin64(kKT, kend - k0));
-        if (!(k0 > warp_last || wr >= nrows)) {
-            // S = Q K^T (16 rows x 32 keys), fp16 hi/lo split on both operands
-            float s[4][4];
+                for (int c = 0; c < 4; ++c) umma::wait_ld(v[c]);
+                umma::fence_before();
+                mbar_arrive(s_free + sb);
+                float s[64];
 #pragma unroll
-            for (int nt = 0; nt < 4; ++nt)
+                for (int c = 0; c < 64; ++c) s[c] = __uint_as_float(v[c >> 4][c & 15]);
+                const int64_t k0 = static_cast<int64_t>(j) * kPrefillKT;
+                const uint32_t sm0 = __ldg(smask + (k0 >> 5)), sm1 = __ldg(smask + (k0 >> 5) + 1);
+                if (k0 + kPrefillKT - 1 > q0 || k0 + kPrefillKT > T || (sm0 | sm1)) {
+                    const int64_t lim = lmin64(qpos + 1, T) - k0;  // keys k0 + c, c < lim, are in range
 #pragma unroll
-                for (int c = 0; c < 4; ++c) s[nt][c] = 0.f;
-#pragma unroll
-            for (int ks = 0; ks < 8; ++ks) {
-                uint32_t ah[4], al[4];
-                ldsm_x4(ah, qa_hi + ks * 32);
-                ldsm_x4(al, qa_lo + ks * 32);
-#pragma unroll
-                for (int np = 0; np < 2; ++np) {  // n-tile pairs (2np, 2np+1)
-                    uint32_t bh[4], bl[4];
-                    const uint32_t off = kb_off + (np * 16 * kRowH + ks * 16) * 2;
-                    ldsm_x4(bh, khs + off);
-                    ldsm_x4(bl, kls + off);
-#pragma unroll
-                    for (int j = 0; j < 2; ++j) {
-                        float (&acc)[4] = s[2 * np + j];
-                        mma16816(acc, ah, bh[2 * j], bh[2 * j + 1], acc);
-                        mma16816(acc, ah, bl[2 * j], bl[2 * j + 1], acc);
-                        mma16816(acc, al, bh[2 * j], bh[2 * j + 1], acc);
+                    for (int c = 0; c < 64; ++c) {
+                        const bool sink = ((c < 32 ? sm0 : sm1) >> (c & 31)) & 1u;
+                        s[c] = (c < lim && !sink) ? s[c] : -INFINITY;
                     }
                 }
-            }
-            // mask (causal, length, sinks) -- only tiles that need it: the warp's
-            // first row sees the whole tile, no sink in it, tile full
-            float mx[2] = {-INFINITY, -INFINITY};
-            const bool full = nk == kKT && mbits == 0u && k0 + kKT - 1 <= qpos0 + wr;
-            if (!full) {
+                float mx8[8];
 #pragma unroll
-                for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        const int kk = nt * 8 + 2 * tl + (c & 1);
-                        const int64_t kp = k0 + kk;
-                        const int64_t qp = (c >> 1) ? qp_b : qp_a;
-                        const bool ok = kk < nk && kp <= qp && !((mbits >> kk) & 1u);
-                        s[nt][c] = ok ? s[nt][c] : -INFINITY;
+                for (int i = 0; i < 8; ++i) {
+                    mx8[i] = fmaxf(fmaxf(s[i], s[i + 8]), s[i + 16]);
+                    mx8[i] = fmaxf(fmaxf(mx8[i], s[i + 24]), s[i + 32]);
+                    mx8[i] = fmaxf(fmaxf(mx8[i], s[i + 40]), s[i + 48]);
+                    mx8[i] = fmaxf(mx8[i], s[i + 56]);
+                }
+                const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                       fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+                float alpha = 1.0f;
+                bool resc = false;
+                if (mx != -INFINITY) {
+                    if (m == -INFINITY) {
+                        m = mx;
+                    } else if (mx > m + kLazy) {
+                        alpha = ex2(m - mx);
+                        m = mx;
+                        resc = true;
                     }
-            }
-#pragma unroll
-            for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-                for (int c = 0; c < 4; ++c) mx[c >> 1] = fmaxf(mx[c >> 1], s[nt][c]);
-            float alpha[2];
-#pragma unroll
-            for (int r = 0; r < 2; ++r) {
-                mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
-                mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
-                const float mn = fmaxf(m_r[r], mx[r]);
-                alpha[r] = mn == -INFINITY ? 1.0f : ex2(m_r[r] - mn);
-                m_r[r] = mn;
-                l_r[r] *= alpha[r];
-                zc_r[r] *= alpha[r];
-            }
-            if (alpha[0] != 1.0f || alpha[1] != 1.0f) {
-#pragma unroll
-                for (int e = 0; e < 16; ++e) {
-                    o[e][0] *= alpha[0];
-                    o[e][1] *= alpha[0];
-                    o[e][2] *= alpha[1];
-                    o[e][3] *= alpha[1];
                 }
-            }
-            // P (x the key's V scale, fp16) as the A operand of P.V; zero point folded per row
-            uint32_t pa[2][4];
+                if (__any_sync(0xffffffffu, resc)) {  // O holds PV(0..j-1): wait for the last one, rescale in TMEM
+                    mbar_wait(pv_done + ((j - 1) & 1), ((j - 1) >> 1) & 1);
+                    umma::fence_after();
+#pragma unroll 1
+                    for (int c = 0; c < 8; ++c) {
+                        uint32_t o[16];
+                        umma::ld16(tmem + lrow + 128u + 16u * c, o);
+                        umma::wait_ld(o);
 #pragma unroll
-            for (int nt = 0; nt < 4; ++nt) {
-                float w[4], zr[4];
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    const int kk = nt * 8 + 2 * tl + (c & 1);
-                    const float pr = s[nt][c] == -INFINITY ? 0.f : ex2(s[nt][c] - m_r[c >> 1]);
-                    l_r[c >> 1] += pr;
-                    const uint32_t vm = pr > 0.f ? vms[kk] : 0u;
-                    w[c] = pr * h2f(static_cast<uint16_t>(vm & 0xffffu));
-                    zr[c] = h2f(static_cast<uint16_t>(vm >> 16));
+                        for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+                        umma::st16(tmem + lrow + 128u + 16u * c, o);
+                    }
+                    umma::wait_st();
+                    l *= alpha;
                 }
-                const uint32_t p01 = pack_h2(w[0], w[1]), p23 = pack_h2(w[2], w[3]);
-                const uint32_t z01 = pack_h2(zr[0], zr[1]), z23 = pack_h2(zr[2], zr[3]);
-                zc_r[0] = fhfma<0, 0>(p01, z01, zc_r[0]);
-                zc_r[0] = fhfma<1, 1>(p01, z01, zc_r[0]);
-                zc_r[1] = fhfma<0, 0>(p23, z23, zc_r[1]);
-                zc_r[1] = fhfma<1, 1>(p23, z23, zc_r[1]);
-                pa[nt >> 1][(nt & 1) * 2 + 0] = p01;  // rows g: keys 2tl..(+8)
-                pa[nt >> 1][(nt & 1) * 2 + 1] = p23;  // rows g+8
-            }
+                const float mu = m == -INFINITY ? 0.f : m;
+                const float2 mu2 = make_float2(mu, mu);
+                float2 ls[4];
+                uint32_t hv[32];
 #pragma unroll
-            for (int kb = 0; kb < 2; ++kb) {
-                const uint32_t a[4] = {pa[kb][0], pa[kb][1], pa[kb][2], pa[kb][3]};
-                const int ka = 16 * kb + 2 * tl;
-                const uint32_t w0 = vws[ka * 8 + g], w1 = vws[(ka + 1) * 8 + g];
-                const uint32_t w8 = vws[(ka + 8) * 8 + g], w9 = vws[(ka + 9) * 8 + g];
-                const uint32_t xl0 = prmt(w0, w1, 0x5410u), xh0 = prmt(w0, w1, 0x7632u);
-                const uint32_t xl8 = prmt(w8, w9, 0x5410u), xh8 = prmt(w8, w9, 0x7632u);
-                const uint32_t xl0s = xl0 >> 10, xh0s = xh0 >> 10, xl8s = xl8 >> 10, xh8s = xh8 >> 10;
-#pragma unroll
-                for (int e = 0; e < 16; ++e) {
-                    const int ee = e & 7;
-                    const int sh = ee < 5 ? ee : ee - 5;
-                    const uint32_t m = 0x00030003u << (2 * sh);
-                    const uint32_t b0 = (e < 8 ? (ee < 5 ? xl0 : xl0s) : (ee < 5 ? xh0 : xh0s)) & m;
-                    const uint32_t b1 = (e < 8 ? (ee < 5 ? xl8 : xl8s) : (ee < 5 ? xh8 : xh8s)) & m;
-                    mma16816(o[e], a, b0, b1, o[e]);
+                for (int i = 0; i < 32; ++i) {
+                    const float2 d = sub2(make_float2(s[2 * i], s[2 * i + 1]), mu2);
+                    const float2 pp = make_float2(ex2(d.x), ex2(d.y));
+                    ls[i & 3] = i < 4 ? pp : add2(ls[i & 3], pp);
+                    hv[i] = pack_h2(pp.x, pp.y);
                 }
+                const float2 lt = add2(add2(ls[0], ls[1]), add2(ls[2], ls[3]));
+                l += lt.x + lt.y;
+                if (j >= 2) mbar_wait(pv_done + sb, ((j >> 1) - 1) & 1);  // PV(j - 2) released this P buffer
+                unsigned char* prow = smem + kOffP + sb * kPBuf;
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    *reinterpret_cast<uint4*>(prow + umma::sw128(static_cast<uint32_t>(row), static_cast<uint32_t>(c))) =
+                        make_uint4(hv[4 * c], hv[4 * c + 1], hv[4 * c + 2], hv[4 * c + 3]);
+                umma::fence_proxy_async();
+                umma::fence_before();
+                mbar_arrive(p_full + sb);
+            }
+            if (row < nrows) {
+                const int64_t orow = (static_cast<int64_t>(b) * nq + i0 + row) * p.Hq + h;
+                p.ws_ml[orow * 2] = m;
+                p.ws_ml[orow * 2 + 1] = l;
+            }
+            float4* dst = reinterpret_cast<float4*>(p.ws_o + ((static_cast<int64_t>(b) * nq + i0 + row) * p.Hq + h) * 128);
+            if (nt > 0) {
+                mbar_wait(pv_done + ((nt - 1) & 1), ((nt - 1) >> 1) & 1);
+                umma::fence_after();
+#pragma unroll 1
+                for (int c = 0; c < 8; ++c) {
+                    uint32_t o[16];
+                    umma::ld16(tmem + lrow + 128u + 16u * c, o);
+                    umma::wait_ld(o);
+                    if (row < nrows)
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+                            dst[4 * c + i] = make_float4(__uint_as_float(o[4 * i]), __uint_as_float(o[4 * i + 1]),
+                                                         __uint_as_float(o[4 * i + 2]), __uint_as_float(o[4 * i + 3]));
+                }
+            } else if (row < nrows) {
+                for (int c = 0; c < 32; ++c) dst[c] = make_float4(0.f, 0.f, 0.f, 0.f);
             }
         }
-        __syncthreads();  // buffer bi free for the tile after next
     }
-    // per-row partials: l, zc summed over the quad; o' = o * 2^(24-2e') - zc
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-        l_r[r] += __shfl_xor_sync(0xffffffffu, l_r[r], 1);
-        l_r[r] += __shfl_xor_sync(0xffffffffu, l_r[r], 2);
-        zc_r[r] += __shfl_xor_sync(0xffffffffu, zc_r[r], 1);
-        zc_r[r] += __shfl_xor_sync(0xffffffffu, zc_r[r], 2);
-    }
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-        const int row = wr + g + 8 * r;
-        if (row >= nrows) continue;
-        const int64_t orow = (static_cast<int64_t>(b) * nq + i0 + row) * Hq + h;
-        if (tl == 0) {
-            p.ws_ml[orow * 2] = m_r[r];
-            p.ws_ml[orow * 2 + 1] = l_r[r];
-        }
-        float* dst = p.ws_o + orow * 128;
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-            const int ee = e & 7, sh = ee < 5 ? ee : ee - 5;
-            const float sc = __int_as_float((127 + 24 - 2 * sh) << 23);
-#pragma unroll
-            for (int c = 0; c < 2; ++c) dst[(2 * tl + c) * 16 + e] = o[e][2 * r + c] * sc - zc_r[r];
-        }
+    umma::fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        umma::fence_after();
+        umma::dealloc<256>(tmem);
     }
 }
 
-// ---------------------------------------------------------------- 3. combine
+// ---------------------------------------------------------------- 4. combine
 __global__ void __launch_bounds__(128) prefill_combine_kernel(PrefillParams p) {
     const int lane = threadIdx.x & 31;
     const int64_t nq = p.num_q;
@@ -524,7 +608,7 @@ __global__ void __launch_bounds__(128) prefill_combine_kernel(PrefillParams p) {
 
 }  // namespace
 
-size_t prefill_attn_smem() { return static_cast<size_t>(2 * kQB * kRowH) * 2 + 2 * static_cast<size_t>(kTileBytes); }
+size_t prefill_attn_smem() { return kAttnSmem; }
 
 cudaError_t launch_prefill(const rkv_layer_desc& d, const PrefillParams& p, int64_t max_seq_len, cudaStream_t s) {
     const int C = p.C, W = C / 16, MG = C / 128;
@@ -547,13 +631,16 @@ cudaError_t launch_prefill(const rkv_layer_desc& d, const PrefillParams& p, int6
         return cudaErrorInvalidValue;
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    const size_t asmem = prefill_attn_smem();
-    if ((e = cudaFuncSetAttribute(prefill_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(asmem))) != cudaSuccess)
-        return e;
-    const dim3 agrid(static_cast<unsigned>((p.num_q + kQB - 1) / kQB), static_cast<unsigned>(p.Hq),
+    const dim3 vgrid(static_cast<unsigned>((max_seq_len + kPrefillKT - 1) / kPrefillKT), static_cast<unsigned>(p.Hkv),
                      static_cast<unsigned>(d.batch));
-    prefill_attn_kernel<<<agrid, 128, asmem, s>>>(p);
+    reconstruct_values_kernel<<<vgrid, 128, 0, s>>>(p);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(prefill_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kAttnSmem))) != cudaSuccess)
+        return e;
+    const dim3 agrid(static_cast<unsigned>((p.num_q + kQR - 1) / kQR), static_cast<unsigned>(p.Hq),
+                     static_cast<unsigned>(d.batch));
+    prefill_attn_kernel<<<agrid, kAttnThreads, kAttnSmem, s>>>(p);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     const int64_t warps = static_cast<int64_t>(d.batch) * p.num_q * p.Hq;
     prefill_combine_kernel<<<static_cast<unsigned>((warps + 3) / 4), 128, 0, s>>>(p);

@@ -402,12 +402,19 @@ rkv_status rkv_decode_attention(const rkv_layer_desc* desc, const uint16_t* q, c
     return RKV_OK;
 }
 
+namespace {
+// reconstructed K (hi, lo) + V tiles: 48 KB per (sequence, KV head, 64 keys)
+size_t prefill_tile_bytes(const rkv_layer_desc& d) {
+    const size_t nt = static_cast<size_t>((d.max_tokens + rkv::kPrefillKT - 1) / rkv::kPrefillKT);
+    return static_cast<size_t>(d.batch) * d.num_kv_heads * nt * rkv::kPrefillTileBytes;
+}
+}  // namespace
+
 size_t rkv_prefill_workspace_bytes(const rkv_layer_desc* desc, int64_t num_q, int64_t max_seq_len) {
     if (validate(desc) != RKV_OK || num_q < 0 || max_seq_len < 0) return 0;
     const size_t C = static_cast<size_t>(desc->num_kv_heads) * desc->head_dim, B = static_cast<size_t>(desc->batch);
     const size_t rows = B * static_cast<size_t>(num_q) * desc->num_q_heads;
-    const size_t keys = B * static_cast<size_t>(desc->max_tokens) * C * 2;  // fp16 per plane
-    return 2 * al256(keys) + al256(rows * 2 * sizeof(float)) + al256(rows * 128 * sizeof(float));
+    return al256(prefill_tile_bytes(*desc)) + al256(rows * 2 * sizeof(float)) + al256(rows * 128 * sizeof(float));
 }
 
 rkv_status rkv_prefill_attention(const rkv_layer_desc* desc, const uint16_t* q, int64_t num_q, const int64_t* q_start,
@@ -429,7 +436,7 @@ rkv_status rkv_prefill_attention(const rkv_layer_desc* desc, const uint16_t* q, 
     if (ws_bytes < rkv_prefill_workspace_bytes(desc, num_q, max_seq_len))
         return fail(RKV_ERR_INVALID_ARGUMENT, "prefill: workspace too small");
     const size_t C = static_cast<size_t>(desc->num_kv_heads) * desc->head_dim, B = static_cast<size_t>(desc->batch);
-    const size_t keys = B * static_cast<size_t>(desc->max_tokens) * C * 2;
+    const size_t tiles = al256(prefill_tile_bytes(*desc));
     const size_t rows = B * static_cast<size_t>(num_q) * desc->num_q_heads;
     char* w = static_cast<char*>(workspace);
     rkv::PrefillParams p{};
@@ -439,10 +446,10 @@ rkv_status rkv_prefill_attention(const rkv_layer_desc* desc, const uint16_t* q, 
     p.plan = static_cast<const uint32_t*>(layer_plan);
     p.rope = reinterpret_cast<const float4*>(rope_table);
     p.cache = *cache;
-    p.kr_hi = reinterpret_cast<uint16_t*>(w);
-    p.kr_lo = reinterpret_cast<uint16_t*>(w + al256(keys));
-    p.ws_ml = reinterpret_cast<float*>(w + 2 * al256(keys));
-    p.ws_o = reinterpret_cast<float*>(w + 2 * al256(keys) + al256(rows * 2 * sizeof(float)));
+    p.kv_tiles = reinterpret_cast<unsigned char*>(w);
+    p.kv_tiles_per_seq = (desc->max_tokens + rkv::kPrefillKT - 1) / rkv::kPrefillKT;
+    p.ws_ml = reinterpret_cast<float*>(w + tiles);
+    p.ws_o = reinterpret_cast<float*>(w + tiles + al256(rows * 2 * sizeof(float)));
     p.out = out;
     p.max_tokens = desc->max_tokens;
     p.num_q = num_q;

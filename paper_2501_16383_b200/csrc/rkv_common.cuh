@@ -85,6 +85,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// mbar_wait for a role thread that may wait long (TMA producer, MMA issuer):
+// the try_wait suspends in hardware for up to `hint` ns between polls instead
+// of spinning, leaving issue slots to the warps sharing its SM sub-partition
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "RKV_WAITS_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "@!p bra RKV_WAITS_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(1000000u)
+        : "memory");
+}
 // 1-D TMA bulk copy global -> shared (SASS: UBLKCP), completes on `bar`.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile(

@@ -51,6 +51,9 @@ struct DecodeParams {
     float qscale;  // log2(e) / sqrt(d)
 };
 
+// prefill operand tiles (prefill.cu): 64 keys per tile, K hi + K lo + V^T
+constexpr int kPrefillKT = 64;
+constexpr size_t kPrefillTileBytes = 3 * 16384;
 struct PrefillParams {
     const uint16_t* q;        // [B][num_q][Hq][128] fp16 pre-RoPE
     const int64_t* q_start;   // [B] position of query row 0
@@ -58,8 +61,11 @@ struct PrefillParams {
     const uint32_t* plan;     // layer plan (tensor-core layout)
     const float4* rope;       // rope table (decode_attention.cu layout)
     rkv_cache cache;
-    uint16_t* kr_hi;          // [B][max_tokens][C] reconstructed keys, fp16 hi
-    uint16_t* kr_lo;          //                               and fp16 lo
+    // reconstructed operand tiles, [B][Hkv][kv_tiles] x 48 KB: per 64 keys the
+    // keys' fp16 hi and lo planes (2 x 2 K-major SWIZZLE_128B slabs of 64 dims)
+    // and the dequantized values transposed ([128 channels][64 keys], one slab)
+    unsigned char* kv_tiles;
+    int64_t kv_tiles_per_seq;
     float* ws_ml;             // [B][num_q][Hq][2]
     float* ws_o;              // [B][num_q][Hq][128]
     float* out;               // [B][num_q][Hq][128]
