@@ -230,40 +230,129 @@ __global__ void __launch_bounds__(128) reconstruct_values_kernel(PrefillParams p
     }
 }
 
-// ------------------------------------------------------------- 3. attention
+// --------------------------------------------------------------- 3. queries
+// Query rows, staged once for every (head, 128-row block) CTA: RoPE at the
+// row's position, x log2(e)/sqrt(d), split into fp16 hi + lo and written as
+// the 512-byte TMEM-ready row the attention kernel bulk-copies (u32 u =
+// dims (2u, 2u + 1) of hi for u < 64, of lo for u >= 64; 16-byte chunk c
+// stored at c ^ (row & 31) so the per-row shared-memory reads do not
+// conflict).  Warp = (sequence, query row, 4 heads); lane = frequencies
+// 2 lane, 2 lane + 1; padding rows (>= num_q) are zero.
+__global__ void __launch_bounds__(128) prepare_queries_kernel(PrefillParams p) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t i = blockIdx.x;
+    const int b = blockIdx.z, h0 = (blockIdx.y * 4 + warp) * 4;
+    if (h0 >= p.Hq) return;
+    const bool live = i < p.num_q;
+    const int f = 2 * lane;
+    float cs[2] = {0.f, 0.f}, sn[2] = {0.f, 0.f};
+    if (live) {
+        const int64_t pos = p.q_start[b] + i;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const float2 r = rope_cs(p.rope, pos, f + k);
+            cs[k] = r.x;
+            sn[k] = r.y;
+        }
+    }
+    const uint32_t sw = static_cast<uint32_t>(i & 31);
+    auto put = [&](uint32_t* row, uint32_t u, uint32_t v) { row[((((u >> 2) ^ sw) & 31u) << 2) | (u & 3u)] = v; };
+    for (int h = h0; h < min(h0 + 4, p.Hq); ++h) {
+        float qa[2] = {0.f, 0.f}, qv[2] = {0.f, 0.f};
+        if (live) {
+            const uint16_t* qr = p.q + ((static_cast<int64_t>(b) * p.num_q + i) * p.Hq + h) * 128;
+            const uint32_t wa = *reinterpret_cast<const uint32_t*>(qr + f), wb = *reinterpret_cast<const uint32_t*>(qr + f + 64);
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const float a = h2f(static_cast<uint16_t>(k ? wa >> 16 : wa & 0xffffu));
+                const float bb = h2f(static_cast<uint16_t>(k ? wb >> 16 : wb & 0xffffu));
+                qa[k] = (a * cs[k] - bb * sn[k]) * p.qscale;
+                qv[k] = (a * sn[k] + bb * cs[k]) * p.qscale;
+            }
+        }
+        uint32_t* row = reinterpret_cast<uint32_t*>(p.q_rows + ((static_cast<int64_t>(b) * p.Hq + h) * p.num_q_pad + i) * 512);
+        const uint32_t ha = pack_h2(qa[0], qa[1]), hb = pack_h2(qv[0], qv[1]);
+        put(row, lane, ha);
+        put(row, 32 + lane, hb);
+        put(row, 64 + lane, pack_h2(sub_lo(qa[0], ha), sub_hi(qa[1], ha)));
+        put(row, 96 + lane, pack_h2(sub_lo(qv[0], hb), sub_hi(qv[1], hb)));
+    }
+}
+
+// ------------------------------------------------------------- 4. attention
 // Flash attention on the 5th-generation tensor cores.  CTA = (sequence, q
-// head, 128 query rows); 8 warps: warp 0 streams the operand tiles
-// (cp.async.bulk; keys 3 tiles deep, values 2), warp 1 (one elected lane)
-// issues tcgen05.mma, warps 2-7 stage the query block, then warps 4-7 run
-// the softmax with one query row per thread (TMEM lane = row).  Per 64-key
-// tile j:
+// head, 128 query rows); 8 warps: warp 0 bulk-copies the staged query block
+// and streams the key tiles (cp.async.bulk, 3 deep), warp 3 streams the
+// value tiles (2 deep), warp 1 (one elected lane) issues tcgen05.mma, warp 2
+// stages the sink rows, warps 4-7 run the softmax and the epilogue with one
+// query row per thread (TMEM lane = row).  Per 64-key tile j:
 //   S_j (TMEM, double-buffered) = Qhi Khi^T + Qhi Klo^T + Qlo Khi^T
 //     (M = 128, N = 64, 3 x 8 K-steps; ~2^-22 relative, as the mma.sync path),
 //   softmax: causal / length / sink mask, running max with lazy rescale (O in
 //     TMEM is rescaled only when a row's max grows by more than 2^14), P = 2^(S - m)
-//     as fp16 into shared memory (K-major SWIZZLE_128B, double-buffered),
+//     as fp16 pairs into tensor memory (double-buffered),
 //   O (TMEM, 128 x 128 fp32) += P V_j (M = 128, N = 128, 4 K-steps).
-// The MMA lane issues QK(j + 1) before PV(j), so S_{j+1} is ready when the
-// softmax of tile j ends and the tensor core runs PV(j) + QK(j + 2) under the
-// softmax of tile j + 1.  Every hand-off is an mbarrier (TMA transaction
-// bytes, tcgen05.commit, or the 128 / 192 arrivals of the softmax / staging
-// threads).
-constexpr int kQR = 128, kAttnThreads = 256, kKSlots = 3, kVSlots = 2;
-constexpr uint32_t kQSlab = 16384, kKSlab = 8192, kKTile = 32768, kVTile = 16384, kPBuf = 16384;
-constexpr uint32_t kOffQlo = 2 * kQSlab, kOffK = 4 * kQSlab, kOffV = kOffK + kKSlots * kKTile,
-                   kOffP = kOffV + kVSlots * kVTile, kOffBar = kOffP + 2 * kPBuf;
-constexpr size_t kAttnSmem = kOffBar + 192 + 1024;  // + barriers, + alignment slack
-constexpr float kLazy = 14.0f;                       // rescale O only when the max grows by > 2^14 (P <= 2^14 in fp16)
-constexpr int kStageThreads = kAttnThreads - 64;     // warps 2-7 stage the query block
+// Q (hi, lo) and P are A operands read from tensor memory, so shared memory
+// only carries the K / V tiles (TMA writes + one B-operand read each).
+// The MMA lane issues QK(j + 2) as soon as the softmax has read S_j, then
+// PV(j) once P_j is written, so the tensor core computes the next scores
+// while the softmax of tile j runs.  Every hand-off is an mbarrier (TMA
+// transaction bytes, tcgen05.commit, or thread arrivals).
+// Epilogue (the reference's exact sink rows, as decode_combine_kernel): the
+// row's sink logits q . RoPE(k_s) join the running (m, l), then
+// out = (H_128 O / sqrt(128) * 2^(m - M) + sum_s 2^(e_s - M) v_s) / L.
+#ifdef RKV_PF_TRACE
+// development trace (build with RKV_NVCC_EXTRA=-DRKV_PF_TRACE): SM clock at
+// per-tile hand-off events of CTA (0, 0, 0), read back by rkv_debug_prefill_trace
+__device__ long long g_pf_trace[8][256];
+__device__ unsigned long long g_pf_cta[4096][4];  // %globaltimer: start, q staged, last P, end
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define PF_CTA(k)                                                                                       \
+    do {                                                                                                \
+        const int cid = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;                  \
+        if (cid < 4096) g_pf_cta[cid][k] = gtimer();                                                    \
+    } while (0)
+#define PF_TRACE(ev, j)                                                                                     \
+    do {                                                                                                  \
+        if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (j) < 256) g_pf_trace[ev][j] = clock64(); \
+    } while (0)
+#else
+#define PF_TRACE(ev, j) \
+    do {                \
+    } while (0)
+#define PF_CTA(k) \
+    do {          \
+    } while (0)
+#endif
+#define PF_CTA_START()         \
+    do {                       \
+        if (threadIdx.x == 0) PF_CTA(0); \
+    } while (0)
+constexpr int kQR = 128, kAttnThreads = 256, kKSlots = 3, kVSlots = 2, kMaxSinkRows = 16;
+constexpr uint32_t kQRow = 512, kKSlab = 8192, kKTile = 32768, kVTile = 16384;
+constexpr uint32_t kOffK = kQR * kQRow, kOffV = kOffK + kKSlots * kKTile, kOffSink = kOffV + kVSlots * kVTile,
+                   kOffBar = kOffSink + kMaxSinkRows * 128 * 6 + 64;
+constexpr size_t kAttnSmem = kOffBar + 256 + 1024;  // + barriers, + alignment slack
+// tensor-memory columns
+constexpr uint32_t kColO = 128, kColQhi = 256, kColQlo = 320, kColP = 384;  // S_0 0, S_1 64; P_i at 384 + 32 i
+constexpr float kLazy = 14.0f;  // rescale O only when the max grows by > 2^14 (P <= 2^14 in fp16)
 
 __global__ void __launch_bounds__(kAttnThreads, 1) prefill_attn_kernel(PrefillParams p) {
     extern __shared__ unsigned char smem_raw[];
     unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // 1024-byte aligned
     const uint32_t sbase = smem_u32(smem);
+    float* sink_k = reinterpret_cast<float*>(smem + kOffSink);                          // [16][128] RoPE'd
+    uint16_t* sink_v = reinterpret_cast<uint16_t*>(smem + kOffSink + kMaxSinkRows * 512);  // [16][128] fp16
+    int* sink_p = reinterpret_cast<int*>(smem + kOffSink + kMaxSinkRows * 768);             // [16] positions
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kOffBar);
-    uint64_t *kfull = bar, *kempty = bar + 3, *vfull = bar + 6, *vempty = bar + 8, *s_full = bar + 10,
-             *s_free = bar + 12, *p_full = bar + 14, *pv_done = bar + 16, *q_full = bar + 18;
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 19);
+    uint64_t *kfull = bar, *kempty = bar + kKSlots, *vfull = bar + 2 * kKSlots, *vempty = vfull + 2, *s_full = vfull + 4,
+             *s_free = vfull + 6, *p_full = vfull + 8, *pv_done = vfull + 10, *q_full = vfull + 12, *q_tmem = vfull + 13,
+             *sink_ready = vfull + 14;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(sink_ready + 1);
 
     const int qb = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, b = blockIdx.z;  // heaviest query blocks first
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -273,7 +362,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1) prefill_attn_kernel(PrefillPa
     const int64_t q0 = p.q_start[b] + i0, T = p.seq_len[b];
     const int64_t kend = lmin64(T, q0 + nrows);
     const int nt = kend > 0 ? static_cast<int>((kend + kPrefillKT - 1) / kPrefillKT) : 0;
+    const int nsink = min(min(p.cache.sink_count[b], p.max_sinks), kMaxSinkRows);
 
+    PF_CTA_START();
     if (tid == 0) {
         for (int i = 0; i < kKSlots; ++i) {
             mbar_init(kfull + i, 1);
@@ -287,19 +378,24 @@ __global__ void __launch_bounds__(kAttnThreads, 1) prefill_attn_kernel(PrefillPa
             mbar_init(p_full + i, 128);
             mbar_init(pv_done + i, 1);
         }
-        mbar_init(q_full, kStageThreads);
+        mbar_init(q_full, 1);
+        mbar_init(q_tmem, 128);
+        mbar_init(sink_ready, 32);
         mbar_fence_init();
     }
-    if (warp == 1) umma::alloc<256>(tslot);
+    if (warp == 1) umma::alloc<512>(tslot);
     umma::fence_before();
     __syncthreads();
     umma::fence_after();
-    const uint32_t tmem = *tslot;  // S_0: columns [0, 64), S_1: [64, 128), O: [128, 256)
+    const uint32_t tmem = *tslot;
 
     if (warp == 0) {
-        // ---- producer: K(j + 2) runs ahead of V(j)
+        // ---- query block, then the key tiles (kKSlots deep)
         if (umma::elect_one()) {
-            auto load_k = [&](int j) {
+            mbar_arrive_expect_tx(q_full, kQR * kQRow);
+            const unsigned char* qsrc = p.q_rows + ((static_cast<int64_t>(b) * p.Hq + h) * p.num_q_pad + i0) * kQRow;
+            for (int c = 0; c < 4; ++c) bulk_g2s(smem + c * 16384, qsrc + c * 16384, 16384, q_full);
+            for (int j = 0; j < nt; ++j) {
                 const int sl = j % kKSlots;
                 if (j >= kKSlots) mbar_wait_sleep(kempty + sl, ((j / kKSlots) - 1) & 1);
                 const unsigned char* src = kv_tile(p, b, kvh, j);
@@ -307,18 +403,6 @@ __global__ void __launch_bounds__(kAttnThreads, 1) prefill_attn_kernel(PrefillPa
                 mbar_arrive_expect_tx(kfull + sl, kKTile);
                 bulk_g2s(dst, src, kKTile / 2, kfull + sl);
                 bulk_g2s(dst + kKTile / 2, src + kKTile / 2, kKTile / 2, kfull + sl);
-            };
-            auto load_v = [&](int j) {
-                const int sl = j & 1;
-                if (j >= kVSlots) mbar_wait_sleep(vempty + sl, ((j >> 1) - 1) & 1);
-                mbar_arrive_expect_tx(vfull + sl, kVTile);
-                bulk_g2s(smem + kOffV + sl * kVTile, kv_tile(p, b, kvh, j) + kKTile, kVTile, vfull + sl);
-            };
-            if (nt > 0) load_k(0);
-            if (nt > 1) load_k(1);
-            for (int j = 0; j < nt; ++j) {
-                if (j + 2 < nt) load_k(j + 2);
-                load_v(j);
             }
         }
         __syncwarp();
@@ -326,289 +410,295 @@ __global__ void __launch_bounds__(kAttnThreads, 1) prefill_attn_kernel(PrefillPa
         // ---- MMA issuer
         if (umma::elect_one()) {
             constexpr uint32_t idS = umma::idesc_f16(128, 64), idO = umma::idesc_f16(128, 128);
-            mbar_wait_sleep(q_full, 0);
+            mbar_wait(q_tmem, 0);
+            PF_CTA(1);
             auto qk = [&](int j) {
                 const int sl = j % kKSlots, sb = j & 1;
-                mbar_wait_sleep(kfull + sl, (j / kKSlots) & 1);
-                if (j >= 2) mbar_wait_sleep(s_free + sb, ((j >> 1) - 1) & 1);
+                mbar_wait(kfull + sl, (j / kKSlots) & 1);
+                if (j >= 2) mbar_wait(s_free + sb, ((j >> 1) - 1) & 1);
                 umma::fence_after();
+                PF_TRACE(4, j);
                 const uint32_t d = tmem + 64u * sb, kb = sbase + kOffK + sl * kKTile;
 #pragma unroll
                 for (int ks = 0; ks < 8; ++ks) {
-                    const uint32_t qo = (ks >> 2) * kQSlab + (ks & 3) * 32, ko = (ks >> 2) * kKSlab + (ks & 3) * 32;
-                    const uint64_t ah = umma::sdesc(sbase + qo), al = umma::sdesc(sbase + kOffQlo + qo);
+                    const uint32_t ko = (ks >> 2) * kKSlab + (ks & 3) * 32;
                     const uint64_t bh = umma::sdesc(kb + ko), bl = umma::sdesc(kb + 2 * kKSlab + ko);
-                    umma::mma_f16(d, ah, bh, idS, ks > 0);
-                    umma::mma_f16(d, ah, bl, idS, 1);
-                    umma::mma_f16(d, al, bh, idS, 1);
+                    umma::mma_f16_ts(d, tmem + kColQhi + 8 * ks, bh, idS, ks > 0);
+                    umma::mma_f16_ts(d, tmem + kColQhi + 8 * ks, bl, idS, 1);
+                    umma::mma_f16_ts(d, tmem + kColQlo + 8 * ks, bh, idS, 1);
                 }
                 umma::commit(s_full + sb);
                 umma::commit(kempty + sl);
             };
             auto pv = [&](int j) {
                 const int sb = j & 1;
-                mbar_wait_sleep(vfull + sb, (j >> 1) & 1);
-                mbar_wait_sleep(p_full + sb, (j >> 1) & 1);
+                mbar_wait(vfull + sb, (j >> 1) & 1);
+                mbar_wait(p_full + sb, (j >> 1) & 1);
                 umma::fence_after();
-                const uint32_t pa = sbase + kOffP + sb * kPBuf, vb = sbase + kOffV + sb * kVTile;
+                PF_TRACE(2, j);
+                const uint32_t vb = sbase + kOffV + sb * kVTile;
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk)
-                    umma::mma_f16(tmem + 128, umma::sdesc(pa + kk * 32), umma::sdesc(vb + kk * 32), idO, (j > 0 || kk > 0));
+                    umma::mma_f16_ts(tmem + kColO, tmem + kColP + 32 * sb + 8 * kk, umma::sdesc(vb + kk * 32), idO,
+                                     (j > 0 || kk > 0));
                 umma::commit(vempty + sb);
                 umma::commit(pv_done + sb);
+                PF_TRACE(3, j);
             };
             if (nt > 0) qk(0);
+            if (nt > 1) qk(1);
             for (int j = 0; j < nt; ++j) {
-                if (j + 1 < nt) qk(j + 1);
+                if (j + 2 < nt) qk(j + 2);
                 pv(j);
             }
         }
         __syncwarp();
-    } else {
-        // ---- warps 2-7: the query block, RoPE at each row's position,
-        // x log2(e)/sqrt(d), fp16 hi + lo; item = (row, 8 frequencies)
-        for (int idx = tid - 64; idx < kQR * 8; idx += kStageThreads) {
-            const int r = idx >> 3, c = idx & 7, f = 8 * c;
-            float qa[8], qv[8];
-            if (r < nrows) {
-                const uint16_t* qr = p.q + ((static_cast<int64_t>(b) * nq + i0 + r) * p.Hq + h) * 128;
-                const uint4 ua = *reinterpret_cast<const uint4*>(qr + f), ub = *reinterpret_cast<const uint4*>(qr + f + 64);
-                const uint16_t* ha = reinterpret_cast<const uint16_t*>(&ua);
-                const uint16_t* hb = reinterpret_cast<const uint16_t*>(&ub);
-                const int64_t pos = q0 + r;
-                const float4* rr = p.rope + (pos >> 1) * kRopeRowF4 + f;
-                const bool odd = pos & 1;
+    } else if (warp == 2) {
+        // ---- sink rows of this KV head: keys RoPE'd at their own position (fp32), values raw
+        for (int s = 0; s < nsink; ++s) {
+            const int pos = p.cache.sink_pos[b * p.max_sinks + s];
+            const int64_t srow = (static_cast<int64_t>(b) * p.max_sinks + s) * p.C + kvh * 128;
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const float4 r4 = __ldg(rr + i);
-                    const float cs = odd ? r4.y : r4.x, sn = odd ? r4.w : r4.z;
-                    const float a = h2f(ha[i]), bb = h2f(hb[i]);
-                    qa[i] = (a * cs - bb * sn) * p.qscale;
-                    qv[i] = (a * sn + bb * cs) * p.qscale;
-                }
-            } else {
-#pragma unroll
-                for (int i = 0; i < 8; ++i) qa[i] = qv[i] = 0.f;
+            for (int k = 0; k < 2; ++k) {
+                const int f = lane + 32 * k;
+                const float ka = h2f(p.cache.sink_k[srow + f]), kb = h2f(p.cache.sink_k[srow + f + 64]);
+                const float2 r = rope_cs(p.rope, pos, f);
+                sink_k[s * 128 + f] = ka * r.x - kb * r.y;
+                sink_k[s * 128 + f + 64] = ka * r.y + kb * r.x;
             }
-            uint32_t hia[4], loa[4], hib[4], lob[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                hia[i] = pack_h2(qa[2 * i], qa[2 * i + 1]);
-                loa[i] = pack_h2(sub_lo(qa[2 * i], hia[i]), sub_hi(qa[2 * i + 1], hia[i]));
-                hib[i] = pack_h2(qv[2 * i], qv[2 * i + 1]);
-                lob[i] = pack_h2(sub_lo(qv[2 * i], hib[i]), sub_hi(qv[2 * i + 1], hib[i]));
-            }
-            const uint32_t off = umma::sw128(static_cast<uint32_t>(r), static_cast<uint32_t>(c));
-            *reinterpret_cast<uint4*>(smem + off) = make_uint4(hia[0], hia[1], hia[2], hia[3]);
-            *reinterpret_cast<uint4*>(smem + kQSlab + off) = make_uint4(hib[0], hib[1], hib[2], hib[3]);
-            *reinterpret_cast<uint4*>(smem + kOffQlo + off) = make_uint4(loa[0], loa[1], loa[2], loa[3]);
-            *reinterpret_cast<uint4*>(smem + kOffQlo + kQSlab + off) = make_uint4(lob[0], lob[1], lob[2], lob[3]);
+            reinterpret_cast<uint2*>(sink_v + s * 128)[lane] = *reinterpret_cast<const uint2*>(p.cache.sink_v + srow + 4 * lane);
+            if (lane == 0) sink_p[s] = pos;
         }
-        umma::fence_proxy_async();
-        mbar_arrive(q_full);
-
-        if (warp >= 4) {
-            // ---- softmax: one query row per thread
-            const int row = 32 * (warp - 4) + lane;
-            const int64_t qpos = q0 + row;
-            const uint32_t lrow = static_cast<uint32_t>(32 * (warp - 4)) << 16;
-            const uint32_t* smask = p.cache.sink_mask + static_cast<int64_t>(b) * ((p.max_tokens + 31) / 32);
-            float m = -INFINITY, l = 0.f;
+        mbar_arrive(sink_ready);
+    } else if (warp == 3) {
+        // ---- value tiles
+        if (umma::elect_one()) {
             for (int j = 0; j < nt; ++j) {
-                const int sb = j & 1;
-                mbar_wait(s_full + sb, (j >> 1) & 1);
-                umma::fence_after();
-                uint32_t v[4][16];
-#pragma unroll
-                for (int c = 0; c < 4; ++c) umma::ld16(tmem + lrow + 64u * sb + 16u * c, v[c]);
-#pragma unroll
-                for (int c = 0; c < 4; ++c) umma::wait_ld(v[c]);
-                umma::fence_before();
-                mbar_arrive(s_free + sb);
-                float s[64];
-#pragma unroll
-                for (int c = 0; c < 64; ++c) s[c] = __uint_as_float(v[c >> 4][c & 15]);
-                const int64_t k0 = static_cast<int64_t>(j) * kPrefillKT;
-                const uint32_t sm0 = __ldg(smask + (k0 >> 5)), sm1 = __ldg(smask + (k0 >> 5) + 1);
-                if (k0 + kPrefillKT - 1 > q0 || k0 + kPrefillKT > T || (sm0 | sm1)) {
-                    const int64_t lim = lmin64(qpos + 1, T) - k0;  // keys k0 + c, c < lim, are in range
-#pragma unroll
-                    for (int c = 0; c < 64; ++c) {
-                        const bool sink = ((c < 32 ? sm0 : sm1) >> (c & 31)) & 1u;
-                        s[c] = (c < lim && !sink) ? s[c] : -INFINITY;
-                    }
-                }
-                float mx8[8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    mx8[i] = fmaxf(fmaxf(s[i], s[i + 8]), s[i + 16]);
-                    mx8[i] = fmaxf(fmaxf(mx8[i], s[i + 24]), s[i + 32]);
-                    mx8[i] = fmaxf(fmaxf(mx8[i], s[i + 40]), s[i + 48]);
-                    mx8[i] = fmaxf(mx8[i], s[i + 56]);
-                }
-                const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                                       fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-                float alpha = 1.0f;
-                bool resc = false;
-                if (mx != -INFINITY) {
-                    if (m == -INFINITY) {
-                        m = mx;
-                    } else if (mx > m + kLazy) {
-                        alpha = ex2(m - mx);
-                        m = mx;
-                        resc = true;
-                    }
-                }
-                if (__any_sync(0xffffffffu, resc)) {  // O holds PV(0..j-1): wait for the last one, rescale in TMEM
-                    mbar_wait(pv_done + ((j - 1) & 1), ((j - 1) >> 1) & 1);
-                    umma::fence_after();
+                const int sl = j & 1;
+                if (j >= kVSlots) mbar_wait_sleep(vempty + sl, ((j >> 1) - 1) & 1);
+                PF_TRACE(5, j);
+                mbar_arrive_expect_tx(vfull + sl, kVTile);
+                bulk_g2s(smem + kOffV + sl * kVTile, kv_tile(p, b, kvh, j) + kKTile, kVTile, vfull + sl);
+            }
+        }
+        __syncwarp();
+    } else {
+        // ---- softmax: one query row per thread
+        const int row = 32 * (warp - 4) + lane;
+        const int64_t qpos = q0 + row;
+        const uint32_t lrow = static_cast<uint32_t>(32 * (warp - 4)) << 16;
+        const unsigned char* qrow = smem + row * kQRow;
+        auto qchunk = [&](int c) { return *reinterpret_cast<const uint4*>(qrow + (((c ^ row) & 31) << 4)); };
+        // this row of Q hi / lo -> tensor memory
+        mbar_wait(q_full, 0);
 #pragma unroll 1
-                    for (int c = 0; c < 8; ++c) {
-                        uint32_t o[16];
-                        umma::ld16(tmem + lrow + 128u + 16u * c, o);
-                        umma::wait_ld(o);
+        for (int pl = 0; pl < 2; ++pl) {
+            uint32_t v[64];
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-                        umma::st16(tmem + lrow + 128u + 16u * c, o);
-                    }
-                    umma::wait_st();
-                    l *= alpha;
-                }
-                const float mu = m == -INFINITY ? 0.f : m;
-                const float2 mu2 = make_float2(mu, mu);
-                float2 ls[4];
-                uint32_t hv[32];
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    const float2 d = sub2(make_float2(s[2 * i], s[2 * i + 1]), mu2);
-                    const float2 pp = make_float2(ex2(d.x), ex2(d.y));
-                    ls[i & 3] = i < 4 ? pp : add2(ls[i & 3], pp);
-                    hv[i] = pack_h2(pp.x, pp.y);
-                }
-                const float2 lt = add2(add2(ls[0], ls[1]), add2(ls[2], ls[3]));
-                l += lt.x + lt.y;
-                if (j >= 2) mbar_wait(pv_done + sb, ((j >> 1) - 1) & 1);  // PV(j - 2) released this P buffer
-                unsigned char* prow = smem + kOffP + sb * kPBuf;
-#pragma unroll
-                for (int c = 0; c < 8; ++c)
-                    *reinterpret_cast<uint4*>(prow + umma::sw128(static_cast<uint32_t>(row), static_cast<uint32_t>(c))) =
-                        make_uint4(hv[4 * c], hv[4 * c + 1], hv[4 * c + 2], hv[4 * c + 3]);
-                umma::fence_proxy_async();
-                umma::fence_before();
-                mbar_arrive(p_full + sb);
+            for (int c = 0; c < 16; ++c) {
+                const uint4 u = qchunk(16 * pl + c);
+                v[4 * c] = u.x;
+                v[4 * c + 1] = u.y;
+                v[4 * c + 2] = u.z;
+                v[4 * c + 3] = u.w;
             }
-            if (row < nrows) {
-                const int64_t orow = (static_cast<int64_t>(b) * nq + i0 + row) * p.Hq + h;
-                p.ws_ml[orow * 2] = m;
-                p.ws_ml[orow * 2 + 1] = l;
+            const uint32_t col = tmem + lrow + (pl ? kColQlo : kColQhi);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) umma::st16(col + 16 * c, reinterpret_cast<const uint32_t(&)[16]>(v[16 * c]));
+        }
+        umma::wait_st();
+        umma::fence_before();
+        mbar_arrive(q_tmem);
+
+        const uint32_t* smask = p.cache.sink_mask + static_cast<int64_t>(b) * ((p.max_tokens + 31) / 32);
+        float m = -INFINITY, l = 0.f;
+        for (int j = 0; j < nt; ++j) {
+            const int sb = j & 1;
+            mbar_wait(s_full + sb, (j >> 1) & 1);
+            umma::fence_after();
+            if (lane == 0 && warp == 4) PF_TRACE(0, j);
+            uint32_t v[4][16];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) umma::ld16(tmem + lrow + 64u * sb + 16u * c, v[c]);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) umma::wait_ld(v[c]);
+            umma::fence_before();
+            mbar_arrive(s_free + sb);
+            float s[64];
+#pragma unroll
+            for (int c = 0; c < 64; ++c) s[c] = __uint_as_float(v[c >> 4][c & 15]);
+            const int64_t k0 = static_cast<int64_t>(j) * kPrefillKT;
+            const uint32_t sm0 = __ldg(smask + (k0 >> 5)), sm1 = __ldg(smask + (k0 >> 5) + 1);
+            if (k0 + kPrefillKT - 1 > q0 || k0 + kPrefillKT > T || (sm0 | sm1)) {
+                const int64_t lim = lmin64(qpos + 1, T) - k0;  // keys k0 + c, c < lim, are in range
+#pragma unroll
+                for (int c = 0; c < 64; ++c) {
+                    const bool sink = ((c < 32 ? sm0 : sm1) >> (c & 31)) & 1u;
+                    s[c] = (c < lim && !sink) ? s[c] : -INFINITY;
+                }
             }
-            float4* dst = reinterpret_cast<float4*>(p.ws_o + ((static_cast<int64_t>(b) * nq + i0 + row) * p.Hq + h) * 128);
-            if (nt > 0) {
-                mbar_wait(pv_done + ((nt - 1) & 1), ((nt - 1) >> 1) & 1);
+            float mx8[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                mx8[i] = fmaxf(fmaxf(s[i], s[i + 8]), s[i + 16]);
+                mx8[i] = fmaxf(fmaxf(mx8[i], s[i + 24]), s[i + 32]);
+                mx8[i] = fmaxf(fmaxf(mx8[i], s[i + 40]), s[i + 48]);
+                mx8[i] = fmaxf(mx8[i], s[i + 56]);
+            }
+            const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                   fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+            float alpha = 1.0f;
+            bool resc = false;
+            if (mx != -INFINITY) {
+                if (m == -INFINITY) {
+                    m = mx;
+                } else if (mx > m + kLazy) {
+                    alpha = ex2(m - mx);
+                    m = mx;
+                    resc = true;
+                }
+            }
+            if (__any_sync(0xffffffffu, resc)) {  // O holds PV(0..j-1): wait for the last one, rescale in TMEM
+                mbar_wait(pv_done + ((j - 1) & 1), ((j - 1) >> 1) & 1);
                 umma::fence_after();
 #pragma unroll 1
                 for (int c = 0; c < 8; ++c) {
                     uint32_t o[16];
-                    umma::ld16(tmem + lrow + 128u + 16u * c, o);
+                    umma::ld16(tmem + lrow + kColO + 16u * c, o);
                     umma::wait_ld(o);
-                    if (row < nrows)
 #pragma unroll
-                        for (int i = 0; i < 4; ++i)
-                            dst[4 * c + i] = make_float4(__uint_as_float(o[4 * i]), __uint_as_float(o[4 * i + 1]),
-                                                         __uint_as_float(o[4 * i + 2]), __uint_as_float(o[4 * i + 3]));
+                    for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+                    umma::st16(tmem + lrow + kColO + 16u * c, o);
                 }
-            } else if (row < nrows) {
-                for (int c = 0; c < 32; ++c) dst[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+                umma::wait_st();
+                l *= alpha;
             }
+            const float mu = m == -INFINITY ? 0.f : m;
+            const float2 mu2 = make_float2(mu, mu);
+            float2 ls[4];
+            uint32_t hv[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const float2 d = sub2(make_float2(s[2 * i], s[2 * i + 1]), mu2);
+                const float2 pp = make_float2(ex2(d.x), ex2(d.y));
+                ls[i & 3] = i < 4 ? pp : add2(ls[i & 3], pp);
+                hv[i] = pack_h2(pp.x, pp.y);
+            }
+            const float2 lt = add2(add2(ls[0], ls[1]), add2(ls[2], ls[3]));
+            l += lt.x + lt.y;
+            if (j >= 2) mbar_wait(pv_done + sb, ((j >> 1) - 1) & 1);  // PV(j - 2) released this P buffer
+            umma::st16(tmem + lrow + kColP + 32 * sb, reinterpret_cast<const uint32_t(&)[16]>(hv[0]));
+            umma::st16(tmem + lrow + kColP + 32 * sb + 16, reinterpret_cast<const uint32_t(&)[16]>(hv[16]));
+            umma::wait_st();
+            umma::fence_before();
+            mbar_arrive(p_full + sb);
+            if (lane == 0 && warp == 4) PF_TRACE(1, j);
+        }
+        if (tid == 128) PF_CTA(2);
+
+        // ---- epilogue: sink logits (q = hi + lo from the staged row), merged state
+        mbar_wait(sink_ready, 0);
+        float es[kMaxSinkRows];
+        float M = m;
+#pragma unroll 1
+        for (int s = 0; s < nsink; ++s) {
+            const int pos = sink_p[s];
+            float e = -INFINITY;
+            if (pos <= qpos && pos < T) {
+                const float* kr = sink_k + s * 128;
+                float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int c = 0; c < 16; ++c) {
+                    const uint4 hi = qchunk(c), lo = qchunk(16 + c);
+                    const uint32_t hw[4] = {hi.x, hi.y, hi.z, hi.w}, lw[4] = {lo.x, lo.y, lo.z, lo.w};
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const float2 qh = __half22float2(*reinterpret_cast<const __half2*>(&hw[k]));
+                        const float2 ql = __half22float2(*reinterpret_cast<const __half2*>(&lw[k]));
+                        const float2 kk = *reinterpret_cast<const float2*>(kr + 8 * c + 2 * k);
+                        acc = fma2(add2(qh, ql), kk, acc);
+                    }
+                }
+                e = acc.x + acc.y;
+            }
+            es[s & (kMaxSinkRows - 1)] = e;
+            M = fmaxf(M, e);
+        }
+        const float so = (m == -INFINITY || nt == 0) ? 0.f : ex2(m - M);
+        float L = l * so;
+        for (int s = 0; s < nsink; ++s) {
+            const float w = es[s] == -INFINITY ? 0.f : ex2(es[s] - M);
+            es[s] = w;
+            L += w;
+        }
+        const float inv = L > 0.f ? 1.0f / L : 0.f;
+        float o[128];
+        if (nt > 0) {
+            mbar_wait(pv_done + ((nt - 1) & 1), ((nt - 1) >> 1) & 1);
+            umma::fence_after();
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                uint32_t u[16];
+                umma::ld16(tmem + lrow + kColO + 16u * c, u);
+                umma::wait_ld(u);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) o[16 * c + i] = __uint_as_float(u[i]);
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < 128; ++i) o[i] = 0.f;
+        }
+        // V's inverse rotation: unnormalised H_128 butterflies in registers
+#pragma unroll
+        for (int len = 1; len < 128; len <<= 1)
+#pragma unroll
+            for (int i = 0; i < 128; ++i)
+                if (!(i & len)) {
+                    const float a = o[i], c = o[i + len];
+                    o[i] = a + c;
+                    o[i + len] = a - c;
+                }
+        const float sc = so * inv * (1.0f / sqrtf(128.0f));
+#pragma unroll
+        for (int i = 0; i < 128; ++i) o[i] *= sc;
+#pragma unroll 1
+        for (int s = 0; s < nsink; ++s) {
+            const float w = es[s] * inv;
+            if (w != 0.f) {
+                const __half2* vr = reinterpret_cast<const __half2*>(sink_v + s * 128);
+#pragma unroll
+                for (int i = 0; i < 64; ++i) {
+                    const float2 vv = __half22float2(vr[i]);
+                    o[2 * i] += w * vv.x;
+                    o[2 * i + 1] += w * vv.y;
+                }
+            }
+        }
+        if (row < nrows) {
+            float4* dst = reinterpret_cast<float4*>(p.out + ((static_cast<int64_t>(b) * nq + i0 + row) * p.Hq + h) * 128);
+#pragma unroll
+            for (int c = 0; c < 32; ++c) dst[c] = make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
         }
     }
     umma::fence_before();
     __syncthreads();
     if (warp == 1) {
         umma::fence_after();
-        umma::dealloc<256>(tmem);
+        umma::dealloc<512>(tmem);
     }
-}
-
-// ---------------------------------------------------------------- 4. combine
-__global__ void __launch_bounds__(128) prefill_combine_kernel(PrefillParams p) {
-    const int lane = threadIdx.x & 31;
-    const int64_t nq = p.num_q;
-    const int64_t wid = static_cast<int64_t>(blockIdx.x) * 4 + (threadIdx.x >> 5);
-    if (wid >= static_cast<int64_t>(p.B) * nq * p.Hq) return;
-    const int h = static_cast<int>(wid % p.Hq);
-    const int64_t bi = wid / p.Hq;
-    const int b = static_cast<int>(bi / nq);
-    const int64_t i = bi % nq;
-    const int C = p.C, kvh = h / (p.Hq / p.Hkv);
-    const int64_t qp = p.q_start[b] + i, T = p.seq_len[b];
-    float M = p.ws_ml[wid * 2], L = p.ws_ml[wid * 2 + 1];
-    float4 rot = M == -INFINITY ? make_float4(0.f, 0.f, 0.f, 0.f) : reinterpret_cast<const float4*>(p.ws_o + wid * 128)[lane];
-    if (M == -INFINITY) L = 0.f;
-    float4 raw = make_float4(0.f, 0.f, 0.f, 0.f);
-    const int nsink = min(min(p.cache.sink_count[b], p.max_sinks), 16);
-    if (nsink > 0) {
-        float qd[4];
-        const uint16_t* qh = p.q + (bi * p.Hq + h) * 128;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int d = 4 * lane + j, f = d & 63;
-            const float a = h2f(qh[f]), bb = h2f(qh[f + 64]);
-            const float2 r = rope_cs(p.rope, qp, f);
-            qd[j] = (d < 64 ? (a * r.x - bb * r.y) : (a * r.y + bb * r.x)) * p.qscale;
-        }
-        for (int s = 0; s < nsink; ++s) {
-            const int pos = p.cache.sink_pos[b * p.max_sinks + s];
-            if (pos > qp || pos >= T) continue;
-            const int64_t srow = (static_cast<int64_t>(b) * p.max_sinks + s) * C + kvh * 128;
-            float prod = 0.f;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int d = 4 * lane + j, f = d & 63;
-                const float ka = h2f(p.cache.sink_k[srow + f]), kb = h2f(p.cache.sink_k[srow + f + 64]);
-                const float2 rk = rope_cs(p.rope, pos, f);
-                prod += qd[j] * (d < 64 ? (ka * rk.x - kb * rk.y) : (ka * rk.y + kb * rk.x));
-            }
-#pragma unroll
-            for (int o = 16; o >= 1; o >>= 1) prod += __shfl_xor_sync(0xffffffffu, prod, o);
-            const float mn = fmaxf(M, prod);
-            const float a = exp2f(M - mn), e = exp2f(prod - mn);
-            L = L * a + e;
-            rot = make_float4(rot.x * a, rot.y * a, rot.z * a, rot.w * a);
-            const uint2 vv = *reinterpret_cast<const uint2*>(p.cache.sink_v + srow + 4 * lane);
-            raw = make_float4(raw.x * a + e * h2f(static_cast<uint16_t>(vv.x & 0xffffu)),
-                              raw.y * a + e * h2f(static_cast<uint16_t>(vv.x >> 16)),
-                              raw.z * a + e * h2f(static_cast<uint16_t>(vv.y & 0xffffu)),
-                              raw.w * a + e * h2f(static_cast<uint16_t>(vv.y >> 16)));
-            M = mn;
-        }
-    }
-    float x[4] = {rot.x, rot.y, rot.z, rot.w};
-    {
-        const float a0 = x[0] + x[1], a1 = x[0] - x[1], a2 = x[2] + x[3], a3 = x[2] - x[3];
-        x[0] = a0 + a2;
-        x[1] = a1 + a3;
-        x[2] = a0 - a2;
-        x[3] = a1 - a3;
-    }
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const bool upper = lane & o;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const float y = __shfl_xor_sync(0xffffffffu, x[j], o);
-            x[j] = upper ? y - x[j] : x[j] + y;
-        }
-    }
-    const float inv = L > 0.f ? 1.0f / L : 0.f, nrm = 1.0f / sqrtf(128.0f);
-    reinterpret_cast<float4*>(p.out + wid * 128)[lane] =
-        make_float4((x[0] * nrm + raw.x) * inv, (x[1] * nrm + raw.y) * inv, (x[2] * nrm + raw.z) * inv,
-                    (x[3] * nrm + raw.w) * inv);
+    if (tid == 0) PF_CTA(3);
 }
 
 }  // namespace
 
-size_t prefill_attn_smem() { return kAttnSmem; }
+#ifdef RKV_PF_TRACE
+extern "C" int rkv_debug_prefill_trace(long long* out) {
+    return cudaMemcpyFromSymbol(out, g_pf_trace, sizeof(g_pf_trace)) == cudaSuccess ? 0 : 1;
+}
+extern "C" int rkv_debug_prefill_cta(unsigned long long* out) {
+    return cudaMemcpyFromSymbol(out, g_pf_cta, sizeof(g_pf_cta)) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 cudaError_t launch_prefill(const rkv_layer_desc& d, const PrefillParams& p, int64_t max_seq_len, cudaStream_t s) {
     const int C = p.C, W = C / 16, MG = C / 128;
@@ -635,15 +725,15 @@ cudaError_t launch_prefill(const rkv_layer_desc& d, const PrefillParams& p, int6
                      static_cast<unsigned>(d.batch));
     reconstruct_values_kernel<<<vgrid, 128, 0, s>>>(p);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    prepare_queries_kernel<<<dim3(static_cast<unsigned>(p.num_q_pad), static_cast<unsigned>((p.Hq + 15) / 16),
+                                  static_cast<unsigned>(d.batch)),
+                             128, 0, s>>>(p);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if ((e = cudaFuncSetAttribute(prefill_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(kAttnSmem))) != cudaSuccess)
         return e;
-    const dim3 agrid(static_cast<unsigned>((p.num_q + kQR - 1) / kQR), static_cast<unsigned>(p.Hq),
-                     static_cast<unsigned>(d.batch));
+    const dim3 agrid(static_cast<unsigned>(p.num_q_pad / kQR), static_cast<unsigned>(p.Hq), static_cast<unsigned>(d.batch));
     prefill_attn_kernel<<<agrid, kAttnThreads, kAttnSmem, s>>>(p);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    const int64_t warps = static_cast<int64_t>(d.batch) * p.num_q * p.Hq;
-    prefill_combine_kernel<<<static_cast<unsigned>((warps + 3) / 4), 128, 0, s>>>(p);
     return cudaGetLastError();
 }
 

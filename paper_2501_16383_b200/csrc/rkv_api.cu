@@ -413,8 +413,8 @@ size_t prefill_tile_bytes(const rkv_layer_desc& d) {
 size_t rkv_prefill_workspace_bytes(const rkv_layer_desc* desc, int64_t num_q, int64_t max_seq_len) {
     if (validate(desc) != RKV_OK || num_q < 0 || max_seq_len < 0) return 0;
     const size_t C = static_cast<size_t>(desc->num_kv_heads) * desc->head_dim, B = static_cast<size_t>(desc->batch);
-    const size_t rows = B * static_cast<size_t>(num_q) * desc->num_q_heads;
-    return al256(prefill_tile_bytes(*desc)) + al256(rows * 2 * sizeof(float)) + al256(rows * 128 * sizeof(float));
+    const size_t rows = B * static_cast<size_t>(rkv::prefill_q_pad(num_q)) * desc->num_q_heads;
+    return al256(prefill_tile_bytes(*desc)) + al256(rows * 512);
 }
 
 rkv_status rkv_prefill_attention(const rkv_layer_desc* desc, const uint16_t* q, int64_t num_q, const int64_t* q_start,
@@ -437,7 +437,6 @@ rkv_status rkv_prefill_attention(const rkv_layer_desc* desc, const uint16_t* q, 
         return fail(RKV_ERR_INVALID_ARGUMENT, "prefill: workspace too small");
     const size_t C = static_cast<size_t>(desc->num_kv_heads) * desc->head_dim, B = static_cast<size_t>(desc->batch);
     const size_t tiles = al256(prefill_tile_bytes(*desc));
-    const size_t rows = B * static_cast<size_t>(num_q) * desc->num_q_heads;
     char* w = static_cast<char*>(workspace);
     rkv::PrefillParams p{};
     p.q = q;
@@ -448,8 +447,8 @@ rkv_status rkv_prefill_attention(const rkv_layer_desc* desc, const uint16_t* q, 
     p.cache = *cache;
     p.kv_tiles = reinterpret_cast<unsigned char*>(w);
     p.kv_tiles_per_seq = (desc->max_tokens + rkv::kPrefillKT - 1) / rkv::kPrefillKT;
-    p.ws_ml = reinterpret_cast<float*>(w + tiles);
-    p.ws_o = reinterpret_cast<float*>(w + tiles + al256(rows * 2 * sizeof(float)));
+    p.q_rows = reinterpret_cast<unsigned char*>(w + tiles);
+    p.num_q_pad = rkv::prefill_q_pad(num_q);
     p.out = out;
     p.max_tokens = desc->max_tokens;
     p.num_q = num_q;

@@ -54,6 +54,7 @@ struct DecodeParams {
 // prefill operand tiles (prefill.cu): 64 keys per tile, K hi + K lo + V^T
 constexpr int kPrefillKT = 64;
 constexpr size_t kPrefillTileBytes = 3 * 16384;
+inline int64_t prefill_q_pad(int64_t num_q) { return (num_q + 127) / 128 * 128; }  // 128 query rows per CTA
 struct PrefillParams {
     const uint16_t* q;        // [B][num_q][Hq][128] fp16 pre-RoPE
     const int64_t* q_start;   // [B] position of query row 0
@@ -66,8 +67,10 @@ struct PrefillParams {
     // and the dequantized values transposed ([128 channels][64 keys], one slab)
     unsigned char* kv_tiles;
     int64_t kv_tiles_per_seq;
-    float* ws_ml;             // [B][num_q][Hq][2]
-    float* ws_o;              // [B][num_q][Hq][128]
+    // staged query rows, [B][Hq][num_q_pad] x 512 B: RoPE'd, x log2(e)/sqrt(d),
+    // fp16 hi (64 words) + lo (64 words), 16-byte chunk c at c ^ (row & 31)
+    unsigned char* q_rows;
+    int64_t num_q_pad;
     float* out;               // [B][num_q][Hq][128]
     int64_t max_tokens, num_q;
     int B, Hq, Hkv, C, max_sinks;

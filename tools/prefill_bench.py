@@ -43,3 +43,30 @@ ms = e0.elapsed_time(e1) / iters
 flops = 4.0 * B * w.num_q_heads * 128 * T * (T + 1) / 2  # causal QK^T + PV, 2 flops per MAC
 print(json.dumps({"workload": w.name, "batch": B, "prompt_tokens": T, "ms": round(ms, 3),
                   "prompt_tokens_per_s": B * T / (ms / 1e3), "attention_tflops": flops / (ms / 1e3) / 1e12}))
+
+if os.environ.get("RKV_PF_TRACE"):  # library built with RKV_NVCC_EXTRA=-DRKV_PF_TRACE: hand-off timeline of CTA 0
+    import ctypes
+    buf = (ctypes.c_longlong * (8 * 256))()
+    P.rotatekv.lib().rkv_debug_prefill_trace(buf)
+    tr = np.array(buf, dtype=np.int64).reshape(8, 256)
+    names = ["s_ready", "p_done", "mma_p_seen", "mma_pv_issued", "mma_qk_start", "prod_v_issue"]
+    t0 = tr[0, 0]
+    nt = int((tr[0] != 0).sum())
+    print("tile " + " ".join(f"{n:>13}" for n in names))
+    for j in range(min(nt, 40)):
+        print(f"{j:4d} " + " ".join(f"{int(tr[e, j] - t0) if tr[e, j] else -1:13d}" for e in range(6)))
+    d = np.diff(tr[0, 4:nt])
+    print("steady tile period (cycles): median", int(np.median(d)), "softmax span median", int(np.median(tr[1, 4:nt] - tr[0, 4:nt])))
+    cta = (ctypes.c_ulonglong * (4096 * 4))()
+    P.rotatekv.lib().rkv_debug_prefill_cta(cta)
+    c = np.array(cta, dtype=np.int64).reshape(4096, 4)
+    n = int((c[:, 0] != 0).sum())
+    c = c[:n]
+    t0 = c[:, 0].min()
+    print(f"CTAs {n}: kernel span {(c[:, 3].max() - t0) / 1e3:.1f} us; per CTA (us) median: "
+          f"setup+q {np.median(c[:, 1] - c[:, 0]) / 1e3:.2f}, tiles {np.median(c[:, 2] - c[:, 1]) / 1e3:.2f}, "
+          f"epilogue {np.median(c[:, 3] - c[:, 2]) / 1e3:.2f}; sum of CTA times / 148 = {(c[:, 3] - c[:, 0]).sum() / 148 / 1e3:.1f} us")
+    nq = (c[:, 0] != 0).sum()
+    for k in (0, 1, 15, 16, 31):  # grid x index = 31 - qb
+        row = c[k]
+        print(f"  cta x={k}: setup+q {(row[1] - row[0]) / 1e3:.2f} tiles {(row[2] - row[1]) / 1e3:.2f} epi {(row[3] - row[2]) / 1e3:.2f} us")
