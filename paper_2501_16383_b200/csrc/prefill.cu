@@ -281,26 +281,30 @@ __global__ void __launch_bounds__(128) prepare_queries_kernel(PrefillParams p) {
 
 // ------------------------------------------------------------- 4. attention
 // Flash attention on the 5th-generation tensor cores.  CTA = (sequence, q
-// head, 128 query rows); 8 warps: warp 0 bulk-copies the staged query block
+// head, 128 query rows); 12 warps: warp 0 bulk-copies the staged query block
 // and streams the key tiles (cp.async.bulk, 3 deep), warp 3 streams the
 // value tiles (2 deep), warp 1 (one elected lane) issues tcgen05.mma, warp 2
-// stages the sink rows, warps 4-7 run the softmax and the epilogue with one
-// query row per thread (TMEM lane = row).  Per 64-key tile j:
-//   S_j (TMEM, double-buffered) = Qhi Khi^T + Qhi Klo^T + Qlo Khi^T
-//     (M = 128, N = 64, 3 x 8 K-steps; ~2^-22 relative, as the mma.sync path),
-//   softmax: causal / length / sink mask, running max with lazy rescale (O in
-//     TMEM is rescaled only when a row's max grows by more than 2^14), P = 2^(S - m)
-//     as fp16 pairs into tensor memory (double-buffered),
-//   O (TMEM, 128 x 128 fp32) += P V_j (M = 128, N = 128, 4 K-steps).
-// Q (hi, lo) and P are A operands read from tensor memory, so shared memory
-// only carries the K / V tiles (TMA writes + one B-operand read each).
-// The MMA lane issues QK(j + 2) as soon as the softmax has read S_j, then
-// PV(j) once P_j is written, so the tensor core computes the next scores
-// while the softmax of tile j runs.  Every hand-off is an mbarrier (TMA
+// stages the sink rows, and two softmax groups of 4 warps (one query row
+// per thread, TMEM lane = row) take the 64-key tiles in turn: group X owns
+// the tiles j = X mod 2, its score buffer S_X and its own output
+// accumulator O_X and running (m, l), merged in the epilogue.  Per tile j:
+//   S_X = Qhi Khi^T + Qhi Klo^T + Qlo Khi^T   (M = 128, N = 64, 3 x 8 K-steps;
+//     ~2^-22 relative, Q hi / lo read from tensor memory),
+//   softmax: causal / length / sink mask, running max with lazy rescale (O_X
+//     rescaled in place only when the row max grows by more than 2^14),
+//     P = 2^(S - m) as fp16 pairs written over the first 32 columns of S_X,
+//   O_X += P V_j   (M = 128, N = 128, 4 K-steps, P read from tensor memory).
+// The MMA lane issues PV(j) and then QK(j + 2) into the same S_X: tcgen05
+// operations of one thread execute in order, so the scores of j + 2 never
+// overwrite P_j before PV(j) read it, and S(j) being complete implies PV(j - 2)
+// is, so O_X can be rescaled without waiting.  While group X runs its
+// softmax the tensor core works on the other group's tile.  Shared memory
+// only carries the K / V tiles.  Every hand-off is an mbarrier (TMA
 // transaction bytes, tcgen05.commit, or thread arrivals).
 // Epilogue (the reference's exact sink rows, as decode_combine_kernel): the
-// row's sink logits q . RoPE(k_s) join the running (m, l), then
-// out = (H_128 O / sqrt(128) * 2^(m - M) + sum_s 2^(e_s - M) v_s) / L.
+// row's sink logits q . RoPE(k_s) join the merged (m, l);
+// out = (H_128 O / sqrt(128) * 2^(m - M) + sum_s 2^(e_s - M) v_s) / L, where
+// group X produces output dims [64 X, 64 X + 64) through H_128 = H_2 (x) H_64.
 #ifdef RKV_PF_TRACE
 // development trace (build with RKV_NVCC_EXTRA=-DRKV_PF_TRACE): SM clock at
 // per-tile hand-off events of CTA (0, 0, 0), read back by rkv_debug_prefill_trace
@@ -332,13 +336,13 @@ __device__ __forceinline__ unsigned long long gtimer() {
     do {                       \
         if (threadIdx.x == 0) PF_CTA(0); \
     } while (0)
-constexpr int kQR = 128, kAttnThreads = 256, kKSlots = 3, kVSlots = 2, kMaxSinkRows = 16;
+constexpr int kQR = 128, kAttnThreads = 384, kKSlots = 3, kVSlots = 2, kMaxSinkRows = 16;
 constexpr uint32_t kQRow = 512, kKSlab = 8192, kKTile = 32768, kVTile = 16384;
 constexpr uint32_t kOffK = kQR * kQRow, kOffV = kOffK + kKSlots * kKTile, kOffSink = kOffV + kVSlots * kVTile,
-                   kOffBar = kOffSink + kMaxSinkRows * 128 * 6 + 64;
+                   kOffML = kOffSink + kMaxSinkRows * 128 * 6 + 64, kOffBar = kOffML + 2 * 128 * 8;
 constexpr size_t kAttnSmem = kOffBar + 256 + 1024;  // + barriers, + alignment slack
-// tensor-memory columns
-constexpr uint32_t kColO = 128, kColQhi = 256, kColQlo = 320, kColP = 384;  // S_0 0, S_1 64; P_i at 384 + 32 i
+// tensor-memory columns: S_0 [0, 64), S_1 [64, 128), O_0 [128, 256), O_1 [256, 384), Q hi [384, 448), Q lo [448, 512)
+constexpr uint32_t kColO = 128, kColQhi = 384, kColQlo = 448;
 constexpr float kLazy = 14.0f;  // rescale O only when the max grows by > 2^14 (P <= 2^14 in fp16)
 
 __global__ void __launch_bounds__(kAttnThreads, 1) prefill_attn_kernel(PrefillParams p) {
@@ -348,10 +352,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1) prefill_attn_kernel(PrefillPa
     float* sink_k = reinterpret_cast<float*>(smem + kOffSink);                          // [16][128] RoPE'd
     uint16_t* sink_v = reinterpret_cast<uint16_t*>(smem + kOffSink + kMaxSinkRows * 512);  // [16][128] fp16
     int* sink_p = reinterpret_cast<int*>(smem + kOffSink + kMaxSinkRows * 768);             // [16] positions
+    float2* ml_s = reinterpret_cast<float2*>(smem + kOffML);                               // [2][128] (m, l)
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kOffBar);
     uint64_t *kfull = bar, *kempty = bar + kKSlots, *vfull = bar + 2 * kKSlots, *vempty = vfull + 2, *s_full = vfull + 4,
-             *s_free = vfull + 6, *p_full = vfull + 8, *pv_done = vfull + 10, *q_full = vfull + 12, *q_tmem = vfull + 13,
-             *sink_ready = vfull + 14;
+             *p_full = vfull + 6, *o_done = vfull + 8, *q_full = vfull + 9, *q_tmem = vfull + 10, *sink_ready = vfull + 11;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(sink_ready + 1);
 
     const int qb = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, b = blockIdx.z;  // heaviest query blocks first
@@ -374,12 +378,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1) prefill_attn_kernel(PrefillPa
             mbar_init(vfull + i, 1);
             mbar_init(vempty + i, 1);
             mbar_init(s_full + i, 1);
-            mbar_init(s_free + i, 128);
             mbar_init(p_full + i, 128);
-            mbar_init(pv_done + i, 1);
         }
+        mbar_init(o_done, 1);
         mbar_init(q_full, 1);
-        mbar_init(q_tmem, 128);
+        mbar_init(q_tmem, 256);
         mbar_init(sink_ready, 32);
         mbar_fence_init();
     }
@@ -415,7 +418,6 @@ __global__ void __launch_bounds__(kAttnThreads, 1) prefill_attn_kernel(PrefillPa
             auto qk = [&](int j) {
                 const int sl = j % kKSlots, sb = j & 1;
                 mbar_wait(kfull + sl, (j / kKSlots) & 1);
-                if (j >= 2) mbar_wait(s_free + sb, ((j >> 1) - 1) & 1);
                 umma::fence_after();
                 PF_TRACE(4, j);
                 const uint32_t d = tmem + 64u * sb, kb = sbase + kOffK + sl * kKTile;
@@ -439,18 +441,18 @@ __global__ void __launch_bounds__(kAttnThreads, 1) prefill_attn_kernel(PrefillPa
                 const uint32_t vb = sbase + kOffV + sb * kVTile;
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk)
-                    umma::mma_f16_ts(tmem + kColO, tmem + kColP + 32 * sb + 8 * kk, umma::sdesc(vb + kk * 32), idO,
-                                     (j > 0 || kk > 0));
+                    umma::mma_f16_ts(tmem + kColO + 128u * sb, tmem + 64u * sb + 8 * kk, umma::sdesc(vb + kk * 32), idO,
+                                     (j >= 2 || kk > 0));
                 umma::commit(vempty + sb);
-                umma::commit(pv_done + sb);
                 PF_TRACE(3, j);
             };
             if (nt > 0) qk(0);
             if (nt > 1) qk(1);
             for (int j = 0; j < nt; ++j) {
-                if (j + 2 < nt) qk(j + 2);
                 pv(j);
+                if (j + 2 < nt) qk(j + 2);
             }
+            umma::commit(o_done);
         }
         __syncwarp();
     } else if (warp == 2) {
@@ -482,27 +484,28 @@ __global__ void __launch_bounds__(kAttnThreads, 1) prefill_attn_kernel(PrefillPa
             }
         }
         __syncwarp();
-    } else {
-        // ---- softmax: one query row per thread
-        const int row = 32 * (warp - 4) + lane;
+    } else if (warp >= 4) {
+        // ---- softmax group X = (warp - 4) / 4: tiles j = X mod 2, one query row per thread
+        const int X = (warp - 4) >> 2;
+        const int row = 32 * (warp & 3) + lane;
         const int64_t qpos = q0 + row;
-        const uint32_t lrow = static_cast<uint32_t>(32 * (warp - 4)) << 16;
+        const uint32_t lrow = static_cast<uint32_t>(32 * (warp & 3)) << 16;
+        const uint32_t colS = 64u * X, colO = kColO + 128u * X;
         const unsigned char* qrow = smem + row * kQRow;
         auto qchunk = [&](int c) { return *reinterpret_cast<const uint4*>(qrow + (((c ^ row) & 31) << 4)); };
-        // this row of Q hi / lo -> tensor memory
+        // this row of Q hi (group 0) / lo (group 1) -> tensor memory
         mbar_wait(q_full, 0);
-#pragma unroll 1
-        for (int pl = 0; pl < 2; ++pl) {
+        {
             uint32_t v[64];
 #pragma unroll
             for (int c = 0; c < 16; ++c) {
-                const uint4 u = qchunk(16 * pl + c);
+                const uint4 u = qchunk(16 * X + c);
                 v[4 * c] = u.x;
                 v[4 * c + 1] = u.y;
                 v[4 * c + 2] = u.z;
                 v[4 * c + 3] = u.w;
             }
-            const uint32_t col = tmem + lrow + (pl ? kColQlo : kColQhi);
+            const uint32_t col = tmem + lrow + (X ? kColQlo : kColQhi);
 #pragma unroll
             for (int c = 0; c < 4; ++c) umma::st16(col + 16 * c, reinterpret_cast<const uint32_t(&)[16]>(v[16 * c]));
         }
@@ -512,18 +515,15 @@ __global__ void __launch_bounds__(kAttnThreads, 1) prefill_attn_kernel(PrefillPa
 
         const uint32_t* smask = p.cache.sink_mask + static_cast<int64_t>(b) * ((p.max_tokens + 31) / 32);
         float m = -INFINITY, l = 0.f;
-        for (int j = 0; j < nt; ++j) {
-            const int sb = j & 1;
-            mbar_wait(s_full + sb, (j >> 1) & 1);
+        for (int j = X; j < nt; j += 2) {
+            mbar_wait(s_full + X, (j >> 1) & 1);
             umma::fence_after();
             if (lane == 0 && warp == 4) PF_TRACE(0, j);
             uint32_t v[4][16];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) umma::ld16(tmem + lrow + 64u * sb + 16u * c, v[c]);
+            for (int c = 0; c < 4; ++c) umma::ld16(tmem + lrow + colS + 16u * c, v[c]);
 #pragma unroll
             for (int c = 0; c < 4; ++c) umma::wait_ld(v[c]);
-            umma::fence_before();
-            mbar_arrive(s_free + sb);
             float s[64];
 #pragma unroll
             for (int c = 0; c < 64; ++c) s[c] = __uint_as_float(v[c >> 4][c & 15]);
@@ -558,19 +558,16 @@ __global__ void __launch_bounds__(kAttnThreads, 1) prefill_attn_kernel(PrefillPa
                     resc = true;
                 }
             }
-            if (__any_sync(0xffffffffu, resc)) {  // O holds PV(0..j-1): wait for the last one, rescale in TMEM
-                mbar_wait(pv_done + ((j - 1) & 1), ((j - 1) >> 1) & 1);
-                umma::fence_after();
+            if (__any_sync(0xffffffffu, resc)) {  // PV(j - 2) is complete (it precedes QK(j)): rescale O_X in place
 #pragma unroll 1
                 for (int c = 0; c < 8; ++c) {
                     uint32_t o[16];
-                    umma::ld16(tmem + lrow + kColO + 16u * c, o);
+                    umma::ld16(tmem + lrow + colO + 16u * c, o);
                     umma::wait_ld(o);
 #pragma unroll
                     for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-                    umma::st16(tmem + lrow + kColO + 16u * c, o);
+                    umma::st16(tmem + lrow + colO + 16u * c, o);
                 }
-                umma::wait_st();
                 l *= alpha;
             }
             const float mu = m == -INFINITY ? 0.f : m;
@@ -586,20 +583,23 @@ __global__ void __launch_bounds__(kAttnThreads, 1) prefill_attn_kernel(PrefillPa
             }
             const float2 lt = add2(add2(ls[0], ls[1]), add2(ls[2], ls[3]));
             l += lt.x + lt.y;
-            if (j >= 2) mbar_wait(pv_done + sb, ((j >> 1) - 1) & 1);  // PV(j - 2) released this P buffer
-            umma::st16(tmem + lrow + kColP + 32 * sb, reinterpret_cast<const uint32_t(&)[16]>(hv[0]));
-            umma::st16(tmem + lrow + kColP + 32 * sb + 16, reinterpret_cast<const uint32_t(&)[16]>(hv[16]));
+            umma::st16(tmem + lrow + colS, reinterpret_cast<const uint32_t(&)[16]>(hv[0]));
+            umma::st16(tmem + lrow + colS + 16, reinterpret_cast<const uint32_t(&)[16]>(hv[16]));
             umma::wait_st();
             umma::fence_before();
-            mbar_arrive(p_full + sb);
+            mbar_arrive(p_full + X);
             if (lane == 0 && warp == 4) PF_TRACE(1, j);
         }
         if (tid == 128) PF_CTA(2);
 
-        // ---- epilogue: sink logits (q = hi + lo from the staged row), merged state
+        // ---- epilogue: merge the two groups' (m, l), the sink logits (q = hi + lo of the staged row)
+        ml_s[X * 128 + row] = make_float2(m, l);
+        asm volatile("bar.sync 2, 256;" ::: "memory");
+        const float2 other = ml_s[(1 - X) * 128 + row];
+        const float mA = X ? other.x : m, lA = X ? other.y : l, mB = X ? m : other.x, lB = X ? l : other.y;
         mbar_wait(sink_ready, 0);
         float es[kMaxSinkRows];
-        float M = m;
+        float M = fmaxf(mA, mB);
 #pragma unroll 1
         for (int s = 0; s < nsink; ++s) {
             const int pos = sink_p[s];
@@ -624,60 +624,70 @@ __global__ void __launch_bounds__(kAttnThreads, 1) prefill_attn_kernel(PrefillPa
             es[s & (kMaxSinkRows - 1)] = e;
             M = fmaxf(M, e);
         }
-        const float so = (m == -INFINITY || nt == 0) ? 0.f : ex2(m - M);
-        float L = l * so;
+        const float aA = mA == -INFINITY ? 0.f : ex2(mA - M), aB = mB == -INFINITY ? 0.f : ex2(mB - M);
+        float L = lA * aA + lB * aB;
         for (int s = 0; s < nsink; ++s) {
             const float w = es[s] == -INFINITY ? 0.f : ex2(es[s] - M);
             es[s] = w;
             L += w;
         }
         const float inv = L > 0.f ? 1.0f / L : 0.f;
-        float o[128];
+        // u = O[0:64] +/- O[64:128] (group 0: +, group 1: -), O = aA O_0 + aB O_1; a group
+        // without tiles never wrote its accumulator and is skipped
+        float u[64];
+#pragma unroll
+        for (int i = 0; i < 64; ++i) u[i] = 0.f;
         if (nt > 0) {
-            mbar_wait(pv_done + ((nt - 1) & 1), ((nt - 1) >> 1) & 1);
+            mbar_wait(o_done, 0);
             umma::fence_after();
+            const float sg = X ? -1.f : 1.f;
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                uint32_t u[16];
-                umma::ld16(tmem + lrow + kColO + 16u * c, u);
-                umma::wait_ld(u);
+            for (int g = 0; g < 2; ++g) {
+                const float ag = g ? aB : aA;
+                if (g == 1 && nt < 2) break;
 #pragma unroll
-                for (int i = 0; i < 16; ++i) o[16 * c + i] = __uint_as_float(u[i]);
-            }
-        } else {
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t lo[16], hi[16];
+                    umma::ld16(tmem + lrow + kColO + 128u * g + 16u * c, lo);
+                    umma::ld16(tmem + lrow + kColO + 128u * g + 64u + 16u * c, hi);
+                    umma::wait_ld(lo);
+                    umma::wait_ld(hi);
 #pragma unroll
-            for (int i = 0; i < 128; ++i) o[i] = 0.f;
-        }
-        // V's inverse rotation: unnormalised H_128 butterflies in registers
-#pragma unroll
-        for (int len = 1; len < 128; len <<= 1)
-#pragma unroll
-            for (int i = 0; i < 128; ++i)
-                if (!(i & len)) {
-                    const float a = o[i], c = o[i + len];
-                    o[i] = a + c;
-                    o[i + len] = a - c;
+                    for (int i = 0; i < 16; ++i)
+                        u[16 * c + i] += ag * (__uint_as_float(lo[i]) + sg * __uint_as_float(hi[i]));
                 }
-        const float sc = so * inv * (1.0f / sqrtf(128.0f));
+            }
+        }
+        // H_64 butterflies in registers (with the H_2 stage above: V's inverse rotation H_128)
 #pragma unroll
-        for (int i = 0; i < 128; ++i) o[i] *= sc;
+        for (int len = 1; len < 64; len <<= 1)
+#pragma unroll
+            for (int i = 0; i < 64; ++i)
+                if (!(i & len)) {
+                    const float a = u[i], c = u[i + len];
+                    u[i] = a + c;
+                    u[i + len] = a - c;
+                }
+        const float sc = inv * (1.0f / sqrtf(128.0f));
+#pragma unroll
+        for (int i = 0; i < 64; ++i) u[i] *= sc;
 #pragma unroll 1
         for (int s = 0; s < nsink; ++s) {
             const float w = es[s] * inv;
             if (w != 0.f) {
-                const __half2* vr = reinterpret_cast<const __half2*>(sink_v + s * 128);
+                const __half2* vr = reinterpret_cast<const __half2*>(sink_v + s * 128 + 64 * X);
 #pragma unroll
-                for (int i = 0; i < 64; ++i) {
+                for (int i = 0; i < 32; ++i) {
                     const float2 vv = __half22float2(vr[i]);
-                    o[2 * i] += w * vv.x;
-                    o[2 * i + 1] += w * vv.y;
+                    u[2 * i] += w * vv.x;
+                    u[2 * i + 1] += w * vv.y;
                 }
             }
         }
         if (row < nrows) {
-            float4* dst = reinterpret_cast<float4*>(p.out + ((static_cast<int64_t>(b) * nq + i0 + row) * p.Hq + h) * 128);
+            float4* dst = reinterpret_cast<float4*>(p.out + ((static_cast<int64_t>(b) * nq + i0 + row) * p.Hq + h) * 128 + 64 * X);
 #pragma unroll
-            for (int c = 0; c < 32; ++c) dst[c] = make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
+            for (int c = 0; c < 16; ++c) dst[c] = make_float4(u[4 * c], u[4 * c + 1], u[4 * c + 2], u[4 * c + 3]);
         }
     }
     umma::fence_before();
