@@ -164,10 +164,12 @@ rkv_status rkv_decode_attention(const rkv_layer_desc* desc, const uint16_t* q, c
  *   max_seq_len: host upper bound of seq_len (sizes the key reconstruction)
  *   out        : [B][num_q][Hq][d] fp32, V's rotation undone (like decode)
  *   workspace  : rkv_prefill_workspace_bytes(desc, num_q, max_seq_len) bytes
- * Keys are reconstructed once (tensor-core FWHT + RoPE, fp16 hi/lo), then a
- * flash-attention kernel runs Q.K^T and P.V on the tensor cores; sinks are
- * added exactly.  Layer shapes: those with a tensor-core decode kernel
- * (G = 4 with Hq == Hkv, G = 2 with Hq == 4 Hkv).  Stream-ordered. */
+ * Keys (tensor-core FWHT + RoPE, fp16 hi/lo) and values (dequantized fp16)
+ * are reconstructed once into 64-key operand tiles, the queries are staged,
+ * then a flash-attention kernel runs Q.K^T and P.V on tcgen05 (accumulators
+ * in tensor memory); sinks are merged exactly in its epilogue.  Layer shapes:
+ * those with a tensor-core decode kernel (G = 4 with Hq == Hkv, G = 2 with
+ * Hq == 4 Hkv).  Stream-ordered. */
 size_t rkv_prefill_workspace_bytes(const rkv_layer_desc* desc, int64_t num_q, int64_t max_seq_len);
 rkv_status rkv_prefill_attention(const rkv_layer_desc* desc, const uint16_t* q, int64_t num_q, const int64_t* q_start,
                                  const int64_t* seq_len, int64_t max_seq_len, const rkv_cache* cache,
