@@ -167,7 +167,8 @@ rkv_status rkv_decode_attention(const rkv_layer_desc* desc, const uint16_t* q, c
  * Keys (tensor-core FWHT + RoPE, fp16 hi/lo) and values (dequantized fp16)
  * are reconstructed once into 64-key operand tiles, the queries are staged,
  * then a flash-attention kernel runs Q.K^T and P.V on tcgen05 (accumulators
- * in tensor memory); sinks are merged exactly in its epilogue.  Layer shapes:
+ * in tensor memory); sinks are merged exactly in its epilogue (max_sinks
+ * <= 16, else RKV_ERR_INVALID_ARGUMENT).  Layer shapes:
  * those with a tensor-core decode kernel (G = 4 with Hq == Hkv, G = 2 with
  * Hq == 4 Hkv).  Stream-ordered. */
 size_t rkv_prefill_workspace_bytes(const rkv_layer_desc* desc, int64_t num_q, int64_t max_seq_len);

@@ -485,7 +485,7 @@ __global__ void __launch_bounds__(128) decode_combine_kernel(DecodeParams p) {
         }
     }
     // sinks: logits from q and the raw fp16 key rows, both RoPE'd (log2 domain)
-    const int nsink = min(min(p.cache.sink_count[b], p.max_sinks), 16);
+    const int nsink = min(p.cache.sink_count[b], p.max_sinks);
     float4 raw = make_float4(0.f, 0.f, 0.f, 0.f);
     if (nsink > 0) {
         float qd[4];

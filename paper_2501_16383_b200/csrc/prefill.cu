@@ -336,7 +336,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
     do {                       \
         if (threadIdx.x == 0) PF_CTA(0); \
     } while (0)
-constexpr int kQR = 128, kAttnThreads = 384, kKSlots = 3, kVSlots = 2, kMaxSinkRows = 16;
+constexpr int kQR = 128, kAttnThreads = 384, kKSlots = 3, kVSlots = 2, kMaxSinkRows = kPrefillMaxSinks;
 constexpr uint32_t kQRow = 512, kKSlab = 8192, kKTile = 32768, kVTile = 16384;
 constexpr uint32_t kOffK = kQR * kQRow, kOffV = kOffK + kKSlots * kKTile, kOffSink = kOffV + kVSlots * kVTile,
                    kOffML = kOffSink + kMaxSinkRows * 128 * 6 + 64, kOffBar = kOffML + 2 * 128 * 8;

@@ -433,6 +433,8 @@ rkv_status rkv_prefill_attention(const rkv_layer_desc* desc, const uint16_t* q, 
     if (rkv::decode_kind(*desc) != rkv::kDecodeMma)
         return fail(RKV_ERR_INVALID_ARGUMENT,
                     "prefill: the tensor-core path covers G = 4 with Hq == Hkv and G = 2 with Hq == 4 Hkv");
+    if (desc->max_sinks > rkv::kPrefillMaxSinks)
+        return fail(RKV_ERR_INVALID_ARGUMENT, "prefill: at most 16 sink rows per sequence (max_sinks <= 16)");
     if (ws_bytes < rkv_prefill_workspace_bytes(desc, num_q, max_seq_len))
         return fail(RKV_ERR_INVALID_ARGUMENT, "prefill: workspace too small");
     const size_t C = static_cast<size_t>(desc->num_kv_heads) * desc->head_dim, B = static_cast<size_t>(desc->batch);

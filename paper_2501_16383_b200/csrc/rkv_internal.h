@@ -53,6 +53,7 @@ struct DecodeParams {
 
 // prefill operand tiles (prefill.cu): 64 keys per tile, K hi + K lo + V^T
 constexpr int kPrefillKT = 64;
+constexpr int kPrefillMaxSinks = 16;  // sink rows staged per attention CTA
 constexpr size_t kPrefillTileBytes = 3 * 16384;
 inline int64_t prefill_q_pad(int64_t num_q) { return (num_q + 127) / 128 * 128; }  // 128 query rows per CTA
 struct PrefillParams {

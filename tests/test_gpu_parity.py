@@ -209,6 +209,27 @@ def test_decode_ragged_lengths(oracle):
         assert rel_err(out[b], want) < REL_TOL, (b, T)
 
 
+def test_decode_many_sinks(oracle):
+    """More sink tokens than any fixed staging size: 20 sinks in one sequence,
+    every one merged into the decode output (no silent cap)."""
+    w = small_workload(8, 8, 4)
+    B, T = 2, 90
+    layer, perm = build_layer(w, B, 96, seed=21, max_sinks=24)
+    k, v = WL.make_kv(w, 21, B, T)
+    sinks = torch.zeros(B, T, dtype=torch.uint8)
+    sinks[0, 0:80:4] = 1  # 20 sinks
+    sinks[1, 0] = 1
+    layer.append(k, v, sinks)
+    q = WL.make_q(w, 21, B)
+    out = layer.decode(q).cpu().numpy()
+    got = cache_host(layer)
+    for b in range(B):
+        want = oracle_decode(oracle, layer, got, b, T, q[b].cpu().numpy(), w, perm, k[b].cpu().numpy(),
+                             v[b].cpu().numpy())
+        assert rel_err(out[b], want) < REL_TOL, b
+        assert cosine(out[b], want) > COS_TOL
+
+
 def test_decode_step_loop_vs_reference_semantics(oracle):
     """decode_step semantics: append the token, then attend with q at its
     position; several steps, each checked against the oracle."""

@@ -94,6 +94,40 @@ def test_prefill_rejects_bad_arguments():
         layer.prefill_attention(q.float())
 
 
+def test_prefill_rejects_more_than_16_sink_rows():
+    """The attention CTA stages at most 16 sink rows: larger max_sinks is refused loudly."""
+    w = WL.Workload("prefill", 1, 8, 8, 8, 4, 10000.0, 4, (10.0, 30.0))
+    cfg = P.LayerConfig(batch=1, num_q_heads=8, num_kv_heads=8, heads_per_group=4, max_tokens=16, max_sinks=17)
+    layer = P.RotateKVLayer(cfg, WL.calibration_perm(w, 3))
+    k, v = WL.make_kv(w, 3, 1, 8)
+    layer.append(k, v, torch.zeros(1, 8, dtype=torch.uint8))
+    q = torch.zeros(1, 8, 8, 128, dtype=torch.float16, device="cuda")
+    with pytest.raises(ValueError, match="16 sink rows"):
+        layer.prefill_attention(q, q_start=np.zeros(1, np.int64))
+
+
+def test_prefill_sixteen_sinks_and_ragged_blocks(oracle):
+    """16 sink rows (the staging maximum), 150 query rows (a partial 128-row
+    block), a second sequence with one sink."""
+    B, T = 2, 150
+    w = WL.Workload("prefill", B, 8, 8, T, 4, 10000.0, 4, (10.0, 30.0))
+    perm = WL.calibration_perm(w, 31)
+    cfg = P.LayerConfig(batch=B, num_q_heads=8, num_kv_heads=8, heads_per_group=4, max_tokens=T, max_sinks=16)
+    layer = P.RotateKVLayer(cfg, perm)
+    k, v = WL.make_kv(w, 31, B, T)
+    flags = torch.zeros(B, T, dtype=torch.uint8)
+    flags[0, 0:144:9] = 1  # 16 sinks
+    flags[1, 0] = 1
+    layer.append(k, v, flags)
+    gen = torch.Generator(device="cuda").manual_seed(33)
+    q = torch.randn(B, T, 8, 128, generator=gen, device="cuda").to(torch.float16)
+    out = layer.prefill_attention(q, q_start=np.zeros(B, np.int64)).cpu().numpy()
+    for b in range(B):
+        rows = list(range(0, T, 7)) + [T - 1]
+        want = expected_rows(oracle, layer, k, v, flags, q, perm, b, rows)
+        check(out[b, rows], want)
+
+
 @pytest.mark.parametrize("heads,g,T,sinks,seed", [(8, 4, 48, (0, 20), 11), (4, 4, 9, (0,), 12), (16, 4, 64, (0, 1, 63), 13)])
 def test_prefill_matches_reference_prefill(oracle, heads, g, T, sinks, seed):
     """Against the UNMODIFIED reference's prefill (identity projections: each
