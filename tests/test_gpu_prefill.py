@@ -150,3 +150,37 @@ def test_prefill_matches_reference_prefill(oracle, heads, g, T, sinks, seed):
     out = layer.prefill_attention(xt.reshape(1, T, heads, 128), q_start=np.zeros(1, np.int64)).cpu().numpy()
     want = oracle.ref_prefill(x.astype(np.float32), flags, perm, heads, 128, g, 10000.0)
     check(out[0].reshape(T, C), want)
+
+
+@pytest.mark.parametrize("cfg_id,B", [(1, 1), (3, 2)])
+def test_prefill_full_size_rows_match_decode(oracle, cfg_id, B):
+    """BASELINE shapes at full prompt length (config 1: 32 heads x 4096 tokens;
+    config 3: GQA 32/8 heads x 8192 tokens): sampled prompt rows must equal the
+    independent decode kernel run at seq_len = p + 1 with the same query (a
+    size-independent property), and the first rows the oracle."""
+    w = WL.CONFIGS[cfg_id]
+    T = w.tokens
+    perm = WL.calibration_perm(w, 40 + cfg_id)
+    cfg = P.LayerConfig(batch=B, num_q_heads=w.num_q_heads, num_kv_heads=w.num_kv_heads,
+                        heads_per_group=w.heads_per_group, max_tokens=T, max_sinks=4, rope_base=w.rope_base)
+    layer = P.RotateKVLayer(cfg, perm)
+    flags = torch.zeros(B, T, dtype=torch.uint8)
+    flags[:, 0] = 1
+    ks, vs = [], []
+    for t0 in range(0, T, 2048):
+        k, v = WL.make_kv(w, 40 + t0, B, min(2048, T - t0))
+        layer.append(k, v, flags[:, t0:t0 + k.shape[1]])
+        if t0 == 0:
+            ks.append(k)
+            vs.append(v)
+    gen = torch.Generator(device="cuda").manual_seed(41)
+    q = torch.randn(B, T, w.num_q_heads, 128, generator=gen, device="cuda").to(torch.float16)
+    out = layer.prefill_attention(q, q_start=np.zeros(B, np.int64)).cpu().numpy()
+    rows = [0, 1, 63, 64, 127, 128, 1000, T // 2 - 1, T // 2, T - 65, T - 1]
+    for p in rows:
+        dec = layer.decode(q[:, p].contiguous(), seq_len=np.full(B, p + 1, np.int64)).cpu().numpy()
+        for b in range(B):
+            check(out[b, p], dec[b])
+    k0, v0 = ks[0], vs[0]
+    want = expected_rows(oracle, layer, k0, v0, flags, q, perm, 0, [0, 5, 70, 300])
+    check(out[0, [0, 5, 70, 300]], want)
