@@ -10,6 +10,7 @@
 //   LayerKVCache(cfg, C); append(k, v, sink)     DeviceLayerCache(desc, perm); append(...)
 //   LayerKVCache::size()/is_sink()               DeviceLayerCache::size(b)/sink_count(b)
 //   decode_step(...) attention half              DeviceLayerCache::decode_attention(q, out)
+//   prefill(...) attention half                  DeviceLayerCache::prefill_attention(q, n, q_start, out)
 //
 // Exceptions are the reference's: std::invalid_argument, std::out_of_range,
 // std::runtime_error (CUDA failures included).
@@ -148,6 +149,8 @@ public:
         cudaFree(ws_);
         cudaFree(plan_);
         cudaFree(dev_pos_);
+        cudaFree(dev_qs_);
+        cudaFree(pf_ws_);
     }
 
     int64_t size(int b) const { return len_.at(static_cast<size_t>(b)); }
@@ -209,6 +212,37 @@ public:
         check_cuda(cudaStreamSynchronize(stream_), "decode");
     }
 
+    // The attention half of prefill (proj/src/pipeline.cpp:156-191: reconstruct_cache,
+    // causal reference_attention): q [B][num_q][Hq][d] fp16 device, row i of
+    // sequence b at position q_start[b] + i attending to cache tokens
+    // 0 .. q_start[b] + i; out [B][num_q][Hq][d] fp32 device.
+    void prefill_attention(const uint16_t* q, int64_t num_q, const std::vector<int64_t>& q_start, float* out) {
+        if (q_start.size() != len_.size()) throw std::invalid_argument("prefill: q_start must hold one entry per sequence");
+        if (num_q < 0) throw std::invalid_argument("prefill: negative query count");
+        int64_t mx = 1;
+        for (size_t b = 0; b < len_.size(); ++b) {
+            if (q_start[b] < 0 || q_start[b] + num_q > len_[b])
+                throw std::out_of_range("prefill: query rows past the cache length");
+            mx = std::max(mx, len_[b]);
+        }
+        if (num_q == 0) return;
+        const size_t need = rkv_prefill_workspace_bytes(&desc_, num_q, mx);
+        if (need > pf_ws_bytes_) {
+            cudaFree(pf_ws_);
+            pf_ws_ = nullptr;
+            check_cuda(cudaMalloc(&pf_ws_, need), "cudaMalloc prefill workspace");
+            pf_ws_bytes_ = need;
+        }
+        if (!dev_qs_) check_cuda(cudaMalloc(&dev_qs_, len_.size() * sizeof(int64_t)), "cudaMalloc q_start");
+        check_cuda(cudaMemcpyAsync(dev_qs_, q_start.data(), len_.size() * sizeof(int64_t), cudaMemcpyHostToDevice,
+                                   stream_), "q_start");
+        check_cuda(cudaMemcpyAsync(dev_pos_, len_.data(), len_.size() * sizeof(int64_t), cudaMemcpyHostToDevice,
+                                   stream_), "seq_len");
+        check(rkv_prefill_attention(&desc_, q, num_q, dev_qs_, dev_pos_, mx, &cache_, plan_,
+                                    static_cast<const float*>(rope_), out, pf_ws_, pf_ws_bytes_, stream_));
+        check_cuda(cudaStreamSynchronize(stream_), "prefill");
+    }
+
     // LayerKVCache::serialize (proj/src/kv_cache.cpp:119-139) of sequence b;
     // format RKV_WIRE_REFERENCE (the reference's bytes, e4m3 scales) or
     // RKV_WIRE_FP16_SCALE (lossless for fp16 scales).
@@ -246,6 +280,9 @@ private:
     void* plan_ = nullptr;
     size_t plan_bytes_ = 0;
     int64_t* dev_pos_ = nullptr;
+    int64_t* dev_qs_ = nullptr;
+    void* pf_ws_ = nullptr;
+    size_t pf_ws_bytes_ = 0;
     std::vector<int32_t> perm_host_;
 };
 

@@ -156,6 +156,39 @@ int main() {
             CHECK(err / mx < 2e-3);
         }
 
+        // prefill attention half: the last prompt row (position T-1) with the decode query
+        // must reproduce the decode output; rows past the cache are refused
+        {
+            const size_t row = static_cast<size_t>(H) * D;
+            std::vector<uint16_t> qp(static_cast<size_t>(B) * T * row);
+            for (size_t i = 0; i < qp.size(); ++i) qp[i] = q[i % q.size()];
+            for (int b = 0; b < B; ++b)
+                std::copy(q.begin() + static_cast<long>(b * row), q.begin() + static_cast<long>((b + 1) * row),
+                          qp.begin() + static_cast<long>((static_cast<size_t>(b) * T + T - 1) * row));
+            uint16_t* dqp = nullptr;
+            float* dpo = nullptr;
+            cudaMalloc(&dqp, qp.size() * 2);
+            cudaMalloc(&dpo, qp.size() * 4);
+            cudaMemcpy(dqp, qp.data(), qp.size() * 2, cudaMemcpyHostToDevice);
+            cache.prefill_attention(dqp, T, std::vector<int64_t>(static_cast<size_t>(B), 0), dpo);
+            std::vector<float> po(qp.size());
+            cudaMemcpy(po.data(), dpo, po.size() * 4, cudaMemcpyDeviceToHost);
+            for (int b = 0; b < B; ++b) {
+                double mx = 0, err = 0;
+                for (size_t i = 0; i < row; ++i) {
+                    const double d = out[static_cast<size_t>(b) * row + i];
+                    mx = std::fmax(mx, std::fabs(d));
+                    err = std::fmax(err, std::fabs(d - po[(static_cast<size_t>(b) * T + T - 1) * row + i]));
+                }
+                std::printf("sequence %d: prefill last row vs decode rel err %.3g\n", b, err / mx);
+                CHECK(err / mx < 2e-3);
+            }
+            CHECK_THROWS_AS(cache.prefill_attention(dqp, T, std::vector<int64_t>(static_cast<size_t>(B), 1), dpo),
+                            std::out_of_range);
+            cudaFree(dqp);
+            cudaFree(dpo);
+        }
+
         // LayerKVCache::serialize / deserialize round trip (fp16-scale wire format)
         const std::vector<uint8_t> blob = cache.serialize(1, RKV_WIRE_FP16_SCALE);
         rotatekv_b200::DeviceLayerCache other(desc, perm);
