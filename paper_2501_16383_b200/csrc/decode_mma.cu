@@ -50,6 +50,7 @@
 
 #include "rkv_common.cuh"
 #include "rkv_mma.cuh"
+#include "rkv_umma.cuh"
 #include "rkv_internal.h"
 #include "rkv_layout.h"
 
@@ -472,8 +473,12 @@ __host__ __device__ inline MmaSmem gqa_smem(int C, int TT, int chunk) {
     return s;
 }
 
-template <int REP, int PW>
-__global__ void __launch_bounds__(32 * 4 * PW, 1) decode_gqa_kernel(DecodeParams p) {
+// TM: the 64 P.V accumulators and the 32 RoPE'd query registers of every lane
+// are parked in tensor memory between the phases that use them (tcgen05.st /
+// tcgen05.ld, a few instructions per tile), so the register peak is the larger
+// phase instead of their sum and two CTAs fit on an SM.
+template <int REP, int PW, bool TM>
+__global__ void __launch_bounds__(32 * 4 * PW, TM ? 2 : 1) decode_gqa_kernel(DecodeParams p) {
     static_assert(REP == 4, "decode_gqa_kernel: 4 q heads per KV head");
     constexpr int G = 2, N = 256, NJ = 2, TT = 8 * PW, PPT = TT / 2;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -522,7 +527,17 @@ __global__ void __launch_bounds__(32 * 4 * PW, 1) decode_gqa_kernel(DecodeParams
         for (int s = 0; s < kGqaNS; ++s) mbar_init(mbar + s, 1);
         mbar_fence_init();
     }
+    __shared__ uint32_t s_tmem;
+    if constexpr (TM) {
+        if (warp == 0) umma::alloc<256>(&s_tmem);
+        umma::fence_before();
+    }
     __syncthreads();
+    uint32_t tq = 0;  // this warp's columns: q (32) then accumulators (64), lanes of quarter warp & 3
+    if constexpr (TM) {
+        umma::fence_after();
+        tq = s_tmem + ((32u * (warp & 3)) << 16) + 96u * (warp >> 2);
+    }
     if (tid == 0)
         for (int it = 0; it < kGqaNS && it < ntiles; ++it) issue_tile(it);
 
@@ -628,8 +643,70 @@ __global__ void __launch_bounds__(32 * 4 * PW, 1) decode_gqa_kernel(DecodeParams
         for (int e = 0; e < 8; ++e)
 #pragma unroll
             for (int c = 0; c < 4; ++c) acc[h][e][c] = 0.f;
+    // tensor-memory parking (TM): q at columns [0, 32), accumulators [32, 96)
+    auto park_q = [&]() {
+        if constexpr (TM) {
+            uint32_t v[2][16];
+#pragma unroll
+            for (int f1 = 0; f1 < 2; ++f1)
+#pragma unroll
+                for (int r = 0; r < REP; ++r) {
+                    v[f1][4 * r] = __float_as_uint(QA[f1][r].x);
+                    v[f1][4 * r + 1] = __float_as_uint(QA[f1][r].y);
+                    v[f1][4 * r + 2] = __float_as_uint(QB[f1][r].x);
+                    v[f1][4 * r + 3] = __float_as_uint(QB[f1][r].y);
+                }
+            umma::st16(tq, v[0]);
+            umma::st16(tq + 16, v[1]);
+            umma::wait_st();
+        }
+    };
+    auto fetch_q = [&]() {
+        if constexpr (TM) {
+            uint32_t v[2][16];
+            umma::ld16(tq, v[0]);
+            umma::ld16(tq + 16, v[1]);
+            umma::wait_ld(v[0]);
+            umma::wait_ld(v[1]);
+#pragma unroll
+            for (int f1 = 0; f1 < 2; ++f1)
+#pragma unroll
+                for (int r = 0; r < REP; ++r) {
+                    QA[f1][r] = make_float2(__uint_as_float(v[f1][4 * r]), __uint_as_float(v[f1][4 * r + 1]));
+                    QB[f1][r] = make_float2(__uint_as_float(v[f1][4 * r + 2]), __uint_as_float(v[f1][4 * r + 3]));
+                }
+        }
+    };
+    auto park_acc = [&]() {
+        if constexpr (TM) {
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+                uint32_t v[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] = __float_as_uint(acc[q4 >> 1][4 * (q4 & 1) + (i >> 2)][i & 3]);
+                umma::st16(tq + 32 + 16 * q4, v);
+            }
+            umma::wait_st();
+        }
+    };
+    auto fetch_acc = [&]() {
+        if constexpr (TM) {
+            uint32_t v[4][16];
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) umma::ld16(tq + 32 + 16 * q4, v[q4]);
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+                umma::wait_ld(v[q4]);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) acc[q4 >> 1][4 * (q4 & 1) + (i >> 2)][i & 3] = __uint_as_float(v[q4][i]);
+            }
+        }
+    };
+    park_q();
+    park_acc();
 
     auto compute_tile = [&](int it, int slot) {
+        fetch_q();
         const int64_t t0 = t_begin + static_cast<int64_t>(it) * TT;
         const int nv = static_cast<int>(lmin64(TT, t_end - t0));
         const unsigned char* st = smem + lay.stages + slot * lay.stage_bytes;
@@ -713,6 +790,7 @@ __global__ void __launch_bounds__(32 * 4 * PW, 1) decode_gqa_kernel(DecodeParams
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
         const float m_new = fmaxf(m_run, mx);
+        fetch_acc();
         if (__any_sync(0xffffffffu, m_new > m_run)) {
             const float alpha = m_new > m_run ? ex2(m_run - m_new) : 1.0f;
             l_part *= alpha;
@@ -759,6 +837,7 @@ __global__ void __launch_bounds__(32 * 4 * PW, 1) decode_gqa_kernel(DecodeParams
                 mma1688(acc[h][e], (e < 5 ? xl : xls) & m, (e < 5 ? xh : xhs) & m, bv[h]);
             }
         }
+        park_acc();
     };
 
     __syncthreads();  // mask words and plan
@@ -784,6 +863,7 @@ __global__ void __launch_bounds__(32 * 4 * PW, 1) decode_gqa_kernel(DecodeParams
     lsum += __shfl_xor_sync(0xffffffffu, lsum, 2);
     zsum += __shfl_xor_sync(0xffffffffu, zsum, 1);
     zsum += __shfl_xor_sync(0xffffffffu, zsum, 2);
+    fetch_acc();
     const int64_t rbase = (static_cast<int64_t>(b) * p.NP + static_cast<int64_t>(split) * PW + pw) * Hq;
     if (tl == 0) {
         const int hq = (gam * G + kvh) * REP + (g & 3);
@@ -810,6 +890,14 @@ __global__ void __launch_bounds__(32 * 4 * PW, 1) decode_gqa_kernel(DecodeParams
                 }
             }
         }
+    if constexpr (TM) {
+        umma::fence_before();
+        __syncthreads();
+        if (warp == 0) {
+            umma::fence_after();
+            umma::dealloc<256>(s_tmem);
+        }
+    }
 }
 
 }  // namespace
@@ -826,8 +914,15 @@ int gqa_pw() {
     if (const char* e = std::getenv("RKV_GQA_PW")) pw = std::max(2, std::min(4, std::atoi(e)));
     return pw;
 }
+bool gqa_tmem() {
+    const char* e = std::getenv("RKV_GQA_TMEM");
+    return !(e && std::atoi(e) == 0);
+}
 template <int PW>
-void* gqa_kernel_ptr() { return reinterpret_cast<void*>(decode_gqa_kernel<4, PW>); }
+void* gqa_kernel_ptr() {
+    return gqa_tmem() ? reinterpret_cast<void*>(decode_gqa_kernel<4, PW, true>)
+                      : reinterpret_cast<void*>(decode_gqa_kernel<4, PW, false>);
+}
 void* gqa_kernel(int pw) {
     switch (pw) {
         case 4: return gqa_kernel_ptr<4>();
