@@ -154,6 +154,29 @@ rkv_status rkv_decode_attention(const rkv_layer_desc* desc, const uint16_t* q, c
                                 const float* rope_table, float* out, void* workspace, size_t ws_bytes,
                                 void* stream);
 
+/* Sequence-parallel decode (batch < GPUs, split-K across ranks
+ * plus one small all-gather).  A rank attends to the quantized cache tokens
+ * [tok_begin[b], tok_end[b]) of every sequence (device [B] int64; tok_begin a
+ * multiple of 64, tok_end a multiple of 64 or >= seq_len; sink tokens are
+ * skipped) with q at position seq_len[b] - 1, and emits one unnormalised
+ * partial per (b, h):
+ *   part_ml : [B][Hq][2] fp32 (running max in log2 units, sum of weights)
+ *   part_o  : [B][Hq][d] fp32 (rotated V frame)
+ *   max_span: host bound of tok_end - tok_begin (sizes the split plan)
+ *   workspace: rkv_decode_workspace_bytes(desc, max_span) bytes
+ * rkv_decode_merge then folds num_parts gathered partials, laid out
+ * [B][num_parts][Hq][2] and [B][num_parts][Hq][d], with the exact sink rows
+ * and V's inverse rotation into out [B][Hq][d] -- the same combine the
+ * single-GPU decode runs over its splits.  Stream-ordered. */
+rkv_status rkv_decode_attention_partial(const rkv_layer_desc* desc, const uint16_t* q, const int64_t* seq_len,
+                                        const int64_t* tok_begin, const int64_t* tok_end, int64_t max_span,
+                                        const rkv_cache* cache, const void* layer_plan, const float* rope_table,
+                                        float* part_ml, float* part_o, void* workspace, size_t workspace_bytes,
+                                        void* stream);
+rkv_status rkv_decode_merge(const rkv_layer_desc* desc, const uint16_t* q, const int64_t* seq_len, int32_t num_parts,
+                            const float* parts_ml, const float* parts_o, const rkv_cache* cache,
+                            const float* rope_table, float* out, void* stream);
+
 /* Causal attention of a block of queries over the cache (the
  * attention half of prefill, proj/src/pipeline.cpp:156-191 -- reconstruct_cache
  * then causal reference_attention, proj/src/attention.cpp:20-49):

@@ -125,8 +125,9 @@ __global__ void __launch_bounds__(max_threads<N>(), 1) decode_split_kernel(Decod
     const int g = lg % NG, pp = lg / NG;
     const int b = blockIdx.y, split = blockIdx.x;
     const int64_t T = p.seq_len[b];
-    const int64_t t_begin = static_cast<int64_t>(split) * p.chunk;
-    const int64_t t_end = lmin(T, t_begin + p.chunk);
+    const int64_t tb = p.tok_begin ? p.tok_begin[b] : 0, te = p.tok_end ? lmin(p.tok_end[b], T) : T;
+    const int64_t t_begin = tb + static_cast<int64_t>(split) * p.chunk;
+    const int64_t t_end = lmin(te, t_begin + p.chunk);
 
     if (t_begin >= t_end) {  // empty split: neutral partials for every lane group
         for (int i = tid; i < PP * Hq; i += NT) {
@@ -484,6 +485,14 @@ __global__ void __launch_bounds__(128) decode_combine_kernel(DecodeParams p) {
             rot = make_float4(rot.x + wk * o.x, rot.y + wk * o.y, rot.z + wk * o.z, rot.w + wk * o.w);
         }
     }
+    if (p.partial_ml) {  // sequence-parallel partial: merged (m, l) and the unnormalised rotated o'
+        if (lane == 0) {
+            p.partial_ml[wid * 2] = M;
+            p.partial_ml[wid * 2 + 1] = L;
+        }
+        reinterpret_cast<float4*>(p.out + wid * 128)[lane] = rot;
+        return;
+    }
     // sinks: logits from q and the raw fp16 key rows, both RoPE'd (log2 domain)
     const int nsink = min(p.cache.sink_count[b], p.max_sinks);
     float4 raw = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -542,7 +551,7 @@ __global__ void __launch_bounds__(128) decode_combine_kernel(DecodeParams p) {
             x[j] = upper ? y - x[j] : x[j] + y;
         }
     }
-    const float inv = 1.0f / L, nrm = 1.0f / sqrtf(128.0f);
+    const float inv = L > 0.f ? 1.0f / L : 0.f, nrm = 1.0f / sqrtf(128.0f);
     reinterpret_cast<float4*>(p.out + (static_cast<int64_t>(b) * p.Hq + h) * 128)[lane] =
         make_float4((x[0] * nrm + raw.x) * inv, (x[1] * nrm + raw.y) * inv, (x[2] * nrm + raw.z) * inv,
                     (x[3] * nrm + raw.w) * inv);

@@ -114,8 +114,9 @@ __global__ void __launch_bounds__(320, kCtasPerSm) decode_mma_kernel(DecodeParam
     const int gam = warp % NG;
     const int b = blockIdx.y, split = blockIdx.x;
     const int64_t T = p.seq_len[b];
-    const int64_t t_begin = static_cast<int64_t>(split) * p.chunk;
-    const int64_t t_end = lmin64(T, t_begin + p.chunk);
+    const int64_t tb = p.tok_begin ? p.tok_begin[b] : 0, te = p.tok_end ? lmin64(p.tok_end[b], T) : T;
+    const int64_t t_begin = tb + static_cast<int64_t>(split) * p.chunk;
+    const int64_t t_end = lmin64(te, t_begin + p.chunk);
 
     if (t_begin >= t_end) {  // empty split: neutral partials
         for (int i = tid; i < Hq; i += NT) {
@@ -492,8 +493,9 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? 2 : 1) decode_gqa_kernel(Dec
     const int gam = warp % NG, pw = warp / NG;
     const int b = blockIdx.y, split = blockIdx.x;
     const int64_t T = p.seq_len[b];
-    const int64_t t_begin = static_cast<int64_t>(split) * p.chunk;
-    const int64_t t_end = lmin64(T, t_begin + p.chunk);
+    const int64_t tb = p.tok_begin ? p.tok_begin[b] : 0, te = p.tok_end ? lmin64(p.tok_end[b], T) : T;
+    const int64_t t_begin = tb + static_cast<int64_t>(split) * p.chunk;
+    const int64_t t_end = lmin64(te, t_begin + p.chunk);
 
     if (t_begin >= t_end) {  // empty split: neutral partials
         for (int i = tid; i < PW * Hq; i += NT) {

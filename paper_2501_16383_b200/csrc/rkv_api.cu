@@ -349,6 +349,40 @@ rkv_status rkv_layer_plan_init(const rkv_layer_desc* desc, const int32_t* perm, 
     return RKV_OK;
 }
 
+namespace {
+rkv::DecodeParams decode_params(const rkv_layer_desc* desc, const rkv::DecodePlan& pl, const uint16_t* q,
+                                const int64_t* seq_len, const rkv_cache* cache, const void* layer_plan,
+                                const float* rope_table, float* out, void* workspace) {
+    const size_t rows = static_cast<size_t>(desc->batch) * pl.NP * desc->num_q_heads;
+    rkv::DecodeParams p{};
+    p.q = q;
+    p.seq_len = seq_len;
+    p.plan = static_cast<const uint32_t*>(layer_plan);
+    p.rope = reinterpret_cast<const float4*>(rope_table);
+    p.cache = *cache;
+    if (workspace) {
+        p.ws_ml = static_cast<float*>(workspace);
+        p.ws_o = reinterpret_cast<float*>(static_cast<char*>(workspace) + al256(rows * 2 * sizeof(float)));
+    }
+    p.out = out;
+    p.max_tokens = desc->max_tokens;
+    p.B = desc->batch;
+    p.Hq = desc->num_q_heads;
+    p.Hkv = desc->num_kv_heads;
+    p.C = desc->num_kv_heads * desc->head_dim;
+    p.S = pl.S;
+    p.NP = pl.NP;
+    p.max_sinks = desc->max_sinks;
+    p.chunk = pl.chunk;
+    p.P = pl.P;
+    p.P_pairs = pl.PP;
+    p.stages = pl.stages;
+    p.k_norm = 1.0f / std::sqrt(static_cast<float>(desc->heads_per_group * desc->head_dim));
+    p.qscale = rkv::kLog2eHost / std::sqrt(static_cast<float>(desc->head_dim));
+    return p;
+}
+}  // namespace
+
 size_t rkv_decode_workspace_bytes(const rkv_layer_desc* desc, int64_t max_seq_len) {
     if (validate(desc) != RKV_OK) return 0;
     rkv::DecodePlan pl = rkv::plan_decode(*desc, max_seq_len);
@@ -373,32 +407,54 @@ rkv_status rkv_decode_attention(const rkv_layer_desc* desc, const uint16_t* q, c
     rkv::DecodePlan pl = rkv::plan_decode(*desc, max_seq_len);
     if (!pl.ok)
         return fail(RKV_ERR_INVALID_ARGUMENT, "decode_attention: layer shape exceeds the sm_100a kernel's tile budget");
-    const size_t rows = static_cast<size_t>(desc->batch) * pl.NP * desc->num_q_heads;
-    rkv::DecodeParams p{};
-    p.q = q;
-    p.seq_len = seq_len;
-    p.plan = static_cast<const uint32_t*>(layer_plan);
-    p.rope = reinterpret_cast<const float4*>(rope_table);
-    p.cache = *cache;
-    p.ws_ml = static_cast<float*>(workspace);
-    p.ws_o = reinterpret_cast<float*>(static_cast<char*>(workspace) + al256(rows * 2 * sizeof(float)));
-    p.out = out;
-    p.max_tokens = desc->max_tokens;
-    p.B = desc->batch;
-    p.Hq = desc->num_q_heads;
-    p.Hkv = desc->num_kv_heads;
-    p.C = desc->num_kv_heads * desc->head_dim;
-    p.S = pl.S;
-    p.NP = pl.NP;
-    p.max_sinks = desc->max_sinks;
-    p.chunk = pl.chunk;
-    p.P = pl.P;
-    p.P_pairs = pl.PP;
-    p.stages = pl.stages;
-    p.k_norm = 1.0f / std::sqrt(static_cast<float>(desc->heads_per_group * desc->head_dim));
-    p.qscale = rkv::kLog2eHost / std::sqrt(static_cast<float>(desc->head_dim));
+    rkv::DecodeParams p = decode_params(desc, pl, q, seq_len, cache, layer_plan, rope_table, out, workspace);
     cudaError_t e = rkv::launch_decode(*desc, pl, p, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "decode_attention");
+    return RKV_OK;
+}
+
+rkv_status rkv_decode_attention_partial(const rkv_layer_desc* desc, const uint16_t* q, const int64_t* seq_len,
+                                        const int64_t* tok_begin, const int64_t* tok_end, int64_t max_span,
+                                        const rkv_cache* cache, const void* layer_plan, const float* rope_table,
+                                        float* part_ml, float* part_o, void* workspace, size_t ws_bytes,
+                                        void* stream) {
+    rkv_status st = validate(desc);
+    if (st != RKV_OK) return st;
+    if ((st = check_cache(cache)) != RKV_OK) return st;
+    if (!q || !seq_len || !tok_begin || !tok_end || !layer_plan || !rope_table || !part_ml || !part_o || !workspace)
+        return fail(RKV_ERR_INVALID_ARGUMENT, "decode_attention_partial: null argument");
+    if (max_span < 1 || max_span > desc->max_tokens)
+        return fail(RKV_ERR_OUT_OF_RANGE, "decode_attention_partial: max_span must be in [1, max_tokens]");
+    if (ws_bytes < rkv_decode_workspace_bytes(desc, max_span))
+        return fail(RKV_ERR_INVALID_ARGUMENT, "decode_attention_partial: workspace too small");
+    rkv::DecodePlan pl = rkv::plan_decode(*desc, max_span);
+    if (!pl.ok)
+        return fail(RKV_ERR_INVALID_ARGUMENT, "decode_attention_partial: layer shape exceeds the kernel's tile budget");
+    rkv::DecodeParams p = decode_params(desc, pl, q, seq_len, cache, layer_plan, rope_table, part_o, workspace);
+    p.tok_begin = tok_begin;
+    p.tok_end = tok_end;
+    p.partial_ml = part_ml;
+    cudaError_t e = rkv::launch_decode(*desc, pl, p, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "decode_attention_partial");
+    return RKV_OK;
+}
+
+rkv_status rkv_decode_merge(const rkv_layer_desc* desc, const uint16_t* q, const int64_t* seq_len, int32_t num_parts,
+                            const float* parts_ml, const float* parts_o, const rkv_cache* cache,
+                            const float* rope_table, float* out, void* stream) {
+    rkv_status st = validate(desc);
+    if (st != RKV_OK) return st;
+    if ((st = check_cache(cache)) != RKV_OK) return st;
+    if (!q || !seq_len || !parts_ml || !parts_o || !rope_table || !out)
+        return fail(RKV_ERR_INVALID_ARGUMENT, "decode_merge: null argument");
+    if (num_parts < 1) return fail(RKV_ERR_INVALID_ARGUMENT, "decode_merge: num_parts must be >= 1");
+    rkv::DecodePlan pl{};
+    pl.NP = num_parts;
+    rkv::DecodeParams p = decode_params(desc, pl, q, seq_len, cache, nullptr, rope_table, out, nullptr);
+    p.ws_ml = const_cast<float*>(parts_ml);  // [B][num_parts][Hq][2]
+    p.ws_o = const_cast<float*>(parts_o);    // [B][num_parts][Hq][d]
+    cudaError_t e = rkv::launch_decode_combine(p, desc->batch, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "decode_merge");
     return RKV_OK;
 }
 

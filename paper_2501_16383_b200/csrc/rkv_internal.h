@@ -30,7 +30,11 @@ struct QuantParams {
 
 struct DecodeParams {
     const uint16_t* q;
-    const int64_t* seq_len;
+    const int64_t* seq_len;    // [B] cache length; q sits at position seq_len - 1
+    const int64_t* tok_begin;  // [B] or null: attend to cache tokens [tok_begin, tok_end) only
+    const int64_t* tok_end;    //     (sequence-parallel partials; multiples of 64 apart from seq_len)
+    float* partial_ml;         // non-null: the combine emits the merged partial (m, l) here and the
+                               // unnormalised rotated o' in out, without sinks or H_128
     const uint32_t* plan;  // rkv_layer_plan_init (rkv_layout.h)
     const float4* rope;  // [max_pos/2][128]: section 1 (cos p0, cos p1, sin p0, sin p1) x 64, section 2
                          // two [32] frequency-pair rows (decode_attention.cu, kRopeRow)

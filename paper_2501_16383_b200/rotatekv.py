@@ -83,6 +83,9 @@ def lib():
         L.rkv_decode_workspace_bytes.restype = C.c_size_t
         L.rkv_decode_workspace_bytes.argtypes = [D, C.c_int64]
         L.rkv_decode_attention.argtypes = [D, P, P, C.c_int64, C.POINTER(CacheView), P, P, P, P, C.c_size_t, P]
+        L.rkv_decode_attention_partial.argtypes = [D, P, P, P, P, C.c_int64, C.POINTER(CacheView), P, P, P, P, P,
+                                                   C.c_size_t, P]
+        L.rkv_decode_merge.argtypes = [D, P, P, C.c_int32, P, P, C.POINTER(CacheView), P, P, P]
         L.rkv_layer_plan_bytes.restype = C.c_size_t
         L.rkv_layer_plan_bytes.argtypes = [D]
         L.rkv_layer_plan_build.argtypes = [D, P, P, C.c_size_t, C.POINTER(C.c_int32)]
@@ -109,7 +112,7 @@ def lib():
                      "rkv_quantize_kv", "rkv_decode_attention", "rkv_rotate_keys", "rkv_calibrate_reorder",
                      "rkv_detect_sinks", "rkv_detect_sinks_device", "rkv_layer_plan_build", "rkv_layer_plan_init",
                      "rkv_calibrate_reorder_device", "rkv_cache_export", "rkv_cache_import",
-                     "rkv_prefill_attention"):
+                     "rkv_prefill_attention", "rkv_decode_attention_partial", "rkv_decode_merge"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -437,6 +440,52 @@ class RotateKVLayer:
         _check(lib().rkv_decode_attention(C.byref(self._desc), _ptr(q), _ptr(self._lens_t), msl,
                                           C.byref(self._view), _ptr(self.plan), _ptr(self.rope), _ptr(out),
                                           _ptr(ws), need, self._stream()))
+        return out
+
+    # -- sequence-parallel decode (fewer sequences than GPUs)
+    def decode_partial(self, q, tok_begin, tok_end, seq_len=None):
+        """This rank's share of a decode step: attend to cache tokens
+        [tok_begin[b], tok_end[b]) only (sinks excluded), q at position
+        seq_len-1.  Returns (ml [B, Hq, 2], o [B, Hq, 128]) fp32 partials in the
+        rotated V frame, to be all-gathered and folded by merge_partials."""
+        torch = self.torch
+        B, Hq = self.cfg.batch, self.cfg.num_q_heads
+        if q.dtype != torch.float16 or tuple(q.shape) != (B, Hq, self.cfg.head_dim):
+            raise ValueError("decode_step: input must have d_model elements")
+        lens = self.lengths if seq_len is None else _np(seq_len, np.int64)
+        if np.any(lens < 1) or np.any(lens > self.lengths):
+            raise ValueError("decode_step: position must equal current cache length")
+        tb, te = _np(tok_begin, np.int64), _np(tok_end, np.int64)
+        if tb.shape != (B,) or te.shape != (B,) or np.any(tb < 0) or np.any(te < tb):
+            raise ValueError("decode_partial: token ranges must be [B] with 0 <= begin <= end")
+        live = tb < np.minimum(te, lens)  # empty ranges need no alignment
+        if np.any(live & (tb % 64 != 0)) or np.any(live & (te % 64 != 0) & (te < lens)):
+            raise ValueError("decode_partial: range bounds must be multiples of 64 (or the sequence end)")
+        span = int(max(1, int((np.minimum(te, lens) - tb).max())))
+        ml = torch.empty((B, Hq, 2), dtype=torch.float32, device=self.device)
+        o = torch.empty((B, Hq, self.cfg.head_dim), dtype=torch.float32, device=self.device)
+        ws, need = self.workspace(span)
+        dev = [torch.from_numpy(a).to(self.device) for a in (lens, tb, te)]
+        _check(lib().rkv_decode_attention_partial(C.byref(self._desc), _ptr(q.contiguous()), _ptr(dev[0]), _ptr(dev[1]),
+                                                  _ptr(dev[2]), span, C.byref(self._view), _ptr(self.plan),
+                                                  _ptr(self.rope), _ptr(ml), _ptr(o), _ptr(ws), need, self._stream()))
+        return ml, o
+
+    def merge_partials(self, q, parts_ml, parts_o, seq_len=None, out=None):
+        """Fold gathered partials ([B, R, Hq, 2], [B, R, Hq, 128]) with the sink
+        rows and V's inverse rotation: the decode output for q."""
+        torch = self.torch
+        B, Hq = self.cfg.batch, self.cfg.num_q_heads
+        lens = self.lengths if seq_len is None else _np(seq_len, np.int64)
+        R = parts_ml.shape[1]
+        if tuple(parts_ml.shape) != (B, R, Hq, 2) or tuple(parts_o.shape) != (B, R, Hq, self.cfg.head_dim):
+            raise ValueError("merge_partials: partials must be [B, R, Hq, 2] and [B, R, Hq, d]")
+        if out is None:
+            out = torch.empty((B, Hq, self.cfg.head_dim), dtype=torch.float32, device=self.device)
+        lens_t = torch.from_numpy(lens).to(self.device)
+        _check(lib().rkv_decode_merge(C.byref(self._desc), _ptr(q.contiguous()), _ptr(lens_t), R,
+                                      _ptr(parts_ml.contiguous()), _ptr(parts_o.contiguous()), C.byref(self._view),
+                                      _ptr(self.rope), _ptr(out), self._stream()))
         return out
 
     def decode_device(self, q, seq_len_t, max_seq_len, out, ws, ws_bytes):

@@ -48,3 +48,31 @@ def gather_batch(local, global_batch: int, group=None):
         _, c = batch_shard(global_batch, world, r)
         out.append(parts[r][:c])
     return torch.cat(out, 0)
+
+
+def token_shard(seq_len: int, world: int, rank: int, align: int = 64) -> tuple[int, int]:
+    """Sequence-parallel decode (batch < GPUs): rank's contiguous token range
+    [begin, end) of one sequence, bounds on multiples of `align` (the decode
+    kernels' tile alignment) and sizes within one `align` block of each other.
+    Every token lands in exactly one rank's range; ranks past the end get an
+    empty range."""
+    if seq_len < 0 or world < 1 or not 0 <= rank < world or align < 1:
+        raise ValueError("token_shard: need seq_len >= 0, world >= 1, 0 <= rank < world, align >= 1")
+    blocks = (seq_len + align - 1) // align
+    start, count = batch_shard(blocks, world, rank)
+    return min(seq_len, start * align), min(seq_len, (start + count) * align)
+
+
+def merge_partials_reference(ml, o):
+    """Host restatement of the partial fold (log2-domain online softmax) used
+    by rkv_decode_merge before the sink rows and H_128: ml [R, 2], o [R, d] ->
+    (m, l, o) of the union.  For tests of the multi-rank host logic."""
+    import numpy as np
+
+    ml = np.asarray(ml, np.float64)
+    o = np.asarray(o, np.float64)
+    m = ml[:, 0].max()
+    if not np.isfinite(m):
+        return -np.inf, 0.0, np.zeros(o.shape[1])
+    w = np.where(np.isfinite(ml[:, 0]), np.exp2(ml[:, 0] - m), 0.0)
+    return m, float((w * ml[:, 1]).sum()), (w[:, None] * o).sum(0)

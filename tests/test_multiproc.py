@@ -87,3 +87,68 @@ def test_shard_rows_views():
     x = np.arange(10 * 3).reshape(10, 3)
     parts = [shard_rows(x, 4, r) for r in range(4)]
     assert np.array_equal(np.concatenate(parts), x)
+
+
+def test_token_shard_partition():
+    from paper_2501_16383_b200.sharding import token_shard
+
+    for T in (0, 1, 63, 64, 65, 700, 4097, 32768):
+        for world in (1, 2, 3, 8):
+            ranges = [token_shard(T, world, r) for r in range(world)]
+            covered = []
+            for a, b in ranges:
+                assert a <= b and (a == b or a % 64 == 0) and (b % 64 == 0 or b == T)
+                covered += list(range(a, b))
+            assert covered == list(range(T))
+    with pytest.raises(ValueError):
+        token_shard(10, 2, 2)
+
+
+def _seqpar_worker(rank, world, port, logits, values, out_q):
+    """Rank-local partial over its token range (a numpy stand-in for
+    rkv_decode_attention_partial), all-gathered over gloo, folded with the
+    host restatement of rkv_decode_merge's partial fold."""
+    from paper_2501_16383_b200.sharding import merge_partials_reference, token_shard
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    a, b = token_shard(len(logits), world, rank)
+    s, v = logits[a:b], values[a:b]
+    if b > a:
+        m = s.max()
+        w = np.exp2(s - m)
+        part = np.concatenate([[m, w.sum()], (w[:, None] * v).sum(0)])
+    else:
+        part = np.concatenate([[-np.inf, 0.0], np.zeros(values.shape[1])])
+    t = torch.from_numpy(part)
+    parts = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(parts, t)
+    ps = torch.stack(parts).numpy()
+    out_q.put((rank, merge_partials_reference(ps[:, :2], ps[:, 2:])))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_sequence_parallel_fold_matches_single_process():
+    rng = np.random.default_rng(11)
+    T, d = 300, 16
+    logits = rng.standard_normal(T) * 6
+    values = rng.standard_normal((T, d))
+    m = logits.max()
+    w = np.exp2(logits - m)
+    want = (w[:, None] * values).sum(0) / w.sum()
+    ctx = mp.get_context("spawn")
+    out_q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_seqpar_worker, args=(r, 2, port, logits, values, out_q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = dict(out_q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(2):
+        mm, ll, oo = results[r]
+        assert mm == m
+        np.testing.assert_allclose(oo / ll, want, rtol=1e-12, atol=1e-12)
