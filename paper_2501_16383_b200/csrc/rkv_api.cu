@@ -468,8 +468,8 @@ size_t prefill_tile_bytes(const rkv_layer_desc& d) {
 
 size_t rkv_prefill_workspace_bytes(const rkv_layer_desc* desc, int64_t num_q, int64_t max_seq_len) {
     if (validate(desc) != RKV_OK || num_q < 0 || max_seq_len < 0) return 0;
-    const size_t C = static_cast<size_t>(desc->num_kv_heads) * desc->head_dim, B = static_cast<size_t>(desc->batch);
-    const size_t rows = B * static_cast<size_t>(rkv::prefill_q_pad(num_q)) * desc->num_q_heads;
+    const size_t rows = static_cast<size_t>(desc->batch) * static_cast<size_t>(rkv::prefill_q_pad(num_q)) *
+                        static_cast<size_t>(desc->num_q_heads);
     return al256(prefill_tile_bytes(*desc)) + al256(rows * 512);
 }
 
@@ -493,7 +493,7 @@ rkv_status rkv_prefill_attention(const rkv_layer_desc* desc, const uint16_t* q, 
         return fail(RKV_ERR_INVALID_ARGUMENT, "prefill: at most 16 sink rows per sequence (max_sinks <= 16)");
     if (ws_bytes < rkv_prefill_workspace_bytes(desc, num_q, max_seq_len))
         return fail(RKV_ERR_INVALID_ARGUMENT, "prefill: workspace too small");
-    const size_t C = static_cast<size_t>(desc->num_kv_heads) * desc->head_dim, B = static_cast<size_t>(desc->batch);
+    const size_t C = static_cast<size_t>(desc->num_kv_heads) * desc->head_dim;
     const size_t tiles = al256(prefill_tile_bytes(*desc));
     char* w = static_cast<char*>(workspace);
     rkv::PrefillParams p{};
