@@ -766,7 +766,7 @@ cudaError_t launch_rope_table(const rkv_layer_desc& d, float4* table, int64_t ma
     if (e != cudaSuccess) return e;
     const int64_t npos = 2 * npairs;
     rope_table2_kernel<<<static_cast<unsigned>((npos * 32 + 255) / 256), 256, 0, s>>>(
-        table, npos, d.rope_base, d.heads_per_group == 4 ? 1 : 0);
+        table, npos, d.rope_base, decode_kind(d) == kDecodeMma && mma_layout_n(d) == 512 ? 1 : 0);
     return cudaGetLastError();
 }
 

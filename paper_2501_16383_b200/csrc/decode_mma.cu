@@ -96,9 +96,12 @@ constexpr int kPP = 2, kTT = 2 * kPP, kNS = 3, kCtasPerSm = 2;
 // G = 4 (N = 512), one q head per KV head.  NGC = number of FWHT groups
 // (C / 512) when known at compile time (8: LLaMA-2-7B, 10: 13B), so every
 // shared-memory offset folds into an immediate; 0 = taken from the launch.
-template <int G, int REP, int NGC>
+// AG = heads per rotation group of the layer (4, 2 or 1): the kernel always
+// works on 512-channel (pseudo-)groups; only the second FWHT factor differs
+// (hadamard_f2_frag) -- the head bits 7, 8 pass through it when AG < 4.
+template <int G, int REP, int NGC, int AG, bool SP = false>
 __global__ void __launch_bounds__(320, kCtasPerSm) decode_mma_kernel(DecodeParams p) {
-    static_assert(G == 4 && REP == 1, "decode_mma_kernel: G = 4, MHA");
+    static_assert(G == 4 && REP == 1 && (AG == 4 || AG == 2 || AG == 1), "decode_mma_kernel: MHA, 512-channel tiles");
     constexpr int N = 128 * G;
     constexpr int NJ = N / 128;  // MMA-1 instances per token (F2 bit 3, outer bit 6)
 
@@ -114,7 +117,8 @@ __global__ void __launch_bounds__(320, kCtasPerSm) decode_mma_kernel(DecodeParam
     const int gam = warp % NG;
     const int b = blockIdx.y, split = blockIdx.x;
     const int64_t T = p.seq_len[b];
-    const int64_t tb = p.tok_begin ? p.tok_begin[b] : 0, te = p.tok_end ? lmin64(p.tok_end[b], T) : T;
+    // SP (sequence-parallel partial): only cache tokens [tok_begin, tok_end)
+    const int64_t tb = SP ? p.tok_begin[b] : 0, te = SP ? lmin64(p.tok_end[b], T) : T;
     const int64_t t_begin = tb + static_cast<int64_t>(split) * p.chunk;
     const int64_t t_end = lmin64(te, t_begin + p.chunk);
 
@@ -219,8 +223,17 @@ __global__ void __launch_bounds__(320, kCtasPerSm) decode_mma_kernel(DecodeParam
 
     // ---- compute role constants
     const int g = lane >> 2, tl = lane & 3;
-    uint32_t AH[4];
+    uint32_t AH[4], AF2[4];
     hadamard16_frag(AH, lane, static_cast<uint32_t>(p.max_tokens >> 40));  // max_tokens <= 2^30
+    if constexpr (AG != 4) hadamard_f2_frag<AG>(AF2, lane, static_cast<uint32_t>(p.max_tokens >> 40));
+    // second FWHT factor: H_16 itself (AH) for AG = 4
+    auto mma_f2 = [&](float (&d)[4], uint32_t b0, uint32_t b1, const float (&c)[4]) {
+        if constexpr (AG == 4) {
+            mma16816(d, AH, b0, b1, c);
+        } else {
+            mma16816(d, AF2, b0, b1, c);
+        }
+    };
     // q: RoPE at T-1, x log2(e)/sqrt(d) x 1/sqrt(N).  Frequency pair (f, f+1),
     // f = 2tl + 8 f1 + 16 (g&3); head hq = 4 gam + (g>>2) + 2 rh.
     float2 P2[2][2], Q2[2][2];
@@ -301,8 +314,8 @@ __global__ void __launch_bounds__(320, kCtasPerSm) decode_mma_kernel(DecodeParam
                         const uint32_t l0 = pack_h2(sub_lo(ya[2 * f1], h0), sub_hi(ya[2 * f1 + 1], h0));
                         const uint32_t l1 = pack_h2(sub_lo(yb[2 * f1], h1), sub_hi(yb[2 * f1 + 1], h1));
                         float t4[4];
-                        mma16816(t4, AH, h0, h1, zero);
-                        mma16816(z[o], AH, l0, l1, t4);
+                        mma_f2(t4, h0, h1, zero);
+                        mma_f2(z[o], l0, l1, t4);
                     }
                     // RoPE (bit-6 butterfly folded into u, w) and q.k over the frequency pair
                     const float4 r4 = rope4[(2 * pq + tk) * 32 + fpi + 4 * f1];  // (u f, u f+1, w f, w f+1)
@@ -478,7 +491,7 @@ __host__ __device__ inline MmaSmem gqa_smem(int C, int TT, int chunk) {
 // are parked in tensor memory between the phases that use them (tcgen05.st /
 // tcgen05.ld, a few instructions per tile), so the register peak is the larger
 // phase instead of their sum and two CTAs fit on an SM.
-template <int REP, int PW, bool TM>
+template <int REP, int PW, bool TM, bool SP = false>
 __global__ void __launch_bounds__(32 * 4 * PW, TM ? 2 : 1) decode_gqa_kernel(DecodeParams p) {
     static_assert(REP == 4, "decode_gqa_kernel: 4 q heads per KV head");
     constexpr int G = 2, N = 256, NJ = 2, TT = 8 * PW, PPT = TT / 2;
@@ -493,7 +506,8 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? 2 : 1) decode_gqa_kernel(Dec
     const int gam = warp % NG, pw = warp / NG;
     const int b = blockIdx.y, split = blockIdx.x;
     const int64_t T = p.seq_len[b];
-    const int64_t tb = p.tok_begin ? p.tok_begin[b] : 0, te = p.tok_end ? lmin64(p.tok_end[b], T) : T;
+    // SP (sequence-parallel partial): only cache tokens [tok_begin, tok_end)
+    const int64_t tb = SP ? p.tok_begin[b] : 0, te = SP ? lmin64(p.tok_end[b], T) : T;
     const int64_t t_begin = tb + static_cast<int64_t>(split) * p.chunk;
     const int64_t t_end = lmin64(te, t_begin + p.chunk);
 
@@ -904,13 +918,30 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? 2 : 1) decode_gqa_kernel(Dec
 
 }  // namespace
 
-bool decode_mma_supported(int N, int REP, int C) {
-    if (N == 512) return REP == 1 && C / N * 32 <= kMmaMaxThreads;
-    if (N == 256) return REP == 4 && C / N <= 4;  // GQA kernel: 4 groups x 32 x PW threads
+// MHA (one q head per KV head) with G = 4, 2 or 1 heads per rotation group
+// runs on 512-channel tiles (C a multiple of 512); GQA with G = 2 and 4 q heads
+// per KV head has its own kernel (256-channel groups, at most 4 per CTA).
+bool decode_mma_supported(int G, int REP, int C) {
+    if (REP == 1 && (G == 4 || G == 2 || G == 1)) return C % 512 == 0 && C / 512 * 32 <= kMmaMaxThreads;
+    if (REP == 4 && G == 2) return C % 256 == 0 && C / 256 <= 4;
     return false;
 }
 
+int mma_layout_n(const rkv_layer_desc& d) {
+    return d.heads_per_group == 2 && d.num_q_heads == 4 * d.num_kv_heads ? 256 : 512;
+}
+
 namespace {
+using MhaKernel = void (*)(DecodeParams);
+// compile-time tile counts for the LLaMA-2-7B / 13B widths (8 and 10 tiles of 512 channels)
+template <int AG>
+MhaKernel mha_kernel_g(int NG, bool sp) {
+    if (sp) return decode_mma_kernel<4, 1, 0, AG, true>;  // partials: generic tile count
+    return NG == 10 ? decode_mma_kernel<4, 1, 10, AG> : NG == 8 ? decode_mma_kernel<4, 1, 8, AG> : decode_mma_kernel<4, 1, 0, AG>;
+}
+MhaKernel mha_kernel(int NG, int G, bool sp = false) {
+    return G == 1 ? mha_kernel_g<1>(NG, sp) : G == 2 ? mha_kernel_g<2>(NG, sp) : mha_kernel_g<4>(NG, sp);
+}
 int gqa_pw() {
     int pw = 2;
     if (const char* e = std::getenv("RKV_GQA_PW")) pw = std::max(2, std::min(4, std::atoi(e)));
@@ -925,7 +956,8 @@ void* gqa_kernel_ptr() {
     return gqa_tmem() ? reinterpret_cast<void*>(decode_gqa_kernel<4, PW, true>)
                       : reinterpret_cast<void*>(decode_gqa_kernel<4, PW, false>);
 }
-void* gqa_kernel(int pw) {
+void* gqa_kernel(int pw, bool sp = false) {
+    if (sp) return reinterpret_cast<void*>(decode_gqa_kernel<4, 2, true, true>);  // partials: default shape
     switch (pw) {
         case 4: return gqa_kernel_ptr<4>();
         case 3: return gqa_kernel_ptr<3>();
@@ -935,17 +967,18 @@ void* gqa_kernel(int pw) {
 }  // namespace
 
 int decode_kind(const rkv_layer_desc& d) {
-    const int N = d.heads_per_group * d.head_dim, REP = d.num_q_heads / d.num_kv_heads;
+    const int REP = d.num_q_heads / d.num_kv_heads;
     if (const char* e = std::getenv("RKV_DECODE_KERNEL"))
         if (std::strcmp(e, "simt") == 0) return kDecodeSimt;
-    return decode_mma_supported(N, REP, d.num_kv_heads * d.head_dim) ? kDecodeMma : kDecodeSimt;
+    if (d.head_dim != 128 || d.num_q_heads % d.num_kv_heads != 0) return kDecodeSimt;
+    return decode_mma_supported(d.heads_per_group, REP, d.num_kv_heads * d.head_dim) ? kDecodeMma : kDecodeSimt;
 }
 
 DecodePlan plan_decode_mma(const rkv_layer_desc& d, int64_t max_seq_len) {
     DecodePlan pl{};
     const int C = d.num_kv_heads * d.head_dim;
     pl.kind = kDecodeMma;
-    pl.N = d.heads_per_group * d.head_dim;
+    pl.N = mma_layout_n(d);
     pl.REP = d.num_q_heads / d.num_kv_heads;
     const int NG = C / pl.N;
     const bool gqa = pl.N == 256;
@@ -963,7 +996,7 @@ DecodePlan plan_decode_mma(const rkv_layer_desc& d, int64_t max_seq_len) {
     pl.per_sm = std::max(1, std::min(kCtasPerSm, static_cast<int>((227u * 1024u) / (pl.smem + 1024))));
     {
         int n = 0;
-        const void* kern = gqa ? gqa_kernel(PW) : reinterpret_cast<const void*>(decode_mma_kernel<4, 1, 0>);
+        const void* kern = gqa ? gqa_kernel(PW) : reinterpret_cast<const void*>(mha_kernel(NG, d.heads_per_group));
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pl.smem)) ==
                 cudaSuccess &&
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, pl.NT, pl.smem) == cudaSuccess && n > 0)
@@ -998,8 +1031,10 @@ DecodePlan plan_decode_mma(const rkv_layer_desc& d, int64_t max_seq_len) {
 }
 
 cudaError_t launch_decode_mma(const rkv_layer_desc& d, const DecodePlan& plan, const DecodeParams& p, cudaStream_t s) {
+    const bool sp = p.tok_begin != nullptr;
     if (plan.N == 256) {
-        const void* kern = gqa_kernel(plan.P);
+        if (sp && plan.P != 2) return cudaErrorNotSupported;  // partials are instantiated for the default PW = 2
+        const void* kern = gqa_kernel(plan.P, sp);
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(plan.smem));
         if (e != cudaSuccess) return e;
         DecodeParams pp = p;
@@ -1009,7 +1044,7 @@ cudaError_t launch_decode_mma(const rkv_layer_desc& d, const DecodePlan& plan, c
         return launch_decode_combine(p, d.batch, s);
     }
     const int NG = p.C / 512;
-    auto kern = NG == 10 ? decode_mma_kernel<4, 1, 10> : NG == 8 ? decode_mma_kernel<4, 1, 8> : decode_mma_kernel<4, 1, 0>;
+    auto kern = mha_kernel(p.C / 512, d.heads_per_group, sp);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(plan.smem));
     if (e != cudaSuccess) return e;
     kern<<<dim3(plan.S, d.batch), plan.NT, plan.smem, s>>>(p);

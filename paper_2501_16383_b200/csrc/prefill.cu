@@ -63,7 +63,9 @@ __device__ __forceinline__ void store_key_pair(const PrefillParams& p, int b, in
 
 // ------------------------------------------------------------------ 1. keys
 // CTA = (4-token tile, sequence), one warp per FWHT group.
-template <int G>
+// G = 4: 512-channel tiles (the MHA decode layout; AG = heads per rotation
+// group, 4, 2 or 1, picks the second FWHT factor); G = 2: GQA 256-channel groups.
+template <int G, int AG = G>
 __global__ void __launch_bounds__(512) reconstruct_keys_kernel(PrefillParams p) {
     constexpr int N = 128 * G, NJ = N / 128, TT = 4;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -110,8 +112,10 @@ __global__ void __launch_bounds__(512) reconstruct_keys_kernel(PrefillParams p) 
     __syncthreads();
     if (warp >= NG) return;
     const int gam = warp, g = lane >> 2, tl = lane & 3;
-    uint32_t AH[4];
+    uint32_t AH[4], AF2buf[4];
     hadamard16_frag(AH, lane, static_cast<uint32_t>(p.max_tokens >> 40));
+    if constexpr (AG != G) hadamard_f2_frag<AG>(AF2buf, lane, static_cast<uint32_t>(p.max_tokens >> 40));
+    uint32_t(&AF2)[4] = *(AG == G ? &AH : &AF2buf);  // second FWHT factor of the 512-channel tile
     const float kn = p.k_norm;
     const int swz = mma_swz(N, lane);
     const unsigned char* lbase = knat + gam * N * 4 + lane * NJ * 16;
@@ -151,8 +155,8 @@ __global__ void __launch_bounds__(512) reconstruct_keys_kernel(PrefillParams p) 
                         const uint32_t l0 = pack_h2(sub_lo(ya[2 * f1], h0), sub_hi(ya[2 * f1 + 1], h0));
                         const uint32_t l1 = pack_h2(sub_lo(yb[2 * f1], h1), sub_hi(yb[2 * f1 + 1], h1));
                         float t4[4];
-                        mma16816(t4, AH, h0, h1, zero);
-                        mma16816(z[o], AH, l0, l1, t4);
+                        mma16816(t4, AF2, h0, h1, zero);
+                        mma16816(z[o], AF2, l0, l1, t4);
                     }
 #pragma unroll
                     for (int rh = 0; rh < 2; ++rh) {
@@ -712,16 +716,19 @@ extern "C" int rkv_debug_prefill_cta(unsigned long long* out) {
 
 cudaError_t launch_prefill(const rkv_layer_desc& d, const PrefillParams& p, int64_t max_seq_len, cudaStream_t s) {
     const int C = p.C, W = C / 16, MG = C / 128;
-    const int N = d.heads_per_group * d.head_dim, NG = C / N;
+    const int N = mma_layout_n(d), NG = C / N;
     const size_t ksmem = 2 * static_cast<size_t>(C) * 4 + 4 * static_cast<size_t>(W + MG) * 4;
     const int nthreads = std::min(512, std::max(NG * 32, ((2 * W + 31) / 32) * 32));
     const dim3 kgrid(static_cast<unsigned>((max_seq_len + 3) / 4), static_cast<unsigned>(d.batch));
     cudaError_t e;
     if (N == 512) {
-        if ((e = cudaFuncSetAttribute(reconstruct_keys_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(ksmem))) != cudaSuccess)
+        auto kern = d.heads_per_group == 1   ? reconstruct_keys_kernel<4, 1>
+                    : d.heads_per_group == 2 ? reconstruct_keys_kernel<4, 2>
+                                             : reconstruct_keys_kernel<4, 4>;
+        if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ksmem))) !=
+            cudaSuccess)
             return e;
-        reconstruct_keys_kernel<4><<<kgrid, nthreads, ksmem, s>>>(p);
+        kern<<<kgrid, nthreads, ksmem, s>>>(p);
     } else if (N == 256) {
         if ((e = cudaFuncSetAttribute(reconstruct_keys_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(ksmem))) != cudaSuccess)

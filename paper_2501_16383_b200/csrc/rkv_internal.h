@@ -97,7 +97,8 @@ cudaError_t launch_decode(const rkv_layer_desc& d, const DecodePlan& plan, const
 cudaError_t launch_decode_combine(const DecodeParams& p, int B, cudaStream_t s);
 // decode_mma.cu (tensor-core FWHT kernel)
 int decode_kind(const rkv_layer_desc& d);  // kDecodeSimt / kDecodeMma (rkv_layout.h)
-bool decode_mma_supported(int N, int REP, int C);
+bool decode_mma_supported(int G, int REP, int C);
+int mma_layout_n(const rkv_layer_desc& d);  // channels per tensor-core FWHT tile: 512 (MHA) or 256 (GQA)
 DecodePlan plan_decode_mma(const rkv_layer_desc& d, int64_t max_seq_len);
 cudaError_t launch_decode_mma(const rkv_layer_desc& d, const DecodePlan& plan, const DecodeParams& p,
                               cudaStream_t s);

@@ -106,5 +106,25 @@ __device__ __forceinline__ void hadamard16_frag(uint32_t (&a)[4], int lane, uint
     a[3] ^= opaque_zero;
 }
 
+// A fragment of the second FWHT factor of a 512-channel (pseudo-)group, over
+// channel bits (4, 5, 7, 8) = k bits (0, 1, 2, 3):  AG = 4 (G = 4 heads per
+// rotation group): H_16;  AG = 2: H_8 on bits 4, 5, 7 and the identity on
+// bit 8 (two 256-channel groups);  AG = 1: H_4 on bits 4, 5 and the identity
+// on the head bits 7, 8 (four per-head rotations).  Entries +-1 or 0.
+template <int AG>
+__device__ __forceinline__ void hadamard_f2_frag(uint32_t (&a)[4], int lane, uint32_t opaque_zero) {
+    constexpr int kMask = AG == 4 ? 15 : AG == 2 ? 7 : 3;
+    const int g = lane >> 2, t = lane & 3;
+    auto h = [](int m, int k) -> uint32_t {
+        if ((m & ~kMask) != (k & ~kMask)) return 0u;
+        return (__popc(m & k & kMask) & 1) ? 0xBC00u : 0x3C00u;
+    };
+    const int rows[4] = {g, g + 8, g, g + 8}, cols[4] = {2 * t, 2 * t, 2 * t + 8, 2 * t + 8};
+#pragma unroll
+    for (int r = 0; r < 4; ++r) a[r] = h(rows[r], cols[r]) | (h(rows[r], cols[r] + 1) << 16);
+    a[2] ^= opaque_zero;
+    a[3] ^= opaque_zero;
+}
+
 }  // namespace mma
 }  // namespace rkv

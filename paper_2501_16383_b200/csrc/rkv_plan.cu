@@ -52,8 +52,8 @@ int group_cost(const int* cls, const int* words, int GS) {
 }  // namespace
 
 bool build_decode_plan(const rkv_layer_desc& d, const int32_t* perm, std::vector<uint32_t>& out, int& cost_out) {
-    const int C = d.num_kv_heads * d.head_dim, N = d.heads_per_group * d.head_dim;
     const int kind = decode_kind(d);
+    const int C = d.num_kv_heads * d.head_dim, N = kind == kDecodeMma ? mma_layout_n(d) : d.heads_per_group * d.head_dim;
     const int GS = kind == kDecodeMma ? 32 : 16;  // lanes whose stores share a wavefront
     const int W = C / 16, G = W / GS;
     auto pos = [&](int c) { return kind == kDecodeMma ? mma_pos(N, c) : knat_pos(N, c) * 8; };

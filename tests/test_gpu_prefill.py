@@ -64,6 +64,8 @@ def check(got, want):
     (40, 40, 4, 70, (0,), 3),
     (32, 8, 2, 90, (0, 3, 64), 4),
     (32, 8, 2, 33, (), 5),
+    (8, 8, 1, 70, (0, 9), 6),
+    (8, 8, 2, 45, (0,), 7),
 ])
 def test_prefill_matches_oracle(oracle, hq, hkv, g, T, sinks, seed):
     layer, k, v, flags, q, perm = build(hq, hkv, g, T, sinks, seed)

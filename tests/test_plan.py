@@ -48,19 +48,24 @@ def test_mma_positions_are_a_bijection():
         assert pos == list(range(0, 4 * C, 4))
 
 
-@pytest.mark.parametrize("hq,hkv,g,seed", [(40, 40, 4, 0), (32, 32, 4, 1), (32, 8, 2, 2), (8, 8, 4, 3), (4, 4, 1, 4)])
+@pytest.mark.parametrize("hq,hkv,g,seed", [(40, 40, 4, 0), (32, 32, 4, 1), (32, 8, 2, 2), (8, 8, 4, 3), (4, 4, 1, 4),
+                                           (8, 8, 1, 5), (8, 8, 2, 6), (40, 40, 1, 7)])
 def test_plan_is_a_valid_scatter(hq, hkv, g, seed):
     cfg = P.LayerConfig(batch=1, num_q_heads=hq, num_kv_heads=hkv, heads_per_group=g)
     C = hkv * 128
-    N = 128 * g
     perm = np.random.default_rng(seed).permutation(C).astype(np.int32)
     words, cost = P.layer_plan_build(cfg, perm)
+    mma = int(words[7]) == 1  # PH_KIND: tensor-core decode layout
+    # tensor-core layouts tile 512 channels (MHA, G = 4, 2 or 1 heads per rotation
+    # group) or 256 (GQA, G = 2); the CUDA-core layout follows the rotation group
+    gqa = g == 2 and hq == 4 * hkv
+    N = (256 if gqa else 512) if mma else 128 * g
+    assert mma == (gqa or C % 512 == 0)
     assert int(words[0]) == 0x504B5652 and int(words[2]) == N and int(words[4]) == C
     W = C // 16
     omega = words[HEADER:HEADER + W].astype(np.int64)
     addr = words[HEADER + W:HEADER + W + 16 * W].reshape(4, W, 4)
     assert sorted(omega.tolist()) == list(range(W))
-    mma = int(words[7]) == 1  # PH_KIND: tensor-core decode layout
     pos = (lambda c: mma_pos(N, c)) if mma else (lambda c: knat_pos(N, c) * 8)
     for wp in range(W):
         w = omega[wp]

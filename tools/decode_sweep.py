@@ -2,11 +2,12 @@
 development tool next to bench.py): fills a seeded 2-bit cache per config and
 times rkv_decode_attention alone with CUDA events.
 
-    python tools/decode_sweep.py [cfg ...]      (default: 2 3 4)
+    python tools/decode_sweep.py [cfg ...]      (default: 2 3 4; "2g1" = config 2 with G = 1)
     RKV_DECODE_KERNEL=simt python tools/decode_sweep.py   # the CUDA-core kernel
 
 cfg 4 (8 x 32768 tokens) is timed at full size; cfg 3 at batch 64 x 8192.
 """
+import dataclasses
 import json
 import os
 import sys
@@ -24,8 +25,10 @@ def decode_bytes(w, B, T, nsinks):
     return B * ((T - nsinks) * 2 * (c // 4 + 4 * c // 128) + nsinks * 4 * c) + B * w.num_q_heads * 128 * 6
 
 
-def run(cfg_id, iters=20):
+def run(cfg_id, iters=20, g=None):
     w = WL.CONFIGS[cfg_id]
+    if g is not None:  # same shape with another rotation group size (e.g. the reference default G = 1)
+        w = dataclasses.replace(w, heads_per_group=g, name=f"{w.name}-g{g}")
     dev = torch.device("cuda", 0)
     B, T = w.batch, w.tokens
     perm = WL.calibration_perm(w, 42 + cfg_id, device=dev)
@@ -61,6 +64,8 @@ def run(cfg_id, iters=20):
 
 
 if __name__ == "__main__":
-    ids = [int(a) for a in sys.argv[1:]] or [2, 3, 4]
-    for i in ids:
-        print(json.dumps(run(i)), flush=True)
+    # "2" = config 2; "2g1" = config 2's shape with G = 1
+    ids = sys.argv[1:] or ["2", "3", "4"]
+    for a in ids:
+        cfg, _, g = a.partition("g")
+        print(json.dumps(run(int(cfg), g=int(g) if g else None)), flush=True)
