@@ -587,7 +587,7 @@ __global__ void rope_table2_kernel(float4* table, int64_t npos, double base, int
         c[k] = cos(static_cast<double>(pos) * theta);
         sn[k] = sin(static_cast<double>(pos) * theta);
     }
-    table[(pos >> 1) * kRopeRow + 64 + (pos & 1) * 32 + j] = fold ? make_float4(static_cast<float>(c[0] - sn[0]), static_cast<float>(c[1] - sn[1]),
+    table[(pos >> 1) * kRopeRow + 64 + (pos & 1) * 32 + rope_pair_slot(j)] = fold ? make_float4(static_cast<float>(c[0] - sn[0]), static_cast<float>(c[1] - sn[1]),
                                   static_cast<float>(c[0] + sn[0]), static_cast<float>(c[1] + sn[1]))
                     : make_float4(static_cast<float>(c[0]), static_cast<float>(c[1]), static_cast<float>(sn[0]),
                                   static_cast<float>(sn[1]));

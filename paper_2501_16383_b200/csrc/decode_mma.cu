@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(320, kCtasPerSm) decode_mma_kernel(DecodeParam
 
     const uint32_t lane_off = static_cast<uint32_t>(gam * N * 4 + lane * NJ * 16);
     const int swz = (lane >> 1) & 3;
-    const int fpi = tl + 8 * (g & 3);  // frequency-pair row index of f1 = 0 (f = 2 fpi)
+    const int fpi = tl + 4 * (g & 3);  // RoPE slot of frequency pair f / 2, f = 2 tl + 16 (g & 3) (+ 8 f1: slot + 16)
 
     // K phase of a tile: logits lg[tk] of head hv (log2 domain)
     auto k_tile = [&](int slot, float (&lg)[kTT]) {
@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(320, kCtasPerSm) decode_mma_kernel(DecodeParam
                         mma_f2(z[o], l0, l1, t4);
                     }
                     // RoPE (bit-6 butterfly folded into u, w) and q.k over the frequency pair
-                    const float4 r4 = rope4[(2 * pq + tk) * 32 + fpi + 4 * f1];  // (u f, u f+1, w f, w f+1)
+                    const float4 r4 = rope4[(2 * pq + tk) * 32 + fpi + 16 * f1];  // (u f, u f+1, w f, w f+1)
                     const float2 u = make_float2(r4.x, r4.y), w = make_float2(r4.z, r4.w);
 #pragma unroll
                     for (int rh = 0; rh < 2; ++rh) {
@@ -649,7 +649,7 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? 2 : 1) decode_gqa_kernel(Dec
     }
     const uint32_t lane_off = static_cast<uint32_t>(gam * N * 4 + lane * NJ * 16);
     const int swz = (lane >> 2) & 1;
-    const int fpi = tl + 8 * (g & 3);
+    const int fpi = tl + 4 * (g & 3);  // rope_pair_slot(tl + 8 (g & 3)); f1 adds 16
     // softmax state of head (kvh, r = g & 3) over this lane's tokens (replicated over tl lanes)
     float m_run = -INFINITY, l_part = 0.f, zc_part = 0.f;
     float acc[2][8][4];  // P.V accumulators [kvh][code position][fragment]
@@ -763,7 +763,7 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? 2 : 1) decode_gqa_kernel(Dec
                     mma16816(t4, AH, h0, h1, zero);
                     mma16816(z, AH, l0, l1, t4);
                     // z: (c0, c1) channels f, f+1 (bit 6 = 0), (c2, c3) channels f+64, f+65
-                    const float4 r4 = rope4[(2 * tp + tk) * 32 + fpi + 4 * f1];  // (cos f, cos f+1, sin f, sin f+1)
+                    const float4 r4 = rope4[(2 * tp + tk) * 32 + fpi + 16 * f1];  // (cos f, cos f+1, sin f, sin f+1)
                     const float2 cs2 = make_float2(r4.x, r4.y), sn2 = make_float2(r4.z, r4.w);
                     const float2 a2 = make_float2(z[0], z[1]), b2 = make_float2(z[2], z[3]);
                     const float2 kra = fma2(cs2, a2, mul2(make_float2(-sn2.x, -sn2.y), b2));

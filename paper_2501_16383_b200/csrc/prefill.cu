@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(512) reconstruct_keys_kernel(PrefillParams p) 
 #pragma unroll
             for (int f1 = 0; f1 < 2; ++f1) {
                 const int f = 2 * tl + 8 * f1 + 16 * (g & 3);
-                const float4 r4 = __ldg(rrow + (f >> 1));
+                const float4 r4 = __ldg(rrow + rope_pair_slot(f >> 1));
                 if constexpr (G == 4) {
                     float z[2][4];
 #pragma unroll

@@ -43,6 +43,12 @@ RKV_HD inline int knat_pair_f2(int N, int C) { return (C / N) * knat_unit(N); } 
 // (+ 2*outer).  Each lane's EPL = N/32 elements (4 per 16-byte chunk, one
 // chunk per instance) are contiguous; chunks are XOR-swizzled by lane so the
 // per-lane LDS.128 fragment loads are bank-conflict free.
+// Slot of frequency pair j (f = 2j, 2j+1) in section 2 of a RoPE table row:
+// the tensor-core kernels read pairs j = tl + 4 f1 + 8 q (lane bits tl, q) as
+// one LDS.128 per lane; with slot = tl + 4 q + 16 f1 a warp's 16 distinct
+// entries are 256 contiguous bytes (2 wavefronts, no bank conflict).
+RKV_HD constexpr int rope_pair_slot(int j) { return (j & 3) | (((j >> 3) & 3) << 2) | (((j >> 2) & 1) << 4); }
+
 RKV_HD inline int mma_nj(int N) { return N / 128; }  // MMA-1 instances = 16-byte chunks per lane
 RKV_HD inline int mma_swz(int N, int lane) { return N == 512 ? (lane >> 1) & 3 : (lane >> 2) & 1; }
 RKV_HD inline int mma_pos(int N, int c) {  // byte offset of channel c in a token-pair row
