@@ -22,6 +22,7 @@
 //      RoPE at their own position) and applies H_128 (V's inverse rotation),
 //      like decode_combine_kernel, with the row's own query position.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 
 #include "rkv_common.cuh"
@@ -327,6 +328,8 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define PF_TRACE(ev, j)                                                                                     \
     do {                                                                                                  \
         if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (j) < 256) g_pf_trace[ev][j] = clock64(); \
+        if (blockIdx.x == 1 && blockIdx.y == 0 && blockIdx.z == 0 && (j) < 256 && (ev) <= 1)                  \
+            g_pf_trace[6 + (ev)][j] = clock64();                                                            \
     } while (0)
 #else
 #define PF_TRACE(ev, j) \
@@ -342,14 +345,24 @@ __device__ __forceinline__ unsigned long long gtimer() {
     } while (0)
 constexpr int kQR = 128, kAttnThreads = 384, kKSlots = 3, kVSlots = 2, kMaxSinkRows = kPrefillMaxSinks;
 constexpr uint32_t kQRow = 512, kKSlab = 8192, kKTile = 32768, kVTile = 16384;
-constexpr uint32_t kOffK = kQR * kQRow, kOffV = kOffK + kKSlots * kKTile, kOffSink = kOffV + kVSlots * kVTile,
-                   kOffML = kOffSink + kMaxSinkRows * 128 * 6 + 64, kOffBar = kOffML + 2 * 128 * 8;
-constexpr size_t kAttnSmem = kOffBar + 256 + 1024;  // + barriers, + alignment slack
+// shared-memory carve-up; PAIR (2-SM mode): each CTA of the cluster holds half of every K tile
+// (keys 32 r .. 32 r + 31: 4 half-slabs of 4 KB) and half of every V^T tile (channels 64 r ..)
+template <bool PAIR>
+struct AttnSmem {
+    static constexpr uint32_t kt = PAIR ? kKTile / 2 : kKTile, vt = PAIR ? kVTile / 2 : kVTile;
+    static constexpr uint32_t k = kQR * kQRow, v = k + kKSlots * kt, sink = v + kVSlots * vt,
+                              ml = sink + kMaxSinkRows * 128 * 6 + 64, bar = ml + 2 * 128 * 8;
+    static constexpr size_t total = bar + 256 + 1024;  // + barriers, + alignment slack
+};
 // tensor-memory columns: S_0 [0, 64), S_1 [64, 128), O_0 [128, 256), O_1 [256, 384), Q hi [384, 448), Q lo [448, 512)
 constexpr uint32_t kColO = 128, kColQhi = 384, kColQlo = 448;
 constexpr float kLazy = 14.0f;  // rescale O only when the max grows by > 2^14 (P <= 2^14 in fp16)
 
+template <bool PAIR>
 __global__ void __launch_bounds__(kAttnThreads, 1) prefill_attn_kernel(PrefillParams p) {
+    using L = AttnSmem<PAIR>;
+    constexpr uint32_t kOffK = L::k, kOffV = L::v, kOffSink = L::sink, kOffML = L::ml, kOffBar = L::bar;
+    constexpr uint32_t kKT2 = L::kt, kVT2 = L::vt;
     extern __shared__ unsigned char smem_raw[];
     unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // 1024-byte aligned
     const uint32_t sbase = smem_u32(smem);
@@ -359,16 +372,23 @@ __global__ void __launch_bounds__(kAttnThreads, 1) prefill_attn_kernel(PrefillPa
     float2* ml_s = reinterpret_cast<float2*>(smem + kOffML);                               // [2][128] (m, l)
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kOffBar);
     uint64_t *kfull = bar, *kempty = bar + kKSlots, *vfull = bar + 2 * kKSlots, *vempty = vfull + 2, *s_full = vfull + 4,
-             *p_full = vfull + 6, *o_done = vfull + 8, *q_full = vfull + 9, *q_tmem = vfull + 10, *sink_ready = vfull + 11;
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(sink_ready + 1);
+             *p_full = vfull + 6, *o_done = vfull + 8, *q_full = vfull + 9, *q_tmem = vfull + 10, *sink_ready = vfull + 11,
+             *kpeer = vfull + 12, *vpeer = kpeer + kKSlots,  // PAIR: the upper CTA's K / V halves landed,
+             *ppeer = vpeer + 2, *qpeer = ppeer + 2;          // its P rows and its Q rows are in TMEM
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(qpeer + 1);
 
-    const int qb = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, b = blockIdx.z;  // heaviest query blocks first
+    const int h = blockIdx.y, b = blockIdx.z;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int REP = p.Hq / p.Hkv, kvh = h / REP;
-    const int64_t nq = p.num_q, i0 = static_cast<int64_t>(qb) * kQR;
-    const int nrows = static_cast<int>(lmin64(kQR, nq - i0));
+    const int64_t nq = p.num_q;
+    // heaviest query blocks first; PAIR: a cluster of two CTAs takes 256 rows, CTA rank r rows 128 r ..
+    const uint32_t rank = PAIR ? umma::cluster_rank() : 0u;
+    const int64_t blk0 = PAIR ? static_cast<int64_t>((gridDim.x >> 1) - 1 - (blockIdx.x >> 1)) * 2 * kQR
+                              : static_cast<int64_t>(gridDim.x - 1 - blockIdx.x) * kQR;
+    const int64_t i0 = blk0 + kQR * rank;
+    const int nrows = static_cast<int>(lmin64(kQR, nq - i0));  // may be <= 0 for the upper CTA of the last pair
     const int64_t q0 = p.q_start[b] + i0, T = p.seq_len[b];
-    const int64_t kend = lmin64(T, q0 + nrows);
+    const int64_t kend = lmin64(T, p.q_start[b] + blk0 + lmin64(PAIR ? 2 * kQR : kQR, nq - blk0));
     const int nt = kend > 0 ? static_cast<int>((kend + kPrefillKT - 1) / kPrefillKT) : 0;
     const int nsink = min(min(p.cache.sink_count[b], p.max_sinks), kMaxSinkRows);
 
@@ -383,18 +403,33 @@ __global__ void __launch_bounds__(kAttnThreads, 1) prefill_attn_kernel(PrefillPa
             mbar_init(vempty + i, 1);
             mbar_init(s_full + i, 1);
             mbar_init(p_full + i, 128);
+            mbar_init(vpeer + i, 1);
+            mbar_init(ppeer + i, 1);
         }
+        for (int i = 0; i < kKSlots; ++i) mbar_init(kpeer + i, 1);
+        mbar_init(qpeer, 1);
         mbar_init(o_done, 1);
         mbar_init(q_full, 1);
         mbar_init(q_tmem, 256);
         mbar_init(sink_ready, 32);
         mbar_fence_init();
     }
-    if (warp == 1) umma::alloc<512>(tslot);
+    if (warp == 1) {
+        if constexpr (PAIR) umma::alloc2<512>(tslot);
+        else umma::alloc<512>(tslot);
+    }
     umma::fence_before();
-    __syncthreads();
+    if constexpr (PAIR) umma::cluster_sync();  // the leader's barriers exist before any remote arrival
+    else __syncthreads();
     umma::fence_after();
     const uint32_t tmem = *tslot;
+    // hand-offs to the MMA issuer: every thread arrives in its own CTA (cheap, CTA scope); in PAIR
+    // mode one thread of the upper CTA relays each completed phase to the leader's *peer barrier
+    // with a single cluster-scope arrive, and the leader waits for both
+    auto wait_both = [&](uint64_t* local, uint64_t* peer, uint32_t parity) {
+        mbar_wait(local, parity);
+        if constexpr (PAIR) umma::mbar_wait_cluster(peer, parity);
+    };
 
     if (warp == 0) {
         // ---- query block, then the key tiles (kKSlots deep)
@@ -406,48 +441,63 @@ __global__ void __launch_bounds__(kAttnThreads, 1) prefill_attn_kernel(PrefillPa
                 const int sl = j % kKSlots;
                 if (j >= kKSlots) mbar_wait_sleep(kempty + sl, ((j / kKSlots) - 1) & 1);
                 const unsigned char* src = kv_tile(p, b, kvh, j);
-                unsigned char* dst = smem + kOffK + sl * kKTile;
-                mbar_arrive_expect_tx(kfull + sl, kKTile);
-                bulk_g2s(dst, src, kKTile / 2, kfull + sl);
-                bulk_g2s(dst + kKTile / 2, src + kKTile / 2, kKTile / 2, kfull + sl);
+                unsigned char* dst = smem + kOffK + sl * kKT2;
+                mbar_arrive_expect_tx(kfull + sl, kKT2);
+                if constexpr (PAIR) {  // rows 32 r .. of the 4 slabs (hi s0, hi s1, lo s0, lo s1)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) bulk_g2s(dst + q * 4096, src + q * 8192 + rank * 4096, 4096, kfull + sl);
+                } else {
+                    bulk_g2s(dst, src, kKTile / 2, kfull + sl);
+                    bulk_g2s(dst + kKTile / 2, src + kKTile / 2, kKTile / 2, kfull + sl);
+                }
             }
         }
         __syncwarp();
-    } else if (warp == 1) {
-        // ---- MMA issuer
+    } else if (warp == 1 && rank == 0) {
+        // ---- MMA issuer (PAIR: the leader issues 2-SM MMAs, M = 256, B halves in both CTAs)
         if (umma::elect_one()) {
-            constexpr uint32_t idS = umma::idesc_f16(128, 64), idO = umma::idesc_f16(128, 128);
-            mbar_wait(q_tmem, 0);
+            constexpr int M = PAIR ? 256 : 128;
+            constexpr uint32_t idS = umma::idesc_f16(M, 64), idO = umma::idesc_f16(M, 128);
+            constexpr uint32_t kHiSlab = PAIR ? 4096 : kKSlab, kLoOff = PAIR ? 8192 : 2 * kKSlab;
+            auto mma = [&](uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+                if constexpr (PAIR) umma::mma2_f16_ts(d, a, bdesc, idesc, acc);
+                else umma::mma_f16_ts(d, a, bdesc, idesc, acc);
+            };
+            auto commit_all = [&](uint64_t* bar) {
+                if constexpr (PAIR) umma::commit2(bar);
+                else umma::commit(bar);
+            };
+            wait_both(q_tmem, qpeer, 0);
             PF_CTA(1);
             auto qk = [&](int j) {
                 const int sl = j % kKSlots, sb = j & 1;
-                mbar_wait(kfull + sl, (j / kKSlots) & 1);
+                wait_both(kfull + sl, kpeer + sl, (j / kKSlots) & 1);
                 umma::fence_after();
                 PF_TRACE(4, j);
-                const uint32_t d = tmem + 64u * sb, kb = sbase + kOffK + sl * kKTile;
+                const uint32_t d = tmem + 64u * sb, kb = sbase + kOffK + sl * kKT2;
 #pragma unroll
                 for (int ks = 0; ks < 8; ++ks) {
-                    const uint32_t ko = (ks >> 2) * kKSlab + (ks & 3) * 32;
-                    const uint64_t bh = umma::sdesc(kb + ko), bl = umma::sdesc(kb + 2 * kKSlab + ko);
-                    umma::mma_f16_ts(d, tmem + kColQhi + 8 * ks, bh, idS, ks > 0);
-                    umma::mma_f16_ts(d, tmem + kColQhi + 8 * ks, bl, idS, 1);
-                    umma::mma_f16_ts(d, tmem + kColQlo + 8 * ks, bh, idS, 1);
+                    const uint32_t ko = (ks >> 2) * kHiSlab + (ks & 3) * 32;
+                    const uint64_t bh = umma::sdesc(kb + ko), bl = umma::sdesc(kb + kLoOff + ko);
+                    mma(d, tmem + kColQhi + 8 * ks, bh, idS, ks > 0);
+                    mma(d, tmem + kColQhi + 8 * ks, bl, idS, 1);
+                    mma(d, tmem + kColQlo + 8 * ks, bh, idS, 1);
                 }
-                umma::commit(s_full + sb);
-                umma::commit(kempty + sl);
+                commit_all(s_full + sb);
+                commit_all(kempty + sl);
             };
             auto pv = [&](int j) {
                 const int sb = j & 1;
-                mbar_wait(vfull + sb, (j >> 1) & 1);
+                wait_both(vfull + sb, vpeer + sb, (j >> 1) & 1);
                 mbar_wait(p_full + sb, (j >> 1) & 1);
+                if constexpr (PAIR) umma::mbar_wait_cluster(ppeer + sb, (j >> 1) & 1);
                 umma::fence_after();
                 PF_TRACE(2, j);
-                const uint32_t vb = sbase + kOffV + sb * kVTile;
+                const uint32_t vb = sbase + kOffV + sb * kVT2;
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk)
-                    umma::mma_f16_ts(tmem + kColO + 128u * sb, tmem + 64u * sb + 8 * kk, umma::sdesc(vb + kk * 32), idO,
-                                     (j >= 2 || kk > 0));
-                umma::commit(vempty + sb);
+                    mma(tmem + kColO + 128u * sb, tmem + 64u * sb + 8 * kk, umma::sdesc(vb + kk * 32), idO, (j >= 2 || kk > 0));
+                commit_all(vempty + sb);
                 PF_TRACE(3, j);
             };
             if (nt > 0) qk(0);
@@ -456,7 +506,20 @@ __global__ void __launch_bounds__(kAttnThreads, 1) prefill_attn_kernel(PrefillPa
                 pv(j);
                 if (j + 2 < nt) qk(j + 2);
             }
-            umma::commit(o_done);
+            commit_all(o_done);
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        // ---- PAIR, upper CTA: relay "Q rows in TMEM", then per tile "V half landed" and
+        // "P rows written" to the leader
+        if (umma::elect_one()) {
+            // suspending waits: a spinning relay would take issue slots from the softmax warps
+            mbar_wait_sleep(q_tmem, 0);
+            umma::mbar_arrive_cluster(umma::peer_addr(qpeer, 0));
+            for (int j = 0; j < nt; ++j) {
+                mbar_wait_sleep(vfull + (j & 1), (j >> 1) & 1);
+                umma::mbar_arrive_cluster(umma::peer_addr(vpeer + (j & 1), 0));
+            }
         }
         __syncwarp();
     } else if (warp == 2) {
@@ -476,6 +539,20 @@ __global__ void __launch_bounds__(kAttnThreads, 1) prefill_attn_kernel(PrefillPa
             if (lane == 0) sink_p[s] = pos;
         }
         mbar_arrive(sink_ready);
+        if (PAIR && rank == 1) {
+            if (lane == 0) {  // tell the leader when this CTA's K halves have landed
+                for (int j = 0; j < nt; ++j) {
+                    mbar_wait_sleep(kfull + j % kKSlots, (j / kKSlots) & 1);
+                    umma::mbar_arrive_cluster(umma::peer_addr(kpeer + j % kKSlots, 0));
+                }
+            } else if (lane == 1) {  // ... and when this CTA's P rows of tile j are in TMEM
+                for (int j = 0; j < nt; ++j) {  // on the critical path: a polling wait
+                    mbar_wait(p_full + (j & 1), (j >> 1) & 1);
+                    umma::mbar_arrive_cluster(umma::peer_addr(ppeer + (j & 1), 0));
+                }
+            }
+        }
+        __syncwarp();
     } else if (warp == 3) {
         // ---- value tiles
         if (umma::elect_one()) {
@@ -483,8 +560,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1) prefill_attn_kernel(PrefillPa
                 const int sl = j & 1;
                 if (j >= kVSlots) mbar_wait_sleep(vempty + sl, ((j >> 1) - 1) & 1);
                 PF_TRACE(5, j);
-                mbar_arrive_expect_tx(vfull + sl, kVTile);
-                bulk_g2s(smem + kOffV + sl * kVTile, kv_tile(p, b, kvh, j) + kKTile, kVTile, vfull + sl);
+                mbar_arrive_expect_tx(vfull + sl, kVT2);
+                bulk_g2s(smem + kOffV + sl * kVT2, kv_tile(p, b, kvh, j) + kKTile + rank * kVT2, kVT2, vfull + sl);
             }
         }
         __syncwarp();
@@ -695,10 +772,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1) prefill_attn_kernel(PrefillPa
         }
     }
     umma::fence_before();
-    __syncthreads();
+    if constexpr (PAIR) umma::cluster_sync();  // the peer's shared memory / TMEM stay live until both are done
+    else __syncthreads();
     if (warp == 1) {
         umma::fence_after();
-        umma::dealloc<512>(tmem);
+        if constexpr (PAIR) umma::dealloc2<512>(tmem);
+        else umma::dealloc<512>(tmem);
     }
     if (tid == 0) PF_CTA(3);
 }
@@ -713,6 +792,16 @@ extern "C" int rkv_debug_prefill_cta(unsigned long long* out) {
     return cudaMemcpyFromSymbol(out, g_pf_cta, sizeof(g_pf_cta)) == cudaSuccess ? 0 : 1;
 }
 #endif
+
+namespace {
+// 2-SM mode (opt-in, RKV_PREFILL_PAIR=1): correct, but the per-tile cluster-scope hand-offs
+// (P rows of the upper CTA -> leader) cost ~2,000 cycles, more than the halved shared-memory
+// traffic saves
+bool prefill_pair() {
+    const char* e = std::getenv("RKV_PREFILL_PAIR");
+    return e && std::atoi(e) == 1;
+}
+}  // namespace
 
 cudaError_t launch_prefill(const rkv_layer_desc& d, const PrefillParams& p, int64_t max_seq_len, cudaStream_t s) {
     const int C = p.C, W = C / 16, MG = C / 128;
@@ -746,11 +835,31 @@ cudaError_t launch_prefill(const rkv_layer_desc& d, const PrefillParams& p, int6
                                   static_cast<unsigned>(d.batch)),
                              128, 0, s>>>(p);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    if ((e = cudaFuncSetAttribute(prefill_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(kAttnSmem))) != cudaSuccess)
-        return e;
     const dim3 agrid(static_cast<unsigned>(p.num_q_pad / kQR), static_cast<unsigned>(p.Hq), static_cast<unsigned>(d.batch));
-    prefill_attn_kernel<<<agrid, kAttnThreads, kAttnSmem, s>>>(p);
+    if (prefill_pair()) {  // 2-SM clusters (num_q_pad is a multiple of 256)
+        constexpr size_t sm = AttnSmem<true>::total;
+        if ((e = cudaFuncSetAttribute(prefill_attn_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(sm))) != cudaSuccess)
+            return e;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = agrid;
+        cfg.blockDim = dim3(kAttnThreads);
+        cfg.dynamicSmemBytes = sm;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, prefill_attn_kernel<true>, p);
+    }
+    constexpr size_t sm = AttnSmem<false>::total;
+    if ((e = cudaFuncSetAttribute(prefill_attn_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(sm))) != cudaSuccess)
+        return e;
+    prefill_attn_kernel<false><<<agrid, kAttnThreads, sm, s>>>(p);
     return cudaGetLastError();
 }
 

@@ -59,7 +59,7 @@ struct DecodeParams {
 constexpr int kPrefillKT = 64;
 constexpr int kPrefillMaxSinks = 16;  // sink rows staged per attention CTA
 constexpr size_t kPrefillTileBytes = 3 * 16384;
-inline int64_t prefill_q_pad(int64_t num_q) { return (num_q + 127) / 128 * 128; }  // 128 query rows per CTA
+inline int64_t prefill_q_pad(int64_t num_q) { return (num_q + 255) / 256 * 256; }  // 256 query rows per CTA pair
 struct PrefillParams {
     const uint16_t* q;        // [B][num_q][Hq][128] fp16 pre-RoPE
     const int64_t* q_start;   // [B] position of query row 0

@@ -186,3 +186,17 @@ def test_prefill_full_size_rows_match_decode(oracle, cfg_id, B):
     k0, v0 = ks[0], vs[0]
     want = expected_rows(oracle, layer, k0, v0, flags, q, perm, 0, [0, 5, 70, 300])
     check(out[0, [0, 5, 70, 300]], want)
+
+
+@pytest.mark.parametrize("hq,hkv,g,T,sinks,seed", [(8, 8, 4, 300, (0, 41), 21), (32, 8, 2, 200, (0,), 22),
+                                                   (8, 8, 1, 129, (0, 128), 23)])
+def test_prefill_two_sm_pairs_match_oracle(oracle, monkeypatch, hq, hkv, g, T, sinks, seed):
+    """The opt-in 2-SM mode (cta_group::2 MMAs over CTA pairs, 256 query rows,
+    each CTA holding half of every K/V tile) against the oracle."""
+    monkeypatch.setenv("RKV_PREFILL_PAIR", "1")
+    layer, k, v, flags, q, perm = build(hq, hkv, g, T, sinks, seed)
+    out = layer.prefill_attention(q, q_start=np.zeros(2, np.int64)).cpu().numpy()
+    rows = list(range(0, T, 5)) + [T - 1]
+    for b in range(2):
+        want = expected_rows(oracle, layer, k, v, flags, q, perm, b, rows)
+        check(out[b, rows], want)

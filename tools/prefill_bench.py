@@ -49,12 +49,13 @@ if os.environ.get("RKV_PF_TRACE"):  # library built with RKV_NVCC_EXTRA=-DRKV_PF
     buf = (ctypes.c_longlong * (8 * 256))()
     P.rotatekv.lib().rkv_debug_prefill_trace(buf)
     tr = np.array(buf, dtype=np.int64).reshape(8, 256)
-    names = ["s_ready", "p_done", "mma_p_seen", "mma_pv_issued", "mma_qk_start", "prod_v_issue"]
+    names = ["s_ready", "p_done", "mma_p_seen", "mma_pv_issued", "mma_qk_start", "prod_v_issue", "r1_s_ready",
+             "r1_p_done"]
     t0 = tr[0, 0]
     nt = int((tr[0] != 0).sum())
     print("tile " + " ".join(f"{n:>13}" for n in names))
     for j in range(min(nt, 40)):
-        print(f"{j:4d} " + " ".join(f"{int(tr[e, j] - t0) if tr[e, j] else -1:13d}" for e in range(6)))
+        print(f"{j:4d} " + " ".join(f"{int(tr[e, j] - t0) if tr[e, j] else -1:13d}" for e in range(8)))
     d = np.diff(tr[0, 4:nt])
     print("steady tile period (cycles): median", int(np.median(d)), "softmax span median", int(np.median(tr[1, 4:nt] - tr[0, 4:nt])))
     cta = (ctypes.c_ulonglong * (4096 * 4))()
