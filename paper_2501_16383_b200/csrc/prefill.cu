@@ -3,24 +3,21 @@
 // proj/src/pipeline.cpp:156-191: reconstruct_cache, then causal
 // reference_attention, proj/src/attention.cpp:20-49).
 //
-// Three launches, mirroring the reference's decomposition:
+// Four launches, mirroring the reference's decomposition (reconstruct the
+// cache, then attend):
 //   1. reconstruct_keys_kernel (== reconstruct_cache for K): per token the
 //      un-reorder scatter, the tensor-core inverse FWHT of decode_mma.cu (two
 //      chained H_16 mma.sync with the fp16 hi/lo split) and RoPE at the
-//      token's position, written once as fp16 hi + fp16 lo rows [B][T][C]
-//      (natural channel order, FWHT normalisation applied).  Every key is
-//      reconstructed once and reused by every query.
-//   2. prefill_attn_kernel: flash attention per (sequence, q head, 64-query
-//      block), 4 warps x 16 query rows.  S = Q K^T on mma.sync m16n8k16 with
-//      both operands split into fp16 hi + lo (three MMAs: hi.hi + hi.lo +
-//      lo.hi, ~2^-22 relative); causal + sink + length mask; online softmax
-//      in the exp2 domain; P.V on mma.sync with the 2-bit V codes as exact fp16
-//      subnormals (B operand) and fp16(p * s) as the A operand (the chained S
-//      accumulator fragment), the zero point folded per row.  Sink tokens are
-//      skipped here and one (m, l, o') partial per query row is written.
-//   3. prefill_combine_kernel: adds the fp16 sink rows (exact, natural frame,
-//      RoPE at their own position) and applies H_128 (V's inverse rotation),
-//      like decode_combine_kernel, with the row's own query position.
+//      token's position, stored as fp16 hi + lo straight into 64-key operand
+//      tiles (K-major SWIZZLE_128B).  Every key is reconstructed once.
+//   2. reconstruct_values_kernel: the dequantized rotated values, fp16,
+//      transposed into the same tiles.
+//   3. prepare_queries_kernel: RoPE'd, scaled, hi/lo-split query rows laid out
+//      for tensor memory.
+//   4. prefill_attn_kernel: flash attention on tcgen05 (section 4 below):
+//      S and O accumulate in tensor memory, Q and P are A operands from tensor
+//      memory, K/V tiles stream through shared memory by cp.async.bulk; sink
+//      rows and V's inverse rotation H_128 are applied in its epilogue.
 #include <algorithm>
 #include <cstdlib>
 #include <cmath>
