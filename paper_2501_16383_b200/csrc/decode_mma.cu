@@ -25,23 +25,29 @@
 // ~2^-22 (tools/hmma_precision.py: 2e-5 normalised max error vs 7.6e-4 with a
 // single fp16 rounding; the north star allows 2e-3).
 //
-// Pipeline per CTA (one split of one sequence; NG = C/N FWHT groups, one warp
-// per group, PW warps per group splitting the token pairs):
-//   * TMA bulk copies stream each tile (packed K/V words, scale|zero words,
-//     the tile's RoPE rows) into an NS-stage ring (mbarrier complete_tx).
-//   * scatter: every thread takes one packed K word for each token pair of
-//     the NEXT tile, dequantises its 16 codes for both tokens as half2 ops
-//     (code -> 2^(10-2e)+c by one LOP3 on the interleaved pair, HSUB2 of the
-//     zero point, HMUL2 of the scale) and stores them (STS.32) to their
-//     natural channel (slot j -> perm[j]) in B-fragment order, double
-//     buffered, so one __syncthreads per tile separates scatter and compute.
-//   * compute (per warp = FWHT group, per token pair): 4 LDS.128 + PRMT give
-//     the B fragments of both tokens, 4 + 8 mma.sync per token, RoPE+q.k on
-//     the fp32 fragments (FFMA2 over the token pair), a 5-shuffle
-//     reduce-scatter, online softmax, and the V accumulation on CUDA cores:
-//     one LOP3 turns two codes into fp16 subnormals c*2^(2e-24) and a mixed
-//     FHFMA (fp16 x fp16 + fp32) adds p*s*c; the zero point is folded once
-//     per token.
+// G = 1 and 2 (one q head per KV head) run on the same 512-channel tiles: the
+// second factor becomes H_4 (x) I_4 / H_8 (x) I_2 over the same bits, leaving
+// the head bits to the q.k stage (hadamard_f2_frag, template parameter AG).
+//
+// Pipeline per CTA (one split of one sequence; one warp per 512-channel tile):
+//   * TMA bulk copies stream each 4-token tile (packed K/V words, scale|zero
+//     words, the tile's RoPE rows) into a 3-stage ring (mbarrier complete_tx).
+//   * scatter (all threads, thread = word position): dequantise the word's 16
+//     codes for both tokens of a pair as half2 ops (code -> 2^(10-2e)+c by one
+//     LOP3 on the interleaved pair, HSUB2 of the zero point, HMUL2 of the
+//     scale) and store them (STS.32) to their natural channel (slot j ->
+//     perm[j]) in B-fragment order; a barrier separates scatter and compute,
+//     a second one protects the single token-pair buffer and the stage.
+//   * compute (warp = tile, per token pair): 4 LDS.128 + PRMT give the B
+//     fragments of both tokens, 4 + 8 mma.sync per token, RoPE+q.k on the fp32
+//     fragments (FFMA2), a reduce-scatter over shuffles, online softmax, and
+//     the V accumulation on CUDA cores: one LOP3 turns two codes into fp16
+//     subnormals c*2^(2e-24) and a mixed FHFMA (fp16 x fp16 + fp32) adds p*s*c;
+//     the zero point is folded once per token.
+// The GQA kernel (G = 2, 4 q heads per KV head) shares the K side, runs P.V on
+// m16n8k8 and parks its accumulators in tensor memory between phases.  SP
+// instantiations restrict a split to a token range (sequence-parallel
+// partials, rkv_decode_attention_partial).
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
