@@ -455,6 +455,30 @@ __global__ void __launch_bounds__(128) decode_combine_kernel(DecodeParams p) {
     // merge the packed partials: lanes fetch (m, l) of 32 partials at a time,
     // the warp max fixes the weights, then the o' rows are summed with loads
     // that do not depend on each other (unrolled), in a fixed order
+    // Latency-bound (a few warps per SM): everything that does not depend on
+    // the partials' weights is requested up front -- the o' rows of the first
+    // 32 partials, the query values and RoPE row for the sink logits.
+    const int nsink = p.partial_ml ? 0 : min(p.cache.sink_count[b], p.max_sinks);
+    float qraw[8];
+    float2 rq[4];
+    {
+        const uint16_t* qh = p.q + (static_cast<int64_t>(b) * p.Hq + h) * 128;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int f = (4 * lane + j) & 63;
+            qraw[2 * j] = h2f(qh[f]);
+            qraw[2 * j + 1] = h2f(qh[f + 64]);
+            rq[j] = rope_at(p.rope, T - 1, f);
+        }
+    }
+    float4 ov[32];
+    {
+        const int n0 = min(32, p.NP);
+        const float4* src = reinterpret_cast<const float4*>(p.ws_o + (base + h) * 128) + lane;
+        const int64_t stride = static_cast<int64_t>(p.Hq) * 32;  // float4 per partial row step
+#pragma unroll
+        for (int k = 0; k < 32; ++k) ov[k] = k < n0 ? src[k * stride] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
     float M = -INFINITY, L = 0.f;
     float4 rot = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int s0 = 0; s0 < p.NP; s0 += 32) {
@@ -476,13 +500,16 @@ __global__ void __launch_bounds__(128) decode_combine_kernel(DecodeParams p) {
         rot = make_float4(rot.x * a, rot.y * a, rot.z * a, rot.w * a);
         M = mn;
         const int n = min(32, p.NP - s0);
-        const float4* src = reinterpret_cast<const float4*>(p.ws_o + (base + static_cast<int64_t>(s0) * p.Hq + h) * 128) + lane;
-        const int64_t stride = static_cast<int64_t>(p.Hq) * 32;  // float4 per partial row step
-#pragma unroll 4
-        for (int k = 0; k < n; ++k) {
-            const float wk = __shfl_sync(0xffffffffu, w, k);
-            const float4 o = src[k * stride];
-            rot = make_float4(rot.x + wk * o.x, rot.y + wk * o.y, rot.z + wk * o.z, rot.w + wk * o.w);
+        if (s0 > 0) {  // partials beyond the first 32 (long sequences with many splits)
+            const float4* src = reinterpret_cast<const float4*>(p.ws_o + (base + static_cast<int64_t>(s0) * p.Hq + h) * 128) + lane;
+            const int64_t stride = static_cast<int64_t>(p.Hq) * 32;
+#pragma unroll
+            for (int k = 0; k < 32; ++k) ov[k] = k < n ? src[k * stride] : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+            const float wk = __shfl_sync(0xffffffffu, w, k);  // 0 past n (ms = -inf)
+            rot = make_float4(rot.x + wk * ov[k].x, rot.y + wk * ov[k].y, rot.z + wk * ov[k].z, rot.w + wk * ov[k].w);
         }
     }
     if (p.partial_ml) {  // sequence-parallel partial: merged (m, l) and the unnormalised rotated o'
@@ -494,16 +521,14 @@ __global__ void __launch_bounds__(128) decode_combine_kernel(DecodeParams p) {
         return;
     }
     // sinks: logits from q and the raw fp16 key rows, both RoPE'd (log2 domain)
-    const int nsink = min(p.cache.sink_count[b], p.max_sinks);
     float4 raw = make_float4(0.f, 0.f, 0.f, 0.f);
     if (nsink > 0) {
         float qd[4];
-        const uint16_t* qh = p.q + (static_cast<int64_t>(b) * p.Hq + h) * 128;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            const int d = 4 * lane + j, f = d & 63;
-            const float a = h2f(qh[f]), bb = h2f(qh[f + 64]);
-            const float2 r = rope_at(p.rope, T - 1, f);
+            const int d = 4 * lane + j;
+            const float a = qraw[2 * j], bb = qraw[2 * j + 1];
+            const float2 r = rq[j];
             qd[j] = (d < 64 ? (a * r.x - bb * r.y) : (a * r.y + bb * r.x)) * p.qscale;
         }
         for (int s = 0; s < nsink; ++s) {
