@@ -361,3 +361,28 @@ def test_cpp_api_program(tmp_path):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("env,hq,hkv,g", [("RKV_GQA_TMEM=0", 32, 8, 2), ("RKV_DECODE_KERNEL=simt", 8, 8, 4),
+                                          ("RKV_DECODE_KERNEL=simt", 32, 8, 2)])
+def test_alternative_decode_kernels(oracle, monkeypatch, env, hq, hkv, g):
+    """The env-selectable kernels (register-resident GQA, the CUDA-core kernel
+    on tensor-core shapes) stay parity-green.  The layer (plan and RoPE table
+    layout) is built under the same selection."""
+    k_, v_ = env.split("=")
+    monkeypatch.setenv(k_, v_)
+    w = small_workload(hq, hkv, g)
+    B, T = 2, 150
+    layer, perm = build_layer(w, B, T + 8, seed=77)
+    k, v = WL.make_kv(w, 77, B, T)
+    sinks = torch.zeros(B, T, dtype=torch.uint8)
+    sinks[:, 0] = 1
+    layer.append(k, v, sinks)
+    q = WL.make_q(w, 77, B)
+    out = layer.decode(q).cpu().numpy()
+    got = cache_host(layer)
+    for b in range(B):
+        want = oracle_decode(oracle, layer, got, b, T, q[b].cpu().numpy(), w, perm, k[b].cpu().numpy(),
+                             v[b].cpu().numpy())
+        assert rel_err(out[b], want) < REL_TOL
+        assert cosine(out[b], want) > COS_TOL
