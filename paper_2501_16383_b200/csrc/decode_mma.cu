@@ -105,6 +105,29 @@ constexpr int kPP = 2, kTT = 2 * kPP, kNS = 3, kCtasPerSm = 2;
 // AG = heads per rotation group of the layer (4, 2 or 1): the kernel always
 // works on 512-channel (pseudo-)groups; only the second FWHT factor differs
 // (hadamard_f2_frag) -- the head bits 7, 8 pass through it when AG < 4.
+#ifdef RKV_DEC_TRACE
+// per-CTA timeline (tools/decode_trace.py): [start, loop start, end, SM id]
+__device__ unsigned long long g_dec_trace[4096][4];
+__device__ __forceinline__ unsigned long long dec_gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define DEC_TRACE(k)                                                                   \
+    do {                                                                               \
+        const int cid = blockIdx.y * gridDim.x + blockIdx.x;                           \
+        if (threadIdx.x == 0 && cid < 4096) {                                          \
+            unsigned sm;                                                               \
+            asm volatile("mov.u32 %0, %smid;" : "=r"(sm));                            \
+            g_dec_trace[cid][k] = dec_gtimer();                                        \
+            g_dec_trace[cid][3] = sm;                                                  \
+        }                                                                              \
+    } while (0)
+#else
+#define DEC_TRACE(k) \
+    do {             \
+    } while (0)
+#endif
 template <int G, int REP, int NGC, int AG, bool SP = false>
 __global__ void __launch_bounds__(320, kCtasPerSm) decode_mma_kernel(DecodeParams p) {
     static_assert(G == 4 && REP == 1 && (AG == 4 || AG == 2 || AG == 1), "decode_mma_kernel: MHA, 512-channel tiles");
@@ -138,6 +161,7 @@ __global__ void __launch_bounds__(320, kCtasPerSm) decode_mma_kernel(DecodeParam
         }
         return;
     }
+    DEC_TRACE(0);
     const int ntiles = static_cast<int>((t_end - t_begin + kTT - 1) / kTT);
     const int64_t row0 = static_cast<int64_t>(b) * p.max_tokens;
 
@@ -424,6 +448,7 @@ __global__ void __launch_bounds__(320, kCtasPerSm) decode_mma_kernel(DecodeParam
     // softmax + V, barrier, re-arm the stage with tile it + kNS.  The second
     // resident CTA fills the barrier bubbles.
     __syncthreads();  // mask words and plan
+    DEC_TRACE(1);
     int slot = 0;
     uint32_t phase = 0;
     for (int it = 0; it < ntiles; ++it) {
@@ -459,6 +484,7 @@ __global__ void __launch_bounds__(320, kCtasPerSm) decode_mma_kernel(DecodeParam
     dst[1] = make_float4(o[4], o[5], o[6], o[7]);
     dst[2] = make_float4(o[8], o[9], o[10], o[11]);
     dst[3] = make_float4(o[12], o[13], o[14], o[15]);
+    DEC_TRACE(2);
 }
 
 // ---------------------------------------------------------------------------
@@ -1059,3 +1085,9 @@ cudaError_t launch_decode_mma(const rkv_layer_desc& d, const DecodePlan& plan, c
 }
 
 }  // namespace rkv
+
+#ifdef RKV_DEC_TRACE
+extern "C" int rkv_debug_decode_trace(unsigned long long* out) {
+    return cudaMemcpyFromSymbol(out, rkv::g_dec_trace, sizeof(rkv::g_dec_trace)) == cudaSuccess ? 0 : 1;
+}
+#endif
