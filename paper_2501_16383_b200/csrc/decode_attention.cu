@@ -444,10 +444,15 @@ __global__ void __launch_bounds__(max_threads<N>(), 1) decode_split_kernel(Decod
 // out = (H_128 o'_rot / sqrt(128) + o_sink) / l.  One warp per (b, h); lane
 // owns channels 4*lane .. 4*lane+3, so H_128 is 2 register stages + 5 shuffle
 // stages and the sink dot products are warp reductions.
-__global__ void __launch_bounds__(128) decode_combine_kernel(DecodeParams p) {
-    const int lane = threadIdx.x & 31;
-    const int64_t wid = static_cast<int64_t>(blockIdx.x) * 4 + (threadIdx.x >> 5);
+__global__ void __launch_bounds__(256) decode_combine_kernel(DecodeParams p, int nw) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // nw == 1: four (b, h) per CTA, a warp merges all partials; nw > 1 (few
+    // heads, many partials): a CTA per (b, h), warp w merges the w-th range of
+    // partials and warp 0 folds the nw results in order
+    const int64_t wid = nw == 1 ? static_cast<int64_t>(blockIdx.x) * 4 + warp : blockIdx.x;
     if (wid >= static_cast<int64_t>(p.B) * p.Hq) return;
+    const int span = (p.NP + nw - 1) / nw;
+    const int s_begin = nw == 1 ? 0 : warp * span, s_end = nw == 1 ? p.NP : min(p.NP, s_begin + span);
     const int b = static_cast<int>(wid / p.Hq), h = static_cast<int>(wid % p.Hq), C = p.C;
     const int64_t base = static_cast<int64_t>(b) * p.NP * p.Hq;
     const int64_t T = p.seq_len[b];
@@ -461,7 +466,7 @@ __global__ void __launch_bounds__(128) decode_combine_kernel(DecodeParams p) {
     const int nsink = p.partial_ml ? 0 : min(p.cache.sink_count[b], p.max_sinks);
     float qraw[8];
     float2 rq[4];
-    {
+    if (warp == 0 || nw == 1) {
         const uint16_t* qh = p.q + (static_cast<int64_t>(b) * p.Hq + h) * 128;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -473,19 +478,19 @@ __global__ void __launch_bounds__(128) decode_combine_kernel(DecodeParams p) {
     }
     float4 ov[32];
     {
-        const int n0 = min(32, p.NP);
-        const float4* src = reinterpret_cast<const float4*>(p.ws_o + (base + h) * 128) + lane;
+        const int n0 = min(32, s_end - s_begin);
+        const float4* src = reinterpret_cast<const float4*>(p.ws_o + (base + static_cast<int64_t>(s_begin) * p.Hq + h) * 128) + lane;
         const int64_t stride = static_cast<int64_t>(p.Hq) * 32;  // float4 per partial row step
 #pragma unroll
         for (int k = 0; k < 32; ++k) ov[k] = k < n0 ? src[k * stride] : make_float4(0.f, 0.f, 0.f, 0.f);
     }
     float M = -INFINITY, L = 0.f;
     float4 rot = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int s0 = 0; s0 < p.NP; s0 += 32) {
+    for (int s0 = s_begin; s0 < s_end; s0 += 32) {
         const int s = s0 + lane;
         const int64_t r = base + static_cast<int64_t>(s) * p.Hq + h;
-        const float ms = s < p.NP ? p.ws_ml[r * 2] : -INFINITY;
-        const float ls = s < p.NP ? p.ws_ml[r * 2 + 1] : 0.f;
+        const float ms = s < s_end ? p.ws_ml[r * 2] : -INFINITY;
+        const float ls = s < s_end ? p.ws_ml[r * 2 + 1] : 0.f;
         float mx = ms;
 #pragma unroll
         for (int o = 16; o >= 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -499,8 +504,8 @@ __global__ void __launch_bounds__(128) decode_combine_kernel(DecodeParams p) {
         L = L * a + lw;
         rot = make_float4(rot.x * a, rot.y * a, rot.z * a, rot.w * a);
         M = mn;
-        const int n = min(32, p.NP - s0);
-        if (s0 > 0) {  // partials beyond the first 32 (long sequences with many splits)
+        const int n = min(32, s_end - s0);
+        if (s0 > s_begin) {  // partials beyond the first 32 (long sequences with many splits)
             const float4* src = reinterpret_cast<const float4*>(p.ws_o + (base + static_cast<int64_t>(s0) * p.Hq + h) * 128) + lane;
             const int64_t stride = static_cast<int64_t>(p.Hq) * 32;
 #pragma unroll
@@ -510,6 +515,26 @@ __global__ void __launch_bounds__(128) decode_combine_kernel(DecodeParams p) {
         for (int k = 0; k < 32; ++k) {
             const float wk = __shfl_sync(0xffffffffu, w, k);  // 0 past n (ms = -inf)
             rot = make_float4(rot.x + wk * ov[k].x, rot.y + wk * ov[k].y, rot.z + wk * ov[k].z, rot.w + wk * ov[k].w);
+        }
+    }
+    if (nw > 1) {  // fold the warps' (M, L, rot) in warp order
+        __shared__ float4 s_rot[8][32];
+        __shared__ float s_ml[8][2];
+        s_rot[warp][lane] = rot;
+        if (lane == 0) {
+            s_ml[warp][0] = M;
+            s_ml[warp][1] = L;
+        }
+        __syncthreads();
+        if (warp != 0) return;
+        for (int w = 1; w < nw; ++w) {
+            const float mw = s_ml[w][0];
+            if (mw == -INFINITY) continue;
+            const float mn = fmaxf(M, mw), a = exp2f(M - mn), c = exp2f(mw - mn);
+            const float4 r = s_rot[w][lane];
+            L = L * a + s_ml[w][1] * c;
+            rot = make_float4(rot.x * a + r.x * c, rot.y * a + r.y * c, rot.z * a + r.z * c, rot.w * a + r.w * c);
+            M = mn;
         }
     }
     if (p.partial_ml) {  // sequence-parallel partial: merged (m, l) and the unnormalised rotated o'
@@ -668,8 +693,14 @@ cudaError_t launch_decode_nr(const DecodePlan& plan, const DecodeParams& p, int 
 }  // namespace
 
 cudaError_t launch_decode_combine(const DecodeParams& p, int B, cudaStream_t s) {
-    const int64_t warps = static_cast<int64_t>(B) * p.Hq;
-    decode_combine_kernel<<<static_cast<unsigned>((warps + 3) / 4), 128, 0, s>>>(p);
+    const int64_t heads = static_cast<int64_t>(B) * p.Hq;
+    // few heads and many partials (small batch, long splits): one CTA per head,
+    // up to 8 warps each merging a range of partials
+    const int nw = heads < 2 * num_sms() ? static_cast<int>(std::min<int64_t>(8, (p.NP + 31) / 32)) : 1;
+    if (nw > 1)
+        decode_combine_kernel<<<static_cast<unsigned>(heads), 32 * nw, 0, s>>>(p, nw);
+    else
+        decode_combine_kernel<<<static_cast<unsigned>((heads + 3) / 4), 128, 0, s>>>(p, 1);
     return cudaGetLastError();
 }
 

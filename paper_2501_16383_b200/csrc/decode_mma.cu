@@ -1075,7 +1075,6 @@ cudaError_t launch_decode_mma(const rkv_layer_desc& d, const DecodePlan& plan, c
         if (e != cudaSuccess) return e;
         return launch_decode_combine(p, d.batch, s);
     }
-    const int NG = p.C / 512;
     auto kern = mha_kernel(p.C / 512, d.heads_per_group, sp);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(plan.smem));
     if (e != cudaSuccess) return e;
