@@ -101,7 +101,9 @@ constexpr int kPP = 2, kTT = 2 * kPP, kNS = 3, kCtasPerSm = 2;
 
 // G = 4 (N = 512), one q head per KV head.  NGC = number of FWHT groups
 // (C / 512) when known at compile time (8: LLaMA-2-7B, 10: 13B), so every
-// shared-memory offset folds into an immediate; 0 = taken from the launch.
+// shared-memory offset folds into an immediate; 0 = taken from the launch
+// (<= 10 groups: 320 threads, two CTAs per SM); -1 = taken from the launch,
+// 11 or 12 groups (384 threads, one CTA per SM).
 // AG = heads per rotation group of the layer (4, 2 or 1): the kernel always
 // works on 512-channel (pseudo-)groups; only the second FWHT factor differs
 // (hadamard_f2_frag) -- the head bits 7, 8 pass through it when AG < 4.
@@ -129,14 +131,14 @@ __device__ __forceinline__ unsigned long long dec_gtimer() {
     } while (0)
 #endif
 template <int G, int REP, int NGC, int AG, bool SP = false>
-__global__ void __launch_bounds__(320, kCtasPerSm) decode_mma_kernel(DecodeParams p) {
+__global__ void __launch_bounds__(NGC < 0 ? kMmaMaxThreads : 320, NGC < 0 ? 1 : kCtasPerSm) decode_mma_kernel(DecodeParams p) {
     static_assert(G == 4 && REP == 1 && (AG == 4 || AG == 2 || AG == 1), "decode_mma_kernel: MHA, 512-channel tiles");
     constexpr int N = 128 * G;
     constexpr int NJ = N / 128;  // MMA-1 instances per token (F2 bit 3, outer bit 6)
 
     extern __shared__ __align__(128) unsigned char smem[];
-    const int NG = NGC ? NGC : p.C / N;
-    const int C = NG * N, W = C / 16, MG = C / 128, Hq = NGC ? NGC * G * REP : p.Hq;
+    const int NG = NGC > 0 ? NGC : p.C / N;
+    const int C = NG * N, W = C / 16, MG = C / 128, Hq = NGC > 0 ? NGC * G * REP : p.Hq;
     const MmaSmem lay = mma_smem(C, kTT, p.chunk, kNS);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + lay.mbar);
     uint32_t* mask_s = reinterpret_cast<uint32_t*>(smem + lay.mask);
@@ -968,6 +970,7 @@ using MhaKernel = void (*)(DecodeParams);
 // compile-time tile counts for the LLaMA-2-7B / 13B widths (8 and 10 tiles of 512 channels)
 template <int AG>
 MhaKernel mha_kernel_g(int NG, bool sp) {
+    if (NG > 10) return sp ? decode_mma_kernel<4, 1, -1, AG, true> : decode_mma_kernel<4, 1, -1, AG>;
     if (sp) return decode_mma_kernel<4, 1, 0, AG, true>;  // partials: generic tile count
     return NG == 10 ? decode_mma_kernel<4, 1, 10, AG> : NG == 8 ? decode_mma_kernel<4, 1, 8, AG> : decode_mma_kernel<4, 1, 0, AG>;
 }

@@ -170,6 +170,8 @@ def oracle_decode(oracle, layer, got, b, T, q, w, perm, kraw, vraw):
     (16, 8, 4, 10000.0, 77), (32, 32, 4, 10000.0, 1500),
     # per-head (G = 1) and two-head (G = 2) rotations on the 512-channel tensor-core tiles
     (8, 8, 1, 10000.0, 300), (40, 40, 1, 10000.0, 513), (40, 40, 2, 10000.0, 257), (32, 32, 1, 500000.0, 1024),
+    # the widest tensor-core tiles: 11 and 12 FWHT groups per CTA (C = 5632, 6144)
+    (44, 44, 4, 10000.0, 90), (48, 48, 4, 10000.0, 130), (48, 48, 1, 10000.0, 70),
 ])
 def test_decode_vs_oracle(oracle, hq, hkv, g, base, T):
     w = small_workload(hq, hkv, g, base=base)

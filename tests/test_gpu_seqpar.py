@@ -23,7 +23,8 @@ def rel(a, b):
     return float(np.abs(a - b).max() / np.abs(b).max())
 
 
-@pytest.mark.parametrize("hq,hkv,g,world", [(8, 8, 4, 2), (8, 8, 4, 5), (32, 8, 2, 3), (4, 4, 1, 2), (40, 40, 4, 8)])
+@pytest.mark.parametrize("hq,hkv,g,world", [(8, 8, 4, 2), (8, 8, 4, 5), (32, 8, 2, 3), (4, 4, 1, 2), (40, 40, 4, 8),
+                                              (48, 48, 4, 3)])
 def test_partials_merge_to_the_full_decode(oracle, hq, hkv, g, world):
     lens = [700, 129, 64, 1]
     B, T = len(lens), max(lens)
