@@ -172,6 +172,8 @@ def oracle_decode(oracle, layer, got, b, T, q, w, perm, kraw, vraw):
     (8, 8, 1, 10000.0, 300), (40, 40, 1, 10000.0, 513), (40, 40, 2, 10000.0, 257), (32, 32, 1, 500000.0, 1024),
     # the widest tensor-core tiles: 11 and 12 FWHT groups per CTA (C = 5632, 6144)
     (44, 44, 4, 10000.0, 90), (48, 48, 4, 10000.0, 130), (48, 48, 1, 10000.0, 70),
+    # beyond the tensor-core tiles: C = 8192 (CUDA-core kernel), GQA 4:1 at 16 KV heads
+    (64, 64, 4, 10000.0, 70), (64, 16, 2, 500000.0, 70),
 ])
 def test_decode_vs_oracle(oracle, hq, hkv, g, base, T):
     w = small_workload(hq, hkv, g, base=base)
@@ -191,6 +193,18 @@ def test_decode_vs_oracle(oracle, hq, hkv, g, base, T):
                              v[b].cpu().numpy())
         assert rel_err(out[b], want) < REL_TOL
         assert cosine(out[b], want) > COS_TOL
+
+
+@pytest.mark.parametrize("hq,hkv,g", [(64, 16, 4), (96, 8, 2), (64, 64, 1)])
+def test_decode_unsupported_shapes_refused(hq, hkv, g):
+    """Shapes no sm_100a decode kernel tiles raise ValueError (the reference's
+    std::invalid_argument) instead of launching anything."""
+    w = small_workload(hq, hkv, g)
+    with pytest.raises(ValueError):
+        layer, _ = build_layer(w, 2, 78, seed=1)
+        k, v = WL.make_kv(w, 70, 2, 70)
+        layer.append(k, v)
+        layer.decode(WL.make_q(w, 70, 2))
 
 
 def test_decode_ragged_lengths(oracle):
