@@ -66,6 +66,9 @@ def check(got, want):
     (32, 8, 2, 33, (), 5),
     (8, 8, 1, 70, (0, 9), 6),
     (8, 8, 2, 45, (0,), 7),
+    # the widest tensor-core layer: 12 FWHT groups (C = 6144)
+    (48, 48, 4, 50, (0, 7), 8),
+    (48, 48, 1, 40, (0,), 9),
 ])
 def test_prefill_matches_oracle(oracle, hq, hkv, g, T, sinks, seed):
     layer, k, v, flags, q, perm = build(hq, hkv, g, T, sinks, seed)
@@ -94,6 +97,14 @@ def test_prefill_rejects_bad_arguments():
         layer.prefill_attention(q, q_start=np.full(2, 5, np.int64))  # rows past the cache
     with pytest.raises(ValueError):
         layer.prefill_attention(q.float())
+
+
+@pytest.mark.parametrize("hq,hkv,g", [(64, 64, 4), (64, 16, 2), (16, 8, 4)])
+def test_prefill_refuses_shapes_outside_the_tensor_core_path(hq, hkv, g):
+    """C = 8192, GQA beyond 8 KV heads and 2:1 GQA: ValueError, nothing launched."""
+    layer, k, v, flags, q, perm = build(hq, hkv, g, 20, (0,), 1)
+    with pytest.raises(ValueError, match="tensor-core path"):
+        layer.prefill_attention(q, q_start=np.zeros(2, np.int64))
 
 
 def test_prefill_rejects_more_than_16_sink_rows():
