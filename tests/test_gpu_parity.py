@@ -57,6 +57,8 @@ def cache_host(layer):
     (8, 8, 4, P.SCALE_FP16_CEIL), (8, 8, 2, P.SCALE_FP16_CEIL), (4, 4, 1, P.SCALE_FP16_CEIL),
     (40, 40, 4, P.SCALE_FP16_CEIL), (32, 8, 2, P.SCALE_FP16_CEIL), (8, 8, 4, P.SCALE_E4M3_CEIL),
     (40, 40, 4, P.SCALE_E4M3_CEIL),
+    # the widest rows (C = 8192; 256 regions per token) and a narrow 4:1 GQA layer at G = 1 (C = 512)
+    (64, 64, 4, P.SCALE_FP16_CEIL), (64, 64, 1, P.SCALE_E4M3_CEIL), (16, 4, 1, P.SCALE_FP16_CEIL),
 ])
 def test_quantize_kv_bit_exact_vs_oracle(oracle, hq, hkv, g, fmt):
     w = small_workload(hq, hkv, g)
