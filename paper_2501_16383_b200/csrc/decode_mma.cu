@@ -1055,6 +1055,8 @@ DecodePlan plan_decode_mma(const rkv_layer_desc& d, int64_t max_seq_len) {
         }
         if (best >= 0.95) break;
     }
+    if (const char* e = std::getenv("RKV_DEC_SPLITS"))  // experiment knob: splits per sequence
+        if (std::atoi(e) > 0) S = static_cast<int>(std::min<int64_t>(max_split, std::atoi(e)));
     int64_t chunk = (max_seq_len + S - 1) / S;
     chunk = (chunk + pl.TT - 1) / pl.TT * pl.TT;
     pl.chunk = static_cast<int>(chunk);
