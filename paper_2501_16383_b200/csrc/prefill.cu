@@ -77,9 +77,12 @@ __global__ void __launch_bounds__(512) reconstruct_keys_kernel(PrefillParams p) 
     unsigned char* knat = smem;                                             // 2 token-pair rows
     uint32_t* kcs = reinterpret_cast<uint32_t*>(smem + 2 * pair_bytes);    // [TT][W]
     uint32_t* kms = kcs + TT * W;                                           // [TT][MG]
+    float4* rps = reinterpret_cast<float4*>(kms + TT * MG);                // [TT][32] RoPE frequency-pair rows
     const int64_t row0 = static_cast<int64_t>(b) * p.max_tokens + t0;
     for (int i = tid; i < TT * W; i += NT) kcs[i] = i / W < nv ? p.cache.k_codes[row0 * W + i] : 0u;
     for (int i = tid; i < TT * MG; i += NT) kms[i] = i / MG < nv ? p.cache.k_meta[row0 * MG + i] : 0u;
+    for (int i = tid; i < TT * 32; i += NT)  // staged with the codes: no dependent load in the MMA half
+        if (i / 32 < nv) rps[i] = __ldg(p.rope + ((t0 + i / 32) >> 1) * kRopeRowF4 + 64 + ((t0 + i / 32) & 1) * 32 + (i & 31));
     __syncthreads();
     // scatter (same plan and arithmetic as the decode kernel): thread = word position(s)
     const uint32_t* plan = p.plan + kPlanHeader;
@@ -137,11 +140,11 @@ __global__ void __launch_bounds__(512) reconstruct_keys_kernel(PrefillParams p) 
 #pragma unroll
             for (int jc = 0; jc < NJ; ++jc) mma16816(yf[jc], AH, bf[tk][jc][0], bf[tk][jc][1], zero);
             // frequency-pair row of the token (rope section 2): (u,u',w,w') for G = 4, (c,c',s,s') else
-            const float4* rrow = p.rope + (pos >> 1) * kRopeRowF4 + 64 + (pos & 1) * 32;
+            const float4* rrow = rps + tt * 32;
 #pragma unroll
             for (int f1 = 0; f1 < 2; ++f1) {
                 const int f = 2 * tl + 8 * f1 + 16 * (g & 3);
-                const float4 r4 = __ldg(rrow + rope_pair_slot(f >> 1));
+                const float4 r4 = rrow[rope_pair_slot(f >> 1)];
                 if constexpr (G == 4) {
                     float z[2][4];
 #pragma unroll
@@ -803,7 +806,7 @@ bool prefill_pair() {
 cudaError_t launch_prefill(const rkv_layer_desc& d, const PrefillParams& p, int64_t max_seq_len, cudaStream_t s) {
     const int C = p.C, W = C / 16, MG = C / 128;
     const int N = mma_layout_n(d), NG = C / N;
-    const size_t ksmem = 2 * static_cast<size_t>(C) * 4 + 4 * static_cast<size_t>(W + MG) * 4;
+    const size_t ksmem = 2 * static_cast<size_t>(C) * 4 + 4 * static_cast<size_t>(W + MG) * 4 + 4 * 32 * 16;
     const int nthreads = std::min(512, std::max(NG * 32, ((2 * W + 31) / 32) * 32));
     const dim3 kgrid(static_cast<unsigned>((max_seq_len + 3) / 4), static_cast<unsigned>(d.batch));
     cudaError_t e;
