@@ -262,11 +262,24 @@ __global__ void __launch_bounds__(128) prepare_queries_kernel(PrefillParams p) {
     }
     const uint32_t sw = static_cast<uint32_t>(i & 31);
     auto put = [&](uint32_t* row, uint32_t u, uint32_t v) { row[((((u >> 2) ^ sw) & 31u) << 2) | (u & 3u)] = v; };
-    for (int h = h0; h < min(h0 + 4, p.Hq); ++h) {
+    // the 4 heads' query words, requested together before any store
+    uint32_t qw[4][2] = {};
+    if (live)
+#pragma unroll
+        for (int hh = 0; hh < 4; ++hh)
+            if (h0 + hh < p.Hq) {
+                const uint32_t* qr = reinterpret_cast<const uint32_t*>(
+                    p.q + ((static_cast<int64_t>(b) * p.num_q + i) * p.Hq + h0 + hh) * 128);
+                qw[hh][0] = __ldg(qr + lane);
+                qw[hh][1] = __ldg(qr + 32 + lane);
+            }
+#pragma unroll
+    for (int hh = 0; hh < 4; ++hh) {
+        const int h = h0 + hh;
+        if (h >= p.Hq) break;
         float qa[2] = {0.f, 0.f}, qv[2] = {0.f, 0.f};
         if (live) {
-            const uint16_t* qr = p.q + ((static_cast<int64_t>(b) * p.num_q + i) * p.Hq + h) * 128;
-            const uint32_t wa = *reinterpret_cast<const uint32_t*>(qr + f), wb = *reinterpret_cast<const uint32_t*>(qr + f + 64);
+            const uint32_t wa = qw[hh][0], wb = qw[hh][1];
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
                 const float a = h2f(static_cast<uint16_t>(k ? wa >> 16 : wa & 0xffffu));
