@@ -123,6 +123,34 @@ rkv_status rkv_quantize_kv(const rkv_layer_desc* desc, const uint16_t* k_new, co
                            const int32_t* perm, const uint8_t* sink_flags, const int64_t* start_pos,
                            int64_t num_new, const rkv_cache* cache, void* stream);
 
+/* promote_to_sink / route_sinks (proj/src/kv_cache.cpp:43-55,
+ * proj/src/sink.cpp:47-63): move already-appended tokens into the fp16
+ * sidecar.
+ *   tokens   : [B][num_tokens] int64, device: token index per sequence (-1 = no entry)
+ *   k_rows, v_rows : [B][num_tokens][C] fp16, device: the raw (pre-rotation,
+ *              pre-RoPE) K/V rows of those tokens -- what append's sink path stores
+ *   promoted : [B] int32 device (tokens newly promoted per sequence) or NULL
+ * Per sequence, tokens are taken in list order: indices outside
+ * [0, max_tokens) and tokens that are already sinks are skipped (the
+ * reference returns early for sinks: idempotent, duplicates included), and a
+ * full sidecar (max_sinks) leaves the rest quantized.  A promoted token gets
+ * the next sidecar slot, its sink-mask bit and sink_pos, and its packed
+ * words and metadata are zeroed.  The caller checks token < cache length
+ * (the reference's std::out_of_range; the device cannot throw).
+ * num_tokens <= 256.  Stream-ordered, graph-capturable. */
+rkv_status rkv_promote_sinks(const rkv_layer_desc* desc, const rkv_cache* cache, const int64_t* tokens,
+                             int64_t num_tokens, const uint16_t* k_rows, const uint16_t* v_rows, int32_t* promoted,
+                             void* stream);
+
+/* Experiment switches (process-global; defaults are the production
+ * choices): "decode_kernel_simt" (1 = decode tensor-core shapes on the
+ * CUDA-core kernel), "gqa_warps_per_group" (2..4), "gqa_tmem" (0/1),
+ * "decode_splits" (> 0 forces the split count), "prefill_pair" (1 = 2-SM
+ * prefill attention), "simt_pairs", "simt_stages".  The kernel selection is
+ * recorded in layer plans and RoPE tables: build them after setting a switch
+ * (a decode with a plan of another kernel kind returns NaN). */
+rkv_status rkv_set_debug_option(const char* name, int64_t value);
+
 /* Per-layer decode plan (once per layer, after calibration): from the HOST
  * permutation perm [C] (slot j <- channel perm[j]) choose which packed word
  * each decode thread un-reorders so the shared-memory scatter's bank

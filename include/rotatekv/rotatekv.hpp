@@ -137,7 +137,11 @@ public:
         check(rkv_layer_plan_init(&desc_, perm.data(), plan_, plan_bytes_, stream_));
         ws_bytes_ = rkv_decode_workspace_bytes(&desc_, desc.max_tokens);
         check_cuda(cudaMalloc(&ws_, ws_bytes_), "cudaMalloc workspace");
-        check_cuda(cudaMalloc(&dev_pos_, static_cast<size_t>(desc.batch) * sizeof(int64_t)), "cudaMalloc pos");
+        // a small ring of device length vectors: each call stages the host lengths
+        // into the next slot (stream-ordered, no synchronization per call)
+        check_cuda(cudaMalloc(&dev_pos_, kPosRing * static_cast<size_t>(desc.batch) * sizeof(int64_t)),
+                   "cudaMalloc pos");
+        sink_set_.resize(static_cast<size_t>(desc.batch));
         check(rkv_cache_reset(&desc_, &cache_, stream_));
     }
     DeviceLayerCache(const DeviceLayerCache&) = delete;
@@ -151,6 +155,8 @@ public:
         cudaFree(dev_pos_);
         cudaFree(dev_qs_);
         cudaFree(pf_ws_);
+        cudaFree(flags_);
+        cudaFree(tok_);
     }
 
     int64_t size(int b) const { return len_.at(static_cast<size_t>(b)); }
@@ -160,6 +166,9 @@ public:
 
     // LayerKVCache::append for num_new tokens of every sequence.
     // k_new/v_new: device [B][num_new][C] fp16; sink_flags_host: [B][num_new] or empty.
+    // Stream-ordered: returns without synchronizing (k_new/v_new must stay valid
+    // until the stream reaches the append).  No allocation after the first
+    // call of a given flag size.
     void append(const uint16_t* k_new, const uint16_t* v_new, int64_t num_new,
                 const std::vector<uint8_t>& sink_flags_host = {}) {
         const int B = desc_.batch;
@@ -176,41 +185,78 @@ public:
                 if (sinks_[static_cast<size_t>(b)] + add > desc_.max_sinks)
                     throw std::out_of_range("cache: sink sidecar capacity exceeded");
             }
-            check_cuda(cudaMalloc(&dflags, sink_flags_host.size()), "cudaMalloc flags");
+            dflags = static_cast<uint8_t*>(grow(flags_, flags_bytes_, sink_flags_host.size()));
+            // pageable source: the call returns once the bytes are staged, so the
+            // host vector may change afterwards; the device copy is stream-ordered
             check_cuda(cudaMemcpyAsync(dflags, sink_flags_host.data(), sink_flags_host.size(), cudaMemcpyHostToDevice,
                                        stream_), "flags");
         }
-        check_cuda(cudaMemcpyAsync(dev_pos_, len_.data(), static_cast<size_t>(B) * sizeof(int64_t),
-                                   cudaMemcpyHostToDevice, stream_), "positions");
-        rkv_status st = rkv_quantize_kv(&desc_, k_new, v_new, perm_, dflags, dev_pos_, num_new, &cache_, stream_);
-        if (dflags) {
-            cudaStreamSynchronize(stream_);
-            cudaFree(dflags);
-        }
-        check(st);
+        int64_t* pos = stage_lengths();
+        check(rkv_quantize_kv(&desc_, k_new, v_new, perm_, dflags, pos, num_new, &cache_, stream_));
         for (int b = 0; b < B; ++b) {
             len_[static_cast<size_t>(b)] += num_new;
             if (!sink_flags_host.empty())
                 for (int64_t i = 0; i < num_new; ++i)
-                    sinks_[static_cast<size_t>(b)] += sink_flags_host[static_cast<size_t>(b * num_new + i)] != 0;
+                    if (sink_flags_host[static_cast<size_t>(b * num_new + i)]) {
+                        ++sinks_[static_cast<size_t>(b)];
+                        sink_set_[static_cast<size_t>(b)].push_back(len_[static_cast<size_t>(b)] - num_new + i);
+                    }
         }
-        check_cuda(cudaStreamSynchronize(stream_), "append");  // dev_pos_ is reused by the next call
+    }
+
+    // LayerKVCache::promote_to_sink / route_sinks (proj/src/kv_cache.cpp:43-55,
+    // proj/src/sink.cpp:47-63): tokens[b] = token indices of sequence b;
+    // k_rows/v_rows: device [B][n][C] fp16 raw rows of those tokens, n = the
+    // longest list (row i of sequence b belongs to tokens[b][i]).  Tokens that
+    // are already sinks are skipped; indices past the cache length throw
+    // std::out_of_range like the reference.  Stream-ordered.
+    void route_sinks(const std::vector<std::vector<int64_t>>& tokens, const uint16_t* k_rows, const uint16_t* v_rows) {
+        const int B = desc_.batch;
+        if (tokens.size() != static_cast<size_t>(B)) throw std::invalid_argument("route_sinks: one token list per sequence");
+        size_t n = 1;
+        for (const auto& t : tokens) n = std::max(n, t.size());
+        std::vector<int64_t> flat(static_cast<size_t>(B) * n, -1);
+        std::vector<std::vector<int64_t>> fresh(static_cast<size_t>(B));
+        for (int b = 0; b < B; ++b) {
+            auto& known = sink_set_[static_cast<size_t>(b)];
+            for (size_t i = 0; i < tokens[static_cast<size_t>(b)].size(); ++i) {
+                const int64_t t = tokens[static_cast<size_t>(b)][i];
+                if (t < 0 || t >= len_[static_cast<size_t>(b)]) throw std::out_of_range("route_sinks: token index out of range");
+                flat[static_cast<size_t>(b) * n + i] = t;
+                if (std::find(known.begin(), known.end(), t) == known.end() &&
+                    std::find(fresh[static_cast<size_t>(b)].begin(), fresh[static_cast<size_t>(b)].end(), t) ==
+                        fresh[static_cast<size_t>(b)].end())
+                    fresh[static_cast<size_t>(b)].push_back(t);
+            }
+            if (sinks_[static_cast<size_t>(b)] + static_cast<int64_t>(fresh[static_cast<size_t>(b)].size()) >
+                desc_.max_sinks)
+                throw std::out_of_range("cache: sink sidecar capacity exceeded");
+        }
+        int64_t* dtok = static_cast<int64_t*>(grow(tok_, tok_bytes_, flat.size() * sizeof(int64_t)));
+        check_cuda(cudaMemcpyAsync(dtok, flat.data(), flat.size() * sizeof(int64_t), cudaMemcpyHostToDevice, stream_),
+                   "tokens");
+        check(rkv_promote_sinks(&desc_, &cache_, dtok, static_cast<int64_t>(n), k_rows, v_rows, nullptr, stream_));
+        for (int b = 0; b < B; ++b) {
+            sinks_[static_cast<size_t>(b)] += static_cast<int64_t>(fresh[static_cast<size_t>(b)].size());
+            for (int64_t t : fresh[static_cast<size_t>(b)]) sink_set_[static_cast<size_t>(b)].push_back(t);
+        }
     }
 
     // The attention half of decode_step (proj/src/pipeline.cpp:211-261): q
     // [B][Hq][d] fp16 device (pre-RoPE, position = size-1), out [B][Hq][d] fp32.
+    // Stream-ordered: synchronize the stream (or copy out on it) before reading out.
     void decode_attention(const uint16_t* q, float* out) {
         int64_t mx = 0;
         for (int64_t l : len_) {
             if (l < 1) throw std::invalid_argument("decode_step: position must equal current cache length");
             mx = l > mx ? l : mx;
         }
-        check_cuda(cudaMemcpyAsync(dev_pos_, len_.data(), len_.size() * sizeof(int64_t), cudaMemcpyHostToDevice,
-                                   stream_), "seq_len");
-        check(rkv_decode_attention(&desc_, q, dev_pos_, mx, &cache_, plan_, static_cast<const float*>(rope_), out, ws_,
+        int64_t* lens = stage_lengths();
+        check(rkv_decode_attention(&desc_, q, lens, mx, &cache_, plan_, static_cast<const float*>(rope_), out, ws_,
                                    ws_bytes_, stream_));
-        check_cuda(cudaStreamSynchronize(stream_), "decode");
     }
+
+    void synchronize() const { check_cuda(cudaStreamSynchronize(stream_), "synchronize"); }
 
     // The attention half of prefill (proj/src/pipeline.cpp:156-191: reconstruct_cache,
     // causal reference_attention): q [B][num_q][Hq][d] fp16 device, row i of
@@ -236,11 +282,9 @@ public:
         if (!dev_qs_) check_cuda(cudaMalloc(&dev_qs_, len_.size() * sizeof(int64_t)), "cudaMalloc q_start");
         check_cuda(cudaMemcpyAsync(dev_qs_, q_start.data(), len_.size() * sizeof(int64_t), cudaMemcpyHostToDevice,
                                    stream_), "q_start");
-        check_cuda(cudaMemcpyAsync(dev_pos_, len_.data(), len_.size() * sizeof(int64_t), cudaMemcpyHostToDevice,
-                                   stream_), "seq_len");
-        check(rkv_prefill_attention(&desc_, q, num_q, dev_qs_, dev_pos_, mx, &cache_, plan_,
+        int64_t* lens = stage_lengths();
+        check(rkv_prefill_attention(&desc_, q, num_q, dev_qs_, lens, mx, &cache_, plan_,
                                     static_cast<const float*>(rope_), out, pf_ws_, pf_ws_bytes_, stream_));
-        check_cuda(cudaStreamSynchronize(stream_), "prefill");
     }
 
     // LayerKVCache::serialize (proj/src/kv_cache.cpp:119-139) of sequence b;
@@ -263,9 +307,36 @@ public:
         int32_t count = 0;
         check_cuda(cudaMemcpy(&count, cache_.sink_count + b, sizeof(int32_t), cudaMemcpyDeviceToHost), "sink count");
         sinks_[static_cast<size_t>(b)] = count;
+        std::vector<int32_t> pos(static_cast<size_t>(count));
+        if (count > 0)
+            check_cuda(cudaMemcpy(pos.data(), cache_.sink_pos + static_cast<int64_t>(b) * desc_.max_sinks,
+                                  pos.size() * sizeof(int32_t), cudaMemcpyDeviceToHost),
+                       "sink positions");
+        sink_set_[static_cast<size_t>(b)].assign(pos.begin(), pos.end());
     }
 
 private:
+    static constexpr size_t kPosRing = 8;
+    // copy the host lengths into the next device slot (stream-ordered)
+    int64_t* stage_lengths() {
+        int64_t* slot = dev_pos_ + (pos_next_++ % kPosRing) * len_.size();
+        check_cuda(cudaMemcpyAsync(slot, len_.data(), len_.size() * sizeof(int64_t), cudaMemcpyHostToDevice, stream_),
+                   "lengths");
+        return slot;
+    }
+    // grow-only device scratch (the old buffer is freed only when it grows)
+    void* grow(void*& buf, size_t& have, size_t need) {
+        if (need > have) {
+            if (buf) {
+                check_cuda(cudaStreamSynchronize(stream_), "scratch");
+                cudaFree(buf);
+                buf = nullptr;
+            }
+            check_cuda(cudaMalloc(&buf, need), "cudaMalloc scratch");
+            have = need;
+        }
+        return buf;
+    }
     rkv_layer_desc desc_;
     cudaStream_t stream_;
     std::vector<int64_t> len_, sinks_;
@@ -283,6 +354,12 @@ private:
     int64_t* dev_qs_ = nullptr;
     void* pf_ws_ = nullptr;
     size_t pf_ws_bytes_ = 0;
+    void* flags_ = nullptr;
+    size_t flags_bytes_ = 0;
+    void* tok_ = nullptr;
+    size_t tok_bytes_ = 0;
+    size_t pos_next_ = 0;
+    std::vector<std::vector<int64_t>> sink_set_;
     std::vector<int32_t> perm_host_;
 };
 

@@ -117,6 +117,9 @@ def ref():
         R.ref_bench_step.restype = C.c_double
         R.ref_bench_step.argtypes = [C.c_void_p, C.c_int]
         R.ref_bench_destroy.argtypes = [C.c_void_p]
+        R.ref_bench_set_memo.argtypes = [C.c_void_p, C.c_int]
+        R.ref_decode_step_routed.argtypes = ([C.c_int64] * 3 + [C.c_void_p] * 3 + [C.c_int64, C.c_void_p, C.c_int64,
+                                             C.c_void_p, C.c_double, C.c_void_p, C.c_void_p])
     return _ref
 
 
@@ -324,6 +327,26 @@ def ref_decode_step(k_raw, v_raw, sink, perm, x, num_heads, head_dim, heads_per_
                                _p(perm), float(rope_base), _p(x), _p(out))
     if rc != 0:
         raise ValueError("ref_decode_step failed")
+    return out
+
+
+def ref_decode_step_routed(k_raw, v_raw, sink, promote, perm, x, num_heads, head_dim, heads_per_group, rope_base):
+    """The reference's cache filled with append-time sinks `sink`, then
+    route_sinks(promote) with the fused-frame rows, then one decode_step."""
+    k_raw = f32(k_raw)
+    v_raw = f32(v_raw)
+    T, c = k_raw.shape
+    sink = np.ascontiguousarray(sink, dtype=np.uint8)
+    promote = np.ascontiguousarray(promote, dtype=np.int64)
+    perm = np.ascontiguousarray(perm, dtype=np.int32)
+    x = f32(x)
+    out = np.empty(c, np.float32)
+    rc = ref().ref_decode_step_routed(num_heads, head_dim, heads_per_group, _p(k_raw), _p(v_raw), _p(sink), T,
+                                      _p(promote), promote.size, _p(perm), float(rope_base), _p(x), _p(out))
+    if rc == -1:
+        raise IndexError("ref_decode_step_routed: the reference threw")
+    if rc != 0:
+        raise ValueError(f"ref_decode_step_routed failed ({rc})")
     return out
 
 

@@ -56,6 +56,8 @@ struct RefBench {
     PipelineConfig cfg;
     AttentionWeights w;
     std::vector<LayerKVCache> caches;
+    std::vector<DecodeMemo> memos;  // the reference's own memoisation of reconstructed keys (pipeline.hpp:78-81)
+    bool use_memo = true;
     std::vector<int64_t> position;
     uint64_t seed = 0;
 };
@@ -338,6 +340,7 @@ void* ref_bench_create(int64_t num_heads, int64_t head_dim, int64_t hpg, int64_t
         b->w.wo = eye(b->c);
         fuse_weights(b->w, b->cfg.key_rotation, b->cfg.reorder, b->cfg.value_rotation);
         b->caches.assign(static_cast<size_t>(nseq), LayerKVCache(q, b->c));
+        b->memos.assign(static_cast<size_t>(nseq), DecodeMemo{});
         b->position.assign(static_cast<size_t>(nseq), T);
         parallel_for(nseq, nthreads, [&](int64_t s) {
             Tensor k = synth_rows(T, b->c, seed ^ (0x1000ULL + static_cast<uint64_t>(s)));
@@ -361,7 +364,8 @@ double ref_bench_step(void* handle, int nthreads) {
     parallel_for(static_cast<int64_t>(b->caches.size()), nthreads, [&](int64_t s) {
         auto& pos = b->position[static_cast<size_t>(s)];
         Tensor x = synth_rows(1, b->c, b->seed ^ (0x3000ULL + static_cast<uint64_t>(s) * 7919ULL + static_cast<uint64_t>(pos)));
-        Tensor o = decode_step(x, b->caches[static_cast<size_t>(s)], b->w, b->cfg, pos, nullptr);
+        Tensor o = decode_step(x, b->caches[static_cast<size_t>(s)], b->w, b->cfg, pos,
+                               b->use_memo ? &b->memos[static_cast<size_t>(s)] : nullptr);
         (void)o;
         ++pos;
     });
@@ -370,5 +374,53 @@ double ref_bench_step(void* handle, int nthreads) {
 }
 
 void ref_bench_destroy(void* handle) { delete static_cast<RefBench*>(handle); }
+
+// memo = 1 (default): decode_step memoises the reconstructed post-RoPE keys
+// across steps (the reference's DecodeMemo; the first step after creation
+// reconstructs the whole cache once); memo = 0: every step reconstructs it.
+void ref_bench_set_memo(void* handle, int memo) { static_cast<RefBench*>(handle)->use_memo = memo != 0; }
+
+// route_sinks after the fact (proj/src/sink.cpp:47-63 -> kv_cache.cpp:43-55):
+// the cache is filled like ref_decode_step (sinks flagged at append time in
+// `sink`), then the tokens `promote[0..np)` are routed to the fp32 sidecar with
+// their fused-frame rows, then one decode_step with x.  Returns -1 on an
+// exception (e.g. an out-of-range token), -2 if promote_to_sink did not make
+// the tokens sinks.
+int ref_decode_step_routed(int64_t num_heads, int64_t head_dim, int64_t hpg, const float* k_raw, const float* v_raw,
+                           const uint8_t* sink, int64_t T, const int64_t* promote, int64_t np, const int32_t* perm,
+                           double rope_base, const float* x, float* out) {
+    try {
+        int64_t c = num_heads * head_dim;
+        QuantConfig q;
+        q.bits = 2;
+        q.group_size = 128;
+        PipelineConfig cfg = PipelineConfig::make(PipelineMode::RotateKV, num_heads, head_dim, hpg, q, true);
+        cfg.reorder = plan_from_perm(perm, c);
+        cfg.rope.base = rope_base;
+        AttentionWeights w;
+        w.wq = eye(c);
+        w.wk = eye(c);
+        w.wv = eye(c);
+        w.wo = eye(c);
+        fuse_weights(w, cfg.key_rotation, cfg.reorder, cfg.value_rotation);
+        LayerKVCache cache(q, c);
+        Tensor k({T, c}, std::vector<float>(k_raw, k_raw + T * c));
+        Tensor v({T, c}, std::vector<float>(v_raw, v_raw + T * c));
+        Tensor kt = apply_reorder(rotate_rows(k, cfg.key_rotation, false), cfg.reorder, 0, false);
+        Tensor vt = rotate_rows(v, cfg.value_rotation, false);
+        for (int64_t t = 0; t < T; ++t)
+            cache.append(std::span<const float>(kt.data() + t * c, static_cast<size_t>(c)),
+                         std::span<const float>(vt.data() + t * c, static_cast<size_t>(c)), sink[t] != 0);
+        SinkSet set;
+        for (int64_t i = 0; i < np; ++i) set.tokens.push_back(promote[i]);
+        route_sinks(cache, set, kt, vt);
+        for (int64_t i = 0; i < np; ++i)
+            if (!cache.is_sink(promote[i])) return -2;
+        Tensor row({1, c}, std::vector<float>(x, x + c));
+        Tensor o = decode_step(row, cache, w, cfg, T, nullptr);
+        std::memcpy(out, o.data(), sizeof(float) * static_cast<size_t>(c));
+        return 0;
+    } catch (const std::exception&) { return -1; }
+}
 
 }  // extern "C"

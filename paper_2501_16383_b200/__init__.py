@@ -21,4 +21,5 @@ from .rotatekv import (  # noqa: F401
     layer_plan_build,
     lib,
     rotate_keys,
+    set_debug_option,
 )

@@ -18,7 +18,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "librotatekv_b200.so")
 INCLUDE = os.path.join(ROOT, "include")
-SOURCES = ["rkv_api.cu", "rkv_plan.cu", "quantize_kv.cu", "decode_attention.cu", "decode_mma.cu", "prefill.cu", "sink_detect.cu"]
+SOURCES = ["rkv_api.cu", "rkv_runtime.cu", "rkv_plan.cu", "quantize_kv.cu", "decode_attention.cu", "decode_mma.cu", "prefill.cu", "sink_detect.cu"]
 HEADERS = ["rkv_common.cuh", "rkv_internal.h", "rkv_layout.h", "rkv_mma.cuh", "rkv_umma.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
@@ -40,25 +40,41 @@ def _stale(target: str, deps) -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(INCLUDE, "rotatekv", "rotatekv.h")]
-    if not force and not _stale(LIB, deps):
-        return LIB
+    """Compile every source to an object (in parallel; an object is rebuilt when
+    its source, a shared header or the compiler flags changed) and link the
+    shared library."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    hdrs = [os.path.join(CSRC, f) for f in HEADERS] + [os.path.join(INCLUDE, "rotatekv", "rotatekv.h")]
+    extra = os.environ.get("RKV_NVCC_EXTRA", "").split()  # experiment flags (e.g. -DRKV_DEC_TRACE)
     os.makedirs(LIBDIR, exist_ok=True)
-    objs = []
+    stamp = os.path.join(LIBDIR, ".flags")
+    flags = " ".join(ARCH + NVCC_FLAGS + extra)
+    flags_changed = not os.path.exists(stamp) or open(stamp).read() != flags
+    objs, jobs = [], []
     for src in SOURCES:
         obj = os.path.join(LIBDIR, src.replace(".cu", ".o"))
-        extra = os.environ.get("RKV_NVCC_EXTRA", "").split()  # experiment flags (e.g. -DRKV_QREG=0)
-        cmd = [_nvcc(), *ARCH, *NVCC_FLAGS, *extra, "-I", INCLUDE, "-c", os.path.join(CSRC, src), "-o", obj]
+        objs.append(obj)
+        if force or flags_changed or _stale(obj, [os.path.join(CSRC, src)] + hdrs):
+            cmd = [_nvcc(), *ARCH, *NVCC_FLAGS, *extra, "-I", INCLUDE, "-c", os.path.join(CSRC, src), "-o", obj]
+            if verbose:
+                cmd.insert(1, "-Xptxas=-v")
+            jobs.append(cmd)
+    if not jobs and not _stale(LIB, objs):
+        return LIB
+
+    def run(cmd):
         if verbose:
-            cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
-        objs.append(obj)
+
+    with ThreadPoolExecutor(max_workers=min(8, max(1, len(jobs)))) as ex:
+        list(ex.map(run, jobs))
+    with open(stamp, "w") as f:
+        f.write(flags)
     tmp = LIB + ".tmp"
     subprocess.run([_nvcc(), *ARCH, "-shared", "-o", tmp, *objs], check=True)
     os.replace(tmp, LIB)
-    for o in objs:
-        os.remove(o)
     return LIB
 
 

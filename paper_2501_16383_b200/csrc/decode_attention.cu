@@ -129,13 +129,15 @@ __global__ void __launch_bounds__(max_threads<N>(), 1) decode_split_kernel(Decod
     const int64_t t_begin = tb + static_cast<int64_t>(split) * p.chunk;
     const int64_t t_end = lmin(te, t_begin + p.chunk);
 
-    if (t_begin >= t_end) {  // empty split: neutral partials for every lane group
+    const bool bad_plan = !plan_matches(p.plan, kDecodeSimt, N, C);
+    if (t_begin >= t_end || bad_plan) {  // empty split: neutral partials for every lane group (NaN: foreign plan)
+        const float fill = bad_plan ? __int_as_float(0x7fc00000) : 0.0f;
         for (int i = tid; i < PP * Hq; i += NT) {
             const int64_t row = (static_cast<int64_t>(b) * p.NP + static_cast<int64_t>(split) * PP + i / Hq) * Hq + i % Hq;
-            p.ws_ml[row * 2] = -INFINITY;
-            p.ws_ml[row * 2 + 1] = 0.0f;
+            p.ws_ml[row * 2] = bad_plan ? fill : -INFINITY;
+            p.ws_ml[row * 2 + 1] = fill;
             float4* o = reinterpret_cast<float4*>(p.ws_o + row * 128);
-            for (int k = 0; k < 32; ++k) o[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int k = 0; k < 32; ++k) o[k] = make_float4(fill, fill, fill, fill);
         }
         return;
     }
@@ -643,23 +645,32 @@ __global__ void rope_table2_kernel(float4* table, int64_t npos, double base, int
                                   static_cast<float>(sn[1]));
 }
 
+constexpr int kRotRows = 8;  // rows per rotate_keys CTA
+
 template <int N, int L>
+// CTA = kRotRows rows x L lanes (one FWHT unit u = blockIdx.y of each row); rows
+// on grid.x (2^31 - 1 blocks), so calibration sets of any practical size
+// launch in one go.  The L lanes of a row sit in one warp: __syncwarp orders
+// the shared-memory transpose.
 __global__ void rotate_keys_kernel(const uint16_t* __restrict__ k, int64_t rows, int C, float norm, float* out) {
     constexpr int R = N / L, LR = ilog2(R), LN = ilog2(N), LL = ilog2(L);
-    const int64_t r = blockIdx.y;
-    const int u = blockIdx.x, lam = threadIdx.x;
-    const uint16_t* src = k + r * C + u * N;
-    __shared__ float buf[N];
+    const int rr = threadIdx.x / L, lam = threadIdx.x % L;
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * (blockDim.x / L) + rr;
+    const int u = blockIdx.y;
+    __shared__ float buf[kRotRows][N];
+    const bool ok = r < rows;
+    const uint16_t* src = k + (ok ? r : 0) * C + u * N;
     float2 x[R];
 #pragma unroll
-    for (int j = 0; j < R; ++j) x[j] = make_float2(h2f(src[lam * R + j]), 0.f);
+    for (int j = 0; j < R; ++j) x[j] = make_float2(ok ? h2f(src[lam * R + j]) : 0.f, 0.f);
     bfly_range<R, 0, LR>(x);
 #pragma unroll
-    for (int j = 0; j < R; ++j) buf[lam * R + j] = x[j].x;
-    __syncthreads();
+    for (int j = 0; j < R; ++j) buf[rr][lam * R + j] = x[j].x;
+    __syncwarp();
 #pragma unroll
-    for (int j = 0; j < R; ++j) x[j] = make_float2(buf[lam + L * j], 0.f);
+    for (int j = 0; j < R; ++j) x[j] = make_float2(buf[rr][lam + L * j], 0.f);
     bfly_range<R, LR - LL, LN - LL>(x);
+    if (!ok) return;
 #pragma unroll
     for (int j = 0; j < R; ++j) out[r * C + u * N + lam + L * j] = __fmul_rn(x[j].x, norm);
 }
@@ -683,7 +694,7 @@ __global__ void channel_stats_kernel(const float* __restrict__ x, int64_t rows, 
 template <int N, int REP>
 cudaError_t launch_decode_nr(const DecodePlan& plan, const DecodeParams& p, int B, cudaStream_t s) {
     auto kern = decode_split_kernel<N, REP>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(plan.smem));
+    cudaError_t e = ensure_smem_k(kern, plan.smem);
     if (e != cudaSuccess) return e;
     kern<<<dim3(plan.S, B), plan.NT, plan.smem, s>>>(p);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -704,21 +715,10 @@ cudaError_t launch_decode_combine(const DecodeParams& p, int B, cudaStream_t s) 
     return cudaGetLastError();
 }
 
-int num_sms() {
-    static int n = 0;
-    if (n == 0) {
-        int dev = 0;
-        if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-            n = 148;
-    }
-    return n;
-}
-
 template <int N, int REP>
 int occupancy_nr(const DecodePlan& pl) {
     int n = 0;
-    if (cudaFuncSetAttribute(decode_split_kernel<N, REP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(pl.smem)) != cudaSuccess ||
+    if (ensure_smem_k(decode_split_kernel<N, REP>, pl.smem) != cudaSuccess ||
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, decode_split_kernel<N, REP>, pl.NT, pl.smem) != cudaSuccess) {
         cudaGetLastError();
         const int by_smem = static_cast<int>((227u * 1024u) / (pl.smem + 1024));
@@ -764,8 +764,8 @@ DecodePlan plan_decode(const rkv_layer_desc& d, int64_t max_seq_len) {
     if (P > 4) P = 4;
     if (P < 1) P = 1;
     pl.stages = 3;
-    if (const char* e = std::getenv("RKV_DECODE_P")) P = std::max(1, std::min(P, std::atoi(e)));  // tuning knobs
-    if (const char* e = std::getenv("RKV_DECODE_STAGES")) pl.stages = std::max(2, std::min(kMaxStages, std::atoi(e)));
+    if (const int o = options().simt_p.load()) P = std::max(1, std::min(P, o));  // experiment switches
+    if (const int o = options().simt_stages.load()) pl.stages = std::max(2, std::min(kMaxStages, o));
     pl.P = P;
     pl.TT = 2 * P;
     pl.NT = NG * P * L;
@@ -829,11 +829,16 @@ cudaError_t launch_rope_table(const rkv_layer_desc& d, float4* table, int64_t ma
 cudaError_t launch_rotate_keys(const rkv_layer_desc& d, const uint16_t* k, int64_t rows, float* out, cudaStream_t s) {
     const int C = d.num_kv_heads * d.head_dim, N = d.heads_per_group * d.head_dim;
     const float norm = 1.0f / sqrtf(static_cast<float>(N));
-    dim3 grid(C / N, static_cast<unsigned>(rows));
+    if (rows <= 0) return cudaSuccess;
+    const int L = N == 128 ? 8 : 16;
+    const int64_t blocks = (rows + kRotRows - 1) / kRotRows;
+    if (blocks > 0x7fffffff) return cudaErrorInvalidValue;
+    const dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>(C / N));
+    const unsigned threads = static_cast<unsigned>(kRotRows * L);
     switch (N) {
-        case 128: rotate_keys_kernel<128, 8><<<grid, 8, 0, s>>>(k, rows, C, norm, out); break;
-        case 256: rotate_keys_kernel<256, 16><<<grid, 16, 0, s>>>(k, rows, C, norm, out); break;
-        case 512: rotate_keys_kernel<512, 16><<<grid, 16, 0, s>>>(k, rows, C, norm, out); break;
+        case 128: rotate_keys_kernel<128, 8><<<grid, threads, 0, s>>>(k, rows, C, norm, out); break;
+        case 256: rotate_keys_kernel<256, 16><<<grid, threads, 0, s>>>(k, rows, C, norm, out); break;
+        case 512: rotate_keys_kernel<512, 16><<<grid, threads, 0, s>>>(k, rows, C, norm, out); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

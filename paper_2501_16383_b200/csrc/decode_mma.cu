@@ -153,13 +153,15 @@ __global__ void __launch_bounds__(NGC < 0 ? kMmaMaxThreads : 320, NGC < 0 ? 1 : 
     const int64_t t_begin = tb + static_cast<int64_t>(split) * p.chunk;
     const int64_t t_end = lmin64(te, t_begin + p.chunk);
 
-    if (t_begin >= t_end) {  // empty split: neutral partials
+    const bool bad_plan = !plan_matches(p.plan, kDecodeMma, N, C);
+    if (t_begin >= t_end || bad_plan) {  // empty split: neutral partials (NaN: foreign plan)
+        const float fill = bad_plan ? __int_as_float(0x7fc00000) : 0.0f;
         for (int i = tid; i < Hq; i += NT) {
             const int64_t row = (static_cast<int64_t>(b) * p.NP + split) * Hq + i;
-            p.ws_ml[row * 2] = -INFINITY;
-            p.ws_ml[row * 2 + 1] = 0.0f;
+            p.ws_ml[row * 2] = bad_plan ? fill : -INFINITY;
+            p.ws_ml[row * 2 + 1] = fill;
             float4* o = reinterpret_cast<float4*>(p.ws_o + row * 128);
-            for (int k = 0; k < 32; ++k) o[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int k = 0; k < 32; ++k) o[k] = make_float4(fill, fill, fill, fill);
         }
         return;
     }
@@ -545,13 +547,15 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? 2 : 1) decode_gqa_kernel(Dec
     const int64_t t_begin = tb + static_cast<int64_t>(split) * p.chunk;
     const int64_t t_end = lmin64(te, t_begin + p.chunk);
 
-    if (t_begin >= t_end) {  // empty split: neutral partials
+    const bool bad_plan = !plan_matches(p.plan, kDecodeMma, N, C);
+    if (t_begin >= t_end || bad_plan) {  // empty split: neutral partials (NaN: foreign plan)
+        const float fill = bad_plan ? __int_as_float(0x7fc00000) : 0.0f;
         for (int i = tid; i < PW * Hq; i += NT) {
             const int64_t row = (static_cast<int64_t>(b) * p.NP + static_cast<int64_t>(split) * PW + i / Hq) * Hq + i % Hq;
-            p.ws_ml[row * 2] = -INFINITY;
-            p.ws_ml[row * 2 + 1] = 0.0f;
+            p.ws_ml[row * 2] = bad_plan ? fill : -INFINITY;
+            p.ws_ml[row * 2 + 1] = fill;
             float4* o = reinterpret_cast<float4*>(p.ws_o + row * 128);
-            for (int k = 0; k < 32; ++k) o[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int k = 0; k < 32; ++k) o[k] = make_float4(fill, fill, fill, fill);
         }
         return;
     }
@@ -977,15 +981,8 @@ MhaKernel mha_kernel_g(int NG, bool sp) {
 MhaKernel mha_kernel(int NG, int G, bool sp = false) {
     return G == 1 ? mha_kernel_g<1>(NG, sp) : G == 2 ? mha_kernel_g<2>(NG, sp) : mha_kernel_g<4>(NG, sp);
 }
-int gqa_pw() {
-    int pw = 2;
-    if (const char* e = std::getenv("RKV_GQA_PW")) pw = std::max(2, std::min(4, std::atoi(e)));
-    return pw;
-}
-bool gqa_tmem() {
-    const char* e = std::getenv("RKV_GQA_TMEM");
-    return !(e && std::atoi(e) == 0);
-}
+int gqa_pw() { return std::max(2, std::min(4, options().gqa_pw.load())); }
+bool gqa_tmem() { return options().gqa_tmem.load() != 0; }
 template <int PW>
 void* gqa_kernel_ptr() {
     return gqa_tmem() ? reinterpret_cast<void*>(decode_gqa_kernel<4, PW, true>)
@@ -1003,8 +1000,7 @@ void* gqa_kernel(int pw, bool sp = false) {
 
 int decode_kind(const rkv_layer_desc& d) {
     const int REP = d.num_q_heads / d.num_kv_heads;
-    if (const char* e = std::getenv("RKV_DECODE_KERNEL"))
-        if (std::strcmp(e, "simt") == 0) return kDecodeSimt;
+    if (options().force_simt.load()) return kDecodeSimt;
     if (d.head_dim != 128 || d.num_q_heads % d.num_kv_heads != 0) return kDecodeSimt;
     return decode_mma_supported(d.heads_per_group, REP, d.num_kv_heads * d.head_dim) ? kDecodeMma : kDecodeSimt;
 }
@@ -1032,8 +1028,7 @@ DecodePlan plan_decode_mma(const rkv_layer_desc& d, int64_t max_seq_len) {
     {
         int n = 0;
         const void* kern = gqa ? gqa_kernel(PW) : reinterpret_cast<const void*>(mha_kernel(NG, d.heads_per_group));
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pl.smem)) ==
-                cudaSuccess &&
+        if (ensure_smem(kern, pl.smem) == cudaSuccess &&
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, pl.NT, pl.smem) == cudaSuccess && n > 0)
             pl.per_sm = n;
         else
@@ -1055,8 +1050,8 @@ DecodePlan plan_decode_mma(const rkv_layer_desc& d, int64_t max_seq_len) {
         }
         if (best >= 0.95) break;
     }
-    if (const char* e = std::getenv("RKV_DEC_SPLITS"))  // experiment knob: splits per sequence
-        if (std::atoi(e) > 0) S = static_cast<int>(std::min<int64_t>(max_split, std::atoi(e)));
+    if (const int o = options().dec_splits.load())  // experiment switch: splits per sequence
+        if (o > 0) S = static_cast<int>(std::min<int64_t>(max_split, o));
     int64_t chunk = (max_seq_len + S - 1) / S;
     chunk = (chunk + pl.TT - 1) / pl.TT * pl.TT;
     pl.chunk = static_cast<int>(chunk);
@@ -1072,7 +1067,7 @@ cudaError_t launch_decode_mma(const rkv_layer_desc& d, const DecodePlan& plan, c
     if (plan.N == 256) {
         if (sp && plan.P != 2) return cudaErrorNotSupported;  // partials are instantiated for the default PW = 2
         const void* kern = gqa_kernel(plan.P, sp);
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(plan.smem));
+        cudaError_t e = ensure_smem(kern, plan.smem);
         if (e != cudaSuccess) return e;
         DecodeParams pp = p;
         void* args[] = {&pp};
@@ -1081,7 +1076,7 @@ cudaError_t launch_decode_mma(const rkv_layer_desc& d, const DecodePlan& plan, c
         return launch_decode_combine(p, d.batch, s);
     }
     auto kern = mha_kernel(p.C / 512, d.heads_per_group, sp);
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(plan.smem));
+    cudaError_t e = ensure_smem_k(kern, plan.smem);
     if (e != cudaSuccess) return e;
     kern<<<dim3(plan.S, d.batch), plan.NT, plan.smem, s>>>(p);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;

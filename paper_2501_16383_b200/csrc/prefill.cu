@@ -607,7 +607,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1) prefill_attn_kernel(PrefillPa
         umma::fence_before();
         mbar_arrive(q_tmem);
 
-        const uint32_t* smask = p.cache.sink_mask + static_cast<int64_t>(b) * ((p.max_tokens + 31) / 32);
+        const int64_t mask_words = (p.max_tokens + 31) / 32;
+        const uint32_t* smask = p.cache.sink_mask + static_cast<int64_t>(b) * mask_words;
         float m = -INFINITY, l = 0.f;
         for (int j = X; j < nt; j += 2) {
             mbar_wait(s_full + X, (j >> 1) & 1);
@@ -622,7 +623,9 @@ __global__ void __launch_bounds__(kAttnThreads, 1) prefill_attn_kernel(PrefillPa
 #pragma unroll
             for (int c = 0; c < 64; ++c) s[c] = __uint_as_float(v[c >> 4][c & 15]);
             const int64_t k0 = static_cast<int64_t>(j) * kPrefillKT;
-            const uint32_t sm0 = __ldg(smask + (k0 >> 5)), sm1 = __ldg(smask + (k0 >> 5) + 1);
+            // the second word exists only when the row has one past k0/32 (max_tokens > k0 + 32)
+            const uint32_t sm0 = __ldg(smask + (k0 >> 5));
+            const uint32_t sm1 = (k0 >> 5) + 1 < mask_words ? __ldg(smask + (k0 >> 5) + 1) : 0u;
             if (k0 + kPrefillKT - 1 > q0 || k0 + kPrefillKT > T || (sm0 | sm1)) {
                 const int64_t lim = lmin64(qpos + 1, T) - k0;  // keys k0 + c, c < lim, are in range
 #pragma unroll
@@ -810,10 +813,7 @@ namespace {
 // 2-SM mode (opt-in, RKV_PREFILL_PAIR=1): correct, but the per-tile cluster-scope hand-offs
 // (P rows of the upper CTA -> leader) cost ~2,000 cycles, more than the halved shared-memory
 // traffic saves
-bool prefill_pair() {
-    const char* e = std::getenv("RKV_PREFILL_PAIR");
-    return e && std::atoi(e) == 1;
-}
+bool prefill_pair() { return options().prefill_pair.load() == 1; }
 }  // namespace
 
 cudaError_t launch_prefill(const rkv_layer_desc& d, const PrefillParams& p, int64_t max_seq_len, cudaStream_t s) {
@@ -827,14 +827,10 @@ cudaError_t launch_prefill(const rkv_layer_desc& d, const PrefillParams& p, int6
         auto kern = d.heads_per_group == 1   ? reconstruct_keys_kernel<4, 1>
                     : d.heads_per_group == 2 ? reconstruct_keys_kernel<4, 2>
                                              : reconstruct_keys_kernel<4, 4>;
-        if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ksmem))) !=
-            cudaSuccess)
-            return e;
+        if ((e = ensure_smem_k(kern, ksmem)) != cudaSuccess) return e;
         kern<<<kgrid, nthreads, ksmem, s>>>(p);
     } else if (N == 256) {
-        if ((e = cudaFuncSetAttribute(reconstruct_keys_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(ksmem))) != cudaSuccess)
-            return e;
+        if ((e = ensure_smem_k(reconstruct_keys_kernel<2>, ksmem)) != cudaSuccess) return e;
         reconstruct_keys_kernel<2><<<kgrid, nthreads, ksmem, s>>>(p);
     } else {
         return cudaErrorInvalidValue;
@@ -851,9 +847,7 @@ cudaError_t launch_prefill(const rkv_layer_desc& d, const PrefillParams& p, int6
     const dim3 agrid(static_cast<unsigned>(p.num_q_pad / kQR), static_cast<unsigned>(p.Hq), static_cast<unsigned>(d.batch));
     if (prefill_pair()) {  // 2-SM clusters (num_q_pad is a multiple of 256)
         constexpr size_t sm = AttnSmem<true>::total;
-        if ((e = cudaFuncSetAttribute(prefill_attn_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(sm))) != cudaSuccess)
-            return e;
+        if ((e = ensure_smem_k(prefill_attn_kernel<true>, sm)) != cudaSuccess) return e;
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = agrid;
         cfg.blockDim = dim3(kAttnThreads);
@@ -869,9 +863,7 @@ cudaError_t launch_prefill(const rkv_layer_desc& d, const PrefillParams& p, int6
         return cudaLaunchKernelEx(&cfg, prefill_attn_kernel<true>, p);
     }
     constexpr size_t sm = AttnSmem<false>::total;
-    if ((e = cudaFuncSetAttribute(prefill_attn_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(sm))) != cudaSuccess)
-        return e;
+    if ((e = ensure_smem_k(prefill_attn_kernel<false>, sm)) != cudaSuccess) return e;
     prefill_attn_kernel<false><<<agrid, kAttnThreads, sm, s>>>(p);
     return cudaGetLastError();
 }

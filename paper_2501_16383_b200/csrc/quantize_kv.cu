@@ -280,10 +280,14 @@ __global__ void __launch_bounds__(256, 2) quantize_kv_kernel(QuantParams p, uint
         if (tid < 2) {
             int slot = -1;
             const int i = r.i0 + tid;
-            if (p.sink_flags && i < num_new && p.sink_flags[static_cast<int64_t>(r.b) * num_new + i]) {
+            const int64_t pos = p.start_pos[r.b] + i;
+            if (p.sink_flags && i < num_new && pos >= 0 && pos < p.max_tokens &&
+                p.sink_flags[static_cast<int64_t>(r.b) * num_new + i]) {
                 int before = 0;
                 for (int q = 0; q < i; ++q) before += p.sink_flags[static_cast<int64_t>(r.b) * num_new + q] ? 1 : 0;
                 slot = p.cache.sink_count[r.b] + before;
+                // a full sidecar keeps the token quantized (mask bit clear, not counted)
+                if (slot >= p.max_sinks) slot = -1;
             }
             s_slot[tid] = slot;
         }
@@ -319,9 +323,11 @@ __global__ void __launch_bounds__(256, 2) quantize_kv_kernel(QuantParams p, uint
             uint32_t* codes = r.isv ? p.cache.v_codes : p.cache.k_codes;
             uint32_t* meta = r.isv ? p.cache.v_meta : p.cache.k_meta;
             const int64_t row0 = static_cast<int64_t>(r.b) * p.max_tokens + p.start_pos[r.b] + r.i0;
+            const int64_t pos0 = p.start_pos[r.b] + r.i0;
 #pragma unroll
             for (int tok = 0; tok < 2; ++tok) {
                 if (tok == 1 && !r.has1) break;
+                if (pos0 + tok < 0 || pos0 + tok >= p.max_tokens) break;  // past the cache: never written
                 const bool sink = s_slot[tok] >= 0;
                 const int64_t rowi = row0 + tok;
                 *reinterpret_cast<uint2*>(codes + rowi * W + 2 * g) =
@@ -334,7 +340,7 @@ __global__ void __launch_bounds__(256, 2) quantize_kv_kernel(QuantParams p, uint
 #pragma unroll
         for (int tok = 0; tok < 2; ++tok) {
             const int slot = s_slot[tok];
-            if (slot < 0 || slot >= p.max_sinks) continue;
+            if (slot < 0) continue;  // slot < max_sinks by construction
             const uint4* srcr = reinterpret_cast<const uint4*>(
                 (r.isv ? p.v_new : p.k_new) + (static_cast<int64_t>(r.b) * p.num_new + r.i0 + tok) * C);
             uint16_t* side = r.isv ? p.cache.sink_v : p.cache.sink_k;
@@ -371,7 +377,68 @@ __global__ void quantize_sink_count_kernel(QuantParams p) {
     }
     if (local) atomicAdd(&s_count, local);
     __syncthreads();
-    if (threadIdx.x == 0 && s_count) p.cache.sink_count[b] += s_count;
+    // the main kernel gave sidecar slots to the first (max_sinks - count) of them only
+    if (threadIdx.x == 0 && s_count) {
+        const int c = p.cache.sink_count[b];
+        p.cache.sink_count[b] = c + min(s_count, max(0, p.max_sinks - c));
+    }
+}
+
+// promote_to_sink / route_sinks (proj/src/kv_cache.cpp:43-55,
+// proj/src/sink.cpp:47-63): one CTA per sequence.  Thread 0 walks the
+// sequence's token list in order (deterministic slots): tokens out of
+// [0, max_tokens), already sinks (the reference returns early: idempotent,
+// also for duplicates in the list) or past a full sidecar are skipped; the
+// others get the next sidecar slot, their mask bit and sink_pos.  Then the
+// CTA copies the raw fp16 rows into the sidecar and zeroes the token's packed
+// words and metadata (the reference clears its blocks).
+constexpr int kPromoteMax = 256;  // tokens per sequence and call
+__global__ void promote_sinks_kernel(QuantParams p, const int64_t* __restrict__ tokens, int n,
+                                     int32_t* __restrict__ promoted) {
+    __shared__ int s_slot[kPromoteMax];
+    __shared__ int64_t s_tok[kPromoteMax];
+    const int b = blockIdx.x, C = p.C, W = C / 16, MG = C / kQuantGroup;
+    const int64_t mwords = (p.max_tokens + 31) / 32;
+    uint32_t* mask = p.cache.sink_mask + static_cast<int64_t>(b) * mwords;
+    if (threadIdx.x == 0) {
+        int cnt = p.cache.sink_count[b], np = 0;  // np: promoted by this call
+        for (int i = 0; i < n; ++i) {
+            const int64_t t = tokens[static_cast<int64_t>(b) * n + i];
+            s_slot[i] = -1;
+            if (t < 0 || t >= p.max_tokens) continue;
+            const uint32_t bit = 1u << (t & 31);
+            if (mask[t >> 5] & bit) continue;  // already a sink
+            if (cnt >= p.max_sinks) continue;  // sidecar full: stays quantized
+            mask[t >> 5] |= bit;
+            p.cache.sink_pos[b * p.max_sinks + cnt] = static_cast<int32_t>(t);
+            s_slot[i] = cnt++;
+            s_tok[i] = t;
+            ++np;
+        }
+        p.cache.sink_count[b] = cnt;
+        if (promoted) promoted[b] = np;
+    }
+    __syncthreads();
+    for (int i = 0; i < n; ++i) {
+        const int slot = s_slot[i];
+        if (slot < 0) continue;
+        const int64_t t = s_tok[i];
+        const int64_t src = (static_cast<int64_t>(b) * n + i) * C;
+        const int64_t dst = (static_cast<int64_t>(b) * p.max_sinks + slot) * C;
+        for (int j = threadIdx.x; j < C; j += blockDim.x) {
+            p.cache.sink_k[dst + j] = p.k_new[src + j];
+            p.cache.sink_v[dst + j] = p.v_new[src + j];
+        }
+        const int64_t row = static_cast<int64_t>(b) * p.max_tokens + t;
+        for (int j = threadIdx.x; j < W; j += blockDim.x) {
+            p.cache.k_codes[row * W + j] = 0u;
+            p.cache.v_codes[row * W + j] = 0u;
+        }
+        for (int j = threadIdx.x; j < MG; j += blockDim.x) {
+            p.cache.k_meta[row * MG + j] = 0u;
+            p.cache.v_meta[row * MG + j] = 0u;
+        }
+    }
 }
 
 template <int N, int FMT>
@@ -383,8 +450,7 @@ cudaError_t launch_quantize_n(const QuantParams& p, int B, cudaStream_t s) {
     // the shared-memory limit is a per-kernel attribute: set it for THIS launch's
     // size every time (a layer of another width may have lowered it)
     {
-        const cudaError_t e = cudaFuncSetAttribute(quantize_kv_kernel<N, FMT>,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        const cudaError_t e = ensure_smem_k(quantize_kv_kernel<N, FMT>, smem);
         if (e != cudaSuccess) return e;
     }
     if (per_sm == 0) {
@@ -415,6 +481,14 @@ cudaError_t launch_quantize_fmt(const QuantParams& p, int B, cudaStream_t s) {
 }
 
 }  // namespace
+
+cudaError_t launch_promote_sinks(const rkv_layer_desc& d, const QuantParams& p, const int64_t* tokens, int n,
+                                 int32_t* promoted, cudaStream_t s) {
+    if (n < 1 || n > kPromoteMax) return cudaErrorInvalidValue;
+    promote_sinks_kernel<<<d.batch, 256, 0, s>>>(p, tokens, n, promoted);
+    return cudaGetLastError();
+}
+int promote_sinks_max() { return kPromoteMax; }
 
 cudaError_t launch_quantize(const rkv_layer_desc& d, const QuantParams& p, cudaStream_t s) {
     const int n = d.heads_per_group * d.head_dim;

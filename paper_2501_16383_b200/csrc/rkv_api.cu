@@ -308,6 +308,32 @@ rkv_status rkv_quantize_kv(const rkv_layer_desc* desc, const uint16_t* k_new, co
     return RKV_OK;
 }
 
+rkv_status rkv_promote_sinks(const rkv_layer_desc* desc, const rkv_cache* cache, const int64_t* tokens,
+                             int64_t num_tokens, const uint16_t* k_rows, const uint16_t* v_rows, int32_t* promoted,
+                             void* stream) {
+    rkv_status st = validate(desc);
+    if (st != RKV_OK) return st;
+    if ((st = check_cache(cache)) != RKV_OK) return st;
+    if (num_tokens < 0) return fail(RKV_ERR_INVALID_ARGUMENT, "promote_sinks: num_tokens must be >= 0");
+    if (num_tokens == 0) return RKV_OK;
+    if (num_tokens > rkv::promote_sinks_max())
+        return fail(RKV_ERR_INVALID_ARGUMENT, "promote_sinks: at most 256 tokens per sequence and call");
+    if (!tokens || !k_rows || !v_rows) return fail(RKV_ERR_INVALID_ARGUMENT, "promote_sinks: null argument");
+    if (!cache->sink_k || !cache->sink_v || !cache->sink_pos)
+        return fail(RKV_ERR_INVALID_ARGUMENT, "promote_sinks: the cache has no sidecar arrays");
+    rkv::QuantParams p{};
+    p.k_new = k_rows;
+    p.v_new = v_rows;
+    p.max_tokens = desc->max_tokens;
+    p.C = desc->num_kv_heads * desc->head_dim;
+    p.max_sinks = desc->max_sinks;
+    p.cache = *cache;
+    cudaError_t e = rkv::launch_promote_sinks(*desc, p, tokens, static_cast<int>(num_tokens), promoted,
+                                              static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "promote_sinks");
+    return RKV_OK;
+}
+
 size_t rkv_layer_plan_bytes(const rkv_layer_desc* desc) {
     if (validate(desc) != RKV_OK) return 0;
     const int W = desc->num_kv_heads * desc->head_dim / 16;
@@ -385,7 +411,7 @@ rkv::DecodeParams decode_params(const rkv_layer_desc* desc, const rkv::DecodePla
 
 size_t rkv_decode_workspace_bytes(const rkv_layer_desc* desc, int64_t max_seq_len) {
     if (validate(desc) != RKV_OK) return 0;
-    rkv::DecodePlan pl = rkv::plan_decode(*desc, max_seq_len);
+    const rkv::DecodePlan& pl = rkv::cached_plan(*desc, max_seq_len);
     const size_t rows = static_cast<size_t>(desc->batch) * pl.NP * desc->num_q_heads;
     return al256(rows * 2 * sizeof(float)) + al256(rows * 128 * sizeof(float));
 }
@@ -404,7 +430,7 @@ rkv_status rkv_decode_attention(const rkv_layer_desc* desc, const uint16_t* q, c
     if (max_seq_len == 0) max_seq_len = desc->max_tokens;
     if (ws_bytes < rkv_decode_workspace_bytes(desc, max_seq_len))
         return fail(RKV_ERR_INVALID_ARGUMENT, "decode_attention: workspace too small");
-    rkv::DecodePlan pl = rkv::plan_decode(*desc, max_seq_len);
+    const rkv::DecodePlan& pl = rkv::cached_plan(*desc, max_seq_len);
     if (!pl.ok)
         return fail(RKV_ERR_INVALID_ARGUMENT, "decode_attention: layer shape exceeds the sm_100a kernel's tile budget");
     rkv::DecodeParams p = decode_params(desc, pl, q, seq_len, cache, layer_plan, rope_table, out, workspace);
@@ -427,7 +453,7 @@ rkv_status rkv_decode_attention_partial(const rkv_layer_desc* desc, const uint16
         return fail(RKV_ERR_OUT_OF_RANGE, "decode_attention_partial: max_span must be in [1, max_tokens]");
     if (ws_bytes < rkv_decode_workspace_bytes(desc, max_span))
         return fail(RKV_ERR_INVALID_ARGUMENT, "decode_attention_partial: workspace too small");
-    rkv::DecodePlan pl = rkv::plan_decode(*desc, max_span);
+    const rkv::DecodePlan& pl = rkv::cached_plan(*desc, max_span);
     if (!pl.ok)
         return fail(RKV_ERR_INVALID_ARGUMENT, "decode_attention_partial: layer shape exceeds the kernel's tile budget");
     rkv::DecodeParams p = decode_params(desc, pl, q, seq_len, cache, layer_plan, rope_table, part_o, workspace);

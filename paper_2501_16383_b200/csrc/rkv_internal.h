@@ -3,12 +3,34 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <vector>
 
 #include "rotatekv/rotatekv.h"
 
 namespace rkv {
+
+// Experiment switches (rkv_set_debug_option, rkv_runtime.cu).  Defaults are the
+// production choices; the epoch bumps on every change so cached plans rebuild.
+struct Options {
+    std::atomic<int> force_simt{0};    // decode on the CUDA-core kernel for tensor-core shapes
+    std::atomic<int> gqa_pw{2};        // GQA kernel: warps per FWHT group (2..4)
+    std::atomic<int> gqa_tmem{1};      // GQA kernel: park accumulators in tensor memory
+    std::atomic<int> dec_splits{0};    // > 0: force the split count per sequence
+    std::atomic<int> prefill_pair{0};  // 2-SM (cta_group::2) prefill attention
+    std::atomic<int> simt_p{0};        // CUDA-core kernel: token pairs per tile (0 = planner)
+    std::atomic<int> simt_stages{0};   // CUDA-core kernel: TMA ring depth (0 = planner)
+    std::atomic<int> epoch{0};
+};
+Options& options();
+int current_device();
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device, high-water mark)
+cudaError_t ensure_smem(const void* kern, size_t bytes);
+template <typename K>
+inline cudaError_t ensure_smem_k(K* kern, size_t bytes) {
+    return ensure_smem(reinterpret_cast<const void*>(kern), bytes);
+}
 
 constexpr float kLog2eHost = 1.4426950408889634f;
 
@@ -84,6 +106,9 @@ struct PrefillParams {
 
 // quantize_kv.cu
 cudaError_t launch_quantize(const rkv_layer_desc& d, const QuantParams& p, cudaStream_t s);
+cudaError_t launch_promote_sinks(const rkv_layer_desc& d, const QuantParams& p, const int64_t* tokens, int n,
+                                 int32_t* promoted, cudaStream_t s);
+int promote_sinks_max();
 // decode_attention.cu
 struct DecodePlan {
     int kind, N, REP, P, PP, TT, NT, S, NP, chunk, stages, per_sm;
@@ -92,6 +117,7 @@ struct DecodePlan {
 };
 bool decode_supported(int N, int REP);
 DecodePlan plan_decode(const rkv_layer_desc& d, int64_t max_seq_len);
+const DecodePlan& cached_plan(const rkv_layer_desc& d, int64_t max_seq_len);  // memoised plan_decode
 cudaError_t launch_decode(const rkv_layer_desc& d, const DecodePlan& plan, const DecodeParams& p,
                           cudaStream_t s);
 cudaError_t launch_decode_combine(const DecodeParams& p, int B, cudaStream_t s);

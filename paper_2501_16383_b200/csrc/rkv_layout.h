@@ -83,4 +83,12 @@ enum { kDecodeSimt = 0, kDecodeMma = 1 };
 
 RKV_HD inline int plan_words(int W) { return kPlanHeader + W + 16 * W; }
 
+// Header check in the decode kernels' prologue: a plan built for another layer
+// shape or kernel kind makes the decode emit NaN (loud) instead of attention
+// computed with the wrong scatter offsets or RoPE layout.
+RKV_HD inline bool plan_matches(const uint32_t* plan, int kind, int N, int C) {
+    return plan[PH_MAGIC] == kPlanMagic && plan[PH_KIND] == static_cast<uint32_t>(kind) &&
+           plan[PH_N] == static_cast<uint32_t>(N) && plan[PH_C] == static_cast<uint32_t>(C);
+}
+
 }  // namespace rkv

@@ -1,0 +1,102 @@
+// rkv_runtime.cu -- host-side runtime state shared by the launchers.
+//
+//  * options(): the experiment switches (kernel selection, split counts, the
+//    2-SM prefill).  They used to be getenv() calls on every launch; now they
+//    are process-global atomics set through rkv_set_debug_option and read
+//    when a plan is built.  Every layer plan records the kernel kind it was
+//    built for and the decode kernels check it, so a plan built under other
+//    switches yields NaN outputs instead of silently wrong attention.
+//  * ensure_smem(): cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per
+//    (kernel, device, size high-water mark) instead of on every launch.
+//  * cached_plan(): decode plans memoised per (descriptor, max_seq_len,
+//    device, option epoch) -- the planner runs occupancy queries.
+#include <atomic>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "rkv_internal.h"
+
+namespace rkv {
+
+Options& options() {
+    static Options o;
+    return o;
+}
+
+int current_device() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        dev = 0;
+    }
+    return dev;
+}
+
+int num_sms() {
+    static std::atomic<int> cache[64];
+    const int dev = current_device();
+    const int slot = dev & 63;
+    int n = cache[slot].load(std::memory_order_relaxed);
+    if (n == 0) {
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
+            cudaGetLastError();
+            n = 148;
+        }
+        cache[slot].store(n, std::memory_order_relaxed);
+    }
+    return n;
+}
+
+cudaError_t ensure_smem(const void* kern, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> set;
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& have = set[{kern, dev}];
+    if (have >= bytes && have != 0) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+    if (e == cudaSuccess) have = bytes;
+    return e;
+}
+
+const DecodePlan& cached_plan(const rkv_layer_desc& d, int64_t max_seq_len) {
+    static std::mutex mu;
+    using Key = std::tuple<std::string, int64_t, int, int>;
+    static std::map<Key, DecodePlan> plans;
+    if (max_seq_len <= 0 || max_seq_len > d.max_tokens) max_seq_len = d.max_tokens;
+    Key key{std::string(reinterpret_cast<const char*>(&d), sizeof(d)), max_seq_len, current_device(),
+            options().epoch.load()};
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = plans.find(key);
+        if (it != plans.end()) return it->second;
+    }
+    DecodePlan pl = plan_decode(d, max_seq_len);  // outside the lock: occupancy queries
+    std::lock_guard<std::mutex> lk(mu);
+    if (plans.size() > 4096) plans.clear();  // bounded (a serving process sees few shapes)
+    return plans.emplace(key, pl).first->second;
+}
+
+}  // namespace rkv
+
+extern "C" rkv_status rkv_set_debug_option(const char* name, int64_t value) {
+    rkv::Options& o = rkv::options();
+    if (!name) return RKV_ERR_INVALID_ARGUMENT;
+    const std::string n(name);
+    std::atomic<int>* slot = nullptr;
+    if (n == "decode_kernel_simt") slot = &o.force_simt;
+    else if (n == "gqa_warps_per_group") slot = &o.gqa_pw;
+    else if (n == "gqa_tmem") slot = &o.gqa_tmem;
+    else if (n == "decode_splits") slot = &o.dec_splits;
+    else if (n == "prefill_pair") slot = &o.prefill_pair;
+    else if (n == "simt_pairs") slot = &o.simt_p;
+    else if (n == "simt_stages") slot = &o.simt_stages;
+    if (!slot) return RKV_ERR_INVALID_ARGUMENT;
+    slot->store(static_cast<int>(value));
+    o.epoch.fetch_add(1);
+    return RKV_OK;
+}

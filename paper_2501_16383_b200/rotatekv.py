@@ -108,7 +108,9 @@ def lib():
         L.rkv_calibrate_workspace_bytes.restype = C.c_size_t
         L.rkv_calibrate_workspace_bytes.argtypes = [D, C.c_int64]
         L.rkv_calibrate_reorder_device.argtypes = [D, P, C.c_int64, C.c_int32, P, C.c_size_t, P, P, P]
-        for name in ("rkv_layer_validate", "rkv_cache_carve", "rkv_cache_reset", "rkv_rope_table_init",
+        L.rkv_promote_sinks.argtypes = [D, C.POINTER(CacheView), P, C.c_int64, P, P, P, P]
+        L.rkv_set_debug_option.argtypes = [C.c_char_p, C.c_int64]
+        for name in ("rkv_promote_sinks", "rkv_set_debug_option", "rkv_layer_validate", "rkv_cache_carve", "rkv_cache_reset", "rkv_rope_table_init",
                      "rkv_quantize_kv", "rkv_decode_attention", "rkv_rotate_keys", "rkv_calibrate_reorder",
                      "rkv_detect_sinks", "rkv_detect_sinks_device", "rkv_layer_plan_build", "rkv_layer_plan_init",
                      "rkv_calibrate_reorder_device", "rkv_cache_export", "rkv_cache_import",
@@ -167,6 +169,12 @@ class LayerConfig:
 
 
 # ------------------------------------------------------------ host helpers
+
+def set_debug_option(name: str, value: int) -> None:
+    """Process-global experiment switch (rkv_set_debug_option): kernel
+    selection etc.  Build layers (plan + RoPE table) after changing one."""
+    _check(lib().rkv_set_debug_option(name.encode(), int(value)))
+
 
 WIRE_REFERENCE, WIRE_FP16_SCALE = 0, 1
 
@@ -281,6 +289,7 @@ class RotateKVLayer:
                                          self._stream_or_none(stream)))
         self.lengths = np.zeros(cfg.batch, np.int64)
         self.sink_counts = np.zeros(cfg.batch, np.int64)
+        self.sink_tokens = [set() for _ in range(cfg.batch)]  # host mirror of the sink masks
         self._ws = None
         self._ws_for = None
         self.stream = stream
@@ -300,6 +309,7 @@ class RotateKVLayer:
         _check(lib().rkv_cache_reset(C.byref(self._desc), C.byref(self._view), self._stream()))
         self.lengths[:] = 0
         self.sink_counts[:] = 0
+        self.sink_tokens = [set() for _ in range(self.cfg.batch)]
 
     def _arr(self, name, dtype, shape):
         """A torch view of one carved cache array."""
@@ -379,7 +389,58 @@ class RotateKVLayer:
                                       self._stream()))
         self.lengths[seq] = n.value
         self.sink_counts[seq] = int(self.arrays()["sink_count"][seq].item())
+        cnt = int(self.sink_counts[seq])
+        self.sink_tokens[seq] = set(int(t) for t in self.arrays()["sink_pos"][seq, :cnt].cpu().numpy())
         return n.value
+
+    # -- LayerKVCache::promote_to_sink / route_sinks (proj/src/kv_cache.cpp:43-55, proj/src/sink.cpp:47-63)
+    def promote_sinks(self, tokens, k_rows, v_rows):
+        """route_sinks for every sequence: tokens = per-sequence lists of token
+        indices (or a [B, n] int array, -1 = no entry); k_rows/v_rows = [B, n, C]
+        fp16 CUDA tensors holding those tokens' raw (pre-rotation, pre-RoPE)
+        rows.  Tokens already sinks are skipped (idempotent).  Out-of-range
+        tokens raise IndexError like the reference; a full sidecar raises
+        IndexError before anything is changed."""
+        torch = self.torch
+        B, Cc = self.cfg.batch, self.cfg.channels
+        if isinstance(tokens, np.ndarray) and tokens.ndim == 2:
+            tok = _np(tokens, np.int64)
+        else:
+            lists = [list(t) for t in tokens]
+            if len(lists) != B:
+                raise ValueError("route_sinks: one token list per sequence")
+            n = max([len(t) for t in lists] + [1])
+            tok = np.full((B, n), -1, np.int64)
+            for b, t in enumerate(lists):
+                tok[b, :len(t)] = t
+        n = tok.shape[1]
+        if tok.shape[0] != B:
+            raise ValueError("route_sinks: one token list per sequence")
+        if k_rows.dtype != torch.float16 or v_rows.dtype != torch.float16 or tuple(k_rows.shape) != (B, n, Cc) \
+                or tuple(v_rows.shape) != (B, n, Cc):
+            raise ValueError("route_sinks: k_rows/v_rows must be matching [tokens, channels]")
+        new = []
+        for b in range(B):
+            fresh = []
+            for t in tok[b]:
+                if t == -1:
+                    continue
+                if t < 0 or t >= self.lengths[b]:
+                    raise IndexError("route_sinks: token index out of range")
+                if int(t) not in self.sink_tokens[b] and int(t) not in fresh:
+                    fresh.append(int(t))
+            if self.sink_counts[b] + len(fresh) > self.cfg.max_sinks:
+                raise IndexError("cache: sink sidecar capacity exceeded")
+            new.append(fresh)
+        tok_t = torch.from_numpy(tok).to(self.device)
+        k_rows, v_rows = k_rows.contiguous(), v_rows.contiguous()
+        _check(lib().rkv_promote_sinks(C.byref(self._desc), C.byref(self._view), _ptr(tok_t), n, _ptr(k_rows),
+                                       _ptr(v_rows), None, self._stream()))
+        for b in range(B):
+            self.sink_tokens[b].update(new[b])
+            self.sink_counts[b] += len(new[b])
+        self._keep_promote = (tok_t, k_rows, v_rows)
+        return [len(x) for x in new]
 
     # -- LayerKVCache::append (proj/src/kv_cache.cpp:8-22), batched
     def append(self, k, v, sink_flags=None, start_pos=None):
@@ -405,6 +466,9 @@ class RotateKVLayer:
             if np.any(self.sink_counts + add > self.cfg.max_sinks):
                 raise IndexError("cache: sink sidecar capacity exceeded")
             self.sink_counts += add
+            fh = f.cpu().numpy()
+            for b in range(B):
+                self.sink_tokens[b].update(int(start[b]) + np.nonzero(fh[b])[0])
             flags_t = f.to(self.device).contiguous()
         k = k.contiguous()
         v = v.contiguous()
@@ -496,7 +560,14 @@ class RotateKVLayer:
         return out
 
     def append_device(self, k, v, start_t, sink_flags_t=None):
-        """Allocation-free append with device-resident start positions."""
+        """Allocation-free append with device-resident start positions (no
+        host mirror update).  Positions past max_tokens are never written (the
+        kernel skips them; the device cannot raise)."""
+        B, Cc = self.cfg.batch, self.cfg.channels
+        if k.dim() != 3 or tuple(k.shape[::2]) != (B, Cc) or v.shape != k.shape:
+            raise ValueError("cache append: row length must equal channel count")
+        if k.shape[1] > self.cfg.max_tokens or tuple(start_t.shape) != (B,):
+            raise IndexError("cache: token index out of range")
         _check(lib().rkv_quantize_kv(C.byref(self._desc), _ptr(k), _ptr(v), _ptr(self.perm), _ptr(sink_flags_t),
                                      _ptr(start_t), k.shape[1], C.byref(self._view), self._stream()))
 

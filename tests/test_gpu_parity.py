@@ -381,14 +381,31 @@ def test_cpp_api_program(tmp_path):
     assert r.returncode == 0, r.stdout + r.stderr
 
 
-@pytest.mark.parametrize("env,hq,hkv,g", [("RKV_GQA_TMEM=0", 32, 8, 2), ("RKV_DECODE_KERNEL=simt", 8, 8, 4),
-                                          ("RKV_DECODE_KERNEL=simt", 32, 8, 2)])
-def test_alternative_decode_kernels(oracle, monkeypatch, env, hq, hkv, g):
-    """The env-selectable kernels (register-resident GQA, the CUDA-core kernel
-    on tensor-core shapes) stay parity-green.  The layer (plan and RoPE table
-    layout) is built under the same selection."""
-    k_, v_ = env.split("=")
-    monkeypatch.setenv(k_, v_)
+@pytest.fixture
+def debug_option():
+    """Set an experiment switch for one test and restore the default after."""
+    import paper_2501_16383_b200 as P
+
+    defaults = {"gqa_tmem": 1, "decode_kernel_simt": 0, "prefill_pair": 0, "decode_splits": 0}
+    touched = []
+
+    def set_(name, value):
+        touched.append(name)
+        P.set_debug_option(name, value)
+
+    yield set_
+    for name in touched:
+        P.set_debug_option(name, defaults[name])
+
+
+@pytest.mark.parametrize("opt,hq,hkv,g", [("gqa_tmem=0", 32, 8, 2), ("decode_kernel_simt=1", 8, 8, 4),
+                                          ("decode_kernel_simt=1", 32, 8, 2)])
+def test_alternative_decode_kernels(oracle, debug_option, opt, hq, hkv, g):
+    """The switch-selectable kernels (register-resident GQA, the CUDA-core
+    kernel on tensor-core shapes) stay parity-green.  The layer (plan and RoPE
+    table layout) is built under the same selection."""
+    k_, v_ = opt.split("=")
+    debug_option(k_, int(v_))
     w = small_workload(hq, hkv, g)
     B, T = 2, 150
     layer, perm = build_layer(w, B, T + 8, seed=77)

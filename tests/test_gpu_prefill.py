@@ -201,10 +201,19 @@ def test_prefill_full_size_rows_match_decode(oracle, cfg_id, B):
 
 @pytest.mark.parametrize("hq,hkv,g,T,sinks,seed", [(8, 8, 4, 300, (0, 41), 21), (32, 8, 2, 200, (0,), 22),
                                                    (8, 8, 1, 129, (0, 128), 23)])
-def test_prefill_two_sm_pairs_match_oracle(oracle, monkeypatch, hq, hkv, g, T, sinks, seed):
+def test_prefill_two_sm_pairs_match_oracle(oracle, hq, hkv, g, T, sinks, seed):
     """The opt-in 2-SM mode (cta_group::2 MMAs over CTA pairs, 256 query rows,
     each CTA holding half of every K/V tile) against the oracle."""
-    monkeypatch.setenv("RKV_PREFILL_PAIR", "1")
+    import paper_2501_16383_b200 as P
+
+    P.set_debug_option("prefill_pair", 1)
+    try:
+        _two_sm_case(oracle, hq, hkv, g, T, sinks, seed)
+    finally:
+        P.set_debug_option("prefill_pair", 0)
+
+
+def _two_sm_case(oracle, hq, hkv, g, T, sinks, seed):
     layer, k, v, flags, q, perm = build(hq, hkv, g, T, sinks, seed)
     out = layer.prefill_attention(q, q_start=np.zeros(2, np.int64)).cpu().numpy()
     rows = list(range(0, T, 5)) + [T - 1]

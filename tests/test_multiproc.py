@@ -152,3 +152,23 @@ def test_two_rank_sequence_parallel_fold_matches_single_process():
         mm, ll, oo = results[r]
         assert mm == m
         np.testing.assert_allclose(oo / ll, want, rtol=1e-12, atol=1e-12)
+
+
+def test_bench_spawns_ranks_dry_run():
+    """`bench.py --gpus 2` launches the two ranks itself (no torchrun) and rank
+    0 prints one JSON line with n_gpus = 2 (gloo rendezvous on 127.0.0.1)."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "LOCAL_RANK", "WORLD_SIZE")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-run", "--steps", "2",
+                        "--warmup", "3"], capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stderr
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["dry_run"] is True
+    assert d["max_rank_seen"] == 1.0  # the MAX reduction saw rank 1
+    assert d["config"]["batch_per_gpu"] == 4
