@@ -488,11 +488,13 @@ __global__ void __launch_bounds__(256) decode_combine_kernel(DecodeParams p, int
     }
     float M = -INFINITY, L = 0.f;
     float4 rot = make_float4(0.f, 0.f, 0.f, 0.f);
+    bool poisoned = false;  // a partial's m is NaN: the decode kernel rejected the layer plan
     for (int s0 = s_begin; s0 < s_end; s0 += 32) {
         const int s = s0 + lane;
         const int64_t r = base + static_cast<int64_t>(s) * p.Hq + h;
         const float ms = s < s_end ? p.ws_ml[r * 2] : -INFINITY;
         const float ls = s < s_end ? p.ws_ml[r * 2 + 1] : 0.f;
+        poisoned |= __any_sync(0xffffffffu, ms != ms);
         float mx = ms;
 #pragma unroll
         for (int o = 16; o >= 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -518,6 +520,10 @@ __global__ void __launch_bounds__(256) decode_combine_kernel(DecodeParams p, int
             const float wk = __shfl_sync(0xffffffffu, w, k);  // 0 past n (ms = -inf)
             rot = make_float4(rot.x + wk * ov[k].x, rot.y + wk * ov[k].y, rot.z + wk * ov[k].z, rot.w + wk * ov[k].w);
         }
+    }
+    if (poisoned) {  // keep the NaN visible through the fold and the normalisation
+        M = 0.f;
+        L = __int_as_float(0x7fc00000);
     }
     if (nw > 1) {  // fold the warps' (M, L, rot) in warp order
         __shared__ float4 s_rot[8][32];
@@ -603,7 +609,7 @@ __global__ void __launch_bounds__(256) decode_combine_kernel(DecodeParams p, int
             x[j] = upper ? y - x[j] : x[j] + y;
         }
     }
-    const float inv = L > 0.f ? 1.0f / L : 0.f, nrm = 1.0f / sqrtf(128.0f);
+    const float inv = (L > 0.f || L != L) ? 1.0f / L : 0.f, nrm = 1.0f / sqrtf(128.0f);  // NaN L: foreign plan
     reinterpret_cast<float4*>(p.out + (static_cast<int64_t>(b) * p.Hq + h) * 128)[lane] =
         make_float4((x[0] * nrm + raw.x) * inv, (x[1] * nrm + raw.y) * inv, (x[2] * nrm + raw.z) * inv,
                     (x[3] * nrm + raw.w) * inv);

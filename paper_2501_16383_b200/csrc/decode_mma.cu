@@ -330,7 +330,11 @@ __global__ void __launch_bounds__(NGC < 0 ? kMmaMaxThreads : 320, NGC < 0 ? 1 : 
 #pragma unroll
             for (int tk = 0; tk < 2; ++tk) {
                 // Y = H_16(F1) X in fp32; B fragments of the second MMA: hi = fp16(Y)
-                // and the residual lo = fp16(Y - hi) (one FHADD per element)
+                // and the residual lo = fp16(Y - hi) (one FHADD per element).
+                // (The tensor core can produce the split itself -- fp16
+                // accumulator, C = -hi, exact: tools/mb_f16acc.cu -- but the
+                // extra MMA per instance and the register-pair MOVs it needs
+                // made the kernel slower: 247 vs 242 us at config 2.)
                 float yf[NJ][4];
                 const float zero[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll

@@ -81,6 +81,23 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], 
           "f"(c[3]));
 }
 
+// D = RN16(A(16x16) * B(16x8) + C), fp16 accumulator.  The tensor core adds
+// the exact products and C and rounds once (tools/mb_f16acc.cu: 8.4 M
+// dequantised-K-like H_16 products, every result == RN16 of the exact sum),
+// so with C = 0 it yields hi = RN16(Y) and with A = -H, C = hi the residual
+// -(Y - hi) rounded once: the fp16 hi/lo split of Y without F2FP/FHADD.
+__device__ __forceinline__ void mma16816h(uint32_t (&d)[2], const uint32_t (&a)[4], uint32_t b0, uint32_t b1,
+                                          uint32_t c0, uint32_t c1) {
+    asm("mma.sync.aligned.m16n8k16.row.col.f16.f16.f16.f16 {%0,%1}, {%2,%3,%4,%5}, {%6,%7}, {%8,%9};"
+        : "=r"(d[0]), "=r"(d[1])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "r"(c0), "r"(c1));
+}
+// the same fragment negated (sign bit of every fp16 entry; 0 -> -0 is harmless)
+__device__ __forceinline__ void negate_frag(uint32_t (&dst)[4], const uint32_t (&src)[4]) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) dst[r] = src[r] ^ 0x80008000u;
+}
+
 __device__ __forceinline__ void mma1688(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t b) {
     asm("mma.sync.aligned.m16n8k8.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
         : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])

@@ -79,8 +79,8 @@ def test_promote_batched_vs_oracle_and_idempotent(oracle):
     assert layer.promote_sinks(toks, _rows(k, [t + [0] * (4 - len(t)) for t in toks]),
                                _rows(v, [t + [0] * (4 - len(t)) for t in toks])) == [0, 0, 0]
     after = cache_host(layer)
-    for name in before:
-        assert np.array_equal(before[name], after[name]), name
+    for name in before:  # bit patterns: unused sidecar slots may hold NaN garbage
+        assert np.array_equal(before[name].view(np.uint8), after[name].view(np.uint8)), name
 
 
 def test_promote_errors_and_device_guards():

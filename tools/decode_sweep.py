@@ -3,7 +3,7 @@ development tool next to bench.py): fills a seeded 2-bit cache per config and
 times rkv_decode_attention alone with CUDA events.
 
     python tools/decode_sweep.py [cfg ...]      (default: 2 3 4; "2g1" = config 2 with G = 1)
-    RKV_DECODE_KERNEL=simt python tools/decode_sweep.py   # the CUDA-core kernel
+    RKV_DECODE_KERNEL=simt python tools/decode_sweep.py   # the CUDA-core kernel (debug option)
 
 cfg 4 (8 x 32768 tokens) is timed at full size; cfg 3 at batch 64 x 8192.
 """
@@ -64,6 +64,8 @@ def run(cfg_id, iters=20, g=None):
 
 
 if __name__ == "__main__":
+    if os.environ.get("RKV_DECODE_KERNEL") == "simt":
+        P.set_debug_option("decode_kernel_simt", 1)
     # "2" = config 2; "2g1" = config 2's shape with G = 1
     ids = sys.argv[1:] or ["2", "3", "4"]
     for a in ids:
