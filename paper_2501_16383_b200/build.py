@@ -18,7 +18,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "librotatekv_b200.so")
 INCLUDE = os.path.join(ROOT, "include")
-SOURCES = ["rkv_api.cu", "rkv_runtime.cu", "rkv_plan.cu", "quantize_kv.cu", "decode_attention.cu", "decode_mma.cu", "prefill.cu", "sink_detect.cu"]
+SOURCES = ["rkv_api.cu", "rkv_runtime.cu", "rkv_plan.cu", "quantize_kv.cu", "generic.cu", "decode_attention.cu", "decode_mma.cu", "prefill.cu", "sink_detect.cu"]
 HEADERS = ["rkv_common.cuh", "rkv_internal.h", "rkv_layout.h", "rkv_mma.cuh", "rkv_umma.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",

@@ -52,11 +52,6 @@ __device__ __forceinline__ float2 lds64(const unsigned char* p) { return *reinte
 // RoPE table rows are per position pair, 128 float4 (2 KB): [0, 64) section 1
 // (cos p0, cos p1, sin p0, sin p1) per frequency; [64, 128) section 2 (one
 // 32-float4 frequency-pair row per position, tensor-core decode).
-constexpr int kRopeRow = 128;
-__device__ __forceinline__ float2 rope_at(const float4* t, int64_t pos, int f) {
-    const float4 r = __ldg(t + (pos >> 1) * kRopeRow + f);
-    return (pos & 1) ? make_float2(r.y, r.w) : make_float2(r.x, r.z);
-}
 __device__ __forceinline__ void sts64(uint32_t addr, float2 v) {
     asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(v.x), "f"(v.y) : "memory");
 }
@@ -756,8 +751,24 @@ bool decode_supported(int N, int REP) {
     }
 }
 
+// The CUDA-core split kernel's shape limits (plan_decode below, without the
+// occupancy query): rotation size 128/256/512, its head ratios, C % 512 == 0
+// and a thread count that tiles the packed words.
+bool simt_shape_ok(const rkv_layer_desc& d) {
+    const int C = d.num_kv_heads * d.head_dim, N = d.heads_per_group * d.head_dim;
+    if (d.head_dim != 128 || C % 512 != 0 || (N != 128 && N != 256 && N != 512)) return false;
+    if (d.num_q_heads % d.num_kv_heads != 0 || !decode_supported(N, d.num_q_heads / d.num_kv_heads)) return false;
+    const int L = N >= 256 ? 16 : 8, NG = C / N, max_nt = N == 512 ? 320 : 256, W = C / 16;
+    const int P = std::max(1, std::min(4, max_nt / (NG * L)));
+    const int NT = NG * P * L;
+    if (NT > max_nt || !(NT % W == 0 || W % NT == 0)) return false;
+    return smem_layout(C, d.num_q_heads, 2 * P, 16 + 2 * P, N, 17 * W, 3).total <= 227 * 1024;
+}
+
 DecodePlan plan_decode(const rkv_layer_desc& d, int64_t max_seq_len) {
-    if (decode_kind(d) == kDecodeMma) return plan_decode_mma(d, max_seq_len);
+    const int kind = decode_kind(d);
+    if (kind == kDecodeMma) return plan_decode_mma(d, max_seq_len);
+    if (kind == kDecodeGeneric) return plan_decode_generic(d, max_seq_len);
     DecodePlan pl{};
     pl.kind = kDecodeSimt;
     const int C = d.num_kv_heads * d.head_dim;
@@ -799,6 +810,7 @@ DecodePlan plan_decode(const rkv_layer_desc& d, int64_t max_seq_len) {
 
 cudaError_t launch_decode(const rkv_layer_desc& d, const DecodePlan& plan, const DecodeParams& p, cudaStream_t s) {
     if (plan.kind == kDecodeMma) return launch_decode_mma(d, plan, p, s);
+    if (plan.kind == kDecodeGeneric) return launch_decode_generic(d, plan, p, s);
     const int B = d.batch;
     switch (plan.N * 16 + plan.REP) {
         case 512 * 16 + 1: return launch_decode_nr<512, 1>(plan, p, B, s);
@@ -836,6 +848,7 @@ cudaError_t launch_rotate_keys(const rkv_layer_desc& d, const uint16_t* k, int64
     const int C = d.num_kv_heads * d.head_dim, N = d.heads_per_group * d.head_dim;
     const float norm = 1.0f / sqrtf(static_cast<float>(N));
     if (rows <= 0) return cudaSuccess;
+    if ((N != 128 && N != 256 && N != 512) || C % 512 != 0) return launch_rotate_keys_generic(d, k, rows, out, s);
     const int L = N == 128 ? 8 : 16;
     const int64_t blocks = (rows + kRotRows - 1) / kRotRows;
     if (blocks > 0x7fffffff) return cudaErrorInvalidValue;

@@ -1002,11 +1002,15 @@ void* gqa_kernel(int pw, bool sp = false) {
 }
 }  // namespace
 
+// Kernel family for a layer shape (host only, no CUDA calls): the tensor-core
+// kernels where they tile, else the CUDA-core split kernel, else the generic
+// kernel (any rotation size / head ratio, generic.cu).
 int decode_kind(const rkv_layer_desc& d) {
     const int REP = d.num_q_heads / d.num_kv_heads;
-    if (options().force_simt.load()) return kDecodeSimt;
-    if (d.head_dim != 128 || d.num_q_heads % d.num_kv_heads != 0) return kDecodeSimt;
-    return decode_mma_supported(d.heads_per_group, REP, d.num_kv_heads * d.head_dim) ? kDecodeMma : kDecodeSimt;
+    if (d.head_dim == 128 && d.num_q_heads % d.num_kv_heads == 0 && !options().force_simt.load() &&
+        decode_mma_supported(d.heads_per_group, REP, d.num_kv_heads * d.head_dim))
+        return kDecodeMma;
+    return simt_shape_ok(d) ? kDecodeSimt : kDecodeGeneric;
 }
 
 DecodePlan plan_decode_mma(const rkv_layer_desc& d, int64_t max_seq_len) {

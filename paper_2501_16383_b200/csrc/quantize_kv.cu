@@ -54,52 +54,6 @@ __device__ __forceinline__ void sts64(uint32_t addr, float2 v) {
     asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(v.x), "f"(v.y) : "memory");
 }
 
-struct GroupQuant {
-    float t1, t2, t3;
-    uint32_t meta;
-};
-
-// proj/src/quant.cpp:74-94 for bits = 2 (scale rounded up to fp16
-// or e4m3 as in the reference).
-//   zero = clamp(rhaz(-mn / s), 0, 3): RN64(-mn/s) >= k + 0.5 exactly when
-//   -mn >= (k + 0.5) s (mn is fp32, s has <= 11 significant bits, so the
-//   quotient's rounding can never reach k + 0.5 from below), and (k + 0.5) s
-//   is exact in fp32.
-//   code >= k  <=>  rhaz(x/s) >= m := k - zero  <=>  x >= (m - 0.5) s (m >= 1),
-//   x > (m - 0.5) s (m <= 0); (m - 0.5) s is exact in fp32 and the strict
-//   case becomes >= on the next float up.
-template <int FMT>
-__device__ __forceinline__ GroupQuant group_params(float mn, float mx) {
-    const double range = __dsub_rn(static_cast<double>(mx), static_cast<double>(mn));
-    float raw = __double2float_rn(__ddiv_rn(range, 3.0));
-    if (raw < 1e-8f) raw = 1e-8f;
-    uint16_t sbits;
-    float sf;
-    if constexpr (FMT == RKV_SCALE_E4M3_CEIL) {
-        sf = e4m3_ceil_value(raw);
-        sbits = __half_as_ushort(__float2half_rn(sf));  // exact: e4m3 values are fp16 values
-    } else {
-        sbits = fp16_ceil(raw);
-        sf = __half2float(__ushort_as_half(sbits));
-    }
-    const float nm = -mn;
-    const int z = (nm >= 0.5f * sf) + (nm >= 1.5f * sf) + (nm >= 2.5f * sf);
-    float t[3];
-#pragma unroll
-    for (int k = 1; k <= 3; ++k) {
-        const int m = k - z;
-        float tt = __fmul_rn(static_cast<float>(m) - 0.5f, sf);
-        if (m <= 0) tt = __uint_as_float(__float_as_uint(tt) - 1u);  // tt < 0: next float toward +inf
-        t[k - 1] = tt;
-    }
-    GroupQuant g;
-    g.t1 = t[0];
-    g.t2 = t[1];
-    g.t3 = t[2];
-    g.meta = static_cast<uint32_t>(sbits) | (static_cast<uint32_t>(__half_as_ushort(__int2half_rn(z))) << 16);
-    return g;
-}
-
 // Layout-A half of the FWHT for region g: channels [32g, 32g+32) of both
 // tokens from the fp16 stage rows, stages on channel bits 0..4, stored to the
 // token-pair row.
@@ -132,7 +86,7 @@ __device__ __forceinline__ void fwht_region_a(const uint16_t* st0, const uint16_
 
 // Layout-B half: lane lam of an n-channel unit u (L = n/32 lanes) holds the
 // channels u*n + lam + L*j, j = 0..31; stages on channel bits 5..log2(n)-1,
-// then x norm, back in place.
+// then x norm (proj/src/hadamard.cpp:62-63), back in place.
 template <int N>
 __device__ __forceinline__ void fwht_unit_b(float2* row, int u, int lam, float norm) {
     constexpr int L = N / 32, LL = ilog2(L), LN = ilog2(N);
@@ -218,7 +172,10 @@ __device__ __forceinline__ Item decode_item(uint32_t it, uint32_t npairs, int nu
     Item r;
     r.isv = it & 1u;
     const uint32_t rest = it >> 1;
-    const uint32_t b = rest / npairs;
+    // rest / npairs via the fp32 reciprocal (rest < 2^30): off by at most one, fixed up
+    uint32_t b = __float2uint_rz(__uint2float_rz(rest) * __frcp_rz(__uint2float_rz(npairs)));
+    if (b * npairs > rest) --b;
+    if ((b + 1) * npairs <= rest) ++b;
     r.b = static_cast<int>(b);
     r.i0 = static_cast<int>(rest - b * npairs) * 2;
     r.has1 = r.i0 + 1 < num_new;
@@ -234,29 +191,63 @@ __device__ __forceinline__ void issue_item(const QuantParams& p, uint32_t it, ui
     bulk_g2s(dst, src, bytes, bar);
 }
 
+// Per-item metadata, computed one item ahead by threads 0..2 (global loads
+// off the critical path) and published by the item-end barrier.
+struct ItemMeta {
+    int slot[2];  // sidecar slot of the pair's tokens, -1 = not a sink
+    int64_t pos0; // cache position of the pair's first token
+};
+
+__device__ __forceinline__ void item_meta(const QuantParams& p, uint32_t it, uint32_t npairs, int num_new,
+                                          ItemMeta* m, int tid) {
+    const Item r = decode_item(it, npairs, num_new);
+    const int64_t pos0 = p.start_pos[r.b] + r.i0;
+    if (tid < 2) {
+        int slot = -1;
+        const int i = r.i0 + tid;
+        const int64_t pos = pos0 + tid;
+        if (p.sink_flags && i < num_new && pos >= 0 && pos < p.max_tokens &&
+            p.sink_flags[static_cast<int64_t>(r.b) * num_new + i]) {
+            int before = 0;
+            for (int q = 0; q < i; ++q) before += p.sink_flags[static_cast<int64_t>(r.b) * num_new + q] ? 1 : 0;
+            slot = p.cache.sink_count[r.b] + before;
+            // a full sidecar keeps the token quantized (mask bit clear, not counted)
+            if (slot >= p.max_sinks) slot = -1;
+        }
+        m->slot[tid] = slot;
+    } else {
+        m->pos0 = pos0;
+    }
+}
+
 // Shared memory: row [C/32][33] float2 (8.25 C B) | gather table [8][C/32] of
-// 4 x u16 float2 indices (2C B) | stage [2][C] fp16 (4C B).  One stage buffer:
-// the next item's TMA is issued as soon as every warp has finished layout A.
-template <int N, int FMT>
+// 4 x u16 float2 indices (2C B) | stage [2 buffers][2 tokens][C] fp16 (8C B).
+// Item k's rows land in stage k & 1; item k+1's copy is issued at item k-1's
+// end, so it has a whole item to arrive.
+template <int N, int FMT, int NS>
 __global__ void __launch_bounds__(256, 2) quantize_kv_kernel(QuantParams p, uint32_t items, uint32_t npairs) {
     extern __shared__ __align__(128) uint8_t smem[];
-    __shared__ uint64_t bar;
-    __shared__ int s_slot[2];
+    __shared__ uint64_t bar[2];
+    __shared__ ItemMeta s_meta[2];
     const int C = p.C, G32 = C / 32, W = C / 16, MG = C / kQuantGroup;
     const int num_new = static_cast<int>(p.num_new);
     float2* row = reinterpret_cast<float2*>(smem);
     uint16_t* tbl = reinterpret_cast<uint16_t*>(smem + G32 * 33 * 8);
-    uint16_t* stage = reinterpret_cast<uint16_t*>(smem + G32 * 33 * 8 + 2 * C);
+    uint16_t* stage = reinterpret_cast<uint16_t*>(smem + G32 * 33 * 8 + 2 * C);  // [2][2][C]
 
     const int tid = threadIdx.x, lane = tid & 31;
     const bool act = tid < G32;
     const int g = act ? tid : tid - 16;  // C/32 is a multiple of 16: idle half-warps mirror the previous one
+    const uint32_t step = gridDim.x;
 
     if (tid == 0) {
-        mbar_init(&bar, 1);
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
         mbar_fence_init();
-        if (blockIdx.x < items) issue_item(p, blockIdx.x, npairs, stage, &bar);
+        if (blockIdx.x < items) issue_item(p, blockIdx.x, npairs, stage, &bar[0]);
+        if (NS == 2 && blockIdx.x + step < items) issue_item(p, blockIdx.x + step, npairs, stage + 2 * C, &bar[1]);
     }
+    if (tid < 3 && blockIdx.x < items) item_meta(p, blockIdx.x, npairs, num_new, &s_meta[0], tid);
     // K gather table, only if this CTA sees a K item (even item index):
     // slot j = 32t + 4q + e  ->  tbl[(q * G32 + t) * 4 + e] = float2 index of channel perm[j]
     if (act && ((gridDim.x & 1u) || !(blockIdx.x & 1u))) {
@@ -274,34 +265,25 @@ __global__ void __launch_bounds__(256, 2) quantize_kv_kernel(QuantParams p, uint
     __syncthreads();
 
     uint32_t k = 0;
-    for (uint32_t it = blockIdx.x; it < items; it += gridDim.x, ++k) {
+    for (uint32_t it = blockIdx.x; it < items; it += step, ++k) {
         const Item r = decode_item(it, npairs, num_new);
-        // sink bookkeeping: slot = sink_count + #sinks among earlier new tokens of b
-        if (tid < 2) {
-            int slot = -1;
-            const int i = r.i0 + tid;
-            const int64_t pos = p.start_pos[r.b] + i;
-            if (p.sink_flags && i < num_new && pos >= 0 && pos < p.max_tokens &&
-                p.sink_flags[static_cast<int64_t>(r.b) * num_new + i]) {
-                int before = 0;
-                for (int q = 0; q < i; ++q) before += p.sink_flags[static_cast<int64_t>(r.b) * num_new + q] ? 1 : 0;
-                slot = p.cache.sink_count[r.b] + before;
-                // a full sidecar keeps the token quantized (mask bit clear, not counted)
-                if (slot >= p.max_sinks) slot = -1;
-            }
-            s_slot[tid] = slot;
-        }
-        mbar_wait(&bar, k & 1u);
+        const int sb = k & 1;  // metadata slot; TMA stage sb (NS = 2) or 0 (NS = 1)
+        const uint16_t* st = stage + (NS == 2 ? sb : 0) * 2 * C;
+        mbar_wait(&bar[NS == 2 ? sb : 0], NS == 2 ? (k >> 1) & 1u : k & 1u);
 
-        fwht_region_a(stage, r.has1 ? stage + C : stage, row, g);
+        fwht_region_a(st, r.has1 ? st + C : st, row, g);
         __syncwarp();
         if (!r.isv) {
             fwht_unit_b<N>(row, g / (N / 32), g % (N / 32), p.k_norm);
         } else {
             fwht_unit_b<128>(row, g / 4, g % 4, p.v_norm);
         }
-        __syncthreads();  // stage consumed, row complete, s_slot visible
-        if (tid == 0 && it + gridDim.x < items) issue_item(p, it + gridDim.x, npairs, stage, &bar);
+        __syncthreads();  // stage sb consumed, row complete
+        if (NS == 2 && tid == 0 && it + 2 * step < items)
+            issue_item(p, it + 2 * step, npairs, stage + sb * 2 * C, &bar[sb]);
+        if (NS == 1 && tid == 0 && it + step < items) issue_item(p, it + step, npairs, stage, &bar[0]);
+        if (tid < 3 && it + step < items) item_meta(p, it + step, npairs, num_new, &s_meta[sb ^ 1], tid);
+        const ItemMeta& meta = s_meta[sb];  // read from shared memory where used (registers are tight)
 
         float2 x[32];
         if (!r.isv) {
@@ -321,45 +303,43 @@ __global__ void __launch_bounds__(256, 2) quantize_kv_kernel(QuantParams p, uint
         const QuantOut qo = quantize_run<FMT>(x, lane);
         if (act) {
             uint32_t* codes = r.isv ? p.cache.v_codes : p.cache.k_codes;
-            uint32_t* meta = r.isv ? p.cache.v_meta : p.cache.k_meta;
-            const int64_t row0 = static_cast<int64_t>(r.b) * p.max_tokens + p.start_pos[r.b] + r.i0;
-            const int64_t pos0 = p.start_pos[r.b] + r.i0;
+            uint32_t* mt = r.isv ? p.cache.v_meta : p.cache.k_meta;
+            const int64_t row0 = static_cast<int64_t>(r.b) * p.max_tokens + meta.pos0;
 #pragma unroll
             for (int tok = 0; tok < 2; ++tok) {
                 if (tok == 1 && !r.has1) break;
-                if (pos0 + tok < 0 || pos0 + tok >= p.max_tokens) break;  // past the cache: never written
-                const bool sink = s_slot[tok] >= 0;
+                if (meta.pos0 + tok < 0 || meta.pos0 + tok >= p.max_tokens) break;  // past the cache: never written
+                const bool sink = meta.slot[tok] >= 0;
                 const int64_t rowi = row0 + tok;
                 *reinterpret_cast<uint2*>(codes + rowi * W + 2 * g) =
                     sink ? make_uint2(0u, 0u) : make_uint2(qo.w[tok][0], qo.w[tok][1]);
-                if ((lane & 3) == tok) meta[rowi * MG + g / 4] = sink ? 0u : qo.meta;
+                if ((lane & 3) == tok) mt[rowi * MG + g / 4] = sink ? 0u : qo.meta;
             }
         }
 
         // sink rows: raw fp16 rows into the sidecar (exact, proj/tests/test_kv_cache.cpp:22-45)
 #pragma unroll
         for (int tok = 0; tok < 2; ++tok) {
-            const int slot = s_slot[tok];
+            const int slot = meta.slot[tok];
             if (slot < 0) continue;  // slot < max_sinks by construction
             const uint4* srcr = reinterpret_cast<const uint4*>(
                 (r.isv ? p.v_new : p.k_new) + (static_cast<int64_t>(r.b) * p.num_new + r.i0 + tok) * C);
             uint16_t* side = r.isv ? p.cache.sink_v : p.cache.sink_k;
             uint4* dst = reinterpret_cast<uint4*>(side + (static_cast<int64_t>(r.b) * p.max_sinks + slot) * C);
             for (int j = tid; j < C / 8; j += blockDim.x) dst[j] = __ldg(srcr + j);
-            if (tid == 0 && !r.isv)
-                p.cache.sink_pos[r.b * p.max_sinks + slot] = static_cast<int32_t>(p.start_pos[r.b] + r.i0 + tok);
+            if (tid == 0 && !r.isv) p.cache.sink_pos[r.b * p.max_sinks + slot] = static_cast<int32_t>(meta.pos0 + tok);
         }
         // per-token sink bits (the K item owns them)
         if (tid < 2 && !r.isv && (tid == 0 || r.has1)) {
-            const int64_t pos = p.start_pos[r.b] + r.i0 + tid;
+            const int64_t pos = meta.pos0 + tid;
             if (pos >= 0 && pos < p.max_tokens) {
                 uint32_t* mw = p.cache.sink_mask + static_cast<int64_t>(r.b) * ((p.max_tokens + 31) / 32) + (pos >> 5);
                 const uint32_t bit = 1u << (pos & 31);
-                if (s_slot[tid] >= 0) atomicOr(mw, bit);
+                if (meta.slot[tid] >= 0) atomicOr(mw, bit);
                 else atomicAnd(mw, ~bit);
             }
         }
-        __syncthreads();  // row and s_slot are rewritten next
+        __syncthreads();  // row rewritten next; s_meta[sb ^ 1] visible
     }
 }
 
@@ -441,37 +421,41 @@ __global__ void promote_sinks_kernel(QuantParams p, const int64_t* __restrict__ 
     }
 }
 
-template <int N, int FMT>
-cudaError_t launch_quantize_n(const QuantParams& p, int B, cudaStream_t s) {
-    const size_t smem = static_cast<size_t>(p.C / 32) * 33 * 8 + static_cast<size_t>(p.C) * 6;
+template <int N, int FMT, int NS>
+cudaError_t launch_quantize_ns(const QuantParams& p, int B, cudaStream_t s) {
+    const size_t smem = static_cast<size_t>(p.C / 32) * 33 * 8 + static_cast<size_t>(p.C) * (2 + 4 * NS);
     static int per_sm_cache[9] = {0};  // keyed by C / 1024 (C <= 8192)
     int& per_sm = per_sm_cache[p.C / 1024];
     const int threads = (p.C / 32 + 31) / 32 * 32;
-    // the shared-memory limit is a per-kernel attribute: set it for THIS launch's
-    // size every time (a layer of another width may have lowered it)
     {
-        const cudaError_t e = ensure_smem_k(quantize_kv_kernel<N, FMT>, smem);
+        const cudaError_t e = ensure_smem_k(quantize_kv_kernel<N, FMT, NS>, smem);
         if (e != cudaSuccess) return e;
     }
     if (per_sm == 0) {
         int n = 0;
-        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, quantize_kv_kernel<N, FMT>, threads, smem);
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, quantize_kv_kernel<N, FMT, NS>, threads, smem);
         if (e != cudaSuccess) return e;
         if (n < 1) return cudaErrorInvalidConfiguration;
         per_sm = n;
     }
     const int64_t npairs = (p.num_new + 1) / 2;
     const int64_t items = 2 * static_cast<int64_t>(B) * npairs;
-    if (items >= (int64_t{1} << 31)) return cudaErrorInvalidValue;
+    if (items >= (int64_t{1} << 30)) return cudaErrorInvalidValue;
     int64_t grid = static_cast<int64_t>(num_sms()) * per_sm;
     if (grid > items) grid = items;
-    quantize_kv_kernel<N, FMT><<<static_cast<unsigned>(grid), threads, smem, s>>>(
+    quantize_kv_kernel<N, FMT, NS><<<static_cast<unsigned>(grid), threads, smem, s>>>(
         p, static_cast<uint32_t>(items), static_cast<uint32_t>(npairs));
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (!p.sink_flags) return cudaSuccess;
     quantize_sink_count_kernel<<<B, 256, 0, s>>>(p);
     return cudaGetLastError();
+}
+
+template <int N, int FMT>
+cudaError_t launch_quantize_n(const QuantParams& p, int B, cudaStream_t s) {
+    return options().quant_stages.load() == 2 ? launch_quantize_ns<N, FMT, 2>(p, B, s)
+                                              : launch_quantize_ns<N, FMT, 1>(p, B, s);
 }
 
 template <int N>
@@ -492,6 +476,12 @@ int promote_sinks_max() { return kPromoteMax; }
 
 cudaError_t launch_quantize(const rkv_layer_desc& d, const QuantParams& p, cudaStream_t s) {
     const int n = d.heads_per_group * d.head_dim;
+    if (generic_quantize_needed(d) || p.C % 512 != 0) {  // any other power-of-two rotation size (generic.cu)
+        cudaError_t e = launch_quantize_generic(d, p, s);
+        if (e != cudaSuccess || !p.sink_flags) return e;
+        quantize_sink_count_kernel<<<d.batch, 256, 0, s>>>(p);
+        return cudaGetLastError();
+    }
     switch (n) {
         case 128: return launch_quantize_fmt<128>(p, d.batch, s);
         case 256: return launch_quantize_fmt<256>(p, d.batch, s);

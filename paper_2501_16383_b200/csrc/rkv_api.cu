@@ -76,16 +76,13 @@ rkv_status validate(const rkv_layer_desc* d) {
     if (d->head_dim != 128) return fail(RKV_ERR_INVALID_ARGUMENT, "the sm_100a kernels need head_dim == 128");
     if (d->bits != 2 || d->group_size != 128)
         return fail(RKV_ERR_INVALID_ARGUMENT, "the sm_100a kernels implement bits == 2, group_size == 128");
-    if (n != 128 && n != 256 && n != 512)
-        return fail(RKV_ERR_INVALID_ARGUMENT, "the sm_100a kernels need heads_per_group*head_dim in {128,256,512}");
-    const int rep = d->num_q_heads / d->num_kv_heads;
-    if (!rkv::decode_supported(static_cast<int>(n), rep))
-        return fail(RKV_ERR_INVALID_ARGUMENT,
-                    "unsupported (heads_per_group, q heads per kv head): the sm_100a decode kernel takes "
-                    "G=4 with Hq/Hkv in {1,2}, G in {1,2} with Hq/Hkv in {1,2,4}");
     const int64_t C = static_cast<int64_t>(d->num_kv_heads) * d->head_dim;
-    if (C % 512 != 0) return fail(RKV_ERR_INVALID_ARGUMENT, "num_kv_heads*head_dim must be a multiple of 512");
     if (C > 8192) return fail(RKV_ERR_INVALID_ARGUMENT, "num_kv_heads*head_dim must be <= 8192");
+    // every power-of-two rotation size up to 2^13 and every head ratio has a kernel
+    // (the generic one where the specialised ones do not tile); it keeps a row and
+    // the per-head state in shared memory
+    if (rkv::decode_kind(*d) == rkv::kDecodeGeneric && rkv::generic_decode_smem(*d) > 227 * 1024)
+        return fail(RKV_ERR_INVALID_ARGUMENT, "too many query heads for the generic decode kernel's shared memory");
     return RKV_OK;
 }
 

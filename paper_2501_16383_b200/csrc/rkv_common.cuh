@@ -16,11 +16,14 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "rotatekv/rotatekv.h"
+
 namespace rkv {
 
 constexpr int kHeadDim = 128;
 constexpr int kQuantGroup = 128;
 constexpr float kLog2e = 1.4426950408889634f;
+constexpr int kRopeRow = 128;  // float4 per position pair in the RoPE table (decode_attention.cu)
 
 __host__ __device__ constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x >> 1); }
 
@@ -144,6 +147,58 @@ __device__ __forceinline__ float e4m3_ceil_value(float x) {
     }
     int e = (lo >> 3) & 0xf, m = lo & 7;
     return e == 0 ? ldexpf(static_cast<float>(m), -9) : ldexpf(1.0f + m * 0.125f, e - 7);
+}
+
+struct GroupQuant {
+    float t1, t2, t3;
+    uint32_t meta;
+};
+
+// proj/src/quant.cpp:74-94 for bits = 2 (scale rounded up to fp16
+// or e4m3 as in the reference).
+//   zero = clamp(rhaz(-mn / s), 0, 3): RN64(-mn/s) >= k + 0.5 exactly when
+//   -mn >= (k + 0.5) s (mn is fp32, s has <= 11 significant bits, so the
+//   quotient's rounding can never reach k + 0.5 from below), and (k + 0.5) s
+//   is exact in fp32.
+//   code >= k  <=>  rhaz(x/s) >= m := k - zero  <=>  x >= (m - 0.5) s (m >= 1),
+//   x > (m - 0.5) s (m <= 0); (m - 0.5) s is exact in fp32 and the strict
+//   case becomes >= on the next float up.
+template <int FMT>
+__device__ __forceinline__ GroupQuant group_params(float mn, float mx) {
+    const double range = __dsub_rn(static_cast<double>(mx), static_cast<double>(mn));
+    float raw = __double2float_rn(__ddiv_rn(range, 3.0));
+    if (raw < 1e-8f) raw = 1e-8f;
+    uint16_t sbits;
+    float sf;
+    if constexpr (FMT == RKV_SCALE_E4M3_CEIL) {
+        sf = e4m3_ceil_value(raw);
+        sbits = __half_as_ushort(__float2half_rn(sf));  // exact: e4m3 values are fp16 values
+    } else {
+        sbits = fp16_ceil(raw);
+        sf = __half2float(__ushort_as_half(sbits));
+    }
+    const float nm = -mn;
+    const int z = (nm >= 0.5f * sf) + (nm >= 1.5f * sf) + (nm >= 2.5f * sf);
+    float t[3];
+#pragma unroll
+    for (int k = 1; k <= 3; ++k) {
+        const int m = k - z;
+        float tt = __fmul_rn(static_cast<float>(m) - 0.5f, sf);
+        if (m <= 0) tt = __uint_as_float(__float_as_uint(tt) - 1u);  // tt < 0: next float toward +inf
+        t[k - 1] = tt;
+    }
+    GroupQuant g;
+    g.t1 = t[0];
+    g.t2 = t[1];
+    g.t3 = t[2];
+    g.meta = static_cast<uint32_t>(sbits) | (static_cast<uint32_t>(__half_as_ushort(__int2half_rn(z))) << 16);
+    return g;
+}
+
+// (cos, sin) of position pos, frequency f from section 1 of the RoPE table
+__device__ __forceinline__ float2 rope_at(const float4* t, int64_t pos, int f) {
+    const float4 r = __ldg(t + (pos >> 1) * kRopeRow + f);
+    return (pos & 1) ? make_float2(r.y, r.w) : make_float2(r.x, r.z);
 }
 
 }  // namespace rkv

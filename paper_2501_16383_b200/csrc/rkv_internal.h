@@ -21,6 +21,7 @@ struct Options {
     std::atomic<int> prefill_pair{0};  // 2-SM (cta_group::2) prefill attention
     std::atomic<int> simt_p{0};        // CUDA-core kernel: token pairs per tile (0 = planner)
     std::atomic<int> simt_stages{0};   // CUDA-core kernel: TMA ring depth (0 = planner)
+    std::atomic<int> quant_stages{1};  // quantize kernel: TMA stage buffers (1 or 2)
     std::atomic<int> epoch{0};
 };
 Options& options();
@@ -134,6 +135,16 @@ cudaError_t launch_rotate_keys(const rkv_layer_desc& d, const uint16_t* k, int64
 int num_sms();
 cudaError_t launch_channel_stats(const float* rows_f32, int64_t rows, int64_t C, bool mean_abs, double* stats,
                                  cudaStream_t s);
+// generic.cu (any power-of-two rotation size and head ratio)
+bool generic_quantize_needed(const rkv_layer_desc& d);
+cudaError_t launch_quantize_generic(const rkv_layer_desc& d, const QuantParams& p, cudaStream_t s);
+size_t generic_decode_smem(const rkv_layer_desc& d);
+DecodePlan plan_decode_generic(const rkv_layer_desc& d, int64_t max_seq_len);
+cudaError_t launch_decode_generic(const rkv_layer_desc& d, const DecodePlan& plan, const DecodeParams& p,
+                                  cudaStream_t s);
+bool simt_shape_ok(const rkv_layer_desc& d);
+cudaError_t launch_rotate_keys_generic(const rkv_layer_desc& d, const uint16_t* k, int64_t rows, float* out,
+                                       cudaStream_t s);
 // prefill.cu
 cudaError_t launch_prefill(const rkv_layer_desc& d, const PrefillParams& p, int64_t max_seq_len, cudaStream_t s);
 // sink_detect.cu

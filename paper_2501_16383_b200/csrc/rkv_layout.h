@@ -79,7 +79,7 @@ RKV_HD inline int mma_pos(int N, int c) {  // byte offset of channel c in a toke
 constexpr uint32_t kPlanMagic = 0x504B5652u;  // "RVKP"
 constexpr int kPlanHeader = 16;
 enum { PH_MAGIC = 0, PH_VERSION, PH_N, PH_L, PH_C, PH_W, PH_COST, PH_KIND };
-enum { kDecodeSimt = 0, kDecodeMma = 1 };
+enum { kDecodeSimt = 0, kDecodeMma = 1, kDecodeGeneric = 2 };
 
 RKV_HD inline int plan_words(int W) { return kPlanHeader + W + 16 * W; }
 

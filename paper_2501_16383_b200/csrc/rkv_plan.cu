@@ -54,8 +54,28 @@ int group_cost(const int* cls, const int* words, int GS) {
 bool build_decode_plan(const rkv_layer_desc& d, const int32_t* perm, std::vector<uint32_t>& out, int& cost_out) {
     const int kind = decode_kind(d);
     const int C = d.num_kv_heads * d.head_dim, N = kind == kDecodeMma ? mma_layout_n(d) : d.heads_per_group * d.head_dim;
+    const int W = C / 16;
+    if (kind == kDecodeGeneric) {  // generic kernel: identity word order, offsets = channel index perm[j]
+        out.assign(static_cast<size_t>(plan_words(W)), 0u);
+        out[PH_MAGIC] = kPlanMagic;
+        out[PH_VERSION] = 3;
+        out[PH_N] = static_cast<uint32_t>(N);
+        out[PH_L] = 0;
+        out[PH_C] = static_cast<uint32_t>(C);
+        out[PH_W] = static_cast<uint32_t>(W);
+        out[PH_KIND] = static_cast<uint32_t>(kind);
+        uint32_t* om = out.data() + kPlanHeader;
+        uint32_t* addr = om + W;
+        for (int w = 0; w < W; ++w) {
+            om[w] = static_cast<uint32_t>(w);
+            for (int e = 0; e < 16; ++e)
+                addr[(static_cast<size_t>(e / 4) * W + w) * 4 + e % 4] = static_cast<uint32_t>(perm[w * 16 + e]);
+        }
+        cost_out = 0;
+        return true;
+    }
     const int GS = kind == kDecodeMma ? 32 : 16;  // lanes whose stores share a wavefront
-    const int W = C / 16, G = W / GS;
+    const int G = W / GS;
     auto pos = [&](int c) { return kind == kDecodeMma ? mma_pos(N, c) : knat_pos(N, c) * 8; };
     std::vector<int> cls(static_cast<size_t>(C));
     for (int j = 0; j < C; ++j)

@@ -27,7 +27,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "_lib", "librotatekv_b200.so")
+LIB_PATH = os.environ.get("RKV_LIB") or os.path.join(_PKG, "_lib", "librotatekv_b200.so")  # RKV_LIB: A/B builds
 
 RKV_OK, RKV_ERR_INVALID_ARGUMENT, RKV_ERR_OUT_OF_RANGE, RKV_ERR_RUNTIME, RKV_ERR_CUDA = range(5)
 SCALE_FP16_CEIL, SCALE_E4M3_CEIL = 0, 1

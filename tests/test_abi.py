@@ -66,11 +66,20 @@ def cfg(**kw):
     (dict(head_dim=64), "head_dim == 128"),
     (dict(bits=4), "bits == 2"),
     (dict(max_tokens=0), "max_tokens"),
-    (dict(num_kv_heads=8, num_q_heads=8, heads_per_group=8), "{128,256,512}"),
+    (dict(num_kv_heads=128, num_q_heads=128, heads_per_group=4), "<= 8192"),
+    (dict(num_kv_heads=64, num_q_heads=512, heads_per_group=64), "generic decode kernel's shared memory"),
 ])
 def test_layer_validation_messages(lib, kw, msg):
     with pytest.raises(ValueError, match=re.escape(msg)):
         cfg(**kw).validate()
+
+
+def test_every_power_of_two_rotation_is_accepted(lib):
+    """RotationPlan::make accepts n = G*128 up to 2^13 with G | H
+    (proj/src/hadamard.cpp:18-33); so does the layer (G = 8 .. 64 run on the
+    generic kernels, as does GQA 4:1 at G = 4)."""
+    for hkv, g, hq in ((8, 8, 8), (16, 16, 16), (64, 64, 64), (32, 32, 32), (16, 4, 64), (8, 4, 32), (64, 1, 64)):
+        cfg(num_kv_heads=hkv, num_q_heads=hq, heads_per_group=g).validate()
 
 
 def test_valid_configs(lib):

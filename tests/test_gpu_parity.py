@@ -197,16 +197,61 @@ def test_decode_vs_oracle(oracle, hq, hkv, g, base, T):
         assert cosine(out[b], want) > COS_TOL
 
 
-@pytest.mark.parametrize("hq,hkv,g", [(64, 16, 4), (96, 8, 2), (64, 64, 1)])
-def test_decode_unsupported_shapes_refused(hq, hkv, g):
-    """Shapes no sm_100a decode kernel tiles raise ValueError (the reference's
-    std::invalid_argument) instead of launching anything."""
+@pytest.mark.parametrize("hq,hkv,g,T", [
+    (64, 16, 4, 70),    # GQA 4:1 at the paper's default G = 4 (LLaMA-3-8B shape at G = 4)
+    (32, 8, 4, 300),
+    (96, 8, 2, 70),     # 12 q heads per KV head
+    (64, 64, 1, 90),    # G = 1 at C = 8192
+    (16, 16, 8, 130),   # n = 1024
+    (32, 32, 16, 65),   # n = 2048
+    (64, 64, 64, 40),   # n = 8192 (kMaxHadamardLog2, proj/include/rotatekv/hadamard.hpp:21)
+    (24, 8, 8, 50),     # GQA 3:1 at n = 1024
+])
+def test_generic_shapes_vs_oracle(oracle, hq, hkv, g, T):
+    """Shapes the specialised kernels do not tile run on the generic kernels
+    (any power-of-two rotation size <= 8192, any head ratio): codes bit-exact,
+    decode within the north-star bar of the oracle."""
     w = small_workload(hq, hkv, g)
-    with pytest.raises(ValueError):
-        layer, _ = build_layer(w, 2, 78, seed=1)
-        k, v = WL.make_kv(w, 70, 2, 70)
-        layer.append(k, v)
-        layer.decode(WL.make_q(w, 70, 2))
+    B = 2
+    layer, perm = build_layer(w, B, T + 4, seed=T + g)
+    k, v = WL.make_kv(w, T + g, B, T)
+    sinks = torch.zeros(B, T, dtype=torch.uint8)
+    sinks[:, 0] = 1
+    sinks[1, T // 3] = 1
+    layer.append(k, v, sinks)
+    got = cache_host(layer)
+    for b in range(B):
+        kc, km, vc, vm = oracle.quantize_kv_rows(k[b].cpu().numpy(), v[b].cpu().numpy(), hkv, 128, g, perm)
+        rows = [t for t in range(T) if not sinks[b, t]]
+        assert np.array_equal(got["k_codes"][b, rows].view(np.uint32), kc[rows])
+        assert np.array_equal(got["k_meta"][b, rows].view(np.uint32), km[rows])
+        assert np.array_equal(got["v_codes"][b, rows].view(np.uint32), vc[rows])
+        assert np.array_equal(got["v_meta"][b, rows].view(np.uint32), vm[rows])
+    q = WL.make_q(w, T + g, B)
+    out = layer.decode(q).cpu().numpy()
+    for b in range(B):
+        want = oracle_decode(oracle, layer, got, b, T, q[b].cpu().numpy(), w, perm, k[b].cpu().numpy(),
+                             v[b].cpu().numpy())
+        assert rel_err(out[b], want) < 2e-4, rel_err(out[b], want)  # fp32 dequant: tighter than the bar
+        assert cosine(out[b], want) > 0.99999
+
+
+def test_generic_decode_matches_reference_decode_step(ref):
+    """G = 8 (n = 1024) end to end against the unmodified reference's
+    decode_step (e4m3 scales, identity projections)."""
+    w = small_workload(16, 16, 8)
+    T = 33
+    layer, perm = build_layer(w, 1, T + 1, seed=88, fmt=P.SCALE_E4M3_CEIL)
+    k, v = WL.make_kv(w, 88, 1, T + 1)
+    x = k[:, T:T + 1]
+    sinks = torch.zeros(1, T, dtype=torch.uint8)
+    sinks[0, 0] = 1
+    layer.append(k[:, :T], v[:, :T], sinks)
+    out = layer.decode_step(x, x, x.reshape(1, 16, 128)).cpu().numpy().reshape(-1)
+    want = ref.ref_decode_step(k[0, :T].float().cpu().numpy(), v[0, :T].float().cpu().numpy(), sinks[0].numpy(),
+                               perm, x[0, 0].float().cpu().numpy(), 16, 128, 8, 10000.0)
+    assert rel_err(out, want) < REL_TOL
+    assert cosine(out, want) > COS_TOL
 
 
 def test_decode_ragged_lengths(oracle):
