@@ -142,6 +142,22 @@ rkv_status rkv_promote_sinks(const rkv_layer_desc* desc, const rkv_cache* cache,
                              int64_t num_tokens, const uint16_t* k_rows, const uint16_t* v_rows, int32_t* promoted,
                              void* stream);
 
+/* LayerKVCache::key_row / value_row / keys / values (proj/src/kv_cache.cpp:
+ * 57-85), for tokens [t0, t0 + num_tokens) of sequence seq:
+ *   k_out, v_out : [num_tokens][C] fp32, device
+ *   frame        : RKV_FRAME_STORED -- what the reference returns: the stored
+ *                  fused-frame row s*(c - z) (K reordered + rotated, V rotated;
+ *                  sinks: the fused frame of the exact fp16 row, i.e. the
+ *                  reference's fp32 sidecar content);
+ *                  RKV_FRAME_RAW -- the same rows back in the model's frame
+ *                  (reorder and rotation undone; sinks exact)
+ *   perm         : [C] int32, device (the layer's reorder)
+ * Out-of-range tokens: RKV_ERR_OUT_OF_RANGE (the reference's
+ * std::out_of_range).  Debug / cross-check path, stream-ordered. */
+typedef enum { RKV_FRAME_STORED = 0, RKV_FRAME_RAW = 1 } rkv_row_frame;
+rkv_status rkv_cache_read(const rkv_layer_desc* desc, const rkv_cache* cache, const int32_t* perm, int64_t seq,
+                          int64_t t0, int64_t num_tokens, int32_t frame, float* k_out, float* v_out, void* stream);
+
 /* Experiment switches (process-global; defaults are the production
  * choices): "decode_kernel_simt" (1 = decode tensor-core shapes on the
  * CUDA-core kernel), "gqa_warps_per_group" (2..4), "gqa_tmem" (0/1),

@@ -258,6 +258,16 @@ public:
 
     void synchronize() const { check_cuda(cudaStreamSynchronize(stream_), "synchronize"); }
 
+    // LayerKVCache::key_row / value_row / keys / values (proj/src/kv_cache.cpp:57-85):
+    // tokens [t0, t0 + n) of sequence b into device [n][C] fp32 rows, the stored
+    // fused frame (RKV_FRAME_STORED, the reference's rows) or the model's frame
+    // (RKV_FRAME_RAW).  Throws std::out_of_range past the cache length.
+    void rows(int b, int64_t t0, int64_t n, int32_t frame, float* k_out, float* v_out) const {
+        if (b < 0 || b >= desc_.batch || t0 < 0 || n < 0 || t0 + n > len_[static_cast<size_t>(b)])
+            throw std::out_of_range("cache: token index out of range");
+        check(rkv_cache_read(&desc_, &cache_, perm_, b, t0, n, frame, k_out, v_out, stream_));
+    }
+
     // The attention half of prefill (proj/src/pipeline.cpp:156-191: reconstruct_cache,
     // causal reference_attention): q [B][num_q][Hq][d] fp16 device, row i of
     // sequence b at position q_start[b] + i attending to cache tokens

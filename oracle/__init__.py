@@ -118,6 +118,7 @@ def ref():
         R.ref_bench_step.argtypes = [C.c_void_p, C.c_int]
         R.ref_bench_destroy.argtypes = [C.c_void_p]
         R.ref_bench_set_memo.argtypes = [C.c_void_p, C.c_int]
+        R.ref_cache_rows.argtypes = [C.c_int64] * 3 + [C.c_void_p] * 3 + [C.c_int64] + [C.c_void_p] * 3
         R.ref_decode_step_routed.argtypes = ([C.c_int64] * 3 + [C.c_void_p] * 3 + [C.c_int64, C.c_void_p, C.c_int64,
                                              C.c_void_p, C.c_double, C.c_void_p, C.c_void_p])
     return _ref
@@ -328,6 +329,22 @@ def ref_decode_step(k_raw, v_raw, sink, perm, x, num_heads, head_dim, heads_per_
     if rc != 0:
         raise ValueError("ref_decode_step failed")
     return out
+
+
+def ref_cache_rows(k_raw, v_raw, sink, perm, num_heads, head_dim, heads_per_group):
+    """The reference's LayerKVCache::keys()/values() after appending the rows
+    (fused frame; e4m3 scales)."""
+    k_raw = f32(k_raw)
+    v_raw = f32(v_raw)
+    T, c = k_raw.shape
+    sink = np.ascontiguousarray(sink, dtype=np.uint8)
+    perm = np.ascontiguousarray(perm, dtype=np.int32)
+    ko = np.empty((T, c), np.float32)
+    vo = np.empty((T, c), np.float32)
+    if ref().ref_cache_rows(num_heads, head_dim, heads_per_group, _p(k_raw), _p(v_raw), _p(sink), T, _p(perm), _p(ko),
+                            _p(vo)) != 0:
+        raise ValueError("ref_cache_rows failed")
+    return ko, vo
 
 
 def ref_decode_step_routed(k_raw, v_raw, sink, promote, perm, x, num_heads, head_dim, heads_per_group, rope_base):

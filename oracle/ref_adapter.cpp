@@ -375,6 +375,33 @@ double ref_bench_step(void* handle, int nthreads) {
 
 void ref_bench_destroy(void* handle) { delete static_cast<RefBench*>(handle); }
 
+// LayerKVCache::keys() / values() (proj/src/kv_cache.cpp:68-85) of a cache
+// filled like ref_decode_step: the stored fused-frame rows (dequantised
+// blocks, fp32 sidecar rows for sinks), [T][C] each.
+int ref_cache_rows(int64_t num_heads, int64_t head_dim, int64_t hpg, const float* k_raw, const float* v_raw,
+                   const uint8_t* sink, int64_t T, const int32_t* perm, float* k_out, float* v_out) {
+    try {
+        int64_t c = num_heads * head_dim;
+        QuantConfig q;
+        q.bits = 2;
+        q.group_size = 128;
+        PipelineConfig cfg = PipelineConfig::make(PipelineMode::RotateKV, num_heads, head_dim, hpg, q, true);
+        cfg.reorder = plan_from_perm(perm, c);
+        LayerKVCache cache(q, c);
+        Tensor k({T, c}, std::vector<float>(k_raw, k_raw + T * c));
+        Tensor v({T, c}, std::vector<float>(v_raw, v_raw + T * c));
+        Tensor kt = apply_reorder(rotate_rows(k, cfg.key_rotation, false), cfg.reorder, 0, false);
+        Tensor vt = rotate_rows(v, cfg.value_rotation, false);
+        for (int64_t t = 0; t < T; ++t)
+            cache.append(std::span<const float>(kt.data() + t * c, static_cast<size_t>(c)),
+                         std::span<const float>(vt.data() + t * c, static_cast<size_t>(c)), sink[t] != 0);
+        Tensor ks = cache.keys(), vs = cache.values();
+        std::memcpy(k_out, ks.data(), sizeof(float) * static_cast<size_t>(T * c));
+        std::memcpy(v_out, vs.data(), sizeof(float) * static_cast<size_t>(T * c));
+        return 0;
+    } catch (const std::exception&) { return -1; }
+}
+
 // memo = 1 (default): decode_step memoises the reconstructed post-RoPE keys
 // across steps (the reference's DecodeMemo; the first step after creation
 // reconstructs the whole cache once); memo = 0: every step reconstructs it.

@@ -257,7 +257,81 @@ __global__ void __launch_bounds__(kGenThreads) rotate_keys_generic_kernel(const 
     }
 }
 
+// LayerKVCache::key_row / value_row / keys / values (proj/src/kv_cache.cpp:
+// 57-85): tokens [t0, t0 + n) of sequence b, K and V, as fp32 rows.
+//   frame 0 (RKV_FRAME_STORED): what the reference returns -- the stored
+//     fused-frame row s*(c - z) (K reordered + rotated, V rotated), and for a
+//     sink the fused frame of its raw fp16 row (rotate [+ reorder] in fp32,
+//     the reference's sidecar content);
+//   frame 1 (RKV_FRAME_RAW): back in the model's frame -- dequantised, the
+//     reorder and the rotation undone (K: inverse reorder, then FWHT over G
+//     heads; V: FWHT per head), sinks exact.
+// One CTA per row; the row is staged in shared memory.
+__global__ void __launch_bounds__(kGenThreads) cache_read_kernel(rkv_cache cache, const int32_t* __restrict__ perm,
+                                                              int64_t max_tokens, int max_sinks, int C, int nk,
+                                                              float k_norm, float v_norm, int b, int64_t t0, int64_t n,
+                                                              int frame, float* __restrict__ k_out,
+                                                              float* __restrict__ v_out) {
+    extern __shared__ __align__(16) float crow[];  // [C]
+    float* a = crow;
+    const int W = C / 16, MG = C / kQuantGroup;
+    const uint32_t* smask = cache.sink_mask + static_cast<int64_t>(b) * ((max_tokens + 31) / 32);
+    for (int64_t r = blockIdx.x; r < 2 * n; r += gridDim.x) {
+        const bool isv = r >= n;
+        const int64_t t = t0 + (isv ? r - n : r);
+        const int nn = isv ? kHeadDim : nk;
+        const float norm = isv ? v_norm : k_norm;
+        float* dst = (isv ? v_out : k_out) + (isv ? r - n : r) * C;
+        const bool sink = (smask[t >> 5] >> (t & 31)) & 1u;
+        if (sink) {
+            int slot = 0;
+            while (slot < max_sinks && cache.sink_pos[b * max_sinks + slot] != t) ++slot;
+            const uint16_t* src = (isv ? cache.sink_v : cache.sink_k) + (static_cast<int64_t>(b) * max_sinks + slot) * C;
+            if (frame == 1) {
+                for (int c = threadIdx.x; c < C; c += blockDim.x) dst[c] = h2f(src[c]);
+                continue;
+            }
+            for (int c = threadIdx.x; c < C; c += blockDim.x) a[c] = h2f(src[c]);
+            __syncthreads();
+            fwht_row(a, C, nn);
+            for (int c = threadIdx.x; c < C; c += blockDim.x) {
+                const float x = __fmul_rn(a[isv ? c : perm[c]], norm);  // K: slot c <- channel perm[c]
+                dst[c] = x;
+            }
+            __syncthreads();
+            continue;
+        }
+        const uint32_t* codes = (isv ? cache.v_codes : cache.k_codes) + (static_cast<int64_t>(b) * max_tokens + t) * W;
+        const uint32_t* meta = (isv ? cache.v_meta : cache.k_meta) + (static_cast<int64_t>(b) * max_tokens + t) * MG;
+        for (int j = threadIdx.x; j < C; j += blockDim.x) {  // dequantize_group (proj/src/quant.cpp:99-107)
+            const uint32_t m = meta[j >> 7];
+            const float sc = h2f(static_cast<uint16_t>(m & 0xffffu)), z = h2f(static_cast<uint16_t>(m >> 16));
+            const float x = sc * (static_cast<float>((codes[j >> 4] >> (2 * (j & 15))) & 3u) - z);
+            if (frame == 0) dst[j] = x;
+            else a[isv ? j : perm[j]] = x;  // inverse reorder: channel perm[j] <- slot j
+        }
+        if (frame == 0) continue;
+        __syncthreads();
+        fwht_row(a, C, nn);
+        for (int c = threadIdx.x; c < C; c += blockDim.x) dst[c] = __fmul_rn(a[c], norm);
+        __syncthreads();
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_cache_read(const rkv_layer_desc& d, const rkv_cache& cache, const int32_t* perm, int b, int64_t t0,
+                              int64_t n, int frame, float* k_out, float* v_out, cudaStream_t s) {
+    const int C = d.num_kv_heads * d.head_dim, nk = d.heads_per_group * d.head_dim;
+    const size_t smem = static_cast<size_t>(C) * sizeof(float);
+    cudaError_t e = ensure_smem_k(cache_read_kernel, smem);
+    if (e != cudaSuccess) return e;
+    const int64_t grid = std::min<int64_t>(2 * n, static_cast<int64_t>(num_sms()) * 8);
+    cache_read_kernel<<<static_cast<unsigned>(grid), kGenThreads, smem, s>>>(
+        cache, perm, d.max_tokens, d.max_sinks, C, nk, 1.0f / sqrtf(static_cast<float>(nk)),
+        1.0f / sqrtf(static_cast<float>(d.head_dim)), b, t0, n, frame, k_out, v_out);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_rotate_keys_generic(const rkv_layer_desc& d, const uint16_t* k, int64_t rows, float* out,
                                        cudaStream_t s) {

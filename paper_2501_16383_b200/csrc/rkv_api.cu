@@ -331,6 +331,23 @@ rkv_status rkv_promote_sinks(const rkv_layer_desc* desc, const rkv_cache* cache,
     return RKV_OK;
 }
 
+rkv_status rkv_cache_read(const rkv_layer_desc* desc, const rkv_cache* cache, const int32_t* perm, int64_t seq,
+                          int64_t t0, int64_t num_tokens, int32_t frame, float* k_out, float* v_out, void* stream) {
+    rkv_status st = validate(desc);
+    if (st != RKV_OK) return st;
+    if ((st = check_cache(cache)) != RKV_OK) return st;
+    if (frame != RKV_FRAME_STORED && frame != RKV_FRAME_RAW)
+        return fail(RKV_ERR_INVALID_ARGUMENT, "cache_read: frame must be RKV_FRAME_STORED or RKV_FRAME_RAW");
+    if (seq < 0 || seq >= desc->batch || t0 < 0 || num_tokens < 0 || t0 + num_tokens > desc->max_tokens)
+        return fail(RKV_ERR_OUT_OF_RANGE, "cache: token index out of range");
+    if (num_tokens == 0) return RKV_OK;
+    if (!perm || !k_out || !v_out) return fail(RKV_ERR_INVALID_ARGUMENT, "cache_read: null argument");
+    cudaError_t e = rkv::launch_cache_read(*desc, *cache, perm, static_cast<int>(seq), t0, num_tokens, frame, k_out,
+                                           v_out, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "cache_read");
+    return RKV_OK;
+}
+
 size_t rkv_layer_plan_bytes(const rkv_layer_desc* desc) {
     if (validate(desc) != RKV_OK) return 0;
     const int W = desc->num_kv_heads * desc->head_dim / 16;

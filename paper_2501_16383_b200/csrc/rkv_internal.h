@@ -145,6 +145,8 @@ cudaError_t launch_decode_generic(const rkv_layer_desc& d, const DecodePlan& pla
 bool simt_shape_ok(const rkv_layer_desc& d);
 cudaError_t launch_rotate_keys_generic(const rkv_layer_desc& d, const uint16_t* k, int64_t rows, float* out,
                                        cudaStream_t s);
+cudaError_t launch_cache_read(const rkv_layer_desc& d, const rkv_cache& cache, const int32_t* perm, int b, int64_t t0,
+                              int64_t n, int frame, float* k_out, float* v_out, cudaStream_t s);
 // prefill.cu
 cudaError_t launch_prefill(const rkv_layer_desc& d, const PrefillParams& p, int64_t max_seq_len, cudaStream_t s);
 // sink_detect.cu

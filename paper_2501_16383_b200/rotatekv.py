@@ -109,8 +109,9 @@ def lib():
         L.rkv_calibrate_workspace_bytes.argtypes = [D, C.c_int64]
         L.rkv_calibrate_reorder_device.argtypes = [D, P, C.c_int64, C.c_int32, P, C.c_size_t, P, P, P]
         L.rkv_promote_sinks.argtypes = [D, C.POINTER(CacheView), P, C.c_int64, P, P, P, P]
+        L.rkv_cache_read.argtypes = [D, C.POINTER(CacheView), P, C.c_int64, C.c_int64, C.c_int64, C.c_int32, P, P, P]
         L.rkv_set_debug_option.argtypes = [C.c_char_p, C.c_int64]
-        for name in ("rkv_promote_sinks", "rkv_set_debug_option", "rkv_layer_validate", "rkv_cache_carve", "rkv_cache_reset", "rkv_rope_table_init",
+        for name in ("rkv_promote_sinks", "rkv_set_debug_option", "rkv_cache_read", "rkv_layer_validate", "rkv_cache_carve", "rkv_cache_reset", "rkv_rope_table_init",
                      "rkv_quantize_kv", "rkv_decode_attention", "rkv_rotate_keys", "rkv_calibrate_reorder",
                      "rkv_detect_sinks", "rkv_detect_sinks_device", "rkv_layer_plan_build", "rkv_layer_plan_init",
                      "rkv_calibrate_reorder_device", "rkv_cache_export", "rkv_cache_import",
@@ -392,6 +393,28 @@ class RotateKVLayer:
         cnt = int(self.sink_counts[seq])
         self.sink_tokens[seq] = set(int(t) for t in self.arrays()["sink_pos"][seq, :cnt].cpu().numpy())
         return n.value
+
+    # -- LayerKVCache::key_row / value_row / keys / values (proj/src/kv_cache.cpp:57-85)
+    def rows(self, seq: int, t0: int = 0, n: int | None = None, raw: bool = False):
+        """(K, V) fp32 [n, C] of tokens [t0, t0+n) of sequence seq: the stored
+        fused-frame rows (what the reference's key_row/value_row return) or,
+        with raw=True, back in the model's frame."""
+        torch = self.torch
+        if n is None:
+            n = int(self.lengths[seq]) - t0 if 0 <= seq < self.cfg.batch else 0
+        if not 0 <= seq < self.cfg.batch or t0 < 0 or n < 0 or t0 + n > self.lengths[seq]:
+            raise IndexError("cache: token index out of range")
+        k = torch.empty(max(n, 1), self.cfg.channels, dtype=torch.float32, device=self.device)
+        v = torch.empty_like(k)
+        _check(lib().rkv_cache_read(C.byref(self._desc), C.byref(self._view), _ptr(self.perm), seq, t0, n,
+                                    1 if raw else 0, _ptr(k), _ptr(v), self._stream()))
+        return k[:n], v[:n]
+
+    def key_row(self, seq: int, token: int):
+        return self.rows(seq, token, 1)[0][0]
+
+    def value_row(self, seq: int, token: int):
+        return self.rows(seq, token, 1)[1][0]
 
     # -- LayerKVCache::promote_to_sink / route_sinks (proj/src/kv_cache.cpp:43-55, proj/src/sink.cpp:47-63)
     def promote_sinks(self, tokens, k_rows, v_rows):

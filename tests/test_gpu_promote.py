@@ -108,3 +108,38 @@ def test_promote_errors_and_device_guards():
     assert after["sink_pos"][0, 1] == 9
     assert np.array_equal(after["k_codes"][0, 10], before["k_codes"][0, 10])  # stays quantized
     assert not after["k_codes"][0, 9].any()
+
+
+# ------------------------------------------------------------ row readback
+
+@pytest.mark.parametrize("hq,hkv,g", [(8, 8, 4), (8, 8, 8), (32, 8, 2)])
+def test_cache_rows_match_reference_keys_values(ref, hq, hkv, g):
+    """rkv_cache_read (STORED frame) == the reference's LayerKVCache::keys() /
+    values() bit for bit (e4m3 scales; sinks = fp32 sidecar rows); the RAW
+    frame == inverse reorder + FWHT of those rows (the oracle)."""
+    w = small_workload(hq, hkv, g)
+    T = 40
+    layer, perm = build_layer(w, 2, T, seed=61, fmt=P.SCALE_E4M3_CEIL)
+    k, v = WL.make_kv(w, 61, 2, T)
+    sinks = torch.zeros(2, T, dtype=torch.uint8)
+    sinks[:, 0] = 1
+    sinks[1, 17] = 1
+    layer.append(k, v, sinks)
+    for b in range(2):
+        ks, vs = layer.rows(b)
+        want_k, want_v = ref.ref_cache_rows(k[b].float().cpu().numpy(), v[b].float().cpu().numpy(),
+                                            sinks[b].numpy(), perm, hkv, 128, g)
+        assert np.array_equal(ks.cpu().numpy(), want_k)
+        assert np.array_equal(vs.cpu().numpy(), want_v)
+        kr, vr = layer.rows(b, raw=True)
+        exp_k = ref.rotate_rows(ref.apply_reorder(want_k, perm, inverse=True), 128, g, hkv)
+        exp_v = ref.rotate_rows(want_v, 128, 1, hkv)
+        nonsink = [t for t in range(T) if not sinks[b, t]]
+        assert np.array_equal(kr.cpu().numpy()[nonsink], exp_k[nonsink])
+        assert np.array_equal(vr.cpu().numpy()[nonsink], exp_v[nonsink])
+        for t in range(T):  # sinks come back exact in the raw frame
+            if sinks[b, t]:
+                assert np.array_equal(kr[t].cpu().numpy(), k[b, t].float().cpu().numpy())
+    assert torch.equal(layer.key_row(1, 17), layer.rows(1, 17, 1)[0][0])
+    with pytest.raises(IndexError):
+        layer.rows(0, 35, 10)
