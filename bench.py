@@ -750,6 +750,28 @@ def run_ours(args):
     h2d = wl.qs[0].numel() * 2 * world
     d2h = wl.out.numel() * 4 * world
 
+    # ---- e2e_cpp: the same step through the C++ API (rotatekv.hpp DeviceLayerCache)
+    e2e_cpp = None
+    try:
+        from paper_2501_16383_b200 import build as BLD
+
+        exe = BLD.E2E_CPP
+        if os.path.exists(exe):
+            r = subprocess.run([exe, "--batch", str(wl.B), "--q-heads", str(w.num_q_heads), "--kv-heads",
+                                str(w.num_kv_heads), "--group", str(w.heads_per_group), "--tokens", str(w.tokens),
+                                "--steps", str(args.steps), "--warmup", str(args.warmup), "--device", str(local),
+                                "--seed", str(seed_of(HEADLINE_CFG))], capture_output=True, text=True, timeout=600)
+            d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+            ms_cpp = max_over_ranks([d["ms"]], dev, world)[0]
+            e2e_cpp = {"value": w.batch * args.steps / (ms_cpp / 1e3), "unit": "tokens/s",
+                       "h2d_bytes_per_step": d["h2d_bytes_per_step"] * world,
+                       "d2h_bytes_per_step": d["d2h_bytes_per_step"] * world, "finite": d["finite"],
+                       "path": "C++ API (rotatekv.hpp DeviceLayerCache::decode_attention), pinned host q in / "
+                               "fp32 out per step, one process per GPU (paper_2501_16383_b200/csrc/e2e_cpp.cu)"}
+        else:
+            max_over_ranks([0.0], dev, world)
+    except Exception as exc:
+        e2e_cpp = {"error": str(exc)[:200]}
     roof = hbm_roofline(wl.bytes_per_step(), decode_ms, "rkv_decode_attention (decode_mma_kernel + combine), per rank")
     roof["traffic"], roof["traffic_source"] = traffic_for(f"cfg{HEADLINE_CFG}")
     del wl, graphs
@@ -811,6 +833,7 @@ def run_ours(args):
         "roofline": roof,
         "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "path": "Python host layer -> C ABI rkv_decode_attention, pinned host q in / fp32 out per step"},
+        "e2e_cpp": e2e_cpp,
         "gpu_launches": 2 * args.steps,  # decode_mma_kernel + decode_combine_kernel per step
         "cuda_graph": not args.no_graph,
         "clocks": clocks.summary(),

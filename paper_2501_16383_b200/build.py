@@ -61,6 +61,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 cmd.insert(1, "-Xptxas=-v")
             jobs.append(cmd)
     if not jobs and not _stale(LIB, objs):
+        build_e2e_cpp()
         return LIB
 
     def run(cmd):
@@ -75,7 +76,24 @@ def build(force: bool = False, verbose: bool = False) -> str:
     tmp = LIB + ".tmp"
     subprocess.run([_nvcc(), *ARCH, "-shared", "-o", tmp, *objs], check=True)
     os.replace(tmp, LIB)
+    build_e2e_cpp(force=True)
     return LIB
+
+
+E2E_CPP = os.path.join(LIBDIR, "rkv_e2e_cpp")
+
+
+def build_e2e_cpp(force: bool = False) -> str:
+    """The C++-API decode-step program bench.py times for `e2e_cpp`
+    (csrc/e2e_cpp.cu, linked against the library with an $ORIGIN rpath)."""
+    src = os.path.join(CSRC, "e2e_cpp.cu")
+    hpp = os.path.join(INCLUDE, "rotatekv", "rotatekv.hpp")
+    if not force and not _stale(E2E_CPP, [src, hpp, LIB]):
+        return E2E_CPP
+    subprocess.run([_nvcc(), *ARCH, "-O2", "-std=c++17", "-I", INCLUDE, src, "-o", E2E_CPP + ".tmp", "-L", LIBDIR,
+                    "-lrotatekv_b200", "-Xlinker", "-rpath,$ORIGIN"], check=True)
+    os.replace(E2E_CPP + ".tmp", E2E_CPP)
+    return E2E_CPP
 
 
 if __name__ == "__main__":

@@ -25,7 +25,7 @@ def decode_bytes(w, B, T, nsinks):
     return B * ((T - nsinks) * 2 * (c // 4 + 4 * c // 128) + nsinks * 4 * c) + B * w.num_q_heads * 128 * 6
 
 
-def run(cfg_id, iters=20, g=None):
+def run(cfg_id, iters=20, g=None, warm=3):
     w = WL.CONFIGS[cfg_id]
     if g is not None:  # same shape with another rotation group size (e.g. the reference default G = 1)
         w = dataclasses.replace(w, heads_per_group=g, name=f"{w.name}-g{g}")
@@ -48,7 +48,7 @@ def run(cfg_id, iters=20, g=None):
     lens = torch.full((B,), T, dtype=torch.int64, device=dev)
     out = torch.empty(B, w.num_q_heads, 128, dtype=torch.float32, device=dev)
     ws, wsb = layer.workspace(T)
-    for _ in range(3):
+    for _ in range(warm):
         layer.decode_device(q, lens, T, out, ws, wsb)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -67,7 +67,10 @@ if __name__ == "__main__":
     if os.environ.get("RKV_DECODE_KERNEL") == "simt":
         P.set_debug_option("decode_kernel_simt", 1)
     # "2" = config 2; "2g1" = config 2's shape with G = 1
-    ids = sys.argv[1:] or ["2", "3", "4"]
+    # --profile: one warm-up and one timed launch per config (for ncu captures)
+    prof = "--profile" in sys.argv
+    ids = [a for a in sys.argv[1:] if not a.startswith("--")] or ["2", "3", "4"]
     for a in ids:
         cfg, _, g = a.partition("g")
-        print(json.dumps(run(int(cfg), g=int(g) if g else None)), flush=True)
+        print(json.dumps(run(int(cfg), g=int(g) if g else None, iters=1 if prof else 20, warm=1 if prof else 3)),
+              flush=True)
