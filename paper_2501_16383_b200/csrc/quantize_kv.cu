@@ -168,10 +168,12 @@ struct Item {
     int i0;
 };
 
-__device__ __forceinline__ Item decode_item(uint32_t it, uint32_t npairs, int num_new) {
+// item = (K or V, sequence, token pair); with k_only (V quantized by
+// quantize_v_kernel) the items are K only
+__device__ __forceinline__ Item decode_item(uint32_t it, uint32_t npairs, int num_new, int k_only) {
     Item r;
-    r.isv = it & 1u;
-    const uint32_t rest = it >> 1;
+    r.isv = k_only ? false : (it & 1u);
+    const uint32_t rest = k_only ? it : it >> 1;
     // rest / npairs via the fp32 reciprocal (rest < 2^30): off by at most one, fixed up
     uint32_t b = __float2uint_rz(__uint2float_rz(rest) * __frcp_rz(__uint2float_rz(npairs)));
     if (b * npairs > rest) --b;
@@ -184,7 +186,7 @@ __device__ __forceinline__ Item decode_item(uint32_t it, uint32_t npairs, int nu
 
 __device__ __forceinline__ void issue_item(const QuantParams& p, uint32_t it, uint32_t npairs, uint16_t* dst,
                                            uint64_t* bar) {
-    const Item r = decode_item(it, npairs, static_cast<int>(p.num_new));
+    const Item r = decode_item(it, npairs, static_cast<int>(p.num_new), p.k_only);
     const uint16_t* src = (r.isv ? p.v_new : p.k_new) + (static_cast<int64_t>(r.b) * p.num_new + r.i0) * p.C;
     const uint32_t bytes = static_cast<uint32_t>((r.has1 ? 2 : 1) * p.C * 2);
     mbar_arrive_expect_tx(bar, bytes);
@@ -200,7 +202,7 @@ struct ItemMeta {
 
 __device__ __forceinline__ void item_meta(const QuantParams& p, uint32_t it, uint32_t npairs, int num_new,
                                           ItemMeta* m, int tid) {
-    const Item r = decode_item(it, npairs, num_new);
+    const Item r = decode_item(it, npairs, num_new, p.k_only);
     const int64_t pos0 = p.start_pos[r.b] + r.i0;
     if (tid < 2) {
         int slot = -1;
@@ -250,7 +252,7 @@ __global__ void __launch_bounds__(256, 2) quantize_kv_kernel(QuantParams p, uint
     if (tid < 3 && blockIdx.x < items) item_meta(p, blockIdx.x, npairs, num_new, &s_meta[0], tid);
     // K gather table, only if this CTA sees a K item (even item index):
     // slot j = 32t + 4q + e  ->  tbl[(q * G32 + t) * 4 + e] = float2 index of channel perm[j]
-    if (act && ((gridDim.x & 1u) || !(blockIdx.x & 1u))) {
+    if (act && (p.k_only || (gridDim.x & 1u) || !(blockIdx.x & 1u))) {
         const int4* pv = reinterpret_cast<const int4*>(p.perm) + 8 * g;
         int4 v[8];
 #pragma unroll
@@ -266,7 +268,7 @@ __global__ void __launch_bounds__(256, 2) quantize_kv_kernel(QuantParams p, uint
 
     uint32_t k = 0;
     for (uint32_t it = blockIdx.x; it < items; it += step, ++k) {
-        const Item r = decode_item(it, npairs, num_new);
+        const Item r = decode_item(it, npairs, num_new, p.k_only);
         const int sb = k & 1;  // metadata slot; TMA stage sb (NS = 2) or 0 (NS = 1)
         const uint16_t* st = stage + (NS == 2 ? sb : 0) * 2 * C;
         mbar_wait(&bar[NS == 2 ? sb : 0], NS == 2 ? (k >> 1) & 1u : k & 1u);
@@ -340,6 +342,115 @@ __global__ void __launch_bounds__(256, 2) quantize_kv_kernel(QuantParams p, uint
             }
         }
         __syncthreads();  // row rewritten next; s_meta[sb ^ 1] visible
+    }
+}
+
+// V quantize, warp-independent.  V's rotation is per head (128 channels) and
+// V has no reorder, so a warp can own a 1024-channel segment of a token pair
+// outright: its own TMA stage (double-buffered, its own mbarriers), layout A
+// on its 32 regions, layout B on its 8 heads, quantize on its own slots --
+// only __syncwarp, never a CTA barrier.  Sub-item = (sequence, token pair,
+// segment); the K items (global reorder: a CTA-wide gather) stay on
+// quantize_kv_kernel.  Same arithmetic as there (fwht_region_a,
+// fwht_unit_b<128>, quantize_run): bit-identical codes.
+constexpr int kVSeg = 1024;                       // channels per warp segment (32 regions)
+constexpr int kVWarps = 12;                       // warps per CTA (1 CTA per SM)
+constexpr int kVRowF2 = (kVSeg / 32) * 33;        // float2 per segment row (padded regions)
+constexpr int kVWarpBytes = 2 * 2 * kVSeg * 2 + kVRowF2 * 8;  // 2 stages x 2 tokens fp16 + row
+template <int FMT>
+__global__ void __launch_bounds__(32 * kVWarps, 1) quantize_v_kernel(QuantParams p, uint32_t subitems, uint32_t npairs,
+                                                                    uint32_t nseg) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ uint64_t bar[kVWarps][2];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int C = p.C, W = C / 16, MG = C / kQuantGroup;
+    const int num_new = static_cast<int>(p.num_new);
+    uint8_t* base = smem + warp * kVWarpBytes;
+    uint16_t* stage = reinterpret_cast<uint16_t*>(base);                 // [2][2][kVSeg]
+    float2* row = reinterpret_cast<float2*>(base + 2 * 2 * kVSeg * 2);   // [32][33]
+    const uint32_t gw = blockIdx.x * kVWarps + warp, step = gridDim.x * kVWarps;
+
+    // sub-item -> (b, i0, segment)
+    auto decode = [&](uint32_t si, int& b, int& i0, int& seg) {
+        seg = static_cast<int>(si % nseg);
+        const uint32_t pr = si / nseg;
+        b = static_cast<int>(pr / npairs);
+        i0 = static_cast<int>(pr % npairs) * 2;
+    };
+    auto issue = [&](uint32_t si, int sb) {
+        int b, i0, seg;
+        decode(si, b, i0, seg);
+        const bool has1 = i0 + 1 < num_new;
+        const uint16_t* src = p.v_new + (static_cast<int64_t>(b) * num_new + i0) * C + seg * kVSeg;
+        uint16_t* dst = stage + sb * 2 * kVSeg;
+        mbar_arrive_expect_tx(&bar[warp][sb], (has1 ? 2u : 1u) * kVSeg * 2);
+        bulk_g2s(dst, src, kVSeg * 2, &bar[warp][sb]);
+        if (has1) bulk_g2s(dst + kVSeg, src + C, kVSeg * 2, &bar[warp][sb]);
+    };
+    if (lane == 0) {
+        mbar_init(&bar[warp][0], 1);
+        mbar_init(&bar[warp][1], 1);
+        mbar_fence_init();
+        if (gw < subitems) issue(gw, 0);
+        if (gw + step < subitems) issue(gw + step, 1);
+    }
+    __syncwarp();
+    uint32_t k = 0;
+    for (uint32_t si = gw; si < subitems; si += step, ++k) {
+        int b, i0, seg;
+        decode(si, b, i0, seg);
+        const bool has1 = i0 + 1 < num_new;
+        const int sb = k & 1;
+        // sidecar slots of the pair's tokens (quantize_kv_kernel's rule, same inputs)
+        int slot = -1;
+        if (lane < 2) {
+            const int i = i0 + lane;
+            const int64_t pos = p.start_pos[b] + i;
+            if (p.sink_flags && i < num_new && pos >= 0 && pos < p.max_tokens &&
+                p.sink_flags[static_cast<int64_t>(b) * num_new + i]) {
+                int before = 0;
+                for (int q = 0; q < i; ++q) before += p.sink_flags[static_cast<int64_t>(b) * num_new + q] ? 1 : 0;
+                slot = p.cache.sink_count[b] + before;
+                if (slot >= p.max_sinks) slot = -1;
+            }
+        }
+        const int slot0 = __shfl_sync(0xffffffffu, slot, 0), slot1 = __shfl_sync(0xffffffffu, slot, 1);
+        const int64_t pos0 = p.start_pos[b] + i0;
+        mbar_wait(&bar[warp][sb], (k >> 1) & 1u);
+        const uint16_t* st = stage + sb * 2 * kVSeg;
+        fwht_region_a(st, has1 ? st + kVSeg : st, row, lane);
+        __syncwarp();
+        // the stage is consumed: refill it with the sub-item after next
+        if (lane == 0 && si + 2 * step < subitems) issue(si + 2 * step, sb);
+        fwht_unit_b<128>(row, lane / 4, lane % 4, p.v_norm);
+        __syncwarp();
+        float2 x[32];
+        const float2* srcr = row + 33 * lane;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) x[c] = srcr[c];
+        const QuantOut qo = quantize_run<FMT>(x, lane);
+        const int64_t row0 = static_cast<int64_t>(b) * p.max_tokens + pos0;
+#pragma unroll
+        for (int tok = 0; tok < 2; ++tok) {
+            if (tok == 1 && !has1) break;
+            if (pos0 + tok < 0 || pos0 + tok >= p.max_tokens) break;  // past the cache: never written
+            const bool sink = (tok ? slot1 : slot0) >= 0;
+            const int64_t rowi = row0 + tok;
+            *reinterpret_cast<uint2*>(p.cache.v_codes + rowi * W + seg * (kVSeg / 16) + 2 * lane) =
+                sink ? make_uint2(0u, 0u) : make_uint2(qo.w[tok][0], qo.w[tok][1]);
+            if ((lane & 3) == tok) p.cache.v_meta[rowi * MG + seg * (kVSeg / 128) + lane / 4] = sink ? 0u : qo.meta;
+        }
+#pragma unroll
+        for (int tok = 0; tok < 2; ++tok) {  // sink rows: this segment of the raw fp16 row into the sidecar
+            const int sl = tok ? slot1 : slot0;
+            if (sl < 0) continue;
+            const uint4* srcv = reinterpret_cast<const uint4*>(p.v_new + (static_cast<int64_t>(b) * num_new + i0 + tok) * C +
+                                                               seg * kVSeg);
+            uint4* dst = reinterpret_cast<uint4*>(p.cache.sink_v + (static_cast<int64_t>(b) * p.max_sinks + sl) * C +
+                                                  seg * kVSeg);
+            for (int j = lane; j < kVSeg / 8; j += 32) dst[j] = __ldg(srcv + j);
+        }
+        __syncwarp();  // the row is rewritten by the next sub-item
     }
 }
 
@@ -439,12 +550,27 @@ cudaError_t launch_quantize_ns(const QuantParams& p, int B, cudaStream_t s) {
         per_sm = n;
     }
     const int64_t npairs = (p.num_new + 1) / 2;
-    const int64_t items = 2 * static_cast<int64_t>(B) * npairs;
+    QuantParams pk = p;
+    // V on the warp-independent kernel when the row splits into 1024-channel segments
+    const bool vsplit = p.C % kVSeg == 0 && options().quant_vsplit.load() != 0;
+    if (vsplit) {
+        const size_t vsmem = static_cast<size_t>(kVWarps) * kVWarpBytes;
+        cudaError_t e = ensure_smem_k(quantize_v_kernel<FMT>, vsmem);
+        if (e != cudaSuccess) return e;
+        const int64_t nseg = p.C / kVSeg, sub = static_cast<int64_t>(B) * npairs * nseg;
+        if (sub >= (int64_t{1} << 31)) return cudaErrorInvalidValue;
+        const int64_t vgrid = std::min<int64_t>(num_sms(), (sub + kVWarps - 1) / kVWarps);
+        quantize_v_kernel<FMT><<<static_cast<unsigned>(vgrid), 32 * kVWarps, vsmem, s>>>(
+            p, static_cast<uint32_t>(sub), static_cast<uint32_t>(npairs), static_cast<uint32_t>(nseg));
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        pk.k_only = 1;
+    }
+    const int64_t items = (vsplit ? 1 : 2) * static_cast<int64_t>(B) * npairs;
     if (items >= (int64_t{1} << 30)) return cudaErrorInvalidValue;
     int64_t grid = static_cast<int64_t>(num_sms()) * per_sm;
     if (grid > items) grid = items;
     quantize_kv_kernel<N, FMT, NS><<<static_cast<unsigned>(grid), threads, smem, s>>>(
-        p, static_cast<uint32_t>(items), static_cast<uint32_t>(npairs));
+        pk, static_cast<uint32_t>(items), static_cast<uint32_t>(npairs));
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (!p.sink_flags) return cudaSuccess;

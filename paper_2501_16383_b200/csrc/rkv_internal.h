@@ -22,6 +22,7 @@ struct Options {
     std::atomic<int> simt_p{0};        // CUDA-core kernel: token pairs per tile (0 = planner)
     std::atomic<int> simt_stages{0};   // CUDA-core kernel: TMA ring depth (0 = planner)
     std::atomic<int> quant_stages{1};  // quantize kernel: TMA stage buffers (1 or 2)
+    std::atomic<int> quant_vsplit{1};  // quantize: V on the warp-independent kernel
     std::atomic<int> epoch{0};
 };
 Options& options();
@@ -49,6 +50,7 @@ struct QuantParams {
     float k_norm;  // 1.0f / sqrtf(float(G*d))   (proj/src/hadamard.cpp:62)
     float v_norm;  // 1.0f / sqrtf(float(d))
     rkv_cache cache;
+    int k_only;    // quantize_kv_kernel: K items only (V runs on quantize_v_kernel)
 };
 
 struct DecodeParams {

@@ -96,6 +96,7 @@ extern "C" rkv_status rkv_set_debug_option(const char* name, int64_t value) {
     else if (n == "simt_pairs") slot = &o.simt_p;
     else if (n == "simt_stages") slot = &o.simt_stages;
     else if (n == "quant_stages") slot = &o.quant_stages;
+    else if (n == "quant_vsplit") slot = &o.quant_vsplit;
     if (!slot) return RKV_ERR_INVALID_ARGUMENT;
     slot->store(static_cast<int>(value));
     o.epoch.fetch_add(1);

@@ -16,6 +16,8 @@ from paper_2501_16383_b200 import workload as WL  # noqa: E402
 
 if len(sys.argv) > 1 and hasattr(P, "set_debug_option"):
     P.set_debug_option("quant_stages", int(sys.argv[1]))
+if len(sys.argv) > 2:
+    P.set_debug_option("quant_vsplit", int(sys.argv[2]))
 B, T = 128, 2048
 w = WL.CONFIGS[5]
 perm = WL.calibration_perm(w, 49)
@@ -37,5 +39,5 @@ for i in range(6):
     times.append(e0.elapsed_time(e1))
 ms = min(times[1:])
 rows = B * T
-print(f"quantize {B}x{T} (stages {sys.argv[1] if len(sys.argv) > 1 else 'default'}): {ms:.3f} ms "
+print(f"quantize {B}x{T} (args {sys.argv[1:]}): {ms:.3f} ms "
       f"(all: {' '.join(f'{t:.3f}' for t in times)}), {rows * 23360 / ms / 1e6:.1f} GB/s")
