@@ -353,21 +353,28 @@ __global__ void __launch_bounds__(256, 2) quantize_kv_kernel(QuantParams p, uint
 // segment); the K items (global reorder: a CTA-wide gather) stay on
 // quantize_kv_kernel.  Same arithmetic as there (fwht_region_a,
 // fwht_unit_b<128>, quantize_run): bit-identical codes.
-constexpr int kVSeg = 1024;                       // channels per warp segment (32 regions)
-constexpr int kVWarps = 12;                       // warps per CTA (1 CTA per SM)
-constexpr int kVRowF2 = (kVSeg / 32) * 33;        // float2 per segment row (padded regions)
-constexpr int kVWarpBytes = 2 * 2 * kVSeg * 2 + kVRowF2 * 8;  // 2 stages x 2 tokens fp16 + row
-template <int FMT>
-__global__ void __launch_bounds__(32 * kVWarps, 1) quantize_v_kernel(QuantParams p, uint32_t subitems, uint32_t npairs,
-                                                                    uint32_t nseg) {
+constexpr int kVSeg = 1024;                 // channels per warp segment (32 regions)
+constexpr int kVRowF2 = (kVSeg / 32) * 33;  // float2 per segment row (padded regions)
+// warps per CTA (1 CTA per SM) and TMA stages per warp: VS = 2 gives each
+// copy a whole sub-item of lead time; VS = 1 trades it for occupancy
+template <int VW, int VS>
+struct VCfg {
+    static constexpr int warps = VW, stages = VS;
+    static constexpr int warp_bytes = VS * 2 * kVSeg * 2 + kVRowF2 * 8;
+};
+template <int FMT, int VW, int VS>
+__global__ void __launch_bounds__(32 * VW, 1) quantize_v_kernel(QuantParams p, uint32_t subitems, uint32_t npairs,
+                                                               uint32_t nseg) {
+    constexpr int kVWarps = VW;
+    constexpr int kVWarpBytes = VCfg<VW, VS>::warp_bytes;
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint64_t bar[kVWarps][2];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int C = p.C, W = C / 16, MG = C / kQuantGroup;
     const int num_new = static_cast<int>(p.num_new);
     uint8_t* base = smem + warp * kVWarpBytes;
-    uint16_t* stage = reinterpret_cast<uint16_t*>(base);                 // [2][2][kVSeg]
-    float2* row = reinterpret_cast<float2*>(base + 2 * 2 * kVSeg * 2);   // [32][33]
+    uint16_t* stage = reinterpret_cast<uint16_t*>(base);                  // [VS][2][kVSeg]
+    float2* row = reinterpret_cast<float2*>(base + VS * 2 * kVSeg * 2);   // [32][33]
     const uint32_t gw = blockIdx.x * kVWarps + warp, step = gridDim.x * kVWarps;
 
     // sub-item -> (b, i0, segment)
@@ -392,7 +399,7 @@ __global__ void __launch_bounds__(32 * kVWarps, 1) quantize_v_kernel(QuantParams
         mbar_init(&bar[warp][1], 1);
         mbar_fence_init();
         if (gw < subitems) issue(gw, 0);
-        if (gw + step < subitems) issue(gw + step, 1);
+        if (VS == 2 && gw + step < subitems) issue(gw + step, 1);
     }
     __syncwarp();
     uint32_t k = 0;
@@ -400,7 +407,7 @@ __global__ void __launch_bounds__(32 * kVWarps, 1) quantize_v_kernel(QuantParams
         int b, i0, seg;
         decode(si, b, i0, seg);
         const bool has1 = i0 + 1 < num_new;
-        const int sb = k & 1;
+        const int sb = VS == 2 ? (k & 1) : 0;
         // sidecar slots of the pair's tokens (quantize_kv_kernel's rule, same inputs)
         int slot = -1;
         if (lane < 2) {
@@ -416,12 +423,12 @@ __global__ void __launch_bounds__(32 * kVWarps, 1) quantize_v_kernel(QuantParams
         }
         const int slot0 = __shfl_sync(0xffffffffu, slot, 0), slot1 = __shfl_sync(0xffffffffu, slot, 1);
         const int64_t pos0 = p.start_pos[b] + i0;
-        mbar_wait(&bar[warp][sb], (k >> 1) & 1u);
+        mbar_wait(&bar[warp][sb], VS == 2 ? (k >> 1) & 1u : k & 1u);
         const uint16_t* st = stage + sb * 2 * kVSeg;
         fwht_region_a(st, has1 ? st + kVSeg : st, row, lane);
         __syncwarp();
         // the stage is consumed: refill it with the sub-item after next
-        if (lane == 0 && si + 2 * step < subitems) issue(si + 2 * step, sb);
+        if (lane == 0 && si + VS * step < subitems) issue(si + VS * step, sb);
         fwht_unit_b<128>(row, lane / 4, lane % 4, p.v_norm);
         __syncwarp();
         float2 x[32];
@@ -554,15 +561,23 @@ cudaError_t launch_quantize_ns(const QuantParams& p, int B, cudaStream_t s) {
     // V on the warp-independent kernel when the row splits into 1024-channel segments
     const bool vsplit = p.C % kVSeg == 0 && options().quant_vsplit.load() != 0;
     if (vsplit) {
-        const size_t vsmem = static_cast<size_t>(kVWarps) * kVWarpBytes;
-        cudaError_t e = ensure_smem_k(quantize_v_kernel<FMT>, vsmem);
-        if (e != cudaSuccess) return e;
         const int64_t nseg = p.C / kVSeg, sub = static_cast<int64_t>(B) * npairs * nseg;
         if (sub >= (int64_t{1} << 31)) return cudaErrorInvalidValue;
-        const int64_t vgrid = std::min<int64_t>(num_sms(), (sub + kVWarps - 1) / kVWarps);
-        quantize_v_kernel<FMT><<<static_cast<unsigned>(vgrid), 32 * kVWarps, vsmem, s>>>(
-            p, static_cast<uint32_t>(sub), static_cast<uint32_t>(npairs), static_cast<uint32_t>(nseg));
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        auto launch_v = [&](auto kern, int vw, size_t wb) -> cudaError_t {
+            const size_t vsmem = static_cast<size_t>(vw) * wb;
+            cudaError_t e = ensure_smem_k(kern, vsmem);
+            if (e != cudaSuccess) return e;
+            const int64_t vgrid = std::min<int64_t>(num_sms(), (sub + vw - 1) / vw);
+            kern<<<static_cast<unsigned>(vgrid), 32 * vw, vsmem, s>>>(p, static_cast<uint32_t>(sub),
+                                                                       static_cast<uint32_t>(npairs),
+                                                                       static_cast<uint32_t>(nseg));
+            return cudaGetLastError();
+        };
+        const int vcfg = options().quant_vcfg.load();
+        cudaError_t e = vcfg == 1   ? launch_v(quantize_v_kernel<FMT, 16, 1>, 16, VCfg<16, 1>::warp_bytes)
+                        : vcfg == 2 ? launch_v(quantize_v_kernel<FMT, 14, 1>, 14, VCfg<14, 1>::warp_bytes)
+                                    : launch_v(quantize_v_kernel<FMT, 12, 2>, 12, VCfg<12, 2>::warp_bytes);
+        if (e != cudaSuccess) return e;
         pk.k_only = 1;
     }
     const int64_t items = (vsplit ? 1 : 2) * static_cast<int64_t>(B) * npairs;

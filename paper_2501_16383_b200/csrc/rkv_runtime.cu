@@ -97,6 +97,7 @@ extern "C" rkv_status rkv_set_debug_option(const char* name, int64_t value) {
     else if (n == "simt_stages") slot = &o.simt_stages;
     else if (n == "quant_stages") slot = &o.quant_stages;
     else if (n == "quant_vsplit") slot = &o.quant_vsplit;
+    else if (n == "quant_vcfg") slot = &o.quant_vcfg;
     if (!slot) return RKV_ERR_INVALID_ARGUMENT;
     slot->store(static_cast<int>(value));
     o.epoch.fetch_add(1);

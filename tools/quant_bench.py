@@ -18,6 +18,8 @@ if len(sys.argv) > 1 and hasattr(P, "set_debug_option"):
     P.set_debug_option("quant_stages", int(sys.argv[1]))
 if len(sys.argv) > 2:
     P.set_debug_option("quant_vsplit", int(sys.argv[2]))
+if len(sys.argv) > 3:
+    P.set_debug_option("quant_vcfg", int(sys.argv[3]))
 B, T = 128, 2048
 w = WL.CONFIGS[5]
 perm = WL.calibration_perm(w, 49)
