@@ -66,6 +66,9 @@ def run(cfg_id, iters=20, g=None, warm=3):
 if __name__ == "__main__":
     if os.environ.get("RKV_DECODE_KERNEL") == "simt":
         P.set_debug_option("decode_kernel_simt", 1)
+    for kv in filter(None, os.environ.get("RKV_OPT", "").split(",")):  # e.g. RKV_OPT=mha_pipe=1
+        k_, v_ = kv.split("=")
+        P.set_debug_option(k_, int(v_))
     # "2" = config 2; "2g1" = config 2's shape with G = 1
     # --profile: one warm-up and one timed launch per config (for ncu captures)
     prof = "--profile" in sys.argv
