@@ -170,14 +170,20 @@ struct Item {
 
 // item = (K or V, sequence, token pair); with k_only (V quantized by
 // quantize_v_kernel) the items are K only
+// x / d for 32-bit x, d without the integer-division sequence: the fp64
+// quotient is within one of the truth, fixed up exactly.
+__device__ __forceinline__ uint32_t udiv32(uint32_t x, uint32_t d) {
+    uint32_t q = static_cast<uint32_t>(__dmul_rz(static_cast<double>(x), __drcp_rn(static_cast<double>(d))));
+    if (static_cast<uint64_t>(q) * d > x) --q;
+    else if (static_cast<uint64_t>(q + 1) * d <= x) ++q;
+    return q;
+}
+
 __device__ __forceinline__ Item decode_item(uint32_t it, uint32_t npairs, int num_new, int k_only) {
     Item r;
     r.isv = k_only ? false : (it & 1u);
     const uint32_t rest = k_only ? it : it >> 1;
-    // rest / npairs via the fp32 reciprocal (rest < 2^30): off by at most one, fixed up
-    uint32_t b = __float2uint_rz(__uint2float_rz(rest) * __frcp_rz(__uint2float_rz(npairs)));
-    if (b * npairs > rest) --b;
-    if ((b + 1) * npairs <= rest) ++b;
+    const uint32_t b = udiv32(rest, npairs);
     r.b = static_cast<int>(b);
     r.i0 = static_cast<int>(rest - b * npairs) * 2;
     r.has1 = r.i0 + 1 < num_new;
@@ -379,10 +385,10 @@ __global__ void __launch_bounds__(32 * VW, 1) quantize_v_kernel(QuantParams p, u
 
     // sub-item -> (b, i0, segment)
     auto decode = [&](uint32_t si, int& b, int& i0, int& seg) {
-        seg = static_cast<int>(si % nseg);
-        const uint32_t pr = si / nseg;
-        b = static_cast<int>(pr / npairs);
-        i0 = static_cast<int>(pr % npairs) * 2;
+        const uint32_t pr = udiv32(si, nseg), bb = udiv32(pr, npairs);
+        seg = static_cast<int>(si - pr * nseg);
+        b = static_cast<int>(bb);
+        i0 = static_cast<int>(pr - bb * npairs) * 2;
     };
     auto issue = [&](uint32_t si, int sb) {
         int b, i0, seg;
