@@ -442,6 +442,8 @@ __global__ void __launch_bounds__(max_threads<N>(), 1) decode_split_kernel(Decod
 // owns channels 4*lane .. 4*lane+3, so H_128 is 2 register stages + 5 shuffle
 // stages and the sink dot products are warp reductions.
 __global__ void __launch_bounds__(256) decode_combine_kernel(DecodeParams p, int nw) {
+    pdl_trigger();
+    pdl_wait();  // the split kernel's partials
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // nw == 1: four (b, h) per CTA, a warp merges all partials; nw > 1 (few
     // heads, many partials): a CTA per (b, h), warp w merges the w-th range of
@@ -709,11 +711,8 @@ cudaError_t launch_decode_combine(const DecodeParams& p, int B, cudaStream_t s) 
     // few heads and many partials (small batch, long splits): one CTA per head,
     // up to 8 warps each merging a range of partials
     const int nw = heads < 2 * num_sms() ? static_cast<int>(std::min<int64_t>(8, (p.NP + 31) / 32)) : 1;
-    if (nw > 1)
-        decode_combine_kernel<<<static_cast<unsigned>(heads), 32 * nw, 0, s>>>(p, nw);
-    else
-        decode_combine_kernel<<<static_cast<unsigned>((heads + 3) / 4), 128, 0, s>>>(p, 1);
-    return cudaGetLastError();
+    if (nw > 1) return launch_pdl(decode_combine_kernel, dim3(static_cast<unsigned>(heads)), dim3(32 * nw), 0, s, p, nw);
+    return launch_pdl(decode_combine_kernel, dim3(static_cast<unsigned>((heads + 3) / 4)), dim3(128), 0, s, p, 1);
 }
 
 template <int N, int REP>

@@ -144,6 +144,14 @@ __global__ void __launch_bounds__(NGC < 0 ? kMmaMaxThreads : 320, NGC < 0 ? 1 : 
     uint32_t* mask_s = reinterpret_cast<uint32_t*>(smem + lay.mask);
 
     const int tid = threadIdx.x, NT = blockDim.x;
+    pdl_trigger();
+    // the layer plan is static: stage it while the previous kernel drains
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(p.plan + kPlanHeader);
+        uint4* dst = reinterpret_cast<uint4*>(smem + lay.plan);
+        for (int i = tid; i < 17 * W / 4; i += NT) dst[i] = __ldg(src + i);
+    }
+    pdl_wait();  // lengths, queries and the cache may come from the previous kernel
     const int warp = tid >> 5, lane = tid & 31;
     const int gam = warp % NG;
     const int b = blockIdx.y, split = blockIdx.x;
@@ -200,13 +208,9 @@ __global__ void __launch_bounds__(NGC < 0 ? kMmaMaxThreads : 320, NGC < 0 ? 1 : 
     }
 
     // ---- scatter role: word position wp = tid (NT == W for G = 4); the plan
-    // (omega + the 16 store offsets of each word position) lives in shared memory
+    // (omega + the 16 store offsets of each word position) lives in shared
+    // memory (staged before pdl_wait above)
     const uint32_t* plan_s = reinterpret_cast<const uint32_t*>(smem + lay.plan);
-    {
-        const uint4* src = reinterpret_cast<const uint4*>(p.plan + kPlanHeader);
-        uint4* dst = reinterpret_cast<uint4*>(smem + lay.plan);
-        for (int i = tid; i < 17 * W / 4; i += NT) dst[i] = __ldg(src + i);
-    }
     const uint32_t pair_bytes = static_cast<uint32_t>(C) * 4u;
 
     // B_e = 2^(10 - 2e') as fp16 exponent bits, e' = 0..4: code e' of a 16-bit lane ORed into the mantissa
@@ -536,6 +540,8 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? 2 : 1) decode_gqa_kernel(Dec
     static_assert(REP == 4, "decode_gqa_kernel: 4 q heads per KV head");
     constexpr int G = 2, N = 256, NJ = 2, TT = 8 * PW, PPT = TT / 2;
     extern __shared__ __align__(128) unsigned char smem[];
+    pdl_trigger();
+    pdl_wait();  // lengths, queries and the cache may come from the previous kernel
     const int C = p.C, W = C / 16, MG = C / 128, Hq = p.Hq, NG = C / N;
     const MmaSmem lay = gqa_smem(C, TT, p.chunk);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + lay.mbar);
@@ -1079,15 +1085,24 @@ cudaError_t launch_decode_mma(const rkv_layer_desc& d, const DecodePlan& plan, c
         if (e != cudaSuccess) return e;
         DecodeParams pp = p;
         void* args[] = {&pp};
-        e = cudaLaunchKernel(kern, dim3(plan.S, d.batch), dim3(plan.NT), args, plan.smem, s);
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(plan.S, d.batch);
+        cfg.blockDim = dim3(plan.NT);
+        cfg.dynamicSmemBytes = plan.smem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelExC(&cfg, kern, args);
         if (e != cudaSuccess) return e;
         return launch_decode_combine(p, d.batch, s);
     }
     auto kern = mha_kernel(p.C / 512, d.heads_per_group, sp);
     cudaError_t e = ensure_smem_k(kern, plan.smem);
     if (e != cudaSuccess) return e;
-    kern<<<dim3(plan.S, d.batch), plan.NT, plan.smem, s>>>(p);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = launch_pdl(kern, dim3(plan.S, d.batch), dim3(plan.NT), plan.smem, s, p)) != cudaSuccess) return e;
     return launch_decode_combine(p, d.batch, s);
 }
 

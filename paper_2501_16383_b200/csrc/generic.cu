@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(kGenThreads) quantize_generic_kernel(QuantPara
 // One split of one sequence per CTA, one token at a time.
 __global__ void __launch_bounds__(kGenThreads) decode_generic_kernel(DecodeParams p, int n, int rep) {
     extern __shared__ __align__(16) float dsm[];
+    pdl_trigger();
     const int C = p.C, W = C / 16, MG = C / kQuantGroup, Hq = p.Hq;
     float* krow = dsm;                     // [C]
     float* qr = krow + C;                  // [Hq][128] RoPE'd query x qscale x k_norm

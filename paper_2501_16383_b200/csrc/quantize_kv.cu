@@ -365,7 +365,6 @@ constexpr int kVRowF2 = (kVSeg / 32) * 33;  // float2 per segment row (padded re
 // copy a whole sub-item of lead time; VS = 1 trades it for occupancy
 template <int VW, int VS>
 struct VCfg {
-    static constexpr int warps = VW, stages = VS;
     static constexpr int warp_bytes = VS * 2 * kVSeg * 2 + kVRowF2 * 8;
 };
 template <int FMT, int VW, int VS>

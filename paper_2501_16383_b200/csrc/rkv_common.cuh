@@ -195,6 +195,15 @@ __device__ __forceinline__ GroupQuant group_params(float mn, float mx) {
     return g;
 }
 
+// Programmatic dependent launch (griddepcontrol, sm_90+).  A kernel launched
+// with cudaLaunchAttributeProgrammaticStreamSerialization may start while the
+// previous kernel in the stream drains; pdl_wait() blocks until that kernel
+// has completed and its memory is visible (a no-op without the attribute).
+// pdl_trigger() lets the NEXT kernel's CTAs launch once every CTA of this one
+// has triggered or exited.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // (cos, sin) of position pos, frequency f from section 1 of the RoPE table
 __device__ __forceinline__ float2 rope_at(const float4* t, int64_t pos, int f) {
     const float4 r = __ldg(t + (pos >> 1) * kRopeRow + f);

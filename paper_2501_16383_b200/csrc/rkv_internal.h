@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <utility>
 #include <cstdint>
 #include <vector>
 
@@ -36,6 +37,25 @@ inline cudaError_t ensure_smem_k(K* kern, size_t bytes) {
 }
 
 constexpr float kLog2eHost = 1.4426950408889634f;
+
+// Launch with programmatic stream serialization (the kernel's prologue may
+// overlap the previous kernel's tail; it must pdl_wait() before reading that
+// kernel's outputs).  Exact parameter types, like cudaLaunchKernelEx.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 struct QuantParams {
     const uint16_t* k_new;
