@@ -442,7 +442,6 @@ __global__ void __launch_bounds__(max_threads<N>(), 1) decode_split_kernel(Decod
 // owns channels 4*lane .. 4*lane+3, so H_128 is 2 register stages + 5 shuffle
 // stages and the sink dot products are warp reductions.
 __global__ void __launch_bounds__(256) decode_combine_kernel(DecodeParams p, int nw) {
-    pdl_trigger();
     pdl_wait();  // the split kernel's partials
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // nw == 1: four (b, h) per CTA, a warp merges all partials; nw > 1 (few
@@ -606,6 +605,7 @@ __global__ void __launch_bounds__(256) decode_combine_kernel(DecodeParams p, int
             x[j] = upper ? y - x[j] : x[j] + y;
         }
     }
+    pdl_trigger();  // the next kernel may launch while the combine drains
     const float inv = (L > 0.f || L != L) ? 1.0f / L : 0.f, nrm = 1.0f / sqrtf(128.0f);  // NaN L: foreign plan
     reinterpret_cast<float4*>(p.out + (static_cast<int64_t>(b) * p.Hq + h) * 128)[lane] =
         make_float4((x[0] * nrm + raw.x) * inv, (x[1] * nrm + raw.y) * inv, (x[2] * nrm + raw.z) * inv,

@@ -144,7 +144,6 @@ __global__ void __launch_bounds__(NGC < 0 ? kMmaMaxThreads : 320, NGC < 0 ? 1 : 
     uint32_t* mask_s = reinterpret_cast<uint32_t*>(smem + lay.mask);
 
     const int tid = threadIdx.x, NT = blockDim.x;
-    pdl_trigger();
     // the layer plan is static: stage it while the previous kernel drains
     {
         const uint4* src = reinterpret_cast<const uint4*>(p.plan + kPlanHeader);
@@ -479,6 +478,7 @@ __global__ void __launch_bounds__(NGC < 0 ? kMmaMaxThreads : 320, NGC < 0 ? 1 : 
         }
     }
 
+    pdl_trigger();  // the combine may launch while the last CTAs drain
     // ---- this warp's partial (m, l, o') for head gm
     const int64_t row = (static_cast<int64_t>(b) * p.NP + split) * Hq + gm;
     if ((lane & 7) == 0) {
@@ -540,7 +540,6 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? 2 : 1) decode_gqa_kernel(Dec
     static_assert(REP == 4, "decode_gqa_kernel: 4 q heads per KV head");
     constexpr int G = 2, N = 256, NJ = 2, TT = 8 * PW, PPT = TT / 2;
     extern __shared__ __align__(128) unsigned char smem[];
-    pdl_trigger();
     pdl_wait();  // lengths, queries and the cache may come from the previous kernel
     const int C = p.C, W = C / 16, MG = C / 128, Hq = p.Hq, NG = C / N;
     const MmaSmem lay = gqa_smem(C, TT, p.chunk);
@@ -920,6 +919,7 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? 2 : 1) decode_gqa_kernel(Dec
         }
     }
 
+    pdl_trigger();  // the combine may launch while the last CTAs drain
     // ---- partials: lane (g, tl) holds columns 2tl, 2tl+1 (heads r = (2tl)&3 + c, hi for tl < 2,
     // lo for tl >= 2) of channels g*16 + e and g*16 + e + 8, for both KV heads
     float lsum = l_part, zsum = zc_part;
@@ -1102,7 +1102,12 @@ cudaError_t launch_decode_mma(const rkv_layer_desc& d, const DecodePlan& plan, c
     auto kern = mha_kernel(p.C / 512, d.heads_per_group, sp);
     cudaError_t e = ensure_smem_k(kern, plan.smem);
     if (e != cudaSuccess) return e;
-    if ((e = launch_pdl(kern, dim3(plan.S, d.batch), dim3(plan.NT), plan.smem, s, p)) != cudaSuccess) return e;
+    if (options().decode_pdl.load()) {
+        if ((e = launch_pdl(kern, dim3(plan.S, d.batch), dim3(plan.NT), plan.smem, s, p)) != cudaSuccess) return e;
+    } else {
+        kern<<<dim3(plan.S, d.batch), plan.NT, plan.smem, s>>>(p);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
     return launch_decode_combine(p, d.batch, s);
 }
 

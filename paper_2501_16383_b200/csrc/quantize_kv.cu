@@ -564,7 +564,10 @@ cudaError_t launch_quantize_ns(const QuantParams& p, int B, cudaStream_t s) {
     const int64_t npairs = (p.num_new + 1) / 2;
     QuantParams pk = p;
     // V on the warp-independent kernel when the row splits into 1024-channel segments
-    const bool vsplit = p.C % kVSeg == 0 && options().quant_vsplit.load() != 0;
+    // (only when there are at least as many V segments as the V kernel has warps:
+    // a decode step's one-token append stays one launch)
+    const bool vsplit = p.C % kVSeg == 0 && options().quant_vsplit.load() != 0 &&
+                        static_cast<int64_t>(B) * npairs * (p.C / kVSeg) >= static_cast<int64_t>(num_sms()) * 12;
     if (vsplit) {
         const int64_t nseg = p.C / kVSeg, sub = static_cast<int64_t>(B) * npairs * nseg;
         if (sub >= (int64_t{1} << 31)) return cudaErrorInvalidValue;

@@ -25,6 +25,7 @@ struct Options {
     std::atomic<int> quant_stages{1};  // quantize kernel: TMA stage buffers (1 or 2)
     std::atomic<int> quant_vsplit{1};  // quantize: V on the warp-independent kernel
     std::atomic<int> quant_vcfg{0};    // V kernel shape: 0 = 12 warps x 2 stages, 1 = 16 x 1, 2 = 14 x 1
+    std::atomic<int> decode_pdl{1};    // launch the MHA decode kernel with programmatic stream serialization
     std::atomic<int> epoch{0};
 };
 Options& options();

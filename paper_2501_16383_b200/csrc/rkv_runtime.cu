@@ -98,6 +98,7 @@ extern "C" rkv_status rkv_set_debug_option(const char* name, int64_t value) {
     else if (n == "quant_stages") slot = &o.quant_stages;
     else if (n == "quant_vsplit") slot = &o.quant_vsplit;
     else if (n == "quant_vcfg") slot = &o.quant_vcfg;
+    else if (n == "decode_pdl") slot = &o.decode_pdl;
     if (!slot) return RKV_ERR_INVALID_ARGUMENT;
     slot->store(static_cast<int>(value));
     o.epoch.fetch_add(1);
