@@ -1052,18 +1052,7 @@ DecodePlan plan_decode_mma(const rkv_layer_desc& d, int64_t max_seq_len) {
     // whose CTA total is close to a whole number of waves (within 4x the minimum)
     const int slots = num_sms() * pl.per_sm;
     const int64_t max_split = std::max<int64_t>(1, (max_seq_len + 4 * pl.TT - 1) / (4 * pl.TT));
-    const int S0 = static_cast<int>(std::min<int64_t>(max_split, std::max(1, slots / d.batch)));
-    int S = S0;
-    double best = 0.0;
-    for (int cand = S0; cand <= std::min<int64_t>(max_split, 4 * S0 + 4); ++cand) {
-        const int64_t n = static_cast<int64_t>(cand) * d.batch;
-        const double eff = static_cast<double>(n) / (static_cast<double>((n + slots - 1) / slots) * slots);
-        if (eff > best + 0.02) {
-            best = eff;
-            S = cand;
-        }
-        if (best >= 0.95) break;
-    }
+    int S = choose_splits(slots, d.batch, max_split);
     if (const int o = options().dec_splits.load())  // experiment switch: splits per sequence
         if (o > 0) S = static_cast<int>(std::min<int64_t>(max_split, o));
     int64_t chunk = (max_seq_len + S - 1) / S;

@@ -11,14 +11,15 @@
 //   * quantize_generic_kernel: codes, scales and zeros are bit-identical to
 //     the specialised kernel and to the oracle (same fp32 stage order, same
 //     x 1/sqrt(n) rounding, same exact thresholds: group_params);
-//   * decode_generic_kernel: the dequantised row s*(c - z) stays fp32 (no
-//     fp16 operand rounding at all), is un-reordered (slot j -> perm[j]),
-//     inverse-rotated, RoPE'd per head and dotted with every q head of its KV
-//     head; online softmax and P.V in fp32.  It writes the same split
-//     partials as the other decode kernels, so the shared combine adds the
-//     exact sink rows and V's H_128.
-// They trade speed for generality (a CTA walks one token at a time); the
-// BASELINE configurations all run on the specialised kernels.
+//   * decode_generic_kernel: the dequantised rows s*(c - z) stay fp32 (no
+//     fp16 operand rounding at all), are un-reordered (slot j -> perm[j]),
+//     inverse-rotated, RoPE'd per head and dotted with every q head of their
+//     KV head; online softmax and P.V in fp32, a tile of up to 32 tokens per
+//     CTA step (see the kernel).  It writes the same split partials as the
+//     other decode kernels, so the shared combine adds the exact sink rows and
+//     V's H_128.
+// The quantize kernel trades speed for generality (a CTA walks one row at a
+// time); the BASELINE configurations all run on the specialised kernels.
 #include <cmath>
 
 #include "rkv_common.cuh"
@@ -129,36 +130,190 @@ __global__ void __launch_bounds__(kGenThreads) quantize_generic_kernel(QuantPara
     }
 }
 
-// One split of one sequence per CTA, one token at a time.
-__global__ void __launch_bounds__(kGenThreads) decode_generic_kernel(DecodeParams p, int n, int rep) {
-    extern __shared__ __align__(16) float dsm[];
-    pdl_trigger();
-    const int C = p.C, W = C / 16, MG = C / kQuantGroup, Hq = p.Hq;
-    float* krow = dsm;                     // [C]
-    float* qr = krow + C;                  // [Hq][128] RoPE'd query x qscale x k_norm
-    float* acc = qr + Hq * kHeadDim;       // [Hq][128] P.V (rotated V frame)
-    float* ml = acc + Hq * kHeadDim;       // [Hq][2] running (max, sum), log2 domain
-    const uint32_t* slot_ch = p.plan + kPlanHeader + W;  // generic plan: channel of slot 16 w + e at [(e/4) W + w][e%4]
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+// ---- tiled decode -----------------------------------------------------------
+// One split of one sequence per CTA, TT tokens (<= 32) per tile.  Every phase
+// is spread over the whole CTA and ends in one barrier, so a tile costs
+// log2(n)/5 + 3 barriers instead of log2(n) + 2 per token:
+//   A  dequantise the tile's K rows (exact fp32 s*(c - z), proj/src/quant.cpp:
+//      99-107) and un-reorder them (slot j -> channel perm[j]) into a padded
+//      fp32 tile kt[TT][RS] (4 floats of padding per 32 channels);
+//   B  inverse FWHT over each n-channel unit (H is its own inverse; 1/sqrt(n)
+//      is folded into q), radix-32 passes: a thread holds one 2^nb-element
+//      column of a pass in registers;
+//   L  logits: thread pair per (KV head, token), frequency halves; RoPE on the
+//      key (proj/src/pipeline.cpp:144-152), dot with each q head of the KV
+//      head, pair sum by shuffle;
+//   S  online softmax (log2 domain) per q head over the tile;
+//   V  P.V in the rotated V frame from the packed codes: per (word, head
+//      chunk, channel part) sum_t p s c - sum_t p s z in registers, merged
+//      into the per-head accumulator once per tile (deterministic: each
+//      accumulator element has one owner).
+// Writes the same split partials (m, l, o') as the other decode kernels; the
+// shared combine adds the exact sink rows and V's H_128.
+constexpr int kTileMax = 32;
+
+__host__ __device__ inline int tile_row_stride(int C) { return C + C / 8 + 4; }  // floats; = 4 mod 8
+__device__ __forceinline__ int padc(int c) { return c + ((c >> 5) << 2); }
+constexpr int kAccStride = 136;  // per-head accumulator row (128 + 8), channel padded by 1 per 16
+
+struct TileSmem {
+    size_t kt, q, acc, lg, ml, al, kst, vst, total;
+};
+__host__ __device__ inline TileSmem tile_smem(int C, int Hq, int TT, bool reg_acc) {
+    TileSmem s{};
+    const size_t W = C / 16, MG = C / kQuantGroup;
+    s.kt = 0;
+    s.kst = s.kt + static_cast<size_t>(TT) * tile_row_stride(C) * 4;  // [TT][W] K words + [TT][W] their meta
+    s.vst = s.kst + static_cast<size_t>(TT) * W * 8;                   // [TT][W] V words + [TT][MG] meta
+    s.q = (s.vst + static_cast<size_t>(TT) * (W + MG) * 4 + 15) & ~size_t(15);
+    s.acc = s.q + static_cast<size_t>(Hq) * kHeadDim * 4;
+    s.lg = s.acc + (reg_acc ? 0 : static_cast<size_t>(Hq) * kAccStride * 4);
+    s.ml = s.lg + static_cast<size_t>(TT) * Hq * 4;
+    s.al = s.ml + static_cast<size_t>(Hq) * 8;
+    s.total = (s.al + static_cast<size_t>(Hq) * 4 + 15) & ~size_t(15);
+    return s;
+}
+
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// One radix-2^NB pass of the FWHT over bits [b0, b0 + NB) of every row
+// (b0 == 0: NB == 5, one padded 36-float block per column, float4 accesses;
+// b0 >= 5: column stride 2^b0 channels = 9 * 2^(b0-3) padded floats).  With
+// ROPE (the pass over bits 5 and 6 .. that runs last) the column then holds,
+// for its two frequencies f = c0 and c0 + 32, the (d, d + 64) pairs of every
+// head of the unit, and RoPE_t is applied before the store
+// (proj/src/pipeline.cpp:144-152).
+template <int NB, bool CONTIG, bool ROPE>
+__device__ __forceinline__ void fwht_pass(float* kt, int RS, int TT, int C, int b0, const float4* rope, int64_t t0) {
+    constexpr int M = 1 << NB;
+    const int cols = C >> NB, stride = CONTIG ? 1 : 9 << (b0 - 3);
+    for (int task = threadIdx.x; task < TT * cols; task += blockDim.x) {
+        const int t = task / cols, col = task - t * cols;
+        const int base = ((col >> b0) << (b0 + NB)) | (col & ((1 << b0) - 1));
+        float* row = kt + t * RS + padc(base);
+        float x[M];
+        if (CONTIG) {
+            const float4* r4 = reinterpret_cast<const float4*>(row);
+#pragma unroll
+            for (int j = 0; j < M / 4; ++j) {
+                const float4 v = r4[j];
+                x[4 * j] = v.x, x[4 * j + 1] = v.y, x[4 * j + 2] = v.z, x[4 * j + 3] = v.w;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < M; ++j) x[j] = row[j * stride];
+        }
+#pragma unroll
+        for (int h = 1; h < M; h <<= 1)
+#pragma unroll
+            for (int j = 0; j < M; ++j)
+                if (!(j & h)) {
+                    const float a = x[j], b = x[j + h];
+                    x[j] = a + b;
+                    x[j + h] = a - b;
+                }
+        if (ROPE) {  // j bit 0: frequency f = c0 + 32 (j & 1); bit 1: d vs d + 64; j >> 2: head
+            const int64_t pos = t0 + t;
+            const int c0 = base & 31;
+#pragma unroll
+            for (int fb = 0; fb < 2; ++fb) {
+                const float2 cs = rope_at(rope, pos, c0 + 32 * fb);
+#pragma unroll
+                for (int hh = 0; hh < M / 4; ++hh) {
+                    const float a = x[4 * hh + fb], b = x[4 * hh + 2 + fb];
+                    x[4 * hh + fb] = a * cs.x - b * cs.y;
+                    x[4 * hh + 2 + fb] = a * cs.y + b * cs.x;
+                }
+            }
+        }
+        if (CONTIG) {
+            float4* r4 = reinterpret_cast<float4*>(row);
+#pragma unroll
+            for (int j = 0; j < M / 4; ++j) r4[j] = make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < M; ++j) row[j * stride] = x[j];
+        }
+    }
+}
+
+// Inverse rotation of every n-channel unit of the tile, then RoPE: bits
+// [0, 5), then bits [10, ln) (n > 1024), then bits [5, min(ln, 10)) with RoPE
+// fused (the butterflies of different bits commute).
+__device__ __forceinline__ void fwht_rope_tile(float* kt, int RS, int TT, int C, int ln, const float4* rope,
+                                               int64_t t0) {
+    fwht_pass<5, true, false>(kt, RS, TT, C, 0, rope, t0);
+    __syncthreads();
+    if (ln > 10) {
+        switch (ln - 10) {
+            case 1: fwht_pass<1, false, false>(kt, RS, TT, C, 10, rope, t0); break;
+            case 2: fwht_pass<2, false, false>(kt, RS, TT, C, 10, rope, t0); break;
+            default: fwht_pass<3, false, false>(kt, RS, TT, C, 10, rope, t0); break;
+        }
+        __syncthreads();
+    }
+    switch (ln < 10 ? ln - 5 : 5) {
+        case 2: fwht_pass<2, false, true>(kt, RS, TT, C, 5, rope, t0); break;
+        case 3: fwht_pass<3, false, true>(kt, RS, TT, C, 5, rope, t0); break;
+        case 4: fwht_pass<4, false, true>(kt, RS, TT, C, 5, rope, t0); break;
+        default: fwht_pass<5, false, true>(kt, RS, TT, C, 5, rope, t0); break;
+    }
+    __syncthreads();
+}
+
+// Live (in range, not a sink) tokens of the tile [t0, t0 + TT) as a bit mask.
+__device__ __forceinline__ uint32_t tile_live(const uint32_t* smask, int64_t t0, int64_t t_end, int TT) {
+    const int64_t n = t_end - t0 < TT ? t_end - t0 : TT;
+    if (n <= 0) return 0u;
+    const int sh = static_cast<int>(t0 & 31);
+    uint32_t sinks = smask[t0 >> 5] >> sh;
+    if (sh != 0 && sh + n > 32) sinks |= smask[(t0 >> 5) + 1] << (32 - sh);
+    const uint32_t range = n >= 32 ? 0xffffffffu : (1u << n) - 1u;
+    return range & ~sinks;
+}
+
+// REG: every V unit has its own thread (units <= blockDim.x), whose
+// accumulators stay in registers for the whole split (no shared accumulator).
+template <int CPT, bool REG>
+__global__ void __launch_bounds__(kGenThreads, 2) decode_generic_kernel(DecodeParams p, int ln, int rep, int TT) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    const int C = p.C, W = C / 16, MG = C / kQuantGroup, Hq = p.Hq, Hkv = p.Hkv, RS = tile_row_stride(C);
+    const TileSmem lay = tile_smem(C, Hq, TT, REG);
+    float* kt = reinterpret_cast<float*>(dsm + lay.kt);    // [TT][RS] keys, natural channel order (padded)
+    float* qr = reinterpret_cast<float*>(dsm + lay.q);     // [Hq][128] RoPE'd q x qscale x k_norm
+    float* accs = reinterpret_cast<float*>(dsm + lay.acc); // [Hq][kAccStride] P.V, rotated V frame
+    float* lg = reinterpret_cast<float*>(dsm + lay.lg);    // [TT][Hq] logits, then p
+    float* ml = reinterpret_cast<float*>(dsm + lay.ml);    // [Hq][2] running (max, sum), log2 domain
+    float* al = reinterpret_cast<float*>(dsm + lay.al);    // [Hq] this tile's rescale of the running state
+    uint32_t* kst = reinterpret_cast<uint32_t*>(dsm + lay.kst);  // cp.async stage: K words, per-word meta
+    uint32_t* vst = reinterpret_cast<uint32_t*>(dsm + lay.vst);  // cp.async stage: V words, meta
+    const uint4* slot_ch = reinterpret_cast<const uint4*>(p.plan + kPlanHeader + W);  // [(e/4) W + w] -> 4 padded channels
+    const int tid = threadIdx.x, NT = blockDim.x;
     const int b = blockIdx.y, split = blockIdx.x;
     const int64_t T = p.seq_len[b];
     const int64_t tb = p.tok_begin ? p.tok_begin[b] : 0, te = p.tok_end ? (p.tok_end[b] < T ? p.tok_end[b] : T) : T;
     const int64_t t_begin = tb + static_cast<int64_t>(split) * p.chunk;
     const int64_t t_end = t_begin + p.chunk < te ? t_begin + p.chunk : te;
-    const bool bad_plan = !plan_matches(p.plan, kDecodeGeneric, n, C);
+    const bool bad_plan = !plan_matches(p.plan, kDecodeGeneric, 1 << ln, C);
     if (t_begin >= t_end || bad_plan) {
         const float fill = bad_plan ? __int_as_float(0x7fc00000) : 0.0f;
-        for (int h = threadIdx.x; h < Hq; h += blockDim.x) {
+        for (int h = tid; h < Hq; h += NT) {
             const int64_t row = (static_cast<int64_t>(b) * p.NP + split) * Hq + h;
             p.ws_ml[row * 2] = bad_plan ? fill : -INFINITY;
             p.ws_ml[row * 2 + 1] = fill;
             for (int k = 0; k < kHeadDim; ++k) p.ws_o[row * kHeadDim + k] = fill;
         }
+        pdl_trigger();
         return;
     }
     // query: RoPE at T-1 (proj/src/pipeline.cpp:144-152), x log2(e)/sqrt(d) x 1/sqrt(n)
     const float qs = p.qscale * p.k_norm;
-    for (int i = threadIdx.x; i < Hq * 64; i += blockDim.x) {
+    for (int i = tid; i < Hq * 64; i += NT) {
         const int h = i / 64, f = i % 64;
         const float a = h2f(p.q[(static_cast<int64_t>(b) * Hq + h) * kHeadDim + f]);
         const float bb = h2f(p.q[(static_cast<int64_t>(b) * Hq + h) * kHeadDim + f + 64]);
@@ -166,81 +321,212 @@ __global__ void __launch_bounds__(kGenThreads) decode_generic_kernel(DecodeParam
         qr[h * kHeadDim + f] = (a * cs.x - bb * cs.y) * qs;
         qr[h * kHeadDim + f + 64] = (a * cs.y + bb * cs.x) * qs;
     }
-    for (int i = threadIdx.x; i < Hq * kHeadDim; i += blockDim.x) acc[i] = 0.f;
-    for (int h = threadIdx.x; h < Hq; h += blockDim.x) {
+    if (!REG)
+        for (int i = tid; i < Hq * kAccStride; i += NT) accs[i] = 0.f;
+    for (int h = tid; h < Hq; h += NT) {
         ml[2 * h] = -INFINITY;
         ml[2 * h + 1] = 0.f;
     }
-    __syncthreads();
     const uint32_t* smask = p.cache.sink_mask + static_cast<int64_t>(b) * ((p.max_tokens + 31) / 32);
     const int64_t row0 = static_cast<int64_t>(b) * p.max_tokens;
-    for (int64_t t = t_begin; t < t_end; ++t) {
-        if ((smask[t >> 5] >> (t & 31)) & 1u) continue;  // sinks: exact fp16 rows, added by the combine
-        // dequantise (fp32, exact s*(c - z)) and un-reorder: slot j -> channel perm[j]
-        const uint32_t* kc = p.cache.k_codes + (row0 + t) * W;
-        const uint32_t* km = p.cache.k_meta + (row0 + t) * MG;
-        for (int w = threadIdx.x; w < W; w += blockDim.x) {
-            const uint32_t word = kc[w], m = km[w >> 3];
-            const float s = h2f(static_cast<uint16_t>(m & 0xffffu)), z = h2f(static_cast<uint16_t>(m >> 16));
+    constexpr int NPART = 16 / CPT;
+    const int nhc = (rep + 3) / 4, units = W * NPART * nhc;
+    float racc[4][CPT], rbz[4];  // REG: this thread's unit, running over the split
 #pragma unroll
-            for (int e = 0; e < 16; ++e) {
-                const float c = static_cast<float>((word >> (2 * e)) & 3u);
-                krow[slot_ch[(static_cast<size_t>(e / 4) * W + w) * 4 + e % 4]] = s * (c - z);
+    for (int r = 0; r < 4; ++r) {
+        rbz[r] = 0.f;
+#pragma unroll
+        for (int e = 0; e < CPT; ++e) racc[r][e] = 0.f;
+    }
+    // K of a tile: every thread stages exactly the (token, word) tasks it
+    // dequantises in A (its own cp.async groups, no barrier), with a private
+    // copy of the word's meta
+    auto stage_k = [&](int64_t t0) {
+        const int64_t n = t_end - t0 < TT ? t_end - t0 : TT;
+        for (int i = tid; i < TT * W; i += NT) {
+            const int t = i / W, w = i - t * W;
+            if (t >= n) break;
+            const int64_t r = row0 + t0 + t;
+            cp_async4(kst + i, p.cache.k_codes + r * W + w);
+            cp_async4(kst + TT * W + i, p.cache.k_meta + r * MG + (w >> 3));
+        }
+        cp_async_commit();
+    };
+    auto stage_v = [&](int64_t t0) {  // read in V after a barrier
+        const int64_t n = t_end - t0 < TT ? t_end - t0 : TT;
+        for (int i = tid; i < n * W; i += NT) cp_async4(vst + i, p.cache.v_codes + (row0 + t0) * W + i);
+        for (int i = tid; i < n * MG; i += NT) cp_async4(vst + TT * W + i, p.cache.v_meta + (row0 + t0) * MG + i);
+        cp_async_commit();
+    };
+    stage_k(t_begin);
+    for (int64_t t0 = t_begin; t0 < t_end; t0 += TT) {
+        const uint32_t live = tile_live(smask, t0, t_end, TT);
+        // A: dequantise + un-reorder the tile's keys
+        cp_async_wait<0>();
+        for (int i = tid; i < TT * W; i += NT) {
+            const int t = i / W, w = i - t * W;
+            if (!((live >> t) & 1u)) continue;
+            const uint32_t word = kst[i], m = kst[TT * W + i];
+            const float s = h2f(static_cast<uint16_t>(m & 0xffffu)), z = h2f(static_cast<uint16_t>(m >> 16));
+            float* row = kt + t * RS;
+#pragma unroll
+            for (int e4 = 0; e4 < 4; ++e4) {
+                const uint4 ch = __ldg(slot_ch + e4 * W + w);
+                const uint32_t c4[4] = {ch.x, ch.y, ch.z, ch.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float c = static_cast<float>((word >> (2 * (4 * e4 + e))) & 3u);
+                    row[c4[e]] = s * (c - z);
+                }
             }
         }
         __syncthreads();
-        fwht_row(krow, C, n);  // inverse rotation (H is its own inverse up to 1/n; 1/sqrt(n) is in q)
-        // logits: warp per q head; RoPE the key pair (f, f + 64) at position t
-        for (int h0 = warp; h0 < Hq; h0 += 8 * nwarps) {
+        stage_v(t0);  // the previous tile's V phase is done (barrier above)
+        if (t0 + TT < t_end) stage_k(t0 + TT);
+        else cp_async_commit();  // keep the group count uniform
+        __syncthreads();
+        // B: inverse rotation of every n-channel unit, RoPE on each head
+        fwht_rope_tile(kt, RS, TT, C, ln, p.rope, t0);
+        // L: logits, four threads per (KV head, token), frequency quarter fq
+        for (int i0 = 0; i0 < Hkv * TT * 4; i0 += NT) {
+            const int i = i0 + tid, fq = i & 3, pr = i >> 2, t = pr % TT, kv = pr / TT;
+            const bool act = i < Hkv * TT * 4 && ((live >> t) & 1u);
+            float4 ka[4], kb[4];
+            if (act) {
+                const float* row = kt + t * RS + kv * (kHeadDim + kHeadDim / 8);
 #pragma unroll
-            for (int r = 0; r < 8; ++r) {
-                const int h = h0 + r * nwarps;
-                if (h >= Hq) continue;
-                const int kv = h / rep;
+                for (int j = 0; j < 4; ++j) {
+                    ka[j] = *reinterpret_cast<const float4*>(row + padc(16 * fq + 4 * j));
+                    kb[j] = *reinterpret_cast<const float4*>(row + padc(64 + 16 * fq + 4 * j));
+                }
+            }
+            for (int r = 0; r < rep; ++r) {
+                const int h = kv * rep + r;
                 float part = 0.f;
+                if (act) {
+                    const float4* qa = reinterpret_cast<const float4*>(qr + h * kHeadDim + 16 * fq);
+                    const float4* qb = reinterpret_cast<const float4*>(qr + h * kHeadDim + 64 + 16 * fq);
+                    float s4[4];
 #pragma unroll
-                for (int k = 0; k < 2; ++k) {
-                    const int f = lane + 32 * k;
-                    const float ka = krow[kv * kHeadDim + f], kb = krow[kv * kHeadDim + f + 64];
-                    const float2 cs = rope_at(p.rope, t, f);
-                    part += qr[h * kHeadDim + f] * (ka * cs.x - kb * cs.y) +
-                            qr[h * kHeadDim + f + 64] * (ka * cs.y + kb * cs.x);
+                    for (int j = 0; j < 4; ++j) {  // four independent chains
+                        const float4 x = qa[j], y = qb[j];
+                        float s = x.x * ka[j].x;
+                        s = fmaf(x.y, ka[j].y, s);
+                        s = fmaf(x.z, ka[j].z, s);
+                        s = fmaf(x.w, ka[j].w, s);
+                        s = fmaf(y.x, kb[j].x, s);
+                        s = fmaf(y.y, kb[j].y, s);
+                        s = fmaf(y.z, kb[j].z, s);
+                        s4[j] = fmaf(y.w, kb[j].w, s);
+                    }
+                    part = (s4[0] + s4[1]) + (s4[2] + s4[3]);
                 }
-#pragma unroll
-                for (int o = 16; o >= 1; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-                // online softmax (log2 domain); every lane holds the same values
-                const float m_old = ml[2 * h], m_new = fmaxf(m_old, part);
-                const float alpha = exp2f(m_old - m_new), pr = exp2f(part - m_new);
-                __syncwarp();
-                if (lane == 0) {
-                    ml[2 * h] = m_new;
-                    ml[2 * h + 1] = ml[2 * h + 1] * alpha + pr;
-                }
-                // V of the KV head, rotated frame: lane owns channels 4 lane .. 4 lane + 3
-                const uint32_t vword = p.cache.v_codes[(row0 + t) * W + kv * 8 + (lane >> 2)];
-                const uint32_t vm = p.cache.v_meta[(row0 + t) * MG + kv];
-                const float vs = h2f(static_cast<uint16_t>(vm & 0xffffu)), vz = h2f(static_cast<uint16_t>(vm >> 16));
-                float4* a4 = reinterpret_cast<float4*>(acc + h * kHeadDim) + lane;
-                float4 av = *a4;
-                const int e0 = 4 * (lane & 3);
-                const float v0 = vs * (static_cast<float>((vword >> (2 * e0)) & 3u) - vz);
-                const float v1 = vs * (static_cast<float>((vword >> (2 * e0 + 2)) & 3u) - vz);
-                const float v2 = vs * (static_cast<float>((vword >> (2 * e0 + 4)) & 3u) - vz);
-                const float v3 = vs * (static_cast<float>((vword >> (2 * e0 + 6)) & 3u) - vz);
-                av = make_float4(av.x * alpha + pr * v0, av.y * alpha + pr * v1, av.z * alpha + pr * v2,
-                                 av.w * alpha + pr * v3);
-                *a4 = av;
+                part += __shfl_xor_sync(0xffffffffu, part, 1);
+                part += __shfl_xor_sync(0xffffffffu, part, 2);
+                if (fq == 0 && i < Hkv * TT * 4) lg[t * Hq + h] = act ? part : -INFINITY;
             }
         }
-        __syncthreads();  // krow and the per-head state are rewritten by the next token
-    }
-    for (int h = warp; h < Hq; h += nwarps) {
-        const int64_t row = (static_cast<int64_t>(b) * p.NP + split) * Hq + h;
-        if (lane == 0) {
-            p.ws_ml[row * 2] = ml[2 * h];
-            p.ws_ml[row * 2 + 1] = ml[2 * h + 1];
+        __syncthreads();
+        // S: online softmax per q head over the tile
+        for (int h = tid; h < Hq; h += NT) {
+            const float mo = ml[2 * h];
+            float mt = -INFINITY;
+            for (int t = 0; t < TT; ++t) mt = fmaxf(mt, lg[t * Hq + h]);
+            const float mn = fmaxf(mo, mt);
+            float alpha = 1.f, sum = 0.f;
+            if (mn != -INFINITY) {
+                alpha = exp2f(mo - mn);
+                for (int t = 0; t < TT; ++t) {
+                    const float pv = exp2f(lg[t * Hq + h] - mn);
+                    lg[t * Hq + h] = pv;
+                    sum += pv;
+                }
+            }
+            ml[2 * h] = mn;
+            ml[2 * h + 1] = ml[2 * h + 1] * alpha + sum;
+            al[h] = alpha;
         }
-        reinterpret_cast<float4*>(p.ws_o + row * kHeadDim)[lane] = reinterpret_cast<const float4*>(acc + h * kHeadDim)[lane];
+        cp_async_wait<1>();  // this tile's V stage (the next tile's K may still be in flight)
+        __syncthreads();
+        // V: per (word, head chunk, channel part), sum over the tile in registers
+        for (int u = tid; u < units; u += NT) {
+            const int w = u % W, rest = u / W, part = rest % NPART, hc = rest / NPART;
+            const int kv = w >> 3, h0 = kv * rep + 4 * hc, nh = rep - 4 * hc < 4 ? rep - 4 * hc : 4;
+            float tacc[4][CPT], tbz[4];
+            float (&acc)[4][CPT] = REG ? racc : tacc;
+            float (&bz)[4] = REG ? rbz : tbz;
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                if (REG) {  // rescale the running sums to this tile's maximum
+                    const float a = r < nh ? al[h0 + r] : 0.f;
+                    bz[r] *= a;
+#pragma unroll
+                    for (int e = 0; e < CPT; ++e) acc[r][e] *= a;
+                } else {
+                    bz[r] = 0.f;
+#pragma unroll
+                    for (int e = 0; e < CPT; ++e) acc[r][e] = 0.f;
+                }
+            }
+            for (int t = 0; t < TT; ++t) {
+                if (!((live >> t) & 1u)) continue;
+                const uint32_t word = vst[t * W + w] >> (2 * CPT * part), m = vst[TT * W + t * MG + kv];
+                const float s = h2f(static_cast<uint16_t>(m & 0xffffu)), z = h2f(static_cast<uint16_t>(m >> 16));
+                float ps[4];
+#pragma unroll
+                for (int rr = 0; rr < 4; ++rr) {
+                    ps[rr] = rr < nh ? lg[t * Hq + h0 + rr] * s : 0.f;
+                    bz[rr] = fmaf(ps[rr], z, bz[rr]);
+                }
+#pragma unroll
+                for (int e = 0; e < CPT; ++e) {
+                    const float c = __uint_as_float(0x4B000000u | ((word >> (2 * e)) & 3u)) - 8388608.0f;
+#pragma unroll
+                    for (int rr = 0; rr < 4; ++rr) acc[rr][e] = fmaf(ps[rr], c, acc[rr][e]);
+                }
+            }
+            if (!REG) {
+#pragma unroll
+                for (int rr = 0; rr < 4; ++rr) {
+                    if (rr >= nh) break;
+                    const float a = al[h0 + rr];
+                    float* dst = accs + (h0 + rr) * kAccStride;
+#pragma unroll
+                    for (int e = 0; e < CPT; ++e) {
+                        const int ch = (w & 7) * 16 + part * CPT + e;
+                        const int ci = ch + (ch >> 4);
+                        dst[ci] = fmaf(dst[ci], a, acc[rr][e] - bz[rr]);
+                    }
+                }
+            }
+        }
+        // the next tile's A and L phases touch kt / lg only after their own
+        // barriers; V reads lg and al, rewritten two barriers later
+    }
+    __syncthreads();
+    pdl_trigger();
+    const int64_t prow = (static_cast<int64_t>(b) * p.NP + split) * Hq;
+    for (int h = tid; h < Hq; h += NT) {
+        p.ws_ml[(prow + h) * 2] = ml[2 * h];
+        p.ws_ml[(prow + h) * 2 + 1] = ml[2 * h + 1];
+    }
+    if (REG) {
+        if (tid < units) {
+            const int w = tid % W, rest = tid / W, part = rest % NPART, hc = rest / NPART;
+            const int h0 = (w >> 3) * rep + 4 * hc, nh = rep - 4 * hc < 4 ? rep - 4 * hc : 4;
+#pragma unroll
+            for (int rr = 0; rr < 4; ++rr) {
+                if (rr >= nh) break;
+                float* o = p.ws_o + (prow + h0 + rr) * kHeadDim + (w & 7) * 16 + part * CPT;
+#pragma unroll
+                for (int e = 0; e < CPT; ++e) o[e] = racc[rr][e] - rbz[rr];
+            }
+        }
+    } else {
+        for (int i = tid; i < Hq * kHeadDim; i += NT) {
+            const int h = i / kHeadDim, d = i % kHeadDim;
+            p.ws_o[(prow + h) * kHeadDim + d] = accs[h * kAccStride + d + (d >> 4)];
+        }
     }
 }
 
@@ -367,9 +653,24 @@ cudaError_t launch_quantize_generic(const rkv_layer_desc& d, const QuantParams& 
     return cudaGetLastError();
 }
 
-size_t generic_decode_smem(const rkv_layer_desc& d) {
-    const size_t C = static_cast<size_t>(d.num_kv_heads) * d.head_dim, Hq = static_cast<size_t>(d.num_q_heads);
-    return (C + 2 * Hq * kHeadDim + 2 * Hq) * sizeof(float);
+namespace {
+// channels per V-phase unit: 16 (a whole packed word) unless the CTA would
+// have idle threads, then halves down to 4
+int generic_cpt(const rkv_layer_desc& d) {
+    const int W = d.num_kv_heads * d.head_dim / 16, rep = d.num_q_heads / d.num_kv_heads;
+    const int nhc = (rep + 3) / 4;
+    int cpt = 16;
+    while (cpt > 4 && W * (16 / cpt) * nhc < kGenThreads) cpt /= 2;
+    return cpt;
+}
+bool generic_reg(const rkv_layer_desc& d) {  // every V unit has its own thread (<= 32 accumulators)
+    const int W = d.num_kv_heads * d.head_dim / 16, rep = d.num_q_heads / d.num_kv_heads, cpt = generic_cpt(d);
+    return cpt <= 8 && W * (16 / cpt) * ((rep + 3) / 4) <= kGenThreads;
+}
+}  // namespace
+
+size_t generic_decode_smem(const rkv_layer_desc& d, int TT) {
+    return tile_smem(d.num_kv_heads * d.head_dim, d.num_q_heads, TT, generic_reg(d)).total;
 }
 
 DecodePlan plan_decode_generic(const rkv_layer_desc& d, int64_t max_seq_len) {
@@ -378,15 +679,29 @@ DecodePlan plan_decode_generic(const rkv_layer_desc& d, int64_t max_seq_len) {
     pl.N = d.heads_per_group * d.head_dim;
     pl.REP = d.num_q_heads / d.num_kv_heads;
     pl.P = pl.PP = 1;
-    pl.TT = 1;
     pl.NT = kGenThreads;
-    pl.stages = 1;
-    pl.per_sm = 1;
+    pl.stages = generic_cpt(d) * (generic_reg(d) ? -1 : 1);  // the V-phase specialisation (launch_decode_generic)
     if (max_seq_len <= 0 || max_seq_len > d.max_tokens) max_seq_len = d.max_tokens;
-    pl.smem = generic_decode_smem(d);
-    const int S0 = std::max(1, 2 * num_sms() / std::max(1, d.batch));
-    const int S = static_cast<int>(std::min<int64_t>(S0, std::max<int64_t>(1, (max_seq_len + 15) / 16)));
-    pl.chunk = static_cast<int>((max_seq_len + S - 1) / S);
+    // tile: the largest of 16/8/4 tokens that leaves room for two CTAs per SM,
+    // else the largest of 32..1 that fits one
+    pl.TT = 0;
+    if (const int o = options().generic_tile.load())  // experiment switch
+        if (o >= 1 && o <= kTileMax && generic_decode_smem(d, o) <= 227u * 1024u) pl.TT = o;
+    for (int tt = 16; tt >= 4 && !pl.TT; tt /= 2)
+        if (generic_decode_smem(d, tt) + 1024 <= 227u * 1024u / 2) pl.TT = tt;
+    for (int tt = kTileMax; tt >= 1 && !pl.TT; tt /= 2)
+        if (generic_decode_smem(d, tt) <= 227u * 1024u) pl.TT = tt;
+    if (!pl.TT) pl.TT = 1;
+    pl.smem = generic_decode_smem(d, pl.TT);
+    pl.per_sm = pl.smem + 1024 <= 227u * 1024u / 2 ? 2 : 1;
+    const int slots = num_sms() * pl.per_sm;
+    const int64_t max_split = std::max<int64_t>(1, (max_seq_len + 4 * pl.TT - 1) / (4 * pl.TT));  // >= 4 tiles each
+    int S = choose_splits(slots, d.batch, max_split);
+    if (const int o = options().dec_splits.load())  // experiment switch: splits per sequence
+        if (o > 0) S = static_cast<int>(std::min<int64_t>(max_split, o));
+    int64_t chunk = (max_seq_len + S - 1) / S;
+    chunk = (chunk + pl.TT - 1) / pl.TT * pl.TT;
+    pl.chunk = static_cast<int>(chunk);
     pl.S = static_cast<int>((max_seq_len + pl.chunk - 1) / pl.chunk);
     pl.NP = pl.S;
     pl.ok = pl.smem <= 227 * 1024;
@@ -395,9 +710,24 @@ DecodePlan plan_decode_generic(const rkv_layer_desc& d, int64_t max_seq_len) {
 
 cudaError_t launch_decode_generic(const rkv_layer_desc& d, const DecodePlan& plan, const DecodeParams& p,
                                   cudaStream_t s) {
-    cudaError_t e = ensure_smem_k(decode_generic_kernel, plan.smem);
+    int ln = 0;
+    while ((1 << ln) < plan.N) ++ln;
+    const dim3 grid(plan.S, d.batch);
+    cudaError_t e;
+    auto go = [&](auto kern) {
+        cudaError_t err = ensure_smem_k(kern, plan.smem);
+        if (err != cudaSuccess) return err;
+        kern<<<grid, kGenThreads, plan.smem, s>>>(p, ln, plan.REP, plan.TT);
+        return cudaSuccess;
+    };
+    switch (plan.stages) {
+        case 16: e = go(decode_generic_kernel<16, false>); break;
+        case 8: e = go(decode_generic_kernel<8, false>); break;
+        case 4: e = go(decode_generic_kernel<4, false>); break;
+        case -8: e = go(decode_generic_kernel<8, true>); break;
+        default: e = go(decode_generic_kernel<4, true>); break;
+    }
     if (e != cudaSuccess) return e;
-    decode_generic_kernel<<<dim3(plan.S, d.batch), kGenThreads, plan.smem, s>>>(p, plan.N, plan.REP);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     return launch_decode_combine(p, d.batch, s);
 }

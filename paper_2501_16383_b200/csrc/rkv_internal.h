@@ -26,12 +26,16 @@ struct Options {
     std::atomic<int> quant_vsplit{1};  // quantize: V on the warp-independent kernel
     std::atomic<int> quant_vcfg{0};    // V kernel shape: 0 = 12 warps x 2 stages, 1 = 16 x 1, 2 = 14 x 1
     std::atomic<int> decode_pdl{1};    // launch the MHA decode kernel with programmatic stream serialization
+    std::atomic<int> generic_tile{0};  // generic decode: tokens per tile (0 = planner)
     std::atomic<int> epoch{0};
 };
 Options& options();
 int current_device();
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device, high-water mark)
 cudaError_t ensure_smem(const void* kern, size_t bytes);
+// split count per sequence: fill every resident CTA slot, preferring a count
+// whose CTA total is close to a whole number of waves
+int choose_splits(int slots, int batch, int64_t max_split);
 template <typename K>
 inline cudaError_t ensure_smem_k(K* kern, size_t bytes) {
     return ensure_smem(reinterpret_cast<const void*>(kern), bytes);
@@ -162,7 +166,7 @@ cudaError_t launch_channel_stats(const float* rows_f32, int64_t rows, int64_t C,
 // generic.cu (any power-of-two rotation size and head ratio)
 bool generic_quantize_needed(const rkv_layer_desc& d);
 cudaError_t launch_quantize_generic(const rkv_layer_desc& d, const QuantParams& p, cudaStream_t s);
-size_t generic_decode_smem(const rkv_layer_desc& d);
+size_t generic_decode_smem(const rkv_layer_desc& d, int tile_tokens = 1);
 DecodePlan plan_decode_generic(const rkv_layer_desc& d, int64_t max_seq_len);
 cudaError_t launch_decode_generic(const rkv_layer_desc& d, const DecodePlan& plan, const DecodeParams& p,
                                   cudaStream_t s);

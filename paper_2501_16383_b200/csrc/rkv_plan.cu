@@ -55,7 +55,7 @@ bool build_decode_plan(const rkv_layer_desc& d, const int32_t* perm, std::vector
     const int kind = decode_kind(d);
     const int C = d.num_kv_heads * d.head_dim, N = kind == kDecodeMma ? mma_layout_n(d) : d.heads_per_group * d.head_dim;
     const int W = C / 16;
-    if (kind == kDecodeGeneric) {  // generic kernel: identity word order, offsets = channel index perm[j]
+    if (kind == kDecodeGeneric) {  // generic kernel: identity word order, offsets = padded channel perm[j]
         out.assign(static_cast<size_t>(plan_words(W)), 0u);
         out[PH_MAGIC] = kPlanMagic;
         out[PH_VERSION] = 3;
@@ -69,7 +69,8 @@ bool build_decode_plan(const rkv_layer_desc& d, const int32_t* perm, std::vector
         for (int w = 0; w < W; ++w) {
             om[w] = static_cast<uint32_t>(w);
             for (int e = 0; e < 16; ++e)
-                addr[(static_cast<size_t>(e / 4) * W + w) * 4 + e % 4] = static_cast<uint32_t>(perm[w * 16 + e]);
+                addr[(static_cast<size_t>(e / 4) * W + w) * 4 + e % 4] = static_cast<uint32_t>(
+                    perm[w * 16 + e] + ((perm[w * 16 + e] >> 5) << 2));  // padded (generic.cu padc)
         }
         cost_out = 0;
         return true;

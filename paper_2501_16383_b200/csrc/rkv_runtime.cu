@@ -10,6 +10,7 @@
 //    (kernel, device, size high-water mark) instead of on every launch.
 //  * cached_plan(): decode plans memoised per (descriptor, max_seq_len,
 //    device, option epoch) -- the planner runs occupancy queries.
+#include <algorithm>
 #include <atomic>
 #include <cstring>
 #include <map>
@@ -63,6 +64,23 @@ cudaError_t ensure_smem(const void* kern, size_t bytes) {
     return e;
 }
 
+int choose_splits(int slots, int batch, int64_t max_split) {
+    max_split = std::max<int64_t>(1, max_split);
+    const int S0 = static_cast<int>(std::min<int64_t>(max_split, std::max(1, slots / batch)));
+    int S = S0;
+    double best = 0.0;
+    for (int cand = S0; cand <= std::min<int64_t>(max_split, 4 * S0 + 4); ++cand) {
+        const int64_t n = static_cast<int64_t>(cand) * batch;
+        const double eff = static_cast<double>(n) / (static_cast<double>((n + slots - 1) / slots) * slots);
+        if (eff > best + 0.02) {
+            best = eff;
+            S = cand;
+        }
+        if (best >= 0.95) break;
+    }
+    return S;
+}
+
 const DecodePlan& cached_plan(const rkv_layer_desc& d, int64_t max_seq_len) {
     static std::mutex mu;
     using Key = std::tuple<std::string, int64_t, int, int>;
@@ -99,6 +117,7 @@ extern "C" rkv_status rkv_set_debug_option(const char* name, int64_t value) {
     else if (n == "quant_vsplit") slot = &o.quant_vsplit;
     else if (n == "quant_vcfg") slot = &o.quant_vcfg;
     else if (n == "decode_pdl") slot = &o.decode_pdl;
+    else if (n == "generic_tile") slot = &o.generic_tile;
     if (!slot) return RKV_ERR_INVALID_ARGUMENT;
     slot->store(static_cast<int>(value));
     o.epoch.fetch_add(1);

@@ -236,6 +236,31 @@ def test_generic_shapes_vs_oracle(oracle, hq, hkv, g, T):
         assert cosine(out[b], want) > 0.99999
 
 
+@pytest.mark.parametrize("hq,hkv,g", [(32, 8, 4), (16, 16, 8)])
+def test_generic_tiles_sinks_and_splits(oracle, hq, hkv, g):
+    """The tiled generic decode over many tiles and splits: sinks on both sides
+    of 32-token mask-word boundaries (a tile's live mask spans two words), a
+    sequence with a single sink, and a length that is not a tile multiple."""
+    w = small_workload(hq, hkv, g)
+    B, T = 3, 1501
+    layer, perm = build_layer(w, B, T + 3, seed=5 + g)
+    k, v = WL.make_kv(w, 50 + g, B, T)
+    sinks = torch.zeros(B, T, dtype=torch.uint8)
+    sinks[:, 0] = 1
+    for t in (31, 32, 63, 64, 95, 1023):
+        sinks[1, t] = 1
+    sinks[2, 1500] = 1
+    layer.append(k, v, sinks)
+    got = cache_host(layer)
+    q = WL.make_q(w, 60 + g, B)
+    out = layer.decode(q).cpu().numpy()
+    for b in range(B):
+        want = oracle_decode(oracle, layer, got, b, T, q[b].cpu().numpy(), w, perm, k[b].cpu().numpy(),
+                             v[b].cpu().numpy())
+        assert rel_err(out[b], want) < 2e-4, (b, rel_err(out[b], want))
+        assert cosine(out[b], want) > 0.99999
+
+
 def test_generic_decode_matches_reference_decode_step(ref):
     """G = 8 (n = 1024) end to end against the unmodified reference's
     decode_step (e4m3 scales, identity projections)."""
