@@ -174,6 +174,15 @@ __host__ __device__ inline TileSmem tile_smem(int C, int Hq, int TT, bool reg_ac
     return s;
 }
 
+// floor(x / d) for 0 <= x < 2^17 from rcp = 1/d (d <= 2^13): the quotient's
+// fractional part is >= 0.5/d from an integer, far above the fp32 error
+__device__ __forceinline__ int fdiv(int x, float rcp) { return static_cast<int>((static_cast<float>(x) + 0.5f) * rcp); }
+// the two codes in bits [0, 4) of w as exact floats
+__device__ __forceinline__ float2 code2_f32(uint32_t w) {
+    return add2(make_float2(__uint_as_float(0x4B000000u | (w & 3u)), __uint_as_float(0x4B000000u | ((w >> 2) & 3u))),
+                make_float2(-8388608.0f, -8388608.0f));
+}
+
 __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
@@ -190,54 +199,62 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // (proj/src/pipeline.cpp:144-152).
 template <int NB, bool CONTIG, bool ROPE>
 __device__ __forceinline__ void fwht_pass(float* kt, int RS, int TT, int C, int b0, const float4* rope, int64_t t0) {
-    constexpr int M = 1 << NB;
+    constexpr int M = 1 << NB, M2 = M / 2;
     const int cols = C >> NB, stride = CONTIG ? 1 : 9 << (b0 - 3);
+    const float rcols = 1.0f / static_cast<float>(cols);
     for (int task = threadIdx.x; task < TT * cols; task += blockDim.x) {
-        const int t = task / cols, col = task - t * cols;
+        const int t = fdiv(task, rcols), col = task - t * cols;
         const int base = ((col >> b0) << (b0 + NB)) | (col & ((1 << b0) - 1));
         float* row = kt + t * RS + padc(base);
-        float x[M];
+        float2 cs0, cs1;
+        if (ROPE) {  // issued ahead of the butterflies
+            cs0 = rope_at(rope, t0 + t, base & 31);
+            cs1 = rope_at(rope, t0 + t, (base & 31) + 32);
+        }
+        float2 x[M2];  // x[i] = elements (2i, 2i + 1)
         if (CONTIG) {
             const float4* r4 = reinterpret_cast<const float4*>(row);
 #pragma unroll
             for (int j = 0; j < M / 4; ++j) {
                 const float4 v = r4[j];
-                x[4 * j] = v.x, x[4 * j + 1] = v.y, x[4 * j + 2] = v.z, x[4 * j + 3] = v.w;
+                x[2 * j] = make_float2(v.x, v.y);
+                x[2 * j + 1] = make_float2(v.z, v.w);
             }
         } else {
 #pragma unroll
-            for (int j = 0; j < M; ++j) x[j] = row[j * stride];
+            for (int i = 0; i < M2; ++i) x[i] = make_float2(row[(2 * i) * stride], row[(2 * i + 1) * stride]);
         }
 #pragma unroll
-        for (int h = 1; h < M; h <<= 1)
+        for (int i = 0; i < M2; ++i) x[i] = make_float2(x[i].x + x[i].y, x[i].x - x[i].y);  // stage h = 1
 #pragma unroll
-            for (int j = 0; j < M; ++j)
-                if (!(j & h)) {
-                    const float a = x[j], b = x[j + h];
-                    x[j] = a + b;
-                    x[j + h] = a - b;
+        for (int H = 1; H < M2; H <<= 1)  // stages h = 2H: float2 butterflies
+#pragma unroll
+            for (int i = 0; i < M2; ++i)
+                if (!(i & H)) {
+                    const float2 a = x[i], b = x[i + H];
+                    x[i] = add2(a, b);
+                    x[i + H] = sub2(a, b);
                 }
-        if (ROPE) {  // j bit 0: frequency f = c0 + 32 (j & 1); bit 1: d vs d + 64; j >> 2: head
-            const int64_t pos = t0 + t;
-            const int c0 = base & 31;
+        if (ROPE) {  // element bit 0: frequency f = c0 + 32 (j & 1); bit 1: d vs d + 64; j >> 2: head
+            const float2 c2 = make_float2(cs0.x, cs1.x), s2 = make_float2(cs0.y, cs1.y);
+            const float2 ns2 = make_float2(-cs0.y, -cs1.y);
 #pragma unroll
-            for (int fb = 0; fb < 2; ++fb) {
-                const float2 cs = rope_at(rope, pos, c0 + 32 * fb);
-#pragma unroll
-                for (int hh = 0; hh < M / 4; ++hh) {
-                    const float a = x[4 * hh + fb], b = x[4 * hh + 2 + fb];
-                    x[4 * hh + fb] = a * cs.x - b * cs.y;
-                    x[4 * hh + 2 + fb] = a * cs.y + b * cs.x;
-                }
+            for (int hh = 0; hh < M / 4; ++hh) {
+                const float2 a = x[2 * hh], bq = x[2 * hh + 1];
+                x[2 * hh] = fma2(a, c2, mul2(bq, ns2));
+                x[2 * hh + 1] = fma2(a, s2, mul2(bq, c2));
             }
         }
         if (CONTIG) {
             float4* r4 = reinterpret_cast<float4*>(row);
 #pragma unroll
-            for (int j = 0; j < M / 4; ++j) r4[j] = make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
+            for (int j = 0; j < M / 4; ++j) r4[j] = make_float4(x[2 * j].x, x[2 * j].y, x[2 * j + 1].x, x[2 * j + 1].y);
         } else {
 #pragma unroll
-            for (int j = 0; j < M; ++j) row[j * stride] = x[j];
+            for (int i = 0; i < M2; ++i) {
+                row[(2 * i) * stride] = x[i].x;
+                row[(2 * i + 1) * stride] = x[i].y;
+            }
         }
     }
 }
@@ -278,15 +295,18 @@ __device__ __forceinline__ uint32_t tile_live(const uint32_t* smask, int64_t t0,
 }
 
 // REG: every V unit has its own thread (units <= blockDim.x), whose
-// accumulators stay in registers for the whole split (no shared accumulator).
+// accumulators stay in registers for the whole split (no shared accumulator);
+// ntq > 1 token phases split a tile's tokens over that many units per
+// channel group, merged in a fixed order at the end.
 template <int CPT, bool REG>
-__global__ void __launch_bounds__(kGenThreads, 2) decode_generic_kernel(DecodeParams p, int ln, int rep, int TT) {
+__global__ void __launch_bounds__(kGenThreads, 2) decode_generic_kernel(DecodeParams p, int ln, int rep, int TT,
+                                                                      int ntq) {
     extern __shared__ __align__(16) unsigned char dsm[];
     const int C = p.C, W = C / 16, MG = C / kQuantGroup, Hq = p.Hq, Hkv = p.Hkv, RS = tile_row_stride(C);
     const TileSmem lay = tile_smem(C, Hq, TT, REG);
     float* kt = reinterpret_cast<float*>(dsm + lay.kt);    // [TT][RS] keys, natural channel order (padded)
     float* qr = reinterpret_cast<float*>(dsm + lay.q);     // [Hq][128] RoPE'd q x qscale x k_norm
-    float* accs = reinterpret_cast<float*>(dsm + lay.acc); // [Hq][kAccStride] P.V, rotated V frame
+    float* accs = reinterpret_cast<float*>(dsm + lay.acc); // [Hq][kAccStride] P.V, rotated V frame (!REG)
     float* lg = reinterpret_cast<float*>(dsm + lay.lg);    // [TT][Hq] logits, then p
     float* ml = reinterpret_cast<float*>(dsm + lay.ml);    // [Hq][2] running (max, sum), log2 domain
     float* al = reinterpret_cast<float*>(dsm + lay.al);    // [Hq] this tile's rescale of the running state
@@ -300,13 +320,13 @@ __global__ void __launch_bounds__(kGenThreads, 2) decode_generic_kernel(DecodePa
     const int64_t t_begin = tb + static_cast<int64_t>(split) * p.chunk;
     const int64_t t_end = t_begin + p.chunk < te ? t_begin + p.chunk : te;
     const bool bad_plan = !plan_matches(p.plan, kDecodeGeneric, 1 << ln, C);
+    const int64_t prow = (static_cast<int64_t>(b) * p.NP + split) * Hq;
     if (t_begin >= t_end || bad_plan) {
         const float fill = bad_plan ? __int_as_float(0x7fc00000) : 0.0f;
         for (int h = tid; h < Hq; h += NT) {
-            const int64_t row = (static_cast<int64_t>(b) * p.NP + split) * Hq + h;
-            p.ws_ml[row * 2] = bad_plan ? fill : -INFINITY;
-            p.ws_ml[row * 2 + 1] = fill;
-            for (int k = 0; k < kHeadDim; ++k) p.ws_o[row * kHeadDim + k] = fill;
+            p.ws_ml[(prow + h) * 2] = bad_plan ? fill : -INFINITY;
+            p.ws_ml[(prow + h) * 2 + 1] = fill;
+            for (int k = 0; k < kHeadDim; ++k) p.ws_o[(prow + h) * kHeadDim + k] = fill;
         }
         pdl_trigger();
         return;
@@ -329,23 +349,26 @@ __global__ void __launch_bounds__(kGenThreads, 2) decode_generic_kernel(DecodePa
     }
     const uint32_t* smask = p.cache.sink_mask + static_cast<int64_t>(b) * ((p.max_tokens + 31) / 32);
     const int64_t row0 = static_cast<int64_t>(b) * p.max_tokens;
+    const float rW = 1.0f / static_cast<float>(W);
+    const int ltt = __ffs(TT) - 1;  // TT is a power of two
     constexpr int NPART = 16 / CPT;
-    const int nhc = (rep + 3) / 4, units = W * NPART * nhc;
-    float racc[4][CPT], rbz[4];  // REG: this thread's unit, running over the split
+    const int nhc = (rep + 3) / 4, vunits = W * NPART * nhc, units = vunits * ntq;
+    const float rV = 1.0f / static_cast<float>(vunits);
+    float2 racc[4][CPT / 2];  // REG: this thread's unit, running over the split
+    float rbz[4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
         rbz[r] = 0.f;
 #pragma unroll
-        for (int e = 0; e < CPT; ++e) racc[r][e] = 0.f;
+        for (int e = 0; e < CPT / 2; ++e) racc[r][e] = make_float2(0.f, 0.f);
     }
     // K of a tile: every thread stages exactly the (token, word) tasks it
     // dequantises in A (its own cp.async groups, no barrier), with a private
     // copy of the word's meta
     auto stage_k = [&](int64_t t0) {
         const int64_t n = t_end - t0 < TT ? t_end - t0 : TT;
-        for (int i = tid; i < TT * W; i += NT) {
-            const int t = i / W, w = i - t * W;
-            if (t >= n) break;
+        for (int i = tid; i < n * W; i += NT) {
+            const int t = fdiv(i, rW), w = i - t * W;
             const int64_t r = row0 + t0 + t;
             cp_async4(kst + i, p.cache.k_codes + r * W + w);
             cp_async4(kst + TT * W + i, p.cache.k_meta + r * MG + (w >> 3));
@@ -364,33 +387,33 @@ __global__ void __launch_bounds__(kGenThreads, 2) decode_generic_kernel(DecodePa
         // A: dequantise + un-reorder the tile's keys
         cp_async_wait<0>();
         for (int i = tid; i < TT * W; i += NT) {
-            const int t = i / W, w = i - t * W;
+            const int t = fdiv(i, rW), w = i - t * W;
             if (!((live >> t) & 1u)) continue;
             const uint32_t word = kst[i], m = kst[TT * W + i];
             const float s = h2f(static_cast<uint16_t>(m & 0xffffu)), z = h2f(static_cast<uint16_t>(m >> 16));
             float* row = kt + t * RS;
+            const float2 s2 = make_float2(s, s), nz2 = make_float2(-z, -z);
 #pragma unroll
             for (int e4 = 0; e4 < 4; ++e4) {
                 const uint4 ch = __ldg(slot_ch + e4 * W + w);
-                const uint32_t c4[4] = {ch.x, ch.y, ch.z, ch.w};
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const float c = static_cast<float>((word >> (2 * (4 * e4 + e))) & 3u);
-                    row[c4[e]] = s * (c - z);
-                }
+                const float2 v0 = mul2(s2, add2(code2_f32(word >> (8 * e4)), nz2));  // exact s*(c - z)
+                const float2 v1 = mul2(s2, add2(code2_f32(word >> (8 * e4 + 4)), nz2));
+                row[ch.x] = v0.x;
+                row[ch.y] = v0.y;
+                row[ch.z] = v1.x;
+                row[ch.w] = v1.y;
             }
         }
         __syncthreads();
         stage_v(t0);  // the previous tile's V phase is done (barrier above)
         if (t0 + TT < t_end) stage_k(t0 + TT);
         else cp_async_commit();  // keep the group count uniform
-        __syncthreads();
         // B: inverse rotation of every n-channel unit, RoPE on each head
         fwht_rope_tile(kt, RS, TT, C, ln, p.rope, t0);
         // L: logits, four threads per (KV head, token), frequency quarter fq
         for (int i0 = 0; i0 < Hkv * TT * 4; i0 += NT) {
-            const int i = i0 + tid, fq = i & 3, pr = i >> 2, t = pr % TT, kv = pr / TT;
-            const bool act = i < Hkv * TT * 4 && ((live >> t) & 1u);
+            const int i = i0 + tid, fq = i & 3, pr = i >> 2, t = pr & (TT - 1), kv = pr >> ltt;
+            const bool in = i < Hkv * TT * 4, act = in && ((live >> t) & 1u);
             float4 ka[4], kb[4];
             if (act) {
                 const float* row = kt + t * RS + kv * (kHeadDim + kHeadDim / 8);
@@ -400,30 +423,41 @@ __global__ void __launch_bounds__(kGenThreads, 2) decode_generic_kernel(DecodePa
                     kb[j] = *reinterpret_cast<const float4*>(row + padc(64 + 16 * fq + 4 * j));
                 }
             }
-            for (int r = 0; r < rep; ++r) {
-                const int h = kv * rep + r;
-                float part = 0.f;
-                if (act) {
-                    const float4* qa = reinterpret_cast<const float4*>(qr + h * kHeadDim + 16 * fq);
-                    const float4* qb = reinterpret_cast<const float4*>(qr + h * kHeadDim + 64 + 16 * fq);
-                    float s4[4];
+            auto dot = [&](int h) {
+                const float4* qa = reinterpret_cast<const float4*>(qr + h * kHeadDim + 16 * fq);
+                const float4* qb = reinterpret_cast<const float4*>(qr + h * kHeadDim + 64 + 16 * fq);
+                float2 s2[4];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {  // four independent chains
-                        const float4 x = qa[j], y = qb[j];
-                        float s = x.x * ka[j].x;
-                        s = fmaf(x.y, ka[j].y, s);
-                        s = fmaf(x.z, ka[j].z, s);
-                        s = fmaf(x.w, ka[j].w, s);
-                        s = fmaf(y.x, kb[j].x, s);
-                        s = fmaf(y.y, kb[j].y, s);
-                        s = fmaf(y.z, kb[j].z, s);
-                        s4[j] = fmaf(y.w, kb[j].w, s);
-                    }
-                    part = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+                for (int j = 0; j < 4; ++j) {  // four independent float2 chains
+                    const float4 x = qa[j], y = qb[j];
+                    float2 s = mul2(make_float2(x.x, x.y), make_float2(ka[j].x, ka[j].y));
+                    s = fma2(make_float2(x.z, x.w), make_float2(ka[j].z, ka[j].w), s);
+                    s = fma2(make_float2(y.x, y.y), make_float2(kb[j].x, kb[j].y), s);
+                    s2[j] = fma2(make_float2(y.z, y.w), make_float2(kb[j].z, kb[j].w), s);
                 }
-                part += __shfl_xor_sync(0xffffffffu, part, 1);
-                part += __shfl_xor_sync(0xffffffffu, part, 2);
-                if (fq == 0 && i < Hkv * TT * 4) lg[t * Hq + h] = act ? part : -INFINITY;
+                const float2 u = add2(add2(s2[0], s2[1]), add2(s2[2], s2[3]));
+                return u.x + u.y;
+            };
+            if ((rep & 3) == 0) {  // four heads at a time, reduce-scatter over the quarter lanes
+                for (int r0 = 0; r0 < rep; r0 += 4) {
+                    float v[4];
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) v[r] = act ? dot(kv * rep + r0 + r) : 0.f;
+                    const bool hi = fq & 2, lo = fq & 1;
+                    float k0 = hi ? v[2] : v[0], k1 = hi ? v[3] : v[1];
+                    k0 += __shfl_xor_sync(0xffffffffu, hi ? v[0] : v[2], 2);
+                    k1 += __shfl_xor_sync(0xffffffffu, hi ? v[1] : v[3], 2);
+                    float kk = lo ? k1 : k0;
+                    kk += __shfl_xor_sync(0xffffffffu, lo ? k0 : k1, 1);
+                    if (in) lg[t * Hq + kv * rep + r0 + fq] = act ? kk : -INFINITY;  // lane fq: head r0 + fq
+                }
+            } else {
+                for (int r = 0; r < rep; ++r) {
+                    float part = act ? dot(kv * rep + r) : 0.f;
+                    part += __shfl_xor_sync(0xffffffffu, part, 1);
+                    part += __shfl_xor_sync(0xffffffffu, part, 2);
+                    if (fq == 0 && in) lg[t * Hq + kv * rep + r] = act ? part : -INFINITY;
+                }
             }
         }
         __syncthreads();
@@ -448,12 +482,15 @@ __global__ void __launch_bounds__(kGenThreads, 2) decode_generic_kernel(DecodePa
         }
         cp_async_wait<1>();  // this tile's V stage (the next tile's K may still be in flight)
         __syncthreads();
-        // V: per (word, head chunk, channel part), sum over the tile in registers
+        // V: per (word, channel part, head chunk, token phase), sum over the
+        // phase's tokens of the tile in registers
         for (int u = tid; u < units; u += NT) {
-            const int w = u % W, rest = u / W, part = rest % NPART, hc = rest / NPART;
+            const int tq = fdiv(u, rV), vu = u - tq * vunits;
+            const int rest = fdiv(vu, rW), w = vu - rest * W, part = rest % NPART, hc = rest / NPART;
             const int kv = w >> 3, h0 = kv * rep + 4 * hc, nh = rep - 4 * hc < 4 ? rep - 4 * hc : 4;
-            float tacc[4][CPT], tbz[4];
-            float (&acc)[4][CPT] = REG ? racc : tacc;
+            float2 tacc[4][CPT / 2];
+            float tbz[4];
+            float2 (&acc)[4][CPT / 2] = REG ? racc : tacc;
             float (&bz)[4] = REG ? rbz : tbz;
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
@@ -461,14 +498,14 @@ __global__ void __launch_bounds__(kGenThreads, 2) decode_generic_kernel(DecodePa
                     const float a = r < nh ? al[h0 + r] : 0.f;
                     bz[r] *= a;
 #pragma unroll
-                    for (int e = 0; e < CPT; ++e) acc[r][e] *= a;
+                    for (int e = 0; e < CPT / 2; ++e) acc[r][e] = mul2(acc[r][e], make_float2(a, a));
                 } else {
                     bz[r] = 0.f;
 #pragma unroll
-                    for (int e = 0; e < CPT; ++e) acc[r][e] = 0.f;
+                    for (int e = 0; e < CPT / 2; ++e) acc[r][e] = make_float2(0.f, 0.f);
                 }
             }
-            for (int t = 0; t < TT; ++t) {
+            for (int t = tq; t < TT; t += ntq) {
                 if (!((live >> t) & 1u)) continue;
                 const uint32_t word = vst[t * W + w] >> (2 * CPT * part), m = vst[TT * W + t * MG + kv];
                 const float s = h2f(static_cast<uint16_t>(m & 0xffffu)), z = h2f(static_cast<uint16_t>(m >> 16));
@@ -479,10 +516,10 @@ __global__ void __launch_bounds__(kGenThreads, 2) decode_generic_kernel(DecodePa
                     bz[rr] = fmaf(ps[rr], z, bz[rr]);
                 }
 #pragma unroll
-                for (int e = 0; e < CPT; ++e) {
-                    const float c = __uint_as_float(0x4B000000u | ((word >> (2 * e)) & 3u)) - 8388608.0f;
+                for (int e = 0; e < CPT / 2; ++e) {
+                    const float2 c = code2_f32(word >> (4 * e));
 #pragma unroll
-                    for (int rr = 0; rr < 4; ++rr) acc[rr][e] = fmaf(ps[rr], c, acc[rr][e]);
+                    for (int rr = 0; rr < 4; ++rr) acc[rr][e] = fma2(make_float2(ps[rr], ps[rr]), c, acc[rr][e]);
                 }
             }
             if (!REG) {
@@ -495,7 +532,7 @@ __global__ void __launch_bounds__(kGenThreads, 2) decode_generic_kernel(DecodePa
                     for (int e = 0; e < CPT; ++e) {
                         const int ch = (w & 7) * 16 + part * CPT + e;
                         const int ci = ch + (ch >> 4);
-                        dst[ci] = fmaf(dst[ci], a, acc[rr][e] - bz[rr]);
+                        dst[ci] = fmaf(dst[ci], a, (e & 1 ? acc[rr][e / 2].y : acc[rr][e / 2].x) - bz[rr]);
                     }
                 }
             }
@@ -505,21 +542,35 @@ __global__ void __launch_bounds__(kGenThreads, 2) decode_generic_kernel(DecodePa
     }
     __syncthreads();
     pdl_trigger();
-    const int64_t prow = (static_cast<int64_t>(b) * p.NP + split) * Hq;
     for (int h = tid; h < Hq; h += NT) {
         p.ws_ml[(prow + h) * 2] = ml[2 * h];
         p.ws_ml[(prow + h) * 2 + 1] = ml[2 * h + 1];
     }
     if (REG) {
+        // token phases: partial sums through the (now free) key tile, merged in phase order
+        float* scr = ntq > 1 ? kt : nullptr;
         if (tid < units) {
-            const int w = tid % W, rest = tid / W, part = rest % NPART, hc = rest / NPART;
+            const int tq = fdiv(tid, rV), vu = tid - tq * vunits;
+            const int rest = fdiv(vu, rW), w = vu - rest * W, part = rest % NPART, hc = rest / NPART;
             const int h0 = (w >> 3) * rep + 4 * hc, nh = rep - 4 * hc < 4 ? rep - 4 * hc : 4;
 #pragma unroll
             for (int rr = 0; rr < 4; ++rr) {
                 if (rr >= nh) break;
-                float* o = p.ws_o + (prow + h0 + rr) * kHeadDim + (w & 7) * 16 + part * CPT;
+                const int o = (h0 + rr) * kHeadDim + (w & 7) * 16 + part * CPT;
+                float* dst = scr ? scr + tq * Hq * kHeadDim + o : p.ws_o + prow * kHeadDim + o;
 #pragma unroll
-                for (int e = 0; e < CPT; ++e) o[e] = racc[rr][e] - rbz[rr];
+                for (int e = 0; e < CPT / 2; ++e) {
+                    dst[2 * e] = racc[rr][e].x - rbz[rr];
+                    dst[2 * e + 1] = racc[rr][e].y - rbz[rr];
+                }
+            }
+        }
+        if (scr) {
+            __syncthreads();
+            for (int i = tid; i < Hq * kHeadDim; i += NT) {
+                float s = scr[i];
+                for (int q = 1; q < ntq; ++q) s += scr[q * Hq * kHeadDim + i];
+                p.ws_o[prow * kHeadDim + i] = s;
             }
         }
     } else {
@@ -654,23 +705,37 @@ cudaError_t launch_quantize_generic(const rkv_layer_desc& d, const QuantParams& 
 }
 
 namespace {
-// channels per V-phase unit: 16 (a whole packed word) unless the CTA would
-// have idle threads, then halves down to 4
-int generic_cpt(const rkv_layer_desc& d) {
+// V phase: units of (packed word, channel part of CPT codes, chunk of <= 4 q
+// heads[, token phase]).  Few units (<= 128 at CPT 8): each has a thread of
+// its own and keeps its sums in registers (REG), with token phases filling the
+// CTA; otherwise units loop over the threads and merge into shared memory,
+// CPT 16 halved down to 4 while threads would idle.
+struct GenV {
+    int cpt;
+    bool reg;
+};
+GenV generic_v(const rkv_layer_desc& d) {
     const int W = d.num_kv_heads * d.head_dim / 16, rep = d.num_q_heads / d.num_kv_heads;
-    const int nhc = (rep + 3) / 4;
+    const int base = W * ((rep + 3) / 4);
+    if (2 * base <= kGenThreads) return {8, true};
     int cpt = 16;
-    while (cpt > 4 && W * (16 / cpt) * nhc < kGenThreads) cpt /= 2;
-    return cpt;
+    while (cpt > 4 && base * (16 / cpt) < kGenThreads) cpt /= 2;
+    return {cpt, false};
 }
-bool generic_reg(const rkv_layer_desc& d) {  // every V unit has its own thread (<= 32 accumulators)
-    const int W = d.num_kv_heads * d.head_dim / 16, rep = d.num_q_heads / d.num_kv_heads, cpt = generic_cpt(d);
-    return cpt <= 8 && W * (16 / cpt) * ((rep + 3) / 4) <= kGenThreads;
+int generic_ntq(const rkv_layer_desc& d, int TT) {  // token phases (REG): fill the CTA, partials fit the key tile
+    const GenV v = generic_v(d);
+    if (!v.reg) return 1;
+    const int C = d.num_kv_heads * d.head_dim, base = C / 16 * ((d.num_q_heads / d.num_kv_heads + 3) / 4) * 2;
+    int ntq = 1;
+    while (ntq < 8 && ntq * 2 <= TT && 2 * ntq * base <= kGenThreads &&
+           static_cast<size_t>(2 * ntq) * d.num_q_heads * kHeadDim <= static_cast<size_t>(TT) * tile_row_stride(C))
+        ntq *= 2;
+    return ntq;
 }
 }  // namespace
 
 size_t generic_decode_smem(const rkv_layer_desc& d, int TT) {
-    return tile_smem(d.num_kv_heads * d.head_dim, d.num_q_heads, TT, generic_reg(d)).total;
+    return tile_smem(d.num_kv_heads * d.head_dim, d.num_q_heads, TT, generic_v(d).reg).total;
 }
 
 DecodePlan plan_decode_generic(const rkv_layer_desc& d, int64_t max_seq_len) {
@@ -680,19 +745,20 @@ DecodePlan plan_decode_generic(const rkv_layer_desc& d, int64_t max_seq_len) {
     pl.REP = d.num_q_heads / d.num_kv_heads;
     pl.P = pl.PP = 1;
     pl.NT = kGenThreads;
-    pl.stages = generic_cpt(d) * (generic_reg(d) ? -1 : 1);  // the V-phase specialisation (launch_decode_generic)
+    pl.stages = generic_v(d).cpt * (generic_v(d).reg ? -1 : 1);  // the V-phase specialisation (launch_decode_generic)
     if (max_seq_len <= 0 || max_seq_len > d.max_tokens) max_seq_len = d.max_tokens;
     // tile: the largest of 16/8/4 tokens that leaves room for two CTAs per SM,
     // else the largest of 32..1 that fits one
     pl.TT = 0;
     if (const int o = options().generic_tile.load())  // experiment switch
-        if (o >= 1 && o <= kTileMax && generic_decode_smem(d, o) <= 227u * 1024u) pl.TT = o;
+        if (o >= 1 && o <= kTileMax && !(o & (o - 1)) && generic_decode_smem(d, o) <= 227u * 1024u) pl.TT = o;
     for (int tt = 16; tt >= 4 && !pl.TT; tt /= 2)
         if (generic_decode_smem(d, tt) + 1024 <= 227u * 1024u / 2) pl.TT = tt;
     for (int tt = kTileMax; tt >= 1 && !pl.TT; tt /= 2)
         if (generic_decode_smem(d, tt) <= 227u * 1024u) pl.TT = tt;
     if (!pl.TT) pl.TT = 1;
     pl.smem = generic_decode_smem(d, pl.TT);
+    pl.PP = generic_ntq(d, pl.TT);
     pl.per_sm = pl.smem + 1024 <= 227u * 1024u / 2 ? 2 : 1;
     const int slots = num_sms() * pl.per_sm;
     const int64_t max_split = std::max<int64_t>(1, (max_seq_len + 4 * pl.TT - 1) / (4 * pl.TT));  // >= 4 tiles each
@@ -717,15 +783,14 @@ cudaError_t launch_decode_generic(const rkv_layer_desc& d, const DecodePlan& pla
     auto go = [&](auto kern) {
         cudaError_t err = ensure_smem_k(kern, plan.smem);
         if (err != cudaSuccess) return err;
-        kern<<<grid, kGenThreads, plan.smem, s>>>(p, ln, plan.REP, plan.TT);
+        kern<<<grid, kGenThreads, plan.smem, s>>>(p, ln, plan.REP, plan.TT, plan.PP);
         return cudaSuccess;
     };
     switch (plan.stages) {
         case 16: e = go(decode_generic_kernel<16, false>); break;
         case 8: e = go(decode_generic_kernel<8, false>); break;
         case 4: e = go(decode_generic_kernel<4, false>); break;
-        case -8: e = go(decode_generic_kernel<8, true>); break;
-        default: e = go(decode_generic_kernel<4, true>); break;
+        default: e = go(decode_generic_kernel<8, true>); break;
     }
     if (e != cudaSuccess) return e;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
