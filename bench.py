@@ -128,7 +128,7 @@ def hbm_roofline(nbytes, ms, kernel):
 
 def source_hash():
     h = hashlib.sha256()
-    for f in ("decode_mma.cu", "decode_attention.cu", "rkv_common.cuh", "rkv_mma.cuh"):
+    for f in ("decode_mma.cu", "decode_attention.cu", "generic.cu", "rkv_common.cuh", "rkv_mma.cuh"):
         p = os.path.join(ROOT, "paper_2501_16383_b200", "csrc", f)
         if os.path.exists(p):
             h.update(open(p, "rb").read())
@@ -321,7 +321,9 @@ class DecodeWorkload:
     """`layers` independent layer caches of a decode config's rank shard,
     filled through rkv_quantize_kv with seeded inputs."""
 
-    def __init__(self, cfg_id, world, rank, dev, layers=1, extra_tokens=0):
+    def __init__(self, cfg_id, world, rank, dev, layers=1, extra_tokens=0, g=None):
+        import dataclasses
+
         import numpy as np
         import torch
 
@@ -330,6 +332,8 @@ class DecodeWorkload:
         from paper_2501_16383_b200 import workload as WL
 
         self.w = w = WL.CONFIGS[cfg_id]
+        if g is not None:  # the config's shape at another rotation size (e.g. cfg3 at the paper's G = 4)
+            self.w = w = dataclasses.replace(w, heads_per_group=g, name=f"{w.name}-g{g}")
         self.dev = dev
         start, self.B = sharding.batch_shard(w.batch, world, rank)
         seed = seed_of(cfg_id)
@@ -390,21 +394,25 @@ def max_over_ranks(vals, dev, world):
     return t.tolist()
 
 
-def bench_extra_decode(cfg_id, dev, world, rank, steps):
+def bench_extra_decode(cfg_id, dev, world, rank, steps, g=None):
     """A decode config on its rank shard: per-launch CUDA-event time and the
     HBM roofline of rkv_decode_attention (cache bytes > L2 at these shapes, or
-    layers cycled)."""
+    layers cycled).  g: the config's shape at another rotation size."""
+    import dataclasses
+
     import torch
 
     from paper_2501_16383_b200 import workload as WL
 
     w = WL.CONFIGS[cfg_id]
+    if g is not None:
+        w = dataclasses.replace(w, heads_per_group=g, name=f"{w.name}-g{g}")
     from paper_2501_16383_b200 import sharding
 
     _, b_local = sharding.batch_shard(w.batch, world, rank)
     per_layer = decode_bytes(w, b_local, w.tokens, 1)
     layers = max(1, -(-2 * L2_BYTES // per_layer))
-    wl = DecodeWorkload(cfg_id, world, rank, dev, layers=layers)
+    wl = DecodeWorkload(cfg_id, world, rank, dev, layers=layers, g=g)
     stream = torch.cuda.current_stream(dev)
     for i in range(3):
         wl.decode(i)
@@ -413,7 +421,7 @@ def bench_extra_decode(cfg_id, dev, world, rank, steps):
     res = {"workload": w.name, "sequences_per_gpu": wl.B, "layers_cycled": layers, "ms_per_step": ms,
            "tokens_per_s": w.batch / (ms / 1e3),
            "roofline": hbm_roofline(wl.bytes_per_step(), ms, "rkv_decode_attention (decode + combine)")}
-    traffic, src = traffic_for(f"cfg{cfg_id}")
+    traffic, src = traffic_for(f"cfg{cfg_id}" + (f"_g{g}" if g is not None else ""))
     res["roofline"]["traffic"] = traffic
     res["roofline"]["traffic_source"] = src
     del wl
@@ -780,6 +788,8 @@ def run_ours(args):
     extras = {}
     if not args.no_extras:
         for key, fn in (("cfg3", lambda: bench_extra_decode(3, dev, world, rank, min(args.steps, 30))),
+                        # GQA 4:1 at the paper's default rotation G = 4 (generic tiled kernel)
+                        ("cfg3_g4", lambda: bench_extra_decode(3, dev, world, rank, min(args.steps, 10), g=4)),
                         ("cfg2", (lambda: bench_cfg2_step(dev, min(args.steps, 30))) if world == 1 else None),
                         ("prefill_cfg1", (lambda: bench_prefill_cfg1(dev)) if world == 1 and rank == 0 else None),
                         ("quantize_cfg5", lambda: bench_quantize_cfg5(dev, world, rank))):

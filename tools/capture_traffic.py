@@ -1,7 +1,7 @@
 """DRAM traffic per decode launch, tied to the sources being timed.
 
 Run on the GPU box (after the same decode_sweep command ran clean):
-    python tools/capture_traffic.py [cfg ...]          (default: 4 2 3)
+    python tools/capture_traffic.py [cfg ...]          (default: 4 2 3; "3g4" = cfg3 at G = 4)
 It runs tools/decode_sweep.py --profile under ncu (dram bytes + duration of
 every decode kernel launch: the split kernel and the combine), takes the
 second (timed) rkv_decode_attention of each config, and writes
@@ -52,7 +52,7 @@ per = len(order) // len(cfgs)
 for i, c in enumerate(cfgs):
     grp = order[i * per:(i + 1) * per]
     timed = grp[per // 2:]
-    out["workloads"][f"cfg{c}"] = {"dram_bytes_per_launch": sum(x["bytes"] for x in timed),
+    out["workloads"]["cfg" + c.replace("g", "_g")] = {"dram_bytes_per_launch": sum(x["bytes"] for x in timed),
                                    "kernels": [{"kernel": x["kernel"][:80], "dram_bytes": x["bytes"],
                                                 "ns_cold": x["ns"]} for x in timed]}
 dst = os.path.join(ROOT, "profiles", "decode_traffic.json")
