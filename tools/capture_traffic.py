@@ -55,7 +55,8 @@ for i, c in enumerate(cfgs):
     out["workloads"]["cfg" + c.replace("g", "_g")] = {"dram_bytes_per_launch": sum(x["bytes"] for x in timed),
                                    "kernels": [{"kernel": x["kernel"][:80], "dram_bytes": x["bytes"],
                                                 "ns_cold": x["ns"]} for x in timed]}
-dst = os.path.join(ROOT, "profiles", "decode_traffic.json")
-with open(dst, "w") as f:
-    json.dump(out, f, indent=1)
+# profiles/ (commit it) and gpurun_out/ (the copy a remote run brings back)
+for dst in (os.path.join(ROOT, "profiles", "decode_traffic.json"), os.path.join(ROOT, "gpurun_out", "decode_traffic.json")):
+    with open(dst, "w") as f:
+        json.dump(out, f, indent=1)
 print(json.dumps(out, indent=1))
