@@ -70,7 +70,7 @@ constexpr int kMmaMaxThreads = 384;  // one warp per FWHT group: C <= 6144 at G 
 
 struct MmaSmem {
     size_t stage_bytes, kc, km, vc, vm, rope;  // offsets inside one stage
-    size_t stages, mbar, knat, plan, mask, total;
+    size_t stages, mbar, knat, plan, mask, xch, total;
 };
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -501,7 +501,16 @@ __global__ void __launch_bounds__(NGC < 0 ? kMmaMaxThreads : 320, NGC < 0 ? 1 : 
 
 // ---------------------------------------------------------------------------
 // GQA variant: G = 2 (N = 256, two KV heads per FWHT group), REP q heads per
-// KV head (BASELINE config 3: LLaMA-3-8B, 32 q / 8 KV heads).  The K side is
+// KV head (BASELINE config 3: LLaMA-3-8B, 32 q / 8 KV heads).  G = 4 (the
+// paper's default rotation) runs the same kernel on 256-channel half groups:
+// H_512 = H_2(channel bit 8) (x) H_256, so with u, v the H_256 outputs of the
+// two halves the keys are u + v (KV heads 0, 1 of the group) and u - v (heads
+// 2, 3).  RoPE and q.k are linear, so each warp dots its half's RoPE'd u (or v)
+// with the q heads of both KV heads that use it -- its "own" two (whose
+// softmax and V it runs, as for G = 2) and the partner half's two -- and the
+// two warps of a group swap the partner partial logits through shared memory
+// (one 64-thread named barrier per tile); the minus sign of u - v is folded
+// into the upper half's own queries.  The K side is
 // the same H_16 (x) H_16 chain (no outer bit: channel bit 6, the RoPE
 // partner, is F2 bit 3, i.e. the row half of the second MMA's output).  With
 // REP = 4 the P.V product is a real matrix product and runs on the tensor
@@ -527,7 +536,8 @@ __host__ __device__ inline MmaSmem gqa_smem(int C, int TT, int chunk) {
     s.knat = al16(s.mbar + kGqaNS * 8);
     s.plan = al16(s.knat + size_t(PP) * C * 4);
     s.mask = al16(s.plan + size_t(17) * W * 4);
-    s.total = al16(s.mask + size_t(chunk / 32 + 2) * 4);
+    s.xch = al16(s.mask + size_t(chunk / 32 + 2) * 4);  // G = 4: partial-logit exchange, float2 per thread
+    s.total = al16(s.xch + size_t(C / 256) * (TT / 8) * 32 * 8);
     return s;
 }
 
@@ -535,10 +545,13 @@ __host__ __device__ inline MmaSmem gqa_smem(int C, int TT, int chunk) {
 // are parked in tensor memory between the phases that use them (tcgen05.st /
 // tcgen05.ld, a few instructions per tile), so the register peak is the larger
 // phase instead of their sum and two CTAs fit on an SM.
-template <int REP, int PW, bool TM, bool SP = false>
+template <int REP, int PW, bool TM, bool SP = false, int GR = 2>
 __global__ void __launch_bounds__(32 * 4 * PW, TM ? 2 : 1) decode_gqa_kernel(DecodeParams p) {
     static_assert(REP == 4, "decode_gqa_kernel: 4 q heads per KV head");
-    constexpr int G = 2, N = 256, NJ = 2, TT = 8 * PW, PPT = TT / 2;
+    static_assert(GR == 2 || (GR == 4 && PW == 2 && TM), "decode_gqa_kernel: G = 2, or G = 4 at PW = 2 with TMEM parking");
+    constexpr int G = 2, N = 256, NJ = 2, TT = 8 * PW, PPT = TT / 2;  // G, N: KV heads / channels per warp group
+    constexpr bool X = GR == 4;  // partner-half exchange
+    constexpr uint32_t kQCols = X ? 64 : 32, kWarpCols = kQCols + 64;
     extern __shared__ __align__(128) unsigned char smem[];
     pdl_wait();  // lengths, queries and the cache may come from the previous kernel
     const int C = p.C, W = C / 16, MG = C / 128, Hq = p.Hq, NG = C / N;
@@ -599,7 +612,7 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? 2 : 1) decode_gqa_kernel(Dec
     uint32_t tq = 0;  // this warp's columns: q (32) then accumulators (64), lanes of quarter warp & 3
     if constexpr (TM) {
         umma::fence_after();
-        tq = s_tmem + ((32u * (warp & 3)) << 16) + 96u * (warp >> 2);
+        tq = s_tmem + ((32u * (warp & 3)) << 16) + kWarpCols * (warp >> 2);
     }
     if (tid == 0)
         for (int it = 0; it < kGqaNS && it < ntiles; ++it) issue_tile(it);
@@ -667,7 +680,10 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? 2 : 1) decode_gqa_kernel(Dec
     // RoPE(T-1) q of the frequency pairs (f, f+1), (f+64, f+65).  Slot sl holds
     // head r = sl ^ (g & 3): the first two reduce-scatter steps then keep / send
     // fixed slots on every lane (no selects) and leave head g & 3 in slot 0.
-    float2 QA[2][REP], QB[2][REP];
+    // X: QA/QB[.][REP + r] hold the partner half's KV head (same slot kvh), and
+    // the upper half's own heads are negated (keys u - v)
+    constexpr int NQ = X ? 2 * REP : REP;
+    float2 QA[2][NQ], QB[2][NQ];
     {
         const float4* cs = p.rope + ((T - 1) >> 1) * 128;
         const bool odd = (T - 1) & 1;
@@ -676,9 +692,11 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? 2 : 1) decode_gqa_kernel(Dec
 #pragma unroll
         for (int f1 = 0; f1 < 2; ++f1) {
 #pragma unroll
-            for (int sl = 0; sl < REP; ++sl) {
-                const int r = sl ^ (g & 3);
-                const int hq = (gam * G + kvh) * REP + r;
+            for (int sl = 0; sl < NQ; ++sl) {
+                const int r = (sl % REP) ^ (g & 3);
+                const bool other = sl >= REP;
+                const int hq = ((other ? gam ^ 1 : gam) * G + kvh) * REP + r;
+                const float sg = X && !other && (gam & 1) ? -qs : qs;
                 float a2[2], b2[2];
 #pragma unroll
                 for (int i = 0; i < 2; ++i) {
@@ -686,8 +704,8 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? 2 : 1) decode_gqa_kernel(Dec
                     const float4 r4 = __ldg(cs + f);
                     const float cT = odd ? r4.y : r4.x, sT = odd ? r4.w : r4.z;
                     const float a = h2f(qb[hq * 128 + f]), bb = h2f(qb[hq * 128 + f + 64]);
-                    a2[i] = (a * cT - bb * sT) * qs;
-                    b2[i] = (a * sT + bb * cT) * qs;
+                    a2[i] = (a * cT - bb * sT) * sg;
+                    b2[i] = (a * sT + bb * cT) * sg;
                 }
                 QA[f1][sl] = make_float2(a2[0], a2[1]);
                 QB[f1][sl] = make_float2(b2[0], b2[1]);
@@ -709,35 +727,46 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? 2 : 1) decode_gqa_kernel(Dec
     // tensor-memory parking (TM): q at columns [0, 32), accumulators [32, 96)
     auto park_q = [&]() {
         if constexpr (TM) {
-            uint32_t v[2][16];
 #pragma unroll
-            for (int f1 = 0; f1 < 2; ++f1)
+            for (int hs = 0; hs < NQ / REP; ++hs) {
+                uint32_t v[2][16];
 #pragma unroll
-                for (int r = 0; r < REP; ++r) {
-                    v[f1][4 * r] = __float_as_uint(QA[f1][r].x);
-                    v[f1][4 * r + 1] = __float_as_uint(QA[f1][r].y);
-                    v[f1][4 * r + 2] = __float_as_uint(QB[f1][r].x);
-                    v[f1][4 * r + 3] = __float_as_uint(QB[f1][r].y);
-                }
-            umma::st16(tq, v[0]);
-            umma::st16(tq + 16, v[1]);
+                for (int f1 = 0; f1 < 2; ++f1)
+#pragma unroll
+                    for (int r = 0; r < REP; ++r) {
+                        v[f1][4 * r] = __float_as_uint(QA[f1][hs * REP + r].x);
+                        v[f1][4 * r + 1] = __float_as_uint(QA[f1][hs * REP + r].y);
+                        v[f1][4 * r + 2] = __float_as_uint(QB[f1][hs * REP + r].x);
+                        v[f1][4 * r + 3] = __float_as_uint(QB[f1][hs * REP + r].y);
+                    }
+                umma::st16(tq + 32 * hs, v[0]);
+                umma::st16(tq + 32 * hs + 16, v[1]);
+            }
             umma::wait_st();
         }
     };
     auto fetch_q = [&]() {
         if constexpr (TM) {
-            uint32_t v[2][16];
-            umma::ld16(tq, v[0]);
-            umma::ld16(tq + 16, v[1]);
-            umma::wait_ld(v[0]);
-            umma::wait_ld(v[1]);
+            uint32_t v[NQ / REP][2][16];
 #pragma unroll
-            for (int f1 = 0; f1 < 2; ++f1)
+            for (int hs = 0; hs < NQ / REP; ++hs) {
+                umma::ld16(tq + 32 * hs, v[hs][0]);
+                umma::ld16(tq + 32 * hs + 16, v[hs][1]);
+            }
 #pragma unroll
-                for (int r = 0; r < REP; ++r) {
-                    QA[f1][r] = make_float2(__uint_as_float(v[f1][4 * r]), __uint_as_float(v[f1][4 * r + 1]));
-                    QB[f1][r] = make_float2(__uint_as_float(v[f1][4 * r + 2]), __uint_as_float(v[f1][4 * r + 3]));
-                }
+            for (int hs = 0; hs < NQ / REP; ++hs) {
+                umma::wait_ld(v[hs][0]);
+                umma::wait_ld(v[hs][1]);
+#pragma unroll
+                for (int f1 = 0; f1 < 2; ++f1)
+#pragma unroll
+                    for (int r = 0; r < REP; ++r) {
+                        QA[f1][hs * REP + r] =
+                            make_float2(__uint_as_float(v[hs][f1][4 * r]), __uint_as_float(v[hs][f1][4 * r + 1]));
+                        QB[f1][hs * REP + r] =
+                            make_float2(__uint_as_float(v[hs][f1][4 * r + 2]), __uint_as_float(v[hs][f1][4 * r + 3]));
+                    }
+            }
         }
     };
     auto park_acc = [&]() {
@@ -747,7 +776,7 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? 2 : 1) decode_gqa_kernel(Dec
                 uint32_t v[16];
 #pragma unroll
                 for (int i = 0; i < 16; ++i) v[i] = __float_as_uint(acc[q4 >> 1][4 * (q4 & 1) + (i >> 2)][i & 3]);
-                umma::st16(tq + 32 + 16 * q4, v);
+                umma::st16(tq + kQCols + 16 * q4, v);
             }
             umma::wait_st();
         }
@@ -756,7 +785,7 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? 2 : 1) decode_gqa_kernel(Dec
         if constexpr (TM) {
             uint32_t v[4][16];
 #pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) umma::ld16(tq + 32 + 16 * q4, v[q4]);
+            for (int q4 = 0; q4 < 4; ++q4) umma::ld16(tq + kQCols + 16 * q4, v[q4]);
 #pragma unroll
             for (int q4 = 0; q4 < 4; ++q4) {
                 umma::wait_ld(v[q4]);
@@ -777,7 +806,7 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? 2 : 1) decode_gqa_kernel(Dec
         const uint32_t* vm = reinterpret_cast<const uint32_t*>(st + lay.vm);
         const float4* rope4 = reinterpret_cast<const float4*>(st + lay.rope);
         const unsigned char* bufp = smem + lay.knat;
-        float bq[8];  // per token: the partial logit after the first two reduce-scatter steps
+        float bq[8], bo[8];  // per token: the partial logits (own / X: partner heads) after two reduce-scatter steps
 #pragma unroll
         for (int pq = 0; pq < 4; ++pq) {
             const int tp = 4 * pw + pq;  // token pair in the tile
@@ -797,9 +826,9 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? 2 : 1) decode_gqa_kernel(Dec
                 const float zero[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                 for (int jc = 0; jc < NJ; ++jc) mma16816(yf[jc], AH, bf[tk][jc][0], bf[tk][jc][1], zero);
-                float2 part[REP];
+                float2 part[NQ];
 #pragma unroll
-                for (int r = 0; r < REP; ++r) part[r] = make_float2(0.f, 0.f);
+                for (int r = 0; r < NQ; ++r) part[r] = make_float2(0.f, 0.f);
 #pragma unroll
                 for (int f1 = 0; f1 < 2; ++f1) {
                     const uint32_t h0 = pack_h2(yf[0][2 * f1], yf[0][2 * f1 + 1]);
@@ -816,33 +845,52 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? 2 : 1) decode_gqa_kernel(Dec
                     const float2 kra = fma2(cs2, a2, mul2(make_float2(-sn2.x, -sn2.y), b2));
                     const float2 krb = fma2(sn2, a2, mul2(cs2, b2));
 #pragma unroll
-                    for (int r = 0; r < REP; ++r) {
+                    for (int r = 0; r < NQ; ++r) {
                         part[r] = fma2(QA[f1][r], kra, part[r]);
                         part[r] = fma2(QB[f1][r], krb, part[r]);
                     }
                 }
                 // reduce-scatter steps 1-2 over lanes ^8 and ^4 (partners differ in g & 3,
                 // so slot s+2 / 1 of one lane is slot s / 0 of the other; see QA)
-                float pv[REP];
+                float pv[NQ];
 #pragma unroll
-                for (int r = 0; r < REP; ++r) pv[r] = part[r].x + part[r].y;
+                for (int r = 0; r < NQ; ++r) pv[r] = part[r].x + part[r].y;
                 const float a0 = pv[0] + __shfl_xor_sync(0xffffffffu, pv[2], 8);
                 const float a1 = pv[1] + __shfl_xor_sync(0xffffffffu, pv[3], 8);
                 bq[2 * pq + tk] = a0 + __shfl_xor_sync(0xffffffffu, a1, 4);
+                if constexpr (X) {
+                    const float o0 = pv[REP] + __shfl_xor_sync(0xffffffffu, pv[REP + 2], 8);
+                    const float o1 = pv[REP + 1] + __shfl_xor_sync(0xffffffffu, pv[REP + 3], 8);
+                    bo[2 * pq + tk] = o0 + __shfl_xor_sync(0xffffffffu, o1, 4);
+                }
             }
         }
         // reduce-scatter steps 3-4 over the 16 lanes of the KV head: lane keeps tokens
         // (2tl, 2tl+1) of head r = g & 3
-        float cq[4], d[2];
+        float d[2];
+        auto scatter34 = [&](const float (&in)[8], float (&out)[2]) {
+            float cq[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const float keep = bit1 ? bq[j + 4] : bq[j], send = bit1 ? bq[j] : bq[j + 4];
-            cq[j] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-        }
+            for (int j = 0; j < 4; ++j) {
+                const float keep = bit1 ? in[j + 4] : in[j], send = bit1 ? in[j] : in[j + 4];
+                cq[j] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+            }
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            const float keep = bit0 ? cq[u + 2] : cq[u], send = bit0 ? cq[u] : cq[u + 2];
-            d[u] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+            for (int u = 0; u < 2; ++u) {
+                const float keep = bit0 ? cq[u + 2] : cq[u], send = bit0 ? cq[u] : cq[u + 2];
+                out[u] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+            }
+        };
+        scatter34(bq, d);
+        if constexpr (X) {  // swap the partner half's partial logits (same lane = same head slot and tokens)
+            float dx[2];
+            scatter34(bo, dx);
+            float2* xch = reinterpret_cast<float2*>(smem + lay.xch);
+            xch[warp * 32 + lane] = make_float2(dx[0], dx[1]);
+            asm volatile("bar.sync %0, 64;" ::"r"(1 + (warp >> 1)) : "memory");  // the group's two warps
+            const float2 rx = xch[(warp ^ 1) * 32 + lane];
+            d[0] += rx.x;
+            d[1] += rx.y;
         }
         // online softmax (log2 domain) for head (kvh, g & 3) over the warp's 8 tokens
         const int64_t tw = t0 + 8 * pw;  // multiple of 8
@@ -967,16 +1015,17 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? 2 : 1) decode_gqa_kernel(Dec
 }  // namespace
 
 // MHA (one q head per KV head) with G = 4, 2 or 1 heads per rotation group
-// runs on 512-channel tiles (C a multiple of 512); GQA with G = 2 and 4 q heads
-// per KV head has its own kernel (256-channel groups, at most 4 per CTA).
+// runs on 512-channel tiles (C a multiple of 512); GQA with G = 2 or 4 and 4 q
+// heads per KV head has its own kernel (256-channel (half) groups, at most 4
+// per CTA).
 bool decode_mma_supported(int G, int REP, int C) {
     if (REP == 1 && (G == 4 || G == 2 || G == 1)) return C % 512 == 0 && C / 512 * 32 <= kMmaMaxThreads;
-    if (REP == 4 && G == 2) return C % 256 == 0 && C / 256 <= 4;
+    if (REP == 4 && (G == 2 || G == 4)) return C % (128 * G) == 0 && C / 256 <= 4;
     return false;
 }
 
 int mma_layout_n(const rkv_layer_desc& d) {
-    return d.heads_per_group == 2 && d.num_q_heads == 4 * d.num_kv_heads ? 256 : 512;
+    return (d.heads_per_group == 2 || d.heads_per_group == 4) && d.num_q_heads == 4 * d.num_kv_heads ? 256 : 512;
 }
 
 namespace {
@@ -998,7 +1047,10 @@ void* gqa_kernel_ptr() {
     return gqa_tmem() ? reinterpret_cast<void*>(decode_gqa_kernel<4, PW, true>)
                       : reinterpret_cast<void*>(decode_gqa_kernel<4, PW, false>);
 }
-void* gqa_kernel(int pw, bool sp = false) {
+void* gqa_kernel(int pw, bool sp = false, bool g4 = false) {
+    if (g4)  // G = 4: half-group pairs, PW = 2, accumulators and queries parked in tensor memory
+        return sp ? reinterpret_cast<void*>(decode_gqa_kernel<4, 2, true, true, 4>)
+                  : reinterpret_cast<void*>(decode_gqa_kernel<4, 2, true, false, 4>);
     if (sp) return reinterpret_cast<void*>(decode_gqa_kernel<4, 2, true, true>);  // partials: default shape
     switch (pw) {
         case 4: return gqa_kernel_ptr<4>();
@@ -1026,8 +1078,8 @@ DecodePlan plan_decode_mma(const rkv_layer_desc& d, int64_t max_seq_len) {
     pl.N = mma_layout_n(d);
     pl.REP = d.num_q_heads / d.num_kv_heads;
     const int NG = C / pl.N;
-    const bool gqa = pl.N == 256;
-    const int PW = gqa ? gqa_pw() : 1, PP = gqa ? 4 * PW : kPP;
+    const bool gqa = pl.N == 256, g4 = gqa && d.heads_per_group == 4;
+    const int PW = g4 ? 2 : gqa ? gqa_pw() : 1, PP = gqa ? 4 * PW : kPP;
     pl.stages = gqa ? kGqaNS : kNS;
     pl.P = PW;
     pl.PP = PP;
@@ -1041,7 +1093,7 @@ DecodePlan plan_decode_mma(const rkv_layer_desc& d, int64_t max_seq_len) {
     pl.per_sm = std::max(1, std::min(kCtasPerSm, static_cast<int>((227u * 1024u) / (pl.smem + 1024))));
     {
         int n = 0;
-        const void* kern = gqa ? gqa_kernel(PW) : reinterpret_cast<const void*>(mha_kernel(NG, d.heads_per_group));
+        const void* kern = gqa ? gqa_kernel(PW, false, g4) : reinterpret_cast<const void*>(mha_kernel(NG, d.heads_per_group));
         if (ensure_smem(kern, pl.smem) == cudaSuccess &&
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, pl.NT, pl.smem) == cudaSuccess && n > 0)
             pl.per_sm = n;
@@ -1069,7 +1121,7 @@ cudaError_t launch_decode_mma(const rkv_layer_desc& d, const DecodePlan& plan, c
     const bool sp = p.tok_begin != nullptr;
     if (plan.N == 256) {
         if (sp && plan.P != 2) return cudaErrorNotSupported;  // partials are instantiated for the default PW = 2
-        const void* kern = gqa_kernel(plan.P, sp);
+        const void* kern = gqa_kernel(plan.P, sp, d.heads_per_group == 4);
         cudaError_t e = ensure_smem(kern, plan.smem);
         if (e != cudaSuccess) return e;
         DecodeParams pp = p;

@@ -77,7 +77,8 @@ def test_layer_validation_messages(lib, kw, msg):
 def test_every_power_of_two_rotation_is_accepted(lib):
     """RotationPlan::make accepts n = G*128 up to 2^13 with G | H
     (proj/src/hadamard.cpp:18-33); so does the layer (G = 8 .. 64 run on the
-    generic kernels, as does GQA 4:1 at G = 4)."""
+    generic kernels; GQA 4:1 at G = 4 on the tensor-core GQA kernel up to 8 KV
+    heads, beyond on the generic one)."""
     for hkv, g, hq in ((8, 8, 8), (16, 16, 16), (64, 64, 64), (32, 32, 32), (16, 4, 64), (8, 4, 32), (64, 1, 64)):
         cfg(num_kv_heads=hkv, num_q_heads=hq, heads_per_group=g).validate()
 

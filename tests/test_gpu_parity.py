@@ -176,6 +176,8 @@ def oracle_decode(oracle, layer, got, b, T, q, w, perm, kraw, vraw):
     (44, 44, 4, 10000.0, 90), (48, 48, 4, 10000.0, 130), (48, 48, 1, 10000.0, 70),
     # beyond the tensor-core tiles: C = 8192 (CUDA-core kernel), GQA 4:1 at 16 KV heads
     (64, 64, 4, 10000.0, 70), (64, 16, 2, 500000.0, 70),
+    # GQA 4:1 at the paper's G = 4 on the tensor-core kernel (half-group pairs): C = 512 and 1024
+    (16, 4, 4, 500000.0, 300), (32, 8, 4, 500000.0, 1025), (32, 8, 4, 10000.0, 1),
 ])
 def test_decode_vs_oracle(oracle, hq, hkv, g, base, T):
     w = small_workload(hq, hkv, g, base=base)
@@ -199,7 +201,6 @@ def test_decode_vs_oracle(oracle, hq, hkv, g, base, T):
 
 @pytest.mark.parametrize("hq,hkv,g,T", [
     (64, 16, 4, 70),    # GQA 4:1 at the paper's default G = 4 (LLaMA-3-8B shape at G = 4)
-    (32, 8, 4, 300),
     (96, 8, 2, 70),     # 12 q heads per KV head
     (64, 64, 1, 90),    # G = 1 at C = 8192
     (16, 16, 8, 130),   # n = 1024
@@ -236,7 +237,7 @@ def test_generic_shapes_vs_oracle(oracle, hq, hkv, g, T):
         assert cosine(out[b], want) > 0.99999
 
 
-@pytest.mark.parametrize("hq,hkv,g", [(32, 8, 4), (16, 16, 8)])
+@pytest.mark.parametrize("hq,hkv,g", [(64, 16, 4), (32, 8, 4), (16, 16, 8)])
 def test_generic_tiles_sinks_and_splits(oracle, hq, hkv, g):
     """The tiled generic decode over many tiles and splits: sinks on both sides
     of 32-token mask-word boundaries (a tile's live mask spans two words), a

@@ -25,8 +25,9 @@ def rel(a, b):
 
 @pytest.mark.parametrize("hq,hkv,g,world", [(8, 8, 4, 2), (8, 8, 4, 5), (32, 8, 2, 3), (4, 4, 1, 2), (40, 40, 4, 8),
                                               (48, 48, 4, 3),
-                                              # generic (tiled) kernel: GQA 4:1 at G = 4, n = 1024
-                                              (32, 8, 4, 3), (16, 16, 8, 2)])
+                                              # GQA 4:1 at G = 4: tensor-core (C = 1024) and generic
+                                              # tiled kernel (C = 2048); n = 1024 generic
+                                              (32, 8, 4, 3), (64, 16, 4, 2), (16, 16, 8, 2)])
 def test_partials_merge_to_the_full_decode(oracle, hq, hkv, g, world):
     lens = [700, 129, 64, 1]
     B, T = len(lens), max(lens)
