@@ -10,8 +10,8 @@ costs 7-9e-4) fails loudly:
 
 Measured errors are printed (pytest -s).  Config 1 runs at its exact shape
 (B = 1, T = 4096, C = 4096, G = 4); configs 2-4 check sampled sequences of the
-full-size batch (config 3: one 8-sequence shard of 64; config 4: 2 of the 8
-32,768-token sequences).
+full-size batch (config 3: one 8-sequence shard of 64, also at G = 4; config 4:
+2 of the 8 32,768-token sequences).
 """
 import numpy as np
 import pytest
@@ -31,9 +31,17 @@ REL_GUARD = 2e-4
 COS_GUARD = 0.99999
 
 
-@pytest.mark.parametrize("cfg_id", [1, 2, 3, 4])
+@pytest.mark.parametrize("cfg_id", [1, 2, 3, 4, "3g4"])
 def test_full_size_decode_margin(oracle, cfg_id):
-    w = WL.CONFIGS[cfg_id]
+    """"3g4": config 3's shape at the paper's default rotation G = 4 (the
+    tensor-core GQA kernel's half-group pairs)."""
+    if cfg_id == "3g4":
+        import dataclasses
+
+        w = dataclasses.replace(WL.CONFIGS[3], heads_per_group=4)
+        cfg_id = 3
+    else:
+        w = WL.CONFIGS[cfg_id]
     B = {1: 1, 2: w.batch, 3: 8, 4: 2}[cfg_id]
     T = w.tokens
     layer, perm = build_layer(w, B, T + 1, seed=100 + cfg_id)
