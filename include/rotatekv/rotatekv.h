@@ -236,8 +236,8 @@ rkv_status rkv_decode_merge(const rkv_layer_desc* desc, const uint16_t* q, const
  * then a flash-attention kernel runs Q.K^T and P.V on tcgen05 (accumulators
  * in tensor memory); sinks are merged exactly in its epilogue (max_sinks
  * <= 16, else RKV_ERR_INVALID_ARGUMENT).  Layer shapes:
- * those with a tensor-core decode kernel (G = 4 with Hq == Hkv, G = 2 with
- * Hq == 4 Hkv).  Stream-ordered. */
+ * those with a tensor-core decode kernel (G = 1, 2 or 4 with Hq == Hkv; G = 2
+ * or 4 with Hq == 4 Hkv, Hkv <= 8).  Stream-ordered. */
 size_t rkv_prefill_workspace_bytes(const rkv_layer_desc* desc, int64_t num_q, int64_t max_seq_len);
 rkv_status rkv_prefill_attention(const rkv_layer_desc* desc, const uint16_t* q, int64_t num_q, const int64_t* q_start,
                                  const int64_t* seq_len, int64_t max_seq_len, const rkv_cache* cache,

@@ -63,9 +63,14 @@ __device__ __forceinline__ void store_key_pair(const PrefillParams& p, int b, in
 // CTA = (4-token tile, sequence), one warp per FWHT group.
 // G = 4: 512-channel tiles (the MHA decode layout; AG = heads per rotation
 // group, 4, 2 or 1, picks the second FWHT factor); G = 2: GQA 256-channel groups.
-template <int G, int AG = G>
+// PAIR (GQA at G = 4 on the 256-channel plan, G = 2 here): the group's two
+// half-group warps hold u, v = H_256 of their halves (RoPE'd); the keys are
+// u + v (KV heads 0, 1) and u - v (heads 2, 3) -- swapped through shared
+// memory after all four tokens, one 64-thread named barrier per warp pair.
+template <int G, int AG = G, bool PAIR = false>
 __global__ void __launch_bounds__(512) reconstruct_keys_kernel(PrefillParams p) {
     constexpr int N = 128 * G, NJ = N / 128, TT = 4;
+    static_assert(!PAIR || G == 2, "half-group pairs run on the 256-channel plan");
     extern __shared__ __align__(16) unsigned char smem[];
     const int C = p.C, W = C / 16, MG = C / 128, NG = C / N;
     const int b = blockIdx.y, tid = threadIdx.x, NT = blockDim.x, warp = tid >> 5, lane = tid & 31;
@@ -78,6 +83,7 @@ __global__ void __launch_bounds__(512) reconstruct_keys_kernel(PrefillParams p) 
     uint32_t* kcs = reinterpret_cast<uint32_t*>(smem + 2 * pair_bytes);    // [TT][W]
     uint32_t* kms = kcs + TT * W;                                           // [TT][MG]
     float4* rps = reinterpret_cast<float4*>(kms + TT * MG);                // [TT][32] RoPE frequency-pair rows
+    float4* xk = rps + TT * 32;  // PAIR: [NG warps][TT][2 f1][32 lanes] RoPE'd (ka0, ka1, kb0, kb1)
     const int64_t row0 = static_cast<int64_t>(b) * p.max_tokens + t0;
     for (int i = tid; i < TT * W; i += NT) kcs[i] = i / W < nv ? p.cache.k_codes[row0 * W + i] : 0u;
     for (int i = tid; i < TT * MG; i += NT) kms[i] = i / MG < nv ? p.cache.k_meta[row0 * MG + i] : 0u;
@@ -190,9 +196,30 @@ __global__ void __launch_bounds__(512) reconstruct_keys_kernel(PrefillParams p) 
                         ka[i] = (a * c - bb * s) * kn;
                         kb[i] = (a * s + bb * c) * kn;
                     }
-                    store_key_pair(p, b, pos, kvh, f, ka[0], ka[1]);
-                    store_key_pair(p, b, pos, kvh, f + 64, kb[0], kb[1]);
+                    if constexpr (PAIR) {
+                        xk[((warp * TT + tt) * 2 + f1) * 32 + lane] = make_float4(ka[0], ka[1], kb[0], kb[1]);
+                    } else {
+                        store_key_pair(p, b, pos, kvh, f, ka[0], ka[1]);
+                        store_key_pair(p, b, pos, kvh, f + 64, kb[0], kb[1]);
+                    }
                 }
+            }
+        }
+    }
+    if constexpr (PAIR) {  // lower half: u + v -> KV heads 0, 1; upper half: u - v -> heads 2, 3
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + (warp >> 1)) : "memory");
+        const bool upper = gam & 1;
+        const int kvh = gam * G + (g >> 2);
+        for (int tt = 0; tt < nv; ++tt) {
+#pragma unroll
+            for (int f1 = 0; f1 < 2; ++f1) {
+                const float4 own = xk[((warp * TT + tt) * 2 + f1) * 32 + lane];
+                const float4 oth = xk[(((warp ^ 1) * TT + tt) * 2 + f1) * 32 + lane];
+                const float4 k4 = upper ? make_float4(oth.x - own.x, oth.y - own.y, oth.z - own.z, oth.w - own.w)
+                                        : make_float4(own.x + oth.x, own.y + oth.y, own.z + oth.z, own.w + oth.w);
+                const int f = 2 * tl + 8 * f1 + 16 * (g & 3);
+                store_key_pair(p, b, t0 + tt, kvh, f, k4.x, k4.y);
+                store_key_pair(p, b, t0 + tt, kvh, f + 64, k4.z, k4.w);
             }
         }
     }
@@ -819,7 +846,9 @@ bool prefill_pair() { return options().prefill_pair.load() == 1; }
 cudaError_t launch_prefill(const rkv_layer_desc& d, const PrefillParams& p, int64_t max_seq_len, cudaStream_t s) {
     const int C = p.C, W = C / 16, MG = C / 128;
     const int N = mma_layout_n(d), NG = C / N;
-    const size_t ksmem = 2 * static_cast<size_t>(C) * 4 + 4 * static_cast<size_t>(W + MG) * 4 + 4 * 32 * 16;
+    const bool pair = N == 256 && d.heads_per_group == 4;
+    const size_t ksmem = 2 * static_cast<size_t>(C) * 4 + 4 * static_cast<size_t>(W + MG) * 4 + 4 * 32 * 16 +
+                         (pair ? static_cast<size_t>(NG) * 4 * 2 * 32 * 16 : 0);
     const int nthreads = std::min(512, std::max(NG * 32, ((2 * W + 31) / 32) * 32));
     const dim3 kgrid(static_cast<unsigned>((max_seq_len + 3) / 4), static_cast<unsigned>(d.batch));
     cudaError_t e;
@@ -829,6 +858,9 @@ cudaError_t launch_prefill(const rkv_layer_desc& d, const PrefillParams& p, int6
                                              : reconstruct_keys_kernel<4, 4>;
         if ((e = ensure_smem_k(kern, ksmem)) != cudaSuccess) return e;
         kern<<<kgrid, nthreads, ksmem, s>>>(p);
+    } else if (N == 256 && pair) {  // GQA at G = 4: half-group pairs
+        if ((e = ensure_smem_k(reconstruct_keys_kernel<2, 2, true>, ksmem)) != cudaSuccess) return e;
+        reconstruct_keys_kernel<2, 2, true><<<kgrid, nthreads, ksmem, s>>>(p);
     } else if (N == 256) {
         if ((e = ensure_smem_k(reconstruct_keys_kernel<2>, ksmem)) != cudaSuccess) return e;
         reconstruct_keys_kernel<2><<<kgrid, nthreads, ksmem, s>>>(p);
