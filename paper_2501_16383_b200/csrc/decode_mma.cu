@@ -66,7 +66,7 @@ namespace {
 
 using namespace mma;
 
-constexpr int kMmaMaxThreads = 384;  // one warp per FWHT group: C <= 6144 at G = 4
+constexpr int kMmaMaxThreads = 512;  // one warp per FWHT group: C <= 8192 at G = 4
 
 struct MmaSmem {
     size_t stage_bytes, kc, km, vc, vm, rope;  // offsets inside one stage
@@ -103,7 +103,7 @@ constexpr int kPP = 2, kTT = 2 * kPP, kNS = 3, kCtasPerSm = 2;
 // (C / 512) when known at compile time (8: LLaMA-2-7B, 10: 13B), so every
 // shared-memory offset folds into an immediate; 0 = taken from the launch
 // (<= 10 groups: 320 threads, two CTAs per SM); -1 = taken from the launch,
-// 11 or 12 groups (384 threads, one CTA per SM).
+// 11 .. 16 groups (up to 512 threads, one CTA per SM).
 // AG = heads per rotation group of the layer (4, 2 or 1): the kernel always
 // works on 512-channel (pseudo-)groups; only the second FWHT factor differs
 // (hadamard_f2_frag) -- the head bits 7, 8 pass through it when AG < 4.

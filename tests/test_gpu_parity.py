@@ -174,8 +174,8 @@ def oracle_decode(oracle, layer, got, b, T, q, w, perm, kraw, vraw):
     (8, 8, 1, 10000.0, 300), (40, 40, 1, 10000.0, 513), (40, 40, 2, 10000.0, 257), (32, 32, 1, 500000.0, 1024),
     # the widest tensor-core tiles: 11 and 12 FWHT groups per CTA (C = 5632, 6144)
     (44, 44, 4, 10000.0, 90), (48, 48, 4, 10000.0, 130), (48, 48, 1, 10000.0, 70),
-    # beyond the tensor-core tiles: C = 8192 (CUDA-core kernel), GQA 4:1 at 16 KV heads
-    (64, 64, 4, 10000.0, 70), (64, 16, 2, 500000.0, 70),
+    # C = 8192 (16 FWHT groups, one 512-thread CTA per SM); GQA 4:1 at 16 KV heads (generic)
+    (64, 64, 4, 10000.0, 70), (64, 64, 2, 10000.0, 33), (64, 16, 2, 500000.0, 70),
     # GQA 4:1 at the paper's G = 4 on the tensor-core kernel (half-group pairs): C = 512 and 1024
     (16, 4, 4, 500000.0, 300), (32, 8, 4, 500000.0, 1025), (32, 8, 4, 10000.0, 1),
 ])

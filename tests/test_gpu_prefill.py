@@ -71,6 +71,8 @@ def check(got, want):
     # the widest tensor-core layer: 12 FWHT groups (C = 6144)
     (48, 48, 4, 50, (0, 7), 8),
     (48, 48, 1, 40, (0,), 9),
+    # the widest layer the reference allows: C = 8192 (16 FWHT groups, one CTA per SM)
+    (64, 64, 4, 40, (0, 17), 10),
 ])
 def test_prefill_matches_oracle(oracle, hq, hkv, g, T, sinks, seed):
     layer, k, v, flags, q, perm = build(hq, hkv, g, T, sinks, seed)
@@ -101,9 +103,9 @@ def test_prefill_rejects_bad_arguments():
         layer.prefill_attention(q.float())
 
 
-@pytest.mark.parametrize("hq,hkv,g", [(64, 64, 4), (64, 16, 2), (16, 8, 4)])
+@pytest.mark.parametrize("hq,hkv,g", [(64, 16, 2), (16, 8, 4), (64, 64, 8)])
 def test_prefill_refuses_shapes_outside_the_tensor_core_path(hq, hkv, g):
-    """C = 8192, GQA beyond 8 KV heads and 2:1 GQA: ValueError, nothing launched."""
+    """GQA beyond 8 KV heads, 2:1 GQA and G = 8: ValueError, nothing launched."""
     layer, k, v, flags, q, perm = build(hq, hkv, g, 20, (0,), 1)
     with pytest.raises(ValueError, match="tensor-core path"):
         layer.prefill_attention(q, q_start=np.zeros(2, np.int64))
