@@ -13,6 +13,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import decode_sweep  # noqa: E402
 import paper_2501_16383_b200 as P  # noqa: E402
 
+for kv in filter(None, os.environ.get("RKV_OPT", "").split(",")):  # experiment switches, e.g. RKV_OPT=decode_splits=40
+    k_, v_ = kv.split("=")
+    P.set_debug_option(k_, int(v_))
 decode_sweep.run(int(sys.argv[1]) if len(sys.argv) > 1 else 2, iters=3)
 buf = (ctypes.c_ulonglong * (4096 * 4))()
 P.rotatekv.lib().rkv_debug_decode_trace(buf)
@@ -56,3 +59,11 @@ if len(pairs):
 nsm = 148
 first = cid < nsm
 print(f"first-wave CTAs: loop median {np.median(loop[first]):.1f} | later CTAs: {np.median(loop[~first]):.1f}")
+# the slowest CTAs: linear id, SM, loop time, and their SM partner's
+if os.environ.get("SLOWEST"):
+    order = np.argsort(-loop)[: int(os.environ["SLOWEST"])]
+    for i in order:
+        sm = t[i, 3]
+        partner = [j for j in np.nonzero(t[:, 3] == sm)[0] if j != i]
+        pl = f"{cid[partner[0]]}:{loop[partner[0]]:.1f}" if partner else "-"
+        print(f"cid {cid[i]} sm {sm} loop {loop[i]:.1f} start {(t[i, 0] - t0) / 1e3:.2f} partner {pl}")
