@@ -775,7 +775,8 @@ def run_ours(args):
                        "h2d_bytes_per_step": d["h2d_bytes_per_step"] * world,
                        "d2h_bytes_per_step": d["d2h_bytes_per_step"] * world, "finite": d["finite"],
                        "path": "C++ API (rotatekv.hpp DeviceLayerCache::decode_attention), pinned host q in / "
-                               "fp32 out per step, one process per GPU (paper_2501_16383_b200/csrc/e2e_cpp.cu)"}
+                               "fp32 out per step on a copy stream, double buffered (as e2e), one process per GPU "
+                               "(paper_2501_16383_b200/csrc/e2e_cpp.cu)"}
         else:
             max_over_ranks([0.0], dev, world)
     except Exception as exc:

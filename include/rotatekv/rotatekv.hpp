@@ -137,10 +137,14 @@ public:
         check(rkv_layer_plan_init(&desc_, perm.data(), plan_, plan_bytes_, stream_));
         ws_bytes_ = rkv_decode_workspace_bytes(&desc_, desc.max_tokens);
         check_cuda(cudaMalloc(&ws_, ws_bytes_), "cudaMalloc workspace");
-        // a small ring of device length vectors: each call stages the host lengths
-        // into the next slot (stream-ordered, no synchronization per call)
+        // a small ring of device length vectors: a call whose lengths changed
+        // stages them through pinned host memory into the next slot
+        // (stream-ordered; the slot's event guards the pinned copy's reuse)
         check_cuda(cudaMalloc(&dev_pos_, kPosRing * static_cast<size_t>(desc.batch) * sizeof(int64_t)),
                    "cudaMalloc pos");
+        check_cuda(cudaMallocHost(&host_pos_, kPosRing * static_cast<size_t>(desc.batch) * sizeof(int64_t)),
+                   "cudaMallocHost pos");
+        for (auto& e : pos_ev_) check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "pos event");
         sink_set_.resize(static_cast<size_t>(desc.batch));
         check(rkv_cache_reset(&desc_, &cache_, stream_));
     }
@@ -153,6 +157,8 @@ public:
         cudaFree(ws_);
         cudaFree(plan_);
         cudaFree(dev_pos_);
+        cudaFreeHost(host_pos_);
+        for (auto e : pos_ev_) cudaEventDestroy(e);
         cudaFree(dev_qs_);
         cudaFree(pf_ws_);
         cudaFree(flags_);
@@ -327,11 +333,20 @@ public:
 
 private:
     static constexpr size_t kPosRing = 8;
-    // copy the host lengths into the next device slot (stream-ordered)
+    // the device copy of the host lengths: re-staged only when they changed
+    // since the last upload (a decode step after an append uploads once; repeated
+    // decodes upload nothing)
     int64_t* stage_lengths() {
-        int64_t* slot = dev_pos_ + (pos_next_++ % kPosRing) * len_.size();
-        check_cuda(cudaMemcpyAsync(slot, len_.data(), len_.size() * sizeof(int64_t), cudaMemcpyHostToDevice, stream_),
-                   "lengths");
+        if (last_pos_ && last_len_ == len_) return last_pos_;
+        const size_t k = pos_next_++ % kPosRing;
+        check_cuda(cudaEventSynchronize(pos_ev_[k]), "lengths slot");  // its previous copy has been read
+        int64_t* h = host_pos_ + k * len_.size();
+        std::copy(len_.begin(), len_.end(), h);
+        int64_t* slot = dev_pos_ + k * len_.size();
+        check_cuda(cudaMemcpyAsync(slot, h, len_.size() * sizeof(int64_t), cudaMemcpyHostToDevice, stream_), "lengths");
+        check_cuda(cudaEventRecord(pos_ev_[k], stream_), "lengths event");
+        last_len_ = len_;
+        last_pos_ = slot;
         return slot;
     }
     // grow-only device scratch (the old buffer is freed only when it grows)
@@ -361,6 +376,10 @@ private:
     void* plan_ = nullptr;
     size_t plan_bytes_ = 0;
     int64_t* dev_pos_ = nullptr;
+    int64_t* host_pos_ = nullptr;  // pinned staging ring
+    cudaEvent_t pos_ev_[kPosRing] = {};
+    std::vector<int64_t> last_len_;
+    int64_t* last_pos_ = nullptr;
     int64_t* dev_qs_ = nullptr;
     void* pf_ws_ = nullptr;
     size_t pf_ws_bytes_ = 0;

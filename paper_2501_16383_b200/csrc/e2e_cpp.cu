@@ -10,7 +10,9 @@
 // N(0,1) fp16 K/V generated on the device, token 0 a sink), then times K
 // decode steps, each: H2D of the step's queries from pinned host memory,
 // DeviceLayerCache::decode_attention, D2H of the fp32 output -- all inside
-// the CUDA-event-timed region.  Prints one JSON line.
+// the CUDA-event-timed region.  As in bench.py's e2e (the serving pattern),
+// the copies run on a copy stream, double buffered, so step i+1's upload and
+// step i-1's download overlap step i's kernels.  Prints one JSON line.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -110,22 +112,50 @@ int main(int argc, char** argv) {
         std::mt19937 rng(static_cast<unsigned>(seed) + 1);
         std::normal_distribution<float> nd;
         for (size_t i = 0; i < 4 * qn; ++i) hq[i] = __half_as_ushort(__float2half_rn(nd(rng)));
-        uint16_t* dq = nullptr;
-        float* dout = nullptr;
-        check_cuda(cudaMalloc(&dq, qn * 2), "q");
-        check_cuda(cudaMalloc(&dout, on * 4), "out");
-        auto step = [&](int i) {
-            check_cuda(cudaMemcpyAsync(dq, hq + (i % 4) * qn, qn * 2, cudaMemcpyHostToDevice, s), "H2D q");
-            cache.decode_attention(dq, dout);
-            check_cuda(cudaMemcpyAsync(hout, dout, on * 4, cudaMemcpyDeviceToHost, s), "D2H out");
+        uint16_t* dq[2] = {nullptr, nullptr};
+        float* dout[2] = {nullptr, nullptr};
+        for (int j = 0; j < 2; ++j) {
+            check_cuda(cudaMalloc(&dq[j], qn * 2), "q");
+            check_cuda(cudaMalloc(&dout[j], on * 4), "out");
+        }
+        cudaStream_t cs;
+        check_cuda(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "copy stream");
+        cudaEvent_t up[2], comp[2], down[2];
+        for (int j = 0; j < 2; ++j) {
+            cudaEventCreateWithFlags(&up[j], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&comp[j], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&down[j], cudaEventDisableTiming);
+        }
+        auto upload = [&](int i) {
+            const int j = i & 1;
+            check_cuda(cudaStreamWaitEvent(cs, comp[j], 0), "wait comp");  // step i-2 done reading q buffer j
+            check_cuda(cudaMemcpyAsync(dq[j], hq + (i % 4) * qn, qn * 2, cudaMemcpyHostToDevice, cs), "H2D q");
+            cudaEventRecord(up[j], cs);
         };
-        for (int i = 0; i < warmup; ++i) step(i);
-        check_cuda(cudaStreamSynchronize(s), "warmup");
+        auto step = [&](int i, int n) {
+            const int j = i & 1;
+            if (i == 0) upload(0);
+            if (i + 1 < n) upload(i + 1);
+            check_cuda(cudaStreamWaitEvent(s, up[j], 0), "wait up");
+            check_cuda(cudaStreamWaitEvent(s, down[j], 0), "wait down");  // out buffer j downloaded (step i-2)
+            cache.decode_attention(dq[j], dout[j]);
+            cudaEventRecord(comp[j], s);
+            check_cuda(cudaStreamWaitEvent(cs, comp[j], 0), "wait comp");
+            check_cuda(cudaMemcpyAsync(hout, dout[j], on * 4, cudaMemcpyDeviceToHost, cs), "D2H out");
+            cudaEventRecord(down[j], cs);
+        };
+        for (int i = 0; i < warmup; ++i) step(i, warmup);
+        check_cuda(cudaDeviceSynchronize(), "warmup");
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
         cudaEventRecord(e0, s);
-        for (int i = 0; i < steps; ++i) step(i);
+        check_cuda(cudaStreamWaitEvent(cs, e0, 0), "start");
+        for (int i = 0; i < steps; ++i) step(i, steps);
+        cudaEvent_t last;
+        cudaEventCreateWithFlags(&last, cudaEventDisableTiming);
+        cudaEventRecord(last, cs);
+        check_cuda(cudaStreamWaitEvent(s, last, 0), "last download");  // inside the timed region
         cudaEventRecord(e1, s);
         check_cuda(cudaEventSynchronize(e1), "timed");
         float ms = 0.f;
@@ -139,8 +169,11 @@ int main(int argc, char** argv) {
                     std::isfinite(checksum) ? "true" : "false");
         cudaFree(dk);
         cudaFree(dv);
-        cudaFree(dq);
-        cudaFree(dout);
+        for (int j = 0; j < 2; ++j) {
+            cudaFree(dq[j]);
+            cudaFree(dout[j]);
+        }
+        cudaStreamDestroy(cs);
         cudaFreeHost(hq);
         cudaFreeHost(hout);
         cudaStreamDestroy(s);
