@@ -20,10 +20,13 @@ from paper_2501_16383_b200 import workload as WL  # noqa: E402
 from .test_gpu_parity import (COS_TOL, REL_TOL, build_layer, cache_host, cosine, oracle_decode,  # noqa: E402
                              rel_err, small_workload)
 
-# (Hq, Hkv, G): tensor-core MHA at G = 1/2/4, GQA 4:1 at G = 2, CUDA-core shapes
+# (Hq, Hkv, G): tensor-core MHA at G = 1/2/4 (up to C = 8192), GQA 4:1 at G = 2
+# and 4, CUDA-core shapes, generic (tiled) shapes
 SHAPES = [(8, 8, 4), (8, 8, 2), (8, 8, 1), (12, 12, 4), (40, 40, 4), (16, 4, 2), (32, 8, 2), (16, 8, 4),
-          (8, 4, 2), (16, 4, 1), (4, 4, 1)]
-TC_PREFILL = {(8, 8, 4), (8, 8, 2), (8, 8, 1), (12, 12, 4), (40, 40, 4), (16, 4, 2), (32, 8, 2), (4, 4, 1)}
+          (8, 4, 2), (16, 4, 1), (4, 4, 1), (16, 4, 4), (32, 8, 4), (64, 64, 4), (16, 16, 8), (24, 8, 8),
+          (64, 16, 4)]
+TC_PREFILL = {(8, 8, 4), (8, 8, 2), (8, 8, 1), (12, 12, 4), (40, 40, 4), (16, 4, 2), (32, 8, 2), (4, 4, 1),
+              (16, 4, 4), (32, 8, 4), (64, 64, 4)}
 
 
 def case(i):
@@ -46,7 +49,7 @@ def case(i):
                 base=500000.0 if rng.random() < 0.5 else 10000.0)
 
 
-@pytest.mark.parametrize("i", range(60))
+@pytest.mark.parametrize("i", range(85))
 def test_random_case(oracle, i):
     c = case(i)
     w = small_workload(c["hq"], c["hkv"], c["g"], base=c["base"])
