@@ -382,16 +382,28 @@ __global__ void __launch_bounds__(32 * VW, 1) quantize_v_kernel(QuantParams p, u
     float2* row = reinterpret_cast<float2*>(base + VS * 2 * kVSeg * 2);   // [32][33]
     const uint32_t gw = blockIdx.x * kVWarps + warp, step = gridDim.x * kVWarps;
 
-    // sub-item -> (b, i0, segment)
-    auto decode = [&](uint32_t si, int& b, int& i0, int& seg) {
-        const uint32_t pr = udiv32(si, nseg), bb = udiv32(pr, npairs);
-        seg = static_cast<int>(si - pr * nseg);
-        b = static_cast<int>(bb);
-        i0 = static_cast<int>(pr - bb * npairs) * 2;
+    // sub-item si = (b npairs + ip) nseg + seg.  A warp's sub-items advance by
+    // `step`: the cursors carry (b, ip, seg) forward with two compares instead
+    // of two divisions per sub-item
+    struct Cursor {
+        uint32_t b, ip, seg;
     };
-    auto issue = [&](uint32_t si, int sb) {
-        int b, i0, seg;
-        decode(si, b, i0, seg);
+    auto locate = [&](uint32_t si) {
+        const uint32_t pr = udiv32(si, nseg), bb = udiv32(pr, npairs);
+        return Cursor{bb, pr - bb * npairs, si - pr * nseg};
+    };
+    const Cursor dstep = locate(step);
+    auto advance = [&](Cursor& c) {
+        c.seg += dstep.seg;
+        const uint32_t c1 = c.seg >= nseg ? 1u : 0u;
+        c.seg -= c1 * nseg;
+        c.ip += dstep.ip + c1;
+        const uint32_t c2 = c.ip >= npairs ? 1u : 0u;
+        c.ip -= c2 * npairs;
+        c.b += dstep.b + c2;
+    };
+    auto issue = [&](const Cursor& c, int sb) {
+        const int b = static_cast<int>(c.b), i0 = static_cast<int>(c.ip) * 2, seg = static_cast<int>(c.seg);
         const bool has1 = i0 + 1 < num_new;
         const uint16_t* src = p.v_new + (static_cast<int64_t>(b) * num_new + i0) * C + seg * kVSeg;
         uint16_t* dst = stage + sb * 2 * kVSeg;
@@ -403,14 +415,14 @@ __global__ void __launch_bounds__(32 * VW, 1) quantize_v_kernel(QuantParams p, u
         mbar_init(&bar[warp][0], 1);
         mbar_init(&bar[warp][1], 1);
         mbar_fence_init();
-        if (gw < subitems) issue(gw, 0);
-        if (VS == 2 && gw + step < subitems) issue(gw + step, 1);
+        if (gw < subitems) issue(locate(gw), 0);
+        if (VS == 2 && gw + step < subitems) issue(locate(gw + step), 1);
     }
     __syncwarp();
+    Cursor cur = locate(gw), nxt = locate(gw + VS * step);  // this sub-item, the one whose copy we issue next
     uint32_t k = 0;
-    for (uint32_t si = gw; si < subitems; si += step, ++k) {
-        int b, i0, seg;
-        decode(si, b, i0, seg);
+    for (uint32_t si = gw; si < subitems; si += step, ++k, advance(cur), advance(nxt)) {
+        const int b = static_cast<int>(cur.b), i0 = static_cast<int>(cur.ip) * 2, seg = static_cast<int>(cur.seg);
         const bool has1 = i0 + 1 < num_new;
         const int sb = VS == 2 ? (k & 1) : 0;
         // sidecar slots of the pair's tokens (quantize_kv_kernel's rule, same inputs)
@@ -433,7 +445,7 @@ __global__ void __launch_bounds__(32 * VW, 1) quantize_v_kernel(QuantParams p, u
         fwht_region_a(st, has1 ? st + kVSeg : st, row, lane);
         __syncwarp();
         // the stage is consumed: refill it with the sub-item after next
-        if (lane == 0 && si + VS * step < subitems) issue(si + VS * step, sb);
+        if (lane == 0 && si + VS * step < subitems) issue(nxt, sb);
         fwht_unit_b<128>(row, lane / 4, lane % 4, p.v_norm);
         __syncwarp();
         float2 x[32];
