@@ -425,21 +425,12 @@ __global__ void __launch_bounds__(32 * VW, 1) quantize_v_kernel(QuantParams p, u
         const int b = static_cast<int>(cur.b), i0 = static_cast<int>(cur.ip) * 2, seg = static_cast<int>(cur.seg);
         const bool has1 = i0 + 1 < num_new;
         const int sb = VS == 2 ? (k & 1) : 0;
-        // sidecar slots of the pair's tokens (quantize_kv_kernel's rule, same inputs)
-        int slot = -1;
-        if (lane < 2) {
-            const int i = i0 + lane;
-            const int64_t pos = p.start_pos[b] + i;
-            if (p.sink_flags && i < num_new && pos >= 0 && pos < p.max_tokens &&
-                p.sink_flags[static_cast<int64_t>(b) * num_new + i]) {
-                int before = 0;
-                for (int q = 0; q < i; ++q) before += p.sink_flags[static_cast<int64_t>(b) * num_new + q] ? 1 : 0;
-                slot = p.cache.sink_count[b] + before;
-                if (slot >= p.max_sinks) slot = -1;
-            }
-        }
-        const int slot0 = __shfl_sync(0xffffffffu, slot, 0), slot1 = __shfl_sync(0xffffffffu, slot, 1);
+        // the pair's position and sink flags: loads issued here, used after the
+        // FWHT (the sidecar slot rule of quantize_kv_kernel, same inputs)
         const int64_t pos0 = p.start_pos[b] + i0;
+        const uint8_t flag = lane < 2 && p.sink_flags && i0 + lane < num_new
+                                 ? p.sink_flags[static_cast<int64_t>(b) * num_new + i0 + lane]
+                                 : uint8_t{0};
         mbar_wait(&bar[warp][sb], VS == 2 ? (k >> 1) & 1u : k & 1u);
         const uint16_t* st = stage + sb * 2 * kVSeg;
         fwht_region_a(st, has1 ? st + kVSeg : st, row, lane);
@@ -453,6 +444,15 @@ __global__ void __launch_bounds__(32 * VW, 1) quantize_v_kernel(QuantParams p, u
 #pragma unroll
         for (int c = 0; c < 32; ++c) x[c] = srcr[c];
         const QuantOut qo = quantize_run<FMT>(x, lane);
+        int slot = -1;
+        if (flag && pos0 + lane >= 0 && pos0 + lane < p.max_tokens) {  // lanes 0, 1: tokens i0, i0 + 1
+            const int i = i0 + lane;
+            int before = 0;
+            for (int q = 0; q < i; ++q) before += p.sink_flags[static_cast<int64_t>(b) * num_new + q] ? 1 : 0;
+            slot = p.cache.sink_count[b] + before;
+            if (slot >= p.max_sinks) slot = -1;
+        }
+        const int slot0 = __shfl_sync(0xffffffffu, slot, 0), slot1 = __shfl_sync(0xffffffffu, slot, 1);
         const int64_t row0 = static_cast<int64_t>(b) * p.max_tokens + pos0;
 #pragma unroll
         for (int tok = 0; tok < 2; ++tok) {
