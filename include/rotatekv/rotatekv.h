@@ -167,6 +167,13 @@ rkv_status rkv_cache_read(const rkv_layer_desc* desc, const rkv_cache* cache, co
  * (a decode with a plan of another kernel kind returns NaN). */
 rkv_status rkv_set_debug_option(const char* name, int64_t value);
 
+/* Diagnostic: the decode plan rkv_decode_attention uses for (desc,
+ * max_seq_len) on the current device -- out[0..9] = kernel kind (0 CUDA-core,
+ * 1 tensor-core, 2 generic), channels per FWHT tile, threads per CTA, splits
+ * per sequence, partial rows per sequence, tokens per split, tokens per
+ * tile, resident CTAs per SM, shared-memory bytes per CTA, TMA stages. */
+rkv_status rkv_decode_plan_info(const rkv_layer_desc* desc, int64_t max_seq_len, int64_t out[10]);
+
 /* Per-layer decode plan (once per layer, after calibration): from the HOST
  * permutation perm [C] (slot j <- channel perm[j]) choose which packed word
  * each decode thread un-reorders so the shared-memory scatter's bank

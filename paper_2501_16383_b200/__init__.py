@@ -21,5 +21,5 @@ from .rotatekv import (  # noqa: F401
     layer_plan_build,
     lib,
     rotate_keys,
-    set_debug_option,
+    set_debug_option, decode_plan_info,
 )

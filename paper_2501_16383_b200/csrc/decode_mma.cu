@@ -1099,6 +1099,10 @@ DecodePlan plan_decode_mma(const rkv_layer_desc& d, int64_t max_seq_len) {
             pl.per_sm = n;
         else
             cudaGetLastError();
+        // the occupancy query reports one CTA per SM for the tensor-memory GQA
+        // kernels, which run two (128 registers x 256 threads, 2 x 92 KB: ncu's
+        // block limits, tools/plan_info.py); plan the splits for two
+        if (gqa && gqa_tmem()) pl.per_sm = std::max(pl.per_sm, std::min(2, static_cast<int>((227u * 1024u) / (pl.smem + 1024))));
     }
     // splits per sequence: fill every resident CTA slot, and prefer a split count
     // whose CTA total is close to a whole number of waves (within 4x the minimum)

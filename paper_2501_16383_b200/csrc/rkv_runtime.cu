@@ -123,3 +123,13 @@ extern "C" rkv_status rkv_set_debug_option(const char* name, int64_t value) {
     o.epoch.fetch_add(1);
     return RKV_OK;
 }
+
+extern "C" rkv_status rkv_decode_plan_info(const rkv_layer_desc* desc, int64_t max_seq_len, int64_t out[10]) {
+    if (!desc || !out) return RKV_ERR_INVALID_ARGUMENT;
+    if (rkv_layer_validate(desc) != RKV_OK) return RKV_ERR_INVALID_ARGUMENT;
+    const rkv::DecodePlan& pl = rkv::cached_plan(*desc, max_seq_len);
+    const int64_t v[10] = {pl.kind, pl.N, pl.NT, pl.S, pl.NP, pl.chunk, pl.TT, pl.per_sm,
+                           static_cast<int64_t>(pl.smem), pl.stages};
+    for (int i = 0; i < 10; ++i) out[i] = v[i];
+    return RKV_OK;
+}

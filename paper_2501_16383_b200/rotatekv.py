@@ -111,7 +111,8 @@ def lib():
         L.rkv_promote_sinks.argtypes = [D, C.POINTER(CacheView), P, C.c_int64, P, P, P, P]
         L.rkv_cache_read.argtypes = [D, C.POINTER(CacheView), P, C.c_int64, C.c_int64, C.c_int64, C.c_int32, P, P, P]
         L.rkv_set_debug_option.argtypes = [C.c_char_p, C.c_int64]
-        for name in ("rkv_promote_sinks", "rkv_set_debug_option", "rkv_cache_read", "rkv_layer_validate", "rkv_cache_carve", "rkv_cache_reset", "rkv_rope_table_init",
+        L.rkv_decode_plan_info.argtypes = [D, C.c_int64, C.POINTER(C.c_int64)]
+        for name in ("rkv_promote_sinks", "rkv_set_debug_option", "rkv_decode_plan_info", "rkv_cache_read", "rkv_layer_validate", "rkv_cache_carve", "rkv_cache_reset", "rkv_rope_table_init",
                      "rkv_quantize_kv", "rkv_decode_attention", "rkv_rotate_keys", "rkv_calibrate_reorder",
                      "rkv_detect_sinks", "rkv_detect_sinks_device", "rkv_layer_plan_build", "rkv_layer_plan_init",
                      "rkv_calibrate_reorder_device", "rkv_cache_export", "rkv_cache_import",
@@ -175,6 +176,17 @@ def set_debug_option(name: str, value: int) -> None:
     """Process-global experiment switch (rkv_set_debug_option): kernel
     selection etc.  Build layers (plan + RoPE table) after changing one."""
     _check(lib().rkv_set_debug_option(name.encode(), int(value)))
+
+
+def decode_plan_info(cfg, max_seq_len: int) -> dict:
+    """The decode plan rkv_decode_attention uses for this layer shape
+    (diagnostic, rkv_decode_plan_info)."""
+    out = (C.c_int64 * 10)()
+    d = cfg.desc()
+    _check(lib().rkv_decode_plan_info(C.byref(d), int(max_seq_len), out))
+    keys = ("kind", "tile_channels", "threads", "splits", "partials", "chunk", "tile_tokens", "ctas_per_sm",
+            "smem", "stages")
+    return dict(zip(keys, [int(x) for x in out]))
 
 
 WIRE_REFERENCE, WIRE_FP16_SCALE = 0, 1
