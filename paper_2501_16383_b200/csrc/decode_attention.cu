@@ -474,6 +474,25 @@ __global__ void __launch_bounds__(256) decode_combine_kernel(DecodeParams p, int
             rq[j] = rope_at(p.rope, T - 1, f);
         }
     }
+    // the first sinks' raw rows and positions, requested before the merge
+    // (their RoPE rows once the positions are in): one round trip for all of
+    // them instead of one per sink after it
+    constexpr int kSP = 4;
+    const int npre = min(nsink, kSP);
+    int spos[kSP];
+    uint2 ska[kSP], skb[kSP], sva[kSP];
+    if (warp == 0 || nw == 1) {
+        const int f0 = (4 * lane) & 63;
+#pragma unroll
+        for (int s = 0; s < kSP; ++s) {
+            if (s >= npre) break;
+            const int64_t srow = (static_cast<int64_t>(b) * p.max_sinks + s) * C + kvh * 128;
+            spos[s] = p.cache.sink_pos[b * p.max_sinks + s];
+            ska[s] = *reinterpret_cast<const uint2*>(p.cache.sink_k + srow + f0);
+            skb[s] = *reinterpret_cast<const uint2*>(p.cache.sink_k + srow + f0 + 64);
+            sva[s] = *reinterpret_cast<const uint2*>(p.cache.sink_v + srow + 4 * lane);
+        }
+    }
     float4 ov[32];
     {
         const int n0 = min(32, s_end - s_begin);
@@ -560,17 +579,19 @@ __global__ void __launch_bounds__(256) decode_combine_kernel(DecodeParams p, int
             const float2 r = rq[j];
             qd[j] = (d < 64 ? (a * r.x - bb * r.y) : (a * r.y + bb * r.x)) * p.qscale;
         }
-        for (int s = 0; s < nsink; ++s) {
-            const int pos = p.cache.sink_pos[b * p.max_sinks + s];
-            if (pos >= T) continue;
-            const int64_t srow = (static_cast<int64_t>(b) * p.max_sinks + s) * C + kvh * 128;
+        // one sink: logit from its RoPE'd raw key (k2a: dims f..f+3, k2b: f+64..,
+        // f = (4 lane) & 63), online-softmax fold, raw V row
+        auto fold_sink = [&](int pos, uint2 k2a, uint2 k2b, const float2 (&rk)[4], uint2 vv) {
+            const uint16_t kah[4] = {static_cast<uint16_t>(k2a.x & 0xffffu), static_cast<uint16_t>(k2a.x >> 16),
+                                     static_cast<uint16_t>(k2a.y & 0xffffu), static_cast<uint16_t>(k2a.y >> 16)};
+            const uint16_t kbh[4] = {static_cast<uint16_t>(k2b.x & 0xffffu), static_cast<uint16_t>(k2b.x >> 16),
+                                     static_cast<uint16_t>(k2b.y & 0xffffu), static_cast<uint16_t>(k2b.y >> 16)};
             float prod = 0.f;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                const int d = 4 * lane + j, f = d & 63;
-                const float ka = h2f(p.cache.sink_k[srow + f]), kb = h2f(p.cache.sink_k[srow + f + 64]);
-                const float2 rk = rope_at(p.rope, pos, f);
-                prod += qd[j] * (d < 64 ? (ka * rk.x - kb * rk.y) : (ka * rk.y + kb * rk.x));
+                const int d = 4 * lane + j;
+                const float ka = h2f(kah[j]), kb = h2f(kbh[j]);
+                prod += qd[j] * (d < 64 ? (ka * rk[j].x - kb * rk[j].y) : (ka * rk[j].y + kb * rk[j].x));
             }
 #pragma unroll
             for (int o = 16; o >= 1; o >>= 1) prod += __shfl_xor_sync(0xffffffffu, prod, o);
@@ -578,12 +599,35 @@ __global__ void __launch_bounds__(256) decode_combine_kernel(DecodeParams p, int
             const float a = exp2f(M - mn), e = exp2f(prod - mn);
             L = L * a + e;
             rot = make_float4(rot.x * a, rot.y * a, rot.z * a, rot.w * a);
-            const uint2 vv = *reinterpret_cast<const uint2*>(p.cache.sink_v + srow + 4 * lane);
             raw = make_float4(raw.x * a + e * h2f(static_cast<uint16_t>(vv.x & 0xffffu)),
                               raw.y * a + e * h2f(static_cast<uint16_t>(vv.x >> 16)),
                               raw.z * a + e * h2f(static_cast<uint16_t>(vv.y & 0xffffu)),
                               raw.w * a + e * h2f(static_cast<uint16_t>(vv.y >> 16)));
             M = mn;
+        };
+        float2 srk[kSP][4];  // the prefetched sinks' RoPE rows, all requested at once
+#pragma unroll
+        for (int s = 0; s < kSP; ++s) {
+            if (s >= npre) break;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) srk[s][j] = rope_at(p.rope, spos[s] < T ? spos[s] : 0, (4 * lane + j) & 63);
+        }
+#pragma unroll
+        for (int s = 0; s < kSP; ++s) {
+            if (s >= npre) break;
+            if (spos[s] < T) fold_sink(spos[s], ska[s], skb[s], srk[s], sva[s]);
+        }
+        for (int s = kSP; s < nsink; ++s) {  // beyond the prefetched ones
+            const int pos = p.cache.sink_pos[b * p.max_sinks + s];
+            if (pos >= T) continue;
+            const int64_t srow = (static_cast<int64_t>(b) * p.max_sinks + s) * C + kvh * 128;
+            const int f0 = (4 * lane) & 63;
+            float2 rk[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) rk[j] = rope_at(p.rope, pos, f0 + j);
+            fold_sink(pos, *reinterpret_cast<const uint2*>(p.cache.sink_k + srow + f0),
+                      *reinterpret_cast<const uint2*>(p.cache.sink_k + srow + f0 + 64), rk,
+                      *reinterpret_cast<const uint2*>(p.cache.sink_v + srow + 4 * lane));
         }
     }
     // H_128 on the rotated-frame accumulator (value_rotation inverse): index
