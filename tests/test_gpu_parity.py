@@ -262,6 +262,30 @@ def test_generic_tiles_sinks_and_splits(oracle, hq, hkv, g):
         assert cosine(out[b], want) > 0.99999
 
 
+@pytest.mark.parametrize("hq,hkv,g", [(8, 8, 4), (32, 8, 2), (32, 8, 4)])
+def test_decode_sinks_past_the_combine_prefetch(oracle, hq, hkv, g):
+    """More sink rows than the combine prefetches (4): rows 0..3 take the
+    prefetched path, the rest the per-sink loads; one sequence with none
+    past the first and one whose last sink is the final token."""
+    w = small_workload(hq, hkv, g)
+    B, T = 2, 400
+    layer, perm = build_layer(w, B, T + 2, seed=77 + g, max_sinks=8)
+    k, v = WL.make_kv(w, 77 + g, B, T)
+    sinks = torch.zeros(B, T, dtype=torch.uint8)
+    for t in (0, 5, 31, 32, 200, 333, 399):
+        sinks[0, t] = 1
+    sinks[1, 0] = 1
+    layer.append(k, v, sinks)
+    got = cache_host(layer)
+    q = WL.make_q(w, 78 + g, B)
+    out = layer.decode(q).cpu().numpy()
+    for b in range(B):
+        want = oracle_decode(oracle, layer, got, b, T, q[b].cpu().numpy(), w, perm, k[b].cpu().numpy(),
+                             v[b].cpu().numpy())
+        assert rel_err(out[b], want) < 2e-4, (b, rel_err(out[b], want))
+        assert cosine(out[b], want) > 0.99999
+
+
 def test_generic_decode_matches_reference_decode_step(ref):
     """G = 8 (n = 1024) end to end against the unmodified reference's
     decode_step (e4m3 scales, identity projections)."""
