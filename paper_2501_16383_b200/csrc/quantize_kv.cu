@@ -349,6 +349,9 @@ __global__ void __launch_bounds__(256, 2) quantize_kv_kernel(QuantParams p, uint
         }
         __syncthreads();  // row rewritten next; s_meta[sb ^ 1] visible
     }
+    // launched as the V kernel's programmatic dependent (k_only): this grid's
+    // completion must imply the V grid's, for the sink-count kernel after it
+    pdl_wait();
 }
 
 // V quantize, warp-independent.  V's rotation is per head (128 channels) and
@@ -411,6 +414,7 @@ __global__ void __launch_bounds__(32 * VW, 1) quantize_v_kernel(QuantParams p, u
         bulk_g2s(dst, src, kVSeg * 2, &bar[warp][sb]);
         if (has1) bulk_g2s(dst + kVSeg, src + C, kVSeg * 2, &bar[warp][sb]);
     };
+    pdl_trigger();  // the K kernel (independent outputs) may start in this kernel's tail
     if (lane == 0) {
         mbar_init(&bar[warp][0], 1);
         mbar_init(&bar[warp][1], 1);
@@ -604,9 +608,15 @@ cudaError_t launch_quantize_ns(const QuantParams& p, int B, cudaStream_t s) {
     if (items >= (int64_t{1} << 30)) return cudaErrorInvalidValue;
     int64_t grid = static_cast<int64_t>(num_sms()) * per_sm;
     if (grid > items) grid = items;
-    quantize_kv_kernel<N, FMT, NS><<<static_cast<unsigned>(grid), threads, smem, s>>>(
-        pk, static_cast<uint32_t>(items), static_cast<uint32_t>(npairs));
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e;
+    if (vsplit) {  // programmatic dependent of the V kernel: starts in its tail (no data dependency)
+        e = launch_pdl(quantize_kv_kernel<N, FMT, NS>, dim3(static_cast<unsigned>(grid)), dim3(threads), smem, s, pk,
+                       static_cast<uint32_t>(items), static_cast<uint32_t>(npairs));
+    } else {
+        quantize_kv_kernel<N, FMT, NS><<<static_cast<unsigned>(grid), threads, smem, s>>>(
+            pk, static_cast<uint32_t>(items), static_cast<uint32_t>(npairs));
+        e = cudaGetLastError();
+    }
     if (e != cudaSuccess) return e;
     if (!p.sink_flags) return cudaSuccess;
     quantize_sink_count_kernel<<<B, 256, 0, s>>>(p);
