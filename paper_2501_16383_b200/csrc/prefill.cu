@@ -72,6 +72,7 @@ __global__ void __launch_bounds__(512) reconstruct_keys_kernel(PrefillParams p) 
     constexpr int N = 128 * G, NJ = N / 128, TT = 4;
     static_assert(!PAIR || G == 2, "half-group pairs run on the 256-channel plan");
     extern __shared__ __align__(16) unsigned char smem[];
+    pdl_trigger();  // the value and query kernels do not read the keys: let them start in this one's tail
     const int C = p.C, W = C / 16, MG = C / 128, NG = C / N;
     const int b = blockIdx.y, tid = threadIdx.x, NT = blockDim.x, warp = tid >> 5, lane = tid & 31;
     const int64_t t0 = static_cast<int64_t>(blockIdx.x) * TT;
@@ -232,6 +233,7 @@ __global__ void __launch_bounds__(512) reconstruct_keys_kernel(PrefillParams p) 
 // Thread t: code word w = t >> 4 (channels 16w..16w+15), keys 8kc..8kc+7
 // (kc = (t >> 1) & 7), codes 8 (t & 1) .. + 7 of the word.
 __global__ void __launch_bounds__(128) reconstruct_values_kernel(PrefillParams p) {
+    pdl_trigger();
     const int64_t j = blockIdx.x;
     const int kvh = blockIdx.y, b = blockIdx.z, t = threadIdx.x;
     const int W = p.C / 16, MG = p.C / 128;
@@ -260,6 +262,7 @@ __global__ void __launch_bounds__(128) reconstruct_values_kernel(PrefillParams p
         *reinterpret_cast<uint4*>(vt + umma::sw128(static_cast<uint32_t>(16 * w + e), static_cast<uint32_t>(kc))) =
             make_uint4(h[0], h[1], h[2], h[3]);
     }
+    pdl_wait();  // this grid completes only after the key kernel (the attention kernel waits on the chain)
 }
 
 // --------------------------------------------------------------- 3. queries
@@ -271,6 +274,7 @@ __global__ void __launch_bounds__(128) reconstruct_values_kernel(PrefillParams p
 // conflict).  Warp = (sequence, query row, 4 heads); lane = frequencies
 // 2 lane, 2 lane + 1; padding rows (>= num_q) are zero.
 __global__ void __launch_bounds__(128) prepare_queries_kernel(PrefillParams p) {
+    pdl_trigger();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t i = blockIdx.x;
     const int b = blockIdx.z, h0 = (blockIdx.y * 4 + warp) * 4;
@@ -322,6 +326,7 @@ __global__ void __launch_bounds__(128) prepare_queries_kernel(PrefillParams p) {
         put(row, 64 + lane, pack_h2(sub_lo(qa[0], ha), sub_hi(qa[1], ha)));
         put(row, 96 + lane, pack_h2(sub_lo(qv[0], hb), sub_hi(qv[1], hb)));
     }
+    pdl_wait();  // completes only after the value kernel (and through it the key kernel)
 }
 
 // ------------------------------------------------------------- 4. attention
@@ -417,6 +422,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) prefill_attn_kernel(PrefillPa
              *ppeer = vpeer + 2, *qpeer = ppeer + 2;          // its P rows and its Q rows are in TMEM
     uint32_t* tslot = reinterpret_cast<uint32_t*>(qpeer + 1);
 
+    pdl_wait();  // the key, value and query kernels before it (a chain of programmatic dependents)
     const int h = blockIdx.y, b = blockIdx.z;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int REP = p.Hq / p.Hkv, kvh = h / REP;
@@ -870,12 +876,15 @@ cudaError_t launch_prefill(const rkv_layer_desc& d, const PrefillParams& p, int6
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     const dim3 vgrid(static_cast<unsigned>((max_seq_len + kPrefillKT - 1) / kPrefillKT), static_cast<unsigned>(p.Hkv),
                      static_cast<unsigned>(d.batch));
-    reconstruct_values_kernel<<<vgrid, 128, 0, s>>>(p);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    prepare_queries_kernel<<<dim3(static_cast<unsigned>(p.num_q_pad), static_cast<unsigned>((p.Hq + 15) / 16),
-                                  static_cast<unsigned>(d.batch)),
-                             128, 0, s>>>(p);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    // values and queries are programmatic dependents: they start in the key
+    // kernel's tail; each completes only after its predecessor (pdl_wait at
+    // its end), so the attention kernel's wait covers all three
+    if ((e = launch_pdl(reconstruct_values_kernel, vgrid, dim3(128), 0, s, p)) != cudaSuccess) return e;
+    if ((e = launch_pdl(prepare_queries_kernel,
+                        dim3(static_cast<unsigned>(p.num_q_pad), static_cast<unsigned>((p.Hq + 15) / 16),
+                             static_cast<unsigned>(d.batch)),
+                        dim3(128), 0, s, p)) != cudaSuccess)
+        return e;
     const dim3 agrid(static_cast<unsigned>(p.num_q_pad / kQR), static_cast<unsigned>(p.Hq), static_cast<unsigned>(d.batch));
     if (prefill_pair()) {  // 2-SM clusters (num_q_pad is a multiple of 256)
         constexpr size_t sm = AttnSmem<true>::total;
@@ -896,8 +905,7 @@ cudaError_t launch_prefill(const rkv_layer_desc& d, const PrefillParams& p, int6
     }
     constexpr size_t sm = AttnSmem<false>::total;
     if ((e = ensure_smem_k(prefill_attn_kernel<false>, sm)) != cudaSuccess) return e;
-    prefill_attn_kernel<false><<<agrid, kAttnThreads, sm, s>>>(p);
-    return cudaGetLastError();
+    return launch_pdl(prefill_attn_kernel<false>, agrid, dim3(kAttnThreads), sm, s, p);
 }
 
 }  // namespace rkv
