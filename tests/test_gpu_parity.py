@@ -286,6 +286,29 @@ def test_decode_sinks_past_the_combine_prefetch(oracle, hq, hkv, g):
         assert cosine(out[b], want) > 0.99999
 
 
+@pytest.mark.parametrize("hq,hkv,g", [(8, 8, 4), (16, 4, 2), (16, 4, 4), (16, 16, 8)])
+def test_decode_large_batch(oracle, hq, hkv, g):
+    """More sequences than resident CTA slots (one split each, several
+    waves) and ragged lengths; sampled sequences against the oracle."""
+    w = small_workload(hq, hkv, g)
+    B, T = 320, 48
+    layer, perm = build_layer(w, B, T + 1, seed=400 + g)
+    k, v = WL.make_kv(w, 400 + g, B, T)
+    sinks = torch.zeros(B, T, dtype=torch.uint8)
+    sinks[:, 0] = 1
+    sinks[::7, 17] = 1
+    layer.append(k, v, sinks)
+    lens = [T - (b % 13) for b in range(B)]
+    q = WL.make_q(w, 401 + g, B)
+    out = layer.decode(q, seq_len=lens).cpu().numpy()
+    got = cache_host(layer)
+    for b in (0, 7, 150, B - 1):
+        want = oracle_decode(oracle, layer, got, b, lens[b], q[b].cpu().numpy(), w, perm, k[b].cpu().numpy(),
+                             v[b].cpu().numpy())
+        assert rel_err(out[b], want) < 2e-4, (b, rel_err(out[b], want))
+        assert cosine(out[b], want) > 0.99999
+
+
 def test_generic_decode_matches_reference_decode_step(ref):
     """G = 8 (n = 1024) end to end against the unmodified reference's
     decode_step (e4m3 scales, identity projections)."""
