@@ -553,11 +553,16 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? 2 : 1) decode_gqa_kernel(Dec
     constexpr bool X = GR == 4;  // partner-half exchange
     constexpr uint32_t kQCols = X ? 64 : 32, kWarpCols = kQCols + 64;
     extern __shared__ __align__(128) unsigned char smem[];
-    pdl_wait();  // lengths, queries and the cache may come from the previous kernel
     const int C = p.C, W = C / 16, MG = C / 128, Hq = p.Hq, NG = C / N;
     const MmaSmem lay = gqa_smem(C, TT, p.chunk);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + lay.mbar);
     uint32_t* mask_s = reinterpret_cast<uint32_t*>(smem + lay.mask);
+    {  // the layer plan is static: stage it while the previous kernel drains
+        const uint4* src = reinterpret_cast<const uint4*>(p.plan + kPlanHeader);
+        uint4* dst = reinterpret_cast<uint4*>(smem + lay.plan);
+        for (int i = threadIdx.x; i < 17 * W / 4; i += blockDim.x) dst[i] = __ldg(src + i);
+    }
+    pdl_wait();  // lengths, queries and the cache may come from the previous kernel
 
     const int tid = threadIdx.x, NT = blockDim.x;
     const int warp = tid >> 5, lane = tid & 31;
@@ -624,11 +629,6 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? 2 : 1) decode_gqa_kernel(Dec
         for (int i = tid; i < nw; i += NT) mask_s[i] = smask[mw0 + i];
     }
     const uint32_t* plan_s = reinterpret_cast<const uint32_t*>(smem + lay.plan);
-    {
-        const uint4* src = reinterpret_cast<const uint4*>(p.plan + kPlanHeader);
-        uint4* dst = reinterpret_cast<uint4*>(smem + lay.plan);
-        for (int i = tid; i < 17 * W / 4; i += NT) dst[i] = __ldg(src + i);
-    }
     const uint32_t pair_bytes = static_cast<uint32_t>(C) * 4u;
     auto bexp = [](int sh) -> uint32_t { const uint32_t be = static_cast<uint32_t>(25 - 2 * sh) << 10; return be | (be << 16); };
 
