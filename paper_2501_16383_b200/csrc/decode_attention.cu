@@ -442,7 +442,9 @@ __global__ void __launch_bounds__(max_threads<N>(), 1) decode_split_kernel(Decod
 // owns channels 4*lane .. 4*lane+3, so H_128 is 2 register stages + 5 shuffle
 // stages and the sink dot products are warp reductions.
 __global__ void __launch_bounds__(256) decode_combine_kernel(DecodeParams p, int nw) {
-    pdl_wait();  // the split kernel's partials
+    // the queries, lengths, RoPE table and sink rows predate the split kernel
+    // (it waited for them): requested while it drains; the partials after
+    // pdl_wait below
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // nw == 1: four (b, h) per CTA, a warp merges all partials; nw > 1 (few
     // heads, many partials): a CTA per (b, h), warp w merges the w-th range of
@@ -493,6 +495,7 @@ __global__ void __launch_bounds__(256) decode_combine_kernel(DecodeParams p, int
             sva[s] = *reinterpret_cast<const uint2*>(p.cache.sink_v + srow + 4 * lane);
         }
     }
+    pdl_wait();  // the split kernel's partials
     float4 ov[32];
     {
         const int n0 = min(32, s_end - s_begin);
