@@ -522,6 +522,21 @@ __global__ void __launch_bounds__(NGC < 0 ? kMmaMaxThreads : 320, NGC < 0 ? 1 : 
 // softmax state, and emits one partial per (warp, head).
 constexpr int kGqaNS = 3;
 
+// 64-thread named barrier of warp pair `pair` (ids 1..8 as immediates, so the
+// kernel reserves only the barriers it can use)
+__device__ __forceinline__ void pair_bar_sync(int pair) {
+    switch (pair) {
+        case 0: asm volatile("bar.sync 1, 64;" ::: "memory"); break;
+        case 1: asm volatile("bar.sync 2, 64;" ::: "memory"); break;
+        case 2: asm volatile("bar.sync 3, 64;" ::: "memory"); break;
+        case 3: asm volatile("bar.sync 4, 64;" ::: "memory"); break;
+        case 4: asm volatile("bar.sync 5, 64;" ::: "memory"); break;
+        case 5: asm volatile("bar.sync 6, 64;" ::: "memory"); break;
+        case 6: asm volatile("bar.sync 7, 64;" ::: "memory"); break;
+        default: asm volatile("bar.sync 8, 64;" ::: "memory"); break;
+    }
+}
+
 __host__ __device__ inline MmaSmem gqa_smem(int C, int TT, int chunk) {
     MmaSmem s{};
     const int W = C / 16, MG = C / 128, PP = TT / 2;
@@ -546,9 +561,9 @@ __host__ __device__ inline MmaSmem gqa_smem(int C, int TT, int chunk) {
 // tcgen05.ld, a few instructions per tile), so the register peak is the larger
 // phase instead of their sum and two CTAs fit on an SM.
 template <int REP, int PW, bool TM, bool SP = false, int GR = 2>
-__global__ void __launch_bounds__(32 * 4 * PW, TM ? 2 : 1) decode_gqa_kernel(DecodeParams p) {
+__global__ void __launch_bounds__(32 * 4 * PW, TM ? (PW == 1 ? 4 : 2) : 1) decode_gqa_kernel(DecodeParams p) {
     static_assert(REP == 4, "decode_gqa_kernel: 4 q heads per KV head");
-    static_assert(GR == 2 || (GR == 4 && PW == 2 && TM), "decode_gqa_kernel: G = 2, or G = 4 at PW = 2 with TMEM parking");
+    static_assert(GR == 2 || (GR == 4 && PW <= 2 && TM), "decode_gqa_kernel: G = 2, or G = 4 at PW <= 2 with TMEM parking");
     constexpr int G = 2, N = 256, NJ = 2, TT = 8 * PW, PPT = TT / 2;  // G, N: KV heads / channels per warp group
     constexpr bool X = GR == 4;  // partner-half exchange
     constexpr uint32_t kQCols = X ? 64 : 32, kWarpCols = kQCols + 64;
@@ -610,7 +625,7 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? 2 : 1) decode_gqa_kernel(Dec
     }
     __shared__ uint32_t s_tmem;
     if constexpr (TM) {
-        if (warp == 0) umma::alloc<256>(&s_tmem);
+        if (warp == 0) umma::alloc<PW == 1 ? 128 : 256>(&s_tmem);
         umma::fence_before();
     }
     __syncthreads();
@@ -887,7 +902,7 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? 2 : 1) decode_gqa_kernel(Dec
             scatter34(bo, dx);
             float2* xch = reinterpret_cast<float2*>(smem + lay.xch);
             xch[warp * 32 + lane] = make_float2(dx[0], dx[1]);
-            asm volatile("bar.sync %0, 64;" ::"r"(1 + (warp >> 1)) : "memory");  // the group's two warps
+            pair_bar_sync(warp >> 1);  // the group's two warps
             const float2 rx = xch[(warp ^ 1) * 32 + lane];
             d[0] += rx.x;
             d[1] += rx.y;
@@ -1007,7 +1022,7 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? 2 : 1) decode_gqa_kernel(Dec
         __syncthreads();
         if (warp == 0) {
             umma::fence_after();
-            umma::dealloc<256>(s_tmem);
+            umma::dealloc<PW == 1 ? 128 : 256>(s_tmem);
         }
     }
 }
@@ -1040,7 +1055,7 @@ MhaKernel mha_kernel_g(int NG, bool sp) {
 MhaKernel mha_kernel(int NG, int G, bool sp = false) {
     return G == 1 ? mha_kernel_g<1>(NG, sp) : G == 2 ? mha_kernel_g<2>(NG, sp) : mha_kernel_g<4>(NG, sp);
 }
-int gqa_pw() { return std::max(2, std::min(4, options().gqa_pw.load())); }
+int gqa_pw() { return std::max(1, std::min(4, options().gqa_pw.load())); }
 bool gqa_tmem() { return options().gqa_tmem.load() != 0; }
 template <int PW>
 void* gqa_kernel_ptr() {
@@ -1048,13 +1063,20 @@ void* gqa_kernel_ptr() {
                       : reinterpret_cast<void*>(decode_gqa_kernel<4, PW, false>);
 }
 void* gqa_kernel(int pw, bool sp = false, bool g4 = false) {
-    if (g4)  // G = 4: half-group pairs, PW = 2, accumulators and queries parked in tensor memory
+    if (g4) {  // G = 4: half-group pairs, PW 1 or 2, accumulators and queries parked in tensor memory
+        if (pw == 1)
+            return sp ? reinterpret_cast<void*>(decode_gqa_kernel<4, 1, true, true, 4>)
+                      : reinterpret_cast<void*>(decode_gqa_kernel<4, 1, true, false, 4>);
         return sp ? reinterpret_cast<void*>(decode_gqa_kernel<4, 2, true, true, 4>)
                   : reinterpret_cast<void*>(decode_gqa_kernel<4, 2, true, false, 4>);
-    if (sp) return reinterpret_cast<void*>(decode_gqa_kernel<4, 2, true, true>);  // partials: default shape
+    }
+    if (sp)  // partials: PW 1 or 2 with tensor-memory parking
+        return pw == 1 ? reinterpret_cast<void*>(decode_gqa_kernel<4, 1, true, true>)
+                       : reinterpret_cast<void*>(decode_gqa_kernel<4, 2, true, true>);
     switch (pw) {
         case 4: return gqa_kernel_ptr<4>();
         case 3: return gqa_kernel_ptr<3>();
+        case 1: return gqa_kernel_ptr<1>();
         default: return gqa_kernel_ptr<2>();
     }
 }
@@ -1079,7 +1101,7 @@ DecodePlan plan_decode_mma(const rkv_layer_desc& d, int64_t max_seq_len) {
     pl.REP = d.num_q_heads / d.num_kv_heads;
     const int NG = C / pl.N;
     const bool gqa = pl.N == 256, g4 = gqa && d.heads_per_group == 4;
-    const int PW = g4 ? 2 : gqa ? gqa_pw() : 1, PP = gqa ? 4 * PW : kPP;
+    const int PW = g4 ? std::min(2, gqa_pw()) : gqa ? gqa_pw() : 1, PP = gqa ? 4 * PW : kPP;
     pl.stages = gqa ? kGqaNS : kNS;
     pl.P = PW;
     pl.PP = PP;
@@ -1102,7 +1124,8 @@ DecodePlan plan_decode_mma(const rkv_layer_desc& d, int64_t max_seq_len) {
         // the occupancy query reports one CTA per SM for the tensor-memory GQA
         // kernels, which run two (128 registers x 256 threads, 2 x 92 KB: ncu's
         // block limits, tools/plan_info.py); plan the splits for two
-        if (gqa && gqa_tmem()) pl.per_sm = std::max(pl.per_sm, std::min(2, static_cast<int>((227u * 1024u) / (pl.smem + 1024))));
+        if (gqa && gqa_tmem())
+            pl.per_sm = std::max(pl.per_sm, std::min(PW == 1 ? 4 : 2, static_cast<int>((227u * 1024u) / (pl.smem + 1024))));
     }
     // splits per sequence: fill every resident CTA slot, and prefer a split count
     // whose CTA total is close to a whole number of waves (within 4x the minimum)
@@ -1124,7 +1147,7 @@ DecodePlan plan_decode_mma(const rkv_layer_desc& d, int64_t max_seq_len) {
 cudaError_t launch_decode_mma(const rkv_layer_desc& d, const DecodePlan& plan, const DecodeParams& p, cudaStream_t s) {
     const bool sp = p.tok_begin != nullptr;
     if (plan.N == 256) {
-        if (sp && plan.P != 2) return cudaErrorNotSupported;  // partials are instantiated for the default PW = 2
+        if (sp && plan.P > 2) return cudaErrorNotSupported;  // partials are instantiated for PW = 1, 2
         const void* kern = gqa_kernel(plan.P, sp, d.heads_per_group == 4);
         cudaError_t e = ensure_smem(kern, plan.smem);
         if (e != cudaSuccess) return e;

@@ -16,7 +16,7 @@ namespace rkv {
 // production choices; the epoch bumps on every change so cached plans rebuild.
 struct Options {
     std::atomic<int> force_simt{0};    // decode on the CUDA-core kernel for tensor-core shapes
-    std::atomic<int> gqa_pw{2};        // GQA kernel: warps per FWHT group (2..4)
+    std::atomic<int> gqa_pw{1};        // GQA kernel: warps per FWHT group (1..4)
     std::atomic<int> gqa_tmem{1};      // GQA kernel: park accumulators in tensor memory
     std::atomic<int> dec_splits{0};    // > 0: force the split count per sequence
     std::atomic<int> prefill_pair{0};  // 2-SM (cta_group::2) prefill attention

@@ -504,7 +504,7 @@ def debug_option():
     """Set an experiment switch for one test and restore the default after."""
     import paper_2501_16383_b200 as P
 
-    defaults = {"gqa_tmem": 1, "decode_kernel_simt": 0, "prefill_pair": 0, "decode_splits": 0}
+    defaults = {"gqa_tmem": 1, "decode_kernel_simt": 0, "prefill_pair": 0, "decode_splits": 0, "gqa_warps_per_group": 1}
     touched = []
 
     def set_(name, value):
@@ -517,7 +517,8 @@ def debug_option():
 
 
 @pytest.mark.parametrize("opt,hq,hkv,g", [("gqa_tmem=0", 32, 8, 2), ("decode_kernel_simt=1", 8, 8, 4),
-                                          ("decode_kernel_simt=1", 32, 8, 2)])
+                                          ("decode_kernel_simt=1", 32, 8, 2), ("gqa_warps_per_group=2", 32, 8, 2),
+                                          ("gqa_warps_per_group=2", 32, 8, 4), ("gqa_warps_per_group=4", 32, 8, 2)])
 def test_alternative_decode_kernels(oracle, debug_option, opt, hq, hkv, g):
     """The switch-selectable kernels (register-resident GQA, the CUDA-core
     kernel on tensor-core shapes) stay parity-green.  The layer (plan and RoPE

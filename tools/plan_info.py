@@ -10,6 +10,9 @@ import paper_2501_16383_b200 as P  # noqa: E402
 from paper_2501_16383_b200 import sharding  # noqa: E402
 from paper_2501_16383_b200 import workload as WL  # noqa: E402
 
+for kv in filter(None, os.environ.get("RKV_OPT", "").split(",")):  # experiment switches
+    k_, v_ = kv.split("=")
+    P.set_debug_option(k_, int(v_))
 for cfg_id, g in ((1, None), (2, None), (3, None), (3, 4), (4, None)):
     w = WL.CONFIGS[cfg_id]
     if g:
