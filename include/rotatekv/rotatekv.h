@@ -161,6 +161,7 @@ rkv_status rkv_cache_read(const rkv_layer_desc* desc, const rkv_cache* cache, co
 /* Experiment switches (process-global; defaults are the production
  * choices): "decode_kernel_simt" (1 = decode tensor-core shapes on the
  * CUDA-core kernel), "gqa_warps_per_group" (1..4, default 1), "gqa_tmem" (0/1),
+ * "gqa_head_sets" (1 or 2, default 2: 8 q heads per KV head share a key tile),
  * "decode_splits" (> 0 forces the split count), "prefill_pair" (1 = 2-SM
  * prefill attention), "simt_pairs", "simt_stages".  The kernel selection is
  * recorded in layer plans and RoPE tables: build them after setting a switch

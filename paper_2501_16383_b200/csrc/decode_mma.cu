@@ -560,13 +560,19 @@ __host__ __device__ inline MmaSmem gqa_smem(int C, int TT, int chunk) {
 // are parked in tensor memory between the phases that use them (tcgen05.st /
 // tcgen05.ld, a few instructions per tile), so the register peak is the larger
 // phase instead of their sum and two CTAs fit on an SM.
-template <int REP, int PW, bool TM, bool SP = false, int GR = 2>
-__global__ void __launch_bounds__(32 * 4 * PW, TM ? (PW == 1 ? 4 : 2) : 1) decode_gqa_kernel(DecodeParams p) {
-    static_assert(REP == 4, "decode_gqa_kernel: 4 q heads per KV head");
+// NS = 2 (8 or more q heads per KV head, G = 2): two sets of 4 q heads share
+// each reconstructed key tile -- logits, softmax state and P.V per set, the
+// set's accumulators parked in their own 64 columns.
+template <int REP, int PW, bool TM, bool SP = false, int GR = 2, int NS = 1>
+__global__ void __launch_bounds__(32 * 4 * PW, TM ? (NS == 2 ? 2 : PW == 1 ? 4 : 2) : 1) decode_gqa_kernel(DecodeParams p) {
+    static_assert(REP == 4, "decode_gqa_kernel: 4 q heads per KV head and set");
     static_assert(GR == 2 || (GR == 4 && PW <= 2 && TM), "decode_gqa_kernel: G = 2, or G = 4 at PW <= 2 with TMEM parking");
+    static_assert(NS == 1 || (NS == 2 && GR == 2 && PW == 1 && TM), "decode_gqa_kernel: two head sets at G = 2, PW = 1, TMEM");
     constexpr int G = 2, N = 256, NJ = 2, TT = 8 * PW, PPT = TT / 2;  // G, N: KV heads / channels per warp group
     constexpr bool X = GR == 4;  // partner-half exchange
-    constexpr uint32_t kQCols = X ? 64 : 32, kWarpCols = kQCols + 64;
+    constexpr bool Y = NS == 2;  // second head set
+    constexpr uint32_t kQCols = X || Y ? 64 : 32, kWarpCols = kQCols + 64 * NS;
+    constexpr uint32_t kAlloc = PW == 1 && !Y ? 128 : 256;
     extern __shared__ __align__(128) unsigned char smem[];
     const int C = p.C, W = C / 16, MG = C / 128, Hq = p.Hq, NG = C / N;
     const MmaSmem lay = gqa_smem(C, TT, p.chunk);
@@ -625,7 +631,7 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? (PW == 1 ? 4 : 2) : 1) decod
     }
     __shared__ uint32_t s_tmem;
     if constexpr (TM) {
-        if (warp == 0) umma::alloc<PW == 1 ? 128 : 256>(&s_tmem);
+        if (warp == 0) umma::alloc<kAlloc>(&s_tmem);
         umma::fence_before();
     }
     __syncthreads();
@@ -696,8 +702,9 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? (PW == 1 ? 4 : 2) : 1) decod
     // head r = sl ^ (g & 3): the first two reduce-scatter steps then keep / send
     // fixed slots on every lane (no selects) and leave head g & 3 in slot 0.
     // X: QA/QB[.][REP + r] hold the partner half's KV head (same slot kvh), and
-    // the upper half's own heads are negated (keys u - v)
-    constexpr int NQ = X ? 2 * REP : REP;
+    // the upper half's own heads are negated (keys u - v).  Y: QA/QB[.][REP + r]
+    // hold the second head set
+    constexpr int NQ = X || Y ? 2 * REP : REP;
     float2 QA[2][NQ], QB[2][NQ];
     {
         const float4* cs = p.rope + ((T - 1) >> 1) * 128;
@@ -710,7 +717,8 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? (PW == 1 ? 4 : 2) : 1) decod
             for (int sl = 0; sl < NQ; ++sl) {
                 const int r = (sl % REP) ^ (g & 3);
                 const bool other = sl >= REP;
-                const int hq = ((other ? gam ^ 1 : gam) * G + kvh) * REP + r;
+                const int hq = X ? ((other ? gam ^ 1 : gam) * G + kvh) * p.q_rep + p.q_rep_off + r
+                                 : (gam * G + kvh) * p.q_rep + p.q_rep_off + (other ? REP : 0) + r;
                 const float sg = X && !other && (gam & 1) ? -qs : qs;
                 float a2[2], b2[2];
 #pragma unroll
@@ -731,7 +739,13 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? (PW == 1 ? 4 : 2) : 1) decod
     const int swz = (lane >> 2) & 1;
     const int fpi = tl + 4 * (g & 3);  // rope_pair_slot(tl + 8 (g & 3)); f1 adds 16
     // softmax state of head (kvh, r = g & 3) over this lane's tokens (replicated over tl lanes)
-    float m_run = -INFINITY, l_part = 0.f, zc_part = 0.f;
+    float m_run[NS], l_part[NS], zc_part[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        m_run[s] = -INFINITY;
+        l_part[s] = 0.f;
+        zc_part[s] = 0.f;
+    }
     float acc[2][8][4];  // P.V accumulators [kvh][code position][fragment]
 #pragma unroll
     for (int h = 0; h < 2; ++h)
@@ -739,7 +753,7 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? (PW == 1 ? 4 : 2) : 1) decod
         for (int e = 0; e < 8; ++e)
 #pragma unroll
             for (int c = 0; c < 4; ++c) acc[h][e][c] = 0.f;
-    // tensor-memory parking (TM): q at columns [0, 32), accumulators [32, 96)
+    // tensor-memory parking (TM): q at columns [0, kQCols), then 64 accumulator columns per set
     auto park_q = [&]() {
         if constexpr (TM) {
 #pragma unroll
@@ -784,23 +798,23 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? (PW == 1 ? 4 : 2) : 1) decod
             }
         }
     };
-    auto park_acc = [&]() {
+    auto park_acc = [&](int set) {
         if constexpr (TM) {
 #pragma unroll
             for (int q4 = 0; q4 < 4; ++q4) {
                 uint32_t v[16];
 #pragma unroll
                 for (int i = 0; i < 16; ++i) v[i] = __float_as_uint(acc[q4 >> 1][4 * (q4 & 1) + (i >> 2)][i & 3]);
-                umma::st16(tq + kQCols + 16 * q4, v);
+                umma::st16(tq + kQCols + 64 * set + 16 * q4, v);
             }
             umma::wait_st();
         }
     };
-    auto fetch_acc = [&]() {
+    auto fetch_acc = [&](int set) {
         if constexpr (TM) {
             uint32_t v[4][16];
 #pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) umma::ld16(tq + kQCols + 16 * q4, v[q4]);
+            for (int q4 = 0; q4 < 4; ++q4) umma::ld16(tq + kQCols + 64 * set + 16 * q4, v[q4]);
 #pragma unroll
             for (int q4 = 0; q4 < 4; ++q4) {
                 umma::wait_ld(v[q4]);
@@ -810,7 +824,8 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? (PW == 1 ? 4 : 2) : 1) decod
         }
     };
     park_q();
-    park_acc();
+#pragma unroll
+    for (int s = 0; s < NS; ++s) park_acc(s);
 
     auto compute_tile = [&](int it, int slot) {
         fetch_q();
@@ -873,7 +888,7 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? (PW == 1 ? 4 : 2) : 1) decod
                 const float a0 = pv[0] + __shfl_xor_sync(0xffffffffu, pv[2], 8);
                 const float a1 = pv[1] + __shfl_xor_sync(0xffffffffu, pv[3], 8);
                 bq[2 * pq + tk] = a0 + __shfl_xor_sync(0xffffffffu, a1, 4);
-                if constexpr (X) {
+                if constexpr (X || Y) {
                     const float o0 = pv[REP] + __shfl_xor_sync(0xffffffffu, pv[REP + 2], 8);
                     const float o1 = pv[REP + 1] + __shfl_xor_sync(0xffffffffu, pv[REP + 3], 8);
                     bo[2 * pq + tk] = o0 + __shfl_xor_sync(0xffffffffu, o1, 4);
@@ -897,9 +912,9 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? (PW == 1 ? 4 : 2) : 1) decod
             }
         };
         scatter34(bq, d);
+        float dx[2];  // X: the partner half's partial logits; Y: the second head set's logits
+        if constexpr (X || Y) scatter34(bo, dx);
         if constexpr (X) {  // swap the partner half's partial logits (same lane = same head slot and tokens)
-            float dx[2];
-            scatter34(bo, dx);
             float2* xch = reinterpret_cast<float2*>(smem + lay.xch);
             xch[warp * 32 + lane] = make_float2(dx[0], dx[1]);
             pair_bar_sync(warp >> 1);  // the group's two warps
@@ -912,58 +927,62 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? (PW == 1 ? 4 : 2) : 1) decod
         const int nvw = nv - 8 * pw;
         const uint32_t okm = ~(mask_s[(tw >> 5) - mw0] >> (tw & 31)) & (nvw >= 8 ? 0xffu : nvw > 0 ? (1u << nvw) - 1u : 0u);
         const bool ok0 = (okm >> (2 * tl)) & 1u, ok1 = (okm >> (2 * tl + 1)) & 1u;
-        float mx = fmaxf(ok0 ? d[0] : -INFINITY, ok1 ? d[1] : -INFINITY);
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-        const float m_new = fmaxf(m_run, mx);
-        fetch_acc();
-        if (__any_sync(0xffffffffu, m_new > m_run)) {
-            const float alpha = m_new > m_run ? ex2(m_run - m_new) : 1.0f;
-            l_part *= alpha;
-            zc_part *= alpha;
-            // accumulator columns 2tl, 2tl+1 = heads ((2tl)&3, (2tl+1)&3) of both KV heads
+        auto softmax_pv = [&](int set, const float (&dd)[2]) {
+            float mx = fmaxf(ok0 ? dd[0] : -INFINITY, ok1 ? dd[1] : -INFINITY);
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+            const float m_new = fmaxf(m_run[set], mx);
+            fetch_acc(set);
+            if (__any_sync(0xffffffffu, m_new > m_run[set])) {
+                const float alpha = m_new > m_run[set] ? ex2(m_run[set] - m_new) : 1.0f;
+                l_part[set] *= alpha;
+                zc_part[set] *= alpha;
+                // accumulator columns 2tl, 2tl+1 = heads ((2tl)&3, (2tl+1)&3) of both KV heads
 #pragma unroll
-            for (int h = 0; h < 2; ++h)
+                for (int h = 0; h < 2; ++h)
 #pragma unroll
-                for (int c = 0; c < 2; ++c) {
-                    const int r = (2 * tl + c) & 3;
-                    const float al = __shfl_sync(0xffffffffu, alpha, ((h * 4 + r) << 2));
+                    for (int c = 0; c < 2; ++c) {
+                        const int r = (2 * tl + c) & 3;
+                        const float al = __shfl_sync(0xffffffffu, alpha, ((h * 4 + r) << 2));
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        acc[h][e][c] *= al;
-                        acc[h][e][c + 2] *= al;
+                        for (int e = 0; e < 8; ++e) {
+                            acc[h][e][c] *= al;
+                            acc[h][e][c + 2] *= al;
+                        }
                     }
-                }
-        }
-        m_run = m_new;
-        const float p0 = ok0 ? ex2(d[0] - m_run) : 0.f, p1 = ok1 ? ex2(d[1] - m_run) : 0.f;
-        l_part += p0 + p1;
-        // weights p * s (V scale of the KV head), zero point folded into zc
-        const int tt = 8 * pw + 2 * tl;  // token of d[0] within the tile
-        const uint32_t vm0 = p0 > 0.f ? vm[tt * MG + gam * G + kvh] : 0u;
-        const uint32_t vm1 = p1 > 0.f ? vm[(tt + 1) * MG + gam * G + kvh] : 0u;
-        const float ps0 = p0 * h2f(static_cast<uint16_t>(vm0 & 0xffffu)), ps1 = p1 * h2f(static_cast<uint16_t>(vm1 & 0xffffu));
-        zc_part += ps0 * h2f(static_cast<uint16_t>(vm0 >> 16)) + ps1 * h2f(static_cast<uint16_t>(vm1 >> 16));
-        const uint32_t whi = pack_h2(ps0, ps1);
-        const uint32_t wlo = pack_h2(sub_lo(ps0, whi), sub_hi(ps1, whi));
-        const uint32_t recv = __shfl_xor_sync(0xffffffffu, kvh ? whi : wlo, 16);
-        const uint32_t bv[2] = {kvh ? recv : whi, kvh ? wlo : recv};  // B columns (r = g&3, hi | lo) per KV head
-        // P.V: per KV head and code position, m16n8k8 over the warp's 8 tokens
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int word = gam * (N / 16) + h * 8 + g;
-            const int ta = 8 * pw + 2 * tl;
-            const uint32_t w0 = vc[ta * W + word], w1 = vc[(ta + 1) * W + word];
-            const uint32_t xl = prmt(w0, w1, 0x5410u), xh = prmt(w0, w1, 0x7632u);
-            const uint32_t xls = xl >> 10, xhs = xh >> 10;
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const int sh = e < 5 ? e : e - 5;
-                const uint32_t m = 0x00030003u << (2 * sh);
-                mma1688(acc[h][e], (e < 5 ? xl : xls) & m, (e < 5 ? xh : xhs) & m, bv[h]);
             }
-        }
-        park_acc();
+            m_run[set] = m_new;
+            const float p0 = ok0 ? ex2(dd[0] - m_run[set]) : 0.f, p1 = ok1 ? ex2(dd[1] - m_run[set]) : 0.f;
+            l_part[set] += p0 + p1;
+            // weights p * s (V scale of the KV head), zero point folded into zc
+            const int tt = 8 * pw + 2 * tl;  // token of dd[0] within the tile
+            const uint32_t vm0 = p0 > 0.f ? vm[tt * MG + gam * G + kvh] : 0u;
+            const uint32_t vm1 = p1 > 0.f ? vm[(tt + 1) * MG + gam * G + kvh] : 0u;
+            const float ps0 = p0 * h2f(static_cast<uint16_t>(vm0 & 0xffffu)), ps1 = p1 * h2f(static_cast<uint16_t>(vm1 & 0xffffu));
+            zc_part[set] += ps0 * h2f(static_cast<uint16_t>(vm0 >> 16)) + ps1 * h2f(static_cast<uint16_t>(vm1 >> 16));
+            const uint32_t whi = pack_h2(ps0, ps1);
+            const uint32_t wlo = pack_h2(sub_lo(ps0, whi), sub_hi(ps1, whi));
+            const uint32_t recv = __shfl_xor_sync(0xffffffffu, kvh ? whi : wlo, 16);
+            const uint32_t bv[2] = {kvh ? recv : whi, kvh ? wlo : recv};  // B columns (r = g&3, hi | lo) per KV head
+            // P.V: per KV head and code position, m16n8k8 over the warp's 8 tokens
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int word = gam * (N / 16) + h * 8 + g;
+                const int ta = 8 * pw + 2 * tl;
+                const uint32_t w0 = vc[ta * W + word], w1 = vc[(ta + 1) * W + word];
+                const uint32_t xl = prmt(w0, w1, 0x5410u), xh = prmt(w0, w1, 0x7632u);
+                const uint32_t xls = xl >> 10, xhs = xh >> 10;
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const int sh = e < 5 ? e : e - 5;
+                    const uint32_t m = 0x00030003u << (2 * sh);
+                    mma1688(acc[h][e], (e < 5 ? xl : xls) & m, (e < 5 ? xh : xhs) & m, bv[h]);
+                }
+            }
+            park_acc(set);
+        };
+        softmax_pv(0, d);
+        if constexpr (Y) softmax_pv(1, dx);
     };
 
     __syncthreads();  // mask words and plan
@@ -985,44 +1004,47 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? (PW == 1 ? 4 : 2) : 1) decod
     pdl_trigger();  // the combine may launch while the last CTAs drain
     // ---- partials: lane (g, tl) holds columns 2tl, 2tl+1 (heads r = (2tl)&3 + c, hi for tl < 2,
     // lo for tl >= 2) of channels g*16 + e and g*16 + e + 8, for both KV heads
-    float lsum = l_part, zsum = zc_part;
-    lsum += __shfl_xor_sync(0xffffffffu, lsum, 1);
-    lsum += __shfl_xor_sync(0xffffffffu, lsum, 2);
-    zsum += __shfl_xor_sync(0xffffffffu, zsum, 1);
-    zsum += __shfl_xor_sync(0xffffffffu, zsum, 2);
-    fetch_acc();
     const int64_t rbase = (static_cast<int64_t>(b) * p.NP + static_cast<int64_t>(split) * PW + pw) * Hq;
-    if (tl == 0) {
-        const int hq = (gam * G + kvh) * REP + (g & 3);
-        p.ws_ml[(rbase + hq) * 2] = m_run;
-        p.ws_ml[(rbase + hq) * 2 + 1] = lsum;
-    }
 #pragma unroll
-    for (int h = 0; h < 2; ++h)
+    for (int set = 0; set < NS; ++set) {
+        float lsum = l_part[set], zsum = zc_part[set];
+        lsum += __shfl_xor_sync(0xffffffffu, lsum, 1);
+        lsum += __shfl_xor_sync(0xffffffffu, lsum, 2);
+        zsum += __shfl_xor_sync(0xffffffffu, zsum, 1);
+        zsum += __shfl_xor_sync(0xffffffffu, zsum, 2);
+        fetch_acc(set);
+        if (tl == 0) {
+            const int hq = (gam * G + kvh) * p.q_rep + p.q_rep_off + REP * set + (g & 3);
+            p.ws_ml[(rbase + hq) * 2] = m_run[set];
+            p.ws_ml[(rbase + hq) * 2 + 1] = lsum;
+        }
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            const int r = (2 * tl + c) & 3;
-            const float z = __shfl_sync(0xffffffffu, zsum, ((h * 4 + r) << 2));
-            const int hq = (gam * G + h) * REP + r;
+        for (int h = 0; h < 2; ++h)
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const int sh = e < 5 ? e : e - 5;
-                const float sc = __int_as_float((127 + 24 - 2 * sh) << 23);
-                const float o0 = acc[h][e][c] + __shfl_xor_sync(0xffffffffu, acc[h][e][c], 2);          // hi + lo
-                const float o1 = acc[h][e][c + 2] + __shfl_xor_sync(0xffffffffu, acc[h][e][c + 2], 2);
-                if (tl < 2) {
-                    float* orow = p.ws_o + (rbase + hq) * 128 + g * 16;
-                    orow[e] = o0 * sc - z;
-                    orow[e + 8] = o1 * sc - z;
+            for (int c = 0; c < 2; ++c) {
+                const int r = (2 * tl + c) & 3;
+                const float z = __shfl_sync(0xffffffffu, zsum, ((h * 4 + r) << 2));
+                const int hq = (gam * G + h) * p.q_rep + p.q_rep_off + REP * set + r;
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const int sh = e < 5 ? e : e - 5;
+                    const float sc = __int_as_float((127 + 24 - 2 * sh) << 23);
+                    const float o0 = acc[h][e][c] + __shfl_xor_sync(0xffffffffu, acc[h][e][c], 2);          // hi + lo
+                    const float o1 = acc[h][e][c + 2] + __shfl_xor_sync(0xffffffffu, acc[h][e][c + 2], 2);
+                    if (tl < 2) {
+                        float* orow = p.ws_o + (rbase + hq) * 128 + g * 16;
+                        orow[e] = o0 * sc - z;
+                        orow[e + 8] = o1 * sc - z;
+                    }
                 }
             }
-        }
+    }
     if constexpr (TM) {
         umma::fence_before();
         __syncthreads();
         if (warp == 0) {
             umma::fence_after();
-            umma::dealloc<PW == 1 ? 128 : 256>(s_tmem);
+            umma::dealloc<kAlloc>(s_tmem);
         }
     }
 }
@@ -1035,12 +1057,13 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? (PW == 1 ? 4 : 2) : 1) decod
 // per CTA).
 bool decode_mma_supported(int G, int REP, int C) {
     if (REP == 1 && (G == 4 || G == 2 || G == 1)) return C % 512 == 0 && C / 512 * 32 <= kMmaMaxThreads;
-    if (REP == 4 && (G == 2 || G == 4)) return C % (128 * G) == 0 && C / 256 <= 4;
+    if (REP % 4 == 0 && REP <= 32 && (G == 2 || G == 4)) return C % (128 * G) == 0 && C / 256 <= 4;
     return false;
 }
 
 int mma_layout_n(const rkv_layer_desc& d) {
-    return (d.heads_per_group == 2 || d.heads_per_group == 4) && d.num_q_heads == 4 * d.num_kv_heads ? 256 : 512;
+    const int rep = d.num_q_heads / d.num_kv_heads;
+    return (d.heads_per_group == 2 || d.heads_per_group == 4) && rep % 4 == 0 && rep > 1 ? 256 : 512;
 }
 
 namespace {
@@ -1062,7 +1085,16 @@ void* gqa_kernel_ptr() {
     return gqa_tmem() ? reinterpret_cast<void*>(decode_gqa_kernel<4, PW, true>)
                       : reinterpret_cast<void*>(decode_gqa_kernel<4, PW, false>);
 }
-void* gqa_kernel(int pw, bool sp = false, bool g4 = false) {
+// 4-head sets per launch: two (one key tile, 8 q heads) when the ratio is a
+// multiple of 8 at G = 2 and PW = 1 with tensor-memory parking
+int gqa_sets(const rkv_layer_desc& d, int pw) {
+    const int rep = d.num_q_heads / d.num_kv_heads;
+    return d.heads_per_group == 2 && rep % 8 == 0 && pw == 1 && gqa_tmem() && options().gqa_sets.load() != 1 ? 2 : 1;
+}
+void* gqa_kernel(int pw, bool sp = false, bool g4 = false, int sets = 1) {
+    if (sets == 2)
+        return sp ? reinterpret_cast<void*>(decode_gqa_kernel<4, 1, true, true, 2, 2>)
+                  : reinterpret_cast<void*>(decode_gqa_kernel<4, 1, true, false, 2, 2>);
     if (g4) {  // G = 4: half-group pairs, PW 1 or 2, accumulators and queries parked in tensor memory
         if (pw == 1)
             return sp ? reinterpret_cast<void*>(decode_gqa_kernel<4, 1, true, true, 4>)
@@ -1115,7 +1147,8 @@ DecodePlan plan_decode_mma(const rkv_layer_desc& d, int64_t max_seq_len) {
     pl.per_sm = std::max(1, std::min(kCtasPerSm, static_cast<int>((227u * 1024u) / (pl.smem + 1024))));
     {
         int n = 0;
-        const void* kern = gqa ? gqa_kernel(PW, false, g4) : reinterpret_cast<const void*>(mha_kernel(NG, d.heads_per_group));
+        const int sets = gqa ? gqa_sets(d, PW) : 1;
+        const void* kern = gqa ? gqa_kernel(PW, false, g4, sets) : reinterpret_cast<const void*>(mha_kernel(NG, d.heads_per_group));
         if (ensure_smem(kern, pl.smem) == cudaSuccess &&
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, pl.NT, pl.smem) == cudaSuccess && n > 0)
             pl.per_sm = n;
@@ -1125,7 +1158,7 @@ DecodePlan plan_decode_mma(const rkv_layer_desc& d, int64_t max_seq_len) {
         // kernels, which run two (128 registers x 256 threads, 2 x 92 KB: ncu's
         // block limits, tools/plan_info.py); plan the splits for two
         if (gqa && gqa_tmem())
-            pl.per_sm = std::max(pl.per_sm, std::min(PW == 1 ? 4 : 2, static_cast<int>((227u * 1024u) / (pl.smem + 1024))));
+            pl.per_sm = std::max(pl.per_sm, std::min(PW == 1 && sets == 1 ? 4 : 2, static_cast<int>((227u * 1024u) / (pl.smem + 1024))));
     }
     // splits per sequence: fill every resident CTA slot, and prefer a split count
     // whose CTA total is close to a whole number of waves (within 4x the minimum)
@@ -1148,7 +1181,8 @@ cudaError_t launch_decode_mma(const rkv_layer_desc& d, const DecodePlan& plan, c
     const bool sp = p.tok_begin != nullptr;
     if (plan.N == 256) {
         if (sp && plan.P > 2) return cudaErrorNotSupported;  // partials are instantiated for PW = 1, 2
-        const void* kern = gqa_kernel(plan.P, sp, d.heads_per_group == 4);
+        const int sets = gqa_sets(d, plan.P);
+        const void* kern = gqa_kernel(plan.P, sp, d.heads_per_group == 4, sets);
         cudaError_t e = ensure_smem(kern, plan.smem);
         if (e != cudaSuccess) return e;
         DecodeParams pp = p;
@@ -1163,8 +1197,14 @@ cudaError_t launch_decode_mma(const rkv_layer_desc& d, const DecodePlan& plan, c
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        e = cudaLaunchKernelExC(&cfg, kern, args);
-        if (e != cudaSuccess) return e;
+        // 4 (sets = 2: 8) q heads per KV head per launch: larger ratios run as
+        // passes over disjoint head sets (each pass re-reads the cache), one combine
+        const int rep = d.num_q_heads / d.num_kv_heads;
+        for (int off = 0; off < rep; off += 4 * sets) {
+            pp.q_rep = rep;
+            pp.q_rep_off = off;
+            if ((e = cudaLaunchKernelExC(&cfg, kern, args)) != cudaSuccess) return e;
+        }
         return launch_decode_combine(p, d.batch, s);
     }
     auto kern = mha_kernel(p.C / 512, d.heads_per_group, sp);

@@ -27,6 +27,7 @@ struct Options {
     std::atomic<int> quant_vcfg{0};    // V kernel shape: 0 = 12 warps x 2 stages, 1 = 16 x 1, 2 = 14 x 1
     std::atomic<int> decode_pdl{1};    // launch the MHA decode kernel with programmatic stream serialization
     std::atomic<int> generic_tile{0};  // generic decode: tokens per tile (0 = planner)
+    std::atomic<int> gqa_sets{2};      // GQA kernel: 4-head sets sharing one key tile (1 or 2)
     std::atomic<int> epoch{0};
 };
 Options& options();
@@ -102,6 +103,9 @@ struct DecodeParams {
     int P_pairs;  // mma kernel: token pairs per tile
     int stages; // TMA ring depth
     int max_sinks;
+    // GQA kernel passes (q heads per KV head a multiple of 4): this launch
+    // covers q heads kv * q_rep + q_rep_off + 0..3 of every KV head kv
+    int q_rep, q_rep_off;
     float k_norm;  // 1/sqrt(G*d), folded into q
     float qscale;  // log2(e) / sqrt(d)
 };

@@ -118,6 +118,7 @@ extern "C" rkv_status rkv_set_debug_option(const char* name, int64_t value) {
     else if (n == "quant_vcfg") slot = &o.quant_vcfg;
     else if (n == "decode_pdl") slot = &o.decode_pdl;
     else if (n == "generic_tile") slot = &o.generic_tile;
+    else if (n == "gqa_head_sets") slot = &o.gqa_sets;
     if (!slot) return RKV_ERR_INVALID_ARGUMENT;
     slot->store(static_cast<int>(value));
     o.epoch.fetch_add(1);

@@ -24,9 +24,9 @@ from .test_gpu_parity import (COS_TOL, REL_TOL, build_layer, cache_host, cosine,
 # and 4, CUDA-core shapes, generic (tiled) shapes
 SHAPES = [(8, 8, 4), (8, 8, 2), (8, 8, 1), (12, 12, 4), (40, 40, 4), (16, 4, 2), (32, 8, 2), (16, 8, 4),
           (8, 4, 2), (16, 4, 1), (4, 4, 1), (16, 4, 4), (32, 8, 4), (64, 64, 4), (16, 16, 8), (24, 8, 8),
-          (64, 16, 4)]
+          (64, 16, 4), (64, 8, 2), (32, 4, 4)]
 TC_PREFILL = {(8, 8, 4), (8, 8, 2), (8, 8, 1), (12, 12, 4), (40, 40, 4), (16, 4, 2), (32, 8, 2), (4, 4, 1),
-              (16, 4, 4), (32, 8, 4), (64, 64, 4)}
+              (16, 4, 4), (32, 8, 4), (64, 64, 4), (64, 8, 2), (32, 4, 4)}
 
 
 def case(i):

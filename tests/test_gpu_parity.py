@@ -178,6 +178,9 @@ def oracle_decode(oracle, layer, got, b, T, q, w, perm, kraw, vraw):
     (64, 64, 4, 10000.0, 70), (64, 64, 2, 10000.0, 33), (64, 16, 2, 500000.0, 70),
     # GQA 4:1 at the paper's G = 4 on the tensor-core kernel (half-group pairs): C = 512 and 1024
     (16, 4, 4, 500000.0, 300), (32, 8, 4, 500000.0, 1025), (32, 8, 4, 10000.0, 1),
+    # GQA 8:1 (LLaMA-2/3-70B) and 16:1 as passes of the 4-head kernel, G = 2 and 4
+    (64, 8, 2, 500000.0, 300), (64, 8, 4, 500000.0, 129), (32, 4, 2, 10000.0, 77), (64, 4, 4, 10000.0, 65),
+    (96, 8, 2, 10000.0, 70), (64, 4, 2, 500000.0, 200), (128, 8, 2, 10000.0, 33),
 ])
 def test_decode_vs_oracle(oracle, hq, hkv, g, base, T):
     w = small_workload(hq, hkv, g, base=base)
@@ -200,8 +203,8 @@ def test_decode_vs_oracle(oracle, hq, hkv, g, base, T):
 
 
 @pytest.mark.parametrize("hq,hkv,g,T", [
-    (64, 16, 4, 70),    # GQA 4:1 at the paper's default G = 4 (LLaMA-3-8B shape at G = 4)
-    (96, 8, 2, 70),     # 12 q heads per KV head
+    (80, 8, 2, 70),     # 10 q heads per KV head (ratios not a multiple of 4)
+    (40, 8, 4, 70),     # 5 q heads per KV head at the paper's default G = 4
     (64, 64, 1, 90),    # G = 1 at C = 8192
     (16, 16, 8, 130),   # n = 1024
     (32, 32, 16, 65),   # n = 2048
@@ -408,7 +411,7 @@ def test_decode_matches_reference_decode_step(ref):
     assert cosine(out, want) > COS_TOL
 
 
-@pytest.mark.parametrize("hq,hkv,g", [(40, 40, 4), (32, 8, 2), (32, 8, 4), (16, 16, 8), (16, 8, 4)])
+@pytest.mark.parametrize("hq,hkv,g", [(40, 40, 4), (32, 8, 2), (32, 8, 4), (16, 16, 8), (16, 8, 4), (64, 8, 2)])
 def test_decode_deterministic(hq, hkv, g):
     """Bit-identical outputs run to run on every decode kernel family (fixed
     split partition, fixed merge order)."""
@@ -507,7 +510,8 @@ def debug_option():
     """Set an experiment switch for one test and restore the default after."""
     import paper_2501_16383_b200 as P
 
-    defaults = {"gqa_tmem": 1, "decode_kernel_simt": 0, "prefill_pair": 0, "decode_splits": 0, "gqa_warps_per_group": 1}
+    defaults = {"gqa_tmem": 1, "decode_kernel_simt": 0, "prefill_pair": 0, "decode_splits": 0, "gqa_warps_per_group": 1,
+                "gqa_head_sets": 2}
     touched = []
 
     def set_(name, value):
@@ -521,7 +525,9 @@ def debug_option():
 
 @pytest.mark.parametrize("opt,hq,hkv,g", [("gqa_tmem=0", 32, 8, 2), ("decode_kernel_simt=1", 8, 8, 4),
                                           ("decode_kernel_simt=1", 32, 8, 2), ("gqa_warps_per_group=2", 32, 8, 2),
-                                          ("gqa_warps_per_group=2", 32, 8, 4), ("gqa_warps_per_group=4", 32, 8, 2)])
+                                          ("gqa_warps_per_group=2", 32, 8, 4), ("gqa_warps_per_group=4", 32, 8, 2),
+                                          ("gqa_head_sets=1", 64, 8, 2), ("gqa_tmem=0", 64, 8, 2),
+                                          ("gqa_warps_per_group=2", 64, 8, 2)])
 def test_alternative_decode_kernels(oracle, debug_option, opt, hq, hkv, g):
     """The switch-selectable kernels (register-resident GQA, the CUDA-core
     kernel on tensor-core shapes) stay parity-green.  The layer (plan and RoPE

@@ -66,6 +66,8 @@ def check(got, want):
     (32, 8, 2, 33, (), 5),
     # GQA 4:1 at the paper's G = 4 (half-group pairs in the key reconstruction)
     (32, 8, 4, 90, (0, 3, 64), 6), (16, 4, 4, 131, (0,), 7),
+    # GQA 8:1 (the decode kernel's head passes; prefill attention is per q head)
+    (64, 8, 2, 70, (0, 9), 11), (64, 8, 4, 40, (0,), 12),
     (8, 8, 1, 70, (0, 9), 6),
     (8, 8, 2, 45, (0,), 7),
     # the widest tensor-core layer: 12 FWHT groups (C = 6144)
