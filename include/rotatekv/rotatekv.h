@@ -123,6 +123,24 @@ rkv_status rkv_quantize_kv(const rkv_layer_desc* desc, const uint16_t* k_new, co
                            const int32_t* perm, const uint8_t* sink_flags, const int64_t* start_pos,
                            int64_t num_new, const rkv_cache* cache, void* stream);
 
+/* Fused-frame append (the reference's own deployment frame).
+ * With fuse_weights (proj/src/pipeline.cpp:88-99) the projections already
+ * emit K' = P H_G k (rotated + reordered, pre-RoPE) and V' = H_128 v, and
+ * LayerKVCache::append (proj/src/kv_cache.cpp:8-22; called at
+ * proj/src/pipeline.cpp:171-176, 207-209) only quantizes them -- this call.
+ *   k_rows, v_rows : [B][num_new][C] fused-frame rows, 16-byte aligned, in
+ *                    `dtype`: RKV_ROWS_F32 (what append receives) or RKV_ROWS_F16
+ *   perm           : [C] int32 (only the sink rows use it, see below)
+ * Other arguments, errors and the device-side rules as rkv_quantize_kv.  The
+ * packed words and metadata equal rkv_quantize_kv's for raw rows whose fp32
+ * rotated + reordered image is k_rows / v_rows (the same quantizer).  Sink
+ * tokens: the sidecar keeps model-frame fp16 rows, so K' / V' go back
+ * through the inverse reorder and FWHT and are rounded to fp16. */
+typedef enum { RKV_ROWS_F32 = 0, RKV_ROWS_F16 = 1 } rkv_rows_dtype;
+rkv_status rkv_quantize_kv_fused(const rkv_layer_desc* desc, const void* k_rows, const void* v_rows, int32_t dtype,
+                                 const int32_t* perm, const uint8_t* sink_flags, const int64_t* start_pos,
+                                 int64_t num_new, const rkv_cache* cache, void* stream);
+
 /* promote_to_sink / route_sinks (proj/src/kv_cache.cpp:43-55,
  * proj/src/sink.cpp:47-63): move already-appended tokens into the fp16
  * sidecar.

@@ -177,6 +177,26 @@ public:
     // call of a given flag size.
     void append(const uint16_t* k_new, const uint16_t* v_new, int64_t num_new,
                 const std::vector<uint8_t>& sink_flags_host = {}) {
+        append_with(num_new, sink_flags_host, [&](const uint8_t* dflags, const int64_t* pos) {
+            return rkv_quantize_kv(&desc_, k_new, v_new, perm_, dflags, pos, num_new, &cache_, stream_);
+        });
+    }
+
+    // LayerKVCache::append in the reference's fused frame (fuse_weights,
+    // proj/src/pipeline.cpp:88-99): k_rows = P H_G k, v_rows = H_128 v, device
+    // [B][num_new][C] in `dtype` (RKV_ROWS_F32 = what the reference appends).
+    // Quantization only (rkv_quantize_kv_fused); otherwise as append().
+    void append_fused(const void* k_rows, const void* v_rows, rkv_rows_dtype dtype, int64_t num_new,
+                      const std::vector<uint8_t>& sink_flags_host = {}) {
+        append_with(num_new, sink_flags_host, [&](const uint8_t* dflags, const int64_t* pos) {
+            return rkv_quantize_kv_fused(&desc_, k_rows, v_rows, dtype, perm_, dflags, pos, num_new, &cache_, stream_);
+        });
+    }
+
+  private:
+    // capacity checks, flag staging and the host mirror around one append call
+    template <typename Call>
+    void append_with(int64_t num_new, const std::vector<uint8_t>& sink_flags_host, Call&& call) {
         const int B = desc_.batch;
         for (int b = 0; b < B; ++b)
             if (len_[static_cast<size_t>(b)] + num_new > desc_.max_tokens)
@@ -198,7 +218,7 @@ public:
                                        stream_), "flags");
         }
         int64_t* pos = stage_lengths();
-        check(rkv_quantize_kv(&desc_, k_new, v_new, perm_, dflags, pos, num_new, &cache_, stream_));
+        check(call(dflags, pos));
         for (int b = 0; b < B; ++b) {
             len_[static_cast<size_t>(b)] += num_new;
             if (!sink_flags_host.empty())
@@ -210,6 +230,7 @@ public:
         }
     }
 
+  public:
     // LayerKVCache::promote_to_sink / route_sinks (proj/src/kv_cache.cpp:43-55,
     // proj/src/sink.cpp:47-63): tokens[b] = token indices of sequence b;
     // k_rows/v_rows: device [B][n][C] fp16 raw rows of those tokens, n = the

@@ -5,6 +5,8 @@ _lib/librotatekv_b200.so (include/rotatekv/rotatekv.h); rotatekv.py is the
 Python host layer mirroring the reference's C++ API.
 """
 from .rotatekv import (  # noqa: F401
+    ROWS_F16,
+    ROWS_F32,
     SCALE_E4M3_CEIL,
     SCALE_FP16_CEIL,
     STAT_MEAN_ABS,

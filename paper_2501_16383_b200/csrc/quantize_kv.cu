@@ -482,6 +482,124 @@ __global__ void __launch_bounds__(32 * VW, 1) quantize_v_kernel(QuantParams p, u
     }
 }
 
+// Fused-frame append (the reference's own deployment frame).
+// With fuse_weights (proj/src/pipeline.cpp:88-99) the projections emit
+// K' = P H_G k and V' = H_128 v directly and LayerKVCache::append
+// (proj/src/kv_cache.cpp:8-22, called at proj/src/pipeline.cpp:171-176 and
+// :207-209) only quantizes them.  No rotation and no reorder, so a warp owns
+// a 1024-slot segment of a token pair of K' or V' outright: its 32-slot runs
+// straight from global memory into registers (float2 = one slot of both
+// tokens), quantize_run (the exact thresholds of the other kernels: codes
+// bit-identical to rkv_quantize_kv's when K'/V' are the fp32 rows it forms),
+// the packed words and metadata out.  Sub-item = ((sequence, token pair,
+// segment), K or V).  Sink tokens get zero words/meta and the K sub-item of
+// segment 0 owns their mask bits; their sidecar rows come from
+// fused_sink_rows_kernel (generic.cu).
+__device__ __forceinline__ void load_run(const float* r0, const float* r1, float2 (&x)[32]) {
+    const float4* a4 = reinterpret_cast<const float4*>(r0);
+    const float4* b4 = reinterpret_cast<const float4*>(r1);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const float4 a = __ldg(a4 + q), b = __ldg(b4 + q);
+        x[4 * q] = make_float2(a.x, b.x);
+        x[4 * q + 1] = make_float2(a.y, b.y);
+        x[4 * q + 2] = make_float2(a.z, b.z);
+        x[4 * q + 3] = make_float2(a.w, b.w);
+    }
+}
+__device__ __forceinline__ void load_run(const uint16_t* r0, const uint16_t* r1, float2 (&x)[32]) {
+    const uint4* a4 = reinterpret_cast<const uint4*>(r0);
+    const uint4* b4 = reinterpret_cast<const uint4*>(r1);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const uint4 a = __ldg(a4 + q), b = __ldg(b4 + q);
+        const uint16_t* ha = reinterpret_cast<const uint16_t*>(&a);
+        const uint16_t* hb = reinterpret_cast<const uint16_t*>(&b);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) x[8 * q + e] = make_float2(h2f(ha[e]), h2f(hb[e]));
+    }
+}
+
+constexpr int kFusedSeg = 1024;  // slots per warp sub-item
+template <int FMT, typename IN>
+__global__ void __launch_bounds__(128, 4) quantize_fused_kernel(QuantParams p, const IN* __restrict__ kf,
+                                                             const IN* __restrict__ vf, uint32_t subitems,
+                                                             uint32_t npairs, uint32_t nseg) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, step = (gridDim.x * blockDim.x) >> 5;
+    const int C = p.C, W = C / 16, MG = C / kQuantGroup;
+    const int num_new = static_cast<int>(p.num_new);
+    for (uint32_t si = gw; si < subitems; si += step) {
+        const bool isv = si & 1u;
+        const uint32_t rest = si >> 1, pr = udiv32(rest, nseg), bb = udiv32(pr, npairs);
+        const int b = static_cast<int>(bb), seg = static_cast<int>(rest - pr * nseg);
+        const int i0 = static_cast<int>(pr - bb * npairs) * 2;
+        const bool has1 = i0 + 1 < num_new;
+        const int s0 = seg * kFusedSeg + 32 * lane;
+        const bool act = s0 < C;  // C % 128 == 0: a 4-lane group is live or idle as a whole
+        const int64_t pos0 = p.start_pos[b] + i0;
+        const uint8_t flag = lane < 2 && p.sink_flags && i0 + lane < num_new
+                                 ? p.sink_flags[static_cast<int64_t>(b) * num_new + i0 + lane]
+                                 : uint8_t{0};
+        const IN* r0 = (isv ? vf : kf) + (static_cast<int64_t>(b) * num_new + i0) * C + (act ? s0 : 0);
+        float2 x[32];
+        load_run(r0, has1 ? r0 + C : r0, x);
+        const QuantOut qo = quantize_run<FMT>(x, lane);
+        int slot = -1;  // the sidecar slot rule of the other quantize kernels
+        if (flag && pos0 + lane >= 0 && pos0 + lane < p.max_tokens) {
+            const int i = i0 + lane;
+            int before = 0;
+            for (int q = 0; q < i; ++q) before += p.sink_flags[static_cast<int64_t>(b) * num_new + q] ? 1 : 0;
+            slot = p.cache.sink_count[b] + before;
+            if (slot >= p.max_sinks) slot = -1;
+        }
+        const int slot0 = __shfl_sync(0xffffffffu, slot, 0), slot1 = __shfl_sync(0xffffffffu, slot, 1);
+        uint32_t* codes = isv ? p.cache.v_codes : p.cache.k_codes;
+        uint32_t* mt = isv ? p.cache.v_meta : p.cache.k_meta;
+        const int64_t row0 = static_cast<int64_t>(b) * p.max_tokens + pos0;
+#pragma unroll
+        for (int tok = 0; tok < 2; ++tok) {
+            if (tok == 1 && !has1) break;
+            if (pos0 + tok < 0 || pos0 + tok >= p.max_tokens) break;  // past the cache: never written
+            const bool sink = (tok ? slot1 : slot0) >= 0;
+            const int64_t rowi = row0 + tok;
+            if (act) {
+                *reinterpret_cast<uint2*>(codes + rowi * W + s0 / 16) =
+                    sink ? make_uint2(0u, 0u) : make_uint2(qo.w[tok][0], qo.w[tok][1]);
+                if ((lane & 3) == tok) mt[rowi * MG + s0 / kQuantGroup] = sink ? 0u : qo.meta;
+            }
+        }
+        // per-token sink bits: the K sub-item of segment 0
+        if (!isv && seg == 0 && lane < 2 && (lane == 0 || has1)) {
+            const int64_t pos = pos0 + lane;
+            if (pos >= 0 && pos < p.max_tokens) {
+                uint32_t* mw = p.cache.sink_mask + static_cast<int64_t>(b) * ((p.max_tokens + 31) / 32) + (pos >> 5);
+                const uint32_t bit = 1u << (pos & 31);
+                if (slot >= 0) atomicOr(mw, bit);
+                else atomicAnd(mw, ~bit);
+            }
+        }
+    }
+}
+
+template <int FMT, typename IN>
+cudaError_t launch_quantize_fused_t(const QuantParams& p, int B, const IN* kf, const IN* vf, cudaStream_t s) {
+    const int64_t npairs = (p.num_new + 1) / 2, nseg = (p.C + kFusedSeg - 1) / kFusedSeg;
+    const int64_t sub = 2 * static_cast<int64_t>(B) * npairs * nseg;
+    if (sub >= (int64_t{1} << 31)) return cudaErrorInvalidValue;
+    static int per_sm = 0;
+    if (per_sm == 0) {
+        int n = 0;
+        const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, quantize_fused_kernel<FMT, IN>, 128, 0);
+        if (e != cudaSuccess) return e;
+        per_sm = n > 0 ? n : 1;
+    }
+    const int64_t grid = std::min<int64_t>(static_cast<int64_t>(num_sms()) * per_sm, (sub + 3) / 4);
+    quantize_fused_kernel<FMT, IN><<<static_cast<unsigned>(grid), 128, 0, s>>>(
+        p, kf, vf, static_cast<uint32_t>(sub), static_cast<uint32_t>(npairs), static_cast<uint32_t>(nseg));
+    return cudaGetLastError();
+}
+
 // Sink counts for the appended tokens (only launched with sink flags; it runs
 // after every item has read the old count).
 __global__ void quantize_sink_count_kernel(QuantParams p) {
@@ -644,6 +762,27 @@ cudaError_t launch_promote_sinks(const rkv_layer_desc& d, const QuantParams& p, 
     return cudaGetLastError();
 }
 int promote_sinks_max() { return kPromoteMax; }
+
+cudaError_t launch_quantize_fused(const rkv_layer_desc& d, const QuantParams& p, const void* k_rows,
+                                  const void* v_rows, int dtype, cudaStream_t s) {
+    cudaError_t e;
+    const bool e4 = p.scale_format == RKV_SCALE_E4M3_CEIL;
+    if (dtype == RKV_ROWS_F16) {
+        const auto* kf = static_cast<const uint16_t*>(k_rows);
+        const auto* vf = static_cast<const uint16_t*>(v_rows);
+        e = e4 ? launch_quantize_fused_t<RKV_SCALE_E4M3_CEIL>(p, d.batch, kf, vf, s)
+               : launch_quantize_fused_t<RKV_SCALE_FP16_CEIL>(p, d.batch, kf, vf, s);
+    } else {
+        const auto* kf = static_cast<const float*>(k_rows);
+        const auto* vf = static_cast<const float*>(v_rows);
+        e = e4 ? launch_quantize_fused_t<RKV_SCALE_E4M3_CEIL>(p, d.batch, kf, vf, s)
+               : launch_quantize_fused_t<RKV_SCALE_FP16_CEIL>(p, d.batch, kf, vf, s);
+    }
+    if (e != cudaSuccess || !p.sink_flags) return e;
+    if ((e = launch_fused_sink_rows(d, p, k_rows, v_rows, dtype, s)) != cudaSuccess) return e;
+    quantize_sink_count_kernel<<<d.batch, 256, 0, s>>>(p);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_quantize(const rkv_layer_desc& d, const QuantParams& p, cudaStream_t s) {
     const int n = d.heads_per_group * d.head_dim;

@@ -305,6 +305,40 @@ rkv_status rkv_quantize_kv(const rkv_layer_desc* desc, const uint16_t* k_new, co
     return RKV_OK;
 }
 
+rkv_status rkv_quantize_kv_fused(const rkv_layer_desc* desc, const void* k_rows, const void* v_rows, int32_t dtype,
+                                 const int32_t* perm, const uint8_t* sink_flags, const int64_t* start_pos,
+                                 int64_t num_new, const rkv_cache* cache, void* stream) {
+    rkv_status st = validate(desc);
+    if (st != RKV_OK) return st;
+    if ((st = check_cache(cache)) != RKV_OK) return st;
+    if (dtype != RKV_ROWS_F32 && dtype != RKV_ROWS_F16)
+        return fail(RKV_ERR_INVALID_ARGUMENT, "quantize_kv_fused: dtype must be RKV_ROWS_F32 or RKV_ROWS_F16");
+    if (num_new < 0) return fail(RKV_ERR_INVALID_ARGUMENT, "quantize_kv_fused: num_new must be >= 0");
+    if (num_new == 0) return RKV_OK;
+    if (!k_rows || !v_rows || !perm || !start_pos)
+        return fail(RKV_ERR_INVALID_ARGUMENT, "quantize_kv_fused: k_rows, v_rows, perm and start_pos must be non-null");
+    if (num_new > desc->max_tokens) return fail(RKV_ERR_OUT_OF_RANGE, "quantize_kv_fused: num_new exceeds max_tokens");
+    if ((reinterpret_cast<uintptr_t>(k_rows) | reinterpret_cast<uintptr_t>(v_rows)) & 15u)
+        return fail(RKV_ERR_INVALID_ARGUMENT, "quantize_kv_fused: k_rows and v_rows must be 16-byte aligned");
+    if (sink_flags && (!cache->sink_k || !cache->sink_v || !cache->sink_pos))
+        return fail(RKV_ERR_INVALID_ARGUMENT, "quantize_kv_fused: sink flags need the sidecar arrays");
+    rkv::QuantParams p{};
+    p.perm = perm;
+    p.sink_flags = sink_flags;
+    p.start_pos = start_pos;
+    p.num_new = num_new;
+    p.max_tokens = desc->max_tokens;
+    p.C = desc->num_kv_heads * desc->head_dim;
+    p.max_sinks = desc->max_sinks;
+    p.scale_format = desc->scale_format;
+    p.k_norm = 1.0f / std::sqrt(static_cast<float>(desc->heads_per_group * desc->head_dim));
+    p.v_norm = 1.0f / std::sqrt(static_cast<float>(desc->head_dim));
+    p.cache = *cache;
+    cudaError_t e = rkv::launch_quantize_fused(*desc, p, k_rows, v_rows, dtype, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "quantize_kv_fused");
+    return RKV_OK;
+}
+
 rkv_status rkv_promote_sinks(const rkv_layer_desc* desc, const rkv_cache* cache, const int64_t* tokens,
                              int64_t num_tokens, const uint16_t* k_rows, const uint16_t* v_rows, int32_t* promoted,
                              void* stream) {

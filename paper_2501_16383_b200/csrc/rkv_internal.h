@@ -139,6 +139,11 @@ struct PrefillParams {
 
 // quantize_kv.cu
 cudaError_t launch_quantize(const rkv_layer_desc& d, const QuantParams& p, cudaStream_t s);
+// fused-frame append (rkv_quantize_kv_fused): K'/V' rows in `dtype` (rkv_rows_dtype)
+cudaError_t launch_quantize_fused(const rkv_layer_desc& d, const QuantParams& p, const void* k_rows,
+                                  const void* v_rows, int dtype, cudaStream_t s);
+cudaError_t launch_fused_sink_rows(const rkv_layer_desc& d, const QuantParams& p, const void* k_rows,
+                                   const void* v_rows, int dtype, cudaStream_t s);
 cudaError_t launch_promote_sinks(const rkv_layer_desc& d, const QuantParams& p, const int64_t* tokens, int n,
                                  int32_t* promoted, cudaStream_t s);
 int promote_sinks_max();

@@ -31,6 +31,7 @@ LIB_PATH = os.environ.get("RKV_LIB") or os.path.join(_PKG, "_lib", "librotatekv_
 
 RKV_OK, RKV_ERR_INVALID_ARGUMENT, RKV_ERR_OUT_OF_RANGE, RKV_ERR_RUNTIME, RKV_ERR_CUDA = range(5)
 SCALE_FP16_CEIL, SCALE_E4M3_CEIL = 0, 1
+ROWS_F32, ROWS_F16 = 0, 1  # rkv_rows_dtype: fused-frame append inputs
 STAT_SUM, STAT_MEAN_ABS = 0, 1
 
 
@@ -80,6 +81,7 @@ def lib():
         L.rkv_rope_table_bytes.argtypes = [D, C.c_int64]
         L.rkv_rope_table_init.argtypes = [D, P, C.c_int64, P]
         L.rkv_quantize_kv.argtypes = [D, P, P, P, P, P, C.c_int64, C.POINTER(CacheView), P]
+        L.rkv_quantize_kv_fused.argtypes = [D, P, P, C.c_int32, P, P, P, C.c_int64, C.POINTER(CacheView), P]
         L.rkv_decode_workspace_bytes.restype = C.c_size_t
         L.rkv_decode_workspace_bytes.argtypes = [D, C.c_int64]
         L.rkv_decode_attention.argtypes = [D, P, P, C.c_int64, C.POINTER(CacheView), P, P, P, P, C.c_size_t, P]
@@ -113,7 +115,7 @@ def lib():
         L.rkv_set_debug_option.argtypes = [C.c_char_p, C.c_int64]
         L.rkv_decode_plan_info.argtypes = [D, C.c_int64, C.POINTER(C.c_int64)]
         for name in ("rkv_promote_sinks", "rkv_set_debug_option", "rkv_decode_plan_info", "rkv_cache_read", "rkv_layer_validate", "rkv_cache_carve", "rkv_cache_reset", "rkv_rope_table_init",
-                     "rkv_quantize_kv", "rkv_decode_attention", "rkv_rotate_keys", "rkv_calibrate_reorder",
+                     "rkv_quantize_kv", "rkv_quantize_kv_fused", "rkv_decode_attention", "rkv_rotate_keys", "rkv_calibrate_reorder",
                      "rkv_detect_sinks", "rkv_detect_sinks_device", "rkv_layer_plan_build", "rkv_layer_plan_init",
                      "rkv_calibrate_reorder_device", "rkv_cache_export", "rkv_cache_import",
                      "rkv_prefill_attention", "rkv_decode_attention_partial", "rkv_decode_merge"):
@@ -512,6 +514,44 @@ class RotateKVLayer:
                                      _ptr(start_t), n, C.byref(self._view), self._stream()))
         self.lengths = np.maximum(self.lengths, start + n)
         self._keep = (k, v, flags_t, start_t)  # keep inputs alive until the stream consumes them
+
+    def append_fused(self, k_rows, v_rows, sink_flags=None, start_pos=None):
+        """LayerKVCache::append in the reference's fused frame (proj/src/
+        kv_cache.cpp:8-22 after fuse_weights, proj/src/pipeline.cpp:88-99):
+        k_rows = P H_G k (rotated + reordered), v_rows = H_128 v, [B, n, C]
+        fp32 (what the reference appends) or fp16 CUDA tensors.  Quantization
+        only; sinks and positions as append()."""
+        torch = self.torch
+        B, Cc = self.cfg.batch, self.cfg.channels
+        if k_rows.dtype not in (torch.float32, torch.float16) or v_rows.dtype != k_rows.dtype:
+            raise ValueError("cache append_fused: rows must be fp32 or fp16 (both the same)")
+        if k_rows.dim() != 3 or k_rows.shape[0] != B or k_rows.shape[2] != Cc or v_rows.shape != k_rows.shape:
+            raise ValueError("cache append: row length must equal channel count")
+        n = k_rows.shape[1]
+        start = self.lengths.copy() if start_pos is None else _np(start_pos, np.int64)
+        if np.any(start < 0) or np.any(start + n > self.cfg.max_tokens):
+            raise IndexError("cache: token index out of range")
+        flags_t = None
+        if sink_flags is not None:
+            f = torch.as_tensor(sink_flags).to(torch.uint8)
+            if tuple(f.shape) != (B, n):
+                raise ValueError("sink flags must be [batch, new tokens]")
+            add = f.cpu().numpy().astype(np.int64).sum(axis=1)
+            if np.any(self.sink_counts + add > self.cfg.max_sinks):
+                raise IndexError("cache: sink sidecar capacity exceeded")
+            self.sink_counts += add
+            fh = f.cpu().numpy()
+            for b in range(B):
+                self.sink_tokens[b].update(int(start[b]) + np.nonzero(fh[b])[0])
+            flags_t = f.to(self.device).contiguous()
+        k_rows = k_rows.contiguous()
+        v_rows = v_rows.contiguous()
+        dtype = ROWS_F32 if k_rows.dtype == torch.float32 else ROWS_F16
+        start_t = torch.from_numpy(start).to(self.device)
+        _check(lib().rkv_quantize_kv_fused(C.byref(self._desc), _ptr(k_rows), _ptr(v_rows), dtype, _ptr(self.perm),
+                                           _ptr(flags_t), _ptr(start_t), n, C.byref(self._view), self._stream()))
+        self.lengths = np.maximum(self.lengths, start + n)
+        self._keep = (k_rows, v_rows, flags_t, start_t)
 
     def workspace(self, max_seq_len: int):
         need = lib().rkv_decode_workspace_bytes(C.byref(self._desc), max_seq_len)
