@@ -477,13 +477,16 @@ def bench_cfg2_step(dev, steps):
     return res
 
 
-def bench_quantize_cfg5(dev, world, rank):
+def bench_quantize_cfg5(dev, world, rank, fused=None):
     """BASELINE config 5: bulk prefill quantization of a 40-layer
     LLaMA-2-13B-shaped KV cache (128 sequences x 2048 tokens, 40 heads x 128,
     per-layer seeded outlier channels and reorder permutations, sink at token
     0), batch-sharded 128/N.  Inputs are generated per layer on the device
     (214.7 GB of fp16 K/V does not fit one GPU); only the quantize-append
-    kernels are timed (CUDA events, device-resident positions and flags)."""
+    kernels are timed (CUDA events, device-resident positions and flags).
+    fused = "f16" / "f32": the same rows appended in the fused frame
+    (rkv_quantize_kv_fused: quantization only), as fp16 or fp32
+    rows -- the generated values stand in for K' / V'."""
     import torch
 
     import paper_2501_16383_b200 as P
@@ -495,8 +498,10 @@ def bench_quantize_cfg5(dev, world, rank):
     _, B = sharding.batch_shard(w.batch, world, rank)
     T, Cc = w.tokens, w.channels
     stream = torch.cuda.current_stream(dev)
-    k = torch.empty(B, T, Cc, dtype=torch.float16, device=dev)
+    k = torch.empty(B, T, Cc, dtype=torch.float32 if fused == "f32" else torch.float16, device=dev)
     v = torch.empty_like(k)
+    append = (lambda lay: lay.append_device(k, v, start, flags)) if fused is None else \
+        (lambda lay: lay.append_fused_device(k, v, start, flags))
     flags = torch.zeros(B, T, dtype=torch.uint8, device=dev)
     flags[:, 0] = 1
     start = torch.zeros(B, dtype=torch.int64, device=dev)
@@ -513,22 +518,28 @@ def bench_quantize_cfg5(dev, world, rank):
             v[b0:b0 + vv.shape[0]].copy_(vv)
             del kk, vv
         if layer == 0:  # warm-up launch (same shapes)
-            lay.append_device(k, v, start, flags)
+            append(lay)
             lay.reset()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        lay.append_device(k, v, start, flags)
+        append(lay)
         e1.record(stream)
         torch.cuda.synchronize()
         total_ms += e0.elapsed_time(e1)
         layers.append(lay)  # keep the 40-layer cache resident
     total_ms = max_over_ranks([total_ms], dev, world)[0]
     rows = B * T * w.layers
-    bytes_ = rows * (2 * Cc * 2 + 2 * (Cc // 4 + Cc // 32))
+    bytes_ = rows * (2 * Cc * k.element_size() + 2 * (Cc // 4 + Cc // 32))
     res = {"workload": w.name, "sequences_per_gpu": B, "layers": w.layers, "token_rows_per_gpu": rows,
            "ms": total_ms, "tokens_per_s": w.batch * T * w.layers / (total_ms / 1e3),
-           "roofline": hbm_roofline(bytes_, total_ms, "rkv_quantize_kv (40 launches)")}
+           "roofline": hbm_roofline(bytes_, total_ms, "rkv_quantize_kv (40 launches)" if fused is None else
+                                    f"rkv_quantize_kv_fused, {fused} rows (40 launches)")}
+    if fused is not None:
+        res["input"] = f"fused-frame rows ({fused}): quantization only, no rotation or reorder"
+        del layers, k, v
+        torch.cuda.empty_cache()
+        return res
     try:  # the reference's quantize chain (rotate_rows -> apply_reorder -> quantize_token) on the host
         import oracle
 
@@ -789,11 +800,15 @@ def run_ours(args):
     extras = {}
     if not args.no_extras:
         for key, fn in (("cfg3", lambda: bench_extra_decode(3, dev, world, rank, min(args.steps, 30))),
-                        # GQA 4:1 at the paper's default rotation G = 4 (generic tiled kernel)
+                        # GQA 4:1 at the paper's default rotation G = 4 (tensor-core half-group pairs)
                         ("cfg3_g4", lambda: bench_extra_decode(3, dev, world, rank, min(args.steps, 10), g=4)),
                         ("cfg2", (lambda: bench_cfg2_step(dev, min(args.steps, 30))) if world == 1 else None),
                         ("prefill_cfg1", (lambda: bench_prefill_cfg1(dev)) if world == 1 and rank == 0 else None),
-                        ("quantize_cfg5", lambda: bench_quantize_cfg5(dev, world, rank))):
+                        ("quantize_cfg5", lambda: bench_quantize_cfg5(dev, world, rank)),
+                        # the same rows in the reference's fused frame (quantization only): fp32 rows
+                        # (what LayerKVCache::append receives) and fp16 rows
+                        ("quantize_cfg5_fused", lambda: bench_quantize_cfg5(dev, world, rank, fused="f32")),
+                        ("quantize_cfg5_fused_f16", lambda: bench_quantize_cfg5(dev, world, rank, fused="f16"))):
             if fn is None:
                 continue
             try:

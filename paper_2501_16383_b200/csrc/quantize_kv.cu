@@ -487,32 +487,37 @@ __global__ void __launch_bounds__(32 * VW, 1) quantize_v_kernel(QuantParams p, u
 // K' = P H_G k and V' = H_128 v directly and LayerKVCache::append
 // (proj/src/kv_cache.cpp:8-22, called at proj/src/pipeline.cpp:171-176 and
 // :207-209) only quantizes them.  No rotation and no reorder, so a warp owns
-// a 1024-slot segment of a token pair of K' or V' outright: its 32-slot runs
-// straight from global memory into registers (float2 = one slot of both
-// tokens), quantize_run (the exact thresholds of the other kernels: codes
-// bit-identical to rkv_quantize_kv's when K'/V' are the fp32 rows it forms),
-// the packed words and metadata out.  Sub-item = ((sequence, token pair,
-// segment), K or V).  Sink tokens get zero words/meta and the K sub-item of
-// segment 0 owns their mask bits; their sidecar rows come from
+// a 1024-slot segment of a token pair of K' or V' outright.  Each lane's 32
+// slots of both tokens are copied by the warp with coalesced 16-byte
+// cp.async into padded per-lane runs (conflict-free LDS.128 afterwards),
+// double-buffered so the next sub-item streams in while this one is
+// quantized; then quantize_run (the exact thresholds of the other kernels:
+// codes bit-identical to rkv_quantize_kv's when K'/V' are the fp32 rows it
+// forms) and the packed words and metadata out.  Sub-item = ((sequence,
+// token pair, segment), K or V).  Sink tokens get zero words/meta and the K
+// sub-item of segment 0 owns their mask bits; their sidecar rows come from
 // fused_sink_rows_kernel (generic.cu).
-__device__ __forceinline__ void load_run(const float* r0, const float* r1, float2 (&x)[32]) {
-    const float4* a4 = reinterpret_cast<const float4*>(r0);
-    const float4* b4 = reinterpret_cast<const float4*>(r1);
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// one lane's 32-slot run of both tokens (padded runs in shared memory) -> float2 per slot
+__device__ __forceinline__ void read_run(const float* r0, const float* r1, float2 (&x)[32]) {
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-        const float4 a = __ldg(a4 + q), b = __ldg(b4 + q);
-        x[4 * q] = make_float2(a.x, b.x);
-        x[4 * q + 1] = make_float2(a.y, b.y);
-        x[4 * q + 2] = make_float2(a.z, b.z);
-        x[4 * q + 3] = make_float2(a.w, b.w);
+        const uint4 a = lds128(r0 + 4 * q), b = lds128(r1 + 4 * q);
+        x[4 * q] = make_float2(__uint_as_float(a.x), __uint_as_float(b.x));
+        x[4 * q + 1] = make_float2(__uint_as_float(a.y), __uint_as_float(b.y));
+        x[4 * q + 2] = make_float2(__uint_as_float(a.z), __uint_as_float(b.z));
+        x[4 * q + 3] = make_float2(__uint_as_float(a.w), __uint_as_float(b.w));
     }
 }
-__device__ __forceinline__ void load_run(const uint16_t* r0, const uint16_t* r1, float2 (&x)[32]) {
-    const uint4* a4 = reinterpret_cast<const uint4*>(r0);
-    const uint4* b4 = reinterpret_cast<const uint4*>(r1);
+__device__ __forceinline__ void read_run(const uint16_t* r0, const uint16_t* r1, float2 (&x)[32]) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-        const uint4 a = __ldg(a4 + q), b = __ldg(b4 + q);
+        const uint4 a = lds128(r0 + 8 * q), b = lds128(r1 + 8 * q);
         const uint16_t* ha = reinterpret_cast<const uint16_t*>(&a);
         const uint16_t* hb = reinterpret_cast<const uint16_t*>(&b);
 #pragma unroll
@@ -521,29 +526,100 @@ __device__ __forceinline__ void load_run(const uint16_t* r0, const uint16_t* r1,
 }
 
 constexpr int kFusedSeg = 1024;  // slots per warp sub-item
+template <typename IN>
+struct FusedStage {
+    static constexpr int run = 32 * static_cast<int>(sizeof(IN));  // bytes of one lane's 32 slots
+    static constexpr int stride = run + 16;                         // padded: conflict-free LDS.128
+    static constexpr int chunks = run / 16;
+    static constexpr int buf = 2 * 32 * stride;                     // both tokens
+    static constexpr int warp_bytes = 2 * buf;                      // double-buffered
+};
+constexpr int kFusedWarps = 4;
+#ifndef RKV_FUSED_F16_CTAS
+#define RKV_FUSED_F16_CTAS 4  // resident CTAs per SM for fp16 rows (fp32 rows: 3, the shared memory)
+#endif
+
 template <int FMT, typename IN>
-__global__ void __launch_bounds__(128, 4) quantize_fused_kernel(QuantParams p, const IN* __restrict__ kf,
-                                                             const IN* __restrict__ vf, uint32_t subitems,
-                                                             uint32_t npairs, uint32_t nseg) {
-    const int lane = threadIdx.x & 31;
-    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, step = (gridDim.x * blockDim.x) >> 5;
+__global__ void __launch_bounds__(32 * kFusedWarps, sizeof(IN) == 4 ? 3 : RKV_FUSED_F16_CTAS) quantize_fused_kernel(QuantParams p, const IN* __restrict__ kf,
+                                                                            const IN* __restrict__ vf,
+                                                                            uint32_t subitems, uint32_t npairs,
+                                                                            uint32_t nseg) {
+    using S = FusedStage<IN>;
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t gw = blockIdx.x * kFusedWarps + warp, step = gridDim.x * kFusedWarps;
     const int C = p.C, W = C / 16, MG = C / kQuantGroup;
     const int num_new = static_cast<int>(p.num_new);
-    for (uint32_t si = gw; si < subitems; si += step) {
-        const bool isv = si & 1u;
+    const uint32_t wbase = smem_u32(smem) + static_cast<uint32_t>(warp * S::warp_bytes);
+    // sub-item si = ((b npairs + ip) nseg + seg) 2 + isv; a warp's sub-items
+    // advance by `step`: cursors carry (b, ip, seg, isv) forward with compares
+    // instead of divisions (as quantize_v_kernel)
+    struct Sub {
+        uint32_t b, ip, seg, isv;
+    };
+    auto locate = [&](uint32_t si) {
         const uint32_t rest = si >> 1, pr = udiv32(rest, nseg), bb = udiv32(pr, npairs);
-        const int b = static_cast<int>(bb), seg = static_cast<int>(rest - pr * nseg);
-        const int i0 = static_cast<int>(pr - bb * npairs) * 2;
+        return Sub{bb, pr - bb * npairs, rest - pr * nseg, si & 1u};
+    };
+    const Sub dstep = locate(step);
+    auto advance = [&](Sub& c) {
+        c.isv += dstep.isv;
+        const uint32_t c0 = c.isv >> 1;
+        c.isv &= 1u;
+        c.seg += dstep.seg + c0;
+        const uint32_t c1 = c.seg >= nseg ? 1u : 0u;
+        c.seg -= c1 * nseg;
+        c.ip += dstep.ip + c1;
+        const uint32_t c2 = c.ip >= npairs ? 1u : 0u;
+        c.ip -= c2 * npairs;
+        c.b += dstep.b + c2;
+    };
+    // chunk c of the segment (16 bytes, coalesced over the warp) -> run c / chunks, part c % chunks
+    auto issue = [&](const Sub& u, int buf) {
+        const int seg = static_cast<int>(u.seg), i0 = static_cast<int>(u.ip) * 2;
+        const int live = min(kFusedSeg, C - seg * kFusedSeg) * static_cast<int>(sizeof(IN)) / 16;
+        const uint8_t* src = reinterpret_cast<const uint8_t*>((u.isv ? vf : kf) +
+                                                              (static_cast<int64_t>(u.b) * num_new + i0) * C +
+                                                              seg * kFusedSeg);
+        const uint32_t dst = wbase + static_cast<uint32_t>(buf * S::buf);
         const bool has1 = i0 + 1 < num_new;
+#pragma unroll
+        for (int tok = 0; tok < 2; ++tok) {
+            const uint8_t* st = tok && has1 ? src + static_cast<int64_t>(C) * sizeof(IN) : src;
+#pragma unroll
+            for (int j = 0; j < S::chunks; ++j) {
+                const int c = j * 32 + lane;
+                if (c < live)
+                    cp_async16(dst + static_cast<uint32_t>(tok * 32 * S::stride + (c / S::chunks) * S::stride +
+                                                           (c % S::chunks) * 16),
+                               st + c * 16);
+            }
+        }
+        cp_async_commit();
+    };
+    Sub cur = locate(gw), nxt = locate(gw + step);  // this sub-item, the one whose copies we issue next
+    if (gw < subitems) issue(cur, 0);
+    int buf = 0;
+    for (uint32_t si = gw; si < subitems; si += step, buf ^= 1, advance(cur), advance(nxt)) {
+        if (si + step < subitems) issue(nxt, buf ^ 1);
+        else cp_async_commit();  // an empty group keeps wait_group 1 meaning "this sub-item's copies"
+        const Sub& c = cur;
+        const int b = static_cast<int>(c.b), seg = static_cast<int>(c.seg), i0 = static_cast<int>(c.ip) * 2;
+        const bool isv = c.isv != 0u, has1 = i0 + 1 < num_new;
         const int s0 = seg * kFusedSeg + 32 * lane;
         const bool act = s0 < C;  // C % 128 == 0: a 4-lane group is live or idle as a whole
         const int64_t pos0 = p.start_pos[b] + i0;
         const uint8_t flag = lane < 2 && p.sink_flags && i0 + lane < num_new
                                  ? p.sink_flags[static_cast<int64_t>(b) * num_new + i0 + lane]
                                  : uint8_t{0};
-        const IN* r0 = (isv ? vf : kf) + (static_cast<int64_t>(b) * num_new + i0) * C + (act ? s0 : 0);
+        cp_async_wait1();
+        __syncwarp();  // every lane's copies of this buffer have landed
         float2 x[32];
-        load_run(r0, has1 ? r0 + C : r0, x);
+        {
+            const uint8_t* rb = smem + warp * S::warp_bytes + buf * S::buf + lane * S::stride;
+            read_run(reinterpret_cast<const IN*>(rb), reinterpret_cast<const IN*>(rb + 32 * S::stride), x);
+        }
+        __syncwarp();  // the buffer is refilled by the next iteration's issue
         const QuantOut qo = quantize_run<FMT>(x, lane);
         int slot = -1;  // the sidecar slot rule of the other quantize kernels
         if (flag && pos0 + lane >= 0 && pos0 + lane < p.max_tokens) {
@@ -587,15 +663,19 @@ cudaError_t launch_quantize_fused_t(const QuantParams& p, int B, const IN* kf, c
     const int64_t npairs = (p.num_new + 1) / 2, nseg = (p.C + kFusedSeg - 1) / kFusedSeg;
     const int64_t sub = 2 * static_cast<int64_t>(B) * npairs * nseg;
     if (sub >= (int64_t{1} << 31)) return cudaErrorInvalidValue;
+    const size_t smem = static_cast<size_t>(kFusedWarps) * FusedStage<IN>::warp_bytes;
+    cudaError_t e = ensure_smem_k(quantize_fused_kernel<FMT, IN>, smem);
+    if (e != cudaSuccess) return e;
     static int per_sm = 0;
     if (per_sm == 0) {
         int n = 0;
-        const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, quantize_fused_kernel<FMT, IN>, 128, 0);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, quantize_fused_kernel<FMT, IN>, 32 * kFusedWarps, smem);
         if (e != cudaSuccess) return e;
         per_sm = n > 0 ? n : 1;
     }
-    const int64_t grid = std::min<int64_t>(static_cast<int64_t>(num_sms()) * per_sm, (sub + 3) / 4);
-    quantize_fused_kernel<FMT, IN><<<static_cast<unsigned>(grid), 128, 0, s>>>(
+    const int64_t grid =
+        std::min<int64_t>(static_cast<int64_t>(num_sms()) * per_sm, (sub + kFusedWarps - 1) / kFusedWarps);
+    quantize_fused_kernel<FMT, IN><<<static_cast<unsigned>(grid), 32 * kFusedWarps, smem, s>>>(
         p, kf, vf, static_cast<uint32_t>(sub), static_cast<uint32_t>(npairs), static_cast<uint32_t>(nseg));
     return cudaGetLastError();
 }

@@ -646,6 +646,19 @@ class RotateKVLayer:
         _check(lib().rkv_quantize_kv(C.byref(self._desc), _ptr(k), _ptr(v), _ptr(self.perm), _ptr(sink_flags_t),
                                      _ptr(start_t), k.shape[1], C.byref(self._view), self._stream()))
 
+    def append_fused_device(self, k_rows, v_rows, start_t, sink_flags_t=None):
+        """append_fused without the host mirror (device-resident start
+        positions, no allocation); fp32 or fp16 rows."""
+        B, Cc = self.cfg.batch, self.cfg.channels
+        if k_rows.dim() != 3 or tuple(k_rows.shape[::2]) != (B, Cc) or v_rows.shape != k_rows.shape:
+            raise ValueError("cache append: row length must equal channel count")
+        if k_rows.shape[1] > self.cfg.max_tokens or tuple(start_t.shape) != (B,):
+            raise IndexError("cache: token index out of range")
+        dtype = ROWS_F32 if k_rows.dtype == self.torch.float32 else ROWS_F16
+        _check(lib().rkv_quantize_kv_fused(C.byref(self._desc), _ptr(k_rows), _ptr(v_rows), dtype, _ptr(self.perm),
+                                           _ptr(sink_flags_t), _ptr(start_t), k_rows.shape[1], C.byref(self._view),
+                                           self._stream()))
+
     def decode_step(self, k_new, v_new, q):
         """decode_step without projections: append the new token (never a sink,
         proj/src/pipeline.cpp:207-209), then attend over the whole cache."""
