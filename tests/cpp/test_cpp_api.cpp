@@ -189,6 +189,45 @@ int main() {
             cudaFree(dpo);
         }
 
+        // LayerKVCache::append in the fused frame (fuse_weights, proj/src/pipeline.cpp:88-99):
+        // the oracle's K' = reorder(H_G k) and V' = H_128 v as fp32 rows give the same words
+        {
+            std::vector<float> kr(k.size()), kf(k.size()), vf(v.size());
+            for (size_t i = 0; i < k.size(); ++i) {
+                kr[i] = rkvo_half_to_float(k[i]);
+                vf[i] = rkvo_half_to_float(v[i]);
+            }
+            rkvo_rotate_rows(kr.data(), static_cast<int64_t>(B) * T, D, G, H);
+            rkvo_apply_reorder(kr.data(), static_cast<int64_t>(B) * T, C, perm.data(), 0, kf.data());
+            rkvo_rotate_rows(vf.data(), static_cast<int64_t>(B) * T, D, 1, H);
+            float *dkf = nullptr, *dvf = nullptr;
+            cudaMalloc(&dkf, kf.size() * 4);
+            cudaMalloc(&dvf, vf.size() * 4);
+            cudaMemcpy(dkf, kf.data(), kf.size() * 4, cudaMemcpyHostToDevice);
+            cudaMemcpy(dvf, vf.data(), vf.size() * 4, cudaMemcpyHostToDevice);
+            rotatekv_b200::DeviceLayerCache fused(desc, perm);
+            fused.append_fused(dkf, dvf, RKV_ROWS_F32, T, flags);
+            CHECK(fused.size(0) == T && fused.sink_count(1) == 1);
+            const auto& fv = fused.view();
+            std::vector<uint32_t> fkc(kc.size()), fkm(km.size()), fvc(vc.size()), fvm(vm.size());
+            cudaMemcpy(fkc.data(), fv.k_codes, fkc.size() * 4, cudaMemcpyDeviceToHost);
+            cudaMemcpy(fkm.data(), fv.k_meta, fkm.size() * 4, cudaMemcpyDeviceToHost);
+            cudaMemcpy(fvc.data(), fv.v_codes, fvc.size() * 4, cudaMemcpyDeviceToHost);
+            cudaMemcpy(fvm.data(), fv.v_meta, fvm.size() * 4, cudaMemcpyDeviceToHost);
+            bool same = true;
+            for (int b = 0; b < B; ++b)
+                for (int t = 0; t < T; ++t) {
+                    const size_t r = static_cast<size_t>(b) * desc.max_tokens + t;
+                    for (int w = 0; w < W; ++w) same = same && fkc[r * W + w] == kc[r * W + w] && fvc[r * W + w] == vc[r * W + w];
+                    for (int m = 0; m < MG; ++m) same = same && fkm[r * MG + m] == km[r * MG + m] && fvm[r * MG + m] == vm[r * MG + m];
+                }
+            CHECK(same);
+            CHECK_THROWS_AS(fused.append_fused(dkf, dvf, RKV_ROWS_F32, 9), std::out_of_range);
+            CHECK_THROWS_AS(fused.append_fused(dkf, dvf, static_cast<rkv_rows_dtype>(7), 1), std::invalid_argument);
+            cudaFree(dkf);
+            cudaFree(dvf);
+        }
+
         // LayerKVCache::serialize / deserialize round trip (fp16-scale wire format)
         const std::vector<uint8_t> blob = cache.serialize(1, RKV_WIRE_FP16_SCALE);
         rotatekv_b200::DeviceLayerCache other(desc, perm);
