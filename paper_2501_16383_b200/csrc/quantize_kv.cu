@@ -496,7 +496,7 @@ __global__ void __launch_bounds__(32 * VW, 1) quantize_v_kernel(QuantParams p, u
 // forms) and the packed words and metadata out.  Sub-item = ((sequence,
 // token pair, segment), K or V).  Sink tokens get zero words/meta and the K
 // sub-item of segment 0 owns their mask bits; their sidecar rows come from
-// fused_sink_rows_kernel (generic.cu).
+// fused_sink_rows_kernel (below).
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
@@ -680,6 +680,80 @@ cudaError_t launch_quantize_fused_t(const QuantParams& p, int B, const IN* kf, c
     return cudaGetLastError();
 }
 
+// Sidecar rows of sink tokens appended in the fused frame
+// (rkv_quantize_kv_fused).  The reference's sidecar keeps the fused-frame fp32
+// row (proj/src/kv_cache.cpp:8-22); this cache's sidecar keeps the model-frame
+// fp16 row (decode applies RoPE to it directly), so K' goes back through the
+// inverse reorder (channel perm[j] <- slot j) and H_G, V' through H_128 (each
+// an involution after its 1/sqrt(n)), rounded once to fp16.  One CTA per
+// sequence walks its flagged tokens in order (ballot ranks) and applies the
+// quantize kernels' slot rule.
+constexpr int kSinkThreads = 256;
+// radix-2 FWHT of every n-channel unit of a shared-memory row (any n; the
+// sidecar rows need no particular stage order: they are rounded to fp16)
+__device__ __forceinline__ void fwht_row_smem(float* row, int C, int n) {
+    for (int half = 1; half < n; half <<= 1) {
+        for (int i = threadIdx.x; i < C / 2; i += blockDim.x) {
+            const int lo = (i / half) * 2 * half + i % half;
+            const float a = row[lo], b = row[lo + half];
+            row[lo] = a + b;
+            row[lo + half] = a - b;
+        }
+        __syncthreads();
+    }
+}
+__device__ __forceinline__ float load_row_elem(const float* r, int64_t i) { return r[i]; }
+__device__ __forceinline__ float load_row_elem(const uint16_t* r, int64_t i) { return h2f(r[i]); }
+
+template <typename IN>
+__global__ void __launch_bounds__(kSinkThreads) fused_sink_rows_kernel(QuantParams p, const IN* __restrict__ kf,
+                                                                    const IN* __restrict__ vf, int nk) {
+    extern __shared__ __align__(16) float srow[];  // [C]
+    __shared__ int s_list[kSinkThreads];
+    __shared__ int s_wcnt[kSinkThreads / 32];
+    const int b = blockIdx.x, C = p.C, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int num_new = static_cast<int>(p.num_new);
+    const int count = p.cache.sink_count[b];
+    int before = 0;  // flagged tokens of earlier chunks
+    for (int c0 = 0; c0 < num_new; c0 += kSinkThreads) {
+        const int i = c0 + tid;
+        const bool f = i < num_new && p.sink_flags[static_cast<int64_t>(b) * num_new + i];
+        const uint32_t bal = __ballot_sync(0xffffffffu, f);
+        if (lane == 0) s_wcnt[warp] = __popc(bal);
+        __syncthreads();
+        int rank = __popc(bal & ((1u << lane) - 1u)), total = 0;
+        for (int w = 0; w < kSinkThreads / 32; ++w) {
+            rank += w < warp ? s_wcnt[w] : 0;
+            total += s_wcnt[w];
+        }
+        if (f) s_list[rank] = i;
+        __syncthreads();
+        for (int e = 0; e < total; ++e) {
+            const int ti = s_list[e];
+            const int64_t pos = p.start_pos[b] + ti;
+            const int slot = count + before + e;
+            if (pos < 0 || pos >= p.max_tokens || slot >= p.max_sinks) continue;  // uniform over the CTA
+            const int64_t src = (static_cast<int64_t>(b) * num_new + ti) * C;
+            const int64_t dst = (static_cast<int64_t>(b) * p.max_sinks + slot) * C;
+            for (int j = tid; j < C; j += blockDim.x) srow[p.perm[j]] = load_row_elem(kf, src + j);
+            __syncthreads();
+            fwht_row_smem(srow, C, nk);
+            for (int c = tid; c < C; c += blockDim.x)
+                p.cache.sink_k[dst + c] = __half_as_ushort(__float2half_rn(__fmul_rn(srow[c], p.k_norm)));
+            __syncthreads();
+            for (int c = tid; c < C; c += blockDim.x) srow[c] = load_row_elem(vf, src + c);
+            __syncthreads();
+            fwht_row_smem(srow, C, kHeadDim);
+            for (int c = tid; c < C; c += blockDim.x)
+                p.cache.sink_v[dst + c] = __half_as_ushort(__float2half_rn(__fmul_rn(srow[c], p.v_norm)));
+            if (tid == 0) p.cache.sink_pos[b * p.max_sinks + slot] = static_cast<int32_t>(pos);
+            __syncthreads();
+        }
+        before += total;
+        __syncthreads();  // s_wcnt / s_list reused
+    }
+}
+
 // Sink counts for the appended tokens (only launched with sink flags; it runs
 // after every item has read the old count).
 __global__ void quantize_sink_count_kernel(QuantParams p) {
@@ -842,6 +916,26 @@ cudaError_t launch_promote_sinks(const rkv_layer_desc& d, const QuantParams& p, 
     return cudaGetLastError();
 }
 int promote_sinks_max() { return kPromoteMax; }
+
+cudaError_t launch_fused_sink_rows(const rkv_layer_desc& d, const QuantParams& p, const void* k_rows,
+                                   const void* v_rows, int dtype, cudaStream_t s) {
+    const size_t smem = static_cast<size_t>(p.C) * sizeof(float);
+    const int nk = d.heads_per_group * d.head_dim;
+    if (dtype == RKV_ROWS_F16) {
+        auto kern = fused_sink_rows_kernel<uint16_t>;
+        cudaError_t e = ensure_smem_k(kern, smem);
+        if (e != cudaSuccess) return e;
+        kern<<<d.batch, kSinkThreads, smem, s>>>(p, static_cast<const uint16_t*>(k_rows),
+                                                static_cast<const uint16_t*>(v_rows), nk);
+    } else {
+        auto kern = fused_sink_rows_kernel<float>;
+        cudaError_t e = ensure_smem_k(kern, smem);
+        if (e != cudaSuccess) return e;
+        kern<<<d.batch, kSinkThreads, smem, s>>>(p, static_cast<const float*>(k_rows),
+                                                static_cast<const float*>(v_rows), nk);
+    }
+    return cudaGetLastError();
+}
 
 cudaError_t launch_quantize_fused(const rkv_layer_desc& d, const QuantParams& p, const void* k_rows,
                                   const void* v_rows, int dtype, cudaStream_t s) {
