@@ -511,7 +511,7 @@ def debug_option():
     import paper_2501_16383_b200 as P
 
     defaults = {"gqa_tmem": 1, "decode_kernel_simt": 0, "prefill_pair": 0, "decode_splits": 0, "gqa_warps_per_group": 1,
-                "gqa_head_sets": 2}
+                "gqa_head_sets": 2, "quant_stages": 1, "quant_vsplit": 1}
     touched = []
 
     def set_(name, value):
@@ -549,3 +549,29 @@ def test_alternative_decode_kernels(oracle, debug_option, opt, hq, hkv, g):
                              v[b].cpu().numpy())
         assert rel_err(out[b], want) < REL_TOL
         assert cosine(out[b], want) > COS_TOL
+
+
+@pytest.mark.parametrize("opt,hq,hkv,g", [("quant_stages=2", 40, 40, 4), ("quant_stages=2", 64, 64, 2),
+                                          ("quant_vsplit=0", 32, 32, 4), ("quant_vsplit=0", 8, 8, 4)])
+def test_alternative_quantize_kernels(oracle, debug_option, opt, hq, hkv, g):
+    """The switch-selectable quantize variants stay bit-exact (enough token
+    pairs that the V kernel split and several items per CTA engage)."""
+    k_, v_ = opt.split("=")
+    debug_option(k_, int(v_))
+    w = small_workload(hq, hkv, g)
+    B, T = 8, 333
+    layer, perm = build_layer(w, B, T, seed=41)
+    k, v = WL.make_kv(w, 41, B, T)
+    sinks = torch.zeros(B, T, dtype=torch.uint8)
+    sinks[:, 0] = 1
+    sinks[3, 100] = 1
+    layer.append(k, v, sinks)
+    torch.cuda.synchronize()
+    got = cache_host(layer)
+    for b in (0, 3, B - 1):
+        kc, km, vc, vm = oracle.quantize_kv_rows(k[b].cpu().numpy(), v[b].cpu().numpy(), hkv, 128, g, perm)
+        rows = [t for t in range(T) if not sinks[b, t]]
+        assert np.array_equal(got["k_codes"][b, rows].view(np.uint32), kc[rows])
+        assert np.array_equal(got["k_meta"][b, rows].view(np.uint32), km[rows])
+        assert np.array_equal(got["v_codes"][b, rows].view(np.uint32), vc[rows])
+        assert np.array_equal(got["v_meta"][b, rows].view(np.uint32), vm[rows])

@@ -6,6 +6,9 @@ import json, sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, bench
 bench.max_over_ranks = lambda vals, dev, world: vals
+import paper_2501_16383_b200 as P
+for kv in filter(None, os.environ.get("RKV_OPT", "").split(",")):  # experiment switches, e.g. quant_row_buffers=2
+    P.set_debug_option(kv.split("=")[0], int(kv.split("=")[1]))
 dev = torch.device("cuda", 0)
 for f in [None if a == "raw" else a for a in sys.argv[1:]] or (None, "f16", "f32"):
     r = bench.bench_quantize_cfg5(dev, 1, 0, fused=f)
