@@ -1,6 +1,8 @@
 """Seeded randomised parity sweep: random supported shapes, appends in random
 chunk sizes (odd counts, pairs split across calls), random sink tokens,
-ragged decode lengths and both scale formats.  Every case checks the cache
+ragged decode lengths, both scale formats and (a quarter of the cases) the
+fused-frame append of the oracle's rotated + reordered fp32 rows
+(rkv_quantize_kv_fused).  Every case checks the cache
 bit for bit against the oracle (codes, scale|zero words, sink rows, mask)
 and decode (and, on the tensor-core shapes, prefill) against the oracle's
 attention at the bar of test_gpu_parity.py.  Deterministic: case i uses
@@ -45,8 +47,9 @@ def case(i):
     flags[:, 0] = 1
     lens = [int(rng.integers(1, T + 1)) for _ in range(B)]
     lens[int(rng.integers(0, B))] = T
-    return dict(hq=hq, hkv=hkv, g=g, B=B, T=T, fmt=fmt, chunks=chunks, flags=flags, lens=lens,
-                base=500000.0 if rng.random() < 0.5 else 10000.0)
+    base = 500000.0 if rng.random() < 0.5 else 10000.0
+    return dict(hq=hq, hkv=hkv, g=g, B=B, T=T, fmt=fmt, chunks=chunks, flags=flags, lens=lens, base=base,
+                fused=bool(rng.random() < 0.25))
 
 
 @pytest.mark.parametrize("i", range(85))
@@ -58,9 +61,18 @@ def test_random_case(oracle, i):
     layer, perm = build_layer(w, B, T + 3, seed=1000 + i, fmt=c["fmt"], max_sinks=max_sinks)
     k, v = WL.make_kv(w, 1000 + i, B, T)
     flags = torch.from_numpy(c["flags"])
+    if c["fused"]:  # K' = reorder(H_G k), V' = H_128 v in fp32 (the reference's fused projections)
+        C = w.channels
+        kf = oracle.apply_reorder(oracle.rotate_rows(k.float().cpu().numpy().reshape(-1, C), 128, c["g"], c["hkv"]), perm)
+        vf = oracle.rotate_rows(v.float().cpu().numpy().reshape(-1, C), 128, 1, c["hkv"])
+        kf = torch.from_numpy(kf.reshape(B, T, C)).cuda()
+        vf = torch.from_numpy(vf.reshape(B, T, C)).cuda()
     t0 = 0
     for n in c["chunks"]:
-        layer.append(k[:, t0:t0 + n], v[:, t0:t0 + n], flags[:, t0:t0 + n])
+        if c["fused"]:
+            layer.append_fused(kf[:, t0:t0 + n], vf[:, t0:t0 + n], flags[:, t0:t0 + n])
+        else:
+            layer.append(k[:, t0:t0 + n], v[:, t0:t0 + n], flags[:, t0:t0 + n])
         t0 += n
     torch.cuda.synchronize()
     got = cache_host(layer)
@@ -78,7 +90,12 @@ def test_random_case(oracle, i):
         assert got["sink_count"][b] == len(pos)
         assert list(got["sink_pos"][b, :len(pos)]) == list(pos)
         for j, t in enumerate(pos):
-            assert np.array_equal(got["sink_k"][b, j].view(np.uint16), kh[b, t].view(np.uint16))
+            if not c["fused"]:
+                assert np.array_equal(got["sink_k"][b, j].view(np.uint16), kh[b, t].view(np.uint16))
+            else:  # back through the inverse reorder and FWHT: within an fp16 rounding
+                x = kh[b, t].astype(np.float32)
+                y = got["sink_k"][b, j].view(np.float16).astype(np.float32)
+                assert np.all(np.abs(x - y) <= 1e-3 * np.abs(x) + 1e-5 * np.max(np.abs(x))), (i, b, t)
     q = WL.make_q(w, 1000 + i, B)
     out = layer.decode(q, seq_len=c["lens"]).cpu().numpy()
     for b, L in enumerate(c["lens"]):
