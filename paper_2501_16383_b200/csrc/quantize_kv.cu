@@ -525,6 +525,58 @@ __device__ __forceinline__ void read_run(const uint16_t* r0, const uint16_t* r1,
     }
 }
 
+// fp16 rows: quantize_run straight from the padded shared-memory run in two
+// passes (min/max, then the codes), 8 slots of both tokens live at a time
+// instead of 32 -- the same arithmetic, a third of the registers
+template <int FMT>
+__device__ __forceinline__ QuantOut quantize_run_h(const uint16_t* r0, const uint16_t* r1, int lane) {
+    auto chunk = [&](int q, float2 (&x)[8]) {
+        const uint4 a = lds128(r0 + 8 * q), b = lds128(r1 + 8 * q);
+        const uint16_t* ha = reinterpret_cast<const uint16_t*>(&a);
+        const uint16_t* hb = reinterpret_cast<const uint16_t*>(&b);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) x[e] = make_float2(h2f(ha[e]), h2f(hb[e]));
+    };
+    float2 x[8];
+    chunk(0, x);
+    float mn0 = x[0].x, mx0 = x[0].x, mn1 = x[0].y, mx1 = x[0].y;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        if (q) chunk(q, x);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            mn0 = fminf(mn0, x[e].x);
+            mx0 = fmaxf(mx0, x[e].x);
+            mn1 = fminf(mn1, x[e].y);
+            mx1 = fmaxf(mx1, x[e].y);
+        }
+    }
+#pragma unroll
+    for (int o = 1; o < 4; o <<= 1) {
+        mn0 = fminf(mn0, __shfl_xor_sync(0xffffffffu, mn0, o));
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
+        mn1 = fminf(mn1, __shfl_xor_sync(0xffffffffu, mn1, o));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+    }
+    const bool odd = lane & 1;
+    const GroupQuant gq = group_params<FMT>(odd ? mn1 : mn0, odd ? mx1 : mx0);
+    const int l0 = lane & ~3;
+    const float2 n1 = make_float2(-__shfl_sync(0xffffffffu, gq.t1, l0), -__shfl_sync(0xffffffffu, gq.t1, l0 + 1));
+    const float2 n2 = make_float2(-__shfl_sync(0xffffffffu, gq.t2, l0), -__shfl_sync(0xffffffffu, gq.t2, l0 + 1));
+    const float2 n3 = make_float2(-__shfl_sync(0xffffffffu, gq.t3, l0), -__shfl_sync(0xffffffffu, gq.t3, l0 + 1));
+    QuantOut o;
+    o.meta = gq.meta;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        float2 xb[8];
+        chunk(2 * h, x);
+        chunk(2 * h + 1, xb);
+        o.w[0][h] = ~__byte_perm(code_bits8<0>(x, n1, n2, n3), code_bits8<0>(xb, n1, n2, n3), 0x5410);
+        o.w[1][h] = ~__byte_perm(code_bits8<1>(x, n1, n2, n3), code_bits8<1>(xb, n1, n2, n3), 0x5410);
+    }
+    return o;
+}
+
 constexpr int kFusedSeg = 1024;  // slots per warp sub-item
 template <typename IN>
 struct FusedStage {
@@ -536,7 +588,7 @@ struct FusedStage {
 };
 constexpr int kFusedWarps = 4;
 #ifndef RKV_FUSED_F16_CTAS
-#define RKV_FUSED_F16_CTAS 4  // resident CTAs per SM for fp16 rows (fp32 rows: 3, the shared memory)
+#define RKV_FUSED_F16_CTAS 5  // resident CTAs per SM for fp16 rows (fp32 rows: 3, the shared memory)
 #endif
 
 template <int FMT, typename IN>
@@ -614,13 +666,21 @@ __global__ void __launch_bounds__(32 * kFusedWarps, sizeof(IN) == 4 ? 3 : RKV_FU
                                  : uint8_t{0};
         cp_async_wait1();
         __syncwarp();  // every lane's copies of this buffer have landed
-        float2 x[32];
-        {
+        // (the buffer is refilled by the next iteration's issue: __syncwarp once it is read)
+        const QuantOut qo = [&]() -> QuantOut {
             const uint8_t* rb = smem + warp * S::warp_bytes + buf * S::buf + lane * S::stride;
-            read_run(reinterpret_cast<const IN*>(rb), reinterpret_cast<const IN*>(rb + 32 * S::stride), x);
-        }
-        __syncwarp();  // the buffer is refilled by the next iteration's issue
-        const QuantOut qo = quantize_run<FMT>(x, lane);
+            if constexpr (sizeof(IN) == 2) {
+                const QuantOut r = quantize_run_h<FMT>(reinterpret_cast<const uint16_t*>(rb),
+                                                       reinterpret_cast<const uint16_t*>(rb + 32 * S::stride), lane);
+                __syncwarp();
+                return r;
+            } else {
+                float2 x[32];
+                read_run(reinterpret_cast<const IN*>(rb), reinterpret_cast<const IN*>(rb + 32 * S::stride), x);
+                __syncwarp();
+                return quantize_run<FMT>(x, lane);
+            }
+        }();
         int slot = -1;  // the sidecar slot rule of the other quantize kernels
         if (flag && pos0 + lane >= 0 && pos0 + lane < p.max_tokens) {
             const int i = i0 + lane;
