@@ -57,8 +57,7 @@ __device__ __forceinline__ void sts64(uint32_t addr, float2 v) {
 // Layout-A half of the FWHT for region g: channels [32g, 32g+32) of both
 // tokens from the fp16 stage rows, stages on channel bits 0..4, stored to the
 // token-pair row.
-__device__ __forceinline__ void fwht_region_a(const uint16_t* st0, const uint16_t* st1, float2* row, int g) {
-    float2 x[32];
+__device__ __forceinline__ void fwht_region_a_regs(const uint16_t* st0, const uint16_t* st1, int g, float2 (&x)[32]) {
     const int s = (g >> 1) & 3;  // chunk relabel: conflict-free 64-byte-strided LDS.128
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -79,6 +78,10 @@ __device__ __forceinline__ void fwht_region_a(const uint16_t* st0, const uint16_
         x[16 + e] = mul2(x[16 + e], sg2);
         x[24 + e] = mul2(x[24 + e], sg3);
     }
+}
+__device__ __forceinline__ void fwht_region_a(const uint16_t* st0, const uint16_t* st1, float2* row, int g) {
+    float2 x[32];
+    fwht_region_a_regs(st0, st1, g, x);
     const uint32_t dst = smem_u32(row + 33 * g);
 #pragma unroll
     for (int c = 0; c < 32; ++c) sts64(dst + 8 * c, x[c]);
@@ -357,8 +360,10 @@ __global__ void __launch_bounds__(256, 2) quantize_kv_kernel(QuantParams p, uint
 // V quantize, warp-independent.  V's rotation is per head (128 channels) and
 // V has no reorder, so a warp can own a 1024-channel segment of a token pair
 // outright: its own TMA stage (double-buffered, its own mbarriers), layout A
-// on its 32 regions, layout B on its 8 heads, quantize on its own slots --
-// only __syncwarp, never a CTA barrier.  Sub-item = (sequence, token pair,
+// on its 32 regions, then (SH, the default) the head's last two stages as
+// shuffle butterflies between the 4 lanes of a head and quantize on the
+// registers, or (row buffer) layout B on its 8 heads through shared memory,
+// quantize on its own slots -- only __syncwarp, never a CTA barrier.  Sub-item = (sequence, token pair,
 // segment); the K items (global reorder: a CTA-wide gather) stay on
 // quantize_kv_kernel.  Same arithmetic as there (fwht_region_a,
 // fwht_unit_b<128>, quantize_run): bit-identical codes.
@@ -366,15 +371,18 @@ constexpr int kVSeg = 1024;                 // channels per warp segment (32 reg
 constexpr int kVRowF2 = (kVSeg / 32) * 33;  // float2 per segment row (padded regions)
 // warps per CTA (1 CTA per SM) and TMA stages per warp: VS = 2 gives each
 // copy a whole sub-item of lead time; VS = 1 trades it for occupancy
-template <int VW, int VS>
+// SH: the head FWHT's last two stages (channel bits 5, 6 = lane bits 0, 1)
+// as shuffle butterflies between lanes, then quantize_run on the registers:
+// no row buffer, only the TMA stages in shared memory
+template <int VW, int VS, bool SH = false>
 struct VCfg {
-    static constexpr int warp_bytes = VS * 2 * kVSeg * 2 + kVRowF2 * 8;
+    static constexpr int warp_bytes = VS * 2 * kVSeg * 2 + (SH ? 0 : kVRowF2 * 8);
 };
-template <int FMT, int VW, int VS>
+template <int FMT, int VW, int VS, bool SH = false>
 __global__ void __launch_bounds__(32 * VW, 1) quantize_v_kernel(QuantParams p, uint32_t subitems, uint32_t npairs,
                                                                uint32_t nseg) {
     constexpr int kVWarps = VW;
-    constexpr int kVWarpBytes = VCfg<VW, VS>::warp_bytes;
+    constexpr int kVWarpBytes = VCfg<VW, VS, SH>::warp_bytes;
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint64_t bar[kVWarps][2];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -437,16 +445,38 @@ __global__ void __launch_bounds__(32 * VW, 1) quantize_v_kernel(QuantParams p, u
                                  : uint8_t{0};
         mbar_wait(&bar[warp][sb], VS == 2 ? (k >> 1) & 1u : k & 1u);
         const uint16_t* st = stage + sb * 2 * kVSeg;
-        fwht_region_a(st, has1 ? st + kVSeg : st, row, lane);
-        __syncwarp();
-        // the stage is consumed: refill it with the sub-item after next
-        if (lane == 0 && si + VS * step < subitems) issue(nxt, sb);
-        fwht_unit_b<128>(row, lane / 4, lane % 4, p.v_norm);
-        __syncwarp();
         float2 x[32];
-        const float2* srcr = row + 33 * lane;
+        if constexpr (SH) {
+            fwht_region_a_regs(st, has1 ? st + kVSeg : st, lane, x);
+            __syncwarp();
+            // the stage is consumed: refill it with the sub-item after next
+            if (lane == 0 && si + VS * step < subitems) issue(nxt, sb);
+            // stages on channel bits 5, 6 (lane bits 0, 1): lower lane a + b, upper lane a - b
 #pragma unroll
-        for (int c = 0; c < 32; ++c) x[c] = srcr[c];
+            for (int m = 1; m <= 2; m <<= 1) {
+                const float sg = (lane & m) ? -1.0f : 1.0f;
+                const float2 s2 = make_float2(sg, sg);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const float2 q = make_float2(__shfl_xor_sync(0xffffffffu, x[j].x, m),
+                                                 __shfl_xor_sync(0xffffffffu, x[j].y, m));
+                    x[j] = fma2(x[j], s2, q);
+                }
+            }
+            const float2 nn = make_float2(p.v_norm, p.v_norm);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) x[j] = mul2(x[j], nn);
+        } else {
+            fwht_region_a(st, has1 ? st + kVSeg : st, row, lane);
+            __syncwarp();
+            // the stage is consumed: refill it with the sub-item after next
+            if (lane == 0 && si + VS * step < subitems) issue(nxt, sb);
+            fwht_unit_b<128>(row, lane / 4, lane % 4, p.v_norm);
+            __syncwarp();
+            const float2* srcr = row + 33 * lane;
+#pragma unroll
+            for (int c = 0; c < 32; ++c) x[c] = srcr[c];
+        }
         const QuantOut qo = quantize_run<FMT>(x, lane);
         int slot = -1;
         if (flag && pos0 + lane >= 0 && pos0 + lane < p.max_tokens) {  // lanes 0, 1: tokens i0, i0 + 1
@@ -478,7 +508,7 @@ __global__ void __launch_bounds__(32 * VW, 1) quantize_v_kernel(QuantParams p, u
                                                   seg * kVSeg);
             for (int j = lane; j < kVSeg / 8; j += 32) dst[j] = __ldg(srcv + j);
         }
-        __syncwarp();  // the row is rewritten by the next sub-item
+        if (!SH) __syncwarp();  // the row is rewritten by the next sub-item
     }
 }
 
@@ -929,10 +959,15 @@ cudaError_t launch_quantize_ns(const QuantParams& p, int B, cudaStream_t s) {
                                                                        static_cast<uint32_t>(nseg));
             return cudaGetLastError();
         };
+        // shapes (warps x TMA stages per warp): 0 = 16 x 2 with the shuffle
+        // stages (no row buffer), 1 = 16 x 1, 2 = 14 x 1, 3 = 12 x 2 with the row
+        // buffer, 4 = 20 x 2 with the shuffle stages
         const int vcfg = options().quant_vcfg.load();
         cudaError_t e = vcfg == 1   ? launch_v(quantize_v_kernel<FMT, 16, 1>, 16, VCfg<16, 1>::warp_bytes)
                         : vcfg == 2 ? launch_v(quantize_v_kernel<FMT, 14, 1>, 14, VCfg<14, 1>::warp_bytes)
-                                    : launch_v(quantize_v_kernel<FMT, 12, 2>, 12, VCfg<12, 2>::warp_bytes);
+                        : vcfg == 3 ? launch_v(quantize_v_kernel<FMT, 12, 2>, 12, VCfg<12, 2>::warp_bytes)
+                        : vcfg == 4 ? launch_v(quantize_v_kernel<FMT, 20, 2, true>, 20, VCfg<20, 2, true>::warp_bytes)
+                                    : launch_v(quantize_v_kernel<FMT, 16, 2, true>, 16, VCfg<16, 2, true>::warp_bytes);
         if (e != cudaSuccess) return e;
         pk.k_only = 1;
     }

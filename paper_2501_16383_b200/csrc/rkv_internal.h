@@ -24,7 +24,8 @@ struct Options {
     std::atomic<int> simt_stages{0};   // CUDA-core kernel: TMA ring depth (0 = planner)
     std::atomic<int> quant_stages{1};  // quantize kernel: TMA stage buffers (1 or 2)
     std::atomic<int> quant_vsplit{1};  // quantize: V on the warp-independent kernel
-    std::atomic<int> quant_vcfg{0};    // V kernel shape: 0 = 12 warps x 2 stages, 1 = 16 x 1, 2 = 14 x 1
+    std::atomic<int> quant_vcfg{0};    // V kernel shape: 0 = 16 warps x 2 stages, shuffle stages; 1 = 16 x 1,
+                                       // 2 = 14 x 1, 3 = 12 x 2 (row buffer); 4 = 20 x 2, shuffle stages
     std::atomic<int> decode_pdl{1};    // launch the MHA decode kernel with programmatic stream serialization
     std::atomic<int> generic_tile{0};  // generic decode: tokens per tile (0 = planner)
     std::atomic<int> gqa_sets{2};      // GQA kernel: 4-head sets sharing one key tile (1 or 2)

@@ -511,7 +511,7 @@ def debug_option():
     import paper_2501_16383_b200 as P
 
     defaults = {"gqa_tmem": 1, "decode_kernel_simt": 0, "prefill_pair": 0, "decode_splits": 0, "gqa_warps_per_group": 1,
-                "gqa_head_sets": 2, "quant_stages": 1, "quant_vsplit": 1}
+                "gqa_head_sets": 2, "quant_stages": 1, "quant_vsplit": 1, "quant_vcfg": 0}
     touched = []
 
     def set_(name, value):
@@ -552,7 +552,9 @@ def test_alternative_decode_kernels(oracle, debug_option, opt, hq, hkv, g):
 
 
 @pytest.mark.parametrize("opt,hq,hkv,g", [("quant_stages=2", 40, 40, 4), ("quant_stages=2", 64, 64, 2),
-                                          ("quant_vsplit=0", 32, 32, 4), ("quant_vsplit=0", 8, 8, 4)])
+                                          ("quant_vsplit=0", 32, 32, 4), ("quant_vsplit=0", 8, 8, 4),
+                                          ("quant_vcfg=3", 40, 40, 4), ("quant_vcfg=4", 32, 32, 2),
+                                          ("quant_vcfg=1", 40, 40, 4)])
 def test_alternative_quantize_kernels(oracle, debug_option, opt, hq, hkv, g):
     """The switch-selectable quantize variants stay bit-exact (enough token
     pairs that the V kernel split and several items per CTA engage)."""
