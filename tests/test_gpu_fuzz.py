@@ -6,7 +6,9 @@ fused-frame append of the oracle's rotated + reordered fp32 rows
 bit for bit against the oracle (codes, scale|zero words, sink rows, mask)
 and decode (and, on the tensor-core shapes, prefill) against the oracle's
 attention at the bar of test_gpu_parity.py.  Deterministic: case i uses
-numpy seed 1000 + i."""
+numpy seed 1000 + i.  RKV_FUZZ_CASES widens the sweep (default 85)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -52,7 +54,7 @@ def case(i):
                 fused=bool(rng.random() < 0.25))
 
 
-@pytest.mark.parametrize("i", range(85))
+@pytest.mark.parametrize("i", range(int(os.environ.get("RKV_FUZZ_CASES", "85"))))  # wider sweeps: RKV_FUZZ_CASES=400
 def test_random_case(oracle, i):
     c = case(i)
     w = small_workload(c["hq"], c["hkv"], c["g"], base=c["base"])
