@@ -44,8 +44,10 @@
 //     the V accumulation on CUDA cores: one LOP3 turns two codes into fp16
 //     subnormals c*2^(2e-24) and a mixed FHFMA (fp16 x fp16 + fp32) adds p*s*c;
 //     the zero point is folded once per token.
-// The GQA kernel (G = 2, 4 q heads per KV head) shares the K side, runs P.V on
-// m16n8k8 and parks its accumulators in tensor memory between phases.  SP
+// The GQA kernel (G = 2 or 4, 4 q heads per KV head and set; ratios that are
+// multiples of 4 run as head sets, two per key tile at 8:1) shares the K side,
+// runs P.V on m16n8k8 and parks its accumulators in tensor memory between
+// phases.  SP
 // instantiations restrict a split to a token range (sequence-parallel
 // partials, rkv_decode_attention_partial).
 #include <algorithm>
