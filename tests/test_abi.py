@@ -158,6 +158,29 @@ def test_null_and_size_errors(lib):
     assert b"null" in lib.rkv_last_error()
 
 
+def test_fused_append_argument_errors(lib):
+    """rkv_quantize_kv_fused validates before any device work (no GPU needed)."""
+    d = cfg().desc()
+    view = R.CacheView(*([256] * 9))
+    f = lib.rkv_quantize_kv_fused
+    assert f(C.byref(d), None, None, R.ROWS_F32, None, None, None, 0, None, None) == R.RKV_ERR_INVALID_ARGUMENT
+    assert f(C.byref(d), None, None, R.ROWS_F32, None, None, None, 0, C.byref(view), None) == R.RKV_OK
+    assert f(C.byref(d), None, None, 7, None, None, None, 0, C.byref(view), None) == R.RKV_ERR_INVALID_ARGUMENT
+    assert b"dtype" in lib.rkv_last_error()
+    assert f(C.byref(d), None, None, R.ROWS_F16, None, None, None, -1, C.byref(view), None) == R.RKV_ERR_INVALID_ARGUMENT
+    assert f(C.byref(d), None, None, R.ROWS_F16, None, None, None, 4, C.byref(view), None) == R.RKV_ERR_INVALID_ARGUMENT
+    assert b"non-null" in lib.rkv_last_error()
+    raw = np.zeros(512, np.uint8)
+    base = raw.ctypes.data + (-raw.ctypes.data) % 16  # 16-byte aligned
+    buf, mis = C.c_void_p(base), C.c_void_p(base + 4)
+    pos = (C.c_int64 * 4)()
+    perm = (C.c_int32 * 4)()
+    assert f(C.byref(d), mis, buf, R.ROWS_F32, perm, None, pos, 4, C.byref(view), None) == R.RKV_ERR_INVALID_ARGUMENT
+    assert b"aligned" in lib.rkv_last_error()
+    big = d.max_tokens + 1
+    assert f(C.byref(d), buf, buf, R.ROWS_F32, perm, None, pos, big, C.byref(view), None) == R.RKV_ERR_OUT_OF_RANGE
+
+
 def test_cpp_api_program_compiles(tmp_path, lib):
     """include/rotatekv/rotatekv.hpp + the C ABI link into a C++ program."""
     from tests._cpp import build_cpp_test
