@@ -577,3 +577,21 @@ def test_alternative_quantize_kernels(oracle, debug_option, opt, hq, hkv, g):
         assert np.array_equal(got["k_meta"][b, rows].view(np.uint32), km[rows])
         assert np.array_equal(got["v_codes"][b, rows].view(np.uint32), vc[rows])
         assert np.array_equal(got["v_meta"][b, rows].view(np.uint32), vm[rows])
+
+
+@pytest.mark.parametrize("hq,hkv,g", [(64, 8, 2), (32, 4, 2), (128, 8, 2)])
+def test_gqa_head_sets_bit_identical_to_passes(debug_option, hq, hkv, g):
+    """Two 4-head sets per key tile (the 8:1 default) run each head's
+    arithmetic exactly as the 4-head passes do: the outputs are bit-identical."""
+    w = small_workload(hq, hkv, g)
+    B, T = 3, 300
+    layer, perm = build_layer(w, B, T + 4, seed=61)
+    k, v = WL.make_kv(w, 61, B, T)
+    sinks = torch.zeros(B, T, dtype=torch.uint8)
+    sinks[:, 0] = 1
+    layer.append(k, v, sinks)
+    q = WL.make_q(w, 61, B)
+    sets = layer.decode(q).cpu().numpy()
+    debug_option("gqa_head_sets", 1)
+    passes = layer.decode(q).cpu().numpy()
+    assert np.array_equal(sets.view(np.uint32), passes.view(np.uint32))
