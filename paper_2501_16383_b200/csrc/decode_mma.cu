@@ -719,9 +719,12 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? (NS == 2 ? 2 : PW == 1 ? 4 :
             for (int sl = 0; sl < NQ; ++sl) {
                 const int r = (sl % REP) ^ (g & 3);
                 const bool other = sl >= REP;
-                const int hq = X ? ((other ? gam ^ 1 : gam) * G + kvh) * p.q_rep + p.q_rep_off + r
-                                 : (gam * G + kvh) * p.q_rep + p.q_rep_off + (other ? REP : 0) + r;
-                const float sg = X && !other && (gam & 1) ? -qs : qs;
+                // head hr of its KV head; a set's heads past the ratio (e.g. 5:1 as
+                // 4 + 1) get q = 0 and their partials are never written
+                const int hr = p.q_rep_off + (!X && other ? REP : 0) + r;
+                const bool live = hr < p.q_rep;
+                const int hq = ((X && other ? gam ^ 1 : gam) * G + kvh) * p.q_rep + (live ? hr : 0);
+                const float sg = !live ? 0.0f : X && !other && (gam & 1) ? -qs : qs;
                 float a2[2], b2[2];
 #pragma unroll
                 for (int i = 0; i < 2; ++i) {
@@ -1015,7 +1018,7 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? (NS == 2 ? 2 : PW == 1 ? 4 :
         zsum += __shfl_xor_sync(0xffffffffu, zsum, 1);
         zsum += __shfl_xor_sync(0xffffffffu, zsum, 2);
         fetch_acc(set);
-        if (tl == 0) {
+        if (tl == 0 && p.q_rep_off + REP * set + (g & 3) < p.q_rep) {
             const int hq = (gam * G + kvh) * p.q_rep + p.q_rep_off + REP * set + (g & 3);
             p.ws_ml[(rbase + hq) * 2] = m_run[set];
             p.ws_ml[(rbase + hq) * 2 + 1] = lsum;
@@ -1026,14 +1029,15 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? (NS == 2 ? 2 : PW == 1 ? 4 :
             for (int c = 0; c < 2; ++c) {
                 const int r = (2 * tl + c) & 3;
                 const float z = __shfl_sync(0xffffffffu, zsum, ((h * 4 + r) << 2));
-                const int hq = (gam * G + h) * p.q_rep + p.q_rep_off + REP * set + r;
+                const int hr = p.q_rep_off + REP * set + r;
+                const int hq = (gam * G + h) * p.q_rep + hr;
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
                     const int sh = e < 5 ? e : e - 5;
                     const float sc = __int_as_float((127 + 24 - 2 * sh) << 23);
                     const float o0 = acc[h][e][c] + __shfl_xor_sync(0xffffffffu, acc[h][e][c], 2);          // hi + lo
                     const float o1 = acc[h][e][c + 2] + __shfl_xor_sync(0xffffffffu, acc[h][e][c + 2], 2);
-                    if (tl < 2) {
+                    if (tl < 2 && hr < p.q_rep) {
                         float* orow = p.ws_o + (rbase + hq) * 128 + g * 16;
                         orow[e] = o0 * sc - z;
                         orow[e + 8] = o1 * sc - z;
@@ -1059,13 +1063,13 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? (NS == 2 ? 2 : PW == 1 ? 4 :
 // per CTA).
 bool decode_mma_supported(int G, int REP, int C) {
     if (REP == 1 && (G == 4 || G == 2 || G == 1)) return C % 512 == 0 && C / 512 * 32 <= kMmaMaxThreads;
-    if (REP % 4 == 0 && REP <= 32 && (G == 2 || G == 4)) return C % (128 * G) == 0 && C / 256 <= 4;
+    if (REP >= 2 && REP <= 64 && (G == 2 || G == 4)) return C % (128 * G) == 0 && C / 256 <= 4;
     return false;
 }
 
 int mma_layout_n(const rkv_layer_desc& d) {
     const int rep = d.num_q_heads / d.num_kv_heads;
-    return (d.heads_per_group == 2 || d.heads_per_group == 4) && rep % 4 == 0 && rep > 1 ? 256 : 512;
+    return (d.heads_per_group == 2 || d.heads_per_group == 4) && rep > 1 ? 256 : 512;
 }
 
 namespace {
@@ -1087,11 +1091,11 @@ void* gqa_kernel_ptr() {
     return gqa_tmem() ? reinterpret_cast<void*>(decode_gqa_kernel<4, PW, true>)
                       : reinterpret_cast<void*>(decode_gqa_kernel<4, PW, false>);
 }
-// 4-head sets per launch: two (one key tile, 8 q heads) when the ratio is a
-// multiple of 8 at G = 2 and PW = 1 with tensor-memory parking
+// 4-head sets per launch: two (one key tile, up to 8 q heads) when the ratio
+// exceeds 4 at G = 2 and PW = 1 with tensor-memory parking
 int gqa_sets(const rkv_layer_desc& d, int pw) {
     const int rep = d.num_q_heads / d.num_kv_heads;
-    return d.heads_per_group == 2 && rep % 8 == 0 && pw == 1 && gqa_tmem() && options().gqa_sets.load() != 1 ? 2 : 1;
+    return d.heads_per_group == 2 && rep > 4 && pw == 1 && gqa_tmem() && options().gqa_sets.load() != 1 ? 2 : 1;
 }
 void* gqa_kernel(int pw, bool sp = false, bool g4 = false, int sets = 1) {
     if (sets == 2)

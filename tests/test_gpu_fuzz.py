@@ -24,13 +24,14 @@ from paper_2501_16383_b200 import workload as WL  # noqa: E402
 from .test_gpu_parity import (COS_TOL, REL_TOL, build_layer, cache_host, cosine, oracle_decode,  # noqa: E402
                              rel_err, small_workload)
 
-# (Hq, Hkv, G): tensor-core MHA at G = 1/2/4 (up to C = 8192), GQA 4:1 at G = 2
+# (Hq, Hkv, G): tensor-core MHA at G = 1/2/4 (up to C = 8192), GQA (any ratio) at G = 2
 # and 4, CUDA-core shapes, generic (tiled) shapes
 SHAPES = [(8, 8, 4), (8, 8, 2), (8, 8, 1), (12, 12, 4), (40, 40, 4), (16, 4, 2), (32, 8, 2), (16, 8, 4),
           (8, 4, 2), (16, 4, 1), (4, 4, 1), (16, 4, 4), (32, 8, 4), (64, 64, 4), (16, 16, 8), (24, 8, 8),
-          (64, 16, 4), (64, 8, 2), (32, 4, 4)]
+          (64, 16, 4), (64, 8, 2), (32, 4, 4), (40, 8, 2), (24, 8, 4), (16, 8, 2)]
 TC_PREFILL = {(8, 8, 4), (8, 8, 2), (8, 8, 1), (12, 12, 4), (40, 40, 4), (16, 4, 2), (32, 8, 2), (4, 4, 1),
-              (16, 4, 4), (32, 8, 4), (64, 64, 4), (64, 8, 2), (32, 4, 4)}
+              (16, 8, 4), (8, 4, 2),
+              (16, 4, 4), (32, 8, 4), (64, 64, 4), (64, 8, 2), (32, 4, 4), (40, 8, 2), (24, 8, 4), (16, 8, 2)}
 
 
 def case(i):

@@ -181,6 +181,10 @@ def oracle_decode(oracle, layer, got, b, T, q, w, perm, kraw, vraw):
     # GQA 8:1 (LLaMA-2/3-70B) and 16:1 as passes of the 4-head kernel, G = 2 and 4
     (64, 8, 2, 500000.0, 300), (64, 8, 4, 500000.0, 129), (32, 4, 2, 10000.0, 77), (64, 4, 4, 10000.0, 65),
     (96, 8, 2, 10000.0, 70), (64, 4, 2, 500000.0, 200), (128, 8, 2, 10000.0, 33),
+    # any other ratio: partial head sets (2:1, 3:1 one set; 5:1 .. 7:1 two sets; 10:1 two launches)
+    (16, 8, 2, 500000.0, 150), (24, 8, 2, 10000.0, 77), (40, 8, 2, 500000.0, 300), (56, 8, 2, 10000.0, 129),
+    (48, 8, 2, 10000.0, 65), (80, 8, 2, 10000.0, 40), (8, 4, 4, 10000.0, 90), (24, 8, 4, 500000.0, 130),
+    (20, 4, 4, 10000.0, 33),
 ])
 def test_decode_vs_oracle(oracle, hq, hkv, g, base, T):
     w = small_workload(hq, hkv, g, base=base)
@@ -203,8 +207,8 @@ def test_decode_vs_oracle(oracle, hq, hkv, g, base, T):
 
 
 @pytest.mark.parametrize("hq,hkv,g,T", [
-    (80, 8, 2, 70),     # 10 q heads per KV head (ratios not a multiple of 4)
-    (40, 8, 4, 70),     # 5 q heads per KV head at the paper's default G = 4
+    (80, 16, 2, 70),    # 5 q heads per KV head over 16 KV heads (past the tensor-core GQA width)
+    (40, 8, 8, 70),     # 5 q heads per KV head at G = 8
     (64, 64, 1, 90),    # G = 1 at C = 8192
     (16, 16, 8, 130),   # n = 1024
     (32, 32, 16, 65),   # n = 2048
@@ -411,7 +415,8 @@ def test_decode_matches_reference_decode_step(ref):
     assert cosine(out, want) > COS_TOL
 
 
-@pytest.mark.parametrize("hq,hkv,g", [(40, 40, 4), (32, 8, 2), (32, 8, 4), (16, 16, 8), (16, 8, 4), (64, 8, 2)])
+@pytest.mark.parametrize("hq,hkv,g", [(40, 40, 4), (32, 8, 2), (32, 8, 4), (16, 16, 8), (16, 4, 1), (64, 8, 2),
+                                      (40, 8, 2)])
 def test_decode_deterministic(hq, hkv, g):
     """Bit-identical outputs run to run on every decode kernel family (fixed
     split partition, fixed merge order)."""
@@ -579,7 +584,7 @@ def test_alternative_quantize_kernels(oracle, debug_option, opt, hq, hkv, g):
         assert np.array_equal(got["v_meta"][b, rows].view(np.uint32), vm[rows])
 
 
-@pytest.mark.parametrize("hq,hkv,g", [(64, 8, 2), (32, 4, 2), (128, 8, 2)])
+@pytest.mark.parametrize("hq,hkv,g", [(64, 8, 2), (32, 4, 2), (128, 8, 2), (40, 8, 2), (56, 8, 2)])
 def test_gqa_head_sets_bit_identical_to_passes(debug_option, hq, hkv, g):
     """Two 4-head sets per key tile (the 8:1 default) run each head's
     arithmetic exactly as the 4-head passes do: the outputs are bit-identical."""
