@@ -24,6 +24,9 @@
  *   sink_pos          [B][max_sinks]            i32 token position of each sink
  *   sink_count        [B]                       i32
  *   sink_mask         [B][ceil(max_tokens/32)]  u32 bit t%32 of word t/32 = sink
+ * Every array starts 16-byte aligned and its allocation is a multiple of 16
+ * bytes (rkv_cache_carve: 256): the decode kernels copy meta rows in 16-byte
+ * aligned blocks, up to 12 bytes past a row when C is not a multiple of 512.
  */
 #ifndef ROTATEKV_B200_H
 #define ROTATEKV_B200_H

@@ -544,9 +544,10 @@ __host__ __device__ inline MmaSmem gqa_smem(int C, int TT, int chunk) {
     const int W = C / 16, MG = C / 128, PP = TT / 2;
     s.kc = 0;
     s.km = al16(s.kc + size_t(TT) * W * 4);
-    s.vc = al16(s.km + size_t(TT) * MG * 4);
+    const size_t slack = MG % 4 ? 16 : 0;  // meta rows copied from a 16-byte aligned start (C % 512 != 0)
+    s.vc = al16(s.km + size_t(TT) * MG * 4 + slack);
     s.vm = al16(s.vc + size_t(TT) * W * 4);
-    s.rope = al16(s.vm + size_t(TT) * MG * 4);
+    s.rope = al16(s.vm + size_t(TT) * MG * 4 + slack);
     s.stage_bytes = al16(s.rope + size_t(PP) * 64 * 16);
     s.stages = 0;
     s.mbar = s.stages + kGqaNS * s.stage_bytes;
@@ -565,16 +566,28 @@ __host__ __device__ inline MmaSmem gqa_smem(int C, int TT, int chunk) {
 // NS = 2 (8 or more q heads per KV head, G = 2): two sets of 4 q heads share
 // each reconstructed key tile -- logits, softmax state and P.V per set, the
 // set's accumulators parked in their own 64 columns.
-template <int REP, int PW, bool TM, bool SP = false, int GR = 2, int NS = 1>
-__global__ void __launch_bounds__(32 * 4 * PW, TM ? (NS == 2 ? 2 : PW == 1 ? 4 : 2) : 1) decode_gqa_kernel(DecodeParams p) {
+// WIDE: 5 .. 8 (half-)groups per CTA (over 8 KV heads at G = 2), PW = 1 with
+// TM; the launch bounds keep the register budget of the 4-group kernels.
+template <int PW, bool TM, int NS, bool WIDE>
+constexpr int gqa_max_threads() { return WIDE ? 32 * 8 : 32 * 4 * PW; }
+template <int PW, bool TM, int NS, bool WIDE>
+constexpr int gqa_min_blocks() { return WIDE ? (NS == 2 ? 1 : 2) : TM ? (NS == 2 ? 2 : PW == 1 ? 4 : 2) : 1; }
+// tensor-memory columns a CTA of `warps` warps allocates (a power of two >= 32)
+__host__ __device__ constexpr uint32_t gqa_tmem_cols(uint32_t warp_cols, int warps) {
+    const uint32_t need = warp_cols * static_cast<uint32_t>((warps + 3) / 4);
+    return need <= 32 ? 32 : need <= 64 ? 64 : need <= 128 ? 128 : need <= 256 ? 256 : 512;
+}
+template <int REP, int PW, bool TM, bool SP = false, int GR = 2, int NS = 1, bool WIDE = false>
+__global__ void __launch_bounds__(gqa_max_threads<PW, TM, NS, WIDE>(), gqa_min_blocks<PW, TM, NS, WIDE>())
+    decode_gqa_kernel(DecodeParams p) {
     static_assert(REP == 4, "decode_gqa_kernel: 4 q heads per KV head and set");
     static_assert(GR == 2 || (GR == 4 && PW <= 2 && TM), "decode_gqa_kernel: G = 2, or G = 4 at PW <= 2 with TMEM parking");
     static_assert(NS == 1 || (NS == 2 && GR == 2 && PW == 1 && TM), "decode_gqa_kernel: two head sets at G = 2, PW = 1, TMEM");
+    static_assert(!WIDE || (PW == 1 && TM), "decode_gqa_kernel: more than 4 groups at PW = 1 with TMEM");
     constexpr int G = 2, N = 256, NJ = 2, TT = 8 * PW, PPT = TT / 2;  // G, N: KV heads / channels per warp group
     constexpr bool X = GR == 4;  // partner-half exchange
     constexpr bool Y = NS == 2;  // second head set
     constexpr uint32_t kQCols = X || Y ? 64 : 32, kWarpCols = kQCols + 64 * NS;
-    constexpr uint32_t kAlloc = PW == 1 && !Y ? 128 : 256;
     extern __shared__ __align__(128) unsigned char smem[];
     const int C = p.C, W = C / 16, MG = C / 128, Hq = p.Hq, NG = C / N;
     const MmaSmem lay = gqa_smem(C, TT, p.chunk);
@@ -612,17 +625,23 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? (NS == 2 ? 2 : PW == 1 ? 4 :
     const int ntiles = static_cast<int>((t_end - t_begin + TT - 1) / TT);
     const int64_t row0 = static_cast<int64_t>(b) * p.max_tokens;
 
+    // byte offset of token t0's meta row from the 16-byte boundary below it (the
+    // cache arrays are 256-byte aligned, so K and V share it)
+    auto meta_off = [&](int64_t t0) { return MG % 4 ? static_cast<uint32_t>(((row0 + t0) * MG * 4) & 15) : 0u; };
     auto issue_tile = [&](int it) {
         const int64_t t0 = t_begin + static_cast<int64_t>(it) * TT;
         const uint32_t n = static_cast<uint32_t>(lmin64(TT, t_end - t0));
         unsigned char* st = smem + lay.stages + (it % kGqaNS) * lay.stage_bytes;
         uint64_t* bar = mbar + (it % kGqaNS);
         const uint32_t bw = n * W * 4, bm = n * MG * 4, npr = (n + 1) >> 1;
-        mbar_arrive_expect_tx(bar, 2 * bw + 2 * bm + npr * 1024);
+        // meta rows are C/32 bytes: 16-byte aligned only when C % 512 == 0, so the
+        // copy starts at the aligned address below and the readers skip meta_off
+        const uint32_t mo = meta_off(t0), bma = (bm + mo + 15u) & ~15u;
+        mbar_arrive_expect_tx(bar, 2 * bw + 2 * bma + npr * 1024);
         bulk_g2s(st + lay.kc, p.cache.k_codes + (row0 + t0) * W, bw, bar);
-        bulk_g2s(st + lay.km, p.cache.k_meta + (row0 + t0) * MG, bm, bar);
+        bulk_g2s(st + lay.km, reinterpret_cast<const unsigned char*>(p.cache.k_meta + (row0 + t0) * MG) - mo, bma, bar);
         bulk_g2s(st + lay.vc, p.cache.v_codes + (row0 + t0) * W, bw, bar);
-        bulk_g2s(st + lay.vm, p.cache.v_meta + (row0 + t0) * MG, bm, bar);
+        bulk_g2s(st + lay.vm, reinterpret_cast<const unsigned char*>(p.cache.v_meta + (row0 + t0) * MG) - mo, bma, bar);
         for (uint32_t r = 0; r < npr; ++r)
             bulk_g2s(st + lay.rope + r * 1024, p.rope + ((t0 >> 1) + r) * 128 + 64, 1024, bar);
     };
@@ -632,8 +651,14 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? (NS == 2 ? 2 : PW == 1 ? 4 :
         mbar_fence_init();
     }
     __shared__ uint32_t s_tmem;
+    // 4 groups: 128 columns (PW = 1, one set) or 256; WIDE: by the warp count
+    const uint32_t tcols = WIDE ? gqa_tmem_cols(kWarpCols, NT / 32) : PW == 1 && !Y ? 128u : 256u;
     if constexpr (TM) {
-        if (warp == 0) umma::alloc<kAlloc>(&s_tmem);
+        if (warp == 0) {
+            if (tcols <= 128) umma::alloc<128>(&s_tmem);
+            else if (tcols <= 256) umma::alloc<256>(&s_tmem);
+            else umma::alloc<512>(&s_tmem);
+        }
         umma::fence_before();
     }
     __syncthreads();
@@ -657,10 +682,10 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? (NS == 2 ? 2 : PW == 1 ? 4 :
 
     // scatter: thread -> word position wp, token pairs pq0 and pq0 + NT/W (two per thread)
     const int wp = tid % W, pq0 = tid / W, pqs = NT / W;
-    auto scatter_tile = [&](int slot) {
+    auto scatter_tile = [&](int it, int slot) {
         const unsigned char* st = smem + lay.stages + slot * lay.stage_bytes;
         const uint32_t* kc = reinterpret_cast<const uint32_t*>(st + lay.kc);
-        const uint32_t* km = reinterpret_cast<const uint32_t*>(st + lay.km);
+        const uint32_t* km = reinterpret_cast<const uint32_t*>(st + lay.km + meta_off(t_begin + static_cast<int64_t>(it) * TT));
         const uint32_t buf = static_cast<uint32_t>(lay.knat) + smem_u32(smem);
         const int wsrc = static_cast<int>(plan_s[wp]);
         uint32_t ad[16];
@@ -838,7 +863,7 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? (NS == 2 ? 2 : PW == 1 ? 4 :
         const int nv = static_cast<int>(lmin64(TT, t_end - t0));
         const unsigned char* st = smem + lay.stages + slot * lay.stage_bytes;
         const uint32_t* vc = reinterpret_cast<const uint32_t*>(st + lay.vc);
-        const uint32_t* vm = reinterpret_cast<const uint32_t*>(st + lay.vm);
+        const uint32_t* vm = reinterpret_cast<const uint32_t*>(st + lay.vm + meta_off(t0));
         const float4* rope4 = reinterpret_cast<const float4*>(st + lay.rope);
         const unsigned char* bufp = smem + lay.knat;
         float bq[8], bo[8];  // per token: the partial logits (own / X: partner heads) after two reduce-scatter steps
@@ -995,7 +1020,7 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? (NS == 2 ? 2 : PW == 1 ? 4 :
     uint32_t phase = 0;
     for (int it = 0; it < ntiles; ++it) {
         mbar_wait(mbar + slot, phase);
-        scatter_tile(slot);
+        scatter_tile(it, slot);
         __syncthreads();
         compute_tile(it, slot);
         __syncthreads();
@@ -1050,7 +1075,9 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? (NS == 2 ? 2 : PW == 1 ? 4 :
         __syncthreads();
         if (warp == 0) {
             umma::fence_after();
-            umma::dealloc<kAlloc>(s_tmem);
+            if (tcols <= 128) umma::dealloc<128>(s_tmem);
+            else if (tcols <= 256) umma::dealloc<256>(s_tmem);
+            else umma::dealloc<512>(s_tmem);
         }
     }
 }
@@ -1063,7 +1090,7 @@ __global__ void __launch_bounds__(32 * 4 * PW, TM ? (NS == 2 ? 2 : PW == 1 ? 4 :
 // per CTA).
 bool decode_mma_supported(int G, int REP, int C) {
     if (REP == 1 && (G == 4 || G == 2 || G == 1)) return C % 512 == 0 && C / 512 * 32 <= kMmaMaxThreads;
-    if (REP >= 2 && REP <= 64 && (G == 2 || G == 4)) return C % (128 * G) == 0 && C / 256 <= 4;
+    if (REP >= 2 && REP <= 64 && (G == 2 || G == 4)) return C % (128 * G) == 0 && C / 256 <= 8;
     return false;
 }
 
@@ -1097,7 +1124,17 @@ int gqa_sets(const rkv_layer_desc& d, int pw) {
     const int rep = d.num_q_heads / d.num_kv_heads;
     return d.heads_per_group == 2 && rep > 4 && pw == 1 && gqa_tmem() && options().gqa_sets.load() != 1 ? 2 : 1;
 }
-void* gqa_kernel(int pw, bool sp = false, bool g4 = false, int sets = 1) {
+void* gqa_kernel(int pw, bool sp = false, bool g4 = false, int sets = 1, bool wide = false) {
+    if (wide) {  // 5 .. 8 (half-)groups: PW = 1 with tensor-memory parking
+        if (sets == 2)
+            return sp ? reinterpret_cast<void*>(decode_gqa_kernel<4, 1, true, true, 2, 2, true>)
+                      : reinterpret_cast<void*>(decode_gqa_kernel<4, 1, true, false, 2, 2, true>);
+        if (g4)
+            return sp ? reinterpret_cast<void*>(decode_gqa_kernel<4, 1, true, true, 4, 1, true>)
+                      : reinterpret_cast<void*>(decode_gqa_kernel<4, 1, true, false, 4, 1, true>);
+        return sp ? reinterpret_cast<void*>(decode_gqa_kernel<4, 1, true, true, 2, 1, true>)
+                  : reinterpret_cast<void*>(decode_gqa_kernel<4, 1, true, false, 2, 1, true>);
+    }
     if (sets == 2)
         return sp ? reinterpret_cast<void*>(decode_gqa_kernel<4, 1, true, true, 2, 2>)
                   : reinterpret_cast<void*>(decode_gqa_kernel<4, 1, true, false, 2, 2>);
@@ -1139,7 +1176,9 @@ DecodePlan plan_decode_mma(const rkv_layer_desc& d, int64_t max_seq_len) {
     pl.REP = d.num_q_heads / d.num_kv_heads;
     const int NG = C / pl.N;
     const bool gqa = pl.N == 256, g4 = gqa && d.heads_per_group == 4;
-    const int PW = g4 ? std::min(2, gqa_pw()) : gqa ? gqa_pw() : 1, PP = gqa ? 4 * PW : kPP;
+    // more than 4 (half-)groups (over 8 KV heads): one warp per group with tensor-memory parking
+    const bool wide = gqa && NG > 4;
+    const int PW = wide ? 1 : g4 ? std::min(2, gqa_pw()) : gqa ? gqa_pw() : 1, PP = gqa ? 4 * PW : kPP;
     pl.stages = gqa ? kGqaNS : kNS;
     pl.P = PW;
     pl.PP = PP;
@@ -1154,17 +1193,22 @@ DecodePlan plan_decode_mma(const rkv_layer_desc& d, int64_t max_seq_len) {
     {
         int n = 0;
         const int sets = gqa ? gqa_sets(d, PW) : 1;
-        const void* kern = gqa ? gqa_kernel(PW, false, g4, sets) : reinterpret_cast<const void*>(mha_kernel(NG, d.heads_per_group));
+        const void* kern = gqa ? gqa_kernel(PW, false, g4, sets, wide) : reinterpret_cast<const void*>(mha_kernel(NG, d.heads_per_group));
         if (ensure_smem(kern, pl.smem) == cudaSuccess &&
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, pl.NT, pl.smem) == cudaSuccess && n > 0)
             pl.per_sm = n;
         else
             cudaGetLastError();
         // the occupancy query reports one CTA per SM for the tensor-memory GQA
-        // kernels, which run two (128 registers x 256 threads, 2 x 92 KB: ncu's
-        // block limits, tools/plan_info.py); plan the splits for two
-        if (gqa && gqa_tmem())
-            pl.per_sm = std::max(pl.per_sm, std::min(PW == 1 && sets == 1 ? 4 : 2, static_cast<int>((227u * 1024u) / (pl.smem + 1024))));
+        // kernels (it does not see their real limits): plan with tensor memory,
+        // registers (128, or 192 with two head sets) and shared memory
+        if (gqa && (gqa_tmem() || wide)) {
+            const uint32_t wcols = (g4 || sets == 2 ? 64u : 32u) + 64u * static_cast<uint32_t>(sets);
+            const int tm = static_cast<int>(512u / gqa_tmem_cols(wcols, pl.NT / 32));
+            const int rg = 65536 / (pl.NT * (sets == 2 ? 192 : 128));
+            const int sm = static_cast<int>((227u * 1024u) / (pl.smem + 1024));
+            pl.per_sm = std::max(1, std::min(tm, std::min(rg, sm)));
+        }
     }
     // splits per sequence: fill every resident CTA slot, and prefer a split count
     // whose CTA total is close to a whole number of waves (within 4x the minimum)
@@ -1188,7 +1232,8 @@ cudaError_t launch_decode_mma(const rkv_layer_desc& d, const DecodePlan& plan, c
     if (plan.N == 256) {
         if (sp && plan.P > 2) return cudaErrorNotSupported;  // partials are instantiated for PW = 1, 2
         const int sets = gqa_sets(d, plan.P);
-        const void* kern = gqa_kernel(plan.P, sp, d.heads_per_group == 4, sets);
+        const bool wide = d.num_kv_heads * d.head_dim / 256 > 4;
+        const void* kern = gqa_kernel(plan.P, sp, d.heads_per_group == 4, sets, wide);
         cudaError_t e = ensure_smem(kern, plan.smem);
         if (e != cudaSuccess) return e;
         DecodeParams pp = p;

@@ -563,7 +563,7 @@ rkv_status rkv_prefill_attention(const rkv_layer_desc* desc, const uint16_t* q, 
     if (rkv::decode_kind(*desc) != rkv::kDecodeMma)
         return fail(RKV_ERR_INVALID_ARGUMENT,
                     "prefill: the tensor-core path covers Hq == Hkv with G = 1, 2, 4 and C a multiple of 512 "
-                    "up to 8192, and GQA (any Hq / Hkv >= 2) with G = 2 or 4 and Hkv <= 8");
+                    "up to 8192, and GQA (any Hq / Hkv >= 2) with G = 2 or 4 and Hkv <= 16");
     if (desc->max_sinks > rkv::kPrefillMaxSinks)
         return fail(RKV_ERR_INVALID_ARGUMENT, "prefill: at most 16 sink rows per sequence (max_sinks <= 16)");
     if (ws_bytes < rkv_prefill_workspace_bytes(desc, num_q, max_seq_len))

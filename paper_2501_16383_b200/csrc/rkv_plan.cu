@@ -76,7 +76,8 @@ bool build_decode_plan(const rkv_layer_desc& d, const int32_t* perm, std::vector
         return true;
     }
     const int GS = kind == kDecodeMma ? 32 : 16;  // lanes whose stores share a wavefront
-    const int G = W / GS;
+    const int G = (W + GS - 1) / GS;              // store groups; the last one may be partial (e.g. C = 1280)
+    auto gsize = [&](int k) { return std::min(GS, W - k * GS); };
     auto pos = [&](int c) { return kind == kDecodeMma ? mma_pos(N, c) : knat_pos(N, c) * 8; };
     std::vector<int> cls(static_cast<size_t>(C));
     for (int j = 0; j < C; ++j)
@@ -85,7 +86,8 @@ bool build_decode_plan(const rkv_layer_desc& d, const int32_t* perm, std::vector
     std::vector<int> omega(static_cast<size_t>(W));
     for (int w = 0; w < W; ++w) omega[static_cast<size_t>(w)] = w;
     std::vector<int> cost(static_cast<size_t>(G));
-    for (int k = 0; k < G; ++k) cost[static_cast<size_t>(k)] = group_cost(cls.data(), &omega[static_cast<size_t>(k) * GS], GS);
+    for (int k = 0; k < G; ++k)
+        cost[static_cast<size_t>(k)] = group_cost(cls.data(), &omega[static_cast<size_t>(k) * GS], gsize(k));
     if (G > 1) {
         SplitMix rng{0x5EEDULL ^ static_cast<uint64_t>(C) * 0x9E3779B97F4A7C15ULL};
         const long iters = 120000L * std::min(G, 8);
@@ -96,8 +98,8 @@ bool build_decode_plan(const rkv_layer_desc& d, const int32_t* perm, std::vector
             const int g1 = p1 / GS, g2 = p2 / GS;
             if (g1 == g2) continue;
             std::swap(omega[static_cast<size_t>(p1)], omega[static_cast<size_t>(p2)]);
-            const int c1 = group_cost(cls.data(), &omega[static_cast<size_t>(g1) * GS], GS);
-            const int c2 = group_cost(cls.data(), &omega[static_cast<size_t>(g2) * GS], GS);
+            const int c1 = group_cost(cls.data(), &omega[static_cast<size_t>(g1) * GS], gsize(g1));
+            const int c2 = group_cost(cls.data(), &omega[static_cast<size_t>(g2) * GS], gsize(g2));
             const int dl = c1 + c2 - cost[static_cast<size_t>(g1)] - cost[static_cast<size_t>(g2)];
             if (dl <= 0 || rng.uniform() < std::exp(-dl / T)) {
                 cost[static_cast<size_t>(g1)] = c1;

@@ -185,6 +185,9 @@ def oracle_decode(oracle, layer, got, b, T, q, w, perm, kraw, vraw):
     (16, 8, 2, 500000.0, 150), (24, 8, 2, 10000.0, 77), (40, 8, 2, 500000.0, 300), (56, 8, 2, 10000.0, 129),
     (48, 8, 2, 10000.0, 65), (80, 8, 2, 10000.0, 40), (8, 4, 4, 10000.0, 90), (24, 8, 4, 500000.0, 130),
     (20, 4, 4, 10000.0, 33),
+    # more than 8 KV heads (5 .. 8 groups per CTA): Phi-3-medium's 40 q / 10 KV, 16 KV heads at G = 2 and 4
+    (40, 10, 2, 10000.0, 150), (64, 16, 2, 500000.0, 200), (32, 16, 2, 10000.0, 77), (64, 16, 4, 10000.0, 129),
+    (128, 16, 2, 500000.0, 65), (24, 6, 2, 10000.0, 99),  # 6 KV heads: a partial plan store group
 ])
 def test_decode_vs_oracle(oracle, hq, hkv, g, base, T):
     w = small_workload(hq, hkv, g, base=base)
@@ -207,7 +210,7 @@ def test_decode_vs_oracle(oracle, hq, hkv, g, base, T):
 
 
 @pytest.mark.parametrize("hq,hkv,g,T", [
-    (80, 16, 2, 70),    # 5 q heads per KV head over 16 KV heads (past the tensor-core GQA width)
+    (96, 32, 2, 70),    # GQA over 32 KV heads (past the tensor-core GQA width)
     (40, 8, 8, 70),     # 5 q heads per KV head at G = 8
     (64, 64, 1, 90),    # G = 1 at C = 8192
     (16, 16, 8, 130),   # n = 1024

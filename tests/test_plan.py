@@ -35,7 +35,7 @@ def mma_pos(N, c):
 
 def cost_of(cls, omega, gs=16):
     tot = 0
-    for k in range(len(omega) // gs):
+    for k in range((len(omega) + gs - 1) // gs):  # the last store group may be partial
         words = omega[gs * k:gs * k + gs]
         for e in range(16):
             tot += np.bincount(cls[words, e], minlength=gs).max()
@@ -49,7 +49,11 @@ def test_mma_positions_are_a_bijection():
 
 
 @pytest.mark.parametrize("hq,hkv,g,seed", [(40, 40, 4, 0), (32, 32, 4, 1), (32, 8, 2, 2), (8, 8, 4, 3), (4, 4, 1, 4),
-                                           (8, 8, 1, 5), (8, 8, 2, 6), (40, 40, 1, 7)])
+                                           (8, 8, 1, 5), (8, 8, 2, 6), (40, 40, 1, 7),
+                                           # GQA at other ratios and widths; 80 and 48 words leave a
+                                           # partial store group
+                                           (40, 10, 2, 8), (24, 6, 2, 9), (64, 16, 4, 10), (16, 8, 2, 11),
+                                           (128, 16, 2, 12), (24, 8, 4, 13)])
 def test_plan_is_a_valid_scatter(hq, hkv, g, seed):
     cfg = P.LayerConfig(batch=1, num_q_heads=hq, num_kv_heads=hkv, heads_per_group=g)
     C = hkv * 128
@@ -58,9 +62,9 @@ def test_plan_is_a_valid_scatter(hq, hkv, g, seed):
     mma = int(words[7]) == 1  # PH_KIND: tensor-core decode layout
     # tensor-core layouts tile 512 channels (MHA, G = 4, 2 or 1 heads per rotation
     # group) or 256 (GQA, G = 2); the CUDA-core layout follows the rotation group
-    gqa = g == 2 and hq == 4 * hkv
+    gqa = g in (2, 4) and hq >= 2 * hkv and C % (128 * g) == 0 and C // 256 <= 8
     N = (256 if gqa else 512) if mma else 128 * g
-    assert mma == (gqa or C % 512 == 0)
+    assert mma == (gqa or (hq == hkv and C % 512 == 0))
     assert int(words[0]) == 0x504B5652 and int(words[2]) == N and int(words[4]) == C
     W = C // 16
     omega = words[HEADER:HEADER + W].astype(np.int64)
@@ -75,7 +79,8 @@ def test_plan_is_a_valid_scatter(hq, hkv, g, seed):
     cls = np.array([(pos(int(c)) >> 2) % 32 if mma else (pos(int(c)) >> 3) % 16 for c in perm]).reshape(W, 16)
     assert cost == cost_of(cls, omega, gs)
     if W >= 2 * gs:  # more than one store group: the assignment must beat the identity
-        assert cost < 0.85 * cost_of(cls, np.arange(W), gs)
+        ident = cost_of(cls, np.arange(W), gs)
+        assert cost < (0.85 if W >= 4 * gs else 0.95) * ident
 
 
 def test_plan_rejects_non_permutation():
