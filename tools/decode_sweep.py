@@ -25,8 +25,10 @@ def decode_bytes(w, B, T, nsinks):
     return B * ((T - nsinks) * 2 * (c // 4 + 4 * c // 128) + nsinks * 4 * c) + B * w.num_q_heads * 128 * 6
 
 
-def run(cfg_id, iters=20, g=None, warm=3, h=None, b=None, qh=None):
+def run(cfg_id, iters=20, g=None, warm=3, h=None, b=None, qh=None, kv=None):
     w = WL.CONFIGS[cfg_id]
+    if kv is not None:  # KV heads only (e.g. 16: GQA past 8 KV heads)
+        w = dataclasses.replace(w, num_kv_heads=kv, name=f"{w.name}-k{kv}")
     if qh is not None:  # q heads only (another GQA ratio, e.g. 64 over 8 KV heads)
         w = dataclasses.replace(w, num_q_heads=qh, name=f"{w.name}-q{qh}")
     if b is not None:  # a rank shard's batch (e.g. config 4 at 8 GPUs: b = 1)
@@ -76,15 +78,18 @@ if __name__ == "__main__":
         k_, v_ = kv.split("=")
         P.set_debug_option(k_, int(v_))
     # "2" = config 2; "2g1" = config 2's shape with G = 1; "2h64" = with 64 (q = KV) heads;
-    # "4b1" = config 4 with batch 1; "3q64" = config 3 with 64 q heads (GQA 8:1)
+    # "4b1" = config 4 with batch 1; "3q64" = config 3 with 64 q heads (GQA 8:1);
+    # "3k16q64" = config 3 with 16 KV and 64 q heads
     # --profile: one warm-up and one timed launch per config (for ncu captures)
     prof = "--profile" in sys.argv
     ids = [a for a in sys.argv[1:] if not a.startswith("--")] or ["2", "3", "4"]
     for a in ids:
         a, _, qs = a.partition("q")
+        a, _, ks = a.partition("k")
         a, _, bs = a.partition("b")
         a, _, h = a.partition("h")
         cfg, _, g = a.partition("g")
         print(json.dumps(run(int(cfg), g=int(g) if g else None, iters=1 if prof else 20, warm=1 if prof else 3,
-                             h=int(h) if h else None, b=int(bs) if bs else None, qh=int(qs) if qs else None)),
+                             h=int(h) if h else None, b=int(bs) if bs else None, qh=int(qs) if qs else None,
+                             kv=int(ks) if ks else None)),
               flush=True)
