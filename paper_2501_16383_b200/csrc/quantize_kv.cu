@@ -533,7 +533,7 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
-// one lane's 32-slot run of both tokens (padded runs in shared memory) -> float2 per slot
+// one lane's 32-slot run of both tokens (fp32 rows; padded runs in shared memory) -> float2 per slot
 __device__ __forceinline__ void read_run(const float* r0, const float* r1, float2 (&x)[32]) {
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -542,16 +542,6 @@ __device__ __forceinline__ void read_run(const float* r0, const float* r1, float
         x[4 * q + 1] = make_float2(__uint_as_float(a.y), __uint_as_float(b.y));
         x[4 * q + 2] = make_float2(__uint_as_float(a.z), __uint_as_float(b.z));
         x[4 * q + 3] = make_float2(__uint_as_float(a.w), __uint_as_float(b.w));
-    }
-}
-__device__ __forceinline__ void read_run(const uint16_t* r0, const uint16_t* r1, float2 (&x)[32]) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const uint4 a = lds128(r0 + 8 * q), b = lds128(r1 + 8 * q);
-        const uint16_t* ha = reinterpret_cast<const uint16_t*>(&a);
-        const uint16_t* hb = reinterpret_cast<const uint16_t*>(&b);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) x[8 * q + e] = make_float2(h2f(ha[e]), h2f(hb[e]));
     }
 }
 
