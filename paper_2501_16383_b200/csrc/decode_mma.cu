@@ -725,6 +725,11 @@ __global__ void __launch_bounds__(gqa_max_threads<PW, TM, NS, WIDE>(), gqa_min_b
     const int bit0 = lane & 1, bit1 = (lane >> 1) & 1;
     uint32_t AH[4];
     hadamard16_frag(AH, lane, static_cast<uint32_t>(p.max_tokens >> 40));  // max_tokens <= 2^30
+    // second FWHT factor: H_16 (G = 2) or H_8 x I_2 over the head bit (G = 1);
+    // the G = 4 half-group pairs use H_16
+    uint32_t AF2buf[4];
+    if constexpr (!X) hadamard_mask_frag(AF2buf, lane, p.f2_mask, static_cast<uint32_t>(p.max_tokens >> 40));
+    uint32_t(&AF2)[4] = *(X ? &AH : &AF2buf);
     // RoPE(T-1) q of the frequency pairs (f, f+1), (f+64, f+65).  Slot sl holds
     // head r = sl ^ (g & 3): the first two reduce-scatter steps then keep / send
     // fixed slots on every lane (no selects) and leave head g & 3 in slot 0.
@@ -896,8 +901,8 @@ __global__ void __launch_bounds__(gqa_max_threads<PW, TM, NS, WIDE>(), gqa_min_b
                     const uint32_t l0 = pack_h2(sub_lo(yf[0][2 * f1], h0), sub_hi(yf[0][2 * f1 + 1], h0));
                     const uint32_t l1 = pack_h2(sub_lo(yf[1][2 * f1], h1), sub_hi(yf[1][2 * f1 + 1], h1));
                     float t4[4], z[4];
-                    mma16816(t4, AH, h0, h1, zero);
-                    mma16816(z, AH, l0, l1, t4);
+                    mma16816(t4, AF2, h0, h1, zero);
+                    mma16816(z, AF2, l0, l1, t4);
                     // z: (c0, c1) channels f, f+1 (bit 6 = 0), (c2, c3) channels f+64, f+65
                     const float4 r4 = rope4[(2 * tp + tk) * 32 + fpi + 16 * f1];  // (cos f, cos f+1, sin f, sin f+1)
                     const float2 cs2 = make_float2(r4.x, r4.y), sn2 = make_float2(r4.z, r4.w);
@@ -1090,13 +1095,13 @@ __global__ void __launch_bounds__(gqa_max_threads<PW, TM, NS, WIDE>(), gqa_min_b
 // per CTA).
 bool decode_mma_supported(int G, int REP, int C) {
     if (REP == 1 && (G == 4 || G == 2 || G == 1)) return C % 512 == 0 && C / 512 * 32 <= kMmaMaxThreads;
-    if (REP >= 2 && REP <= 64 && (G == 2 || G == 4)) return C % (128 * G) == 0 && C / 256 <= 8;
+    if (REP >= 2 && REP <= 64 && (G == 1 || G == 2 || G == 4)) return C % (128 * std::max(G, 2)) == 0 && C / 256 <= 8;
     return false;
 }
 
 int mma_layout_n(const rkv_layer_desc& d) {
     const int rep = d.num_q_heads / d.num_kv_heads;
-    return (d.heads_per_group == 2 || d.heads_per_group == 4) && rep > 1 ? 256 : 512;
+    return (d.heads_per_group == 1 || d.heads_per_group == 2 || d.heads_per_group == 4) && rep > 1 ? 256 : 512;
 }
 
 namespace {
@@ -1122,7 +1127,7 @@ void* gqa_kernel_ptr() {
 // exceeds 4 at G = 2 and PW = 1 with tensor-memory parking
 int gqa_sets(const rkv_layer_desc& d, int pw) {
     const int rep = d.num_q_heads / d.num_kv_heads;
-    return d.heads_per_group == 2 && rep > 4 && pw == 1 && gqa_tmem() && options().gqa_sets.load() != 1 ? 2 : 1;
+    return d.heads_per_group <= 2 && rep > 4 && pw == 1 && gqa_tmem() && options().gqa_sets.load() != 1 ? 2 : 1;
 }
 void* gqa_kernel(int pw, bool sp = false, bool g4 = false, int sets = 1, bool wide = false) {
     if (wide) {  // 5 .. 8 (half-)groups: PW = 1 with tensor-memory parking
@@ -1248,6 +1253,7 @@ cudaError_t launch_decode_mma(const rkv_layer_desc& d, const DecodePlan& plan, c
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
+        pp.f2_mask = d.heads_per_group == 1 ? 11 : 15;
         // 4 (sets = 2: 8) q heads per KV head per launch: larger ratios run as
         // passes over disjoint head sets (each pass re-reads the cache), one combine
         const int rep = d.num_q_heads / d.num_kv_heads;

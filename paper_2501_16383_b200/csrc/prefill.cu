@@ -62,7 +62,8 @@ __device__ __forceinline__ void store_key_pair(const PrefillParams& p, int b, in
 // ------------------------------------------------------------------ 1. keys
 // CTA = (4-token tile, sequence), one warp per FWHT group.
 // G = 4: 512-channel tiles (the MHA decode layout; AG = heads per rotation
-// group, 4, 2 or 1, picks the second FWHT factor); G = 2: GQA 256-channel groups.
+// group, 4, 2 or 1, picks the second FWHT factor); G = 2: GQA 256-channel groups
+// (AG = 1: per-head rotation, H_8 x I_2 over the head bit in the second factor).
 // PAIR (GQA at G = 4 on the 256-channel plan, G = 2 here): the group's two
 // half-group warps hold u, v = H_256 of their halves (RoPE'd); the keys are
 // u + v (KV heads 0, 1) and u - v (heads 2, 3) -- swapped through shared
@@ -122,8 +123,13 @@ __global__ void __launch_bounds__(512) reconstruct_keys_kernel(PrefillParams p) 
     const int gam = warp, g = lane >> 2, tl = lane & 3;
     uint32_t AH[4], AF2buf[4];
     hadamard16_frag(AH, lane, static_cast<uint32_t>(p.max_tokens >> 40));
-    if constexpr (AG != G) hadamard_f2_frag<AG>(AF2buf, lane, static_cast<uint32_t>(p.max_tokens >> 40));
-    uint32_t(&AF2)[4] = *(AG == G ? &AH : &AF2buf);  // second FWHT factor of the 512-channel tile
+    if constexpr (AG != G) {
+        if constexpr (G == 2)  // 256-channel GQA tile at G = 1: H_8 x I_2 over the head bit
+            hadamard_mask_frag(AF2buf, lane, 11, static_cast<uint32_t>(p.max_tokens >> 40));
+        else
+            hadamard_f2_frag<AG>(AF2buf, lane, static_cast<uint32_t>(p.max_tokens >> 40));
+    }
+    uint32_t(&AF2)[4] = *(AG == G ? &AH : &AF2buf);  // second FWHT factor of the tile
     const float kn = p.k_norm;
     const int swz = mma_swz(N, lane);
     const unsigned char* lbase = knat + gam * N * 4 + lane * NJ * 16;
@@ -186,8 +192,8 @@ __global__ void __launch_bounds__(512) reconstruct_keys_kernel(PrefillParams p) 
                     const uint32_t l0 = pack_h2(sub_lo(yf[0][2 * f1], h0), sub_hi(yf[0][2 * f1 + 1], h0));
                     const uint32_t l1 = pack_h2(sub_lo(yf[1][2 * f1], h1), sub_hi(yf[1][2 * f1 + 1], h1));
                     float t4[4], z[4];
-                    mma16816(t4, AH, h0, h1, zero);
-                    mma16816(z, AH, l0, l1, t4);
+                    mma16816(t4, AF2, h0, h1, zero);
+                    mma16816(z, AF2, l0, l1, t4);
                     const int kvh = gam * G + (g >> 2);
                     float ka[2], kb[2];
 #pragma unroll
@@ -867,9 +873,10 @@ cudaError_t launch_prefill(const rkv_layer_desc& d, const PrefillParams& p, int6
     } else if (N == 256 && pair) {  // GQA at G = 4: half-group pairs
         if ((e = ensure_smem_k(reconstruct_keys_kernel<2, 2, true>, ksmem)) != cudaSuccess) return e;
         reconstruct_keys_kernel<2, 2, true><<<kgrid, nthreads, ksmem, s>>>(p);
-    } else if (N == 256) {
-        if ((e = ensure_smem_k(reconstruct_keys_kernel<2>, ksmem)) != cudaSuccess) return e;
-        reconstruct_keys_kernel<2><<<kgrid, nthreads, ksmem, s>>>(p);
+    } else if (N == 256) {  // GQA at G = 2, or G = 1 (per-head rotation, AG = 1)
+        auto kern = d.heads_per_group == 1 ? reconstruct_keys_kernel<2, 1> : reconstruct_keys_kernel<2>;
+        if ((e = ensure_smem_k(kern, ksmem)) != cudaSuccess) return e;
+        kern<<<kgrid, nthreads, ksmem, s>>>(p);
     } else {
         return cudaErrorInvalidValue;
     }

@@ -107,6 +107,7 @@ struct DecodeParams {
     // GQA kernel passes (q heads per KV head a multiple of 4): this launch
     // covers q heads kv * q_rep + q_rep_off + 0..3 of every KV head kv
     int q_rep, q_rep_off;
+    int f2_mask;   // GQA kernel: second FWHT factor's H mask (15: G = 2, 11: G = 1), hadamard_mask_frag
     float k_norm;  // 1/sqrt(G*d), folded into q
     float qscale;  // log2(e) / sqrt(d)
 };

@@ -123,6 +123,24 @@ __device__ __forceinline__ void hadamard16_frag(uint32_t (&a)[4], int lane, uint
     a[3] ^= opaque_zero;
 }
 
+// A fragment of a masked H_16: (-1)^popcount(m & k & mask) where m and k agree
+// outside `mask`, 0 elsewhere -- H over the mask bits, the identity over the
+// others.  The GQA tiles' second factor contracts over channel bits (4, 5, 7,
+// 6) = k bits (0, 1, 2, 3): mask 15 for G = 2 (H_256), 11 for G = 1 (H_128 per
+// head, the identity over the head bit 7).
+__device__ __forceinline__ void hadamard_mask_frag(uint32_t (&a)[4], int lane, int mask, uint32_t opaque_zero) {
+    const int g = lane >> 2, t = lane & 3;
+    auto h = [mask](int m, int k) -> uint32_t {
+        if ((m ^ k) & ~mask & 15) return 0u;
+        return (__popc(m & k & mask) & 1) ? 0xBC00u : 0x3C00u;
+    };
+    const int rows[4] = {g, g + 8, g, g + 8}, cols[4] = {2 * t, 2 * t, 2 * t + 8, 2 * t + 8};
+#pragma unroll
+    for (int r = 0; r < 4; ++r) a[r] = h(rows[r], cols[r]) | (h(rows[r], cols[r] + 1) << 16);
+    a[2] ^= opaque_zero;
+    a[3] ^= opaque_zero;
+}
+
 // A fragment of the second FWHT factor of a 512-channel (pseudo-)group, over
 // channel bits (4, 5, 7, 8) = k bits (0, 1, 2, 3):  AG = 4 (G = 4 heads per
 // rotation group): H_16;  AG = 2: H_8 on bits 4, 5, 7 and the identity on

@@ -188,6 +188,9 @@ def oracle_decode(oracle, layer, got, b, T, q, w, perm, kraw, vraw):
     # more than 8 KV heads (5 .. 8 groups per CTA): Phi-3-medium's 40 q / 10 KV, 16 KV heads at G = 2 and 4
     (40, 10, 2, 10000.0, 150), (64, 16, 2, 500000.0, 200), (32, 16, 2, 10000.0, 77), (64, 16, 4, 10000.0, 129),
     (128, 16, 2, 500000.0, 65), (24, 6, 2, 10000.0, 99),  # 6 KV heads: a partial plan store group
+    # GQA at the reference's default per-head rotation (G = 1): H_8 x I_2 second factor
+    (32, 8, 1, 500000.0, 300), (16, 4, 1, 10000.0, 77), (64, 8, 1, 10000.0, 129), (40, 8, 1, 500000.0, 65),
+    (64, 16, 1, 10000.0, 90),
 ])
 def test_decode_vs_oracle(oracle, hq, hkv, g, base, T):
     w = small_workload(hq, hkv, g, base=base)
@@ -418,8 +421,8 @@ def test_decode_matches_reference_decode_step(ref):
     assert cosine(out, want) > COS_TOL
 
 
-@pytest.mark.parametrize("hq,hkv,g", [(40, 40, 4), (32, 8, 2), (32, 8, 4), (16, 16, 8), (16, 4, 1), (64, 8, 2),
-                                      (40, 8, 2)])
+@pytest.mark.parametrize("hq,hkv,g", [(40, 40, 4), (32, 8, 2), (32, 8, 4), (16, 16, 8), (64, 32, 1), (64, 8, 2),
+                                      (40, 8, 2), (32, 8, 1)])
 def test_decode_deterministic(hq, hkv, g):
     """Bit-identical outputs run to run on every decode kernel family (fixed
     split partition, fixed merge order)."""

@@ -72,6 +72,8 @@ def check(got, want):
     (16, 8, 2, 50, (0,), 13), (40, 8, 2, 45, (0, 7), 14), (24, 8, 4, 30, (0,), 15),
     # more than 8 KV heads
     (40, 10, 2, 40, (0,), 16), (64, 16, 4, 33, (0, 5), 17),
+    # GQA at G = 1
+    (32, 8, 1, 60, (0, 3), 18), (40, 8, 1, 30, (0,), 19),
     (8, 8, 1, 70, (0, 9), 6),
     (8, 8, 2, 45, (0,), 7),
     # the widest tensor-core layer: 12 FWHT groups (C = 6144)
@@ -109,9 +111,9 @@ def test_prefill_rejects_bad_arguments():
         layer.prefill_attention(q.float())
 
 
-@pytest.mark.parametrize("hq,hkv,g", [(96, 24, 2), (16, 4, 1), (64, 64, 8), (24, 8, 8)])
+@pytest.mark.parametrize("hq,hkv,g", [(96, 24, 2), (12, 3, 1), (64, 64, 8), (24, 8, 8)])
 def test_prefill_refuses_shapes_outside_the_tensor_core_path(hq, hkv, g):
-    """GQA beyond 16 KV heads, GQA at G = 1, and G = 8: ValueError, nothing launched."""
+    """GQA beyond 16 KV heads, an odd KV-head count at G = 1, and G = 8: ValueError, nothing launched."""
     layer, k, v, flags, q, perm = build(hq, hkv, g, 20, (0,), 1)
     with pytest.raises(ValueError, match="tensor-core path"):
         layer.prefill_attention(q, q_start=np.zeros(2, np.int64))

@@ -31,7 +31,7 @@ def rel(a, b):
                                               # GQA 8:1: head passes of the 4-head kernel
                                               (64, 8, 2, 3), (64, 8, 4, 2),
                                               # more than 8 KV heads; a partial head set
-                                              (64, 16, 2, 2), (40, 8, 2, 3)])
+                                              (64, 16, 2, 2), (40, 8, 2, 3), (32, 8, 1, 2)])
 def test_partials_merge_to_the_full_decode(oracle, hq, hkv, g, world):
     lens = [700, 129, 64, 1]
     B, T = len(lens), max(lens)

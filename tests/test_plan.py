@@ -62,7 +62,7 @@ def test_plan_is_a_valid_scatter(hq, hkv, g, seed):
     mma = int(words[7]) == 1  # PH_KIND: tensor-core decode layout
     # tensor-core layouts tile 512 channels (MHA, G = 4, 2 or 1 heads per rotation
     # group) or 256 (GQA, G = 2); the CUDA-core layout follows the rotation group
-    gqa = g in (2, 4) and hq >= 2 * hkv and C % (128 * g) == 0 and C // 256 <= 8
+    gqa = g in (1, 2, 4) and hq >= 2 * hkv and C % (128 * max(g, 2)) == 0 and C // 256 <= 8
     N = (256 if gqa else 512) if mma else 128 * g
     assert mma == (gqa or (hq == hkv and C % 512 == 0))
     assert int(words[0]) == 0x504B5652 and int(words[2]) == N and int(words[4]) == C
