@@ -1,0 +1,134 @@
+"""Out-of-bounds reads of the cache fault instead of passing silently.
+
+The carved cache is placed flush against an unmapped hole in the virtual
+address space (driver VMM: cuMemAddressReserve / cuMemCreate / cuMemMap), once
+with its last byte on the last mapped byte and once with its first byte on the
+first mapped byte.  Batch and max_tokens are chosen so the last sequence's
+sink-mask row (the last carved array) ends exactly at the cache's end, with no
+256-byte padding behind it.  Every kernel family then runs over a full cache:
+a read one word past the last sequence's rows or before the first array is an
+illegal-address fault.  Each placement runs in a child process so a fault
+cannot poison the other GPU tests; results must also equal the same calls on
+an ordinary allocation.  A positive control checks that the neighbouring
+bytes of such a mapping really are unreadable.
+"""
+import os
+import subprocess
+import sys
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+# (hq, hkv, G, batch, max_tokens): B * ceil(T / 32) is a multiple of 64
+CASES = [
+    (8, 8, 4, 4, 500),     # MHA tensor-core kernel
+    (8, 8, 1, 2, 1000),    # MHA at G = 1
+    (16, 4, 2, 4, 500),    # GQA 4:1, G = 2
+    (16, 4, 4, 2, 1000),   # GQA 4:1, G = 4 (half-group pairs)
+    (16, 16, 8, 8, 250),   # tiled generic kernels
+    (40, 40, 4, 4, 500),   # C = 5120, warp-independent V quantize
+]
+
+
+def _child(at):
+    import ctypes as C
+
+    import numpy as np
+    from cuda.bindings import driver as cu
+
+    sys.path.insert(0, ROOT)
+    import paper_2501_16383_b200 as P  # noqa: F401
+    from paper_2501_16383_b200 import rotatekv as RK
+    from paper_2501_16383_b200 import workload as WL
+    from tests.test_gpu_parity import build_layer, small_workload
+
+    def ok(r):
+        assert r[0] == cu.CUresult.CUDA_SUCCESS, r[0]
+        return r[1] if len(r) == 2 else r[1:]
+
+    torch.cuda.init()
+    torch.empty(1, device="cuda")
+    ok((cu.cuInit(0)[0], None))
+    dev = torch.cuda.current_device()
+    prop = cu.CUmemAllocationProp()
+    prop.type = cu.CUmemAllocationType.CU_MEM_ALLOCATION_TYPE_PINNED
+    prop.location.type = cu.CUmemLocationType.CU_MEM_LOCATION_TYPE_DEVICE
+    prop.location.id = dev
+    gran = ok(cu.cuMemGetAllocationGranularity(
+        prop, cu.CUmemAllocationGranularity_flags.CU_MEM_ALLOC_GRANULARITY_MINIMUM))
+
+    for hq, hkv, g, B, T in CASES:
+        w = small_workload(hq, hkv, g)
+        plain, perm = build_layer(w, B, T, seed=71, max_sinks=2)
+        edge, _ = build_layer(w, B, T, seed=71, max_sinks=2, perm=perm)
+        nbytes = RK.lib().rkv_cache_bytes(C.byref(edge._desc))
+        assert nbytes % 256 == 0
+        size = (nbytes + gran - 1) // gran * gran
+        va = int(ok(cu.cuMemAddressReserve(size + 2 * gran, 0, 0, 0)))
+        h = ok(cu.cuMemCreate(size, prop, 0))
+        mapped = va + gran
+        ok((cu.cuMemMap(mapped, size, 0, h, 0)[0], None))
+        acc = cu.CUmemAccessDesc()
+        acc.location.type = cu.CUmemLocationType.CU_MEM_LOCATION_TYPE_DEVICE
+        acc.location.id = dev
+        acc.flags = cu.CUmemAccess_flags.CU_MEM_ACCESS_FLAGS_PROT_READWRITE
+        ok((cu.cuMemSetAccess(mapped, size, [acc], 1)[0], None))
+        base = mapped + size - nbytes if at == "end" else mapped
+        RK._check(RK.lib().rkv_cache_carve(C.byref(edge._desc), base, nbytes, C.byref(edge._view)))
+        edge._buf, edge._base = None, base
+        edge.reset()
+
+        k, v = WL.make_kv(w, 71, B, T)
+        flags = torch.zeros(B, T, dtype=torch.uint8)
+        flags[:, 0] = 1
+        flags[B - 1, T - 1] = 1
+        for lay in (plain, edge):
+            lay.append(k, v, flags)
+        q = WL.make_q(w, 71, B)
+        ragged = np.maximum(1, T - 45 * np.arange(B, dtype=np.int64))
+        for lens in (None, ragged):
+            a, b = plain.decode(q, seq_len=lens), edge.decode(q, seq_len=lens)
+            torch.cuda.synchronize()
+            assert torch.equal(a, b), (hq, hkv, g, "decode")
+        if g != 8:
+            qp = torch.randn(B, 64, hq, 128, generator=torch.Generator().manual_seed(9)).half().cuda()
+            a, b = plain.prefill_attention(qp), edge.prefill_attention(qp)
+            torch.cuda.synchronize()
+            assert torch.equal(a, b), (hq, hkv, g, "prefill")
+        data = edge.serialize(B - 1)
+        assert data == plain.serialize(B - 1), (hq, hkv, g, "export")
+        torch.cuda.synchronize()
+        ok((cu.cuMemUnmap(mapped, size)[0], None))
+        ok((cu.cuMemRelease(h)[0], None))
+        ok((cu.cuMemAddressFree(va, size + 2 * gran)[0], None))
+        print(f"ok {at} {hq}/{hkv} G={g} B={B} T={T}", flush=True)
+
+    # positive control: the byte just outside a mapped region is not readable
+    va = int(ok(cu.cuMemAddressReserve(3 * gran, 0, 0, 0)))
+    h = ok(cu.cuMemCreate(gran, prop, 0))
+    ok((cu.cuMemMap(va + gran, gran, 0, h, 0)[0], None))
+    ok((cu.cuMemSetAccess(va + gran, gran, [acc], 1)[0], None))
+    host = np.zeros(4, np.uint8)
+    assert cu.cuMemcpyDtoH(host, va + gran + gran - 4, 4)[0] == cu.CUresult.CUDA_SUCCESS
+    probe = va + gran + gran if at == "end" else va + gran - 4
+    r = cu.cuMemcpyDtoH(host, probe, 4)[0]
+    assert r != cu.CUresult.CUDA_SUCCESS, "unmapped neighbour was readable"
+    print(f"control {at}: {r}", flush=True)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("at", ["end", "start"])
+def test_cache_reads_stay_inside(at):
+    if not torch.cuda.is_available():  # pragma: no cover
+        pytest.skip("needs a CUDA device")
+    r = subprocess.run([sys.executable, os.path.abspath(__file__), at], capture_output=True, text=True, timeout=600,
+                       cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert r.stdout.count("ok ") == len(CASES) and "control" in r.stdout, r.stdout
+
+
+if __name__ == "__main__":
+    _child(sys.argv[1])
