@@ -7,7 +7,8 @@ first mapped byte.  Batch and max_tokens are chosen so the last sequence's
 sink-mask row (the last carved array) ends exactly at the cache's end, with no
 256-byte padding behind it.  Every kernel family then runs over a full cache:
 a read one word past the last sequence's rows or before the first array is an
-illegal-address fault.  Each placement runs in a child process so a fault
+illegal-address fault.  The appended K/V rows (an odd token count) and the
+queries are placed the same way.  Each placement runs in a child process so a fault
 cannot poison the other GPU tests; results must also equal the same calls on
 an ordinary allocation.  A positive control checks that the neighbouring
 bytes of such a mapping really are unreadable.
@@ -60,50 +61,75 @@ def _child(at):
     gran = ok(cu.cuMemGetAllocationGranularity(
         prop, cu.CUmemAllocationGranularity_flags.CU_MEM_ALLOC_GRANULARITY_MINIMUM))
 
+    acc = cu.CUmemAccessDesc()
+    acc.location.type = cu.CUmemLocationType.CU_MEM_LOCATION_TYPE_DEVICE
+    acc.location.id = dev
+    acc.flags = cu.CUmemAccess_flags.CU_MEM_ACCESS_FLAGS_PROT_READWRITE
+    maps = []
+
+    def edge_alloc(nbytes):
+        """nbytes flush against an unmapped hole at the `at` end"""
+        size = (nbytes + gran - 1) // gran * gran
+        va = int(ok(cu.cuMemAddressReserve(size + 2 * gran, 0, 0, 0)))
+        h = ok(cu.cuMemCreate(size, prop, 0))
+        mapped = va + gran
+        ok((cu.cuMemMap(mapped, size, 0, h, 0)[0], None))
+        ok((cu.cuMemSetAccess(mapped, size, [acc], 1)[0], None))
+        maps.append((va, h, mapped, size))
+        return mapped + size - nbytes if at == "end" else mapped
+
+    class Raw:  # a torch view of raw device memory (no copy)
+        def __init__(self, ptr, shape, typestr):
+            self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (ptr, False),
+                                             "version": 3, "strides": None}
+
+    def edge_like(t):
+        e = torch.as_tensor(Raw(edge_alloc(t.numel() * t.element_size()), t.shape, "<f2"), device="cuda")
+        e.copy_(t)
+        return e
+
+    def release():
+        torch.cuda.synchronize()
+        for va, h, mapped, size in maps:
+            ok((cu.cuMemUnmap(mapped, size)[0], None))
+            ok((cu.cuMemRelease(h)[0], None))
+            ok((cu.cuMemAddressFree(va, size + 2 * gran)[0], None))
+        maps.clear()
+
     for hq, hkv, g, B, T in CASES:
         w = small_workload(hq, hkv, g)
         plain, perm = build_layer(w, B, T, seed=71, max_sinks=2)
         edge, _ = build_layer(w, B, T, seed=71, max_sinks=2, perm=perm)
         nbytes = RK.lib().rkv_cache_bytes(C.byref(edge._desc))
         assert nbytes % 256 == 0
-        size = (nbytes + gran - 1) // gran * gran
-        va = int(ok(cu.cuMemAddressReserve(size + 2 * gran, 0, 0, 0)))
-        h = ok(cu.cuMemCreate(size, prop, 0))
-        mapped = va + gran
-        ok((cu.cuMemMap(mapped, size, 0, h, 0)[0], None))
-        acc = cu.CUmemAccessDesc()
-        acc.location.type = cu.CUmemLocationType.CU_MEM_LOCATION_TYPE_DEVICE
-        acc.location.id = dev
-        acc.flags = cu.CUmemAccess_flags.CU_MEM_ACCESS_FLAGS_PROT_READWRITE
-        ok((cu.cuMemSetAccess(mapped, size, [acc], 1)[0], None))
-        base = mapped + size - nbytes if at == "end" else mapped
+        base = edge_alloc(nbytes)
         RK._check(RK.lib().rkv_cache_carve(C.byref(edge._desc), base, nbytes, C.byref(edge._view)))
         edge._buf, edge._base = None, base
         edge.reset()
 
-        k, v = WL.make_kv(w, 71, B, T)
-        flags = torch.zeros(B, T, dtype=torch.uint8)
+        n = T - 1  # an odd append: the last token pair has one row
+        k, v = WL.make_kv(w, 71, B, n)
+        flags = torch.zeros(B, n, dtype=torch.uint8)
         flags[:, 0] = 1
-        flags[B - 1, T - 1] = 1
-        for lay in (plain, edge):
-            lay.append(k, v, flags)
+        flags[B - 1, n - 1] = 1
+        plain.append(k, v, flags)
+        edge.append(edge_like(k), edge_like(v), flags)  # the new rows flush against a hole too
         q = WL.make_q(w, 71, B)
-        ragged = np.maximum(1, T - 45 * np.arange(B, dtype=np.int64))
+        qe = edge_like(q)
+        ragged = np.maximum(1, n - 45 * np.arange(B, dtype=np.int64))
         for lens in (None, ragged):
-            a, b = plain.decode(q, seq_len=lens), edge.decode(q, seq_len=lens)
+            a, b = plain.decode(q, seq_len=lens), edge.decode(qe, seq_len=lens)
             torch.cuda.synchronize()
             assert torch.equal(a, b), (hq, hkv, g, "decode")
         if g != 8:
             qp = torch.randn(B, 64, hq, 128, generator=torch.Generator().manual_seed(9)).half().cuda()
-            a, b = plain.prefill_attention(qp), edge.prefill_attention(qp)
+            a, b = plain.prefill_attention(qp), edge.prefill_attention(edge_like(qp))
             torch.cuda.synchronize()
             assert torch.equal(a, b), (hq, hkv, g, "prefill")
         data = edge.serialize(B - 1)
         assert data == plain.serialize(B - 1), (hq, hkv, g, "export")
-        torch.cuda.synchronize()
-        ok((cu.cuMemUnmap(mapped, size)[0], None))
-        ok((cu.cuMemRelease(h)[0], None))
-        ok((cu.cuMemAddressFree(va, size + 2 * gran)[0], None))
+        del edge, qe
+        release()
         print(f"ok {at} {hq}/{hkv} G={g} B={B} T={T}", flush=True)
 
     # positive control: the byte just outside a mapped region is not readable
