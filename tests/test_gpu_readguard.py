@@ -7,8 +7,9 @@ first mapped byte.  Batch and max_tokens are chosen so the last sequence's
 sink-mask row (the last carved array) ends exactly at the cache's end, with no
 256-byte padding behind it.  Every kernel family then runs over a full cache:
 a read one word past the last sequence's rows or before the first array is an
-illegal-address fault.  The appended K/V rows (an odd token count) and the
-queries are placed the same way.  Each placement runs in a child process so a fault
+illegal-address fault.  The appended K/V rows (an odd token count), the
+queries, the fused-frame rows, the calibration keys and the sink-detection
+hidden states are placed the same way.  Each placement runs in a child process so a fault
 cannot poison the other GPU tests; results must also equal the same calls on
 an ordinary allocation.  A positive control checks that the neighbouring
 bytes of such a mapping really are unreadable.
@@ -84,9 +85,20 @@ def _child(at):
                                              "version": 3, "strides": None}
 
     def edge_like(t):
-        e = torch.as_tensor(Raw(edge_alloc(t.numel() * t.element_size()), t.shape, "<f2"), device="cuda")
+        ts = {torch.float16: "<f2", torch.float32: "<f4"}[t.dtype]
+        e = torch.as_tensor(Raw(edge_alloc(t.numel() * t.element_size()), t.shape, ts), device="cuda")
         e.copy_(t)
         return e
+
+    def carve_edge(layer):
+        """re-carve the layer's cache at the hole (its arrays() views included)"""
+        nbytes = RK.lib().rkv_cache_bytes(C.byref(layer._desc))
+        assert nbytes % 256 == 0
+        base = edge_alloc(nbytes)
+        RK._check(RK.lib().rkv_cache_carve(C.byref(layer._desc), base, nbytes, C.byref(layer._view)))
+        layer._buf = torch.as_tensor(Raw(base, (nbytes,), "|u1"), device="cuda")
+        layer._base = base
+        layer.reset()
 
     def release():
         torch.cuda.synchronize()
@@ -100,12 +112,7 @@ def _child(at):
         w = small_workload(hq, hkv, g)
         plain, perm = build_layer(w, B, T, seed=71, max_sinks=2)
         edge, _ = build_layer(w, B, T, seed=71, max_sinks=2, perm=perm)
-        nbytes = RK.lib().rkv_cache_bytes(C.byref(edge._desc))
-        assert nbytes % 256 == 0
-        base = edge_alloc(nbytes)
-        RK._check(RK.lib().rkv_cache_carve(C.byref(edge._desc), base, nbytes, C.byref(edge._view)))
-        edge._buf, edge._base = None, base
-        edge.reset()
+        carve_edge(edge)
 
         n = T - 1  # an odd append: the last token pair has one row
         k, v = WL.make_kv(w, 71, B, n)
@@ -132,6 +139,36 @@ def _child(at):
         release()
         print(f"ok {at} {hq}/{hkv} G={g} B={B} T={T}", flush=True)
 
+    # the other readers of caller buffers: the fused-frame append (fp32 and
+    # fp16 rows, odd count), device calibration and device sink detection
+    w = small_workload(40, 40, 4)
+    B, T, n = 4, 500, 499
+    plain, perm = build_layer(w, B, T, seed=72, max_sinks=2)
+    edge, _ = build_layer(w, B, T, seed=72, max_sinks=2, perm=perm)
+    carve_edge(edge)
+    gen = torch.Generator().manual_seed(4)
+    rows = torch.randn(B, n, 5120, generator=gen).cuda()
+    flags = torch.zeros(B, n, dtype=torch.uint8)
+    flags[:, 0] = 1
+    for lo, hi, dt in ((0, 250, torch.float32), (250, n, torch.float16)):
+        kr, vr = rows[:, lo:hi].to(dt).contiguous(), (rows[:, lo:hi] * 0.5).to(dt).contiguous()
+        plain.append_fused(kr, vr, flags[:, lo:hi])
+        edge.append_fused(edge_like(kr), edge_like(vr), flags[:, lo:hi])
+    torch.cuda.synchronize()
+    ta, tb = plain.arrays(), edge.arrays()
+    for name in ("k_codes", "v_codes", "k_meta", "v_meta"):
+        assert torch.equal(ta[name][:, :n], tb[name][:, :n]), ("fused append", name)
+    kcal = torch.randn(1001, 5120, generator=gen).half().cuda()
+    assert np.array_equal(P.calibrate_reorder_device(plain.cfg, kcal)[0],
+                          P.calibrate_reorder_device(plain.cfg, edge_like(kcal))[0]), "calibration"
+    hidden = torch.randn(2, 333, 512, generator=gen).cuda()
+    hidden[:, 7, 3] = 400.0
+    fa, fb = P.detect_massive_activations_device(hidden), P.detect_massive_activations_device(edge_like(hidden))
+    assert torch.equal(fa, fb) and int(fa[7]) == 1, "sink detection"
+    del edge
+    release()
+    print(f"ok {at} fused append / calibration / sink detection", flush=True)
+
     # positive control: the byte just outside a mapped region is not readable
     va = int(ok(cu.cuMemAddressReserve(3 * gran, 0, 0, 0)))
     h = ok(cu.cuMemCreate(gran, prop, 0))
@@ -153,7 +190,7 @@ def test_cache_reads_stay_inside(at):
     r = subprocess.run([sys.executable, os.path.abspath(__file__), at], capture_output=True, text=True, timeout=600,
                        cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
-    assert r.stdout.count("ok ") == len(CASES) and "control" in r.stdout, r.stdout
+    assert r.stdout.count("ok ") == len(CASES) + 1 and "control" in r.stdout, r.stdout
 
 
 if __name__ == "__main__":
